@@ -1,0 +1,804 @@
+/* oracle.c -- UniAP CPU ORACLE: plain, slow, obviously correct.
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Every function cites the passage
+ * of /root/reference/PAPER.md it follows; readings of silent or ambiguous
+ * passages are the A-n items of DESIGN.md Sec. 2.
+ *
+ * Pins (tests/test_oracle_*.py, all "not gpu"):
+ *   - whole objective + argmin: brute force over every stage-and-strategy
+ *     assignment (oracle/brute.py) on the toy and >= 2000 random instances;
+ *   - interval table: textbook tropical matrix-chain product when memory is
+ *     slack; multiple-choice-knapsack brute force when costs vanish;
+ *   - deg=1 path == Appendix C QIP (an independent chain DP);
+ *   - closed forms (R=0, |S|=1, c=1 & O=0 tie-break, large-c min-max);
+ *   - builder': the SPEC.md worked examples and Eq. (1) anchors.
+ */
+#include "oracle.h"
+
+#include <limits.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+typedef unsigned __int128 u128;
+
+#define INF ((int64_t)1 << 60) /* "infeasible" inside the oracle (int64) */
+#define ENTRY_MAX (1 << 22)    /* reading A-10: table entries in [0, 2^22]   */
+#define SUM_MAX (1 << 28)      /* reading A-9: per-config sum bound          */
+
+static int64_t add_sat(int64_t x, int64_t y) { return (x >= INF || y >= INF) ? INF : (x + y >= INF ? INF : x + y); }
+static int64_t min64(int64_t x, int64_t y) { return x < y ? x : y; }
+static int64_t max64(int64_t x, int64_t y) { return x > y ? x : y; }
+
+/* ======================================================================== */
+/* Validation of level-1 tables                                             */
+/* ======================================================================== */
+static int validate_tables(const orc_tables* t) {
+  if (!t || t->L < 1 || t->L > ORC_MAX_L || t->cap < 0 || t->n_cfg < 1 || !t->cfg) return ORC_ERR_ARG;
+  if (t->skip_src < -1 || t->skip_src >= t->L) return ORC_ERR_ARG;
+  int L = t->L;
+  for (int i = 0; i < t->n_cfg; ++i) {
+    const orc_cfg* c = &t->cfg[i];
+    if (c->deg < 1 || c->c < 1 || c->n_strat < 1 || c->n_strat > ORC_MAX_S) return ORC_ERR_ARG;
+    if (!c->A || !c->M || (L > 1 && !c->R)) return ORC_ERR_ARG;
+    for (int j = 0; j < i; ++j)
+      if (t->cfg[j].deg == c->deg && t->cfg[j].c == c->c) return ORC_ERR_ARG;
+    int S = c->n_strat;
+    int64_t sum = 0, osum = 0;
+    for (int u = 0; u < L; ++u) {
+      int64_t ma = 0, mr = 0, ms = 0;
+      for (int k = 0; k < S; ++k) {
+        int32_t a = c->A[u * S + k], m = c->M[u * S + k];
+        if (a < 0 || a > ENTRY_MAX || m < 0) return ORC_ERR_RANGE;
+        ma = max64(ma, a);
+      }
+      if (u >= 1)
+        for (int k = 0; k < S * S; ++k) {
+          int32_t r = c->R[(size_t)(u - 1) * S * S + k];
+          if (r < 0 || r > ENTRY_MAX) return ORC_ERR_RANGE;
+          mr = max64(mr, r);
+        }
+      if (c->Rskip && t->skip_src >= 0 && u >= t->skip_src + 2)
+        for (int k = 0; k < S * S; ++k) {
+          int32_t r = c->Rskip[(size_t)u * S * S + k];
+          if (r < 0 || r > ENTRY_MAX) return ORC_ERR_RANGE;
+          ms = max64(ms, r);
+        }
+      sum += ma + mr + ms;
+    }
+    if (c->O)
+      for (int e = 0; e < L - 1; ++e) {
+        if (c->O[e] < 0 || c->O[e] > ENTRY_MAX) return ORC_ERR_RANGE;
+        osum += c->O[e];
+      }
+    if (sum > SUM_MAX || osum > SUM_MAX) return ORC_ERR_RANGE;
+  }
+  return ORC_OK;
+}
+
+/* ======================================================================== */
+/* Per-layer cost terms of Eq. (3) with the skip-edge conditioning          */
+/* ======================================================================== */
+/* A'_uk: the execution cost A_uk plus, when the skip source s of the graph
+ * lies in the same stage with strategy ks, the resharding term of the skip
+ * edge <s,u> (Eq. 3's quadratic term; readings A-16, A-17). */
+static int64_t A_cond(const orc_tables* t, const orc_cfg* c, int u, int k, int ks) {
+  int S = c->n_strat;
+  int64_t a = c->A[u * S + k];
+  if (ks >= 0 && c->Rskip && u >= t->skip_src + 2)
+    a += c->Rskip[((size_t)u * S + ks) * S + k];
+  return a;
+}
+/* Strategy k of layer u is allowed: memory entry within the cap (Eq. 5 with
+ * the forbidden sentinel), and layer s fixed to ks when conditioning. */
+static int allowed(const orc_tables* t, const orc_cfg* c, int u, int k, int ks) {
+  if (c->M[u * c->n_strat + k] > t->cap) return 0;
+  if (ks >= 0 && u == t->skip_src && k != ks) return 0;
+  return 1;
+}
+static int32_t Rchain(const orc_cfg* c, int u, int k, int l) { /* edge u -> u+1 */
+  int S = c->n_strat;
+  return c->R[((size_t)u * S + k) * S + l];
+}
+static int64_t Ocut(const orc_cfg* c, int e) { return c->O ? c->O[e] : 0; }
+
+/* ======================================================================== */
+/* Interval table: the stage optimum of Eq. (3) under Eq. (5)               */
+/* ======================================================================== */
+/* For a fixed start layer a and skip conditioning ks (-1 = none), the
+ * textbook forward chain DP over (layer, strategy, memory):
+ *   D[a][k][q] = A'_ak                                   if M_ak <= q
+ *   D[u][k][q] = A'_uk + min_k' ( D[u-1][k'][q-M_uk] + R_{u-1,u}[k'][k] )
+ *                                                         if M_uk <= q
+ * (INF otherwise), so D[u][k][q] is the minimum of Eq. (3)'s p over layers
+ * a..u with layer u on strategy k and memory sum (Eq. 5) at most q.
+ * Row b of the result is  min_k D[b][k][cap]. */
+static void interval_row(const orc_tables* t, const orc_cfg* c, int a, int ks, int64_t* row) {
+  int L = t->L, S = c->n_strat, Q = t->cap + 1;
+  int64_t* Dp = (int64_t*)malloc(sizeof(int64_t) * (size_t)S * Q);
+  int64_t* Dc = (int64_t*)malloc(sizeof(int64_t) * (size_t)S * Q);
+  for (int k = 0; k < S; ++k)
+    for (int q = 0; q < Q; ++q)
+      Dc[(size_t)k * Q + q] = (allowed(t, c, a, k, ks) && c->M[a * S + k] <= q) ? A_cond(t, c, a, k, ks) : INF;
+  for (int u = a;; ++u) {
+    int64_t best = INF;
+    for (int k = 0; k < S; ++k) best = min64(best, Dc[(size_t)k * Q + t->cap]);
+    row[u] = best;
+    if (u + 1 >= L) break;
+    int64_t* tmp = Dp; Dp = Dc; Dc = tmp;
+    int v = u + 1;
+    for (int k = 0; k < S; ++k) {
+      int64_t* out = Dc + (size_t)k * Q;
+      for (int q = 0; q < Q; ++q) out[q] = INF;
+      if (!allowed(t, c, v, k, ks)) continue;
+      int m = c->M[v * S + k];
+      int64_t av = A_cond(t, c, v, k, ks);
+      /* min over k' of D[u][k'][q-m] + R[k'][k]  (same min, k' outermost) */
+      for (int kp = 0; kp < S; ++kp) {
+        int64_t r = Rchain(c, u, kp, k);
+        const int64_t* in = Dp + (size_t)kp * Q;
+        for (int q = m; q < Q; ++q) {
+          int64_t x = in[q - m] + r;
+          if (x < out[q]) out[q] = x;
+        }
+      }
+      for (int q = m; q < Q; ++q) out[q] = out[q] >= INF ? INF : out[q] + av;
+    }
+  }
+  free(Dp);
+  free(Dc);
+}
+
+/* P[a][b] for all a <= b.  When the skip source s lies in [a, b) the stage
+ * also pays the skip edges <s,v> with v <= b (Eq. 3 sums every edge with both
+ * ends in the stage), which couples layer s's strategy with later layers: the
+ * minimum is taken over the conditioning ks of layer s (SURVEY.md Sec. 8c C-2
+ * step 2). */
+static void interval_table(const orc_tables* t, const orc_cfg* c, int64_t* P) {
+  int L = t->L, S = c->n_strat, s = t->skip_src;
+  int64_t* row = (int64_t*)malloc(sizeof(int64_t) * L);
+  for (int i = 0; i < L * L; ++i) P[i] = INF;
+  for (int a = 0; a < L; ++a) {
+    int cond = (s >= 0 && c->Rskip && a <= s && s + 2 < L);
+    for (int ks = cond ? 0 : -1; ks < (cond ? S : 0); ++ks) {
+      interval_row(t, c, a, ks, row);
+      for (int b = a; b < L; ++b) P[a * L + b] = min64(P[a * L + b], row[b]);
+    }
+  }
+  free(row);
+}
+
+/* ======================================================================== */
+/* Combine: Eq. (2) over ordered contiguous placements (Pareto-suffix DP)   */
+/* ======================================================================== */
+/* Set(i, a) = the non-dominated pairs (Sigma, mx) over ways to cover layers
+ * [a, L-1] with stages i..deg, where Sigma = sum of their p and of the o of
+ * their cuts and mx = max of those p and o.  Eq. (2) is
+ *   tpi = Sigma + (c-1) * mx,
+ * non-decreasing in both, so dominated pairs never matter. */
+typedef struct { int64_t sig, mx; } pair_t;
+typedef struct { pair_t* v; int n; } pset;
+
+static int pair_cmp(const void* x, const void* y) {
+  const pair_t *p = (const pair_t*)x, *q = (const pair_t*)y;
+  if (p->sig != q->sig) return p->sig < q->sig ? -1 : 1;
+  if (p->mx != q->mx) return p->mx < q->mx ? -1 : 1;
+  return 0;
+}
+static void pareto(pset* s) {
+  qsort(s->v, s->n, sizeof(pair_t), pair_cmp);
+  int w = 0;
+  for (int r = 0; r < s->n; ++r)
+    if (w == 0 || s->v[r].mx < s->v[w - 1].mx) s->v[w++] = s->v[r];
+  s->n = w;
+}
+
+typedef struct {
+  int64_t obj;             /* INF if infeasible */
+  int32_t end[ORC_MAX_L];  /* last layer of stage i */
+  int32_t strat[ORC_MAX_L];
+  int64_t p[ORC_MAX_L], o[ORC_MAX_L];
+  int32_t mem[ORC_MAX_L];
+  int status;
+} cfg_sol;
+
+/* value of Eq. (2) for a prefix (sig0,mx0) + stage (pa,ob) + suffix pair */
+static int64_t tpi(int64_t sig, int64_t mx, int c) { return sig + (int64_t)(c - 1) * mx; }
+
+/* ======================================================================== */
+/* Strategies of one stage: lexicographically smallest optimal vector      */
+/* ======================================================================== */
+/* Backward DP G[u][k][q] = min cost of layers u..b given layer u on k and
+ * memory at most q for u..b; then walk forward taking the smallest k that
+ * still reaches the stage optimum (reading A-11). Returns 1 if found. */
+static int stage_walk(const orc_tables* t, const orc_cfg* c, int a, int b, int ks, int64_t target,
+                      int32_t* out) {
+  int S = c->n_strat, Q = t->cap + 1, n = b - a + 1;
+  int64_t* G = (int64_t*)malloc(sizeof(int64_t) * (size_t)n * S * Q);
+#define GI(u, k, q) G[(((size_t)((u) - a) * S) + (k)) * Q + (q)]
+  for (int u = b; u >= a; --u)
+    for (int k = 0; k < S; ++k)
+      for (int q = 0; q < Q; ++q) {
+        int m = c->M[u * S + k];
+        int64_t v = INF;
+        if (allowed(t, c, u, k, ks) && m <= q) {
+          if (u == b) v = A_cond(t, c, u, k, ks);
+          else {
+            int64_t best = INF;
+            for (int k2 = 0; k2 < S; ++k2) best = min64(best, add_sat(Rchain(c, u, k, k2), GI(u + 1, k2, q - m)));
+            v = add_sat(best, A_cond(t, c, u, k, ks));
+          }
+        }
+        GI(u, k, q) = v;
+      }
+  int64_t rem = target;
+  int q = t->cap, found = 1, kprev = -1;
+  for (int u = a; u <= b && found; ++u) {
+    found = 0;
+    for (int k = 0; k < S; ++k) {
+      int64_t edge = (u > a) ? Rchain(c, u - 1, kprev, k) : 0;
+      if (GI(u, k, q) < INF && edge + GI(u, k, q) == rem) {
+        out[u] = k;
+        rem -= edge + A_cond(t, c, u, k, ks);
+        q -= c->M[u * S + k];
+        kprev = k;
+        found = 1;
+        break;
+      }
+    }
+  }
+#undef GI
+  free(G);
+  return found;
+}
+
+static void stage_strategies(const orc_tables* t, const orc_cfg* c, int a, int b, int64_t target,
+                             int32_t* strat) {
+  int S = c->n_strat, s = t->skip_src;
+  int cond = (s >= 0 && c->Rskip && a <= s && s + 2 <= b);
+  if (!cond) {
+    stage_walk(t, c, a, b, -1, target, strat);
+    return;
+  }
+  int32_t best[ORC_MAX_L], cur[ORC_MAX_L];
+  int have = 0;
+  for (int ks = 0; ks < S; ++ks) {
+    if (!stage_walk(t, c, a, b, ks, target, cur)) continue;
+    int less = !have;
+    for (int u = a; u <= b && !less; ++u) {
+      if (cur[u] != best[u]) { less = cur[u] < best[u]; break; }
+    }
+    if (less) { memcpy(best + a, cur + a, sizeof(int32_t) * (b - a + 1)); have = 1; }
+  }
+  memcpy(strat + a, best + a, sizeof(int32_t) * (b - a + 1));
+}
+
+/* ======================================================================== */
+/* One candidate config: the MIQP of Sec. 3.3 solved exactly                */
+/* ======================================================================== */
+static void solve_cfg(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
+  int L = t->L, deg = c->deg;
+  sol->obj = INF;
+  sol->status = ORC_OK;
+  if (deg > L) return; /* Eq. (7b) cannot hold (reading A-22) */
+  int64_t* P = (int64_t*)malloc(sizeof(int64_t) * L * L);
+  interval_table(t, c, P);
+  /* Set(i,a), i = 1..deg (index i-1), a = 0..L-1 */
+  pset* sets = (pset*)calloc((size_t)deg * L, sizeof(pset));
+#define SET(i, a) sets[(size_t)((i) - 1) * L + (a)]
+  for (int a = 0; a < L; ++a) {
+    pset* s = &SET(deg, a);
+    if (P[a * L + L - 1] < INF) {
+      s->v = (pair_t*)malloc(sizeof(pair_t));
+      s->v[0].sig = P[a * L + L - 1];
+      s->v[0].mx = P[a * L + L - 1];
+      s->n = 1;
+    }
+  }
+  for (int i = deg - 1; i >= 1; --i)
+    for (int a = 0; a < L; ++a) {
+      int cnt = 0;
+      for (int b = a; b + 1 < L; ++b) if (P[a * L + b] < INF) cnt += SET(i + 1, b + 1).n;
+      pset* s = &SET(i, a);
+      if (!cnt) continue;
+      s->v = (pair_t*)malloc(sizeof(pair_t) * cnt);
+      for (int b = a; b + 1 < L; ++b) {
+        int64_t p = P[a * L + b];
+        if (p >= INF) continue;
+        int64_t o = Ocut(c, b);
+        const pset* nx = &SET(i + 1, b + 1);
+        for (int j = 0; j < nx->n; ++j) {
+          s->v[s->n].sig = p + o + nx->v[j].sig;
+          s->v[s->n].mx = max64(max64(p, o), nx->v[j].mx);
+          s->n++;
+        }
+      }
+      pareto(s);
+    }
+  int64_t opt = INF;
+  for (int j = 0; j < SET(1, 0).n; ++j) opt = min64(opt, tpi(SET(1, 0).v[j].sig, SET(1, 0).v[j].mx, c->c));
+  sol->obj = opt;
+  if (opt < INF) {
+    /* Stage ends: the lexicographically smallest stage_of is the largest
+     * feasible end for each stage in turn (reading A-11). */
+    int64_t sig = 0, mx = 0;
+    int a = 0;
+    for (int i = 1; i < deg; ++i) {
+      int chosen = -1;
+      for (int b = L - 2; b >= a && chosen < 0; --b) {
+        int64_t p = P[a * L + b];
+        if (p >= INF) continue;
+        int64_t o = Ocut(c, b);
+        const pset* nx = &SET(i + 1, b + 1);
+        for (int j = 0; j < nx->n; ++j)
+          if (tpi(sig + p + o + nx->v[j].sig, max64(max64(mx, max64(p, o)), nx->v[j].mx), c->c) == opt) {
+            chosen = b;
+            break;
+          }
+      }
+      if (chosen < 0) { sol->status = ORC_ERR_INTERNAL; break; }
+      int64_t p = P[a * L + chosen], o = Ocut(c, chosen);
+      sig += p + o;
+      mx = max64(mx, max64(p, o));
+      sol->end[i - 1] = chosen;
+      sol->p[i - 1] = p;
+      sol->o[i - 1] = o;
+      a = chosen + 1;
+    }
+    sol->end[deg - 1] = L - 1;
+    sol->p[deg - 1] = P[a * L + L - 1];
+    /* strategies per stage */
+    int start = 0;
+    for (int i = 0; i < deg && sol->status == ORC_OK; ++i) {
+      stage_strategies(t, c, start, sol->end[i], sol->p[i], sol->strat);
+      start = sol->end[i] + 1;
+    }
+  }
+  for (int i = 0; i < deg * L; ++i) free(sets[i].v);
+#undef SET
+  free(sets);
+  free(P);
+}
+
+/* Literal re-evaluation of Eqs. (2), (3), (5) from (stage_of, strategy_of). */
+static int check_solution(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
+  int L = t->L, S = c->n_strat, s = t->skip_src, deg = c->deg;
+  int start = 0;
+  int64_t sum = 0, mx = 0;
+  for (int i = 0; i < deg; ++i) {
+    int b = sol->end[i];
+    if (b < start) return ORC_ERR_INTERNAL;
+    int64_t p = 0, mem = 0;
+    for (int u = start; u <= b; ++u) {
+      int k = sol->strat[u];
+      if (k < 0 || k >= S) return ORC_ERR_INTERNAL;
+      p += c->A[u * S + k];
+      mem += c->M[u * S + k];
+      if (u < b) p += Rchain(c, u, k, sol->strat[u + 1]);
+      if (c->Rskip && s >= 0 && start <= s && u >= s + 2) p += c->Rskip[((size_t)u * S + sol->strat[s]) * S + k];
+    }
+    if (mem > t->cap || p != sol->p[i]) return ORC_ERR_INTERNAL;
+    sol->mem[i] = (int32_t)mem;
+    sum += p;
+    mx = max64(mx, p);
+    if (i + 1 < deg) {
+      int64_t o = Ocut(c, b);
+      if (o != sol->o[i]) return ORC_ERR_INTERNAL;
+      sum += o;
+      mx = max64(mx, o);
+    }
+    start = b + 1;
+  }
+  if (start != L) return ORC_ERR_INTERNAL;
+  if (tpi(sum, mx, c->c) != sol->obj) return ORC_ERR_INTERNAL;
+  return ORC_OK;
+}
+
+/* ======================================================================== */
+/* Algorithm 1 outer loop over candidates, optionally on host threads       */
+/* ======================================================================== */
+typedef struct {
+  const orc_tables* t;
+  cfg_sol* sols;
+  int next;
+  pthread_mutex_t mu;
+} pool_t;
+
+static void* worker(void* arg) {
+  pool_t* p = (pool_t*)arg;
+  for (;;) {
+    pthread_mutex_lock(&p->mu);
+    int i = p->next++;
+    pthread_mutex_unlock(&p->mu);
+    if (i >= p->t->n_cfg) break;
+    solve_cfg(p->t, &p->t->cfg[i], &p->sols[i]);
+    if (p->sols[i].status == ORC_OK && p->sols[i].obj < INF)
+      p->sols[i].status = check_solution(p->t, &p->t->cfg[i], &p->sols[i]);
+  }
+  return NULL;
+}
+
+int orc_solve(const orc_tables* t, int n_threads, orc_result* res, int64_t* cfg_obj) {
+  int st = validate_tables(t);
+  if (st != ORC_OK) return st;
+  cfg_sol* sols = (cfg_sol*)calloc(t->n_cfg, sizeof(cfg_sol));
+  pool_t pool = {t, sols, 0, PTHREAD_MUTEX_INITIALIZER};
+  if (n_threads <= 0) n_threads = (int)sysconf(_SC_NPROCESSORS_ONLN);
+  if (n_threads > t->n_cfg) n_threads = t->n_cfg;
+  if (n_threads <= 1) {
+    worker(&pool);
+  } else {
+    pthread_t th[256];
+    if (n_threads > 256) n_threads = 256;
+    for (int i = 0; i < n_threads; ++i) pthread_create(&th[i], NULL, worker, &pool);
+    for (int i = 0; i < n_threads; ++i) pthread_join(th[i], NULL);
+  }
+  /* ordered minimum by (tpi, deg, c)  (PAPER.md:221 strict '<' over the
+   * ascending enumeration; reading A-11) */
+  int win = -1;
+  for (int i = 0; i < t->n_cfg; ++i) {
+    if (sols[i].status != ORC_OK) { st = sols[i].status; break; }
+    if (cfg_obj) cfg_obj[i] = sols[i].obj < INF ? sols[i].obj : INT64_MAX;
+    if (sols[i].obj >= INF) continue;
+    if (win < 0) { win = i; continue; }
+    const orc_cfg *x = &t->cfg[i], *w = &t->cfg[win];
+    if (sols[i].obj < sols[win].obj ||
+        (sols[i].obj == sols[win].obj && (x->deg < w->deg || (x->deg == w->deg && x->c < w->c))))
+      win = i;
+  }
+  memset(res, 0, sizeof(*res));
+  res->L = t->L;
+  res->objective = INT64_MAX;
+  res->cfg_index = -1;
+  if (st == ORC_OK && win < 0) st = ORC_ERR_INFEASIBLE;
+  if (st == ORC_OK) {
+    const cfg_sol* s = &sols[win];
+    const orc_cfg* c = &t->cfg[win];
+    res->objective = s->obj;
+    res->cfg_index = win;
+    res->deg = c->deg;
+    res->c = c->c;
+    int stage = 0;
+    for (int u = 0; u < t->L; ++u) {
+      while (u > s->end[stage]) ++stage;
+      res->stage_of[u] = stage;
+      res->strategy_of[u] = s->strat[u];
+    }
+    for (int i = 0; i < c->deg; ++i) {
+      res->stage_cost[i] = s->p[i];
+      res->stage_mem[i] = s->mem[i];
+      if (i + 1 < c->deg) res->cut_cost[i] = s->o[i];
+    }
+  }
+  free(sols);
+  return st;
+}
+
+int orc_interval_table(const orc_tables* t, int cfg, int64_t* P) {
+  int st = validate_tables(t);
+  if (st != ORC_OK) return st;
+  if (cfg < 0 || cfg >= t->n_cfg) return ORC_ERR_ARG;
+  interval_table(t, &t->cfg[cfg], P);
+  for (int i = 0; i < t->L * t->L; ++i)
+    if (P[i] >= INF) P[i] = INT64_MAX;
+  return ORC_OK;
+}
+
+/* ======================================================================== */
+/* Level 2: builder' -- the cost model of Sec. 3.2 in integers              */
+/* ======================================================================== */
+/* Strategy dictionary SD[deg]: every (TP, FSDP, DP)
+ * degree triple (t,f,d) with t*f*d = g, t a profiled TP size (power of two);
+ * ordered t ascending then f ascending, so index 0 is pure DP, as in
+ * Appendix D's S_{l0}.  Reading A-6. */
+int orc_catalogue(int32_t g, int32_t* tfd, int32_t cap) {
+  int n = 0;
+  if (g < 1) return 0;
+  for (int t = 1; t <= g; t *= 2) {
+    if (g % t) break;
+    for (int f = 1; f <= g / t; ++f) {
+      if ((g / t) % f) continue;
+      int d = g / t / f;
+      if (n < cap) { tfd[3 * n] = t; tfd[3 * n + 1] = f; tfd[3 * n + 2] = d; }
+      ++n;
+    }
+  }
+  return n;
+}
+
+/* Algorithm 1: first deg = 1 (the QIP of App. C, modelled
+ * at batch B, reported as c = 1 -- reading A-4), then every factor deg > 1 of
+ * n and every factor c > 1 of B, deg ascending then c ascending. */
+int orc_candidates(int32_t n, int32_t B, int32_t* pairs, int32_t cap) {
+  int k = 0;
+  if (cap > 0) { pairs[0] = 1; pairs[1] = 1; }
+  k = 1;
+  for (int deg = 2; deg <= n; ++deg) {
+    if (n % deg) continue;
+    for (int c = 2; c <= B; ++c) {
+      if (B % c) continue;
+      if (k < cap) { pairs[2 * k] = deg; pairs[2 * k + 1] = c; }
+      ++k;
+    }
+  }
+  return k;
+}
+
+#define NS_LIMIT ((u128)1 << 62) /* any modelled time / byte count must stay below */
+
+static u128 cdiv(u128 x, u128 y) { return (x + y - 1) / y; }
+
+/* "dividing the size of transmitting tensors by the profiled communication
+ * efficiency" with the ring model of SPEC.md:146; the link is
+ * the inter-node one when the group's device span (stride * G) exceeds a
+ * node (reading: collective bandwidth). */
+static int64_t bw_for(const orc_cluster* cl, int64_t G, int64_t stride) {
+  return (stride * G > cl->node_size) ? cl->bw_inter : cl->bw_intra;
+}
+static u128 t_allreduce(const orc_cluster* cl, u128 V, int64_t G, int64_t stride) {
+  if (G <= 1) return 0;
+  return cdiv((u128)2 * (G - 1) * V * 1000000000u, (u128)G * bw_for(cl, G, stride)) +
+         (u128)2 * (G - 1) * cl->lat_ns;
+}
+static u128 t_allgather(const orc_cluster* cl, u128 V, int64_t G, int64_t stride) {
+  if (G <= 1) return 0;
+  return cdiv((u128)(G - 1) * V * 1000000000u, (u128)G * bw_for(cl, G, stride)) + (u128)(G - 1) * cl->lat_ns;
+}
+static u128 t_p2p(const orc_cluster* cl, u128 V) {
+  return cdiv(V * 1000000000u, (u128)cl->p2p_bw) + (u128)cl->lat_ns;
+}
+/* "multiplies the profiled CCOC by the overlapping interval of computation
+ * and communication": hidden = floor(ccoc * min / 1000)
+ * (reading A-23). */
+static u128 t_overlap(u128 comp, u128 comm, int32_t ccoc_permille) {
+  u128 mn = comp < comm ? comp : comm;
+  return comp + comm - (u128)ccoc_permille * mn / 1000;
+}
+static int ilog2(int x) { int r = 0; while ((1 << (r + 1)) <= x) ++r; return r; }
+
+/* Resharding between the output layout of strategy (t1,f1,d1) and the input
+ * layout of (t2,f2,d2) on a tensor of V bytes: free if the (TP, replica)
+ * layouts match, else an all-reduce-shaped exchange over the
+ * largest ratio of a differing axis, forward + backward (reading A-15). */
+static u128 t_reshard(const orc_cluster* cl, const int32_t* s1, const int32_t* s2, u128 V) {
+  int64_t t1 = s1[0], r1 = (int64_t)s1[1] * s1[2], t2 = s2[0], r2 = (int64_t)s2[1] * s2[2];
+  if (t1 == t2 && r1 == r2) return 0;
+  int64_t G = 1; /* ratio max/min of each differing axis, rounded up */
+  if (t1 != t2) G = max64(G, t1 > t2 ? (t1 + t2 - 1) / t2 : (t2 + t1 - 1) / t1);
+  if (r1 != r2) G = max64(G, r1 > r2 ? (r1 + r2 - 1) / r2 : (r2 + r1 - 1) / r1);
+  return 2 * t_allreduce(cl, V, G, 1);
+}
+
+int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, int32_t* buf,
+              int64_t buf_len, int32_t* n_cfg_out, int32_t* skip_out, int64_t* quantum_out,
+              int64_t* words_out) {
+  if (!m || !cl || !o || m->L < 1 || m->L > ORC_MAX_L || !m->layers) return ORC_ERR_ARG;
+  if (cl->n_dev < 1 || cl->node_size < 1 || cl->bw_intra < 1 || cl->bw_inter < 1 || cl->p2p_bw < 1 ||
+      cl->lat_ns < 0 || cl->ccoc_permille < 0 || cl->ccoc_permille > 1000)
+    return ORC_ERR_ARG;
+  if (o->B < 1 || o->B > 65536 || o->Q < 2 || o->Q > 16384 || (o->precision != 0 && o->precision != 1) ||
+      o->quantum_ns < 0)
+    return ORC_ERR_ARG;
+  int L = m->L, n = cl->n_dev, cap = o->Q - 1;
+  if (cl->mem_bytes <= cl->mem_reserve || cl->mem_reserve < 0) return ORC_ERR_ARG;
+  int64_t unit = (cl->mem_bytes - cl->mem_reserve) / cap; /* reading A-8 */
+  if (unit < 1) return ORC_ERR_ARG;
+  int maxtp = 1;
+  while (n % (maxtp * 2) == 0) maxtp *= 2;
+  const int64_t LIM = (int64_t)1 << 46;
+  for (int u = 0; u < L; ++u) {
+    const orc_layer* ly = &m->layers[u];
+    if (ly->param_bytes < 0 || ly->param_bytes > LIM || ly->ctx_bytes < 0 || ly->ctx_bytes > LIM ||
+        ly->tpcomm_bytes < 0 || ly->tpcomm_bytes > LIM || !ly->fwd_ns || !ly->act_bytes)
+      return ORC_ERR_ARG;
+    for (int i = 0; i <= ilog2(maxtp); ++i)
+      if (ly->fwd_ns[i] < 0 || ly->fwd_ns[i] > ((int64_t)1 << 40) || ly->act_bytes[i] < 0 ||
+          ly->act_bytes[i] > LIM)
+        return ORC_ERR_ARG;
+  }
+  /* edges: chain edges u->u+1, plus skip edges from one source s to v >= s+2 */
+  int skip = -1;
+  int64_t chain_tb[ORC_MAX_L];
+  int has_chain[ORC_MAX_L];
+  int64_t skip_tb[ORC_MAX_L];
+  int has_skip[ORC_MAX_L];
+  memset(has_chain, 0, sizeof has_chain);
+  memset(has_skip, 0, sizeof has_skip);
+  for (int e = 0; e < m->n_edges; ++e) {
+    const orc_edge* ed = &m->edges[e];
+    if (ed->src < 0 || ed->dst >= L || ed->src >= ed->dst || ed->tensor_bytes < 0 || ed->tensor_bytes > LIM)
+      return ORC_ERR_ARG;
+    if (ed->dst == ed->src + 1) {
+      if (has_chain[ed->src]) return ORC_ERR_ARG;
+      has_chain[ed->src] = 1;
+      chain_tb[ed->src] = ed->tensor_bytes;
+    } else {
+      if (skip >= 0 && skip != ed->src) return ORC_ERR_ARG; /* one skip source (NEXT-4 otherwise) */
+      skip = ed->src;
+      if (has_skip[ed->dst]) return ORC_ERR_ARG;
+      has_skip[ed->dst] = 1;
+      skip_tb[ed->dst] = ed->tensor_bytes;
+    }
+  }
+  int32_t cand_buf[2 * 4096];
+  int n_cand;
+  const int32_t* cand;
+  if (o->cand) {
+    n_cand = o->n_cand;
+    cand = o->cand;
+    if (n_cand < 1) return ORC_ERR_ARG;
+    for (int i = 0; i < n_cand; ++i) {
+      int deg = cand[2 * i], c = cand[2 * i + 1];
+      if (deg < 1 || c < 1 || n % deg || o->B % c) return ORC_ERR_ARG;
+      for (int j = 0; j < i; ++j)
+        if (cand[2 * j] == deg && cand[2 * j + 1] == c) return ORC_ERR_ARG;
+    }
+  } else {
+    n_cand = orc_candidates(n, o->B, cand_buf, 4096);
+    if (n_cand > 4096) return ORC_ERR_ARG;
+    cand = cand_buf;
+  }
+  /* pass 1: sizes and the int64 ns/byte values */
+  int64_t words = 0;
+  int Ss[4096];
+  for (int i = 0; i < n_cand; ++i) {
+    int g = n / cand[2 * i];
+    Ss[i] = orc_catalogue(g, NULL, 0);
+    if (Ss[i] > ORC_MAX_S) return ORC_ERR_RANGE;
+    int S = Ss[i];
+    words += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1);
+  }
+  *words_out = words;
+  *n_cfg_out = n_cand;
+  *skip_out = skip;
+  if (!buf || buf_len < words) return ORC_OK; /* size query */
+  /* int64 tables (ns / bytes), then quantised into buf */
+  int64_t* ns = (int64_t*)calloc((size_t)words, sizeof(int64_t));
+  int64_t off = 0;
+  int cdt = o->precision ? 8 : 4; /* c_dtype */
+  int st = ORC_OK;
+  for (int i = 0; i < n_cand && st == ORC_OK; ++i) {
+    int deg = cand[2 * i], c = cand[2 * i + 1], g = n / deg, S = Ss[i];
+    int64_t b = o->B / c; /* micro-batch size b = B / c (Algorithm 1) */
+    int32_t cat[3 * ORC_MAX_S];
+    orc_catalogue(g, cat, ORC_MAX_S);
+    int64_t* blk = ns + off;
+    blk[0] = deg; blk[1] = c; blk[2] = S; blk[3] = g;
+    int64_t* A = blk + 4;
+    int64_t* M = A + (int64_t)L * S;
+    int64_t* R = M + (int64_t)L * S;
+    int64_t* Rs = R + (int64_t)(L - 1) * S * S;
+    int64_t* O = Rs + (int64_t)L * S * S;
+    for (int u = 0; u < L; ++u) {
+      const orc_layer* ly = &m->layers[u];
+      for (int k = 0; k < S; ++k) {
+        int64_t t = cat[3 * k], f = cat[3 * k + 1], d = cat[3 * k + 2], r = f * d;
+        if (b % r) { A[u * S + k] = 0; M[u * S + k] = -1; continue; } /* reading A-7 */
+        int64_t bl = b / r;
+        int lt = ilog2((int)t);
+        /* time cost model: fwd = batch x per-sample time,
+         * bp = 2 fp, TP comm overlapped with computation via CCOC */
+        u128 fp = (u128)bl * ly->fwd_ns[lt];
+        u128 comp = 3 * fp;
+        u128 tpc = 3 * t_allreduce(cl, (u128)bl * ly->tpcomm_bytes, t, 1);
+        u128 ov = t_overlap(comp, tpc, cl->ccoc_permille);
+        u128 ps_t = cdiv((u128)ly->param_bytes, (u128)t);
+        u128 ps_tf = cdiv((u128)ly->param_bytes, (u128)(t * f));
+        u128 fsdp = f > 1 ? 2 * t_allgather(cl, ps_t, f, t) : 0;
+        u128 sync = t_allreduce(cl, ps_tf, d, t * f) + (f > 1 ? t_allgather(cl, ps_t, f, t) : 0);
+        u128 a = ov + fsdp + cdiv(sync, (u128)c);
+        /* memory cost model, Eq. (1) + activations + context */
+        u128 mem = cdiv((u128)cdt * ly->param_bytes, (u128)(t * f)) + (u128)c * bl * ly->act_bytes[lt] +
+                   (u128)ly->ctx_bytes;
+        if (a >= NS_LIMIT || mem >= NS_LIMIT) { st = ORC_ERR_RANGE; break; }
+        A[u * S + k] = (int64_t)a;
+        M[u * S + k] = (int64_t)mem;
+      }
+    }
+    for (int u = 0; u + 1 < L && st == ORC_OK; ++u)
+      for (int k = 0; k < S; ++k)
+        for (int l = 0; l < S; ++l) {
+          u128 v = has_chain[u] ? t_reshard(cl, &cat[3 * k], &cat[3 * l], (u128)b * chain_tb[u]) : 0;
+          if (v >= NS_LIMIT) st = ORC_ERR_RANGE;
+          R[((int64_t)u * S + k) * S + l] = (int64_t)v;
+        }
+    for (int v = 0; v < L && st == ORC_OK; ++v)
+      for (int k = 0; k < S; ++k)
+        for (int l = 0; l < S; ++l) {
+          u128 x = has_skip[v] ? t_reshard(cl, &cat[3 * k], &cat[3 * l], (u128)b * skip_tb[v]) : 0;
+          if (x >= NS_LIMIT) st = ORC_ERR_RANGE;
+          Rs[((int64_t)v * S + k) * S + l] = (int64_t)x;
+        }
+    /* cut cost o_j: the P2P of every edge crossing the cut, forward and
+     * backward (o_j = fo_j + bo_j; readings A-1, A-16) */
+    for (int e = 0; e + 1 < L && st == ORC_OK; ++e) {
+      u128 sum = 0;
+      for (int j = 0; j < m->n_edges; ++j) {
+        const orc_edge* ed = &m->edges[j];
+        if (ed->src <= e && e < ed->dst) sum += 2 * t_p2p(cl, (u128)b * ed->tensor_bytes);
+      }
+      if (sum >= NS_LIMIT) st = ORC_ERR_RANGE;
+      O[e] = (int64_t)sum;
+    }
+    off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1);
+  }
+  /* time quantum (reading A-9): smallest power of two such that every entry
+   * fits 2^22 and every config's sums fit 2^28 (or the caller's quantum). */
+  int64_t qn = o->quantum_ns ? o->quantum_ns : 1;
+  for (; st == ORC_OK; qn *= 2) {
+    int ok = 1;
+    off = 0;
+    for (int i = 0; i < n_cand && ok; ++i) {
+      int S = Ss[i];
+      int64_t* A = ns + off + 4;
+      int64_t* R = A + 2 * (int64_t)L * S;
+      int64_t* Rs = R + (int64_t)(L - 1) * S * S;
+      int64_t* O = Rs + (int64_t)L * S * S;
+      int64_t sum = 0, osum = 0;
+      for (int u = 0; u < L; ++u) {
+        int64_t ma = 0, mr = 0, ms = 0;
+        for (int k = 0; k < S; ++k) ma = max64(ma, (A[u * S + k] + qn - 1) / qn);
+        if (u >= 1)
+          for (int k = 0; k < S * S; ++k) mr = max64(mr, (R[(int64_t)(u - 1) * S * S + k] + qn - 1) / qn);
+        if (skip >= 0 && u >= skip + 2)
+          for (int k = 0; k < S * S; ++k) ms = max64(ms, (Rs[(int64_t)u * S * S + k] + qn - 1) / qn);
+        if (ma > ENTRY_MAX || mr > ENTRY_MAX || ms > ENTRY_MAX) ok = 0;
+        sum += ma + mr + ms;
+      }
+      for (int e = 0; e + 1 < L; ++e) {
+        int64_t x = (O[e] + qn - 1) / qn;
+        if (x > ENTRY_MAX) ok = 0;
+        osum += x;
+      }
+      if (sum > SUM_MAX || osum > SUM_MAX) ok = 0;
+      off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1);
+    }
+    if (ok) break;
+    if (o->quantum_ns) { st = ORC_ERR_RANGE; break; }
+    if (qn >= ((int64_t)1 << 61)) { st = ORC_ERR_RANGE; break; }
+  }
+  if (st == ORC_OK) {
+    *quantum_out = qn;
+    off = 0;
+    for (int i = 0; i < n_cand; ++i) {
+      int S = Ss[i];
+      int64_t* blk = ns + off;
+      int32_t* out = buf + off;
+      for (int j = 0; j < 4; ++j) out[j] = (int32_t)blk[j];
+      int64_t nA = (int64_t)L * S;
+      for (int64_t j = 0; j < nA; ++j) out[4 + j] = (int32_t)((blk[4 + j] + qn - 1) / qn);
+      for (int64_t j = 0; j < nA; ++j) { /* memory buckets (reading A-8) */
+        int64_t byt = blk[4 + nA + j];
+        int64_t bk = byt < 0 ? (int64_t)cap + 1 : (byt + unit - 1) / unit;
+        out[4 + nA + j] = (int32_t)(bk > cap ? cap + 1 : bk);
+      }
+      int64_t rest = (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1);
+      for (int64_t j = 0; j < rest; ++j) out[4 + 2 * nA + j] = (int32_t)((blk[4 + 2 * nA + j] + qn - 1) / qn);
+      off += 4 + 2 * nA + rest;
+    }
+  }
+  free(ns);
+  return st;
+}
+
+/* ---- exported primitives (pinned by tests against SPEC.md's examples) ---- */
+static int64_t clamp62(u128 x) { return x >= NS_LIMIT ? -1 : (int64_t)x; }
+int64_t orc_allreduce_ns(int64_t V, int64_t G, int64_t bw, int64_t lat) {
+  orc_cluster cl = {0};
+  cl.node_size = 1 << 30; cl.bw_intra = cl.bw_inter = bw; cl.lat_ns = lat;
+  return clamp62(t_allreduce(&cl, (u128)V, G, 1));
+}
+int64_t orc_allgather_ns(int64_t V, int64_t G, int64_t bw, int64_t lat) {
+  orc_cluster cl = {0};
+  cl.node_size = 1 << 30; cl.bw_intra = cl.bw_inter = bw; cl.lat_ns = lat;
+  return clamp62(t_allgather(&cl, (u128)V, G, 1));
+}
+int64_t orc_p2p_ns(int64_t V, int64_t bw, int64_t lat) {
+  orc_cluster cl = {0};
+  cl.p2p_bw = bw; cl.lat_ns = lat;
+  return clamp62(t_p2p(&cl, (u128)V));
+}
+int64_t orc_overlap_ns(int64_t comp, int64_t comm, int32_t ccoc_permille) {
+  return clamp62(t_overlap((u128)comp, (u128)comm, ccoc_permille));
+}
