@@ -1,0 +1,215 @@
+/* uniap.h -- C ABI of libuniap.so: exact UniAP strategy search on B200 (sm_100a).
+ *
+ * UniAP (arXiv 2307.16375), /root/reference/PAPER.md.  The library evaluates
+ * exactly the paper's joint inter-/intra-layer objective: for every candidate
+ * pipeline degree deg and micro-batch count c (Algorithm 1)
+ * and every ordered contiguous layer->stage placement (Eqs. 6-7,
+ * PAPER.md:164-192), the optimum of each stage (Eq. 3, PAPER.md:137-145,
+ * under the memory constraint Eq. 5, one strategy per layer
+ * Eq. 8) by a memory-constrained min-plus chain DP over
+ * layer x strategy x memory bucket; the stage optima combined into the GPipe
+ * time per iteration (Eq. 2)
+ *        tpi = sum_i p_i + sum_j o_j + (c-1) * max(P u O)
+ * and the global minimum under the key (tpi, deg, c, stage_of, strategy_of).
+ * Readings of silent passages are DESIGN.md Sec. 2 (A-1 .. A-24).
+ *
+ * Conventions
+ *   - Pointers are HOST pointers unless the name ends in _dev.
+ *   - Inputs are borrowed for the duration of the call; outputs go to
+ *     caller-owned memory.  A handle owns all its device buffers (grown on
+ *     demand, reused across calls) and runs on one CUDA stream; one call at a
+ *     time per handle; handles are independent (one per GPU / thread).
+ *   - Every entry point returns a uniap_status; no exception crosses the ABI.
+ *     uniap_last_error(h) gives a message valid until the next call on h.
+ *   - All costs are integers: time entries in quanta (reading A-9), memory in
+ *     buckets (reading A-8).  The objective is int64.
+ *   - Determinism: results are identical for any world size, run and schedule.
+ *   - There is no CPU fallback: without a usable sm_100 device, uniap_create
+ *     fails with UNIAP_ERR_CUDA.
+ */
+#ifndef UNIAP_H
+#define UNIAP_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UNIAP_INF 0x40000000        /* 2^30: DP "infeasible"; never a table entry (A-10)    */
+#define UNIAP_MAX_ENTRY 0x00400000  /* 2^22: largest A, R, Rskip, O entry (A-10)             */
+#define UNIAP_MAX_SUM 0x10000000    /* 2^28: per-config bound on sum_u (max A + max R into u + max Rskip into u) and on sum O (A-9) */
+#define UNIAP_MAX_LAYERS 64
+#define UNIAP_MAX_STRAT 32
+#define UNIAP_MAX_Q 8192            /* memory buckets (cap + 1) */
+#define UNIAP_MAX_CFG 4096
+
+typedef enum {
+  UNIAP_OK = 0,
+  UNIAP_ERR_ARG = 1,         /* shape / argument violation                                  */
+  UNIAP_ERR_INFEASIBLE = 2,  /* every candidate infeasible (objective = INT64_MAX)          */
+  UNIAP_ERR_RANGE = 3,       /* an entry > 2^22, a sum bound > 2^28, or a modelled value >= 2^62 */
+  UNIAP_ERR_CUDA = 4,        /* CUDA runtime / launch failure, or no sm_100 device          */
+  UNIAP_ERR_COMM = 5,        /* record exchange failure (reported by the binding)           */
+  UNIAP_ERR_OOM = 6,         /* device allocation failed                                    */
+  UNIAP_ERR_INTERNAL = 99    /* self-check of the answer failed (a bug)                      */
+} uniap_status;
+
+typedef struct uniap_handle uniap_handle;
+
+/* Create a handle on CUDA device `device`, issuing work on `cuda_stream`
+ * (a cudaStream_t; NULL = the handle creates and owns its own stream).
+ * Fails with UNIAP_ERR_CUDA if the device is not compute capability 10.x. */
+uniap_status uniap_create(uniap_handle** h, int device, void* cuda_stream);
+void uniap_destroy(uniap_handle* h);
+const char* uniap_last_error(const uniap_handle* h);
+const char* uniap_status_string(uniap_status s);
+const char* uniap_version(void);
+
+/* ---- result ---------------------------------------------------------- */
+/* = SPEC's Assignment + ParallelPlan; the
+ * Algorithm 1 output (cost*, deg*, c*, P*, S*) of PAPER.md:209: stage_of is P
+ * (App. D: P[u][stage_of[u]] = 1), strategy_of is S. */
+typedef struct {
+  int64_t objective;                          /* Eq. 2 in quanta; INT64_MAX if infeasible        */
+  int32_t cfg_index;                          /* winner's index in the candidate list, -1 none   */
+  int32_t deg, c, L;
+  int32_t stage_of[UNIAP_MAX_LAYERS];         /* non-decreasing 0..deg-1                          */
+  int32_t strategy_of[UNIAP_MAX_LAYERS];      /* index into the config's strategy set             */
+  int64_t stage_cost[UNIAP_MAX_LAYERS];       /* p_1..p_deg (Eq. 3)                               */
+  int64_t cut_cost[UNIAP_MAX_LAYERS];         /* o_1..o_{deg-1}                                   */
+  int32_t stage_mem[UNIAP_MAX_LAYERS];        /* buckets used per stage (Eq. 5 left side)         */
+  int64_t* cfg_objective;                     /* IN: caller array [n_cfg] or NULL; OUT: per-config
+                                                 optimum (INT64_MAX = infeasible)                 */
+  int64_t quantum_ns;                         /* time quantum used (level 2), 0 for level 1       */
+  uint64_t dp_cells;                          /* chain-DP cells (instance, layer, strategy, bucket) */
+  uint64_t dp_relax;                          /* min-plus relaxations of the chain DP              */
+  double ms_gpu_dp;                           /* device time of the chain-DP kernels (ms)          */
+  double ms_gpu_total;                        /* device time of the whole path (ms)                */
+  uint64_t h2d_bytes, d2h_bytes;              /* host<->device bytes since the last prepare        */
+  uint32_t n_launches;                        /* kernels this library launched since the last prepare */
+  uint32_t n_k2_launches;                     /* of which chain-DP (K2) launches                    */
+} uniap_result;
+
+/* ---- level 1: integer tables (the parity-test entry) -- */
+typedef struct {
+  int32_t deg, c, n_strat;   /* 1 <= deg, 1 <= c, 1 <= n_strat <= 32                         */
+  const int32_t* A;          /* [L][n_strat]  A_uk, execution cost, 0..2^22   */
+  const int32_t* M;          /* [L][n_strat]  M_uk in buckets, >= 0; > cap => forbidden       */
+  const int32_t* R;          /* [L-1][n_strat][n_strat]  R[u][k][l]: edge u->u+1 with layer u
+                                on k and u+1 on l, 0..2^22 (the quadratic term of Eq. 3)      */
+  const int32_t* Rskip;      /* [L][n_strat][n_strat] or NULL: Rskip[v][k_s][k_v] for the skip
+                                edge skip_src->v, v >= skip_src+2 (other rows ignored)        */
+  const int32_t* O;          /* [L-1] or NULL (= 0): cost of a cut after layer e (Eq. 4 with a
+                                constant R', reading A-1)                                     */
+} uniap_config;
+
+typedef struct {
+  int32_t L;                 /* 1..64 layers in topological order                              */
+  int32_t cap;               /* memory capacity in buckets: Q = cap+1 DP columns, Q <= 8192    */
+  int32_t skip_src;          /* -1, or the one layer whose edges skip ahead (T5 cross-attn)    */
+  int32_t n_cfg;             /* 1..4096 candidate configs, any order; ties broken by the (deg,c)
+                                VALUES; a duplicate (deg,c) is UNIAP_ERR_ARG                   */
+  const uniap_config* cfg;
+} uniap_tables;
+
+/* Solve level-1 tables: UNIAP_OK, UNIAP_ERR_INFEASIBLE (objective INT64_MAX,
+ * cfg_objective filled), UNIAP_ERR_ARG / _RANGE on bad tables, _CUDA. */
+uniap_status uniap_solve_tables(uniap_handle* h, const uniap_tables* t, uniap_result* out);
+
+/* Interval table of one config, for parity tests: P_out[a*L+b] = the stage
+ * optimum of [a,b] (Eq. 3 under Eq. 5), UNIAP_INF if infeasible, for EVERY
+ * a <= b (the solver itself only evaluates the intervals a deg-stage
+ * placement can use).  P_out has L*L int32; entries a > b are UNIAP_INF. */
+uniap_status uniap_interval_table(uniap_handle* h, const uniap_tables* t, int32_t cfg, int32_t* P_out);
+
+/* ---- level 2: profiles (the paper's problem statement) -- */
+typedef struct {
+  const int64_t* fwd_ns_per_sample;   /* [1+log2(maxTP)] forward ns per sample, TP size 1,2,4,..
+                                         (maxTP = largest power of two dividing n_dev)          */
+  int64_t param_bytes;                /* ps, bytes at the training dtype          */
+  const int64_t* act_bytes_per_sample;/* [1+log2(maxTP)] activation bytes per sample by TP size  */
+  int64_t ctx_bytes;                  /* m_c                                                   */
+  int64_t tp_comm_bytes_per_sample;   /* TP collective bytes per sample per forward pass        */
+} uniap_layer;                        /* SPEC.md:22-27; each value in [0, 2^46], fwd <= 2^40  */
+
+typedef struct {
+  int32_t src, dst;                   /* src < dst; dst == src+1 (chain) or a skip edge from
+                                         the single skip source to dst >= src+2               */
+  int64_t tensor_bytes_per_sample;    /* activation bytes crossing the edge per sample         */
+} uniap_edge;
+
+typedef struct {
+  int32_t n_dev, node_size;           /* devices n, devices per node                           */
+  int64_t mem_bytes, mem_reserve_bytes;  /* m and the reserve kept off it (reading A-8)       */
+  int64_t bw_intra_Bps, bw_inter_Bps, p2p_Bps;  /* collective / P2P bandwidths, >= 1         */
+  int64_t lat_ns;                     /* per-hop latency                                       */
+  int32_t ccoc_permille;              /* CCOC in 0..1000                          */
+} uniap_cluster;                      /* SPEC.md:115-120 as an alpha-beta record               */
+
+typedef struct {
+  int32_t L;
+  const uniap_layer* layers;
+  int32_t n_edges;
+  const uniap_edge* edges;
+} uniap_model;                        /* the computation graph G(V,E)           */
+
+typedef struct {
+  int32_t B;                          /* mini-batch size, 1..65536                             */
+  int32_t precision;                  /* 0 = FP32 (c_dtype 4), 1 = FP16 mixed (c_dtype 8) */
+  int32_t Q;                          /* memory buckets, 2..8192 (cap = Q-1)                   */
+  int64_t quantum_ns;                 /* 0 = auto (smallest feasible power of two, A-9)        */
+  const int32_t* cand;                /* NULL = Algorithm 1's list; else n_cand (deg,c) pairs   */
+  int32_t n_cand;
+} uniap_options;
+
+/* Algorithm 1 end to end: cost model on the GPU (K1), then the solve. */
+uniap_status uniap_plan(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
+                        const uniap_options* o, uniap_result* out);
+
+/* The builder's tables (for builder parity tests), per candidate config in
+ * order, as int32 blocks
+ *    [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1]]
+ * Call with buf == NULL to get *words; then with buf_len >= *words. */
+uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
+                                const uniap_options* o, int32_t* buf, int64_t buf_len, int64_t* words,
+                                int32_t* n_cfg, int32_t* skip_src, int64_t* quantum_ns);
+
+/* ---- split pipeline (device-resident timing, multi-GPU) --------------- */
+/* prepare: validate + upload the profile (host->device) and plan the launch.
+ * run:     everything on the device for this rank's share of the candidates
+ *          (LPT over configs, uniap_shard_assign); writes this rank's best
+ *          record into rec_dev (device pointer to one uniap_record; the NCCL
+ *          send buffer of the exchange) or, if NULL, into the handle.
+ * fetch:   device->host of the last run's record (the handle's, or rec_dev,
+ *          which must still be allocated) into *out, plus cfg_objective and
+ *          the counters (bytes copied, kernels launched, device times).      */
+uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
+                           const uniap_options* o);
+uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables* t);
+uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev);
+uniap_status uniap_fetch(uniap_handle* h, uniap_result* out);
+
+typedef struct {                      /* fixed-size record exchanged between ranks            */
+  int64_t objective;                  /* INT64_MAX if this rank holds no feasible config       */
+  int32_t cfg_index, deg, c, L, status, n_cfg_local;
+  int32_t stage_of[UNIAP_MAX_LAYERS], strategy_of[UNIAP_MAX_LAYERS];
+  int64_t stage_cost[UNIAP_MAX_LAYERS], cut_cost[UNIAP_MAX_LAYERS];
+  int32_t stage_mem[UNIAP_MAX_LAYERS];
+  uint64_t dp_cells, dp_relax;
+} uniap_record;
+
+/* Deterministic LPT assignment of the n_cfg candidates of the prepared
+ * problem to `world` ranks: owner_out[i] = rank of candidate i.  Host only. */
+uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32_t* owner_out);
+
+/* Pick the winner among `world` host records by (objective, deg, c); fills
+ * *out (cfg_objective untouched).  Host only (no device needed). */
+uniap_status uniap_pick(const uniap_record* recs, int32_t world, uniap_result* out);
+
+/* Candidate list of Algorithm 1 and the strategy catalogue (host only). */
+int32_t uniap_candidates(int32_t n, int32_t B, int32_t* pairs_out, int32_t cap);
+int32_t uniap_catalogue(int32_t g, int32_t* tfd_out, int32_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UNIAP_H */

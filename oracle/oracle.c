@@ -577,8 +577,8 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
   if (cl->n_dev < 1 || cl->node_size < 1 || cl->bw_intra < 1 || cl->bw_inter < 1 || cl->p2p_bw < 1 ||
       cl->lat_ns < 0 || cl->ccoc_permille < 0 || cl->ccoc_permille > 1000)
     return ORC_ERR_ARG;
-  if (o->B < 1 || o->B > 65536 || o->Q < 2 || o->Q > 16384 || (o->precision != 0 && o->precision != 1) ||
-      o->quantum_ns < 0)
+  if (o->B < 1 || o->B > 65536 || o->Q < 2 || o->Q > 8192 || (o->precision != 0 && o->precision != 1) ||
+      o->quantum_ns < 0 || o->quantum_ns > ((int64_t)1 << 61))
     return ORC_ERR_ARG;
   int L = m->L, n = cl->n_dev, cap = o->Q - 1;
   if (cl->mem_bytes <= cl->mem_reserve || cl->mem_reserve < 0) return ORC_ERR_ARG;

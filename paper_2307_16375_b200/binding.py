@@ -1,0 +1,340 @@
+"""Thin ctypes binding of libuniap.so (include/uniap.h) -- marshalling only.
+
+Every step of the method runs inside the library's CUDA kernels; this module
+only converts the plain dicts of ``gen`` (tables / profiles) into the C
+structs of the ABI and the results back into dicts.  It raises if the
+library is missing (no CPU fallback exists).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libuniap.so")
+INT64_MAX = (1 << 63) - 1
+MAX_L = 64
+
+UNIAP_OK, UNIAP_ERR_ARG, UNIAP_ERR_INFEASIBLE, UNIAP_ERR_RANGE = 0, 1, 2, 3
+UNIAP_ERR_CUDA, UNIAP_ERR_COMM, UNIAP_ERR_OOM, UNIAP_ERR_INTERNAL = 4, 5, 6, 99
+UNIAP_INF = 0x40000000
+
+_P32 = C.POINTER(C.c_int32)
+_P64 = C.POINTER(C.c_int64)
+
+
+class uniap_config(C.Structure):
+    _fields_ = [("deg", C.c_int32), ("c", C.c_int32), ("n_strat", C.c_int32), ("A", _P32), ("M", _P32),
+                ("R", _P32), ("Rskip", _P32), ("O", _P32)]
+
+
+class uniap_tables(C.Structure):
+    _fields_ = [("L", C.c_int32), ("cap", C.c_int32), ("skip_src", C.c_int32), ("n_cfg", C.c_int32),
+                ("cfg", C.POINTER(uniap_config))]
+
+
+class uniap_result(C.Structure):
+    _fields_ = [("objective", C.c_int64), ("cfg_index", C.c_int32), ("deg", C.c_int32), ("c", C.c_int32),
+                ("L", C.c_int32), ("stage_of", C.c_int32 * MAX_L), ("strategy_of", C.c_int32 * MAX_L),
+                ("stage_cost", C.c_int64 * MAX_L), ("cut_cost", C.c_int64 * MAX_L),
+                ("stage_mem", C.c_int32 * MAX_L), ("cfg_objective", _P64), ("quantum_ns", C.c_int64),
+                ("dp_cells", C.c_uint64), ("dp_relax", C.c_uint64), ("ms_gpu_dp", C.c_double),
+                ("ms_gpu_total", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("n_launches", C.c_uint32), ("n_k2_launches", C.c_uint32)]
+
+
+class uniap_layer(C.Structure):
+    _fields_ = [("fwd_ns_per_sample", _P64), ("param_bytes", C.c_int64), ("act_bytes_per_sample", _P64),
+                ("ctx_bytes", C.c_int64), ("tp_comm_bytes_per_sample", C.c_int64)]
+
+
+class uniap_edge(C.Structure):
+    _fields_ = [("src", C.c_int32), ("dst", C.c_int32), ("tensor_bytes_per_sample", C.c_int64)]
+
+
+class uniap_cluster(C.Structure):
+    _fields_ = [("n_dev", C.c_int32), ("node_size", C.c_int32), ("mem_bytes", C.c_int64),
+                ("mem_reserve_bytes", C.c_int64), ("bw_intra_Bps", C.c_int64), ("bw_inter_Bps", C.c_int64),
+                ("p2p_Bps", C.c_int64), ("lat_ns", C.c_int64), ("ccoc_permille", C.c_int32)]
+
+
+class uniap_model(C.Structure):
+    _fields_ = [("L", C.c_int32), ("layers", C.POINTER(uniap_layer)), ("n_edges", C.c_int32),
+                ("edges", C.POINTER(uniap_edge))]
+
+
+class uniap_options(C.Structure):
+    _fields_ = [("B", C.c_int32), ("precision", C.c_int32), ("Q", C.c_int32), ("quantum_ns", C.c_int64),
+                ("cand", _P32), ("n_cand", C.c_int32)]
+
+
+class uniap_record(C.Structure):
+    _fields_ = [("objective", C.c_int64), ("cfg_index", C.c_int32), ("deg", C.c_int32), ("c", C.c_int32),
+                ("L", C.c_int32), ("status", C.c_int32), ("n_cfg_local", C.c_int32),
+                ("stage_of", C.c_int32 * MAX_L), ("strategy_of", C.c_int32 * MAX_L),
+                ("stage_cost", C.c_int64 * MAX_L), ("cut_cost", C.c_int64 * MAX_L),
+                ("stage_mem", C.c_int32 * MAX_L), ("dp_cells", C.c_uint64), ("dp_relax", C.c_uint64)]
+
+
+RECORD_BYTES = C.sizeof(uniap_record)
+
+EXPORTS = ("uniap_create", "uniap_destroy", "uniap_last_error", "uniap_status_string", "uniap_version",
+           "uniap_solve_tables", "uniap_interval_table", "uniap_plan", "uniap_build_tables", "uniap_prepare",
+           "uniap_prepare_tables", "uniap_run", "uniap_fetch", "uniap_shard_assign", "uniap_pick",
+           "uniap_candidates", "uniap_catalogue")
+
+_lib = None
+
+
+def lib():
+    """Load libuniap.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python build.py` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        H = C.c_void_p
+        L.uniap_create.argtypes = [C.POINTER(H), C.c_int, C.c_void_p]
+        L.uniap_destroy.argtypes = [H]
+        L.uniap_destroy.restype = None
+        L.uniap_last_error.argtypes = [H]
+        L.uniap_last_error.restype = C.c_char_p
+        L.uniap_status_string.argtypes = [C.c_int]
+        L.uniap_status_string.restype = C.c_char_p
+        L.uniap_version.restype = C.c_char_p
+        L.uniap_solve_tables.argtypes = [H, C.POINTER(uniap_tables), C.POINTER(uniap_result)]
+        L.uniap_interval_table.argtypes = [H, C.POINTER(uniap_tables), C.c_int32, _P32]
+        L.uniap_plan.argtypes = [H, C.POINTER(uniap_model), C.POINTER(uniap_cluster), C.POINTER(uniap_options),
+                                 C.POINTER(uniap_result)]
+        L.uniap_build_tables.argtypes = [H, C.POINTER(uniap_model), C.POINTER(uniap_cluster),
+                                         C.POINTER(uniap_options), _P32, C.c_int64, _P64, _P32, _P32, _P64]
+        L.uniap_prepare.argtypes = [H, C.POINTER(uniap_model), C.POINTER(uniap_cluster), C.POINTER(uniap_options)]
+        L.uniap_prepare_tables.argtypes = [H, C.POINTER(uniap_tables)]
+        L.uniap_run.argtypes = [H, C.c_int32, C.c_int32, C.c_void_p]
+        L.uniap_fetch.argtypes = [H, C.POINTER(uniap_result)]
+        L.uniap_shard_assign.argtypes = [H, C.c_int32, _P32]
+        L.uniap_pick.argtypes = [C.POINTER(uniap_record), C.c_int32, C.POINTER(uniap_result)]
+        L.uniap_candidates.argtypes = [C.c_int32, C.c_int32, _P32, C.c_int32]
+        L.uniap_catalogue.argtypes = [C.c_int32, _P32, C.c_int32]
+        for f in EXPORTS:
+            if f not in ("uniap_destroy", "uniap_last_error", "uniap_status_string", "uniap_version"):
+                getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+class UniapError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"uniap status {status}: {msg}")
+        self.status = status
+
+
+def _i32(a):
+    return np.ascontiguousarray(np.asarray(a), dtype=np.int32)
+
+
+def _p32(a):
+    return None if a is None else a.ctypes.data_as(_P32)
+
+
+def _tables(t):
+    keep = []
+    L = t["L"]
+    cfgs = (uniap_config * len(t["cfgs"]))()
+    for i, c in enumerate(t["cfgs"]):
+        S = c["n_strat"]
+        A = _i32(c["A"]).reshape(L, S)
+        M = _i32(c["M"]).reshape(L, S)
+        R = _i32(c["R"]).reshape(L - 1, S, S) if L > 1 else np.zeros((1, S, S), np.int32)
+        Rs = _i32(c["Rskip"]).reshape(L, S, S) if c.get("Rskip") is not None else None
+        O = _i32(c["O"]).reshape(L - 1) if c.get("O") is not None and L > 1 else None
+        keep += [A, M, R, Rs, O]
+        cfgs[i] = uniap_config(c["deg"], c["c"], S, _p32(A), _p32(M), _p32(R), _p32(Rs), _p32(O))
+    keep.append(cfgs)
+    return uniap_tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs), keep
+
+
+def _profile(p):
+    keep = []
+    m = p["model"]
+    L = m["L"]
+    layers = (uniap_layer * L)()
+    for u, ly in enumerate(m["layers"]):
+        f = np.ascontiguousarray(ly["fwd_ns_per_sample"], dtype=np.int64)
+        a = np.ascontiguousarray(ly["act_bytes_per_sample"], dtype=np.int64)
+        keep += [f, a]
+        layers[u] = uniap_layer(f.ctypes.data_as(_P64), ly["param_bytes"], a.ctypes.data_as(_P64),
+                                ly["ctx_bytes"], ly["tp_comm_bytes_per_sample"])
+    E = len(m["edges"])
+    edges = (uniap_edge * max(E, 1))()
+    for i, e in enumerate(m["edges"]):
+        edges[i] = uniap_edge(e["src"], e["dst"], e["tensor_bytes_per_sample"])
+    cl = p["cluster"]
+    cluster = uniap_cluster(cl["n_dev"], cl["node_size"], cl["mem_bytes"], cl["mem_reserve_bytes"],
+                            cl["bw_intra_Bps"], cl["bw_inter_Bps"], cl["p2p_Bps"], cl["lat_ns"],
+                            cl["ccoc_permille"])
+    o = p["options"]
+    cand = None
+    if o.get("cand"):
+        cand = np.ascontiguousarray(np.array(o["cand"], dtype=np.int32).reshape(-1))
+    opts = uniap_options(o["B"], o["precision"], o["Q"], o.get("quantum_ns", 0), _p32(cand),
+                         0 if cand is None else len(cand) // 2)
+    keep += [layers, edges, cand]
+    return uniap_model(L, layers, E, edges), cluster, opts, keep
+
+
+def _result_dict(r, n_cfg, cfg_obj):
+    deg = r.deg
+    L = r.L
+    out = {"objective": r.objective, "cfg_index": r.cfg_index, "deg": deg, "c": r.c,
+           "quantum_ns": r.quantum_ns, "dp_cells": r.dp_cells, "dp_relax": r.dp_relax,
+           "ms_gpu_dp": r.ms_gpu_dp, "ms_gpu_total": r.ms_gpu_total, "h2d_bytes": r.h2d_bytes,
+           "d2h_bytes": r.d2h_bytes, "n_launches": r.n_launches, "n_k2_launches": r.n_k2_launches}
+    if cfg_obj is not None:
+        out["cfg_objective"] = [int(x) for x in cfg_obj[:n_cfg]]
+    if r.objective != INT64_MAX:
+        out.update({"stage_of": list(r.stage_of[:L]), "strategy_of": list(r.strategy_of[:L]),
+                    "stage_cost": list(r.stage_cost[:deg]), "cut_cost": list(r.cut_cost[:max(deg - 1, 0)]),
+                    "stage_mem": list(r.stage_mem[:deg])})
+    return out
+
+
+def candidates(n, B):
+    k = lib().uniap_candidates(n, B, None, 0)
+    buf = (C.c_int32 * (2 * k))()
+    lib().uniap_candidates(n, B, buf, k)
+    return [(buf[2 * i], buf[2 * i + 1]) for i in range(k)]
+
+
+def catalogue(g):
+    k = lib().uniap_catalogue(g, None, 0)
+    buf = (C.c_int32 * (3 * max(k, 1)))()
+    lib().uniap_catalogue(g, buf, k)
+    return [tuple(buf[3 * i:3 * i + 3]) for i in range(k)]
+
+
+def pick(records: bytes, world: int):
+    """uniap_pick over `world` host records (bytes of world * RECORD_BYTES)."""
+    arr = (uniap_record * world).from_buffer_copy(records)
+    r = uniap_result()
+    st = lib().uniap_pick(arr, world, C.byref(r))
+    if st not in (UNIAP_OK, UNIAP_ERR_INFEASIBLE):
+        raise UniapError(st, "pick")
+    r.L = arr[0].L
+    return st, _result_dict(r, 0, None)
+
+
+class Handle:
+    """A libuniap handle on one CUDA device (owns its device buffers)."""
+
+    def __init__(self, device=0, stream=None):
+        self._h = C.c_void_p()
+        st = lib().uniap_create(C.byref(self._h), device, C.c_void_p(stream) if stream else None)
+        if st != UNIAP_OK:
+            raise UniapError(st, f"uniap_create(device={device}) failed: needs a compute-capability 10.x GPU")
+        self.n_cfg = 0
+
+    def close(self):
+        if self._h:
+            lib().uniap_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st, what, ok=(UNIAP_OK,)):
+        if st not in ok:
+            raise UniapError(st, f"{what}: {lib().uniap_last_error(self._h).decode()}")
+        return st
+
+    def solve_tables(self, t):
+        tb, keep = _tables(t)
+        n = len(t["cfgs"])
+        cfg_obj = (C.c_int64 * n)()
+        r = uniap_result()
+        r.cfg_objective = cfg_obj
+        st = self._check(lib().uniap_solve_tables(self._h, C.byref(tb), C.byref(r)), "solve_tables",
+                         (UNIAP_OK, UNIAP_ERR_INFEASIBLE))
+        out = _result_dict(r, n, cfg_obj)
+        out["status"] = st
+        return out
+
+    def interval_table(self, t, cfg):
+        tb, keep = _tables(t)
+        L = t["L"]
+        P = np.zeros(L * L, dtype=np.int32)
+        self._check(lib().uniap_interval_table(self._h, C.byref(tb), cfg, P.ctypes.data_as(_P32)), "interval_table")
+        return P.reshape(L, L)
+
+    def plan(self, p):
+        model, cluster, opts, keep = _profile(p)
+        n = len(candidates(p["cluster"]["n_dev"], p["options"]["B"])) if not p["options"].get("cand") \
+            else len(p["options"]["cand"])
+        cfg_obj = (C.c_int64 * n)()
+        r = uniap_result()
+        r.cfg_objective = cfg_obj
+        st = self._check(lib().uniap_plan(self._h, C.byref(model), C.byref(cluster), C.byref(opts), C.byref(r)),
+                         "plan", (UNIAP_OK, UNIAP_ERR_INFEASIBLE))
+        out = _result_dict(r, n, cfg_obj)
+        out["status"] = st
+        return out
+
+    def build_tables(self, p):
+        """The K1 builder's tables in the documented block layout -> (tables dict, quantum, flat buffer)."""
+        model, cluster, opts, keep = _profile(p)
+        words, ncfg, skip, qn = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int64()
+        self._check(lib().uniap_build_tables(self._h, C.byref(model), C.byref(cluster), C.byref(opts), None, 0,
+                                             C.byref(words), C.byref(ncfg), C.byref(skip), C.byref(qn)), "build(size)")
+        buf = np.zeros(words.value, dtype=np.int32)
+        self._check(lib().uniap_build_tables(self._h, C.byref(model), C.byref(cluster), C.byref(opts),
+                                             buf.ctypes.data_as(_P32), words.value, C.byref(words),
+                                             C.byref(ncfg), C.byref(skip), C.byref(qn)), "build")
+        L, cap = p["model"]["L"], p["options"]["Q"] - 1
+        cfgs, off = [], 0
+        for _ in range(ncfg.value):
+            deg, c, S, g = (int(x) for x in buf[off:off + 4])
+            off += 4
+            blk = {}
+            for name, shape in (("A", (L, S)), ("M", (L, S)), ("R", (L - 1, S, S)), ("Rskip", (L, S, S)),
+                                ("O", (L - 1,))):
+                size = int(np.prod(shape))
+                blk[name] = buf[off:off + size].reshape(shape)
+                off += size
+            cfgs.append({"deg": deg, "c": c, "n_strat": S, "g": g, **blk,
+                         "Rskip": blk["Rskip"] if skip.value >= 0 else None})
+        return {"L": L, "cap": cap, "skip_src": skip.value, "cfgs": cfgs}, qn.value, buf
+
+    # ---- split pipeline ----
+    def prepare(self, p):
+        self._keep = _profile(p)
+        model, cluster, opts, _ = self._keep
+        self._check(lib().uniap_prepare(self._h, C.byref(model), C.byref(cluster), C.byref(opts)), "prepare")
+        self.n_cfg = len(candidates(p["cluster"]["n_dev"], p["options"]["B"])) if not p["options"].get("cand") \
+            else len(p["options"]["cand"])
+
+    def prepare_tables(self, t):
+        tb, keep = _tables(t)
+        self._check(lib().uniap_prepare_tables(self._h, C.byref(tb)), "prepare_tables")
+        self.n_cfg = len(t["cfgs"])
+
+    def run(self, rank=0, world=1, rec_dev_ptr=None):
+        self._check(lib().uniap_run(self._h, rank, world, C.c_void_p(rec_dev_ptr) if rec_dev_ptr else None), "run")
+
+    def fetch(self):
+        cfg_obj = (C.c_int64 * max(self.n_cfg, 1))()
+        r = uniap_result()
+        r.cfg_objective = cfg_obj
+        st = self._check(lib().uniap_fetch(self._h, C.byref(r)), "fetch", (UNIAP_OK, UNIAP_ERR_INFEASIBLE))
+        out = _result_dict(r, self.n_cfg, cfg_obj)
+        out["status"] = st
+        return out
+
+    def shard_assign(self, world):
+        owner = (C.c_int32 * max(self.n_cfg, 1))()
+        self._check(lib().uniap_shard_assign(self._h, world, owner), "shard_assign")
+        return list(owner[:self.n_cfg])

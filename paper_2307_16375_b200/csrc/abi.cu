@@ -1,0 +1,808 @@
+// abi.cu -- the C ABI of libuniap.so (include/uniap.h): validation, the
+// candidate enumerator (K0, Algorithm 1), the strategy catalogue, device
+// layout, launch plan (instances, LPT sharding) and the pipeline
+//   K1 builder -> K2 chain DP -> K3 thetas -> K4 combine -> K5a argmin/ends
+//   -> K2 backward sweeps -> K5c strategy walk -> record.
+// Host code does shapes, bookkeeping and launches only; every step of the
+// method's arithmetic runs in the kernels.
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "uniap_impl.h"
+
+using namespace uniap;
+
+namespace {
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc((void**)&p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) n = std::max<size_t>(count, 1);
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+int round4(int x) { return (x + 3) & ~3; }
+
+}  // namespace
+
+struct uniap_handle {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  std::string err;
+  // prepared problem
+  bool ready = false, level2 = false;
+  int L = 0, cap = 0, Q = 0, skip = -1, ncfg = 0;
+  std::vector<CfgDev> cfg;
+  std::vector<K2Class> cls;
+  std::vector<CatDev> cat;
+  int64_t arena_words = 0;
+  ClusterDev cl{};
+  int n_edges = 0;
+  // device buffers
+  DevBuf<int32_t> arena, P, thetas, ntheta, cfglist, scratch, G;
+  DevBuf<int64_t> ns, vals, cfgopt, qcfg, qglob, gofs;
+  DevBuf<int64_t> fwd, act, ps, ctx, tpc, chain, skipb, edges;
+  DevBuf<CfgDev> dcfg;
+  DevBuf<CatDev> dcat;
+  DevBuf<Inst> inst, binst;
+  DevBuf<Winner> win;
+  DevBuf<uniap_record> rec;
+  // last run
+  uniap_record rec_host{};
+  uint64_t cells = 0, relax = 0;
+  float ms_dp = 0.f, ms_total = 0.f;
+  int64_t quantum = 0;
+  cudaEvent_t ev[4] = {};
+  uint64_t h2d = 0, d2h = 0;
+  uint32_t launches = 0, k2_launches = 0;
+  const uniap_record* last_rec = nullptr;  // where the last run wrote its record
+};
+
+// every host<->device copy goes through these (counted for the e2e report)
+static cudaError_t h2d(uniap_handle* h, void* dst, const void* src, size_t bytes) {
+  h->h2d += bytes;
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->st);
+}
+static cudaError_t d2h(uniap_handle* h, void* dst, const void* src, size_t bytes) {
+  h->d2h += bytes;
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->st);
+}
+
+#define FAIL(h, code, ...)                                   \
+  do {                                                       \
+    char _b[512];                                            \
+    snprintf(_b, sizeof _b, __VA_ARGS__);                    \
+    (h)->err = _b;                                           \
+    return (code);                                           \
+  } while (0)
+
+#define CK(h, x)                                                                                       \
+  do {                                                                                                 \
+    cudaError_t _e = (x);                                                                              \
+    if (_e != cudaSuccess) {                                                                           \
+      (h)->err = std::string("CUDA: ") + cudaGetErrorString(_e) + " at " #x;                           \
+      return _e == cudaErrorMemoryAllocation ? UNIAP_ERR_OOM : UNIAP_ERR_CUDA;                         \
+    }                                                                                                  \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// K0 / a-2: candidate enumeration and the strategy catalogue (host).
+// ---------------------------------------------------------------------------
+extern "C" int32_t uniap_candidates(int32_t n, int32_t B, int32_t* pairs, int32_t cap) {
+  // Algorithm 1: the QIP (deg = 1, modelled at batch B,
+  // reported c = 1, reading A-4), then deg in factors(n)\{1} x c in
+  // factors(B)\{1}, deg ascending then c ascending.
+  int32_t k = 0;
+  auto put = [&](int32_t d, int32_t c) {
+    if (k < cap && pairs) { pairs[2 * k] = d; pairs[2 * k + 1] = c; }
+    ++k;
+  };
+  if (n < 1 || B < 1) return 0;
+  put(1, 1);
+  for (int32_t d = 2; d <= n; ++d)
+    if (n % d == 0)
+      for (int32_t c = 2; c <= B; ++c)
+        if (B % c == 0) put(d, c);
+  return k;
+}
+
+extern "C" int32_t uniap_catalogue(int32_t g, int32_t* tfd, int32_t cap) {
+  // SD[deg] (reading A-6): (t,f,d) with t*f*d = g, t a
+  // power of two; t ascending then f ascending (index 0 = pure DP).
+  int32_t k = 0;
+  if (g < 1) return 0;
+  for (int32_t t = 1; t <= g && g % t == 0; t *= 2)
+    for (int32_t f = 1; f <= g / t; ++f)
+      if ((g / t) % f == 0) {
+        if (k < cap && tfd) { tfd[3 * k] = t; tfd[3 * k + 1] = f; tfd[3 * k + 2] = g / t / f; }
+        ++k;
+      }
+  return k;
+}
+
+extern "C" const char* uniap_version(void) { return "uniap-b200 0.1 (sm_100a)"; }
+
+extern "C" const char* uniap_status_string(uniap_status s) {
+  switch (s) {
+    case UNIAP_OK: return "ok";
+    case UNIAP_ERR_ARG: return "invalid argument";
+    case UNIAP_ERR_INFEASIBLE: return "infeasible";
+    case UNIAP_ERR_RANGE: return "value out of range";
+    case UNIAP_ERR_CUDA: return "CUDA error";
+    case UNIAP_ERR_COMM: return "communication error";
+    case UNIAP_ERR_OOM: return "out of device memory";
+    case UNIAP_ERR_INTERNAL: return "internal self-check failed";
+  }
+  return "unknown";
+}
+
+extern "C" const char* uniap_last_error(const uniap_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+extern "C" uniap_status uniap_create(uniap_handle** out, int device, void* stream) {
+  if (!out) return UNIAP_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return UNIAP_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return UNIAP_ERR_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return UNIAP_ERR_CUDA;
+  uniap_handle* h = new uniap_handle();
+  h->device = device;
+  if (stream) {
+    h->st = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) { delete h; return UNIAP_ERR_CUDA; }
+    h->own_stream = true;
+  }
+  for (auto& e : h->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) { delete h; return UNIAP_ERR_CUDA; }
+  *out = h;
+  return UNIAP_OK;
+}
+
+extern "C" void uniap_destroy(uniap_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->st);
+  for (auto* b : {&h->arena, &h->P, &h->thetas, &h->ntheta, &h->cfglist, &h->scratch, &h->G}) b->release();
+  for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->qglob, &h->gofs, &h->fwd, &h->act, &h->ps, &h->ctx,
+                  &h->tpc, &h->chain, &h->skipb, &h->edges})
+    b->release();
+  h->dcfg.release();
+  h->dcat.release();
+  h->inst.release();
+  h->binst.release();
+  h->win.release();
+  h->rec.release();
+  for (auto e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->own_stream) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+// ---------------------------------------------------------------------------
+// Layout of the configs in the device arena.
+// ---------------------------------------------------------------------------
+static uniap_status layout_configs(uniap_handle* h, const std::vector<int>& S, const std::vector<int>& deg,
+                                   const std::vector<int>& c, const std::vector<int>& g, const std::vector<int>& skipc) {
+  const int L = h->L;
+  h->cfg.assign(h->ncfg, CfgDev{});
+  h->cls.assign(h->ncfg, K2Class{});
+  int64_t off = 0;
+  for (int i = 0; i < h->ncfg; ++i) {
+    K2Class k;
+    if (!k2_pick_class(S[i], h->Q, &k)) FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
+    h->cls[i] = k;
+    CfgDev& d = h->cfg[i];
+    const int NSP = round4(k.NS);
+    d.deg = deg[i]; d.c = c[i]; d.S = S[i]; d.NSP = NSP; d.g = g[i]; d.skip = skipc[i];
+    d.offA = off; off += (int64_t)L * NSP;
+    d.offM = off; off += (int64_t)L * NSP;
+    d.offRt = off; off += (int64_t)(L - 1) * NSP * NSP;
+    d.offRf = off; off += (int64_t)(L - 1) * NSP * NSP;
+    d.offRs = off; off += (int64_t)L * NSP * NSP;
+    d.offO = off; off += std::max(4, round4(L - 1));
+    d.offP = (int64_t)i * L * L;
+  }
+  h->arena_words = off;
+  return UNIAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Level-1 tables: validation and upload.
+// ---------------------------------------------------------------------------
+static void reset_counters(uniap_handle* h) { h->h2d = h->d2h = 0; h->launches = h->k2_launches = 0; }
+
+extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables* t) {
+  if (!h) return UNIAP_ERR_ARG;
+  h->ready = false;
+  reset_counters(h);
+  if (!t || !t->cfg) FAIL(h, UNIAP_ERR_ARG, "null tables");
+  const int L = t->L;
+  if (L < 1 || L > UNIAP_MAX_LAYERS) FAIL(h, UNIAP_ERR_ARG, "L=%d out of 1..64", L);
+  if (t->cap < 0 || t->cap + 1 > UNIAP_MAX_Q) FAIL(h, UNIAP_ERR_ARG, "cap=%d out of 0..%d", t->cap, UNIAP_MAX_Q - 1);
+  if (t->skip_src < -1 || t->skip_src >= L) FAIL(h, UNIAP_ERR_ARG, "skip_src=%d", t->skip_src);
+  if (t->n_cfg < 1 || t->n_cfg > UNIAP_MAX_CFG) FAIL(h, UNIAP_ERR_ARG, "n_cfg=%d", t->n_cfg);
+  h->L = L; h->cap = t->cap; h->Q = t->cap + 1; h->skip = t->skip_src; h->ncfg = t->n_cfg; h->level2 = false;
+  std::vector<int> S(h->ncfg), deg(h->ncfg), c(h->ncfg), g(h->ncfg, 0), skc(h->ncfg);
+  for (int i = 0; i < h->ncfg; ++i) {
+    const uniap_config& x = t->cfg[i];
+    if (x.deg < 1 || x.c < 1 || x.n_strat < 1 || x.n_strat > UNIAP_MAX_STRAT)
+      FAIL(h, UNIAP_ERR_ARG, "config %d: deg=%d c=%d n_strat=%d", i, x.deg, x.c, x.n_strat);
+    if (!x.A || !x.M || (L > 1 && !x.R)) FAIL(h, UNIAP_ERR_ARG, "config %d: null table", i);
+    for (int j = 0; j < i; ++j)
+      if (t->cfg[j].deg == x.deg && t->cfg[j].c == x.c) FAIL(h, UNIAP_ERR_ARG, "duplicate (deg,c)=(%d,%d)", x.deg, x.c);
+    const int s = x.n_strat;
+    int64_t sum = 0, osum = 0;
+    for (int u = 0; u < L; ++u) {
+      int64_t ma = 0, mr = 0, ms = 0;
+      for (int k = 0; k < s; ++k) {
+        const int32_t a = x.A[u * s + k], m = x.M[u * s + k];
+        if (a < 0 || a > UNIAP_MAX_ENTRY || m < 0) FAIL(h, UNIAP_ERR_RANGE, "config %d: A/M out of range at layer %d", i, u);
+        ma = std::max<int64_t>(ma, a);
+      }
+      if (u >= 1)
+        for (int k = 0; k < s * s; ++k) {
+          const int32_t r = x.R[(int64_t)(u - 1) * s * s + k];
+          if (r < 0 || r > UNIAP_MAX_ENTRY) FAIL(h, UNIAP_ERR_RANGE, "config %d: R out of range at edge %d", i, u - 1);
+          mr = std::max<int64_t>(mr, r);
+        }
+      if (x.Rskip && t->skip_src >= 0 && u >= t->skip_src + 2)
+        for (int k = 0; k < s * s; ++k) {
+          const int32_t r = x.Rskip[(int64_t)u * s * s + k];
+          if (r < 0 || r > UNIAP_MAX_ENTRY) FAIL(h, UNIAP_ERR_RANGE, "config %d: Rskip out of range at %d", i, u);
+          ms = std::max<int64_t>(ms, r);
+        }
+      sum += ma + mr + ms;
+    }
+    if (x.O)
+      for (int e = 0; e < L - 1; ++e) {
+        if (x.O[e] < 0 || x.O[e] > UNIAP_MAX_ENTRY) FAIL(h, UNIAP_ERR_RANGE, "config %d: O out of range", i);
+        osum += x.O[e];
+      }
+    if (sum > UNIAP_MAX_SUM || osum > UNIAP_MAX_SUM) FAIL(h, UNIAP_ERR_RANGE, "config %d: sum bound exceeds 2^28", i);
+    S[i] = s; deg[i] = x.deg; c[i] = x.c;
+    skc[i] = (x.Rskip && t->skip_src >= 0) ? t->skip_src : -1;
+  }
+  uniap_status st = layout_configs(h, S, deg, c, g, skc);
+  if (st != UNIAP_OK) return st;
+  // pack the host tables into the device layout (pads: A 0, M cap+1, R 0)
+  std::vector<int32_t> a(h->arena_words, 0);
+  for (int i = 0; i < h->ncfg; ++i) {
+    const uniap_config& x = t->cfg[i];
+    const CfgDev& d = h->cfg[i];
+    const int s = x.n_strat, N = d.NSP;
+    for (int u = 0; u < L; ++u)
+      for (int k = 0; k < N; ++k) {
+        a[d.offA + u * N + k] = k < s ? x.A[u * s + k] : 0;
+        a[d.offM + u * N + k] = k < s ? std::min(x.M[u * s + k], h->cap + 1) : h->cap + 1;
+      }
+    for (int e = 0; e + 1 < L; ++e)
+      for (int k = 0; k < s; ++k)
+        for (int l = 0; l < s; ++l) {
+          const int32_t r = x.R[((int64_t)e * s + k) * s + l];
+          a[d.offRf + ((int64_t)e * N + k) * N + l] = r;
+          a[d.offRt + ((int64_t)e * N + l) * N + k] = r;
+        }
+    if (d.skip >= 0)
+      for (int v = d.skip + 2; v < L; ++v)
+        for (int k = 0; k < s; ++k)
+          for (int l = 0; l < s; ++l) a[d.offRs + ((int64_t)v * N + k) * N + l] = x.Rskip[((int64_t)v * s + k) * s + l];
+    if (x.O)
+      for (int e = 0; e + 1 < L; ++e) a[d.offO + e] = x.O[e];
+  }
+  CK(h, cudaSetDevice(h->device));
+  CK(h, h->arena.ensure(h->arena_words));
+  CK(h, h->dcfg.ensure(h->ncfg));
+  CK(h, h2d(h, h->arena.p, a.data(), a.size() * 4));
+  CK(h, h2d(h, h->dcfg.p, h->cfg.data(), h->ncfg * sizeof(CfgDev)));
+  CK(h, cudaStreamSynchronize(h->st));
+  h->ready = true;
+  return UNIAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Level-2 profiles: validation and upload (the builder K1 runs in run()).
+// ---------------------------------------------------------------------------
+extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
+                                      const uniap_options* o) {
+  if (!h) return UNIAP_ERR_ARG;
+  h->ready = false;
+  reset_counters(h);
+  if (!m || !cl || !o || !m->layers) FAIL(h, UNIAP_ERR_ARG, "null argument");
+  const int L = m->L;
+  if (L < 1 || L > UNIAP_MAX_LAYERS) FAIL(h, UNIAP_ERR_ARG, "L=%d", L);
+  if (cl->n_dev < 1 || cl->node_size < 1 || cl->bw_intra_Bps < 1 || cl->bw_inter_Bps < 1 || cl->p2p_Bps < 1 ||
+      cl->lat_ns < 0 || cl->ccoc_permille < 0 || cl->ccoc_permille > 1000)
+    FAIL(h, UNIAP_ERR_ARG, "bad cluster record");
+  if (o->B < 1 || o->B > 65536 || o->Q < 2 || o->Q > UNIAP_MAX_Q || (o->precision != 0 && o->precision != 1) ||
+      o->quantum_ns < 0 || o->quantum_ns > ((int64_t)1 << 61))
+    FAIL(h, UNIAP_ERR_ARG, "bad options");
+  if (cl->mem_reserve_bytes < 0 || cl->mem_bytes <= cl->mem_reserve_bytes) FAIL(h, UNIAP_ERR_ARG, "memory <= reserve");
+  if ((cl->mem_bytes - cl->mem_reserve_bytes) / (o->Q - 1) < 1) FAIL(h, UNIAP_ERR_ARG, "memory unit < 1 byte");
+  const int n = cl->n_dev;
+  int maxtp = 1;
+  while (n % (maxtp * 2) == 0) maxtp *= 2;
+  int NT = 1;
+  while ((1 << (NT - 1)) < maxtp) ++NT;
+  const int64_t LIM = (int64_t)1 << 46;
+  std::vector<int64_t> fwd(L * NT), act(L * NT), ps(L), ctx(L), tpc(L), chain(L, -1), skipb(L, -1);
+  for (int u = 0; u < L; ++u) {
+    const uniap_layer& y = m->layers[u];
+    if (!y.fwd_ns_per_sample || !y.act_bytes_per_sample) FAIL(h, UNIAP_ERR_ARG, "layer %d: null profile", u);
+    if (y.param_bytes < 0 || y.param_bytes > LIM || y.ctx_bytes < 0 || y.ctx_bytes > LIM ||
+        y.tp_comm_bytes_per_sample < 0 || y.tp_comm_bytes_per_sample > LIM)
+      FAIL(h, UNIAP_ERR_ARG, "layer %d: value out of range", u);
+    for (int i = 0; i < NT; ++i) {
+      if (y.fwd_ns_per_sample[i] < 0 || y.fwd_ns_per_sample[i] > ((int64_t)1 << 40) || y.act_bytes_per_sample[i] < 0 ||
+          y.act_bytes_per_sample[i] > LIM)
+        FAIL(h, UNIAP_ERR_ARG, "layer %d: profile out of range", u);
+      fwd[u * NT + i] = y.fwd_ns_per_sample[i];
+      act[u * NT + i] = y.act_bytes_per_sample[i];
+    }
+    ps[u] = y.param_bytes; ctx[u] = y.ctx_bytes; tpc[u] = y.tp_comm_bytes_per_sample;
+  }
+  int skip = -1;
+  std::vector<int64_t> ed;
+  for (int i = 0; i < m->n_edges; ++i) {
+    const uniap_edge& e = m->edges[i];
+    if (e.src < 0 || e.dst >= L || e.src >= e.dst || e.tensor_bytes_per_sample < 0 || e.tensor_bytes_per_sample > LIM)
+      FAIL(h, UNIAP_ERR_ARG, "edge %d invalid", i);
+    if (e.dst == e.src + 1) {
+      if (chain[e.src] >= 0) FAIL(h, UNIAP_ERR_ARG, "duplicate edge %d->%d", e.src, e.dst);
+      chain[e.src] = e.tensor_bytes_per_sample;
+    } else {
+      if (skip >= 0 && skip != e.src) FAIL(h, UNIAP_ERR_ARG, "more than one skip source (general DAGs: NEXT-4)");
+      skip = e.src;
+      if (skipb[e.dst] >= 0) FAIL(h, UNIAP_ERR_ARG, "duplicate edge %d->%d", e.src, e.dst);
+      skipb[e.dst] = e.tensor_bytes_per_sample;
+    }
+    ed.push_back(e.src); ed.push_back(e.dst); ed.push_back(e.tensor_bytes_per_sample);
+  }
+  // candidate list (Algorithm 1 or explicit)
+  std::vector<int32_t> cand;
+  if (o->cand) {
+    if (o->n_cand < 1 || o->n_cand > UNIAP_MAX_CFG) FAIL(h, UNIAP_ERR_ARG, "n_cand=%d", o->n_cand);
+    for (int i = 0; i < o->n_cand; ++i) {
+      const int d = o->cand[2 * i], c = o->cand[2 * i + 1];
+      if (d < 1 || c < 1 || n % d || o->B % c) FAIL(h, UNIAP_ERR_ARG, "candidate (%d,%d) does not divide (n,B)", d, c);
+      for (int j = 0; j < i; ++j)
+        if (o->cand[2 * j] == d && o->cand[2 * j + 1] == c) FAIL(h, UNIAP_ERR_ARG, "duplicate candidate");
+      cand.push_back(d); cand.push_back(c);
+    }
+  } else {
+    const int k = uniap_candidates(n, o->B, nullptr, 0);
+    if (k > UNIAP_MAX_CFG) FAIL(h, UNIAP_ERR_ARG, "too many candidates");
+    cand.resize(2 * k);
+    uniap_candidates(n, o->B, cand.data(), k);
+  }
+  h->L = L; h->Q = o->Q; h->cap = o->Q - 1; h->skip = skip; h->ncfg = (int)cand.size() / 2; h->level2 = true;
+  std::vector<int> S(h->ncfg), deg(h->ncfg), c(h->ncfg), g(h->ncfg), skc(h->ncfg, skip);
+  h->cat.assign(h->ncfg, CatDev{});
+  for (int i = 0; i < h->ncfg; ++i) {
+    deg[i] = cand[2 * i]; c[i] = cand[2 * i + 1]; g[i] = n / deg[i];
+    S[i] = uniap_catalogue(g[i], nullptr, 0);
+    if (S[i] > UNIAP_MAX_STRAT) FAIL(h, UNIAP_ERR_RANGE, "|S(%d)| = %d > 32", g[i], S[i]);
+    uniap_catalogue(g[i], h->cat[i].tfd, UNIAP_MAX_STRAT);
+  }
+  uniap_status st = layout_configs(h, S, deg, c, g, skc);
+  if (st != UNIAP_OK) return st;
+  h->cl = ClusterDev{cl->n_dev, cl->node_size, cl->ccoc_permille, o->B, o->precision, o->Q, NT,
+                     cl->mem_bytes, cl->mem_reserve_bytes, cl->bw_intra_Bps, cl->bw_inter_Bps, cl->p2p_Bps,
+                     cl->lat_ns, o->quantum_ns};
+  h->n_edges = m->n_edges;
+  CK(h, cudaSetDevice(h->device));
+  CK(h, h->arena.ensure(h->arena_words));
+  CK(h, h->ns.ensure(h->arena_words));
+  CK(h, h->dcfg.ensure(h->ncfg));
+  CK(h, h->dcat.ensure(h->ncfg));
+  CK(h, h->qcfg.ensure(h->ncfg));
+  CK(h, h->qglob.ensure(2));
+  CK(h, h->fwd.ensure(fwd.size()));
+  CK(h, h->act.ensure(act.size()));
+  CK(h, h->ps.ensure(L));
+  CK(h, h->ctx.ensure(L));
+  CK(h, h->tpc.ensure(L));
+  CK(h, h->chain.ensure(L));
+  CK(h, h->skipb.ensure(L));
+  CK(h, h->edges.ensure(std::max<size_t>(ed.size(), 3)));
+  auto up = [&](void* d, const void* s, size_t bytes) { return h2d(h, d, s, bytes); };
+  CK(h, up(h->fwd.p, fwd.data(), fwd.size() * 8));
+  CK(h, up(h->act.p, act.data(), act.size() * 8));
+  CK(h, up(h->ps.p, ps.data(), L * 8));
+  CK(h, up(h->ctx.p, ctx.data(), L * 8));
+  CK(h, up(h->tpc.p, tpc.data(), L * 8));
+  CK(h, up(h->chain.p, chain.data(), L * 8));
+  CK(h, up(h->skipb.p, skipb.data(), L * 8));
+  if (!ed.empty()) CK(h, up(h->edges.p, ed.data(), ed.size() * 8));
+  CK(h, up(h->dcfg.p, h->cfg.data(), h->ncfg * sizeof(CfgDev)));
+  CK(h, up(h->dcat.p, h->cat.data(), h->ncfg * sizeof(CatDev)));
+  CK(h, cudaStreamSynchronize(h->st));
+  h->ready = true;
+  return UNIAP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Launch plan
+// ---------------------------------------------------------------------------
+// Forward instances of config i: every start layer a whose interval [a,b] can
+// be a stage of a deg-stage ordered placement (a >= stages before it, enough
+// layers after it); with the skip source inside the sweep, one copy per
+// strategy ks of the skip source (Eq. 3 couples it with later layers).
+static void forward_instances(const uniap_handle* h, int i, bool all_intervals, std::vector<Inst>& out) {
+  const CfgDev& d = h->cfg[i];
+  const int L = h->L;
+  if (!all_intervals && d.deg > L) return;
+  for (int a = 0; a < L; ++a) {
+    int bmax;
+    if (all_intervals) bmax = L - 1;
+    else if (d.deg == 1) { if (a > 0) break; bmax = L - 1; }
+    else bmax = L - 1 - d.deg + std::min(a + 1, d.deg);
+    if (bmax < a) continue;
+    const int n = bmax - a + 1;
+    if (d.skip >= 0 && a <= d.skip && bmax >= d.skip + 2) {
+      for (int ks = 0; ks < d.S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0});
+    } else {
+      out.push_back(Inst{i, a, n, -1, +1, 1, 0});
+    }
+  }
+}
+
+static double config_work(const uniap_handle* h, int i) {
+  std::vector<Inst> v;
+  forward_instances(h, i, false, v);
+  double w = 0;
+  for (auto& x : v) w += (double)x.n * h->cfg[i].S * h->cfg[i].S * h->Q;
+  return w + 1.0;  // + the combine
+}
+
+static void lpt(const uniap_handle* h, int world, std::vector<int>& owner) {
+  std::vector<int> order(h->ncfg);
+  std::vector<double> w(h->ncfg);
+  for (int i = 0; i < h->ncfg; ++i) { order[i] = i; w[i] = config_work(h, i); }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return w[a] > w[b]; });
+  std::vector<double> load(world, 0.0);
+  owner.assign(h->ncfg, 0);
+  for (int i : order) {
+    int r = 0;
+    for (int k = 1; k < world; ++k)
+      if (load[k] < load[r]) r = k;
+    owner[i] = r;
+    load[r] += w[i];
+  }
+}
+
+extern "C" uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32_t* owner_out) {
+  if (!h || !owner_out || world < 1) return UNIAP_ERR_ARG;
+  if (!h->ready) FAIL(h, UNIAP_ERR_ARG, "nothing prepared");
+  std::vector<int> owner;
+  lpt(h, world, owner);
+  for (int i = 0; i < h->ncfg; ++i) owner_out[i] = owner[i];
+  return UNIAP_OK;
+}
+
+// Groups instances by kernel class and launches K2 for each group.
+static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, DevBuf<Inst>& buf, int32_t* Pdev) {
+  // stable order: class, then longest sweep first (LPT within the launch)
+  std::vector<int> clsid(all.size());
+  for (size_t j = 0; j < all.size(); ++j) {
+    const K2Class& k = h->cls[all[j].cfg];
+    clsid[j] = k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C;
+  }
+  std::vector<size_t> idx(all.size());
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
+    if (clsid[a] != clsid[b]) return clsid[a] < clsid[b];
+    return all[a].n > all[b].n;
+  });
+  std::vector<Inst> sorted(all.size());
+  for (size_t j = 0; j < idx.size(); ++j) sorted[j] = all[idx[j]];
+  CK(h, buf.ensure(sorted.size()));
+  if (!sorted.empty())
+    CK(h, h2d(h, buf.p, sorted.data(), sorted.size() * sizeof(Inst)));
+  size_t s = 0;
+  while (s < sorted.size()) {
+    size_t e = s;
+    const int id = clsid[idx[s]];
+    while (e < sorted.size() && clsid[idx[e]] == id) ++e;
+    K2Args args{buf.p + s, h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip};
+    CK(h, k2_launch(h->cls[sorted[s].cfg], args, (int)(e - s), h->st));
+    h->launches++;
+    h->k2_launches++;
+    s = e;
+  }
+  return UNIAP_OK;
+}
+
+static BuildBufs build_bufs(uniap_handle* h) {
+  return BuildBufs{h->fwd.p, h->act.p, h->ps.p, h->ctx.p, h->tpc.p, h->chain.p, h->skipb.p, h->edges.p,
+                   h->n_edges, h->dcat.p, h->ns.p, h->qcfg.p, h->qglob.p};
+}
+
+extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev) {
+  if (!h) return UNIAP_ERR_ARG;
+  if (!h->ready) FAIL(h, UNIAP_ERR_ARG, "nothing prepared");
+  if (world < 1 || rank < 0 || rank >= world) FAIL(h, UNIAP_ERR_ARG, "rank %d / world %d", rank, world);
+  CK(h, cudaSetDevice(h->device));
+  const int L = h->L;
+  uniap_record* rec = rec_dev ? (uniap_record*)rec_dev : nullptr;
+  if (!rec) {
+    CK(h, h->rec.ensure(1));
+    rec = h->rec.p;
+  }
+  h->last_rec = rec;
+  CK(h, cudaEventRecord(h->ev[0], h->st));
+  // K1: the cost tables of every candidate (the quantum is global)
+  if (h->level2) {
+    CK(h, launch_k1(h->cl, build_bufs(h), h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
+    h->launches += 6;
+  }
+  // this rank's configs
+  std::vector<int> owner;
+  lpt(h, world, owner);
+  std::vector<int32_t> local;
+  for (int i = 0; i < h->ncfg; ++i)
+    if (owner[i] == rank) local.push_back(i);
+  const int nl = (int)local.size();
+  // K2 forward
+  std::vector<Inst> fw;
+  for (int i : local) forward_instances(h, i, false, fw);
+  h->cells = h->relax = 0;
+  for (auto& x : fw) {
+    const uint64_t S = h->cfg[x.cfg].S;
+    h->cells += (uint64_t)x.n * S * h->Q;
+    h->relax += (uint64_t)(x.n - 1) * S * S * h->Q;
+  }
+  CK(h, h->P.ensure((size_t)h->ncfg * L * L));
+  CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
+  h->launches++;
+  CK(h, h->G.ensure(1));
+  CK(h, cudaEventRecord(h->ev[1], h->st));
+  {
+    uniap_status s = launch_k2_groups(h, fw, h->inst, h->P.p);
+    if (s != UNIAP_OK) return s;
+  }
+  CK(h, cudaEventRecord(h->ev[2], h->st));
+  // K3, K4, K5a
+  CK(h, h->cfglist.ensure(std::max(nl, 1)));
+  CK(h, h->thetas.ensure((size_t)std::max(nl, 1) * TMAX));
+  CK(h, h->ntheta.ensure(std::max(nl, 1)));
+  CK(h, h->vals.ensure((size_t)std::max(nl, 1) * (TMAX + 2)));
+  CK(h, h->cfgopt.ensure(h->ncfg));
+  CK(h, h->scratch.ensure((size_t)32 * (MAXL + 1) * (MAXL + 1)));
+  CK(h, h->win.ensure(1));
+  {
+    std::vector<int64_t> big(h->ncfg, INT64_MAX);
+    CK(h, h2d(h, h->cfgopt.p, big.data(), h->ncfg * 8));
+  }
+  if (nl > 0) CK(h, h2d(h, h->cfglist.p, local.data(), nl * 4));
+  CK(h, cudaMemsetAsync(h->vals.p, 0xff, (size_t)std::max(nl, 1) * (TMAX + 2) * 8, h->st));
+  CK(h, launch_k3(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->st));
+  CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p, h->st));
+  CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
+                   h->cfgopt.p, h->scratch.p, h->win.p, h->st));
+  h->launches += nl > 0 ? 3 : 1;
+  Winner W;
+  int64_t qg[2] = {0, 0};
+  CK(h, d2h(h, &W, h->win.p, sizeof(Winner)));
+  if (h->level2) CK(h, d2h(h, qg, h->qglob.p, 16));
+  CK(h, cudaStreamSynchronize(h->st));
+  h->quantum = h->level2 ? qg[0] : 0;
+  // record template (counters, status); K5c fills the assignment
+  uniap_record& R = h->rec_host;
+  memset(&R, 0, sizeof R);
+  R.objective = INT64_MAX;
+  R.cfg_index = -1;
+  R.L = L;
+  R.n_cfg_local = nl;
+  R.dp_cells = h->cells;
+  R.dp_relax = h->relax;
+  if (h->level2 && qg[1] != 0) R.status = UNIAP_ERR_RANGE;
+  else if (nl > 0 && W.cfg >= 0 && W.status != 0) R.status = UNIAP_ERR_INTERNAL;
+  CK(h, h2d(h, rec, &R, sizeof R));
+  if (R.status == 0 && nl > 0 && W.cfg >= 0 && W.objective != INT64_MAX) {
+    // K2 backward sweeps: one per stage (per ks when the skip source
+    // conditions the stage), storing every layer's G[u][k][q]
+    const CfgDev& d = h->cfg[W.cfg];
+    std::vector<Inst> bw;
+    std::vector<int64_t> gofs(W.deg * 33, 0);
+    int64_t goff = 0;
+    int a = 0;
+    for (int s = 0; s < W.deg; ++s) {
+      const int b = W.end[s], n = b - a + 1;
+      const bool cond = d.skip >= 0 && a <= d.skip && d.skip + 2 <= b;
+      for (int ks = cond ? 0 : -1; ks < (cond ? d.S : 0); ++ks) {
+        gofs[s * 33 + ks + 1] = goff;
+        bw.push_back(Inst{W.cfg, b, n, ks, -1, 0, goff});
+        goff += (int64_t)n * d.NSP * h->Q;
+      }
+      a = b + 1;
+    }
+    CK(h, h->G.ensure(goff));
+    CK(h, h->gofs.ensure(gofs.size()));
+    CK(h, h2d(h, h->gofs.p, gofs.data(), gofs.size() * 8));
+    uniap_status s = launch_k2_groups(h, bw, h->binst, h->P.p);
+    if (s != UNIAP_OK) return s;
+    CK(h, launch_k5c_grid(W.deg, h->dcfg.p, h->arena.p, h->G.p, h->gofs.p, h->win.p, L, h->cap, h->skip, rec, h->st));
+    h->launches++;
+  }
+  CK(h, cudaEventRecord(h->ev[3], h->st));
+  CK(h, cudaStreamSynchronize(h->st));
+  CK(h, cudaGetLastError());
+  cudaEventElapsedTime(&h->ms_dp, h->ev[1], h->ev[2]);
+  cudaEventElapsedTime(&h->ms_total, h->ev[0], h->ev[3]);
+  return UNIAP_OK;
+}
+
+extern "C" uniap_status uniap_fetch(uniap_handle* h, uniap_result* out) {
+  if (!h || !out) return UNIAP_ERR_ARG;
+  CK(h, cudaSetDevice(h->device));
+  uniap_record R;
+  const uniap_record* src = h->last_rec;
+  if (!src) FAIL(h, UNIAP_ERR_ARG, "nothing has run on this handle");
+  CK(h, d2h(h, &R, src, sizeof R));
+  int64_t* keep = out->cfg_objective;
+  memset(out, 0, sizeof *out);
+  out->cfg_objective = keep;
+  if (keep) CK(h, d2h(h, keep, h->cfgopt.p, h->ncfg * 8));
+  CK(h, cudaStreamSynchronize(h->st));
+  out->objective = R.objective;
+  out->cfg_index = R.cfg_index;
+  out->deg = R.deg;
+  out->c = R.c;
+  out->L = h->L;
+  for (int i = 0; i < UNIAP_MAX_LAYERS; ++i) {
+    out->stage_of[i] = R.stage_of[i];
+    out->strategy_of[i] = R.strategy_of[i];
+    out->stage_cost[i] = R.stage_cost[i];
+    out->cut_cost[i] = R.cut_cost[i];
+    out->stage_mem[i] = R.stage_mem[i];
+  }
+  out->quantum_ns = h->quantum;
+  out->dp_cells = R.dp_cells;
+  out->dp_relax = R.dp_relax;
+  out->ms_gpu_dp = h->ms_dp;
+  out->ms_gpu_total = h->ms_total;
+  out->h2d_bytes = h->h2d;
+  out->d2h_bytes = h->d2h;
+  out->n_launches = h->launches;
+  out->n_k2_launches = h->k2_launches;
+  if (R.status != 0) FAIL(h, (uniap_status)R.status, "device pipeline reported status %d", R.status);
+  if (R.objective == INT64_MAX) FAIL(h, UNIAP_ERR_INFEASIBLE, "every candidate config is infeasible");
+  return UNIAP_OK;
+}
+
+extern "C" uniap_status uniap_solve_tables(uniap_handle* h, const uniap_tables* t, uniap_result* out) {
+  uniap_status s = uniap_prepare_tables(h, t);
+  if (s != UNIAP_OK) return s;
+  s = uniap_run(h, 0, 1, nullptr);
+  if (s != UNIAP_OK) return s;
+  return uniap_fetch(h, out);
+}
+
+extern "C" uniap_status uniap_plan(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
+                                   const uniap_options* o, uniap_result* out) {
+  uniap_status s = uniap_prepare(h, m, cl, o);
+  if (s != UNIAP_OK) return s;
+  s = uniap_run(h, 0, 1, nullptr);
+  if (s != UNIAP_OK) return s;
+  return uniap_fetch(h, out);
+}
+
+extern "C" uniap_status uniap_interval_table(uniap_handle* h, const uniap_tables* t, int32_t cfg, int32_t* P_out) {
+  uniap_status s = uniap_prepare_tables(h, t);
+  if (s != UNIAP_OK) return s;
+  if (cfg < 0 || cfg >= h->ncfg || !P_out) FAIL(h, UNIAP_ERR_ARG, "cfg index %d", cfg);
+  const int L = h->L;
+  std::vector<Inst> fw;
+  forward_instances(h, cfg, true, fw);
+  CK(h, h->P.ensure((size_t)h->ncfg * L * L));
+  CK(h, h->G.ensure(1));
+  CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
+  s = launch_k2_groups(h, fw, h->inst, h->P.p);
+  if (s != UNIAP_OK) return s;
+  CK(h, d2h(h, P_out, h->P.p + h->cfg[cfg].offP, (size_t)L * L * 4));
+  CK(h, cudaStreamSynchronize(h->st));
+  CK(h, cudaGetLastError());
+  return UNIAP_OK;
+}
+
+extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
+                                           const uniap_options* o, int32_t* buf, int64_t buf_len, int64_t* words,
+                                           int32_t* n_cfg, int32_t* skip_src, int64_t* quantum_ns) {
+  uniap_status s = uniap_prepare(h, m, cl, o);
+  if (s != UNIAP_OK) return s;
+  const int L = h->L;
+  int64_t need = 0;
+  for (auto& d : h->cfg) need += 4 + 2 * (int64_t)L * d.S + (int64_t)(L - 1) * d.S * d.S + (int64_t)L * d.S * d.S + (L - 1);
+  if (words) *words = need;
+  if (n_cfg) *n_cfg = h->ncfg;
+  if (skip_src) *skip_src = h->skip;
+  if (!buf) return UNIAP_OK;
+  if (buf_len < need) FAIL(h, UNIAP_ERR_ARG, "buffer too small (%lld < %lld)", (long long)buf_len, (long long)need);
+  CK(h, launch_k1(h->cl, build_bufs(h), h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
+  std::vector<int32_t> a(h->arena_words);
+  int64_t qg[2];
+  CK(h, d2h(h, a.data(), h->arena.p, a.size() * 4));
+  CK(h, d2h(h, qg, h->qglob.p, 16));
+  CK(h, cudaStreamSynchronize(h->st));
+  if (qg[1] != 0) FAIL(h, UNIAP_ERR_RANGE, "modelled value out of range (flags %lld)", (long long)qg[1]);
+  if (quantum_ns) *quantum_ns = qg[0];
+  // unpack the device layout into the documented block layout
+  int64_t w = 0;
+  for (int i = 0; i < h->ncfg; ++i) {
+    const CfgDev& d = h->cfg[i];
+    const int S = d.S, N = d.NSP;
+    buf[w++] = d.deg; buf[w++] = d.c; buf[w++] = S; buf[w++] = d.g;
+    for (int u = 0; u < L; ++u)
+      for (int k = 0; k < S; ++k) buf[w++] = a[d.offA + u * N + k];
+    for (int u = 0; u < L; ++u)
+      for (int k = 0; k < S; ++k) buf[w++] = a[d.offM + u * N + k];
+    for (int e = 0; e + 1 < L; ++e)
+      for (int k = 0; k < S; ++k)
+        for (int l = 0; l < S; ++l) buf[w++] = a[d.offRf + ((int64_t)e * N + k) * N + l];
+    for (int v = 0; v < L; ++v)
+      for (int k = 0; k < S; ++k)
+        for (int l = 0; l < S; ++l) buf[w++] = a[d.offRs + ((int64_t)v * N + k) * N + l];
+    for (int e = 0; e + 1 < L; ++e) buf[w++] = a[d.offO + e];
+  }
+  return UNIAP_OK;
+}
+
+extern "C" uniap_status uniap_pick(const uniap_record* recs, int32_t world, uniap_result* out) {
+  if (!recs || world < 1 || !out) return UNIAP_ERR_ARG;
+  int best = -1;
+  uint64_t cells = 0, relax = 0;
+  for (int r = 0; r < world; ++r) {
+    const uniap_record& x = recs[r];
+    if (x.status != 0) return (uniap_status)x.status;
+    cells += x.dp_cells;
+    relax += x.dp_relax;
+    if (x.objective == INT64_MAX) continue;
+    if (best < 0) { best = r; continue; }
+    const uniap_record& b = recs[best];
+    if (x.objective < b.objective || (x.objective == b.objective && (x.deg < b.deg || (x.deg == b.deg && x.c < b.c))))
+      best = r;
+  }
+  int64_t* keep = out->cfg_objective;
+  memset(out, 0, sizeof *out);
+  out->cfg_objective = keep;
+  out->dp_cells = cells;
+  out->dp_relax = relax;
+  out->objective = INT64_MAX;
+  out->cfg_index = -1;
+  if (best < 0) return UNIAP_ERR_INFEASIBLE;
+  const uniap_record& b = recs[best];
+  out->objective = b.objective;
+  out->cfg_index = b.cfg_index;
+  out->deg = b.deg;
+  out->c = b.c;
+  out->L = b.L;
+  for (int i = 0; i < UNIAP_MAX_LAYERS; ++i) {
+    out->stage_of[i] = b.stage_of[i];
+    out->strategy_of[i] = b.strategy_of[i];
+    out->stage_cost[i] = b.stage_cost[i];
+    out->cut_cost[i] = b.cut_cost[i];
+    out->stage_mem[i] = b.stage_mem[i];
+  }
+  return UNIAP_OK;
+}

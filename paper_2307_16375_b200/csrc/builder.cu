@@ -1,0 +1,240 @@
+// builder.cu -- K1: the cost model of PAPER.md Sec. 3.2 on the GPU.
+//
+// From the integer profiles and the alpha-beta cluster
+// record, per candidate config (g = n/deg devices per stage, micro-batch
+// b = B/c) and strategy (t,f,d) (TP, FSDP, DP degrees; r = f*d replicas):
+//   time: fp = (b/r) * fwd[t]; bp = 2 fp; TP all-reduces
+//     overlapped with computation through the CCOC; FSDP all-gathers; the
+//     per-iteration gradient sync divided by c (reading A-14)
+//   memory (Eq. 1): c_dtype*ps/(t*f) + c*(b/r)*act[t] + ctx
+//   resharding R / Rskip (reading A-15) and cut costs O (readings A-1, A-16)
+// in ns / bytes with 128-bit intermediates, then one global time quantum
+// (reading A-9) and memory buckets (reading A-8), written straight into the
+// device table layout K2 reads (uniap_impl.h).  DESIGN.md Sec. 2 lists the
+// formulas.
+#include "uniap_impl.h"
+
+namespace uniap {
+
+typedef unsigned __int128 u128;
+constexpr int64_t NS_LIM = (int64_t)1 << 62;
+
+__device__ __forceinline__ u128 cdiv128(u128 x, u128 y) { return (x + y - 1) / y; }
+
+struct Coll {
+  const ClusterDev& c;
+  // a group of G devices spread over stride*G consecutive devices crosses
+  // nodes when that span exceeds a node (reading A-24)
+  __device__ int64_t bw(int64_t G, int64_t stride) const { return stride * G > c.node_size ? c.bw_inter : c.bw_intra; }
+  __device__ u128 allreduce(u128 V, int64_t G, int64_t stride) const {  // ring
+    if (G <= 1) return 0;
+    return cdiv128((u128)2 * (G - 1) * V * 1000000000ull, (u128)G * bw(G, stride)) + (u128)2 * (G - 1) * c.lat;
+  }
+  __device__ u128 allgather(u128 V, int64_t G, int64_t stride) const {
+    if (G <= 1) return 0;
+    return cdiv128((u128)(G - 1) * V * 1000000000ull, (u128)G * bw(G, stride)) + (u128)(G - 1) * c.lat;
+  }
+  __device__ u128 p2p(u128 V) const { return cdiv128(V * 1000000000ull, (u128)c.p2p) + (u128)c.lat; }
+  __device__ u128 reshard(const int32_t* s1, const int32_t* s2, u128 V) const {
+    const int64_t t1 = s1[0], r1 = (int64_t)s1[1] * s1[2], t2 = s2[0], r2 = (int64_t)s2[1] * s2[2];
+    if (t1 == t2 && r1 == r2) return 0;  // identical layouts
+    int64_t G = 1;
+    if (t1 != t2) G = max(G, t1 > t2 ? (t1 + t2 - 1) / t2 : (t2 + t1 - 1) / t1);
+    if (r1 != r2) G = max(G, r1 > r2 ? (r1 + r2 - 1) / r2 : (r2 + r1 - 1) / r1);
+    return 2 * allreduce(V, G, 1);  // forward + backward
+  }
+};
+
+__device__ __forceinline__ int lg2(int x) { return 31 - __clz(x); }
+
+__device__ __forceinline__ int64_t checked(u128 v, int64_t* flags) {
+  if (v >= (u128)NS_LIM) {
+    atomicOr(reinterpret_cast<unsigned long long*>(flags), 1ull);
+    return 0;
+  }
+  return (int64_t)v;
+}
+
+// K1a: A (ns) and M (bytes, -1 = forbidden) for every (config, layer, strategy).
+__global__ void k1a_layers(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L) {
+  const CfgDev cf = cfgs[blockIdx.y];
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= L * cf.NSP) return;
+  const int u = idx / cf.NSP, k = idx - u * cf.NSP;
+  int64_t* A = bb.ns + cf.offA;
+  int64_t* M = bb.ns + cf.offM;
+  const int64_t b = cl.B / cf.c;
+  if (k >= cf.S) { A[idx] = 0; M[idx] = -1; return; }
+  const int32_t* s = bb.cat[blockIdx.y].tfd + 3 * k;
+  const int64_t t = s[0], f = s[1], d = s[2], r = f * d;
+  if (b % r) { A[idx] = 0; M[idx] = -1; return; }  // reading A-7
+  const int64_t bl = b / r;
+  const int lt = lg2((int)t);
+  const Coll co{cl};
+  const int64_t ps = bb.ps[u];
+  const u128 fp = (u128)bl * bb.fwd[u * cl.NT + lt];
+  const u128 comp = 3 * fp;                                          // fp + bp, bp = 2 fp
+  const u128 tpc = 3 * co.allreduce((u128)bl * bb.tpc[u], t, 1);     // TP collectives fwd + 2x bwd
+  const u128 mn = comp < tpc ? comp : tpc;
+  const u128 ov = comp + tpc - (u128)cl.ccoc * mn / 1000;            // CCOC overlap (A-23)
+  const u128 ps_t = cdiv128((u128)ps, (u128)t), ps_tf = cdiv128((u128)ps, (u128)(t * f));
+  const u128 fsdp = f > 1 ? 2 * co.allgather(ps_t, f, t) : 0;        // parameter gathers fwd + bwd
+  const u128 sync = co.allreduce(ps_tf, d, t * f) + (f > 1 ? co.allgather(ps_t, f, t) : 0);
+  const u128 a = ov + fsdp + cdiv128(sync, (u128)cf.c);
+  const int64_t cdt = cl.prec ? 8 : 4;                               // c_dtype
+  const u128 mem = cdiv128((u128)cdt * ps, (u128)(t * f)) + (u128)cf.c * bl * bb.act[u * cl.NT + lt] + (u128)bb.ctx[u];
+  A[idx] = checked(a, bb.qglob + 1);
+  M[idx] = checked(mem, bb.qglob + 1);
+}
+
+// K1b: R (edge e = u->u+1), Rskip (edge skip->v) in ns, original [k][l] layout.
+__global__ void k1b_reshard(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L) {
+  const CfgDev cf = cfgs[blockIdx.y];
+  const int NSP = cf.NSP, n2 = NSP * NSP;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nR = (L - 1) * n2, nS = L * n2;
+  if (idx >= nR + nS) return;
+  const bool isR = idx < nR;
+  const int j = isR ? idx : idx - nR;
+  const int e = j / n2, k = (j - e * n2) / NSP, l = j - e * n2 - k * NSP;
+  const int64_t b = cl.B / cf.c;
+  int64_t v = 0;
+  if (k < cf.S && l < cf.S) {
+    const int64_t tb = isR ? bb.chain[e] : bb.skipb[e];
+    if (tb >= 0) {
+      const Coll co{cl};
+      v = checked(co.reshard(bb.cat[blockIdx.y].tfd + 3 * k, bb.cat[blockIdx.y].tfd + 3 * l, (u128)b * tb), bb.qglob + 1);
+    }
+  }
+  (bb.ns + (isR ? cf.offRf : cf.offRs))[j] = v;
+}
+
+// K1c: cut costs: every edge crossing the cut after layer e, fwd + bwd P2P.
+__global__ void k1c_cuts(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L) {
+  const CfgDev cf = cfgs[blockIdx.y];
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= L - 1) return;
+  const int64_t b = cl.B / cf.c;
+  const Coll co{cl};
+  u128 s = 0;
+  for (int i = 0; i < bb.n_edges; ++i) {
+    const int64_t* ed = bb.esrc_dst_bytes + 3 * i;
+    if (ed[0] <= e && e < ed[1]) s += 2 * co.p2p((u128)b * ed[2]);
+  }
+  (bb.ns + cf.offO)[e] = checked(s, bb.qglob + 1);
+}
+
+// K1d: the smallest passing power-of-two quantum of each config (reading A-9):
+// every ceil(x/q) <= 2^22 and sum_u (max A + max R into u + max Rskip into u)
+// <= 2^28, sum_e O <= 2^28.  An explicit quantum is checked as given.
+__global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int skip) {
+  __shared__ int64_t mA[MAXL], mR[MAXL], mS[MAXL], sO[MAXL];
+  __shared__ int okp[64];
+  const CfgDev cf = cfgs[blockIdx.x];
+  const int t = threadIdx.x;
+  const int NSP = cf.NSP, S = cf.S;
+  for (int u = t; u < L; u += blockDim.x) {
+    int64_t a = 0, r = 0, s = 0;
+    for (int k = 0; k < S; ++k) a = max(a, bb.ns[cf.offA + u * NSP + k]);
+    if (u >= 1)
+      for (int k = 0; k < S; ++k)
+        for (int l = 0; l < S; ++l) r = max(r, bb.ns[cf.offRf + ((int64_t)(u - 1) * NSP + k) * NSP + l]);
+    if (skip >= 0 && u >= skip + 2)
+      for (int k = 0; k < S; ++k)
+        for (int l = 0; l < S; ++l) s = max(s, bb.ns[cf.offRs + ((int64_t)u * NSP + k) * NSP + l]);
+    mA[u] = a; mR[u] = r; mS[u] = s;
+    sO[u] = (u < L - 1) ? bb.ns[cf.offO + u] : 0;
+  }
+  __syncthreads();
+  if (t < 64) {
+    const bool expl = cl.quantum > 0;
+    okp[t] = 0;
+    if (!expl || t == 0) {
+      const int64_t q = expl ? cl.quantum : ((int64_t)1 << t);
+      if (expl || t <= 61) {
+        const int64_t EM = (int64_t)UNIAP_MAX_ENTRY, SM = (int64_t)UNIAP_MAX_SUM;
+        bool ok = true;
+        int64_t sum = 0, osum = 0;
+        for (int u = 0; u < L; ++u) {
+          const int64_t a = (mA[u] + q - 1) / q, r = (mR[u] + q - 1) / q, s = (mS[u] + q - 1) / q;
+          const int64_t o = (sO[u] + q - 1) / q;
+          ok = ok && a <= EM && r <= EM && s <= EM && o <= EM;
+          sum += a + r + s;
+          osum += o;
+        }
+        ok = ok && sum <= SM && osum <= SM;
+        okp[t] = ok;
+      }
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    int64_t q = -1;
+    if (cl.quantum > 0) q = okp[0] ? cl.quantum : -1;
+    else
+      for (int p = 0; p <= 61; ++p)
+        if (okp[p]) { q = (int64_t)1 << p; break; }
+    bb.qcfg[blockIdx.x] = q;
+  }
+}
+
+// K1e: global quantum = max over configs (monotone checks), error if any fails.
+__global__ void k1e_global(BuildBufs bb, int ncfg) {
+  int64_t q = 1;
+  for (int i = 0; i < ncfg; ++i) {
+    const int64_t x = bb.qcfg[i];
+    if (x < 0) { atomicOr(reinterpret_cast<unsigned long long*>(bb.qglob + 1), 2ull); q = -1; break; }
+    q = max(q, x);
+  }
+  bb.qglob[0] = q;
+}
+
+// K1f: quantise into the int32 device layout (A, M buckets, Rt, Rf, Rs, O).
+__global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int32_t* arena) {
+  const CfgDev cf = cfgs[blockIdx.y];
+  const int NSP = cf.NSP, n2 = NSP * NSP;
+  const int64_t q = bb.qglob[0] > 0 ? bb.qglob[0] : 1;
+  const int cap = cl.Q - 1;
+  const int64_t unit = (cl.mem_bytes - cl.mem_reserve) / cap;  // reading A-8
+  const int nA = L * NSP, nR = (L - 1) * n2, nS = L * n2, nO = ((L - 1) + 3) & ~3;
+  auto qt = [&](int64_t x) { return (int32_t)((x + q - 1) / q); };
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nA + nR + nS + nO; idx += gridDim.x * blockDim.x) {
+    int j = idx;
+    if (j < nA) { arena[cf.offA + j] = qt(bb.ns[cf.offA + j]); continue; }
+    j -= nA;
+    if (j < nA) {
+      const int64_t byt = bb.ns[cf.offM + j];
+      int64_t bk = byt < 0 ? (int64_t)cap + 1 : (byt + unit - 1) / unit;
+      arena[cf.offM + j] = (int32_t)(bk > cap ? cap + 1 : bk);
+      continue;
+    }
+    j -= nA;
+    if (j < nR) {  // Rf = R, Rt = transpose within each edge
+      const int e = j / n2, k = (j - e * n2) / NSP, l = j - e * n2 - k * NSP;
+      const int32_t v = qt(bb.ns[cf.offRf + j]);
+      arena[cf.offRf + j] = v;
+      arena[cf.offRt + (int64_t)e * n2 + l * NSP + k] = v;
+      continue;
+    }
+    j -= nR;
+    if (j < nS) { arena[cf.offRs + j] = qt(bb.ns[cf.offRs + j]); continue; }
+    j -= nS;
+    arena[cf.offO + j] = j < L - 1 ? qt(bb.ns[cf.offO + j]) : 0;
+  }
+}
+
+cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* cfg, int ncfg, int L, int skip,
+                      int32_t* arena, cudaStream_t st) {
+  const int maxNSP = 32;
+  cudaError_t e = cudaMemsetAsync(bb.qglob, 0, 2 * sizeof(int64_t), st);
+  if (e != cudaSuccess) return e;
+  k1a_layers<<<dim3((L * maxNSP + 127) / 128, ncfg), 128, 0, st>>>(cl, bb, cfg, L);
+  k1b_reshard<<<dim3(((2 * L - 1) * maxNSP * maxNSP + 255) / 256, ncfg), 256, 0, st>>>(cl, bb, cfg, L);
+  k1c_cuts<<<dim3(1, ncfg), 64, 0, st>>>(cl, bb, cfg, L);
+  k1d_quantum<<<ncfg, 64, 0, st>>>(cl, bb, cfg, L, skip);
+  k1e_global<<<1, 1, 0, st>>>(bb, ncfg);
+  k1f_quantise<<<dim3(16, ncfg), 256, 0, st>>>(cl, bb, cfg, L, arena);
+  return cudaGetLastError();
+}
+
+}  // namespace uniap

@@ -1,0 +1,489 @@
+// combine.cu -- K3 (theta candidates), K4 (stage combine, Eq. 2), K5a
+// (per-config and global argmin + stage ends), K5c (strategy walk).
+//
+// Combine (Eq. 2).  For a config with interval optima
+// P[a][b] (K2) and cut costs O[e], the optimum over ordered placements of
+//     tpi = sum_i p_i + sum_j o_j + (c-1) * max(P u O)
+// is  min over theta of  Val(theta) = F_theta + (c-1) * theta,  where
+// F_theta = min sum_i P[a_i][b_i] + sum_j O[b_j] over placements whose every
+// P and O is <= theta, and theta ranges over the distinct P / O values (K3).
+// Proof: for an optimal placement pi* with max X*, F_{X*} <= sum(pi*) so
+// Val(X*) <= OPT; conversely the placement attaining F_theta has tpi <=
+// Val(theta).  The optimal placements are exactly the argmin sets of F_theta
+// over theta with Val(theta) = OPT.  For c = 1, Val =
+// F_theta and the largest theta (no constraint) contains every argmin.
+#include <cub/block/block_scan.cuh>
+
+#include "uniap_impl.h"
+
+namespace uniap {
+
+__global__ void k_fill(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_fill<<<blocks, 256, 0, st>>>(p, n, v);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K3: sorted distinct theta candidates per config (one CTA per config).
+// ---------------------------------------------------------------------------
+constexpr int K3T = 1024;
+__global__ void __launch_bounds__(K3T) k3_thetas(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
+                                                 const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
+                                                 int L, int32_t* __restrict__ thetas, int32_t* __restrict__ ntheta) {
+  __shared__ int32_t v[SORTN];
+  __shared__ int32_t cnt;
+  typedef cub::BlockScan<int, K3T> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  const int t = threadIdx.x;
+  const int ci = cfg_list[blockIdx.x];
+  const CfgDev cf = cfgs[ci];
+  if (t == 0) cnt = 0;
+  for (int i = t; i < SORTN; i += K3T) v[i] = 0x7fffffff;
+  __syncthreads();
+  const int32_t* Pc = P + cf.offP;
+  for (int idx = t; idx < L * L; idx += K3T) {
+    const int a = idx / L, b = idx - a * L;
+    const int32_t x = Pc[idx];
+    if (a <= b && x < INF) v[atomicAdd(&cnt, 1)] = x;
+  }
+  const int32_t* O = arena + cf.offO;
+  for (int e = t; e < L - 1; e += K3T) v[atomicAdd(&cnt, 1)] = O[e];
+  __syncthreads();
+  const int n = cnt;
+  int N = 2;
+  while (N < n) N <<= 1;
+  // bitonic sort of v[0..N)
+  for (int k = 2; k <= N; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = t; i < N; i += K3T) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const int32_t x = v[i], y = v[ixj];
+          if ((x > y) == up) {
+            v[i] = y;
+            v[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  // dedupe: 4 consecutive elements per thread
+  int flags[4], c = 0;
+  for (int r = 0; r < 4; ++r) {
+    const int i = 4 * t + r;
+    flags[r] = (i < n) && (i == 0 || v[i] != v[i - 1]);
+    c += flags[r];
+  }
+  int pos, total;
+  Scan(scan_tmp).ExclusiveSum(c, pos, total);
+  int32_t* out = thetas + (int64_t)blockIdx.x * TMAX;
+  for (int r = 0; r < 4; ++r)
+    if (flags[r]) out[pos++] = v[4 * t + r];
+  if (t == 0) ntheta[blockIdx.x] = total;
+}
+
+cudaError_t launch_k3(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
+                      int L, int32_t* thetas, int32_t* ntheta, cudaStream_t st) {
+  if (n_local <= 0) return cudaSuccess;
+  k3_thetas<<<n_local, K3T, 0, st>>>(cfg, arena, P, cfg_list, L, thetas, ntheta);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// F_theta by a warp: forward DP over (stage i, end b); lanes own b.
+// Returns F_theta (INF if no placement fits).  theta = INF means "no limit".
+// sP: the config's P[L][L] in shared memory; sO: O[L-1]; g: 2*64 scratch.
+// ---------------------------------------------------------------------------
+__device__ int32_t warp_F(const int32_t* sP, const int32_t* sO, int32_t* g, int L, int deg, int32_t theta) {
+  const int lane = threadIdx.x & 31;
+  int32_t* cur = g;
+  int32_t* nxt = g + 64;
+  // stage 1 = [0, b], b <= L-1-(deg-1)
+  for (int b = lane; b < L; b += 32) {
+    const int32_t p = sP[b];
+    cur[b] = (b <= L - deg && p <= theta) ? p : INF;
+  }
+  __syncwarp();
+  for (int i = 2; i <= deg; ++i) {
+    // stage i = [a, b] with i-1 <= a <= b <= L-1-(deg-i); the last stage ends at L-1
+    const int blo = (i == deg) ? L - 1 : i - 1, bhi = L - 1 - (deg - i);
+    const int b0 = lane, b1 = lane + 32;
+    int32_t best0 = INF, best1 = INF;
+    for (int a = i - 1; a <= bhi; ++a) {  // stage i-1 ends at a-1
+      const int32_t gp = cur[a - 1];
+      const int32_t o = sO[a - 1];
+      if (gp >= INF || o > theta) continue;  // warp-uniform
+      const int32_t base = gp + o;
+      if (b0 >= a && b0 >= blo && b0 <= bhi) {
+        const int32_t p = sP[a * L + b0];
+        if (p <= theta) best0 = min(best0, base + p);
+      }
+      if (b1 >= a && b1 >= blo && b1 <= bhi && b1 < L) {
+        const int32_t p = sP[a * L + b1];
+        if (p <= theta) best1 = min(best1, base + p);
+      }
+    }
+    __syncwarp();
+    if (b0 < L) nxt[b0] = min(best0, INF);
+    if (b1 < L) nxt[b1] = min(best1, INF);
+    __syncwarp();
+    int32_t* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+  }
+  const int32_t F = cur[L - 1];
+  __syncwarp();
+  return F;
+}
+
+// ---------------------------------------------------------------------------
+// K4: Val(theta) for every theta of every local config.
+// grid (n_local, K4G); 8 warps per CTA; warp w of CTA y handles theta indices
+// i = y*8+w, i += K4G*8 (ascending), skipping theta once
+// F_inf + (c-1)*theta > best-so-far (strict: ties stay for the tie-break).
+// ---------------------------------------------------------------------------
+constexpr int K4G = 16;
+constexpr int K4W = 8;
+__global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
+                                                   const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
+                                                   int L, const int32_t* __restrict__ thetas,
+                                                   const int32_t* __restrict__ ntheta, int64_t* __restrict__ vals) {
+  __shared__ int32_t sP[MAXL * MAXL];
+  __shared__ int32_t sO[MAXL];
+  __shared__ int32_t g[K4W][128];
+  const int li = blockIdx.x;
+  const CfgDev cf = cfgs[cfg_list[li]];
+  for (int i = threadIdx.x; i < L * L; i += blockDim.x) sP[i] = P[cf.offP + i];
+  for (int i = threadIdx.x; i < L - 1; i += blockDim.x) sO[i] = arena[cf.offO + i];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = ntheta[li];
+  int64_t* V = vals + (int64_t)li * (TMAX + 2);  // [0..nt) Val, [TMAX] F_inf, [TMAX+1] best
+  const int32_t* th = thetas + (int64_t)li * TMAX;
+  if (cf.deg > L) {  // Eq. 7b cannot hold (reading A-22)
+    for (int i = blockIdx.y * K4W + w; i < nt; i += K4G * K4W)
+      if (lane == 0) V[i] = INT64_MAX;
+    if (blockIdx.y == 0 && threadIdx.x == 0) V[TMAX] = INT64_MAX;
+    return;
+  }
+  // every warp computes F_inf itself (cheap, avoids a grid barrier)
+  const int32_t Finf = warp_F(sP, sO, g[w], L, cf.deg, INF);
+  if (blockIdx.y == 0 && w == 0 && lane == 0) V[TMAX] = Finf >= INF ? INT64_MAX : (int64_t)Finf;
+  const int64_t cm1 = cf.c - 1;
+  unsigned long long* best = reinterpret_cast<unsigned long long*>(V + TMAX + 1);
+  for (int i = blockIdx.y * K4W + w; i < nt; i += K4G * K4W) {
+    const int32_t theta = th[i];
+    int64_t val = INT64_MAX;
+    if (Finf < INF && cf.c > 1) {
+      const int64_t lb = (int64_t)Finf + cm1 * theta;
+      const unsigned long long bs = *(volatile unsigned long long*)best;
+      if ((unsigned long long)lb <= bs) {
+        const int32_t F = warp_F(sP, sO, g[w], L, cf.deg, theta);
+        if (F < INF) {
+          val = (int64_t)F + cm1 * theta;
+          if (lane == 0) atomicMin(best, (unsigned long long)val);
+        }
+      }
+    }
+    if (lane == 0) V[i] = val;
+  }
+}
+
+cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
+                      int L, const int32_t* thetas, const int32_t* ntheta, int64_t* vals, cudaStream_t st) {
+  if (n_local <= 0) return cudaSuccess;
+  k4_vals<<<dim3(n_local, K4G), K4W * 32, 0, st>>>(cfg, arena, P, cfg_list, L, thetas, ntheta, vals);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K5a: per-config optimum, global (objective, deg, c) argmin, and the
+// lexicographically largest stage-end vector over the optimal placements
+// (= lexicographically smallest stage_of, reading A-11).  One CTA.
+// ---------------------------------------------------------------------------
+constexpr int K5T = 1024;
+__global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
+                                                  const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
+                                                  int n_local, int L, const int32_t* __restrict__ thetas,
+                                                  const int32_t* __restrict__ ntheta, const int64_t* __restrict__ vals,
+                                                  int64_t* __restrict__ cfg_opt, int32_t* __restrict__ scratch,
+                                                  Winner* __restrict__ win) {
+  __shared__ int32_t sP[MAXL * MAXL];
+  __shared__ int32_t sO[MAXL];
+  __shared__ int64_t red[32];
+  __shared__ int32_t stars[TMAX];
+  __shared__ int32_t nstar;
+  __shared__ int32_t ends[32][MAXL];
+  __shared__ int32_t okw[32];
+  __shared__ int64_t s_opt[1];
+  __shared__ int32_t s_win;
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  // 1. per-config optimum (min over theta of Val; c = 1: F_inf)
+  for (int li = 0; li < n_local; ++li) {
+    const CfgDev cf = cfgs[cfg_list[li]];
+    const int64_t* V = vals + (int64_t)li * (TMAX + 2);
+    int64_t m = INT64_MAX;
+    if (cf.c == 1) m = V[TMAX];
+    else
+      for (int i = t; i < ntheta[li]; i += K5T) m = min(m, V[i]);
+    for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) red[w] = m;
+    __syncthreads();
+    if (t == 0) {
+      int64_t r = INT64_MAX;
+      for (int i = 0; i < 32; ++i) r = min(r, red[i]);
+      cfg_opt[cfg_list[li]] = r;
+    }
+    __syncthreads();
+  }
+  // 2. winner by (objective, deg, c)
+  if (t == 0) {
+    int wi = -1;
+    int64_t best = INT64_MAX;
+    for (int li = 0; li < n_local; ++li) {
+      const int ci = cfg_list[li];
+      const int64_t v = cfg_opt[ci];
+      if (v == INT64_MAX) continue;
+      const CfgDev a = cfgs[ci];
+      bool take = wi < 0 || v < best;
+      if (!take && v == best) {
+        const CfgDev b = cfgs[cfg_list[wi]];
+        take = a.deg < b.deg || (a.deg == b.deg && a.c < b.c);
+      }
+      if (take) { wi = li; best = v; }
+    }
+    s_win = wi;
+    s_opt[0] = best;
+    nstar = 0;
+  }
+  __syncthreads();
+  const int wl = s_win;
+  if (wl < 0) {
+    if (t == 0) { win->objective = INT64_MAX; win->cfg = -1; win->status = 0; }
+    return;
+  }
+  const int ci = cfg_list[wl];
+  const CfgDev cf = cfgs[ci];
+  const int64_t OPT = s_opt[0];
+  const int64_t* V = vals + (int64_t)wl * (TMAX + 2);
+  const int32_t* th = thetas + (int64_t)wl * TMAX;
+  const int nt = ntheta[wl];
+  for (int i = t; i < L * L; i += K5T) sP[i] = P[cf.offP + i];
+  for (int i = t; i < L - 1; i += K5T) sO[i] = arena[cf.offO + i];
+  // 3. Theta*: every theta with Val = OPT (c > 1); the unconstrained one (c = 1)
+  if (cf.c == 1) {
+    if (t == 0) { stars[0] = -1; nstar = 1; }
+  } else {
+    for (int i = t; i < nt; i += K5T)
+      if (V[i] == OPT) stars[atomicAdd(&nstar, 1)] = i;
+  }
+  __syncthreads();
+  const int ns = nstar;
+  const int deg = cf.deg;
+  // 4. per theta in Theta*: suffix DP H_i[a] (cover [a, L-1] with stages i..deg)
+  //    then the greedy largest end per stage.
+  int32_t* H = scratch + (int64_t)w * (MAXL + 1) * (MAXL + 1);  // [i][a], i = 1..deg, a = 0..L
+  int32_t* mine = ends[w];
+  int32_t best_end[MAXL];
+  bool have = false;
+  for (int base = 0; base < ns; base += 32) {
+    const int si = base + w;
+    bool ok = false;
+    if (si < ns) {
+      const int32_t theta = stars[si] < 0 ? INF : th[stars[si]];
+      const int64_t F_target = stars[si] < 0 ? OPT : OPT - (int64_t)(cf.c - 1) * theta;
+      // H_deg[a] = P[a][L-1]
+      for (int a = lane; a <= L; a += 32) {
+        int32_t v = INF;
+        if (a < L) { const int32_t p = sP[a * L + L - 1]; v = p <= theta ? p : INF; }
+        H[deg * (MAXL + 1) + a] = v;
+      }
+      __syncwarp();
+      for (int i = deg - 1; i >= 1; --i) {
+        for (int a = lane; a <= L; a += 32) {
+          int32_t best = INF;
+          if (a < L)
+            for (int b = a; b <= L - 1 - (deg - i); ++b) {
+              const int32_t p = sP[a * L + b], o = sO[b], h = H[(i + 1) * (MAXL + 1) + b + 1];
+              if (p <= theta && o <= theta && h < INF) best = min(best, p + o + h);
+            }
+          H[i * (MAXL + 1) + a] = min(best, INF);
+        }
+        __syncwarp();
+      }
+      ok = (int64_t)H[1 * (MAXL + 1) + 0] == F_target;
+      // greedy: the largest feasible end of each stage
+      int64_t pre = 0;
+      int a = 0;
+      for (int i = 1; i < deg && ok; ++i) {
+        int found = -1;
+        for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
+          const int b = b0 - lane;
+          bool c = false;
+          if (b >= a) {
+            const int32_t p = sP[a * L + b], o = sO[b], h = H[(i + 1) * (MAXL + 1) + b + 1];
+            c = p <= theta && o <= theta && h < INF && pre + p + o + h == F_target;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, c);
+          if (m) found = b0 - (__ffs(m) - 1);
+        }
+        if (found < 0) { ok = false; break; }
+        if (lane == 0) mine[i - 1] = found;
+        pre += sP[a * L + found] + sO[found];
+        a = found + 1;
+      }
+      if (lane == 0) mine[deg - 1] = L - 1;
+      __syncwarp();
+    }
+    if (lane == 0) okw[w] = ok;
+    __syncthreads();
+    // lexicographically largest end vector (theta order is deterministic)
+    if (t == 0) {
+      for (int j = 0; j < 32 && base + j < ns; ++j) {
+        if (!okw[j]) continue;
+        bool better = !have;
+        for (int i = 0; i < deg && !better; ++i) {
+          if (ends[j][i] != best_end[i]) { better = ends[j][i] > best_end[i]; break; }
+        }
+        if (better) {
+          for (int i = 0; i < deg; ++i) best_end[i] = ends[j][i];
+          have = true;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    win->objective = OPT;
+    win->cfg = ci;
+    win->deg = deg;
+    win->c = cf.c;
+    win->S = cf.S;
+    win->NSP = cf.NSP;
+    win->n_theta_star = ns;
+    win->status = have ? 0 : 99;
+    int a = 0;
+    for (int i = 0; i < deg; ++i) {
+      const int b = have ? best_end[i] : L - 1;
+      win->end[i] = b;
+      win->p[i] = sP[a * L + b];
+      win->o[i] = (i + 1 < deg) ? sO[b] : 0;
+      a = b + 1;
+    }
+  }
+}
+
+cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
+                       int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals, int64_t* cfg_opt,
+                       int32_t* scratch, Winner* win, cudaStream_t st) {
+  k5a_winner<<<1, K5T, 0, st>>>(cfg, arena, P, cfg_list, n_local, L, thetas, ntheta, vals, cfg_opt, scratch, win);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K5c: per stage, the lexicographically smallest strategy vector reaching the
+// stage optimum, walking the backward tables G (K2 backward sweeps):
+// at layer u take the smallest k with  R[u-1][k_{u-1}][k] + G[u][k][q] = rest.
+// One CTA per stage; warp w walks the conditioning ks = w (or none).
+// Also writes the record (objective, placement, costs, memory).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
+                                                 const int32_t* __restrict__ G, const int64_t* __restrict__ gofs,
+                                                 const Winner* __restrict__ win, int L, int cap, int skip,
+                                                 uniap_record* __restrict__ rec) {
+  __shared__ int32_t vec[32][MAXL];
+  __shared__ int32_t mem[32];
+  __shared__ int32_t okw[32];
+  const int stage = blockIdx.x;
+  const Winner W = *win;
+  const CfgDev cf = cfgs[W.cfg];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a = stage == 0 ? 0 : W.end[stage - 1] + 1, b = W.end[stage];
+  skip = cf.skip;
+  const bool cond = skip >= 0 && a <= skip && skip + 2 <= b;
+  const int nks = cond ? cf.S : 1;
+  const int NSP = cf.NSP, Q = cap + 1, S = cf.S;
+  const int32_t* A = arena + cf.offA;
+  const int32_t* M = arena + cf.offM;
+  const int32_t* Rf = arena + cf.offRf;
+  const int32_t* Rs = arena + cf.offRs;
+  bool ok = false;
+  if (w < nks) {
+    const int ks = cond ? w : -1;
+    const int32_t* g = G + gofs[stage * 33 + (ks + 1)];
+    int64_t rest = W.p[stage];
+    int q = cap, kprev = -1;
+    int32_t msum = 0;
+    ok = true;
+    for (int u = a; u <= b && ok; ++u) {
+      const int k = lane;
+      bool c = false;
+      int32_t edge = 0, ap = 0;
+      if (k < S) {
+        const int32_t gv = g[((int64_t)(u - a) * NSP + k) * Q + q];
+        edge = (u > a) ? Rf[((int64_t)(u - 1) * NSP + kprev) * NSP + k] : 0;
+        ap = A[u * NSP + k] + ((ks >= 0 && u >= skip + 2) ? Rs[((int64_t)u * NSP + ks) * NSP + k] : 0);
+        c = gv < INF && (int64_t)edge + gv == rest;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, c);
+      if (!m) { ok = false; break; }
+      const int kk = __ffs(m) - 1;
+      const int32_t e2 = __shfl_sync(0xffffffffu, edge, kk);
+      const int32_t a2 = __shfl_sync(0xffffffffu, ap, kk);
+      const int32_t m2 = M[u * NSP + kk];
+      rest -= (int64_t)e2 + a2;
+      q -= m2;
+      msum += m2;
+      kprev = kk;
+      if (lane == 0) vec[w][u] = kk;
+    }
+    if (lane == 0) mem[w] = msum;
+  }
+  if (lane == 0) okw[w] = ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int bw = -1;
+    for (int j = 0; j < nks; ++j) {
+      if (!okw[j]) continue;
+      bool better = bw < 0;
+      for (int u = a; u <= b && !better; ++u)
+        if (vec[j][u] != vec[bw][u]) { better = vec[j][u] < vec[bw][u]; break; }
+      if (better) bw = j;
+    }
+    if (bw < 0) {
+      rec->status = UNIAP_ERR_INTERNAL;
+    } else {
+      for (int u = a; u <= b; ++u) {
+        rec->strategy_of[u] = vec[bw][u];
+        rec->stage_of[u] = stage;
+      }
+      rec->stage_mem[stage] = mem[bw];
+      rec->stage_cost[stage] = W.p[stage];
+      rec->cut_cost[stage] = W.o[stage];
+    }
+    if (stage == 0) {
+      rec->objective = W.objective;
+      rec->cfg_index = W.cfg;
+      rec->deg = W.deg;
+      rec->c = W.c;
+      rec->L = L;
+    }
+  }
+}
+
+cudaError_t launch_k5c_grid(int deg, const CfgDev* cfg, const int32_t* arena, const int32_t* G,
+                            const int64_t* gofs_stage_ks, const Winner* win, int L, int cap, int skip,
+                            uniap_record* rec, cudaStream_t st) {
+  k5c_walk<<<deg, 1024, 0, st>>>(cfg, arena, G, gofs_stage_ks, win, L, cap, skip, rec);
+  return cudaGetLastError();
+}
+
+}  // namespace uniap

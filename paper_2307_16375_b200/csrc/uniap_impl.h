@@ -1,0 +1,119 @@
+// uniap_impl.h -- internal declarations of libuniap.so (not part of the ABI).
+//
+// Device data layout (one "arena" of int32 words per handle, 16-byte aligned
+// blocks; NSP = the padded strategy count of the config's kernel class):
+//   A  [L][NSP]        execution cost A_uk (pad: 0)
+//   M  [L][NSP]        memory buckets M_uk (pad / forbidden: cap+1)
+//   Rt [L-1][NSP][NSP] Rt[e][k][k'] = R[e][k'][k]   (forward sweep: for a
+//                      destination k the sources k' are contiguous)
+//   Rf [L-1][NSP][NSP] Rf[e][k][l]  = R[e][k][l]    (backward sweep)
+//   Rs [L][NSP][NSP]   Rs[v][ks][k] = Rskip[v][ks][k] (0 where no skip edge)
+//   O  [L-1 (pad 4)]   cut cost
+// P arena: [cfg][L][L] int32 interval optima (UNIAP_INF = not computed /
+// infeasible).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "uniap.h"
+
+namespace uniap {
+
+constexpr int32_t INF = UNIAP_INF;
+constexpr int MAXL = UNIAP_MAX_LAYERS;
+constexpr int TMAX = 2176;   // >= L(L+1)/2 + L - 1 theta candidates for L <= 64
+constexpr int SORTN = 4096;  // bitonic size (power of two >= TMAX)
+
+struct CfgDev {
+  int32_t deg, c, S, NSP, g, skip;        // skip: skip source of this config's tables (-1 none)
+  int64_t offA, offM, offRt, offRf, offRs, offO;  // word offsets into the arena
+  int64_t offP;                            // word offset into the P arena
+};
+
+// One chain sweep of K2.
+struct Inst {
+  int32_t cfg;   // config index
+  int32_t a;     // first layer swept
+  int32_t n;     // number of layers swept (>= 1)
+  int32_t ks;    // skip-source conditioning (-1 = none)
+  int32_t dir;   // +1 forward (emit P[a][u]), -1 backward (store G[u])
+  int32_t emit;  // forward: 1 plain store, 2 atomicMin (several copies); backward: 0
+  int64_t gofs;  // backward: word offset of this sweep's G block (layers a-n+1..a)
+};
+
+struct K2Args {
+  const Inst* inst;
+  const CfgDev* cfg;
+  const int32_t* arena;
+  int32_t* P;
+  int32_t* G;
+  int32_t L, cap, skip;
+};
+
+// Kernel class: template shape of K2.
+struct K2Class {
+  int NS;      // strategies (padded)
+  int V;       // buckets per thread
+  int T;       // threads per CTA
+  int C;       // CTAs per cluster
+  bool DB;     // double-buffered E
+};
+
+// chain_dp.cu
+bool k2_pick_class(int S, int Q, K2Class* out);
+int k2_ns_round(int S);
+size_t k2_smem_bytes(const K2Class& c);
+cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st);
+
+// Winner of the combine step (written by K5a, read by the host and K5c).
+struct Winner {
+  int64_t objective;  // INT64_MAX if none
+  int32_t cfg, deg, c, S, NSP, n_theta_star, status;
+  int32_t end[MAXL];
+  int64_t p[MAXL], o[MAXL];
+};
+
+// combine.cu
+cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st);
+cudaError_t launch_k3(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
+                      int n_local, int L, int32_t* thetas, int32_t* ntheta, cudaStream_t st);
+cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
+                      int n_local, int L, const int32_t* thetas, const int32_t* ntheta, int64_t* vals,
+                      cudaStream_t st);
+cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
+                       int n_local, int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals,
+                       int64_t* cfg_opt, int32_t* scratch, Winner* win, cudaStream_t st);
+cudaError_t launch_k5c_grid(int deg, const CfgDev* cfg, const int32_t* arena, const int32_t* G,
+                            const int64_t* gofs_stage_ks, const Winner* win, int L, int cap, int skip,
+                            uniap_record* rec, cudaStream_t st);
+
+// builder.cu (K1)
+struct ClusterDev {
+  int32_t n_dev, node_size, ccoc, B, prec, Q, NT;
+  int64_t mem_bytes, mem_reserve, bw_intra, bw_inter, p2p, lat, quantum;
+};
+struct CatDev {  // per config: catalogue (t,f,d) of its strategies
+  int32_t tfd[UNIAP_MAX_STRAT * 3];
+};
+struct BuildBufs {
+  const int64_t* fwd;     // [L][NT]
+  const int64_t* act;     // [L][NT]
+  const int64_t* ps;      // [L]
+  const int64_t* ctx;     // [L]
+  const int64_t* tpc;     // [L]
+  const int64_t* chain;   // [L] tensor bytes of edge u->u+1, -1 none
+  const int64_t* skipb;   // [L] tensor bytes of edge skip->v, -1 none
+  const int64_t* esrc_dst_bytes;  // [E][3]
+  int32_t n_edges;
+  const CatDev* cat;      // [ncfg]
+  int64_t* ns;            // int64 scratch arena, same offsets as the int32 arena
+  int64_t* qcfg;          // [ncfg] smallest passing quantum per config
+  int64_t* qglob;         // [2]: quantum, error flags
+};
+cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* cfg, int ncfg, int L, int skip,
+                      int32_t* arena, cudaStream_t st);
+
+}  // namespace uniap

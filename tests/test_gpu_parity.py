@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, bit-exact
+(objective, per-config optima, deg, c, stage_of, strategy_of, p, o, memory).
+
+The bar is bit-exact equality: everything is integer (DESIGN.md Sec. 2,
+readings A-8..A-10).  Sizes: the toy; thousands of random tiny instances
+(brute-force-checked oracle); random tables spanning several tiles, ragged
+bucket tails and the cluster (DSMEM) path; the five synthetic model profiles
+at full size (BASELINE.json configs); builder tables; edge cases.
+"""
+import numpy as np
+import pytest
+
+from gen import profiles, tables
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("objective", "cfg_index", "deg", "c", "cfg_objective")
+ASSIGN = ("stage_of", "strategy_of", "stage_cost", "cut_cost", "stage_mem")
+
+
+@pytest.fixture(scope="module")
+def h():
+    import paper_2307_16375_b200 as pkg
+    hd = pkg.Handle(0)
+    yield hd
+    hd.close()
+
+
+def _same(g, o, what=""):
+    for k in KEYS:
+        assert g[k] == o[k], (what, k, g[k], o[k])
+    if o["objective"] != (1 << 63) - 1:
+        for k in ASSIGN:
+            assert g[k] == o[k], (what, k, g[k], o[k])
+
+
+def test_toy(h, orc):
+    for cands in (tables.TOY_GRID, [(1, 1), (2, 2)], [(1, 2)], [(2, 1)]):
+        t = tables.toy_tables(cands)
+        _same(h.solve_tables(t), orc.solve_tables(t), cands)
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_random_tiny(h, orc, chunk):
+    for seed in range(chunk * 600, (chunk + 1) * 600):
+        t = tables.random_tables(seed)
+        _same(h.solve_tables(t), orc.solve_tables(t), seed)
+
+
+def test_random_wide_strategy_sets(h, orc):
+    """|S| up to 32 (every kernel class), L up to 10, tie-heavy and uniform."""
+    rng = np.random.default_rng(5)
+    for seed in range(150):
+        L = int(rng.integers(1, 11))
+        t = tables.random_tables(50_000 + seed, L=L, S_max=int(rng.choice([4, 8, 12, 16, 24, 32])),
+                                 cap=int(rng.integers(0, 40)), n_cfg=int(rng.integers(1, 5)))
+        _same(h.solve_tables(t), orc.solve_tables(t), seed)
+
+
+@pytest.mark.parametrize("Q", [1, 7, 31, 33, 64, 100, 129, 300, 513, 1024, 1025, 2047, 3000, 4096, 5000, 8192])
+def test_interval_table_elementwise(h, orc, Q):
+    """Every interval optimum P[a][b], element by element, across bucket
+    counts that exercise each K2 shape, ragged tails and the cluster path."""
+    rng = np.random.default_rng(Q)
+    for S in (1, 3, 6, 10, 15, 21):
+        if Q > 2048 and S > 15:
+            continue
+        L = 12 if Q <= 1024 else 6
+        skip = int(rng.integers(0, L - 2)) if rng.random() < 0.5 else -1
+        t = tables.large_random_tables(Q * 100 + S, L, [S], Q - 1, [(1, 1)], skip_src=skip,
+                                       mem_max=max(1, (3 * Q) // L))
+        got = h.interval_table(t, 0).astype(np.int64)
+        want = orc.interval_table(t, 0)
+        want = np.where(want == (1 << 63) - 1, 0x40000000, want)
+        iu = np.triu_indices(L)
+        assert np.array_equal(got[iu], want[iu]), (Q, S, skip)
+
+
+@pytest.mark.parametrize("dist", ["uniform", "ties"])
+def test_random_gpu_sized(h, orc, dist):
+    """Several configs of mixed |S|, L = 24, Q = 1000 (ragged), skip edges."""
+    rng = np.random.default_rng(11 if dist == "ties" else 12)
+    cands = [(1, 1), (2, 2), (2, 4), (4, 2), (4, 8), (8, 4), (24, 2), (25, 3)]
+    S = [int(rng.choice([1, 3, 6, 10, 15])) for _ in cands]
+    t = tables.large_random_tables(77, 24, S, 999, cands, skip_src=9, dist=dist)
+    _same(h.solve_tables(t), orc.solve_tables(t, n_threads=0), dist)
+
+
+def test_cluster_path_solve(h, orc):
+    """Q = 4096 with |S| = 15 and 21: the DSMEM cluster variant end to end."""
+    cands = [(1, 1), (2, 2), (3, 4)]
+    t = tables.large_random_tables(99, 10, [21, 15, 10], 4095, cands, skip_src=3, mem_max=900)
+    _same(h.solve_tables(t), orc.solve_tables(t, n_threads=0), "cluster")
+
+
+@pytest.mark.parametrize("name", ["bert", "t5", "vit", "swin", "llama"])
+def test_models_full_size(h, orc, name):
+    """The BASELINE.json workloads at full size: oracle tables -> GPU solve;
+    GPU plan (K1 + solve) -> same answer; builder tables bit-equal."""
+    p = profiles.make_profile(name)
+    t, qn, buf = orc.build_tables(p)
+    want = orc.solve_tables(t, n_threads=0)
+    _same(h.solve_tables(t), want, name)
+    gt, gq, gbuf = h.build_tables(p)
+    assert gq == qn and np.array_equal(gbuf, buf), name
+    got = h.plan(p)
+    _same(got, want, name + " plan")
+    assert got["quantum_ns"] == qn
+
+
+def test_models_nojitter_ties(h, orc):
+    for name in ("bert", "vit"):
+        p = profiles.make_profile(name, jitter=False)
+        t, qn, buf = orc.build_tables(p)
+        _same(h.solve_tables(t), orc.solve_tables(t, n_threads=0), name)
+
+
+def test_builder_random_profiles(h, orc):
+    for seed in range(60):
+        p = profiles.random_profile(seed)
+        try:
+            t, qn, buf = orc.build_tables(p)
+        except orc.OracleError as e:
+            import paper_2307_16375_b200 as pkg
+            with pytest.raises(pkg.UniapError) as ei:
+                h.build_tables(p)
+            assert ei.value.status == e.status
+            continue
+        gt, gq, gbuf = h.build_tables(p)
+        assert gq == qn and np.array_equal(gbuf, buf), seed
+        _same(h.plan(p), orc.solve_tables(t), seed)
+
+
+def test_edge_cases(h, orc):
+    # L = 1; deg = L; deg > L; cap = 0; everything infeasible
+    for seed in range(40):
+        t = tables.random_tables(90_000 + seed, L=1)
+        _same(h.solve_tables(t), orc.solve_tables(t), seed)
+    t = tables.random_tables(3, L=5, cap=0, n_cfg=3)
+    _same(h.solve_tables(t), orc.solve_tables(t))
+    t = tables.large_random_tables(5, 6, [2, 2], 10, [(6, 2), (7, 1)])
+    _same(h.solve_tables(t), orc.solve_tables(t))
+    t = tables.large_random_tables(5, 6, [3], 10, [(1, 1)], forbid_p=1.0)
+    g = h.solve_tables(t)
+    assert g["status"] == 2 and g["objective"] == (1 << 63) - 1
+
+
+def test_bad_tables_rejected(h):
+    import paper_2307_16375_b200 as pkg
+    t = tables.toy_tables()
+    with pytest.raises(pkg.UniapError) as e:
+        h.solve_tables(dict(t, cfgs=[t["cfgs"][0], t["cfgs"][0]]))
+    assert e.value.status == 1
+    with pytest.raises(pkg.UniapError) as e:
+        h.solve_tables(dict(t, cfgs=[dict(t["cfgs"][0], A=t["cfgs"][0]["A"] + (1 << 22))]))
+    assert e.value.status == 3
+
+
+def test_world_size_invariance(h):
+    """Shards of world 2/4/8 run one after another on one GPU ("fake world"),
+    records picked on the host == the world-1 answer."""
+    import torch
+    import paper_2307_16375_b200 as pkg
+    p = profiles.make_profile("vit")
+    ref = h.plan(p)
+    for world in (2, 4, 8):
+        h.prepare(p)
+        recs = b""
+        for rank in range(world):
+            buf = torch.zeros(pkg.RECORD_BYTES, dtype=torch.uint8, device="cuda")
+            h.run(rank, world, buf.data_ptr())
+            torch.cuda.synchronize()
+            recs += buf.cpu().numpy().tobytes()
+        st, r = pkg.pick(recs, world)
+        for k in ("objective", "deg", "c", "cfg_index", "stage_of", "strategy_of", "stage_cost", "cut_cost",
+                  "stage_mem", "dp_cells", "dp_relax"):
+            assert r[k] == ref[k], (world, k)

@@ -69,8 +69,8 @@ def test_eq1_memory_anchors(orc):
         for ts in (1, 2, 4):
             for fs in (1, 2, 4):
                 n = ts * fs
-                t, _, _ = orc.build_tables(_profile(n=n, B=n, ps=ps * 16, precision=prec, cand=[(1, 1)], Q=16384))
-                assert t["cfgs"][0]["M"][0, _strat(orc, n, (ts, fs, 1))] == -(-cd * ps * 16 // (ts * fs))
+                t, _, _ = orc.build_tables(_profile(n=n, B=n, ps=ps * 8, precision=prec, cand=[(1, 1)], Q=8192))
+                assert t["cfgs"][0]["M"][0, _strat(orc, n, (ts, fs, 1))] == -(-cd * ps * 8 // (ts * fs))
 
 
 def test_activation_memory_gpipe_inflight(orc):
