@@ -200,6 +200,9 @@ typedef struct {                      /* fixed-size record exchanged between ran
 /* Deterministic LPT assignment of the n_cfg candidates of the prepared
  * problem to `world` ranks: owner_out[i] = rank of candidate i.  Host only. */
 uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32_t* owner_out);
+/* The same assignment computed from the shapes of level-1 tables alone
+ * (host only, no handle or device). */
+uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world, int32_t* owner_out);
 
 /* Pick the winner among `world` host records by (objective, deg, c); fills
  * *out (cfg_objective untouched).  Host only (no device needed). */

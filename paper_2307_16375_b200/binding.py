@@ -82,7 +82,8 @@ RECORD_BYTES = C.sizeof(uniap_record)
 
 EXPORTS = ("uniap_create", "uniap_destroy", "uniap_last_error", "uniap_status_string", "uniap_version",
            "uniap_solve_tables", "uniap_interval_table", "uniap_plan", "uniap_build_tables", "uniap_prepare",
-           "uniap_prepare_tables", "uniap_run", "uniap_fetch", "uniap_shard_assign", "uniap_pick",
+           "uniap_prepare_tables", "uniap_run", "uniap_fetch", "uniap_shard_assign", "uniap_shard_tables",
+           "uniap_pick",
            "uniap_candidates", "uniap_catalogue")
 
 _lib = None
@@ -115,6 +116,7 @@ def lib():
         L.uniap_run.argtypes = [H, C.c_int32, C.c_int32, C.c_void_p]
         L.uniap_fetch.argtypes = [H, C.POINTER(uniap_result)]
         L.uniap_shard_assign.argtypes = [H, C.c_int32, _P32]
+        L.uniap_shard_tables.argtypes = [C.POINTER(uniap_tables), C.c_int32, _P32]
         L.uniap_pick.argtypes = [C.POINTER(uniap_record), C.c_int32, C.POINTER(uniap_result)]
         L.uniap_candidates.argtypes = [C.c_int32, C.c_int32, _P32, C.c_int32]
         L.uniap_catalogue.argtypes = [C.c_int32, _P32, C.c_int32]
@@ -213,6 +215,16 @@ def catalogue(g):
     buf = (C.c_int32 * (3 * max(k, 1)))()
     lib().uniap_catalogue(g, buf, k)
     return [tuple(buf[3 * i:3 * i + 3]) for i in range(k)]
+
+
+def shard_tables(t, world):
+    """LPT owner rank of every config of level-1 tables (host only)."""
+    tb, keep = _tables(t)
+    owner = (C.c_int32 * len(t["cfgs"]))()
+    st = lib().uniap_shard_tables(C.byref(tb), world, owner)
+    if st != UNIAP_OK:
+        raise UniapError(st, "shard_tables")
+    return list(owner)
 
 
 def pick(records: bytes, world: int):

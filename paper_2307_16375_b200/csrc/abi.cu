@@ -448,40 +448,46 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
 // be a stage of a deg-stage ordered placement (a >= stages before it, enough
 // layers after it); with the skip source inside the sweep, one copy per
 // strategy ks of the skip source (Eq. 3 couples it with later layers).
-static void forward_instances(const uniap_handle* h, int i, bool all_intervals, std::vector<Inst>& out) {
-  const CfgDev& d = h->cfg[i];
-  const int L = h->L;
-  if (!all_intervals && d.deg > L) return;
+static void plan_instances(int L, int i, int deg, int S, int skip, bool all_intervals, std::vector<Inst>& out) {
+  if (!all_intervals && deg > L) return;
   for (int a = 0; a < L; ++a) {
     int bmax;
     if (all_intervals) bmax = L - 1;
-    else if (d.deg == 1) { if (a > 0) break; bmax = L - 1; }
-    else bmax = L - 1 - d.deg + std::min(a + 1, d.deg);
+    else if (deg == 1) { if (a > 0) break; bmax = L - 1; }
+    else bmax = L - 1 - deg + std::min(a + 1, deg);
     if (bmax < a) continue;
     const int n = bmax - a + 1;
-    if (d.skip >= 0 && a <= d.skip && bmax >= d.skip + 2) {
-      for (int ks = 0; ks < d.S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0});
+    if (skip >= 0 && a <= skip && bmax >= skip + 2) {
+      for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0});
     } else {
       out.push_back(Inst{i, a, n, -1, +1, 1, 0});
     }
   }
 }
 
-static double config_work(const uniap_handle* h, int i) {
-  std::vector<Inst> v;
-  forward_instances(h, i, false, v);
-  double w = 0;
-  for (auto& x : v) w += (double)x.n * h->cfg[i].S * h->cfg[i].S * h->Q;
-  return w + 1.0;  // + the combine
+static void forward_instances(const uniap_handle* h, int i, bool all_intervals, std::vector<Inst>& out) {
+  const CfgDev& d = h->cfg[i];
+  plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, out);
 }
 
-static void lpt(const uniap_handle* h, int world, std::vector<int>& owner) {
-  std::vector<int> order(h->ncfg);
-  std::vector<double> w(h->ncfg);
-  for (int i = 0; i < h->ncfg; ++i) { order[i] = i; w[i] = config_work(h, i); }
+// LPT over configs by chain-DP work (sum over instances of n |S|^2 Q); ties
+// keep the candidate order, the least-loaded (then lowest) rank takes the next.
+static void lpt_shapes(int L, int Q, const std::vector<int>& deg, const std::vector<int>& S,
+                       const std::vector<int>& skip, int world, std::vector<int>& owner) {
+  const int n = (int)deg.size();
+  std::vector<int> order(n);
+  std::vector<double> w(n);
+  for (int i = 0; i < n; ++i) {
+    std::vector<Inst> v;
+    plan_instances(L, i, deg[i], S[i], skip[i], false, v);
+    double x = 1.0;  // + the combine
+    for (auto& e : v) x += (double)e.n * S[i] * S[i] * Q;
+    order[i] = i;
+    w[i] = x;
+  }
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return w[a] > w[b]; });
   std::vector<double> load(world, 0.0);
-  owner.assign(h->ncfg, 0);
+  owner.assign(n, 0);
   for (int i : order) {
     int r = 0;
     for (int k = 1; k < world; ++k)
@@ -489,6 +495,25 @@ static void lpt(const uniap_handle* h, int world, std::vector<int>& owner) {
     owner[i] = r;
     load[r] += w[i];
   }
+}
+
+static void lpt(const uniap_handle* h, int world, std::vector<int>& owner) {
+  std::vector<int> deg(h->ncfg), S(h->ncfg), sk(h->ncfg);
+  for (int i = 0; i < h->ncfg; ++i) { deg[i] = h->cfg[i].deg; S[i] = h->cfg[i].S; sk[i] = h->cfg[i].skip; }
+  lpt_shapes(h->L, h->Q, deg, S, sk, world, owner);
+}
+
+extern "C" uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world, int32_t* owner_out) {
+  if (!t || !t->cfg || !owner_out || world < 1 || t->n_cfg < 1 || t->L < 1) return UNIAP_ERR_ARG;
+  std::vector<int> deg(t->n_cfg), S(t->n_cfg), sk(t->n_cfg), owner;
+  for (int i = 0; i < t->n_cfg; ++i) {
+    deg[i] = t->cfg[i].deg;
+    S[i] = t->cfg[i].n_strat;
+    sk[i] = (t->cfg[i].Rskip && t->skip_src >= 0) ? t->skip_src : -1;
+  }
+  lpt_shapes(t->L, t->cap + 1, deg, S, sk, world, owner);
+  for (int i = 0; i < t->n_cfg; ++i) owner_out[i] = owner[i];
+  return UNIAP_OK;
 }
 
 extern "C" uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32_t* owner_out) {
