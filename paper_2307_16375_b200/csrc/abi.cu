@@ -75,6 +75,9 @@ struct uniap_handle {
   uint64_t h2d = 0, d2h = 0;
   uint32_t launches = 0, k2_launches = 0;
   const uniap_record* last_rec = nullptr;  // where the last run wrote its record
+  std::vector<cudaStream_t> side;          // K2 classes run concurrently
+  std::vector<cudaEvent_t> side_ev;
+  cudaEvent_t fork_ev = nullptr;
 };
 
 // every host<->device copy goes through these (counted for the e2e report)
@@ -175,6 +178,7 @@ extern "C" uniap_status uniap_create(uniap_handle** out, int device, void* strea
   }
   for (auto& e : h->ev)
     if (cudaEventCreate(&e) != cudaSuccess) { delete h; return UNIAP_ERR_CUDA; }
+  if (cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming) != cudaSuccess) { delete h; return UNIAP_ERR_CUDA; }
   *out = h;
   return UNIAP_OK;
 }
@@ -195,6 +199,9 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   h->rec.release();
   for (auto e : h->ev)
     if (e) cudaEventDestroy(e);
+  for (auto e : h->side_ev) cudaEventDestroy(e);
+  for (auto x : h->side) cudaStreamDestroy(x);
+  if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   if (h->own_stream) cudaStreamDestroy(h->st);
   delete h;
 }
@@ -544,17 +551,46 @@ static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, De
   CK(h, buf.ensure(sorted.size()));
   if (!sorted.empty())
     CK(h, h2d(h, buf.p, sorted.data(), sorted.size() * sizeof(Inst)));
-  size_t s = 0;
-  while (s < sorted.size()) {
+  // one launch per class; classes run concurrently on side streams (fork /
+  // join with events) so small classes fill the tail of the heavy one
+  struct Grp { size_t s, e; double work; };
+  std::vector<Grp> grp;
+  for (size_t s = 0; s < sorted.size();) {
     size_t e = s;
     const int id = clsid[idx[s]];
-    while (e < sorted.size() && clsid[idx[e]] == id) ++e;
-    K2Args args{buf.p + s, h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip};
-    CK(h, k2_launch(h->cls[sorted[s].cfg], args, (int)(e - s), h->st));
-    h->launches++;
-    h->k2_launches++;
+    double w = 0;
+    while (e < sorted.size() && clsid[idx[e]] == id) {
+      const int S = h->cfg[sorted[e].cfg].S;
+      w += (double)sorted[e].n * S * S * h->Q;
+      ++e;
+    }
+    grp.push_back(Grp{s, e, w});
     s = e;
   }
+  std::stable_sort(grp.begin(), grp.end(), [](const Grp& a, const Grp& b) { return a.work > b.work; });
+  const bool fork = grp.size() > 1;
+  if (fork) {
+    while (h->side.size() < grp.size()) {
+      cudaStream_t x;
+      cudaEvent_t ev;
+      CK(h, cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+      CK(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      h->side.push_back(x);
+      h->side_ev.push_back(ev);
+    }
+    CK(h, cudaEventRecord(h->fork_ev, h->st));
+  }
+  for (size_t g = 0; g < grp.size(); ++g) {
+    cudaStream_t st = fork ? h->side[g] : h->st;
+    if (fork) CK(h, cudaStreamWaitEvent(st, h->fork_ev, 0));
+    K2Args args{buf.p + grp[g].s, h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip};
+    CK(h, k2_launch(h->cls[sorted[grp[g].s].cfg], args, (int)(grp[g].e - grp[g].s), st));
+    h->launches++;
+    h->k2_launches++;
+    if (fork) CK(h, cudaEventRecord(h->side_ev[g], st));
+  }
+  if (fork)
+    for (size_t g = 0; g < grp.size(); ++g) CK(h, cudaStreamWaitEvent(h->st, h->side_ev[g], 0));
   return UNIAP_OK;
 }
 
