@@ -217,7 +217,7 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<int>& S, c
   int64_t off = 0;
   for (int i = 0; i < h->ncfg; ++i) {
     K2Class k;
-    if (!k2_pick_class(S[i], h->Q, &k)) FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
+    if (!k2_pick_class(S[i], h->Q, deg[i] == 1, &k)) FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
     h->cls[i] = k;
     CfgDev& d = h->cfg[i];
     const int NSP = round4(k.NS);
@@ -553,21 +553,23 @@ static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, De
     CK(h, h2d(h, buf.p, sorted.data(), sorted.size() * sizeof(Inst)));
   // one launch per class; classes run concurrently on side streams (fork /
   // join with events) so small classes fill the tail of the heavy one
-  struct Grp { size_t s, e; double work; };
+  // launch order: longest critical path first (the serial chain of one
+  // instance: layers x per-CTA work of a layer), so it starts on free SMs
+  struct Grp { size_t s, e; double crit; };
   std::vector<Grp> grp;
   for (size_t s = 0; s < sorted.size();) {
     size_t e = s;
     const int id = clsid[idx[s]];
-    double w = 0;
+    double c = 0;
     while (e < sorted.size() && clsid[idx[e]] == id) {
-      const int S = h->cfg[sorted[e].cfg].S;
-      w += (double)sorted[e].n * S * S * h->Q;
+      const K2Class& k = h->cls[sorted[e].cfg];
+      c = std::max(c, (double)sorted[e].n * k.NS * k.NS * k.T * k.V);
       ++e;
     }
-    grp.push_back(Grp{s, e, w});
+    grp.push_back(Grp{s, e, c});
     s = e;
   }
-  std::stable_sort(grp.begin(), grp.end(), [](const Grp& a, const Grp& b) { return a.work > b.work; });
+  std::stable_sort(grp.begin(), grp.end(), [](const Grp& a, const Grp& b) { return a.crit > b.crit; });
   const bool fork = grp.size() > 1;
   if (fork) {
     while (h->side.size() < grp.size()) {

@@ -5,12 +5,12 @@
 
 namespace uniap {
 
-#define UNIAP_NS_LIST(X) X(1) X(2) X(3) X(4) X(6) X(8) X(10) X(12) X(15) X(16) X(21) X(24) X(28) X(32)
-#define UNIAP_EXTERN(N) extern template k2_fn k2_get<N>(int, int, bool, bool);
+#define UNIAP_NS_LIST(X) X(1) X(2) X(3) X(4) X(6) X(8) X(10) X(12) X(15) X(16) X(21) X(24) X(32)
+#define UNIAP_EXTERN(N) extern template k2_fn k2_get<N>(int, int, bool);
 UNIAP_NS_LIST(UNIAP_EXTERN)
 #undef UNIAP_EXTERN
 
-static const int kNS[] = {1, 2, 3, 4, 6, 8, 10, 12, 15, 16, 21, 24, 28, 32};
+static const int kNS[] = {1, 2, 3, 4, 6, 8, 10, 12, 15, 16, 21, 24, 32};
 
 int k2_ns_round(int S) {
   for (int n : kNS)
@@ -18,35 +18,44 @@ int k2_ns_round(int S) {
   return -1;
 }
 
-size_t k2_smem_bytes(const K2Class& c) {
-  return (size_t)(c.DB ? 2 : 1) * c.NS * (c.T * c.V + 4) * sizeof(int32_t);
+static size_t smem_words(int NS, int B) {
+  const int NSP = (NS + 3) & ~3;
+  return (size_t)2 * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP);
+}
+
+size_t k2_smem_bytes(const K2Class& c) { return smem_words(c.NS, c.T * c.V) * sizeof(int32_t); }
+
+static int pow2ceil(int x) {
+  int p = 1;
+  while (p < x) p *= 2;
+  return p;
 }
 
 // Shape of the chain DP for |S| strategies and Q = cap+1 buckets.
-//  Q <= 1024: one CTA per instance, B = T*V >= Q buckets per CTA.
-//  larger Q : a thread-block cluster of C CTAs splits the bucket axis
-//             (B = 1024 per CTA), except for small |S| where one 512-thread
-//             CTA holds 4096 buckets (8 per thread) in registers.
-// E is double-buffered (one barrier per layer) whenever it fits in 200 KB.
-bool k2_pick_class(int S, int Q, K2Class* out) {
-  int NS = k2_ns_round(S);
+// A CTA holds B = T*V buckets (V = 2 per thread, up to 512 threads) with E
+// double-buffered in shared memory (<= 200 KB); larger Q splits the bucket
+// axis over a thread-block cluster of C CTAs (DSMEM for the shifted reads).
+// A single long chain (deg = 1) is spread over a cluster of up to 8 CTAs
+// (B >= 128) even when it would fit one CTA: its critical path is serial in
+// the layers, so more SMs per step shorten it.  Small |S| with large Q keep
+// 8 buckets per thread in one 512-thread CTA (B = 4096).
+bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
+  const int NS = k2_ns_round(S);
   if (NS < 0 || Q < 1 || Q > UNIAP_MAX_Q) return false;
-  K2Class c{NS, 4, 256, 1, true};
-  if (Q <= 32) { c.V = 1; c.T = 32; }
-  else if (Q <= 64) { c.V = 2; c.T = 32; }
-  else if (Q <= 128) { c.V = 4; c.T = 32; }
-  else if (Q <= 256) { c.V = 4; c.T = 64; }
-  else if (Q <= 512) { c.V = 4; c.T = 128; }
-  else if (Q <= 1024) { c.V = 4; c.T = 256; }
-  else if (NS <= 6 && Q > 2048) { c.V = 8; c.T = 512; c.C = (Q + 4095) / 4096; }
-  else {
-    c.V = 4; c.T = 256;
-    int need = (Q + 1023) / 1024;
-    c.C = 1;
-    while (c.C < need) c.C *= 2;
-  }
-  c.DB = k2_smem_bytes(K2Class{NS, c.V, c.T, c.C, true}) <= 200 * 1024;
-  if (c.T == 256 && c.V == 4) c.DB = (NS <= 24);
+  int Bmax = 1024;
+  while (Bmax > 32 && smem_words(NS, Bmax) * 4 > 200 * 1024) Bmax /= 2;
+  if (NS <= 6 && Q > 2048 && !single) Bmax = 4096;
+  int B = std::min(Bmax, std::max(32, pow2ceil(Q)));
+  int C = pow2ceil((Q + B - 1) / B);
+  if (single)
+    while (C < 8 && B > 128) {
+      B /= 2;
+      C = pow2ceil((Q + B - 1) / B);
+    }
+  if (C > 16) return false;
+  K2Class c{NS, 2, B / 2, C};
+  if (B == 32) { c.V = 1; c.T = 32; }
+  if (B == 4096) { c.V = 8; c.T = 512; }
   *out = c;
   return true;
 }
@@ -55,7 +64,7 @@ static k2_fn k2_lookup(const K2Class& c) {
   const bool CL = c.C > 1;
   switch (c.NS) {
 #define UNIAP_CASE(N) \
-  case N: return k2_get<N>(c.V, c.T, CL, c.DB);
+  case N: return k2_get<N>(c.V, c.T, CL);
     UNIAP_NS_LIST(UNIAP_CASE)
 #undef UNIAP_CASE
     default: return nullptr;
@@ -68,7 +77,7 @@ cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStre
   if (!fn) return cudaErrorInvalidDeviceFunction;
   const size_t smem = k2_smem_bytes(c);
   {
-    // raise the dynamic shared-memory limit once per kernel
+    // raise the dynamic shared-memory limit (and allow 16-CTA clusters) once per kernel
     static std::mutex mu;
     static std::vector<k2_fn> done;
     std::lock_guard<std::mutex> g(mu);
@@ -76,6 +85,8 @@ cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStre
     for (auto f : done) seen |= (f == fn);
     if (!seen) {
       cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
       done.push_back(fn);
     }

@@ -15,14 +15,16 @@
 //
 // Mapping (sm_100a): a CTA (or a thread-block cluster of C CTAs splitting the
 // bucket axis) owns one instance.  Thread t of CTA r owns buckets
-// q = r*B + j*T + t (j < V): D lives in REGISTERS, the E-step is
-// register-only with one DPX VIADDMNMX per relaxation (__viaddmin_s32), R is a
-// warp-uniform broadcast load reused across the V buckets, E goes to shared
-// memory (double-buffered: one barrier per layer) so the shifted read
-// E[k][q-M] -- a warp-uniform shift -- is bank-conflict-free.  A guard word
-// (INF) before every row turns q < M into a clamped read.  In a cluster the
-// shifted read may cross to the previous CTA's bucket range: DSMEM
-// (ld.shared::cluster) on that path only.
+// q = r*B + j*T + t (j < V): D lives in REGISTERS and the E-step is
+// register-only: one DPX VIADDMNMX (__viaddmin_s32) per relaxation, two
+// destination rows at a time (2V independent chains).  The step's R rows and
+// A'/M rows are staged in shared memory one step ahead by the whole CTA (a
+// broadcast LDS.128 per 4 sources; no L1 dependence, which a cluster barrier
+// flushes).  E goes to shared memory, double-buffered, so each layer costs one
+// barrier; the shifted read E[k][q-M] (M warp-uniform) is bank-conflict-free
+// and a guard word (INF) before every row turns q < M into a clamped read.
+// In a cluster the shifted read may fall in a lower CTA's bucket range:
+// DSMEM (ld.shared::cluster) on that path only.
 #pragma once
 #include "uniap_impl.h"
 
@@ -50,45 +52,43 @@ __device__ __forceinline__ int32_t ld_dsmem(const int32_t* p, uint32_t rank) {
   asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
   return v;
 }
-
-template <int NSP>
-__device__ __forceinline__ void load_row(int32_t (&r)[NSP], const int32_t* __restrict__ p) {
-  const int4* p4 = reinterpret_cast<const int4*>(p);
-#pragma unroll
-  for (int i = 0; i < NSP / 4; ++i) {
-    int4 x = __ldg(p4 + i);
-    r[4 * i] = x.x;
-    r[4 * i + 1] = x.y;
-    r[4 * i + 2] = x.z;
-    r[4 * i + 3] = x.w;
-  }
+__device__ __forceinline__ int4 lds128(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ int2 lds64(uint32_t addr) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ int32_t lds32(uint32_t addr) {
+  int32_t v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
 }
 
-// E[k][.] for one destination strategy k: V independent VIADDMNMX chains of length NS.
-template <int NS, int V, int T, int NSP, int ROW>
-__device__ __forceinline__ void estep_k(const int32_t (&d)[NS][V], const int32_t (&r)[NSP], int32_t* E, int k) {
-  int32_t acc[V];
-#pragma unroll
-  for (int j = 0; j < V; ++j) acc[j] = INF;
-#pragma unroll
-  for (int kp = 0; kp < NS; ++kp)
-#pragma unroll
-    for (int j = 0; j < V; ++j) acc[j] = addmin(d[kp][j], r[kp], acc[j]);
-  int32_t* e = E + k * ROW;
-#pragma unroll
-  for (int j = 0; j < V; ++j) e[j * T] = acc[j];
-}
+__device__ __forceinline__ int comp(const int4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
-template <int NS, int V, int T, bool CL, bool DB>
+// Shared-memory words of one "table stage" (the tables of one layer step):
+// R rows [NS][NSP], then (A', M) pairs [NSP].
+template <int NS>
+struct Stage {
+  static constexpr int NSP = (NS + 3) & ~3;
+  static constexpr int WORDS = NS * NSP + 2 * NSP;
+};
+
+template <int NS, int V, int T, bool CL>
 __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   constexpr int B = T * V;          // buckets per CTA
   constexpr int ROW = B + 4;        // 4 guard words + B buckets
-  constexpr int NSP = (NS + 3) & ~3;
-  constexpr int NB = DB ? 2 : 1;
+  constexpr int NSP = Stage<NS>::NSP;
+  constexpr int SW = Stage<NS>::WORDS;
   constexpr int KUNROLL = 8;
   constexpr int MBIG = UNIAP_MAX_Q * 2 + 1;  // > every bucket index: "never fits"
   extern __shared__ int4 smem4[];
-  int32_t* sE = reinterpret_cast<int32_t*>(smem4);
+  int32_t* sE = reinterpret_cast<int32_t*>(smem4);  // [2][NS][ROW]
+  int32_t* sT = sE + 2 * NS * ROW;                  // [3][SW] staged tables
   const int t = threadIdx.x;
   int rank = 0, ii = blockIdx.x;
   if constexpr (CL) {
@@ -102,33 +102,46 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   const int32_t* __restrict__ gR = args.arena + (in.dir > 0 ? cf.offRt : cf.offRf);
   const int32_t* __restrict__ gRs = args.arena + cf.offRs;
   const int skip = cf.skip, ks = in.ks, cap = args.cap;
+  const int Q = cap + 1;
+  const int L = args.L;
 
-  for (int r = t; r < NB * NS; r += T) *reinterpret_cast<int4*>(sE + r * ROW) = make_int4(INF, INF, INF, INF);
+  for (int r = t; r < 2 * NS; r += T) *reinterpret_cast<int4*>(sE + r * ROW) = make_int4(INF, INF, INF, INF);
 
-  // A'[u][k] (execution cost + skip-edge term when conditioned) and M[u][k];
-  // a strategy excluded by the conditioning gets an unreachable memory.
-  int32_t Ak[NSP], Mk[NSP];
-  auto load_layer = [&](int u) {
-    load_row<NSP>(Ak, gA + (int64_t)u * NSP);
-    load_row<NSP>(Mk, gM + (int64_t)u * NSP);
+  // ---- tables of one layer step, staged by the whole CTA ----------------
+  // word w of a stage: R rows (w < NS*NSP), then (A', M) pairs.  A' adds the
+  // skip-edge term of Eq. 3 when the instance conditions the skip source;
+  // strategies excluded by that conditioning get an unreachable memory.
+  constexpr int PER = (SW + T - 1) / T;
+  auto stage_word = [&](int u, int e, int w) -> int32_t {
+    if (w < NS * NSP) return __ldg(gR + (int64_t)e * NSP * NSP + w);
+    const int x = w - NS * NSP, k = x >> 1;
+    if (x & 1) {
+      int32_t m = min(__ldg(gM + (int64_t)u * NSP + k), MBIG);
+      if (ks >= 0 && u == skip && k != ks) m = MBIG;
+      return m;
+    }
+    int32_t a = __ldg(gA + (int64_t)u * NSP + k);
+    if (ks >= 0 && u >= skip + 2) a += __ldg(gRs + ((int64_t)u * NSP + ks) * NSP + k);
+    return a;
+  };
+  int32_t pre[PER];
+  auto fetch_stage = [&](int step, int u_next) {  // global -> registers (issued early)
+    const int e = in.dir > 0 ? u_next - 1 : u_next;
 #pragma unroll
-    for (int k = 0; k < NSP; ++k) Mk[k] = min(Mk[k], MBIG);
-    if (ks >= 0) {
-      if (u >= skip + 2) {
-        int32_t rs[NSP];
-        load_row<NSP>(rs, gRs + ((int64_t)u * NSP + ks) * NSP);
+    for (int i = 0; i < PER; ++i) {
+      const int w = t + i * T;
+      pre[i] = (w < SW && step < in.n) ? stage_word(u_next, e, w) : 0;
+    }
+  };
+  auto store_stage = [&](int step) {  // registers -> shared (before the barrier)
+    int32_t* dst = sT + (step % 3) * SW;
 #pragma unroll
-        for (int k = 0; k < NSP; ++k) Ak[k] += rs[k];
-      } else if (u == skip) {
-#pragma unroll
-        for (int k = 0; k < NSP; ++k)
-          if (k != ks) Mk[k] = MBIG;
-      }
+    for (int i = 0; i < PER; ++i) {
+      const int w = t + i * T;
+      if (w < SW) dst[w] = pre[i];
     }
   };
 
-  const int Q = cap + 1;
-  const int L = args.L;
   int32_t d[NS][V];
   auto emit = [&](int u) {
     if (in.dir > 0) {
@@ -160,81 +173,132 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     }
   };
 
+  // ---- first layer ----
   int u = in.a;
-  load_layer(u);
+  {
 #pragma unroll
-  for (int k = 0; k < NS; ++k)
+    for (int k = 0; k < NS; ++k) {
+      int32_t a = __ldg(gA + (int64_t)u * NSP + k);
+      int32_t m = min(__ldg(gM + (int64_t)u * NSP + k), MBIG);
+      if (ks >= 0) {
+        if (u >= skip + 2) a += __ldg(gRs + ((int64_t)u * NSP + ks) * NSP + k);
+        if (u == skip && k != ks) m = MBIG;
+      }
 #pragma unroll
-    for (int j = 0; j < V; ++j) d[k][j] = (rank * B + j * T + t >= Mk[k]) ? Ak[k] : INF;
+      for (int j = 0; j < V; ++j) d[k][j] = (rank * B + j * T + t >= m) ? a : INF;
+    }
+  }
+  fetch_stage(1, u + in.dir);
+  store_stage(1);
+  if (in.n > 2) fetch_stage(2, u + 2 * in.dir);
+  __syncthreads();
   emit(u);
 
   for (int step = 1; step < in.n; ++step) {
-    const int up = u;
     u += in.dir;
-    const int e = in.dir > 0 ? up : u;  // chain edge between the two layers
-    const int32_t* __restrict__ Rm = gR + (int64_t)e * NSP * NSP;
-    int32_t* Eb = sE + (DB ? (step & 1) * NS * ROW : 0) + 4;
-    // ---- E-step: registers only ----
+    int32_t* Eb = sE + (step & 1) * NS * ROW + 4;          // row 0, bucket 0
+    const int32_t* Tb = sT + (step % 3) * SW;
+    // ---- E-step: registers only; R broadcast from shared memory ----
     {
       int32_t* Et = Eb + t;
+      auto two_rows = [&](int k) {  // destination rows k, k+1
+        int32_t a0[V], a1[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) a0[j] = a1[j] = INF;
+        const int4* r0 = reinterpret_cast<const int4*>(Tb + k * NSP);
+        const int4* r1 = reinterpret_cast<const int4*>(Tb + (k + 1) * NSP);
+#pragma unroll
+        for (int c = 0; c < NSP / 4; ++c) {
+          const int4 x = r0[c];
+          const int4 y = r1[c];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (4 * c + i < NS)
+#pragma unroll
+              for (int j = 0; j < V; ++j) {
+                a0[j] = addmin(d[4 * c + i][j], comp(x, i), a0[j]);
+                a1[j] = addmin(d[4 * c + i][j], comp(y, i), a1[j]);
+              }
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          Et[k * ROW + j * T] = a0[j];
+          Et[(k + 1) * ROW + j * T] = a1[j];
+        }
+      };
+      auto one_row = [&](int k) {
+        int32_t a0[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) a0[j] = INF;
+        const int4* r0 = reinterpret_cast<const int4*>(Tb + k * NSP);
+#pragma unroll
+        for (int c = 0; c < NSP / 4; ++c) {
+          const int4 x = r0[c];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (4 * c + i < NS)
+#pragma unroll
+              for (int j = 0; j < V; ++j) a0[j] = addmin(d[4 * c + i][j], comp(x, i), a0[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) Et[k * ROW + j * T] = a0[j];
+      };
       if constexpr (NS <= KUNROLL) {
 #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          int32_t r[NSP];
-          load_row<NSP>(r, Rm + k * NSP);
-          estep_k<NS, V, T, NSP, ROW>(d, r, Et, k);
-        }
+        for (int k = 0; k + 1 < NS; k += 2) two_rows(k);
       } else {
-        int32_t ra[NSP], rb[NSP];
-        load_row<NSP>(ra, Rm);
 #pragma unroll 1
-        for (int k = 0; k < NS; k += 2) {
-          if (k + 1 < NS) load_row<NSP>(rb, Rm + (k + 1) * NSP);
-          estep_k<NS, V, T, NSP, ROW>(d, ra, Et, k);
-          if (k + 1 < NS) {
-            if (k + 2 < NS) load_row<NSP>(ra, Rm + (k + 2) * NSP);
-            estep_k<NS, V, T, NSP, ROW>(d, rb, Et, k + 1);
-          }
-        }
+        for (int k = 0; k + 1 < NS; k += 2) two_rows(k);
       }
+      if constexpr (NS % 2) one_row(NS - 1);
     }
-    load_layer(u);
+    // stage the tables of the step after next, then one barrier per layer
+    if (step + 1 < in.n) store_stage(step + 1);
+    if (step + 2 < in.n) fetch_stage(step + 2, u + 2 * in.dir);
     if constexpr (CL) cl_sync();
     else __syncthreads();
     // ---- shift by the layer's memory, add A' ----
     // Byte addresses in the shared window: row k's bucket x sits at
     // rowb_k + 4x; x < 0 is clamped onto the guard word at rowb_k - 4 by one
     // VIADDMNMX (max form), so a cell costs VIADDMNMX + LDS + VIADDMNMX.
-    {
-      const int32_t sb = (int32_t)__cvta_generic_to_shared(Eb);
+    const char* Ec = reinterpret_cast<const char*>(Eb);
 #pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const int32_t rowb = sb + k * ROW * 4;
-        const int32_t bk = rowb + (t - Mk[k]) * 4;
-        const int32_t gk = rowb - 4;
+    for (int k = 0; k < NS; ++k) {
+      const int2 am = *reinterpret_cast<const int2*>(Tb + NS * NSP + 2 * k);
+      const int32_t bk = (k * ROW + t - am.y) * 4;  // byte offset of bucket t - M in row k
+      const int32_t gk = k * ROW * 4 - 4;          // the row's guard word
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-          const int32_t addr = __viaddmax_s32(bk, j * T * 4, gk);
-          int32_t ev;
-          asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ev) : "r"(addr) : "memory");
-          if constexpr (CL) {
-            const int lx = j * T + t - Mk[k];
-            if (lx < 0) {
+      for (int j = 0; j < V; ++j)
+        d[k][j] = addmin(*reinterpret_cast<const int32_t*>(Ec + __viaddmax_s32(bk, j * T * 4, gk)), am.x, INF);
+    }
+    if constexpr (CL) {
+      // buckets whose shifted source q - M lies in a lower CTA's range: the
+      // local read above returned the guard (INF); fetch the value over DSMEM
+      if (rank > 0) {
+        const int wbase = t & ~31;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const int2 am = *reinterpret_cast<const int2*>(Tb + NS * NSP + 2 * k);
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            if (j * T + wbase < am.y) {  // warp-uniform: some lane reads a lower CTA
+              const int lx = j * T + t - am.y;
               const int x = lx + rank * B;
-              if (x >= 0) ev = ld_dsmem(Eb + k * ROW + (x & (B - 1)), (uint32_t)(x / B));
+              if (lx < 0 && x >= 0)
+                d[k][j] = addmin(ld_dsmem(Eb + k * ROW + (x & (B - 1)), (uint32_t)(x / B)), am.x, INF);
             }
           }
-          d[k][j] = addmin(ev, Ak[k], INF);
         }
       }
-    }
-    if constexpr (!DB) {
-      if constexpr (CL) cl_sync();
-      else __syncthreads();
     }
     emit(u);
   }
   if constexpr (CL) cl_sync();  // keep this CTA's E alive for remote readers
+}
+
+template <int NS>
+constexpr size_t k2_smem(int B) {
+  return (size_t)(2 * NS * (B + 4) + 3 * Stage<NS>::WORDS) * sizeof(int32_t);
 }
 
 // Instantiation helper used by the per-NS translation units: only the shapes
@@ -242,23 +306,22 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
 typedef void (*k2_fn)(const K2Args);
 
 template <int NS>
-k2_fn k2_get(int V, int T, bool CL, bool DB) {
-  if (!CL && DB) {
-    if (V == 1 && T == 32) return k2_chain<NS, 1, 32, false, true>;
-    if (V == 2 && T == 32) return k2_chain<NS, 2, 32, false, true>;
-    if (V == 4 && T == 32) return k2_chain<NS, 4, 32, false, true>;
-    if (V == 4 && T == 64) return k2_chain<NS, 4, 64, false, true>;
-    if (V == 4 && T == 128) return k2_chain<NS, 4, 128, false, true>;
+k2_fn k2_get(int V, int T, bool CL) {
+#define UNIAP_SHAPE(VV, TT)                                                 \
+  if (V == VV && T == TT) {                                                 \
+    if constexpr (k2_smem<NS>(VV * TT) <= 200 * 1024)                       \
+      return CL ? k2_chain<NS, VV, TT, true> : k2_chain<NS, VV, TT, false>; \
+    return nullptr;                                                         \
   }
-  if (V == 4 && T == 256) {
-    if constexpr (NS <= 24) {
-      if (DB) return CL ? k2_chain<NS, 4, 256, true, true> : k2_chain<NS, 4, 256, false, true>;
-    } else {
-      if (!DB) return CL ? k2_chain<NS, 4, 256, true, false> : k2_chain<NS, 4, 256, false, false>;
-    }
-  }
+  if (V == 1 && T == 32) return CL ? nullptr : k2_chain<NS, 1, 32, false>;
+  UNIAP_SHAPE(2, 32)
+  UNIAP_SHAPE(2, 64)
+  UNIAP_SHAPE(2, 128)
+  UNIAP_SHAPE(2, 256)
+  UNIAP_SHAPE(2, 512)
+#undef UNIAP_SHAPE
   if constexpr (NS <= 6) {
-    if (V == 8 && T == 512 && DB) return CL ? k2_chain<NS, 8, 512, true, true> : k2_chain<NS, 8, 512, false, true>;
+    if (V == 8 && T == 512) return CL ? k2_chain<NS, 8, 512, true> : k2_chain<NS, 8, 512, false>;
   }
   return nullptr;
 }

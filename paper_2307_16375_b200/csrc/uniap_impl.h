@@ -59,11 +59,12 @@ struct K2Class {
   int V;       // buckets per thread
   int T;       // threads per CTA
   int C;       // CTAs per cluster
-  bool DB;     // double-buffered E
 };
 
 // chain_dp.cu
-bool k2_pick_class(int S, int Q, K2Class* out);
+// single = the config has one long chain (deg = 1): spread its buckets over
+// more SMs (a wider cluster) to shorten the critical path.
+bool k2_pick_class(int S, int Q, bool single, K2Class* out);
 int k2_ns_round(int S);
 size_t k2_smem_bytes(const K2Class& c);
 cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st);
