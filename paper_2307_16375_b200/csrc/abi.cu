@@ -59,7 +59,7 @@ struct uniap_handle {
   int n_edges = 0;
   // device buffers
   DevBuf<int32_t> arena, P, thetas, ntheta, cfglist, scratch, G;
-  DevBuf<int64_t> ns, vals, cfgopt, qcfg, qglob, gofs;
+  DevBuf<int64_t> ns, vals, cfgopt, qcfg, qglob, gofs, qmax;
   DevBuf<int64_t> fwd, act, ps, ctx, tpc, chain, skipb, edges;
   DevBuf<CfgDev> dcfg;
   DevBuf<CatDev> dcat;
@@ -188,7 +188,7 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->st);
   for (auto* b : {&h->arena, &h->P, &h->thetas, &h->ntheta, &h->cfglist, &h->scratch, &h->G}) b->release();
-  for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->qglob, &h->gofs, &h->fwd, &h->act, &h->ps, &h->ctx,
+  for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->qglob, &h->gofs, &h->qmax, &h->fwd, &h->act, &h->ps, &h->ctx,
                   &h->tpc, &h->chain, &h->skipb, &h->edges})
     b->release();
   h->dcfg.release();
@@ -423,6 +423,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   CK(h, h->dcfg.ensure(h->ncfg));
   CK(h, h->dcat.ensure(h->ncfg));
   CK(h, h->qcfg.ensure(h->ncfg));
+  CK(h, h->qmax.ensure((size_t)h->ncfg * MAXL * 4));
   CK(h, h->qglob.ensure(2));
   CK(h, h->fwd.ensure(fwd.size()));
   CK(h, h->act.ensure(act.size()));
@@ -598,7 +599,7 @@ static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, De
 
 static BuildBufs build_bufs(uniap_handle* h) {
   return BuildBufs{h->fwd.p, h->act.p, h->ps.p, h->ctx.p, h->tpc.p, h->chain.p, h->skipb.p, h->edges.p,
-                   h->n_edges, h->dcat.p, h->ns.p, h->qcfg.p, h->qglob.p};
+                   h->n_edges, h->dcat.p, h->ns.p, h->qcfg.p, h->qmax.p, h->qglob.p};
 }
 
 extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev) {
@@ -658,9 +659,9 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
     CK(h, h2d(h, h->cfgopt.p, big.data(), h->ncfg * 8));
   }
   if (nl > 0) CK(h, h2d(h, h->cfglist.p, local.data(), nl * 4));
-  CK(h, cudaMemsetAsync(h->vals.p, 0xff, (size_t)std::max(nl, 1) * (TMAX + 2) * 8, h->st));
   CK(h, launch_k3(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->st));
-  CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p, h->st));
+  CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
+                  h->cfgopt.p, h->st));
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
                    h->cfgopt.p, h->scratch.p, h->win.p, h->st));
   h->launches += nl > 0 ? 3 : 1;

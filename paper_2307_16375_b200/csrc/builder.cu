@@ -47,6 +47,11 @@ struct Coll {
 
 __device__ __forceinline__ int lg2(int x) { return 31 - __clz(x); }
 
+// atomic max of a non-negative value, skipping the atomic when it cannot win
+__device__ __forceinline__ void amax(int64_t* dst, int64_t v) {
+  if (v > *reinterpret_cast<volatile int64_t*>(dst))
+    atomicMax(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)v);
+}
 __device__ __forceinline__ int64_t checked(u128 v, int64_t* flags) {
   if (v >= (u128)NS_LIM) {
     atomicOr(reinterpret_cast<unsigned long long*>(flags), 1ull);
@@ -85,6 +90,7 @@ __global__ void k1a_layers(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict
   const u128 mem = cdiv128((u128)cdt * ps, (u128)(t * f)) + (u128)cf.c * bl * bb.act[u * cl.NT + lt] + (u128)bb.ctx[u];
   A[idx] = checked(a, bb.qglob + 1);
   M[idx] = checked(mem, bb.qglob + 1);
+  amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + u) * 4, A[idx]);
 }
 
 // K1b: R (edge e = u->u+1), Rskip (edge skip->v) in ns, original [k][l] layout.
@@ -107,44 +113,43 @@ __global__ void k1b_reshard(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
     }
   }
   (bb.ns + (isR ? cf.offRf : cf.offRs))[j] = v;
+  // per-layer maxima for the quantum: R of edge e goes into layer e+1
+  if (v > 0 && (isR || (cf.skip >= 0 && e >= cf.skip + 2)))
+    amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + (isR ? e + 1 : e)) * 4 + (isR ? 1 : 2), v);
 }
 
-// K1c: cut costs: every edge crossing the cut after layer e, fwd + bwd P2P.
+// K1c: cut costs: every edge crossing the cut after layer e, fwd + bwd P2P
+// (each edge's P2P time once per config, then one sum per cut).
 __global__ void k1c_cuts(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L) {
-  const CfgDev cf = cfgs[blockIdx.y];
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= L - 1) return;
+  __shared__ unsigned long long pv[512];
+  const CfgDev cf = cfgs[blockIdx.x];
   const int64_t b = cl.B / cf.c;
   const Coll co{cl};
-  u128 s = 0;
-  for (int i = 0; i < bb.n_edges; ++i) {
-    const int64_t* ed = bb.esrc_dst_bytes + 3 * i;
-    if (ed[0] <= e && e < ed[1]) s += 2 * co.p2p((u128)b * ed[2]);
+  for (int i = threadIdx.x; i < bb.n_edges && i < 512; i += blockDim.x)
+    pv[i] = (unsigned long long)checked(2 * co.p2p((u128)b * bb.esrc_dst_bytes[3 * i + 2]), bb.qglob + 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < L - 1; e += blockDim.x) {
+    u128 s = 0;
+    for (int i = 0; i < bb.n_edges && i < 512; ++i) {
+      const int64_t* ed = bb.esrc_dst_bytes + 3 * i;
+      if (ed[0] <= e && e < ed[1]) s += pv[i];
+    }
+    const int64_t v = checked(s, bb.qglob + 1);
+    (bb.ns + cf.offO)[e] = v;
+    bb.qmax[((int64_t)blockIdx.x * MAXL + e) * 4 + 3] = v;
   }
-  (bb.ns + cf.offO)[e] = checked(s, bb.qglob + 1);
 }
 
 // K1d: the smallest passing power-of-two quantum of each config (reading A-9):
 // every ceil(x/q) <= 2^22 and sum_u (max A + max R into u + max Rskip into u)
 // <= 2^28, sum_e O <= 2^28.  An explicit quantum is checked as given.
 __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int skip) {
-  __shared__ int64_t mA[MAXL], mR[MAXL], mS[MAXL], sO[MAXL];
+  __shared__ int64_t mx[MAXL * 4];
   __shared__ int okp[64];
-  const CfgDev cf = cfgs[blockIdx.x];
+  (void)cfgs;
+  (void)skip;
   const int t = threadIdx.x;
-  const int NSP = cf.NSP, S = cf.S;
-  for (int u = t; u < L; u += blockDim.x) {
-    int64_t a = 0, r = 0, s = 0;
-    for (int k = 0; k < S; ++k) a = max(a, bb.ns[cf.offA + u * NSP + k]);
-    if (u >= 1)
-      for (int k = 0; k < S; ++k)
-        for (int l = 0; l < S; ++l) r = max(r, bb.ns[cf.offRf + ((int64_t)(u - 1) * NSP + k) * NSP + l]);
-    if (skip >= 0 && u >= skip + 2)
-      for (int k = 0; k < S; ++k)
-        for (int l = 0; l < S; ++l) s = max(s, bb.ns[cf.offRs + ((int64_t)u * NSP + k) * NSP + l]);
-    mA[u] = a; mR[u] = r; mS[u] = s;
-    sO[u] = (u < L - 1) ? bb.ns[cf.offO + u] : 0;
-  }
+  for (int i = t; i < L * 4; i += blockDim.x) mx[i] = bb.qmax[(int64_t)blockIdx.x * MAXL * 4 + i];
   __syncthreads();
   if (t < 64) {
     const bool expl = cl.quantum > 0;
@@ -156,8 +161,8 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
         bool ok = true;
         int64_t sum = 0, osum = 0;
         for (int u = 0; u < L; ++u) {
-          const int64_t a = (mA[u] + q - 1) / q, r = (mR[u] + q - 1) / q, s = (mS[u] + q - 1) / q;
-          const int64_t o = (sO[u] + q - 1) / q;
+          const int64_t a = (mx[4 * u] + q - 1) / q, r = (mx[4 * u + 1] + q - 1) / q, s = (mx[4 * u + 2] + q - 1) / q;
+          const int64_t o = u < L - 1 ? (mx[4 * u + 3] + q - 1) / q : 0;
           ok = ok && a <= EM && r <= EM && s <= EM && o <= EM;
           sum += a + r + s;
           osum += o;
@@ -228,9 +233,11 @@ cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* c
   const int maxNSP = 32;
   cudaError_t e = cudaMemsetAsync(bb.qglob, 0, 2 * sizeof(int64_t), st);
   if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(bb.qmax, 0, (size_t)ncfg * MAXL * 4 * sizeof(int64_t), st);
+  if (e != cudaSuccess) return e;
   k1a_layers<<<dim3((L * maxNSP + 127) / 128, ncfg), 128, 0, st>>>(cl, bb, cfg, L);
   k1b_reshard<<<dim3(((2 * L - 1) * maxNSP * maxNSP + 255) / 256, ncfg), 256, 0, st>>>(cl, bb, cfg, L);
-  k1c_cuts<<<dim3(1, ncfg), 64, 0, st>>>(cl, bb, cfg, L);
+  k1c_cuts<<<ncfg, 128, 0, st>>>(cl, bb, cfg, L);
   k1d_quantum<<<ncfg, 64, 0, st>>>(cl, bb, cfg, L, skip);
   k1e_global<<<1, 1, 0, st>>>(bb, ncfg);
   k1f_quantise<<<dim3(16, ncfg), 256, 0, st>>>(cl, bb, cfg, L, arena);

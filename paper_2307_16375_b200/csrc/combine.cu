@@ -145,62 +145,117 @@ __device__ int32_t warp_F(const int32_t* sP, const int32_t* sO, int32_t* g, int 
 }
 
 // ---------------------------------------------------------------------------
-// K4: Val(theta) for every theta of every local config.
-// grid (n_local, K4G); 8 warps per CTA; warp w of CTA y handles theta indices
-// i = y*8+w, i += K4G*8 (ascending), skipping theta once
-// F_inf + (c-1)*theta > best-so-far (strict: ties stay for the tie-break).
+// K4: Val(theta) of one config per CTA (32 warps), and the config's optimum.
+//  1. F_inf = F at the largest theta (no limit).  c = 1: OPT = F_inf.
+//  2. theta_min, the smallest theta with a feasible placement (F is finite
+//     exactly for theta >= theta_min), by a 32-ary search over the sorted
+//     candidates (each round: 32 warps probe 32 thetas in parallel).
+//  3. U = Val(theta_min) bounds OPT, so only theta <= (U - F_inf)/(c-1)
+//     can reach it (Val(theta) >= F_inf + (c-1) theta); those are evaluated
+//     in ascending order by the 32 warps, skipping theta once
+//     F_inf + (c-1) theta > best-so-far (strict: ties stay for the tie-break).
+// Unevaluated entries keep Val = INT64_MAX (> OPT, so never in Theta*).
 // ---------------------------------------------------------------------------
-constexpr int K4G = 16;
-constexpr int K4W = 8;
+constexpr int K4W = 32;
 __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
                                                    const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
                                                    int L, const int32_t* __restrict__ thetas,
-                                                   const int32_t* __restrict__ ntheta, int64_t* __restrict__ vals) {
+                                                   const int32_t* __restrict__ ntheta, int64_t* __restrict__ vals,
+                                                   int64_t* __restrict__ cfg_opt) {
   __shared__ int32_t sP[MAXL * MAXL];
   __shared__ int32_t sO[MAXL];
   __shared__ int32_t g[K4W][128];
+  __shared__ int32_t probeF[K4W];
+  __shared__ int s_lo, s_hi;
+  __shared__ unsigned long long s_best;
   const int li = blockIdx.x;
   const CfgDev cf = cfgs[cfg_list[li]];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = ntheta[li];
+  int64_t* V = vals + (int64_t)li * (TMAX + 2);  // [0..nt) Val, [TMAX] F_inf, [TMAX+1] opt
+  const int32_t* th = thetas + (int64_t)li * TMAX;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) V[i] = INT64_MAX;
+  if (cf.deg > L || nt == 0) {  // Eq. 7b cannot hold (reading A-22)
+    if (threadIdx.x == 0) { V[TMAX] = INT64_MAX; cfg_opt[cfg_list[li]] = INT64_MAX; }
+    return;
+  }
   for (int i = threadIdx.x; i < L * L; i += blockDim.x) sP[i] = P[cf.offP + i];
   for (int i = threadIdx.x; i < L - 1; i += blockDim.x) sO[i] = arena[cf.offO + i];
   __syncthreads();
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nt = ntheta[li];
-  int64_t* V = vals + (int64_t)li * (TMAX + 2);  // [0..nt) Val, [TMAX] F_inf, [TMAX+1] best
-  const int32_t* th = thetas + (int64_t)li * TMAX;
-  if (cf.deg > L) {  // Eq. 7b cannot hold (reading A-22)
-    for (int i = blockIdx.y * K4W + w; i < nt; i += K4G * K4W)
-      if (lane == 0) V[i] = INT64_MAX;
-    if (blockIdx.y == 0 && threadIdx.x == 0) V[TMAX] = INT64_MAX;
+  const int64_t cm1 = cf.c - 1;
+  // 1. F_inf
+  if (w == 0) {
+    const int32_t F = warp_F(sP, sO, g[0], L, cf.deg, INF);
+    if (lane == 0) probeF[0] = F;
+  }
+  __syncthreads();
+  const int32_t Finf = probeF[0];
+  if (Finf >= INF || cf.c == 1) {
+    if (threadIdx.x == 0) {
+      V[TMAX] = Finf >= INF ? INT64_MAX : (int64_t)Finf;
+      cfg_opt[cfg_list[li]] = V[TMAX];
+    }
     return;
   }
-  // every warp computes F_inf itself (cheap, avoids a grid barrier)
-  const int32_t Finf = warp_F(sP, sO, g[w], L, cf.deg, INF);
-  if (blockIdx.y == 0 && w == 0 && lane == 0) V[TMAX] = Finf >= INF ? INT64_MAX : (int64_t)Finf;
-  const int64_t cm1 = cf.c - 1;
-  unsigned long long* best = reinterpret_cast<unsigned long long*>(V + TMAX + 1);
-  for (int i = blockIdx.y * K4W + w; i < nt; i += K4G * K4W) {
-    const int32_t theta = th[i];
-    int64_t val = INT64_MAX;
-    if (Finf < INF && cf.c > 1) {
-      const int64_t lb = (int64_t)Finf + cm1 * theta;
-      const unsigned long long bs = *(volatile unsigned long long*)best;
-      if ((unsigned long long)lb <= bs) {
-        const int32_t F = warp_F(sP, sO, g[w], L, cf.deg, theta);
-        if (F < INF) {
-          val = (int64_t)F + cm1 * theta;
-          if (lane == 0) atomicMin(best, (unsigned long long)val);
-        }
+  // 2. theta_min: invariant F(th[hi]) finite, F(th[lo-1]) infinite (lo = 0: none)
+  if (threadIdx.x == 0) { s_lo = 0; s_hi = nt - 1; }
+  __syncthreads();
+  while (true) {
+    const int lo = s_lo, hi = s_hi;
+    if (lo >= hi) break;
+    const int span = hi - lo;  // probes lo + span*w/32 (w < 32), all < hi
+    const int pidx = lo + (int)(((int64_t)span * w) / K4W);
+    const int32_t F = warp_F(sP, sO, g[w], L, cf.deg, th[pidx]);
+    if (lane == 0) probeF[w] = F;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int nlo = lo, nhi = hi;
+      for (int q = 0; q < K4W; ++q) {
+        const int pi = lo + (int)(((int64_t)span * q) / K4W);
+        if (probeF[q] < INF) { nhi = min(nhi, pi); break; }
+        nlo = max(nlo, pi + 1);
       }
+      s_lo = nlo;
+      s_hi = nhi;
     }
-    if (lane == 0) V[i] = val;
+    __syncthreads();
+  }
+  const int imin = s_hi;
+  // 3. U = Val(theta_min); evaluate theta_min .. theta_hi
+  if (w == 0) {
+    const int32_t F = warp_F(sP, sO, g[0], L, cf.deg, th[imin]);
+    if (lane == 0) {
+      const int64_t U = (int64_t)F + cm1 * th[imin];
+      V[imin] = U;
+      s_best = (unsigned long long)U;
+    }
+  }
+  __syncthreads();
+  const int64_t U = (int64_t)s_best;
+  for (int i = imin + 1 + w; i < nt; i += K4W) {
+    const int32_t theta = th[i];
+    const int64_t lb = (int64_t)Finf + cm1 * theta;
+    if (lb > U) break;  // ascending thetas: every later one is worse too
+    if ((unsigned long long)lb > *(volatile unsigned long long*)&s_best) continue;
+    const int32_t F = warp_F(sP, sO, g[w], L, cf.deg, theta);
+    if (F < INF && lane == 0) {
+      const int64_t val = (int64_t)F + cm1 * theta;
+      V[i] = val;
+      atomicMin(&s_best, (unsigned long long)val);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    V[TMAX] = Finf;
+    cfg_opt[cfg_list[li]] = (int64_t)s_best;
   }
 }
 
 cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
-                      int L, const int32_t* thetas, const int32_t* ntheta, int64_t* vals, cudaStream_t st) {
+                      int L, const int32_t* thetas, const int32_t* ntheta, int64_t* vals, int64_t* cfg_opt,
+                      cudaStream_t st) {
   if (n_local <= 0) return cudaSuccess;
-  k4_vals<<<dim3(n_local, K4G), K4W * 32, 0, st>>>(cfg, arena, P, cfg_list, L, thetas, ntheta, vals);
+  k4_vals<<<n_local, K4W * 32, 0, st>>>(cfg, arena, P, cfg_list, L, thetas, ntheta, vals, cfg_opt);
   return cudaGetLastError();
 }
 
@@ -218,7 +273,6 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
                                                   Winner* __restrict__ win) {
   __shared__ int32_t sP[MAXL * MAXL];
   __shared__ int32_t sO[MAXL];
-  __shared__ int64_t red[32];
   __shared__ int32_t stars[TMAX];
   __shared__ int32_t nstar;
   __shared__ int32_t ends[32][MAXL];
@@ -226,24 +280,6 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
   __shared__ int64_t s_opt[1];
   __shared__ int32_t s_win;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  // 1. per-config optimum (min over theta of Val; c = 1: F_inf)
-  for (int li = 0; li < n_local; ++li) {
-    const CfgDev cf = cfgs[cfg_list[li]];
-    const int64_t* V = vals + (int64_t)li * (TMAX + 2);
-    int64_t m = INT64_MAX;
-    if (cf.c == 1) m = V[TMAX];
-    else
-      for (int i = t; i < ntheta[li]; i += K5T) m = min(m, V[i]);
-    for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) red[w] = m;
-    __syncthreads();
-    if (t == 0) {
-      int64_t r = INT64_MAX;
-      for (int i = 0; i < 32; ++i) r = min(r, red[i]);
-      cfg_opt[cfg_list[li]] = r;
-    }
-    __syncthreads();
-  }
   // 2. winner by (objective, deg, c)
   if (t == 0) {
     int wi = -1;
@@ -403,7 +439,7 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
   __shared__ int32_t mem[32];
   __shared__ int32_t okw[32];
   const int stage = blockIdx.x;
-  const Winner W = *win;
+  const Winner& W = *win;  // by reference: fields are read on demand, no per-thread copy
   const CfgDev cf = cfgs[W.cfg];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int a = stage == 0 ? 0 : W.end[stage - 1] + 1, b = W.end[stage];

@@ -83,7 +83,7 @@ cudaError_t launch_k3(const CfgDev* cfg, const int32_t* arena, const int32_t* P,
                       int n_local, int L, int32_t* thetas, int32_t* ntheta, cudaStream_t st);
 cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
                       int n_local, int L, const int32_t* thetas, const int32_t* ntheta, int64_t* vals,
-                      cudaStream_t st);
+                      int64_t* cfg_opt, cudaStream_t st);
 cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
                        int n_local, int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals,
                        int64_t* cfg_opt, int32_t* scratch, Winner* win, cudaStream_t st);
@@ -112,6 +112,7 @@ struct BuildBufs {
   const CatDev* cat;      // [ncfg]
   int64_t* ns;            // int64 scratch arena, same offsets as the int32 arena
   int64_t* qcfg;          // [ncfg] smallest passing quantum per config
+  int64_t* qmax;          // [ncfg][MAXL][4] per layer: max A, max R into u, max Rskip into u, O[u]
   int64_t* qglob;         // [2]: quantum, error flags
 };
 cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* cfg, int ncfg, int L, int skip,

