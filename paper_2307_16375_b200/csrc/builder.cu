@@ -160,9 +160,11 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
         const int64_t EM = (int64_t)UNIAP_MAX_ENTRY, SM = (int64_t)UNIAP_MAX_SUM;
         bool ok = true;
         int64_t sum = 0, osum = 0;
+        // ceil(x / q): a shift for the power-of-two candidates
+        auto cq = [&](int64_t x) { return expl ? (x + q - 1) / q : (x + q - 1) >> t; };
         for (int u = 0; u < L; ++u) {
-          const int64_t a = (mx[4 * u] + q - 1) / q, r = (mx[4 * u + 1] + q - 1) / q, s = (mx[4 * u + 2] + q - 1) / q;
-          const int64_t o = u < L - 1 ? (mx[4 * u + 3] + q - 1) / q : 0;
+          const int64_t a = cq(mx[4 * u]), r = cq(mx[4 * u + 1]), s = cq(mx[4 * u + 2]);
+          const int64_t o = u < L - 1 ? cq(mx[4 * u + 3]) : 0;
           ok = ok && a <= EM && r <= EM && s <= EM && o <= EM;
           sum += a + r + s;
           osum += o;

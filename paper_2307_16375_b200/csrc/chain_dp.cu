@@ -32,29 +32,34 @@ static int pow2ceil(int x) {
 }
 
 // Shape of the chain DP for |S| strategies and Q = cap+1 buckets.
-// A CTA holds B = T*V buckets (V = 2 per thread, up to 512 threads) with E
-// double-buffered in shared memory (<= 200 KB); larger Q splits the bucket
-// axis over a thread-block cluster of C CTAs (DSMEM for the shifted reads).
-// A single long chain (deg = 1) is spread over a cluster of up to 8 CTAs
-// (B >= 128) even when it would fit one CTA: its critical path is serial in
-// the layers, so more SMs per step shorten it.  Small |S| with large Q keep
-// 8 buckets per thread in one 512-thread CTA (B = 4096).
+// A CTA holds B = T*V buckets (up to 512 threads; V = 2, or 4 / 8 buckets per
+// thread for B = 2048 / 4096) with E double-buffered in shared memory: B is
+// the largest span whose E fits 200 KB, so a cluster (DSMEM for the shifted
+// reads, one cluster barrier per layer) is used only when Q exceeds it.
+// A single long chain (deg = 1) is spread over a cluster of up to 8 (16 when
+// Q > 2048) CTAs with B >= 128, even when it would fit one CTA: its critical
+// path is serial in the layers, so more SMs per layer shorten it.
 bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   const int NS = k2_ns_round(S);
   if (NS < 0 || Q < 1 || Q > UNIAP_MAX_Q) return false;
-  int Bmax = 1024;
-  while (Bmax > 32 && smem_words(NS, Bmax) * 4 > 200 * 1024) Bmax /= 2;
-  if (NS <= 6 && Q > 2048 && !single) Bmax = 4096;
+  const size_t lim = 200 * 1024;
+  int Bmax = 32;
+  for (int B : {64, 128, 256, 512, 1024}) if (smem_words(NS, B) * 4 <= lim) Bmax = B;
+  if (NS <= 12 && smem_words(NS, 2048) * 4 <= lim) Bmax = 2048;
+  if (NS <= 6 && smem_words(NS, 4096) * 4 <= lim) Bmax = 4096;
   int B = std::min(Bmax, std::max(32, pow2ceil(Q)));
   int C = pow2ceil((Q + B - 1) / B);
-  if (single)
-    while (C < 8 && B > 128) {
+  if (single) {
+    const int cmax = Q > 2048 ? 16 : 8;
+    while (C < cmax && B > 128) {
       B /= 2;
       C = pow2ceil((Q + B - 1) / B);
     }
+  }
   if (C > 16) return false;
   K2Class c{NS, 2, B / 2, C};
   if (B == 32) { c.V = 1; c.T = 32; }
+  if (B == 2048) { c.V = 4; c.T = 512; }
   if (B == 4096) { c.V = 8; c.T = 512; }
   *out = c;
   return true;

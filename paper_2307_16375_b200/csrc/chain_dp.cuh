@@ -26,6 +26,8 @@
 // In a cluster the shifted read may fall in a lower CTA's bucket range:
 // DSMEM (ld.shared::cluster) on that path only.
 #pragma once
+#include <type_traits>
+
 #include "uniap_impl.h"
 
 namespace uniap {
@@ -199,58 +201,45 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     int32_t* Eb = sE + (step & 1) * NS * ROW + 4;          // row 0, bucket 0
     const int32_t* Tb = sT + (step % 3) * SW;
     // ---- E-step: registers only; R broadcast from shared memory ----
+    // RR destination rows per pass: RR*V independent VIADDMNMX chains.
     {
       int32_t* Et = Eb + t;
-      auto two_rows = [&](int k) {  // destination rows k, k+1
-        int32_t a0[V], a1[V];
+      auto rows = [&](auto rrc, int k) {
+        constexpr int RR = decltype(rrc)::value;
+        int32_t acc[RR][V];
 #pragma unroll
-        for (int j = 0; j < V; ++j) a0[j] = a1[j] = INF;
-        const int4* r0 = reinterpret_cast<const int4*>(Tb + k * NSP);
-        const int4* r1 = reinterpret_cast<const int4*>(Tb + (k + 1) * NSP);
+        for (int r = 0; r < RR; ++r)
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc[r][j] = INF;
 #pragma unroll
         for (int c = 0; c < NSP / 4; ++c) {
-          const int4 x = r0[c];
-          const int4 y = r1[c];
+          int4 x[RR];
+#pragma unroll
+          for (int r = 0; r < RR; ++r) x[r] = reinterpret_cast<const int4*>(Tb + (k + r) * NSP)[c];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             if (4 * c + i < NS)
 #pragma unroll
-              for (int j = 0; j < V; ++j) {
-                a0[j] = addmin(d[4 * c + i][j], comp(x, i), a0[j]);
-                a1[j] = addmin(d[4 * c + i][j], comp(y, i), a1[j]);
-              }
+              for (int r = 0; r < RR; ++r)
+#pragma unroll
+                for (int j = 0; j < V; ++j) acc[r][j] = addmin(d[4 * c + i][j], comp(x[r], i), acc[r][j]);
         }
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-          Et[k * ROW + j * T] = a0[j];
-          Et[(k + 1) * ROW + j * T] = a1[j];
-        }
+        for (int r = 0; r < RR; ++r)
+#pragma unroll
+          for (int j = 0; j < V; ++j) Et[(k + r) * ROW + j * T] = acc[r][j];
       };
-      auto one_row = [&](int k) {
-        int32_t a0[V];
-#pragma unroll
-        for (int j = 0; j < V; ++j) a0[j] = INF;
-        const int4* r0 = reinterpret_cast<const int4*>(Tb + k * NSP);
-#pragma unroll
-        for (int c = 0; c < NSP / 4; ++c) {
-          const int4 x = r0[c];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (4 * c + i < NS)
-#pragma unroll
-              for (int j = 0; j < V; ++j) a0[j] = addmin(d[4 * c + i][j], comp(x, i), a0[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < V; ++j) Et[k * ROW + j * T] = a0[j];
-      };
+      constexpr int RR = (V >= 8) ? 2 : (V >= 4 ? 2 : 4);
+      constexpr int RRC = RR < NS ? RR : NS;
+      constexpr int NFULL = NS / RRC * RRC;
       if constexpr (NS <= KUNROLL) {
 #pragma unroll
-        for (int k = 0; k + 1 < NS; k += 2) two_rows(k);
+        for (int k = 0; k < NFULL; k += RRC) rows(std::integral_constant<int, RRC>{}, k);
       } else {
 #pragma unroll 1
-        for (int k = 0; k + 1 < NS; k += 2) two_rows(k);
+        for (int k = 0; k < NFULL; k += RRC) rows(std::integral_constant<int, RRC>{}, k);
       }
-      if constexpr (NS % 2) one_row(NS - 1);
+      if constexpr (NS - NFULL > 0) rows(std::integral_constant<int, NS - NFULL>{}, NFULL);
     }
     // stage the tables of the step after next, then one barrier per layer
     if (step + 1 < in.n) store_stage(step + 1);
@@ -319,10 +308,9 @@ k2_fn k2_get(int V, int T, bool CL) {
   UNIAP_SHAPE(2, 128)
   UNIAP_SHAPE(2, 256)
   UNIAP_SHAPE(2, 512)
+  if constexpr (NS <= 12) { UNIAP_SHAPE(4, 512) }
+  if constexpr (NS <= 6) { UNIAP_SHAPE(8, 512) }
 #undef UNIAP_SHAPE
-  if constexpr (NS <= 6) {
-    if (V == 8 && T == 512) return CL ? k2_chain<NS, 8, 512, true> : k2_chain<NS, 8, 512, false>;
-  }
   return nullptr;
 }
 

@@ -98,37 +98,46 @@ cudaError_t launch_k3(const CfgDev* cfg, const int32_t* arena, const int32_t* P,
 }
 
 // ---------------------------------------------------------------------------
-// F_theta by a warp: forward DP over (stage i, end b); lanes own b.
-// Returns F_theta (INF if no placement fits).  theta = INF means "no limit".
-// sP: the config's P[L][L] in shared memory; sO: O[L-1]; g: 2*64 scratch.
+// Placement DPs by one warp over (stage i, end b); lanes own b (b = lane,
+// lane + 32).  Stage i = [a, b] with i-1 <= a <= b <= L-1-(deg-i); the last
+// stage ends at L-1.  sP: the config's P[L][L] in shared memory, sO: O[L-1],
+// g: 128 words of warp-private scratch.
+//  warp_F:   F_theta = min sum P + sum O over placements with every P, O <=
+//            theta (theta = INF: no limit)   -- (min, +) semiring
+//  warp_Bmm: the bottleneck min over placements of max(P u O), i.e. the
+//            smallest theta with a feasible placement -- (min, max) semiring
+// The a-loop is branch-free (predicated) and unrolled for ILP.
 // ---------------------------------------------------------------------------
-__device__ int32_t warp_F(const int32_t* sP, const int32_t* sO, int32_t* g, int L, int deg, int32_t theta) {
+template <bool BOTTLENECK>
+__device__ int32_t warp_dp(const int32_t* sP, const int32_t* sO, int32_t* g, int L, int deg, int32_t theta) {
   const int lane = threadIdx.x & 31;
   int32_t* cur = g;
   int32_t* nxt = g + 64;
-  // stage 1 = [0, b], b <= L-1-(deg-1)
   for (int b = lane; b < L; b += 32) {
     const int32_t p = sP[b];
     cur[b] = (b <= L - deg && p <= theta) ? p : INF;
   }
   __syncwarp();
+  const int b0 = lane, b1 = lane + 32;
   for (int i = 2; i <= deg; ++i) {
-    // stage i = [a, b] with i-1 <= a <= b <= L-1-(deg-i); the last stage ends at L-1
     const int blo = (i == deg) ? L - 1 : i - 1, bhi = L - 1 - (deg - i);
-    const int b0 = lane, b1 = lane + 32;
+    const bool v0 = b0 >= blo && b0 <= bhi, v1 = b1 >= blo && b1 <= bhi && b1 < L;
     int32_t best0 = INF, best1 = INF;
+#pragma unroll 4
     for (int a = i - 1; a <= bhi; ++a) {  // stage i-1 ends at a-1
       const int32_t gp = cur[a - 1];
       const int32_t o = sO[a - 1];
-      if (gp >= INF || o > theta) continue;  // warp-uniform
-      const int32_t base = gp + o;
-      if (b0 >= a && b0 >= blo && b0 <= bhi) {
-        const int32_t p = sP[a * L + b0];
-        if (p <= theta) best0 = min(best0, base + p);
-      }
-      if (b1 >= a && b1 >= blo && b1 <= bhi && b1 < L) {
-        const int32_t p = sP[a * L + b1];
-        if (p <= theta) best1 = min(best1, base + p);
+      const int32_t p0 = (v0 && b0 >= a) ? sP[a * L + b0] : INF;
+      const int32_t p1 = (v1 && b1 >= a) ? sP[a * L + b1] : INF;
+      if (BOTTLENECK) {
+        const int32_t base = max(gp, o);
+        best0 = min(best0, max(base, p0));
+        best1 = min(best1, max(base, p1));
+      } else {
+        const bool ok = gp < INF && o <= theta;  // then gp + o < 2^29 + 2^22
+        const int32_t base = gp + o;
+        best0 = min(best0, (ok && p0 <= theta) ? base + p0 : INF);
+        best1 = min(best1, (ok && p1 <= theta) ? base + p1 : INF);
       }
     }
     __syncwarp();
@@ -143,13 +152,16 @@ __device__ int32_t warp_F(const int32_t* sP, const int32_t* sO, int32_t* g, int 
   __syncwarp();
   return F;
 }
+__device__ __forceinline__ int32_t warp_F(const int32_t* sP, const int32_t* sO, int32_t* g, int L, int deg,
+                                          int32_t theta) {
+  return warp_dp<false>(sP, sO, g, L, deg, theta);
+}
 
 // ---------------------------------------------------------------------------
 // K4: Val(theta) of one config per CTA (32 warps), and the config's optimum.
 //  1. F_inf = F at the largest theta (no limit).  c = 1: OPT = F_inf.
 //  2. theta_min, the smallest theta with a feasible placement (F is finite
-//     exactly for theta >= theta_min), by a 32-ary search over the sorted
-//     candidates (each round: 32 warps probe 32 thetas in parallel).
+//     exactly for theta >= theta_min): one bottleneck (min, max) DP.
 //  3. U = Val(theta_min) bounds OPT, so only theta <= (U - F_inf)/(c-1)
 //     can reach it (Val(theta) >= F_inf + (c-1) theta); those are evaluated
 //     in ascending order by the 32 warps, skipping theta once
@@ -166,7 +178,7 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
   __shared__ int32_t sO[MAXL];
   __shared__ int32_t g[K4W][128];
   __shared__ int32_t probeF[K4W];
-  __shared__ int s_lo, s_hi;
+  __shared__ int s_hi;
   __shared__ unsigned long long s_best;
   const int li = blockIdx.x;
   const CfgDev cf = cfgs[cfg_list[li]];
@@ -183,10 +195,13 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
   for (int i = threadIdx.x; i < L - 1; i += blockDim.x) sO[i] = arena[cf.offO + i];
   __syncthreads();
   const int64_t cm1 = cf.c - 1;
-  // 1. F_inf
+  // 1. F_inf (warp 0) and the bottleneck theta_min (warp 1)
   if (w == 0) {
     const int32_t F = warp_F(sP, sO, g[0], L, cf.deg, INF);
     if (lane == 0) probeF[0] = F;
+  } else if (w == 1) {
+    const int32_t Bm = warp_dp<true>(sP, sO, g[1], L, cf.deg, INF);
+    if (lane == 0) probeF[1] = Bm;
   }
   __syncthreads();
   const int32_t Finf = probeF[0];
@@ -197,29 +212,18 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
     }
     return;
   }
-  // 2. theta_min: invariant F(th[hi]) finite, F(th[lo-1]) infinite (lo = 0: none)
-  if (threadIdx.x == 0) { s_lo = 0; s_hi = nt - 1; }
-  __syncthreads();
-  while (true) {
-    const int lo = s_lo, hi = s_hi;
-    if (lo >= hi) break;
-    const int span = hi - lo;  // probes lo + span*w/32 (w < 32), all < hi
-    const int pidx = lo + (int)(((int64_t)span * w) / K4W);
-    const int32_t F = warp_F(sP, sO, g[w], L, cf.deg, th[pidx]);
-    if (lane == 0) probeF[w] = F;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int nlo = lo, nhi = hi;
-      for (int q = 0; q < K4W; ++q) {
-        const int pi = lo + (int)(((int64_t)span * q) / K4W);
-        if (probeF[q] < INF) { nhi = min(nhi, pi); break; }
-        nlo = max(nlo, pi + 1);
-      }
-      s_lo = nlo;
-      s_hi = nhi;
+  // 2. the index of theta_min in the sorted candidates (it is one of them)
+  if (threadIdx.x == 0) {
+    const int32_t tm = probeF[1];
+    int lo = 0, hi = nt - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (th[mid] < tm) lo = mid + 1;
+      else hi = mid;
     }
-    __syncthreads();
+    s_hi = lo;
   }
+  __syncthreads();
   const int imin = s_hi;
   // 3. U = Val(theta_min); evaluate theta_min .. theta_hi
   if (w == 0) {
