@@ -20,7 +20,7 @@ int k2_ns_round(int S) {
 
 static size_t smem_words(int NS, int B) {
   const int NSP = (NS + 3) & ~3;
-  return (size_t)2 * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP);
+  return (size_t)2 * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP) + MAXL;
 }
 
 size_t k2_smem_bytes(const K2Class& c) { return smem_words(c.NS, c.T * c.V) * sizeof(int32_t); }
@@ -36,8 +36,8 @@ static int pow2ceil(int x) {
 // thread for B = 2048 / 4096) with E double-buffered in shared memory: B is
 // the largest span whose E fits 200 KB, so a cluster (DSMEM for the shifted
 // reads, one cluster barrier per layer) is used only when Q exceeds it.
-// A single long chain (deg = 1) is spread over a cluster of up to 8 (16 when
-// Q > 2048) CTAs with B >= 128, even when it would fit one CTA: its critical
+// A single long chain (deg = 1) is spread over a cluster of up to 8 CTAs
+// with B >= 128, even when it would fit one CTA: its critical
 // path is serial in the layers, so more SMs per layer shorten it.
 bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   const int NS = k2_ns_round(S);
@@ -50,7 +50,7 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   int B = std::min(Bmax, std::max(32, pow2ceil(Q)));
   int C = pow2ceil((Q + B - 1) / B);
   if (single) {
-    const int cmax = Q > 2048 ? 16 : 8;
+    const int cmax = 8;
     while (C < cmax && B > 128) {
       B /= 2;
       C = pow2ceil((Q + B - 1) / B);

@@ -47,12 +47,19 @@ __device__ __forceinline__ uint32_t cl_size() {
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-__device__ __forceinline__ int32_t ld_dsmem(const int32_t* p, uint32_t rank) {
-  uint32_t la = (uint32_t)__cvta_generic_to_shared(p), ra;
-  int32_t v;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
-  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
-  return v;
+__device__ __forceinline__ void cl_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cl_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Generic address of the same shared-memory word in CTA `rank` of the
+// cluster (pure: the load itself is an ordinary C++ load, so the compiler
+// keeps it after the barrier and may batch several of them).
+__device__ __forceinline__ const int32_t* map_rank(const int32_t* p, uint32_t rank) {
+  uint64_t r;
+  asm("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<const int32_t*>(r);
 }
 __device__ __forceinline__ int4 lds128(uint32_t addr) {
   int4 v;
@@ -91,6 +98,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   extern __shared__ int4 smem4[];
   int32_t* sE = reinterpret_cast<int32_t*>(smem4);  // [2][NS][ROW]
   int32_t* sT = sE + 2 * NS * ROW;                  // [3][SW] staged tables
+  int32_t* sProw = sT + 3 * SW;                     // [MAXL] this instance's P[a][.]
   const int t = threadIdx.x;
   int rank = 0, ii = blockIdx.x;
   if constexpr (CL) {
@@ -157,9 +165,8 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
             if (j == jc)
 #pragma unroll
               for (int k = 0; k < NS; ++k) v = min(v, d[k][j]);
-          int32_t* dst = args.P + cf.offP + (int64_t)in.a * L + u;
-          if (in.emit == 2) atomicMin(dst, v);
-          else *dst = v;
+          sProw[u] = v;  // written to global after the sweep (no global store
+                         // outstanding at the per-layer cluster barrier)
         }
       }
     } else {
@@ -243,9 +250,13 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     }
     // stage the tables of the step after next, then one barrier per layer
     if (step + 1 < in.n) store_stage(step + 1);
+    // Split-phase: arrive on the cluster barrier (release E), issue the next
+    // table fetch (after the release, so its fence does not wait for it),
+    // sync the CTA, shift from the local E while the other CTAs catch up,
+    // then wait (acquire) before the few reads from a lower CTA's range.
+    if constexpr (CL) cl_arrive();
     if (step + 2 < in.n) fetch_stage(step + 2, u + 2 * in.dir);
-    if constexpr (CL) cl_sync();
-    else __syncthreads();
+    __syncthreads();
     // ---- shift by the layer's memory, add A' ----
     // Byte addresses in the shared window: row k's bucket x sits at
     // rowb_k + 4x; x < 0 is clamped onto the guard word at rowb_k - 4 by one
@@ -263,6 +274,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     if constexpr (CL) {
       // buckets whose shifted source q - M lies in a lower CTA's range: the
       // local read above returned the guard (INF); fetch the value over DSMEM
+      cl_wait();
       if (rank > 0) {
         const int wbase = t & ~31;
 #pragma unroll
@@ -274,7 +286,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
               const int lx = j * T + t - am.y;
               const int x = lx + rank * B;
               if (lx < 0 && x >= 0)
-                d[k][j] = addmin(ld_dsmem(Eb + k * ROW + (x & (B - 1)), (uint32_t)(x / B)), am.x, INF);
+                d[k][j] = addmin(*map_rank(Eb + k * ROW + (x & (B - 1)), (uint32_t)(x / B)), am.x, INF);
             }
           }
         }
@@ -282,12 +294,21 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     }
     emit(u);
   }
+  // the forward sweep's stage optima P[a][a..a+n-1], from its owner thread
+  if (in.dir > 0 && rank == cap / B && t == (cap - (cap / B) * B) % T) {
+    int32_t* dst = args.P + cf.offP + (int64_t)in.a * L;
+    for (int i = 0; i < in.n; ++i) {
+      const int uu = in.a + i;
+      if (in.emit == 2) atomicMin(dst + uu, sProw[uu]);
+      else dst[uu] = sProw[uu];
+    }
+  }
   if constexpr (CL) cl_sync();  // keep this CTA's E alive for remote readers
 }
 
 template <int NS>
 constexpr size_t k2_smem(int B) {
-  return (size_t)(2 * NS * (B + 4) + 3 * Stage<NS>::WORDS) * sizeof(int32_t);
+  return (size_t)(2 * NS * (B + 4) + 3 * Stage<NS>::WORDS + MAXL) * sizeof(int32_t);
 }
 
 // Instantiation helper used by the per-NS translation units: only the shapes
