@@ -1,4 +1,5 @@
 // chain_dp.cu -- K2 class selection and launch (see chain_dp.cuh for the kernel).
+#include <cstdlib>
 #include <mutex>
 
 #include "chain_dp.cuh"
@@ -39,14 +40,20 @@ static int pow2ceil(int x) {
 // A single long chain (deg = 1) is spread over a cluster of up to 8 CTAs
 // with B >= 128, even when it would fit one CTA: its critical
 // path is serial in the layers, so more SMs per layer shorten it.
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   const int NS = k2_ns_round(S);
   if (NS < 0 || Q < 1 || Q > UNIAP_MAX_Q) return false;
   const size_t lim = 200 * 1024;
+  static const int cap_b = env_int("UNIAP_K2_BMAX", 4096);  // tuning knob (experiments)
   int Bmax = 32;
-  for (int B : {64, 128, 256, 512, 1024}) if (smem_words(NS, B) * 4 <= lim) Bmax = B;
-  if (NS <= 12 && smem_words(NS, 2048) * 4 <= lim) Bmax = 2048;
-  if (NS <= 6 && smem_words(NS, 4096) * 4 <= lim) Bmax = 4096;
+  for (int B : {64, 128, 256, 512, 1024}) if (B <= cap_b && smem_words(NS, B) * 4 <= lim) Bmax = B;
+  if (NS <= 12 && 2048 <= cap_b && smem_words(NS, 2048) * 4 <= lim) Bmax = 2048;
+  if (NS <= 6 && 4096 <= cap_b && smem_words(NS, 4096) * 4 <= lim) Bmax = 4096;
   int B = std::min(Bmax, std::max(32, pow2ceil(Q)));
   int C = pow2ceil((Q + B - 1) / B);
   if (single) {

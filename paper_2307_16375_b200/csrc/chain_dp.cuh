@@ -5,10 +5,10 @@
 // The state D[k][q] is the minimum of Eq. (3)'s stage cost over the layers
 // swept so far, with the current layer on strategy k and the memory sum of
 // Eq. (5) at most q buckets.  Each step is
-//   E[k][x] = min_k' ( D[k'][x] + R[k'][k] )        (min-plus mat-vec per bucket;
-//                                                    R = the resharding term of Eq. 3)
-//   D[k][q] = min( INF, A'[u][k] + E[k][q - M[u][k]] )  (shift by the layer's memory,
-//                                                    INF where q < M)
+//   E[k][x] = min( INF, min_k' ( D[k'][x] + R[k'][k] + A'[u][k] ) )
+//                    (min-plus mat-vec per bucket; R = the resharding term of
+//                     Eq. 3, A' = the execution cost A plus skip-edge terms)
+//   D[k][q] = E[k][q - M[u][k]]   (shift by the layer's memory, INF where q < M)
 // and a forward instance emits P[a][u] = min_k D[k][cap] (the stage optimum of
 // [a,u]).  The transposed order of the two updates (E first, then the shift)
 // keeps the |S|^2 work of a bucket inside one thread.
@@ -122,17 +122,25 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   // skip-edge term of Eq. 3 when the instance conditions the skip source;
   // strategies excluded by that conditioning get an unreachable memory.
   constexpr int PER = (SW + T - 1) / T;
+  // R' = R + A'[u][dest]: the layer's execution cost (plus the skip-edge term)
+  // rides on the resharding row of its destination strategy, so the E-step
+  // yields A' + min_k'(D + R) directly and the shift is a plain shifted copy.
+  // (D <= INF = 2^30, R' <= 2^23: no overflow; the INF-initialised
+  // accumulator clamps every E at INF.)
+  auto a_prime = [&](int u, int k) -> int32_t {
+    int32_t a = __ldg(gA + (int64_t)u * NSP + k);
+    if (ks >= 0 && u >= skip + 2) a += __ldg(gRs + ((int64_t)u * NSP + ks) * NSP + k);
+    return a;
+  };
   auto stage_word = [&](int u, int e, int w) -> int32_t {
-    if (w < NS * NSP) return __ldg(gR + (int64_t)e * NSP * NSP + w);
+    if (w < NS * NSP) return __ldg(gR + (int64_t)e * NSP * NSP + w) + a_prime(u, w / NSP);
     const int x = w - NS * NSP, k = x >> 1;
     if (x & 1) {
       int32_t m = min(__ldg(gM + (int64_t)u * NSP + k), MBIG);
       if (ks >= 0 && u == skip && k != ks) m = MBIG;
       return m;
     }
-    int32_t a = __ldg(gA + (int64_t)u * NSP + k);
-    if (ks >= 0 && u >= skip + 2) a += __ldg(gRs + ((int64_t)u * NSP + ks) * NSP + k);
-    return a;
+    return a_prime(u, k);
   };
   int32_t pre[PER];
   auto fetch_stage = [&](int step, int u_next) {  // global -> registers (issued early)
@@ -269,7 +277,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       const int32_t gk = k * ROW * 4 - 4;          // the row's guard word
 #pragma unroll
       for (int j = 0; j < V; ++j)
-        d[k][j] = addmin(*reinterpret_cast<const int32_t*>(Ec + __viaddmax_s32(bk, j * T * 4, gk)), am.x, INF);
+        d[k][j] = *reinterpret_cast<const int32_t*>(Ec + __viaddmax_s32(bk, j * T * 4, gk));
     }
     if constexpr (CL) {
       // buckets whose shifted source q - M lies in a lower CTA's range: the
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
               const int lx = j * T + t - am.y;
               const int x = lx + rank * B;
               if (lx < 0 && x >= 0)
-                d[k][j] = addmin(*map_rank(Eb + k * ROW + (x & (B - 1)), (uint32_t)(x / B)), am.x, INF);
+                d[k][j] = *map_rank(Eb + k * ROW + (x & (B - 1)), (uint32_t)(x / B));
             }
           }
         }
