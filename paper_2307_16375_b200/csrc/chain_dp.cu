@@ -64,7 +64,9 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
     }
   }
   if (C > 16) return false;
+  static const int pref_v = env_int("UNIAP_K2_V", 2);  // tuning knob (experiments)
   K2Class c{NS, 2, B / 2, C};
+  if (B == 1024 && pref_v == 4 && NS <= 16) { c.V = 4; c.T = 256; }
   if (B == 32) { c.V = 1; c.T = 32; }
   if (B == 2048) { c.V = 4; c.T = 512; }
   if (B == 4096) { c.V = 8; c.T = 512; }

@@ -270,9 +270,11 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     // rowb_k + 4x; x < 0 is clamped onto the guard word at rowb_k - 4 by one
     // VIADDMNMX (max form), so a cell costs VIADDMNMX + LDS + VIADDMNMX.
     const char* Ec = reinterpret_cast<const char*>(Eb);
+    int32_t mmax = 0;  // largest shift of this layer (for the DSMEM fix-up test)
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int2 am = *reinterpret_cast<const int2*>(Tb + NS * NSP + 2 * k);
+      if constexpr (CL) mmax = max(mmax, am.y);
       const int32_t bk = (k * ROW + t - am.y) * 4;  // byte offset of bucket t - M in row k
       const int32_t gk = k * ROW * 4 - 4;          // the row's guard word
 #pragma unroll
@@ -283,8 +285,8 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       // buckets whose shifted source q - M lies in a lower CTA's range: the
       // local read above returned the guard (INF); fetch the value over DSMEM
       cl_wait();
-      if (rank > 0) {
-        const int wbase = t & ~31;
+      const int wbase = t & ~31;
+      if (rank > 0 && wbase < mmax) {  // warp-uniform: rare
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
           const int2 am = *reinterpret_cast<const int2*>(Tb + NS * NSP + 2 * k);
@@ -337,6 +339,7 @@ k2_fn k2_get(int V, int T, bool CL) {
   UNIAP_SHAPE(2, 128)
   UNIAP_SHAPE(2, 256)
   UNIAP_SHAPE(2, 512)
+  if constexpr (NS <= 16) { UNIAP_SHAPE(4, 256) }
   if constexpr (NS <= 12) { UNIAP_SHAPE(4, 512) }
   if constexpr (NS <= 6) { UNIAP_SHAPE(8, 512) }
 #undef UNIAP_SHAPE
