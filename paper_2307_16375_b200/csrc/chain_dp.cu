@@ -64,9 +64,13 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
     }
   }
   if (C > 16) return false;
-  static const int pref_v = env_int("UNIAP_K2_V", 2);  // tuning knob (experiments)
+  // One CTA per instance (C = 1): 4 buckets x 256 threads, so two CTAs
+  // (two independent instances) share an SM and overlap each other's
+  // barrier / shift phases; clusters keep 2 x 512 (one CTA per SM by shared
+  // memory, so more threads per CTA).  UNIAP_K2_V overrides (experiments).
+  static const int pref_v = env_int("UNIAP_K2_V", 0);
   K2Class c{NS, 2, B / 2, C};
-  if (B == 1024 && pref_v == 4 && NS <= 16) { c.V = 4; c.T = 256; }
+  if (B == 1024 && NS <= 16 && (pref_v == 4 || (pref_v == 0 && C == 1))) { c.V = 4; c.T = 256; }
   if (B == 32) { c.V = 1; c.T = 32; }
   if (B == 2048) { c.V = 4; c.T = 512; }
   if (B == 4096) { c.V = 8; c.T = 512; }
