@@ -43,6 +43,23 @@ int round4(int x) { return (x + 3) & ~3; }
 
 }  // namespace
 
+// one K2 launch: instances of one kernel class
+struct K2Group {
+  size_t s, e;  // [s, e) in the uploaded instance array
+  K2Class cls;
+  double crit;
+  int max_inst;  // device-sized launches (backward): grid bound
+};
+
+struct RunPlan {
+  bool valid = false;
+  int rank = 0, world = 1;
+  const uniap_record* rec = nullptr;
+  std::vector<int32_t> local;
+  std::vector<K2Group> fgrp, bgrp;
+  int max_deg = 0;
+};
+
 struct uniap_handle {
   int device = 0;
   cudaStream_t st = nullptr;
@@ -78,7 +95,46 @@ struct uniap_handle {
   std::vector<cudaStream_t> side;          // K2 classes run concurrently
   std::vector<cudaEvent_t> side_ev;
   cudaEvent_t fork_ev = nullptr;
+  RunPlan plan;                            // launch plan of the last (rank, world)
+  DevBuf<int32_t> clsid;
+  DevBuf<BwPlan> bwp;
+  cudaGraphExec_t graph_exec = nullptr;    // the captured pipeline of `plan`
+  uint32_t graph_launches = 0, graph_k2 = 0;
+  bool capturing = false, timed = false;
+  std::vector<int64_t> sig;                // what the captured graph depends on
 };
+
+// A prepared problem keeps the launch plan and the captured graph when
+// nothing they depend on changed (shapes, classes, offsets, buffers, and the
+// kernel-parameter values of the builder); otherwise both are rebuilt.
+static void update_signature(uniap_handle* h) {
+  std::vector<int64_t> sg = {h->L, h->Q, h->ncfg, h->skip, h->level2, h->n_edges, h->arena_words};
+  for (int i = 0; i < h->ncfg; ++i) {
+    const CfgDev& d = h->cfg[i];
+    const K2Class& k = h->cls[i];
+    for (int64_t x : {(int64_t)d.deg, (int64_t)d.c, (int64_t)d.S, (int64_t)d.NSP, (int64_t)d.skip, d.offA, d.offP,
+                      (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C})
+      sg.push_back(x);
+  }
+  if (h->level2) {
+    const int64_t* c = reinterpret_cast<const int64_t*>(&h->cl);
+    for (size_t i = 0; i < sizeof(ClusterDev) / 8; ++i) sg.push_back(c[i]);
+  }
+  for (const void* p : {(const void*)h->arena.p, (const void*)h->ns.p, (const void*)h->dcfg.p, (const void*)h->dcat.p,
+                        (const void*)h->fwd.p, (const void*)h->act.p, (const void*)h->ps.p, (const void*)h->ctx.p,
+                        (const void*)h->tpc.p, (const void*)h->chain.p, (const void*)h->skipb.p,
+                        (const void*)h->edges.p, (const void*)h->qcfg.p, (const void*)h->qmax.p,
+                        (const void*)h->qglob.p})
+    sg.push_back(reinterpret_cast<int64_t>(p));
+  if (sg != h->sig) {
+    h->sig.swap(sg);
+    h->plan.valid = false;
+    if (h->graph_exec) {
+      cudaGraphExecDestroy(h->graph_exec);
+      h->graph_exec = nullptr;
+    }
+  }
+}
 
 // every host<->device copy goes through these (counted for the e2e report)
 static cudaError_t h2d(uniap_handle* h, void* dst, const void* src, size_t bytes) {
@@ -191,6 +247,9 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->qglob, &h->gofs, &h->qmax, &h->fwd, &h->act, &h->ps, &h->ctx,
                   &h->tpc, &h->chain, &h->skipb, &h->edges})
     b->release();
+  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+  h->clsid.release();
+  h->bwp.release();
   h->dcfg.release();
   h->dcat.release();
   h->inst.release();
@@ -206,6 +265,8 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   delete h;
 }
 
+static void plan_instances(int L, int i, int deg, int S, int skip, bool all_intervals, std::vector<Inst>& out);
+
 // ---------------------------------------------------------------------------
 // Layout of the configs in the device arena.
 // ---------------------------------------------------------------------------
@@ -216,8 +277,12 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<int>& S, c
   h->cls.assign(h->ncfg, K2Class{});
   int64_t off = 0;
   for (int i = 0; i < h->ncfg; ++i) {
+    // a config with only a few (long) chains spreads each over more SMs
+    std::vector<Inst> v;
+    plan_instances(L, i, deg[i], S[i], skipc[i], false, v);
+    const bool single = !v.empty() && v.size() <= 4;
     K2Class k;
-    if (!k2_pick_class(S[i], h->Q, deg[i] == 1, &k)) FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
+    if (!k2_pick_class(S[i], h->Q, single, &k)) FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
     h->cls[i] = k;
     CfgDev& d = h->cfg[i];
     const int NSP = round4(k.NS);
@@ -323,6 +388,7 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
   CK(h, h2d(h, h->arena.p, a.data(), a.size() * 4));
   CK(h, h2d(h, h->dcfg.p, h->cfg.data(), h->ncfg * sizeof(CfgDev)));
   CK(h, cudaStreamSynchronize(h->st));
+  update_signature(h);
   h->ready = true;
   return UNIAP_OK;
 }
@@ -413,7 +479,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   }
   uniap_status st = layout_configs(h, S, deg, c, g, skc);
   if (st != UNIAP_OK) return st;
-  h->cl = ClusterDev{cl->n_dev, cl->node_size, cl->ccoc_permille, o->B, o->precision, o->Q, NT,
+  h->cl = ClusterDev{cl->n_dev, cl->node_size, cl->ccoc_permille, o->B, o->precision, o->Q, NT, 0,
                      cl->mem_bytes, cl->mem_reserve_bytes, cl->bw_intra_Bps, cl->bw_inter_Bps, cl->p2p_Bps,
                      cl->lat_ns, o->quantum_ns};
   h->n_edges = m->n_edges;
@@ -445,6 +511,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   CK(h, up(h->dcfg.p, h->cfg.data(), h->ncfg * sizeof(CfgDev)));
   CK(h, up(h->dcat.p, h->cat.data(), h->ncfg * sizeof(CatDev)));
   CK(h, cudaStreamSynchronize(h->st));
+  update_signature(h);
   h->ready = true;
   return UNIAP_OK;
 }
@@ -533,61 +600,76 @@ extern "C" uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32
   return UNIAP_OK;
 }
 
-// Groups instances by kernel class and launches K2 for each group.
-static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, DevBuf<Inst>& buf, int32_t* Pdev) {
-  // stable order: class, then longest sweep first (LPT within the launch)
-  std::vector<int> clsid(all.size());
-  for (size_t j = 0; j < all.size(); ++j) {
-    const K2Class& k = h->cls[all[j].cfg];
-    clsid[j] = k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C;
-  }
+// ---------------------------------------------------------------------------
+// K2 launch groups: instances grouped by kernel class (one launch each),
+// sorted longest sweep first (LPT within the launch); classes run
+// concurrently on side streams (fork / join with events), longest critical
+// path first -- the serial chain of one instance: layers x a model of one
+// layer's time (its relaxations at the CTA's share of the ALU rate plus the
+// per-layer synchronisation) -- so it starts on free SMs.
+// ---------------------------------------------------------------------------
+
+static int class_key(const K2Class& k) { return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C; }
+
+static void group_instances(const uniap_handle* h, std::vector<Inst>& all, std::vector<K2Group>& grp) {
+  std::vector<int> key(all.size());
+  for (size_t j = 0; j < all.size(); ++j) key[j] = class_key(h->cls[all[j].cfg]);
   std::vector<size_t> idx(all.size());
   std::iota(idx.begin(), idx.end(), 0);
   std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
-    if (clsid[a] != clsid[b]) return clsid[a] < clsid[b];
+    if (key[a] != key[b]) return key[a] < key[b];
     return all[a].n > all[b].n;
   });
   std::vector<Inst> sorted(all.size());
   for (size_t j = 0; j < idx.size(); ++j) sorted[j] = all[idx[j]];
-  CK(h, buf.ensure(sorted.size()));
-  if (!sorted.empty())
-    CK(h, h2d(h, buf.p, sorted.data(), sorted.size() * sizeof(Inst)));
-  // one launch per class; classes run concurrently on side streams (fork /
-  // join with events) so small classes fill the tail of the heavy one
-  // launch order: longest critical path first (the serial chain of one
-  // instance: layers x per-CTA work of a layer), so it starts on free SMs
-  struct Grp { size_t s, e; double crit; };
-  std::vector<Grp> grp;
+  grp.clear();
   for (size_t s = 0; s < sorted.size();) {
     size_t e = s;
-    const int id = clsid[idx[s]];
+    const int id = class_key(h->cls[sorted[s].cfg]);
     double c = 0;
-    while (e < sorted.size() && clsid[idx[e]] == id) {
+    while (e < sorted.size() && class_key(h->cls[sorted[e].cfg]) == id) {
       const K2Class& k = h->cls[sorted[e].cfg];
-      c = std::max(c, (double)sorted[e].n * k.NS * k.NS * k.T * k.V);
+      const double step = (double)k.NS * k.NS * k.T * k.V / (64.0 * std::min(1.0, k.T / 512.0)) + 3000.0 +
+                          (k.C > 1 ? 3000.0 : 0.0);
+      c = std::max(c, (double)sorted[e].n * step);
       ++e;
     }
-    grp.push_back(Grp{s, e, c});
+    grp.push_back(K2Group{s, e, h->cls[sorted[s].cfg], c, 0});
     s = e;
   }
-  std::stable_sort(grp.begin(), grp.end(), [](const Grp& a, const Grp& b) { return a.crit > b.crit; });
+  std::stable_sort(grp.begin(), grp.end(), [](const K2Group& a, const K2Group& b) { return a.crit > b.crit; });
+  all.swap(sorted);
+}
+
+static uniap_status ensure_side_streams(uniap_handle* h, size_t n) {
+  while (h->side.size() < n) {
+    cudaStream_t x;
+    cudaEvent_t ev;
+    CK(h, cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    CK(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    h->side.push_back(x);
+    h->side_ev.push_back(ev);
+  }
+  return UNIAP_OK;
+}
+
+// Enqueue K2 launches of `grp` (instances at `dinst`) on h->st with fork/join.
+static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp, const Inst* dinst,
+                               const int32_t* dcount_per_class, int32_t* Pdev) {
   const bool fork = grp.size() > 1;
   if (fork) {
-    while (h->side.size() < grp.size()) {
-      cudaStream_t x;
-      cudaEvent_t ev;
-      CK(h, cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
-      CK(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      h->side.push_back(x);
-      h->side_ev.push_back(ev);
-    }
+    uniap_status s = ensure_side_streams(h, grp.size());
+    if (s != UNIAP_OK) return s;
     CK(h, cudaEventRecord(h->fork_ev, h->st));
   }
   for (size_t g = 0; g < grp.size(); ++g) {
     cudaStream_t st = fork ? h->side[g] : h->st;
     if (fork) CK(h, cudaStreamWaitEvent(st, h->fork_ev, 0));
-    K2Args args{buf.p + grp[g].s, h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip};
-    CK(h, k2_launch(h->cls[sorted[grp[g].s].cfg], args, (int)(grp[g].e - grp[g].s), st));
+    const int n = dcount_per_class ? grp[g].max_inst : (int)(grp[g].e - grp[g].s);
+    K2Args args{dcount_per_class ? dinst : dinst + grp[g].s,
+                dcount_per_class ? dcount_per_class + g : nullptr,
+                h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip};
+    CK(h, k2_launch(grp[g].cls, args, n, st));
     h->launches++;
     h->k2_launches++;
     if (fork) CK(h, cudaEventRecord(h->side_ev[g], st));
@@ -597,9 +679,129 @@ static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, De
   return UNIAP_OK;
 }
 
+static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, DevBuf<Inst>& buf, int32_t* Pdev) {
+  std::vector<K2Group> grp;
+  group_instances(h, all, grp);
+  CK(h, buf.ensure(all.size()));
+  if (!all.empty()) CK(h, h2d(h, buf.p, all.data(), all.size() * sizeof(Inst)));
+  return enqueue_k2(h, grp, buf.p, nullptr, Pdev);
+}
+
 static BuildBufs build_bufs(uniap_handle* h) {
   return BuildBufs{h->fwd.p, h->act.p, h->ps.p, h->ctx.p, h->tpc.p, h->chain.p, h->skipb.p, h->edges.p,
                    h->n_edges, h->dcat.p, h->ns.p, h->qcfg.p, h->qmax.p, h->qglob.p};
+}
+
+// ---------------------------------------------------------------------------
+// The launch plan of one (rank, world): data-independent, uploaded once.
+// ---------------------------------------------------------------------------
+static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_record* rec) {
+  RunPlan& R = h->plan;
+  std::vector<int> owner;
+  lpt(h, world, owner);
+  R.local.clear();
+  for (int i = 0; i < h->ncfg; ++i)
+    if (owner[i] == rank) R.local.push_back(i);
+  const int nl = (int)R.local.size();
+  // forward instances
+  std::vector<Inst> fw;
+  for (int i : R.local) forward_instances(h, i, false, fw);
+  h->cells = h->relax = 0;
+  for (auto& x : fw) {
+    const uint64_t S = h->cfg[x.cfg].S;
+    h->cells += (uint64_t)x.n * S * h->Q;
+    h->relax += (uint64_t)(x.n - 1) * S * S * h->Q;
+  }
+  group_instances(h, fw, R.fgrp);
+  // backward: one device-sized launch per kernel class of the local configs
+  std::vector<int32_t> cls_of_cfg(h->ncfg, 0);
+  R.bgrp.clear();
+  int64_t gmax = 1;
+  R.max_deg = 0;
+  for (int i : R.local) {
+    const CfgDev& d = h->cfg[i];
+    const int copies = d.skip >= 0 ? d.S : 1;
+    const int bound = d.deg + copies - 1;  // stages + extra skip copies of one stage
+    gmax = std::max<int64_t>(gmax, (int64_t)copies * h->L * d.NSP * h->Q);
+    R.max_deg = std::max(R.max_deg, std::min(d.deg, h->L));
+    int g = -1;
+    for (size_t j = 0; j < R.bgrp.size(); ++j)
+      if (class_key(R.bgrp[j].cls) == class_key(h->cls[i])) g = (int)j;
+    if (g < 0) {
+      g = (int)R.bgrp.size();
+      R.bgrp.push_back(K2Group{0, 0, h->cls[i], 0.0, 0});
+    }
+    R.bgrp[g].max_inst = std::max(R.bgrp[g].max_inst, bound);
+    cls_of_cfg[i] = g;
+  }
+  if ((int)R.bgrp.size() > MAXCLS) FAIL(h, UNIAP_ERR_ARG, "too many kernel classes");
+  int max_bw = 1;
+  for (auto& g : R.bgrp) max_bw = std::max(max_bw, g.max_inst);
+  // device buffers + uploads (outside any graph)
+  CK(h, h->P.ensure((size_t)h->ncfg * h->L * h->L));
+  CK(h, h->inst.ensure(std::max<size_t>(fw.size(), 1)));
+  CK(h, h->binst.ensure(max_bw));
+  CK(h, h->G.ensure(gmax));
+  CK(h, h->cfglist.ensure(std::max(nl, 1)));
+  CK(h, h->clsid.ensure(h->ncfg));
+  CK(h, h->thetas.ensure((size_t)std::max(nl, 1) * TMAX));
+  CK(h, h->ntheta.ensure(std::max(nl, 1)));
+  CK(h, h->vals.ensure((size_t)std::max(nl, 1) * (TMAX + 2)));
+  CK(h, h->cfgopt.ensure(h->ncfg));
+  CK(h, h->scratch.ensure((size_t)32 * (MAXL + 1) * (MAXL + 1)));
+  CK(h, h->win.ensure(1));
+  CK(h, h->bwp.ensure(1));
+  if (!fw.empty()) CK(h, h2d(h, h->inst.p, fw.data(), fw.size() * sizeof(Inst)));
+  if (nl > 0) CK(h, h2d(h, h->cfglist.p, R.local.data(), nl * 4));
+  CK(h, h2d(h, h->clsid.p, cls_of_cfg.data(), h->ncfg * 4));
+  std::vector<int64_t> big(h->ncfg, INT64_MAX);  // non-local configs stay "infeasible"
+  CK(h, h2d(h, h->cfgopt.p, big.data(), h->ncfg * 8));
+  CK(h, cudaStreamSynchronize(h->st));
+  R.rank = rank;
+  R.world = world;
+  R.rec = rec;
+  R.valid = true;
+  return UNIAP_OK;
+}
+
+// The whole path for this rank, enqueued on h->st with no host
+// synchronisation (so it can be captured as one CUDA graph).
+static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
+  const RunPlan& R = h->plan;
+  const int L = h->L, nl = (int)R.local.size();
+  if (h->level2) {
+    CK(h, launch_k1(h->cl, build_bufs(h), h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
+    h->launches += 6;
+  }
+  CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
+  h->launches++;
+  CK(h, cudaEventRecordWithFlags(h->ev[1], h->st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+  {
+    uniap_status s = enqueue_k2(h, R.fgrp, h->inst.p, nullptr, h->P.p);
+    if (s != UNIAP_OK) return s;
+  }
+  CK(h, cudaEventRecordWithFlags(h->ev[2], h->st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+  CK(h, launch_k3(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->st));
+  CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
+                  h->cfgopt.p, h->st));
+  RecordArgs ra{rec, h->cells, h->relax, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
+                h->binst.p, h->bwp.p};
+  CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
+                   h->cfgopt.p, h->scratch.p, h->win.p, ra, h->st));
+  h->launches += nl > 0 ? 3 : 1;
+  // traceback: backward sweeps sized on the device, then the strategy walk
+  {
+    uniap_status s = enqueue_k2(h, R.bgrp, h->binst.p, h->bwp.p->count, h->P.p);
+    if (s != UNIAP_OK) return s;
+  }
+  CK(h, launch_k5c_grid(R.max_deg, h->dcfg.p, h->arena.p, h->G.p, h->bwp.p, h->win.p, L, h->cap, rec, h->st));
+  if (R.max_deg > 0) h->launches++;
+  return UNIAP_OK;
+}
+
+static bool env_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && *v != '0';
 }
 
 extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev) {
@@ -607,113 +809,49 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
   if (!h->ready) FAIL(h, UNIAP_ERR_ARG, "nothing prepared");
   if (world < 1 || rank < 0 || rank >= world) FAIL(h, UNIAP_ERR_ARG, "rank %d / world %d", rank, world);
   CK(h, cudaSetDevice(h->device));
-  const int L = h->L;
   uniap_record* rec = rec_dev ? (uniap_record*)rec_dev : nullptr;
   if (!rec) {
     CK(h, h->rec.ensure(1));
     rec = h->rec.p;
   }
   h->last_rec = rec;
+  if (!h->plan.valid || h->plan.rank != rank || h->plan.world != world || h->plan.rec != rec) {
+    if (h->graph_exec) { cudaGraphExecDestroy(h->graph_exec); h->graph_exec = nullptr; }
+    uniap_status s = make_plan(h, rank, world, rec);
+    if (s != UNIAP_OK) return s;
+  }
+  const bool use_graph = !env_flag("UNIAP_NO_GRAPH");
   CK(h, cudaEventRecord(h->ev[0], h->st));
-  // K1: the cost tables of every candidate (the quantum is global)
-  if (h->level2) {
-    CK(h, launch_k1(h->cl, build_bufs(h), h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
-    h->launches += 6;
-  }
-  // this rank's configs
-  std::vector<int> owner;
-  lpt(h, world, owner);
-  std::vector<int32_t> local;
-  for (int i = 0; i < h->ncfg; ++i)
-    if (owner[i] == rank) local.push_back(i);
-  const int nl = (int)local.size();
-  // K2 forward
-  std::vector<Inst> fw;
-  for (int i : local) forward_instances(h, i, false, fw);
-  h->cells = h->relax = 0;
-  for (auto& x : fw) {
-    const uint64_t S = h->cfg[x.cfg].S;
-    h->cells += (uint64_t)x.n * S * h->Q;
-    h->relax += (uint64_t)(x.n - 1) * S * S * h->Q;
-  }
-  CK(h, h->P.ensure((size_t)h->ncfg * L * L));
-  CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
-  h->launches++;
-  CK(h, h->G.ensure(1));
-  CK(h, cudaEventRecord(h->ev[1], h->st));
-  {
-    uniap_status s = launch_k2_groups(h, fw, h->inst, h->P.p);
-    if (s != UNIAP_OK) return s;
-  }
-  CK(h, cudaEventRecord(h->ev[2], h->st));
-  // K3, K4, K5a
-  CK(h, h->cfglist.ensure(std::max(nl, 1)));
-  CK(h, h->thetas.ensure((size_t)std::max(nl, 1) * TMAX));
-  CK(h, h->ntheta.ensure(std::max(nl, 1)));
-  CK(h, h->vals.ensure((size_t)std::max(nl, 1) * (TMAX + 2)));
-  CK(h, h->cfgopt.ensure(h->ncfg));
-  CK(h, h->scratch.ensure((size_t)32 * (MAXL + 1) * (MAXL + 1)));
-  CK(h, h->win.ensure(1));
-  {
-    std::vector<int64_t> big(h->ncfg, INT64_MAX);
-    CK(h, h2d(h, h->cfgopt.p, big.data(), h->ncfg * 8));
-  }
-  if (nl > 0) CK(h, h2d(h, h->cfglist.p, local.data(), nl * 4));
-  CK(h, launch_k3(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->st));
-  CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
-                  h->cfgopt.p, h->st));
-  CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
-                   h->cfgopt.p, h->scratch.p, h->win.p, h->st));
-  h->launches += nl > 0 ? 3 : 1;
-  Winner W;
-  int64_t qg[2] = {0, 0};
-  CK(h, d2h(h, &W, h->win.p, sizeof(Winner)));
-  if (h->level2) CK(h, d2h(h, qg, h->qglob.p, 16));
-  CK(h, cudaStreamSynchronize(h->st));
-  h->quantum = h->level2 ? qg[0] : 0;
-  // record template (counters, status); K5c fills the assignment
-  uniap_record& R = h->rec_host;
-  memset(&R, 0, sizeof R);
-  R.objective = INT64_MAX;
-  R.cfg_index = -1;
-  R.L = L;
-  R.n_cfg_local = nl;
-  R.dp_cells = h->cells;
-  R.dp_relax = h->relax;
-  if (h->level2 && qg[1] != 0) R.status = UNIAP_ERR_RANGE;
-  else if (nl > 0 && W.cfg >= 0 && W.status != 0) R.status = UNIAP_ERR_INTERNAL;
-  CK(h, h2d(h, rec, &R, sizeof R));
-  if (R.status == 0 && nl > 0 && W.cfg >= 0 && W.objective != INT64_MAX) {
-    // K2 backward sweeps: one per stage (per ks when the skip source
-    // conditions the stage), storing every layer's G[u][k][q]
-    const CfgDev& d = h->cfg[W.cfg];
-    std::vector<Inst> bw;
-    std::vector<int64_t> gofs(W.deg * 33, 0);
-    int64_t goff = 0;
-    int a = 0;
-    for (int s = 0; s < W.deg; ++s) {
-      const int b = W.end[s], n = b - a + 1;
-      const bool cond = d.skip >= 0 && a <= d.skip && d.skip + 2 <= b;
-      for (int ks = cond ? 0 : -1; ks < (cond ? d.S : 0); ++ks) {
-        gofs[s * 33 + ks + 1] = goff;
-        bw.push_back(Inst{W.cfg, b, n, ks, -1, 0, goff});
-        goff += (int64_t)n * d.NSP * h->Q;
-      }
-      a = b + 1;
+  if (use_graph) {
+    if (!h->graph_exec) {
+      // capture the pipeline once; replay it on every later run of this plan
+      const uint32_t l0 = h->launches, k0 = h->k2_launches;
+      CK(h, cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+      h->capturing = true;
+      uniap_status s = enqueue_pipeline(h, rec);
+      h->capturing = false;
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(h->st, &g);
+      if (s != UNIAP_OK) { if (g) cudaGraphDestroy(g); return s; }
+      CK(h, e);
+      e = cudaGraphInstantiate(&h->graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      CK(h, e);
+      h->graph_launches = h->launches - l0;
+      h->graph_k2 = h->k2_launches - k0;
+      h->launches = l0;
+      h->k2_launches = k0;
     }
-    CK(h, h->G.ensure(goff));
-    CK(h, h->gofs.ensure(gofs.size()));
-    CK(h, h2d(h, h->gofs.p, gofs.data(), gofs.size() * 8));
-    uniap_status s = launch_k2_groups(h, bw, h->binst, h->P.p);
+    CK(h, cudaGraphLaunch(h->graph_exec, h->st));
+    h->launches += h->graph_launches;
+    h->k2_launches += h->graph_k2;
+  } else {
+    uniap_status s = enqueue_pipeline(h, rec);
     if (s != UNIAP_OK) return s;
-    CK(h, launch_k5c_grid(W.deg, h->dcfg.p, h->arena.p, h->G.p, h->gofs.p, h->win.p, L, h->cap, h->skip, rec, h->st));
-    h->launches++;
   }
   CK(h, cudaEventRecord(h->ev[3], h->st));
-  CK(h, cudaStreamSynchronize(h->st));
   CK(h, cudaGetLastError());
-  cudaEventElapsedTime(&h->ms_dp, h->ev[1], h->ev[2]);
-  cudaEventElapsedTime(&h->ms_total, h->ev[0], h->ev[3]);
+  h->timed = true;
   return UNIAP_OK;
 }
 
@@ -724,6 +862,20 @@ extern "C" uniap_status uniap_fetch(uniap_handle* h, uniap_result* out) {
   const uniap_record* src = h->last_rec;
   if (!src) FAIL(h, UNIAP_ERR_ARG, "nothing has run on this handle");
   CK(h, d2h(h, &R, src, sizeof R));
+  if (h->level2) {
+    int64_t qg[2];
+    CK(h, d2h(h, qg, h->qglob.p, 16));
+    CK(h, cudaStreamSynchronize(h->st));
+    h->quantum = qg[0];
+  } else {
+    h->quantum = 0;
+  }
+  if (h->timed) {
+    CK(h, cudaStreamSynchronize(h->st));
+    cudaEventElapsedTime(&h->ms_dp, h->ev[1], h->ev[2]);
+    cudaEventElapsedTime(&h->ms_total, h->ev[0], h->ev[3]);
+    h->timed = false;
+  }
   int64_t* keep = out->cfg_objective;
   memset(out, 0, sizeof *out);
   out->cfg_objective = keep;

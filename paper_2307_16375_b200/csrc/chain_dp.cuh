@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     rank = (int)cl_rank();
     ii = blockIdx.x / (int)cl_size();
   }
+  if (args.n_inst && ii >= *args.n_inst) return;  // device-sized launch: spare CTA (whole cluster)
   const Inst in = args.inst[ii];
   const CfgDev cf = args.cfg[in.cfg];
   const int32_t* __restrict__ gA = args.arena + cf.offA;

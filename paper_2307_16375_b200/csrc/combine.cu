@@ -273,8 +273,8 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
                                                   const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
                                                   int n_local, int L, const int32_t* __restrict__ thetas,
                                                   const int32_t* __restrict__ ntheta, const int64_t* __restrict__ vals,
-                                                  int64_t* __restrict__ cfg_opt, int32_t* __restrict__ scratch,
-                                                  Winner* __restrict__ win) {
+                                                  const int64_t* __restrict__ cfg_opt, int32_t* __restrict__ scratch,
+                                                  Winner* __restrict__ win, RecordArgs ra) {
   __shared__ int32_t sP[MAXL * MAXL];
   __shared__ int32_t sO[MAXL];
   __shared__ int32_t stars[TMAX];
@@ -306,6 +306,27 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
   }
   __syncthreads();
   const int wl = s_win;
+  // the record header: every field K5c does not write (assignment arrays zeroed)
+  if (t < UNIAP_MAX_LAYERS) {
+    uniap_record* r = ra.rec;
+    r->stage_of[t] = 0;
+    r->strategy_of[t] = 0;
+    r->stage_cost[t] = 0;
+    r->cut_cost[t] = 0;
+    r->stage_mem[t] = 0;
+  }
+  if (t < MAXCLS) ra.bw->count[t] = 0;
+  if (t == 0) {
+    uniap_record* r = ra.rec;
+    r->objective = INT64_MAX;
+    r->cfg_index = -1;
+    r->deg = r->c = 0;
+    r->L = ra.L;
+    r->status = (ra.qglob && ra.qglob[1] != 0) ? UNIAP_ERR_RANGE : 0;
+    r->n_cfg_local = ra.n_local;
+    r->dp_cells = ra.cells;
+    r->dp_relax = ra.relax;
+  }
   if (wl < 0) {
     if (t == 0) { win->objective = INT64_MAX; win->cfg = -1; win->status = 0; }
     return;
@@ -418,13 +439,35 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
       win->o[i] = (i + 1 < deg) ? sO[b] : 0;
       a = b + 1;
     }
+    uniap_record* r = ra.rec;
+    if (!have) r->status = UNIAP_ERR_INTERNAL;
+    r->objective = OPT;
+    r->cfg_index = ci;
+    r->deg = deg;
+    r->c = cf.c;
+    // the backward sweeps of the traceback: one per stage, one per skip
+    // conditioning ks when the stage contains the skip source and an edge of it
+    int n = 0;
+    int64_t goff = 0;
+    a = 0;
+    for (int i = 0; i < deg && have && r->status == 0; ++i) {
+      const int b = best_end[i], len = b - a + 1;
+      const bool cond = cf.skip >= 0 && a <= cf.skip && cf.skip + 2 <= b;
+      for (int ks = cond ? 0 : -1; ks < (cond ? cf.S : 0); ++ks) {
+        ra.bw->gofs[i * 33 + ks + 1] = goff;
+        ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff};
+        goff += (int64_t)len * cf.NSP * (ra.cap + 1);
+      }
+      a = b + 1;
+    }
+    ra.bw->count[ra.cls_of_cfg[ci]] = n;
   }
 }
 
 cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
-                       int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals, int64_t* cfg_opt,
-                       int32_t* scratch, Winner* win, cudaStream_t st) {
-  k5a_winner<<<1, K5T, 0, st>>>(cfg, arena, P, cfg_list, n_local, L, thetas, ntheta, vals, cfg_opt, scratch, win);
+                       int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals, const int64_t* cfg_opt,
+                       int32_t* scratch, Winner* win, const RecordArgs& ra, cudaStream_t st) {
+  k5a_winner<<<1, K5T, 0, st>>>(cfg, arena, P, cfg_list, n_local, L, thetas, ntheta, vals, cfg_opt, scratch, win, ra);
   return cudaGetLastError();
 }
 
@@ -436,15 +479,17 @@ cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P
 // Also writes the record (objective, placement, costs, memory).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
-                                                 const int32_t* __restrict__ G, const int64_t* __restrict__ gofs,
-                                                 const Winner* __restrict__ win, int L, int cap, int skip,
+                                                 const int32_t* __restrict__ G, const BwPlan* __restrict__ bw,
+                                                 const Winner* __restrict__ win, int L, int cap,
                                                  uniap_record* __restrict__ rec) {
   __shared__ int32_t vec[32][MAXL];
   __shared__ int32_t mem[32];
   __shared__ int32_t okw[32];
   const int stage = blockIdx.x;
   const Winner& W = *win;  // by reference: fields are read on demand, no per-thread copy
+  if (W.cfg < 0 || W.objective == INT64_MAX || W.status != 0 || stage >= W.deg || rec->status != 0) return;
   const CfgDev cf = cfgs[W.cfg];
+  int skip;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int a = stage == 0 ? 0 : W.end[stage - 1] + 1, b = W.end[stage];
   skip = cf.skip;
@@ -458,7 +503,7 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
   bool ok = false;
   if (w < nks) {
     const int ks = cond ? w : -1;
-    const int32_t* g = G + gofs[stage * 33 + (ks + 1)];
+    const int32_t* g = G + bw->gofs[stage * 33 + (ks + 1)];
     int64_t rest = W.p[stage];
     int q = cap, kprev = -1;
     int32_t msum = 0;
@@ -509,20 +554,14 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
       rec->stage_cost[stage] = W.p[stage];
       rec->cut_cost[stage] = W.o[stage];
     }
-    if (stage == 0) {
-      rec->objective = W.objective;
-      rec->cfg_index = W.cfg;
-      rec->deg = W.deg;
-      rec->c = W.c;
-      rec->L = L;
-    }
   }
 }
 
-cudaError_t launch_k5c_grid(int deg, const CfgDev* cfg, const int32_t* arena, const int32_t* G,
-                            const int64_t* gofs_stage_ks, const Winner* win, int L, int cap, int skip,
-                            uniap_record* rec, cudaStream_t st) {
-  k5c_walk<<<deg, 1024, 0, st>>>(cfg, arena, G, gofs_stage_ks, win, L, cap, skip, rec);
+cudaError_t launch_k5c_grid(int max_deg, const CfgDev* cfg, const int32_t* arena, const int32_t* G,
+                            const BwPlan* bw, const Winner* win, int L, int cap, uniap_record* rec,
+                            cudaStream_t st) {
+  if (max_deg <= 0) return cudaSuccess;
+  k5c_walk<<<max_deg, 1024, 0, st>>>(cfg, arena, G, bw, win, L, cap, rec);
   return cudaGetLastError();
 }
 

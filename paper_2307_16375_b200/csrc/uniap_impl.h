@@ -46,6 +46,7 @@ struct Inst {
 
 struct K2Args {
   const Inst* inst;
+  const int32_t* n_inst;  // device count of valid instances (backward), or nullptr
   const CfgDev* cfg;
   const int32_t* arena;
   int32_t* P;
@@ -77,6 +78,22 @@ struct Winner {
   int64_t p[MAXL], o[MAXL];
 };
 
+// Backward-sweep plan written on the device by K5a for the winner config.
+constexpr int MAXCLS = 32;
+struct BwPlan {
+  int32_t count[MAXCLS];     // backward instances per kernel class (0 but the winner's)
+  int64_t gofs[MAXL * 33];   // G word offset per (stage, ks + 1)
+};
+struct RecordArgs {          // what K5a writes into the record besides the winner
+  uniap_record* rec;
+  uint64_t cells, relax;
+  int32_t n_local, L, cap;
+  const int64_t* qglob;      // builder flags (level 2) or nullptr
+  const int32_t* cls_of_cfg; // kernel class id per config
+  Inst* bw_inst;             // out: backward instances of the winner
+  BwPlan* bw;                // out
+};
+
 // combine.cu
 cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st);
 cudaError_t launch_k3(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
@@ -86,14 +103,15 @@ cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P,
                       int64_t* cfg_opt, cudaStream_t st);
 cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
                        int n_local, int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals,
-                       int64_t* cfg_opt, int32_t* scratch, Winner* win, cudaStream_t st);
-cudaError_t launch_k5c_grid(int deg, const CfgDev* cfg, const int32_t* arena, const int32_t* G,
-                            const int64_t* gofs_stage_ks, const Winner* win, int L, int cap, int skip,
-                            uniap_record* rec, cudaStream_t st);
+                       const int64_t* cfg_opt, int32_t* scratch, Winner* win, const RecordArgs& ra,
+                       cudaStream_t st);
+cudaError_t launch_k5c_grid(int max_deg, const CfgDev* cfg, const int32_t* arena, const int32_t* G,
+                            const BwPlan* bw, const Winner* win, int L, int cap, uniap_record* rec,
+                            cudaStream_t st);
 
 // builder.cu (K1)
 struct ClusterDev {
-  int32_t n_dev, node_size, ccoc, B, prec, Q, NT;
+  int32_t n_dev, node_size, ccoc, B, prec, Q, NT, pad;  // no implicit padding (hashed bytewise)
   int64_t mem_bytes, mem_reserve, bw_intra, bw_inter, p2p, lat, quantum;
 };
 struct CatDev {  // per config: catalogue (t,f,d) of its strategies
