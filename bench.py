@@ -170,7 +170,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2307_16375_b200 as pkg
 
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream shared by the library, the timing
+    # events and the NCCL exchange, so everything is ordered on one stream
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     h = pkg.Handle(local, stream.cuda_stream)
     RB = pkg.RECORD_BYTES
     rec = torch.zeros(RB, dtype=torch.uint8, device="cuda")
