@@ -80,8 +80,10 @@ typedef struct {
   int64_t* cfg_objective;                     /* IN: caller array [n_cfg] or NULL; OUT: per-config
                                                  optimum (INT64_MAX = infeasible)                 */
   int64_t quantum_ns;                         /* time quantum used (level 2), 0 for level 1       */
-  uint64_t dp_cells;                          /* chain-DP cells (instance, layer, strategy, bucket) */
-  uint64_t dp_relax;                          /* min-plus relaxations of the chain DP              */
+  uint64_t dp_cells;                          /* chain-DP cells executed (instance, layer, strategy, bucket) */
+  uint64_t dp_relax;                          /* min-plus relaxations executed by the chain DP      */
+  uint64_t dp_cells_canonical;                /* cells of the canonical plan (one forward sweep per
+                                                 start layer): the workload size */
   double ms_gpu_dp;                           /* device time of the chain-DP kernels (ms)          */
   double ms_gpu_total;                        /* device time of the whole path (ms)                */
   uint64_t h2d_bytes, d2h_bytes;              /* host<->device bytes since the last prepare        */
@@ -194,7 +196,7 @@ typedef struct {                      /* fixed-size record exchanged between ran
   int32_t stage_of[UNIAP_MAX_LAYERS], strategy_of[UNIAP_MAX_LAYERS];
   int64_t stage_cost[UNIAP_MAX_LAYERS], cut_cost[UNIAP_MAX_LAYERS];
   int32_t stage_mem[UNIAP_MAX_LAYERS];
-  uint64_t dp_cells, dp_relax;
+  uint64_t dp_cells, dp_relax, dp_cells_canonical;
 } uniap_record;
 
 /* Deterministic LPT assignment of the n_cfg candidates of the prepared

@@ -40,7 +40,8 @@ class uniap_result(C.Structure):
                 ("L", C.c_int32), ("stage_of", C.c_int32 * MAX_L), ("strategy_of", C.c_int32 * MAX_L),
                 ("stage_cost", C.c_int64 * MAX_L), ("cut_cost", C.c_int64 * MAX_L),
                 ("stage_mem", C.c_int32 * MAX_L), ("cfg_objective", _P64), ("quantum_ns", C.c_int64),
-                ("dp_cells", C.c_uint64), ("dp_relax", C.c_uint64), ("ms_gpu_dp", C.c_double),
+                ("dp_cells", C.c_uint64), ("dp_relax", C.c_uint64), ("dp_cells_canonical", C.c_uint64),
+                ("ms_gpu_dp", C.c_double),
                 ("ms_gpu_total", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("n_launches", C.c_uint32), ("n_k2_launches", C.c_uint32)]
 
@@ -75,7 +76,8 @@ class uniap_record(C.Structure):
                 ("L", C.c_int32), ("status", C.c_int32), ("n_cfg_local", C.c_int32),
                 ("stage_of", C.c_int32 * MAX_L), ("strategy_of", C.c_int32 * MAX_L),
                 ("stage_cost", C.c_int64 * MAX_L), ("cut_cost", C.c_int64 * MAX_L),
-                ("stage_mem", C.c_int32 * MAX_L), ("dp_cells", C.c_uint64), ("dp_relax", C.c_uint64)]
+                ("stage_mem", C.c_int32 * MAX_L), ("dp_cells", C.c_uint64), ("dp_relax", C.c_uint64),
+                ("dp_cells_canonical", C.c_uint64)]
 
 
 RECORD_BYTES = C.sizeof(uniap_record)
@@ -192,6 +194,7 @@ def _result_dict(r, n_cfg, cfg_obj):
     L = r.L
     out = {"objective": r.objective, "cfg_index": r.cfg_index, "deg": deg, "c": r.c,
            "quantum_ns": r.quantum_ns, "dp_cells": r.dp_cells, "dp_relax": r.dp_relax,
+           "dp_cells_canonical": r.dp_cells_canonical,
            "ms_gpu_dp": r.ms_gpu_dp, "ms_gpu_total": r.ms_gpu_total, "h2d_bytes": r.h2d_bytes,
            "d2h_bytes": r.d2h_bytes, "n_launches": r.n_launches, "n_k2_launches": r.n_k2_launches}
     if cfg_obj is not None:

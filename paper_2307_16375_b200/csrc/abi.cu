@@ -41,6 +41,11 @@ struct DevBuf {
 
 int round4(int x) { return (x + 3) & ~3; }
 
+bool env_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && *v != '0';
+}
+
 }  // namespace
 
 // one K2 launch: instances of one kernel class
@@ -85,7 +90,7 @@ struct uniap_handle {
   DevBuf<uniap_record> rec;
   // last run
   uniap_record rec_host{};
-  uint64_t cells = 0, relax = 0;
+  uint64_t cells = 0, relax = 0, cells_canon = 0;
   float ms_dp = 0.f, ms_total = 0.f;
   int64_t quantum = 0;
   cudaEvent_t ev[4] = {};
@@ -523,6 +528,9 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
 // be a stage of a deg-stage ordered placement (a >= stages before it, enough
 // layers after it); with the skip source inside the sweep, one copy per
 // strategy ks of the skip source (Eq. 3 couples it with later layers).
+// Canonical plan (the survey's work definition; also the all-intervals mode
+// of uniap_interval_table): one forward sweep per start layer a, over every
+// interval [a, b] a deg-stage ordered placement can use.
 static void plan_instances(int L, int i, int deg, int S, int skip, bool all_intervals, std::vector<Inst>& out) {
   if (!all_intervals && deg > L) return;
   for (int a = 0; a < L; ++a) {
@@ -533,16 +541,51 @@ static void plan_instances(int L, int i, int deg, int S, int skip, bool all_inte
     if (bmax < a) continue;
     const int n = bmax - a + 1;
     if (skip >= 0 && a <= skip && bmax >= skip + 2) {
-      for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0});
+      for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0, a, bmax});
     } else {
-      out.push_back(Inst{i, a, n, -1, +1, 1, 0});
+      out.push_back(Inst{i, a, n, -1, +1, 1, 0, a, bmax});
     }
+  }
+}
+
+// The plan the solver runs.  Stage 1 of a placement is a prefix [0, b]
+// (b <= L - deg), the last stage a suffix [a, L-1] (a >= deg - 1), the
+// middle stages (deg >= 3) intervals [a, b] with 1 <= a, b <= L - 2.  Every
+// prefix comes from the forward sweep started at 0 and every suffix from ONE
+// backward sweep started at L-1 (the backward DP's min over strategies at
+// layer a is the optimum of [a, L-1]), so only the middle stages need a sweep
+// per start layer: deg = 2 costs 2 sweeps instead of L.  With the skip
+// source s inside a sweep, one copy per strategy ks of s (Eq. 3 couples it
+// with later layers); a suffix sweep emits the conditioned copies for a <= s
+// and an unconditioned sweep for a > s.
+static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>& out) {
+  if (deg > L) return;
+  auto fwd = [&](int a, int bmax) {
+    if (bmax < a) return;
+    const int n = bmax - a + 1;
+    if (skip >= 0 && a <= skip && bmax >= skip + 2) {
+      for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0, a, bmax});
+    } else {
+      out.push_back(Inst{i, a, n, -1, +1, 1, 0, a, bmax});
+    }
+  };
+  if (deg == 1) { fwd(0, L - 1); return; }
+  fwd(0, L - deg);                                               // stage 1: prefixes
+  for (int a = 1; a <= L - 2 && deg >= 3; ++a)                   // middle stages
+    fwd(a, L - 1 - deg + std::min(a + 1, deg - 1));
+  const int amin = deg - 1, b = L - 1;                           // last stage: suffixes
+  if (skip >= 0 && amin <= skip && b >= skip + 2) {
+    for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, b, b - amin + 1, ks, -1, 2, 0, amin, skip});
+    if (skip + 1 <= b) out.push_back(Inst{i, b, b - skip, -1, -1, 1, 0, skip + 1, b});
+  } else {
+    out.push_back(Inst{i, b, b - amin + 1, -1, -1, 1, 0, amin, b});
   }
 }
 
 static void forward_instances(const uniap_handle* h, int i, bool all_intervals, std::vector<Inst>& out) {
   const CfgDev& d = h->cfg[i];
-  plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, out);
+  if (all_intervals || env_flag("UNIAP_CANONICAL_PLAN")) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, out);
+  else plan_fast(h->L, i, d.deg, d.S, d.skip, out);
 }
 
 // LPT over configs by chain-DP work (sum over instances of n |S|^2 Q); ties
@@ -712,6 +755,12 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     h->cells += (uint64_t)x.n * S * h->Q;
     h->relax += (uint64_t)(x.n - 1) * S * S * h->Q;
   }
+  h->cells_canon = 0;
+  for (int i : R.local) {
+    std::vector<Inst> cv;
+    plan_instances(h->L, i, h->cfg[i].deg, h->cfg[i].S, h->cfg[i].skip, false, cv);
+    for (auto& x : cv) h->cells_canon += (uint64_t)x.n * h->cfg[i].S * h->Q;
+  }
   group_instances(h, fw, R.fgrp);
   // backward: one device-sized launch per kernel class of the local configs
   std::vector<int32_t> cls_of_cfg(h->ncfg, 0);
@@ -784,7 +833,7 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   CK(h, launch_k3(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->st));
   CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
                   h->cfgopt.p, h->st));
-  RecordArgs ra{rec, h->cells, h->relax, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
+  RecordArgs ra{rec, h->cells, h->relax, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
                 h->binst.p, h->bwp.p};
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
                    h->cfgopt.p, h->scratch.p, h->win.p, ra, h->st));
@@ -799,10 +848,6 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   return UNIAP_OK;
 }
 
-static bool env_flag(const char* name) {
-  const char* v = getenv(name);
-  return v && *v && *v != '0';
-}
 
 extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev) {
   if (!h) return UNIAP_ERR_ARG;
@@ -896,6 +941,7 @@ extern "C" uniap_status uniap_fetch(uniap_handle* h, uniap_result* out) {
   out->quantum_ns = h->quantum;
   out->dp_cells = R.dp_cells;
   out->dp_relax = R.dp_relax;
+  out->dp_cells_canonical = R.dp_cells_canonical;
   out->ms_gpu_dp = h->ms_dp;
   out->ms_gpu_total = h->ms_total;
   out->h2d_bytes = h->h2d;
@@ -987,12 +1033,13 @@ extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m
 extern "C" uniap_status uniap_pick(const uniap_record* recs, int32_t world, uniap_result* out) {
   if (!recs || world < 1 || !out) return UNIAP_ERR_ARG;
   int best = -1;
-  uint64_t cells = 0, relax = 0;
+  uint64_t cells = 0, relax = 0, canon = 0;
   for (int r = 0; r < world; ++r) {
     const uniap_record& x = recs[r];
     if (x.status != 0) return (uniap_status)x.status;
     cells += x.dp_cells;
     relax += x.dp_relax;
+    canon += x.dp_cells_canonical;
     if (x.objective == INT64_MAX) continue;
     if (best < 0) { best = r; continue; }
     const uniap_record& b = recs[best];
@@ -1004,6 +1051,7 @@ extern "C" uniap_status uniap_pick(const uniap_record* recs, int32_t world, unia
   out->cfg_objective = keep;
   out->dp_cells = cells;
   out->dp_relax = relax;
+  out->dp_cells_canonical = canon;
   out->objective = INT64_MAX;
   out->cfg_index = -1;
   if (best < 0) return UNIAP_ERR_INFEASIBLE;

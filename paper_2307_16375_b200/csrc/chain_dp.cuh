@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
 
   int32_t d[NS][V];
   auto emit = [&](int u) {
-    if (in.dir > 0) {
+    if (in.emit != 0) {
       const int rc = cap / B;
       if (rank == rc) {
         const int lc = cap - rc * B, jc = lc / T, tc = lc - jc * T;
@@ -306,12 +306,12 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     emit(u);
   }
   // the forward sweep's stage optima P[a][a..a+n-1], from its owner thread
-  if (in.dir > 0 && rank == cap / B && t == (cap - (cap / B) * B) % T) {
-    int32_t* dst = args.P + cf.offP + (int64_t)in.a * L;
-    for (int i = 0; i < in.n; ++i) {
-      const int uu = in.a + i;
-      if (in.emit == 2) atomicMin(dst + uu, sProw[uu]);
-      else dst[uu] = sProw[uu];
+  if (in.emit != 0 && rank == cap / B && t == (cap - (cap / B) * B) % T) {
+    int32_t* Pc = args.P + cf.offP;
+    for (int uu = in.elo; uu <= in.ehi; ++uu) {
+      int32_t* dst = in.dir > 0 ? Pc + (int64_t)in.a * L + uu : Pc + (int64_t)uu * L + in.a;
+      if (in.emit == 2) atomicMin(dst, sProw[uu]);
+      else *dst = sProw[uu];
     }
   }
   if constexpr (CL) cl_sync();  // keep this CTA's E alive for remote readers

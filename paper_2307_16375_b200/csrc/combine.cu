@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     r->n_cfg_local = ra.n_local;
     r->dp_cells = ra.cells;
     r->dp_relax = ra.relax;
+    r->dp_cells_canonical = ra.cells_canon;
   }
   if (wl < 0) {
     if (t == 0) { win->objective = INT64_MAX; win->cfg = -1; win->status = 0; }
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
       const bool cond = cf.skip >= 0 && a <= cf.skip && cf.skip + 2 <= b;
       for (int ks = cond ? 0 : -1; ks < (cond ? cf.S : 0); ++ks) {
         ra.bw->gofs[i * 33 + ks + 1] = goff;
-        ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff};
+        ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1};
         goff += (int64_t)len * cf.NSP * (ra.cap + 1);
       }
       a = b + 1;

@@ -40,8 +40,12 @@ struct Inst {
   int32_t n;     // number of layers swept (>= 1)
   int32_t ks;    // skip-source conditioning (-1 = none)
   int32_t dir;   // +1 forward (emit P[a][u]), -1 backward (store G[u])
-  int32_t emit;  // forward: 1 plain store, 2 atomicMin (several copies); backward: 0
-  int64_t gofs;  // backward: word offset of this sweep's G block (layers a-n+1..a)
+  int32_t emit;  // 1: P plain store, 2: P atomicMin (several copies), 0: store G (traceback)
+  int64_t gofs;  // emit 0: word offset of this sweep's G block (layers a-n+1..a)
+  // emit 1/2: P entries of the layers u in [elo, ehi] only -- P[a][u] for a
+  // forward sweep (intervals starting at a), P[u][a] for a backward sweep
+  // (intervals ending at a: the suffix sweep of the last stage)
+  int32_t elo, ehi;
 };
 
 struct K2Args {
@@ -86,7 +90,7 @@ struct BwPlan {
 };
 struct RecordArgs {          // what K5a writes into the record besides the winner
   uniap_record* rec;
-  uint64_t cells, relax;
+  uint64_t cells, relax, cells_canon;
   int32_t n_local, L, cap;
   const int64_t* qglob;      // builder flags (level 2) or nullptr
   const int32_t* cls_of_cfg; // kernel class id per config

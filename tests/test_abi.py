@@ -48,7 +48,7 @@ def test_k2_uses_dpx_viaddmnmx():
 
 
 def test_record_layout():
-    assert pkg.RECORD_BYTES == C.sizeof(binding.uniap_record) == 8 + 6 * 4 + 2 * 64 * 4 + 2 * 64 * 8 + 64 * 4 + 16
+    assert pkg.RECORD_BYTES == C.sizeof(binding.uniap_record) == 8 + 6 * 4 + 2 * 64 * 4 + 2 * 64 * 8 + 64 * 4 + 24
 
 
 def test_candidates_and_catalogue_match_the_oracle(orc):
@@ -66,7 +66,7 @@ def _rec(obj, deg, c, cfg, L=4):
     for u in range(L):
         r.stage_of[u] = u * deg // L
         r.strategy_of[u] = cfg
-    r.dp_cells, r.dp_relax = 10, 20
+    r.dp_cells, r.dp_relax, r.dp_cells_canonical = 10, 20, 30
     return bytes(r)
 
 
@@ -74,7 +74,7 @@ def test_pick_orders_by_objective_then_deg_then_c():
     recs = _rec(7, 2, 4, 5) + _rec(7, 2, 2, 4) + _rec(9, 1, 1, 0) + _rec(pkg.INT64_MAX, 0, 0, -1)
     st, r = pkg.pick(recs, 4)
     assert st == 0 and (r["objective"], r["deg"], r["c"], r["cfg_index"]) == (7, 2, 2, 4)
-    assert r["dp_cells"] == 40 and r["dp_relax"] == 80
+    assert r["dp_cells"] == 40 and r["dp_relax"] == 80 and r["dp_cells_canonical"] == 120
     st, r = pkg.pick(_rec(pkg.INT64_MAX, 0, 0, -1) * 2, 2)
     assert st == binding.UNIAP_ERR_INFEASIBLE and r["objective"] == pkg.INT64_MAX
 

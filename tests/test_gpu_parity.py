@@ -173,5 +173,5 @@ def test_world_size_invariance(h):
             recs += buf.cpu().numpy().tobytes()
         st, r = pkg.pick(recs, world)
         for k in ("objective", "deg", "c", "cfg_index", "stage_of", "strategy_of", "stage_cost", "cut_cost",
-                  "stage_mem", "dp_cells", "dp_relax"):
+                  "stage_mem", "dp_cells", "dp_relax", "dp_cells_canonical"):
             assert r[k] == ref[k], (world, k)
