@@ -157,7 +157,7 @@ def main():
         if torch.cuda.is_available():
             import paper_2307_16375_b200 as pkg
             h = pkg.Handle(0)
-            cells = h.plan(profile)["dp_cells"]
+            cells = h.plan(profile)["dp_cells_canonical"]
             h.close()
         else:
             cells = _cells_host(profile)

@@ -41,6 +41,11 @@ struct DevBuf {
 
 int round4(int x) { return (x + 3) & ~3; }
 
+int k2_flags() {
+  static const int f = getenv("UNIAP_K2_FLAGS") ? atoi(getenv("UNIAP_K2_FLAGS")) : 0;
+  return f;
+}
+
 bool env_flag(const char* name) {
   const char* v = getenv(name);
   return v && *v && *v != '0';
@@ -711,7 +716,7 @@ static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp,
     const int n = dcount_per_class ? grp[g].max_inst : (int)(grp[g].e - grp[g].s);
     K2Args args{dcount_per_class ? dinst : dinst + grp[g].s,
                 dcount_per_class ? dcount_per_class + g : nullptr,
-                h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip};
+                h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip, k2_flags()};
     CK(h, k2_launch(grp[g].cls, args, n, st));
     h->launches++;
     h->k2_launches++;

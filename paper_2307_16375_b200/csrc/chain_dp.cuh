@@ -263,7 +263,10 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     // table fetch (after the release, so its fence does not wait for it),
     // sync the CTA, shift from the local E while the other CTAs catch up,
     // then wait (acquire) before the few reads from a lower CTA's range.
-    if constexpr (CL) cl_arrive();
+    if constexpr (CL) {
+      if (args.flags & 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+      else cl_arrive();
+    }
     if (step + 2 < in.n) fetch_stage(step + 2, u + 2 * in.dir);
     __syncthreads();
     // ---- shift by the layer's memory, add A' ----
