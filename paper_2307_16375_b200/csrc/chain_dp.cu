@@ -56,7 +56,8 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   if (NS <= 6 && 4096 <= cap_b && smem_words(NS, 4096) * 4 <= lim) Bmax = 4096;
   int B = std::min(Bmax, std::max(32, pow2ceil(Q)));
   int C = pow2ceil((Q + B - 1) / B);
-  if (single) {
+  static const int single_ok = env_int("UNIAP_K2_SINGLE", 1);  // tuning knob (experiments)
+  if (single && single_ok) {
     const int cmax = 8;
     while (C < cmax && B > 128) {
       B /= 2;

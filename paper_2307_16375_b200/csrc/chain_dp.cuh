@@ -290,18 +290,22 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       // local read above returned the guard (INF); fetch the value over DSMEM
       cl_wait();
       const int wbase = t & ~31;
-      if (rank > 0 && wbase < mmax) {  // warp-uniform: rare
+      if (rank > 0 && wbase < mmax) {  // warp-uniform: only the low warps of a CTA
+        // unconditional (predicated) loads so that all of them are in flight
+        // together: a cell that needs no fix-up reads its own E word instead
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
-          const int2 am = *reinterpret_cast<const int2*>(Tb + NS * NSP + 2 * k);
+          const int mk = Tb[NS * NSP + 2 * k + 1];
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            if (j * T + wbase < am.y) {  // warp-uniform: some lane reads a lower CTA
-              const int lx = j * T + t - am.y;
-              const int x = lx + rank * B;
-              if (lx < 0 && x >= 0)
-                d[k][j] = *map_rank(Eb + k * ROW + (x & (B - 1)), (uint32_t)(x / B));
-            }
+            const int lx = j * T + t - mk;
+            const int x = lx + rank * B;
+            const bool need = lx < 0 && x >= 0;
+            const int xc = max(x, 0);  // keep the (unused) mapa operands valid
+            const int32_t* src = need ? map_rank(Eb + k * ROW + (xc & (B - 1)), (uint32_t)(xc / B))
+                                      : Eb + k * ROW + j * T + t;
+            const int32_t v = *src;
+            d[k][j] = need ? v : d[k][j];
           }
         }
       }
