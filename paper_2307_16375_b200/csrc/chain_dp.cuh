@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int2 am = *reinterpret_cast<const int2*>(Tb + NS * NSP + 2 * k);
-      if constexpr (CL) mmax = max(mmax, am.y);
+      if constexpr (CL) mmax = max(mmax, am.y <= cap ? am.y : 0);  // forbidden rows are all INF
       const int32_t bk = (k * ROW + t - am.y) * 4;  // byte offset of bucket t - M in row k
       const int32_t gk = k * ROW * 4 - 4;          // the row's guard word
 #pragma unroll
