@@ -53,6 +53,24 @@ __device__ __forceinline__ void cl_arrive() {
 __device__ __forceinline__ void cl_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Cluster wait that also yields a token (0) for the loads that must follow it.
+__device__ __forceinline__ uint32_t cl_wait_tok() {
+  uint32_t tok;
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n\tmov.u32 %0, 0;" : "=r"(tok)::"memory");
+  return tok;
+}
+// 32-bit shared::cluster addressing; the load is not volatile (loads can be
+// batched) and is ordered after the barrier through its address operand.
+__device__ __forceinline__ uint32_t mapa32(uint32_t la, uint32_t rank) {
+  uint32_t r;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(la), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ int32_t ld_cluster(uint32_t addr) {
+  int32_t v;
+  asm("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 // Generic address of the same shared-memory word in CTA `rank` of the
 // cluster (pure: the load itself is an ordinary C++ load, so the compiler
 // keeps it after the barrier and may batch several of them).
@@ -288,11 +306,12 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     if constexpr (CL) {
       // buckets whose shifted source q - M lies in a lower CTA's range: the
       // local read above returned the guard (INF); fetch the value over DSMEM
-      cl_wait();
+      const uint32_t tok = cl_wait_tok();
       const int wbase = t & ~31;
       if (rank > 0 && wbase < mmax) {  // warp-uniform: only the low warps of a CTA
-        // unconditional (predicated) loads so that all of them are in flight
-        // together: a cell that needs no fix-up reads its own E word instead
+        // predicated loads, all in flight together: a cell that needs no
+        // fix-up reads its own E word (shared::cluster window, own rank)
+        const uint32_t ebase = (uint32_t)__cvta_generic_to_shared(Eb) + tok;
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
           const int mk = Tb[NS * NSP + 2 * k + 1];
@@ -301,10 +320,9 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
             const int lx = j * T + t - mk;
             const int x = lx + rank * B;
             const bool need = lx < 0 && x >= 0;
-            const int xc = max(x, 0);  // keep the (unused) mapa operands valid
-            const int32_t* src = need ? map_rank(Eb + k * ROW + (xc & (B - 1)), (uint32_t)(xc / B))
-                                      : Eb + k * ROW + j * T + t;
-            const int32_t v = *src;
+            const int xc = need ? x : rank * B + j * T + t;  // own word when no fix-up
+            const uint32_t la = ebase + (uint32_t)((k * ROW + (xc & (B - 1))) * 4);
+            const int32_t v = ld_cluster(mapa32(la, (uint32_t)(xc / B)));
             d[k][j] = need ? v : d[k][j];
           }
         }
