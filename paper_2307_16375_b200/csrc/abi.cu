@@ -123,7 +123,7 @@ static void update_signature(uniap_handle* h) {
     const CfgDev& d = h->cfg[i];
     const K2Class& k = h->cls[i];
     for (int64_t x : {(int64_t)d.deg, (int64_t)d.c, (int64_t)d.S, (int64_t)d.NSP, (int64_t)d.skip, d.offA, d.offP,
-                      (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C})
+                      (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C, (int64_t)k.DB})
       sg.push_back(x);
   }
   if (h->level2) {
@@ -657,7 +657,7 @@ extern "C" uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32
 // per-layer synchronisation) -- so it starts on free SMs.
 // ---------------------------------------------------------------------------
 
-static int class_key(const K2Class& k) { return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C; }
+static int class_key(const K2Class& k) { return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C + (k.DB ? 0 : 50000); }
 
 static void group_instances(const uniap_handle* h, std::vector<Inst>& all, std::vector<K2Group>& grp) {
   std::vector<int> key(all.size());

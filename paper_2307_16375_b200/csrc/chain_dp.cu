@@ -7,7 +7,7 @@
 namespace uniap {
 
 #define UNIAP_NS_LIST(X) X(1) X(2) X(3) X(4) X(6) X(8) X(10) X(12) X(15) X(16) X(21) X(24) X(32)
-#define UNIAP_EXTERN(N) extern template k2_fn k2_get<N>(int, int, bool);
+#define UNIAP_EXTERN(N) extern template k2_fn k2_get<N>(int, int, bool, bool);
 UNIAP_NS_LIST(UNIAP_EXTERN)
 #undef UNIAP_EXTERN
 
@@ -19,12 +19,12 @@ int k2_ns_round(int S) {
   return -1;
 }
 
-static size_t smem_words(int NS, int B) {
+static size_t smem_words(int NS, int B, int ne = 2) {
   const int NSP = (NS + 3) & ~3;
-  return (size_t)2 * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP) + MAXL;
+  return (size_t)ne * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP) + MAXL;
 }
 
-size_t k2_smem_bytes(const K2Class& c) { return smem_words(c.NS, c.T * c.V) * sizeof(int32_t); }
+size_t k2_smem_bytes(const K2Class& c) { return smem_words(c.NS, c.T * c.V, c.DB ? 2 : 1) * sizeof(int32_t); }
 
 static int pow2ceil(int x) {
   int p = 1;
@@ -83,7 +83,7 @@ static k2_fn k2_lookup(const K2Class& c) {
   const bool CL = c.C > 1;
   switch (c.NS) {
 #define UNIAP_CASE(N) \
-  case N: return k2_get<N>(c.V, c.T, CL);
+  case N: return k2_get<N>(c.V, c.T, CL, c.DB);
     UNIAP_NS_LIST(UNIAP_CASE)
 #undef UNIAP_CASE
     default: return nullptr;

@@ -105,17 +105,19 @@ struct Stage {
   static constexpr int WORDS = NS * NSP + 2 * NSP;
 };
 
-template <int NS, int V, int T, bool CL>
+template <int NS, int V, int T, bool CL, bool DB = true>
 __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
+  static_assert(DB || !CL, "single-buffered E only without clusters");
   constexpr int B = T * V;          // buckets per CTA
   constexpr int ROW = B + 4;        // 4 guard words + B buckets
+  constexpr int NE = DB ? 2 : 1;    // E buffers (single: a second barrier per layer)
   constexpr int NSP = Stage<NS>::NSP;
   constexpr int SW = Stage<NS>::WORDS;
   constexpr int KUNROLL = 8;
   constexpr int MBIG = UNIAP_MAX_Q * 2 + 1;  // > every bucket index: "never fits"
   extern __shared__ int4 smem4[];
   int32_t* sE = reinterpret_cast<int32_t*>(smem4);  // [2][NS][ROW]
-  int32_t* sT = sE + 2 * NS * ROW;                  // [3][SW] staged tables
+  int32_t* sT = sE + NE * NS * ROW;                 // [3][SW] staged tables
   int32_t* sProw = sT + 3 * SW;                     // [MAXL] this instance's P[a][.]
   const int t = threadIdx.x;
   int rank = 0, ii = blockIdx.x;
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   const int Q = cap + 1;
   const int L = args.L;
 
-  for (int r = t; r < 2 * NS; r += T) *reinterpret_cast<int4*>(sE + r * ROW) = make_int4(INF, INF, INF, INF);
+  for (int r = t; r < NE * NS; r += T) *reinterpret_cast<int4*>(sE + r * ROW) = make_int4(INF, INF, INF, INF);
 
   // ---- tables of one layer step, staged by the whole CTA ----------------
   // word w of a stage: R rows (w < NS*NSP), then (A', M) pairs.  A' adds the
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
 
   for (int step = 1; step < in.n; ++step) {
     u += in.dir;
-    int32_t* Eb = sE + (step & 1) * NS * ROW + 4;          // row 0, bucket 0
+    int32_t* Eb = sE + (DB ? (step & 1) * NS * ROW : 0) + 4;  // row 0, bucket 0
     const int32_t* Tb = sT + (step % 3) * SW;
     // ---- E-step: registers only; R broadcast from shared memory ----
     // RR destination rows per pass: RR*V independent VIADDMNMX chains.
@@ -328,6 +330,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
         }
       }
     }
+    if constexpr (!DB) __syncthreads();  // E is rewritten by the next layer
     emit(u);
   }
   // the forward sweep's stage optima P[a][a..a+n-1], from its owner thread
@@ -343,8 +346,8 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
 }
 
 template <int NS>
-constexpr size_t k2_smem(int B) {
-  return (size_t)(2 * NS * (B + 4) + 3 * Stage<NS>::WORDS + MAXL) * sizeof(int32_t);
+constexpr size_t k2_smem(int B, int ne = 2) {
+  return (size_t)(ne * NS * (B + 4) + 3 * Stage<NS>::WORDS + MAXL) * sizeof(int32_t);
 }
 
 // Instantiation helper used by the per-NS translation units: only the shapes
@@ -352,7 +355,14 @@ constexpr size_t k2_smem(int B) {
 typedef void (*k2_fn)(const K2Args);
 
 template <int NS>
-k2_fn k2_get(int V, int T, bool CL) {
+k2_fn k2_get(int V, int T, bool CL, bool DB) {
+  if (!DB) {  // single-buffered E, one CTA per instance (large B without a cluster)
+    if (CL) return nullptr;
+    if constexpr (NS > 24 && k2_smem<NS>(1024, 1) <= 200 * 1024) if (V == 2 && T == 512) return k2_chain<NS, 2, 512, false, false>;
+    if constexpr (NS > 12 && NS <= 24 && k2_smem<NS>(2048, 1) <= 200 * 1024) if (V == 4 && T == 512) return k2_chain<NS, 4, 512, false, false>;
+    if constexpr (NS > 6 && NS <= 10) if (V == 8 && T == 512) return k2_chain<NS, 8, 512, false, false>;
+    return nullptr;
+  }
 #define UNIAP_SHAPE(VV, TT)                                                 \
   if (V == VV && T == TT) {                                                 \
     if constexpr (k2_smem<NS>(VV * TT) <= 200 * 1024)                       \

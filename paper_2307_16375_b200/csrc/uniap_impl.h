@@ -65,6 +65,7 @@ struct K2Class {
   int V;       // buckets per thread
   int T;       // threads per CTA
   int C;       // CTAs per cluster
+  bool DB;     // double-buffered E (one barrier per layer); single: two
 };
 
 // chain_dp.cu
