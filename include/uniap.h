@@ -210,6 +210,11 @@ uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world, int32_t* o
  * *out (cfg_objective untouched).  Host only (no device needed). */
 uniap_status uniap_pick(const uniap_record* recs, int32_t world, uniap_result* out);
 
+/* Host-only self check: every chain-DP kernel shape the planner can choose
+ * for 1 <= |S| <= 32 and 1 <= Q <= 8192 is compiled into the library.
+ * Returns 0, or 1 with the first failing (S, Q, single-chain flag). */
+int32_t uniap_selftest(int32_t* S, int32_t* Q, int32_t* single);
+
 /* Candidate list of Algorithm 1 and the strategy catalogue (host only). */
 int32_t uniap_candidates(int32_t n, int32_t B, int32_t* pairs_out, int32_t cap);
 int32_t uniap_catalogue(int32_t g, int32_t* tfd_out, int32_t cap);

@@ -85,7 +85,7 @@ RECORD_BYTES = C.sizeof(uniap_record)
 EXPORTS = ("uniap_create", "uniap_destroy", "uniap_last_error", "uniap_status_string", "uniap_version",
            "uniap_solve_tables", "uniap_interval_table", "uniap_plan", "uniap_build_tables", "uniap_prepare",
            "uniap_prepare_tables", "uniap_run", "uniap_fetch", "uniap_shard_assign", "uniap_shard_tables",
-           "uniap_pick",
+           "uniap_pick", "uniap_selftest",
            "uniap_candidates", "uniap_catalogue")
 
 _lib = None
@@ -122,6 +122,7 @@ def lib():
         L.uniap_pick.argtypes = [C.POINTER(uniap_record), C.c_int32, C.POINTER(uniap_result)]
         L.uniap_candidates.argtypes = [C.c_int32, C.c_int32, _P32, C.c_int32]
         L.uniap_catalogue.argtypes = [C.c_int32, _P32, C.c_int32]
+        L.uniap_selftest.argtypes = [_P32, _P32, _P32]
         for f in EXPORTS:
             if f not in ("uniap_destroy", "uniap_last_error", "uniap_status_string", "uniap_version"):
                 getattr(L, f).restype = C.c_int
@@ -211,6 +212,13 @@ def candidates(n, B):
     buf = (C.c_int32 * (2 * k))()
     lib().uniap_candidates(n, B, buf, k)
     return [(buf[2 * i], buf[2 * i + 1]) for i in range(k)]
+
+
+def selftest():
+    """Host-only: every K2 kernel shape the planner can choose is compiled in."""
+    a, b, c = C.c_int32(), C.c_int32(), C.c_int32()
+    rc = lib().uniap_selftest(C.byref(a), C.byref(b), C.byref(c))
+    return rc, (a.value, b.value, c.value)
 
 
 def catalogue(g):

@@ -208,6 +208,8 @@ extern "C" int32_t uniap_catalogue(int32_t g, int32_t* tfd, int32_t cap) {
   return k;
 }
 
+extern "C" int32_t uniap_selftest(int32_t* S, int32_t* Q, int32_t* single) { return k2_selftest(S, Q, single); }
+
 extern "C" const char* uniap_version(void) { return "uniap-b200 0.1 (sm_100a)"; }
 
 extern "C" const char* uniap_status_string(uniap_status s) {

@@ -69,8 +69,21 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   // (two independent instances) share an SM and overlap each other's
   // barrier / shift phases; clusters keep 2 x 512 (one CTA per SM by shared
   // memory, so more threads per CTA).  UNIAP_K2_V overrides (experiments).
+  // A cluster is avoidable with a single-buffered E (two CTA barriers per
+  // layer instead of DSMEM and cluster barriers) when the whole bucket range
+  // fits one CTA: |S| <= 10 up to 4096 buckets, <= 24 up to 2048, 32 up to 1024.
+  static const int sb_ok = env_int("UNIAP_K2_SB", 1);
+  if (C > 1 && !single && sb_ok) {
+    const int Bs = std::max(32, pow2ceil(Q));
+    const bool shape = (Bs == 4096 && NS > 6 && NS <= 10) || (Bs == 2048 && NS > 12 && NS <= 24) ||
+                       (Bs == 1024 && NS > 24);
+    if (shape && smem_words(NS, Bs, 1) * 4 <= lim) {
+      *out = K2Class{NS, Bs / 512, 512, 1, false};
+      return true;
+    }
+  }
   static const int pref_v = env_int("UNIAP_K2_V", 0);
-  K2Class c{NS, 2, B / 2, C};
+  K2Class c{NS, 2, B / 2, C, true};
   if (B == 1024 && NS <= 16 && (pref_v == 4 || (pref_v == 0 && C == 1))) { c.V = 4; c.T = 256; }
   if (B == 32) { c.V = 1; c.T = 32; }
   if (B == 2048) { c.V = 4; c.T = 512; }
@@ -88,6 +101,34 @@ static k2_fn k2_lookup(const K2Class& c) {
 #undef UNIAP_CASE
     default: return nullptr;
   }
+}
+
+// Every kernel class the chooser can return has an instantiated kernel
+// (host-only self check; returns the first failing (S, Q, single) or 0).
+int k2_selftest(int* S_out, int* Q_out, int* single_out) {
+  for (int S = 1; S <= UNIAP_MAX_STRAT; ++S)
+    for (int Q = 1; Q <= UNIAP_MAX_Q; Q += (Q < 64 ? 1 : Q < 1100 ? 7 : 61))
+      for (int single = 0; single < 2; ++single) {
+        K2Class c;
+        if (!k2_pick_class(S, Q, single, &c) || !k2_lookup(c)) {
+          *S_out = S;
+          *Q_out = Q;
+          *single_out = single;
+          return 1;
+        }
+      }
+  for (int S = 1; S <= UNIAP_MAX_STRAT; ++S)
+    for (int Q : {2048, 4096, 8192})
+      for (int single = 0; single < 2; ++single) {
+        K2Class c;
+        if (!k2_pick_class(S, Q, single, &c) || !k2_lookup(c)) {
+          *S_out = S;
+          *Q_out = Q;
+          *single_out = single;
+          return 1;
+        }
+      }
+  return 0;
 }
 
 cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st) {

@@ -75,6 +75,7 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out);
 int k2_ns_round(int S);
 size_t k2_smem_bytes(const K2Class& c);
 cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st);
+int k2_selftest(int* S_out, int* Q_out, int* single_out);
 
 // Winner of the combine step (written by K5a, read by the host and K5c).
 struct Winner {
