@@ -502,7 +502,8 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   CK(h, h->dcat.ensure(h->ncfg));
   CK(h, h->qcfg.ensure(h->ncfg));
   CK(h, h->qmax.ensure((size_t)h->ncfg * MAXL * 4));
-  CK(h, h->qglob.ensure(2));
+  CK(h, h->qglob.ensure(3));
+  CK(h, cudaMemsetAsync(h->qglob.p, 0, 3 * sizeof(int64_t), h->st));
   CK(h, h->fwd.ensure(fwd.size()));
   CK(h, h->act.ensure(act.size()));
   CK(h, h->ps.ensure(L));
@@ -827,7 +828,7 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   const int L = h->L, nl = (int)R.local.size();
   if (h->level2) {
     CK(h, launch_k1(h->cl, build_bufs(h), h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
-    h->launches += 6;
+    h->launches += 3;
   }
   CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
   h->launches++;
@@ -837,14 +838,13 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     if (s != UNIAP_OK) return s;
   }
   CK(h, cudaEventRecordWithFlags(h->ev[2], h->st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
-  CK(h, launch_k3(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->st));
   CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
                   h->cfgopt.p, h->st));
   RecordArgs ra{rec, h->cells, h->relax, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
                 h->binst.p, h->bwp.p};
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
                    h->cfgopt.p, h->scratch.p, h->win.p, ra, h->st));
-  h->launches += nl > 0 ? 3 : 1;
+  h->launches += nl > 0 ? 2 : 1;
   // traceback: backward sweeps sized on the device, then the strategy walk
   {
     uniap_status s = enqueue_k2(h, R.bgrp, h->binst.p, h->bwp.p->count, h->P.p);

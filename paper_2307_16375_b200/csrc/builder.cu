@@ -19,7 +19,16 @@ namespace uniap {
 typedef unsigned __int128 u128;
 constexpr int64_t NS_LIM = (int64_t)1 << 62;
 
-__device__ __forceinline__ u128 cdiv128(u128 x, u128 y) { return (x + y - 1) / y; }
+// ceil(x / y), exact; the common case (both below 2^64) takes the much
+// cheaper 64-bit division
+__device__ __forceinline__ u128 cdiv128(u128 x, u128 y) {
+  if (((x | y) >> 64) == 0) {
+    const uint64_t a = (uint64_t)x, b = (uint64_t)y;
+    const uint64_t q = a / b;
+    return (u128)(q + (a - q * b != 0));
+  }
+  return (x + y - 1) / y;
+}
 
 struct Coll {
   const ClusterDev& c;
@@ -61,9 +70,9 @@ __device__ __forceinline__ int64_t checked(u128 v, int64_t* flags) {
 }
 
 // K1a: A (ns) and M (bytes, -1 = forbidden) for every (config, layer, strategy).
-__global__ void k1a_layers(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L) {
+__device__ void k1a_layers(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* __restrict__ cfgs, int L, int bx) {
   const CfgDev cf = cfgs[blockIdx.y];
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int idx = bx * blockDim.x + threadIdx.x;
   if (idx >= L * cf.NSP) return;
   const int u = idx / cf.NSP, k = idx - u * cf.NSP;
   int64_t* A = bb.ns + cf.offA;
@@ -94,10 +103,10 @@ __global__ void k1a_layers(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict
 }
 
 // K1b: R (edge e = u->u+1), Rskip (edge skip->v) in ns, original [k][l] layout.
-__global__ void k1b_reshard(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L) {
+__device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* __restrict__ cfgs, int L, int bx) {
   const CfgDev cf = cfgs[blockIdx.y];
   const int NSP = cf.NSP, n2 = NSP * NSP;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int idx = bx * blockDim.x + threadIdx.x;
   const int nR = (L - 1) * n2, nS = L * n2;
   if (idx >= nR + nS) return;
   const bool isR = idx < nR;
@@ -120,9 +129,9 @@ __global__ void k1b_reshard(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
 
 // K1c: cut costs: every edge crossing the cut after layer e, fwd + bwd P2P
 // (each edge's P2P time once per config, then one sum per cut).
-__global__ void k1c_cuts(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L) {
+__device__ void k1c_cuts(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* __restrict__ cfgs, int L) {
   __shared__ unsigned long long pv[512];
-  const CfgDev cf = cfgs[blockIdx.x];
+  const CfgDev cf = cfgs[blockIdx.y];
   const int64_t b = cl.B / cf.c;
   const Coll co{cl};
   for (int i = threadIdx.x; i < bb.n_edges && i < 512; i += blockDim.x)
@@ -136,8 +145,19 @@ __global__ void k1c_cuts(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__
     }
     const int64_t v = checked(s, bb.qglob + 1);
     (bb.ns + cf.offO)[e] = v;
-    bb.qmax[((int64_t)blockIdx.x * MAXL + e) * 4 + 3] = v;
+    bb.qmax[((int64_t)blockIdx.y * MAXL + e) * 4 + 3] = v;
   }
+}
+
+// K1a-c in one launch: blockIdx.x selects the role (layers | reshards | cuts),
+// blockIdx.y the config.
+constexpr int K1T = 256;
+__global__ void __launch_bounds__(K1T) k1_costs(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L,
+                                                int nbA, int nbR) {
+  const int bx = blockIdx.x;
+  if (bx < nbA) k1a_layers(cl, bb, cfgs, L, bx);
+  else if (bx < nbA + nbR) k1b_reshard(cl, bb, cfgs, L, bx - nbA);
+  else k1c_cuts(cl, bb, cfgs, L);
 }
 
 // K1d: the smallest passing power-of-two quantum of each config (reading A-9):
@@ -182,18 +202,22 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
       for (int p = 0; p <= 61; ++p)
         if (okp[p]) { q = (int64_t)1 << p; break; }
     bb.qcfg[blockIdx.x] = q;
+    // the last config block to finish sets the global quantum = max over the
+    // configs (every check is monotone in q), or flags "no quantum fits"
+    __threadfence();
+    unsigned int* done = reinterpret_cast<unsigned int*>(bb.qglob + 2);
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      int64_t g = 1;
+      for (int i = 0; i < (int)gridDim.x; ++i) {
+        const int64_t x = *reinterpret_cast<volatile int64_t*>(bb.qcfg + i);
+        if (x < 0) { atomicOr(reinterpret_cast<unsigned long long*>(bb.qglob + 1), 2ull); g = -1; break; }
+        g = max(g, x);
+      }
+      bb.qglob[0] = g;
+      *done = 0u;  // ready for the next run (graph replays)
+    }
   }
-}
-
-// K1e: global quantum = max over configs (monotone checks), error if any fails.
-__global__ void k1e_global(BuildBufs bb, int ncfg) {
-  int64_t q = 1;
-  for (int i = 0; i < ncfg; ++i) {
-    const int64_t x = bb.qcfg[i];
-    if (x < 0) { atomicOr(reinterpret_cast<unsigned long long*>(bb.qglob + 1), 2ull); q = -1; break; }
-    q = max(q, x);
-  }
-  bb.qglob[0] = q;
 }
 
 // K1f: quantise into the int32 device layout (A, M buckets, Rt, Rf, Rs, O).
@@ -204,7 +228,9 @@ __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restri
   const int cap = cl.Q - 1;
   const int64_t unit = (cl.mem_bytes - cl.mem_reserve) / cap;  // reading A-8
   const int nA = L * NSP, nR = (L - 1) * n2, nS = L * n2, nO = ((L - 1) + 3) & ~3;
-  auto qt = [&](int64_t x) { return (int32_t)((x + q - 1) / q); };
+  const bool pow2 = (q & (q - 1)) == 0;
+  const int sh = __ffsll(q) - 1;
+  auto qt = [&](int64_t x) { return (int32_t)(pow2 ? (x + q - 1) >> sh : (x + q - 1) / q); };
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nA + nR + nS + nO; idx += gridDim.x * blockDim.x) {
     int j = idx;
     if (j < nA) { arena[cf.offA + j] = qt(bb.ns[cf.offA + j]); continue; }
@@ -232,16 +258,14 @@ __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restri
 
 cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* cfg, int ncfg, int L, int skip,
                       int32_t* arena, cudaStream_t st) {
-  const int maxNSP = 32;
-  cudaError_t e = cudaMemsetAsync(bb.qglob, 0, 2 * sizeof(int64_t), st);
+  cudaError_t e = cudaMemsetAsync(bb.qglob, 0, 2 * sizeof(int64_t), st);  // [2] = done counter (reset by K1d)
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(bb.qmax, 0, (size_t)ncfg * MAXL * 4 * sizeof(int64_t), st);
   if (e != cudaSuccess) return e;
-  k1a_layers<<<dim3((L * maxNSP + 127) / 128, ncfg), 128, 0, st>>>(cl, bb, cfg, L);
-  k1b_reshard<<<dim3(((2 * L - 1) * maxNSP * maxNSP + 255) / 256, ncfg), 256, 0, st>>>(cl, bb, cfg, L);
-  k1c_cuts<<<ncfg, 128, 0, st>>>(cl, bb, cfg, L);
+  const int nbA = (L * 32 + K1T - 1) / K1T;
+  const int nbR = ((2 * L - 1) * 32 * 32 + K1T - 1) / K1T;
+  k1_costs<<<dim3(nbA + nbR + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR);
   k1d_quantum<<<ncfg, 64, 0, st>>>(cl, bb, cfg, L, skip);
-  k1e_global<<<1, 1, 0, st>>>(bb, ncfg);
   k1f_quantise<<<dim3(16, ncfg), 256, 0, st>>>(cl, bb, cfg, L, arena);
   return cudaGetLastError();
 }

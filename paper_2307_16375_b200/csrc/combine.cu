@@ -34,32 +34,27 @@ cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st) {
 // K3: sorted distinct theta candidates per config (one CTA per config).
 // ---------------------------------------------------------------------------
 constexpr int K3T = 1024;
-__global__ void __launch_bounds__(K3T) k3_thetas(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
-                                                 const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
-                                                 int L, int32_t* __restrict__ thetas, int32_t* __restrict__ ntheta) {
-  __shared__ int32_t v[SORTN];
-  __shared__ int32_t cnt;
-  typedef cub::BlockScan<int, K3T> Scan;
-  __shared__ typename Scan::TempStorage scan_tmp;
+typedef cub::BlockScan<int, K3T> K3Scan;
+// Sorted distinct theta candidates of config `cf` into v[0..n) (returns n):
+// valid P[a][b] < INF and every O[e]; bitonic sort + dedupe in shared memory.
+__device__ int sort_thetas(const CfgDev& cf, const int32_t* __restrict__ arena, const int32_t* __restrict__ P, int L,
+                           int32_t* v, int32_t* cnt, typename K3Scan::TempStorage& scan_tmp) {
   const int t = threadIdx.x;
-  const int ci = cfg_list[blockIdx.x];
-  const CfgDev cf = cfgs[ci];
-  if (t == 0) cnt = 0;
+  if (t == 0) *cnt = 0;
   for (int i = t; i < SORTN; i += K3T) v[i] = 0x7fffffff;
   __syncthreads();
   const int32_t* Pc = P + cf.offP;
   for (int idx = t; idx < L * L; idx += K3T) {
     const int a = idx / L, b = idx - a * L;
     const int32_t x = Pc[idx];
-    if (a <= b && x < INF) v[atomicAdd(&cnt, 1)] = x;
+    if (a <= b && x < INF) v[atomicAdd(cnt, 1)] = x;
   }
   const int32_t* O = arena + cf.offO;
-  for (int e = t; e < L - 1; e += K3T) v[atomicAdd(&cnt, 1)] = O[e];
+  for (int e = t; e < L - 1; e += K3T) v[atomicAdd(cnt, 1)] = O[e];
   __syncthreads();
-  const int n = cnt;
+  const int n = *cnt;
   int N = 2;
   while (N < n) N <<= 1;
-  // bitonic sort of v[0..N)
   for (int k = 2; k <= N; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = t; i < N; i += K3T) {
@@ -75,26 +70,21 @@ __global__ void __launch_bounds__(K3T) k3_thetas(const CfgDev* __restrict__ cfgs
       }
       __syncthreads();
     }
-  // dedupe: 4 consecutive elements per thread
   int flags[4], c = 0;
+  int32_t vals[4];
   for (int r = 0; r < 4; ++r) {
     const int i = 4 * t + r;
+    vals[r] = i < SORTN ? v[i] : 0;
     flags[r] = (i < n) && (i == 0 || v[i] != v[i - 1]);
     c += flags[r];
   }
   int pos, total;
-  Scan(scan_tmp).ExclusiveSum(c, pos, total);
-  int32_t* out = thetas + (int64_t)blockIdx.x * TMAX;
+  K3Scan(scan_tmp).ExclusiveSum(c, pos, total);
+  __syncthreads();  // every read of v above is done before the compaction writes
   for (int r = 0; r < 4; ++r)
-    if (flags[r]) out[pos++] = v[4 * t + r];
-  if (t == 0) ntheta[blockIdx.x] = total;
-}
-
-cudaError_t launch_k3(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
-                      int L, int32_t* thetas, int32_t* ntheta, cudaStream_t st) {
-  if (n_local <= 0) return cudaSuccess;
-  k3_thetas<<<n_local, K3T, 0, st>>>(cfg, arena, P, cfg_list, L, thetas, ntheta);
-  return cudaGetLastError();
+    if (flags[r]) v[pos++] = vals[r];
+  __syncthreads();
+  return total;
 }
 
 // ---------------------------------------------------------------------------
@@ -169,23 +159,39 @@ __device__ __forceinline__ int32_t warp_F(const int32_t* sP, const int32_t* sO, 
 // Unevaluated entries keep Val = INT64_MAX (> OPT, so never in Theta*).
 // ---------------------------------------------------------------------------
 constexpr int K4W = 32;
+struct K4Smem {
+  int32_t v[SORTN];  // sorted distinct thetas (K3)
+  int32_t sP[MAXL * MAXL];
+  int32_t sO[MAXL];
+  int32_t g[K4W][128];
+  int32_t probeF[K4W];
+  int32_t cnt, s_hi;
+  unsigned long long s_best;
+  typename K3Scan::TempStorage scan_tmp;
+};
+
 __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
                                                    const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
-                                                   int L, const int32_t* __restrict__ thetas,
-                                                   const int32_t* __restrict__ ntheta, int64_t* __restrict__ vals,
+                                                   int L, int32_t* __restrict__ thetas,
+                                                   int32_t* __restrict__ ntheta, int64_t* __restrict__ vals,
                                                    int64_t* __restrict__ cfg_opt) {
-  __shared__ int32_t sP[MAXL * MAXL];
-  __shared__ int32_t sO[MAXL];
-  __shared__ int32_t g[K4W][128];
-  __shared__ int32_t probeF[K4W];
-  __shared__ int s_hi;
-  __shared__ unsigned long long s_best;
+  extern __shared__ __align__(16) unsigned char k4raw[];
+  K4Smem& S = *reinterpret_cast<K4Smem*>(k4raw);
+  int32_t* sP = S.sP;
+  int32_t* sO = S.sO;
+  int32_t* probeF = S.probeF;
+  int& s_hi = S.s_hi;
+  unsigned long long& s_best = S.s_best;
+  auto g = S.g;
   const int li = blockIdx.x;
   const CfgDev cf = cfgs[cfg_list[li]];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nt = ntheta[li];
+  // K3 fused: the sorted distinct theta candidates (also kept for K5a)
+  const int nt = sort_thetas(cf, arena, P, L, S.v, &S.cnt, S.scan_tmp);
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) thetas[(int64_t)li * TMAX + i] = S.v[i];
+  if (threadIdx.x == 0) ntheta[li] = nt;
   int64_t* V = vals + (int64_t)li * (TMAX + 2);  // [0..nt) Val, [TMAX] F_inf, [TMAX+1] opt
-  const int32_t* th = thetas + (int64_t)li * TMAX;
+  const int32_t* th = S.v;
   for (int i = threadIdx.x; i < nt; i += blockDim.x) V[i] = INT64_MAX;
   if (cf.deg > L || nt == 0) {  // Eq. 7b cannot hold (reading A-22)
     if (threadIdx.x == 0) { V[TMAX] = INT64_MAX; cfg_opt[cfg_list[li]] = INT64_MAX; }
@@ -256,10 +262,15 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
 }
 
 cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
-                      int L, const int32_t* thetas, const int32_t* ntheta, int64_t* vals, int64_t* cfg_opt,
-                      cudaStream_t st) {
+                      int L, int32_t* thetas, int32_t* ntheta, int64_t* vals, int64_t* cfg_opt, cudaStream_t st) {
   if (n_local <= 0) return cudaSuccess;
-  k4_vals<<<n_local, K4W * 32, 0, st>>>(cfg, arena, P, cfg_list, L, thetas, ntheta, vals, cfg_opt);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k4_vals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4Smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k4_vals<<<n_local, K4W * 32, sizeof(K4Smem), st>>>(cfg, arena, P, cfg_list, L, thetas, ntheta, vals, cfg_opt);
   return cudaGetLastError();
 }
 

@@ -103,10 +103,9 @@ struct RecordArgs {          // what K5a writes into the record besides the winn
 
 // combine.cu
 cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st);
-cudaError_t launch_k3(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
-                      int n_local, int L, int32_t* thetas, int32_t* ntheta, cudaStream_t st);
+// K3 (theta candidates) is fused into K4.
 cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
-                      int n_local, int L, const int32_t* thetas, const int32_t* ntheta, int64_t* vals,
+                      int n_local, int L, int32_t* thetas, int32_t* ntheta, int64_t* vals,
                       int64_t* cfg_opt, cudaStream_t st);
 cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
                        int n_local, int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals,
@@ -138,7 +137,7 @@ struct BuildBufs {
   int64_t* ns;            // int64 scratch arena, same offsets as the int32 arena
   int64_t* qcfg;          // [ncfg] smallest passing quantum per config
   int64_t* qmax;          // [ncfg][MAXL][4] per layer: max A, max R into u, max Rskip into u, O[u]
-  int64_t* qglob;         // [2]: quantum, error flags
+  int64_t* qglob;         // [3]: quantum, error flags, completion counter of K1d
 };
 cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* cfg, int ncfg, int L, int skip,
                       int32_t* arena, cudaStream_t st);
