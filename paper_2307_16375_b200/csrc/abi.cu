@@ -80,6 +80,7 @@ struct uniap_handle {
   int L = 0, cap = 0, Q = 0, skip = -1, ncfg = 0;
   std::vector<CfgDev> cfg;
   std::vector<K2Class> cls;
+  std::vector<K2Class> bcls;  // class of the traceback sweeps: spread over a cluster (few instances)
   std::vector<CatDev> cat;
   int64_t arena_words = 0;
   ClusterDev cl{};
@@ -287,6 +288,7 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<int>& S, c
   const int L = h->L;
   h->cfg.assign(h->ncfg, CfgDev{});
   h->cls.assign(h->ncfg, K2Class{});
+  h->bcls.assign(h->ncfg, K2Class{});
   int64_t off = 0;
   for (int i = 0; i < h->ncfg; ++i) {
     // a config with only a few (long) chains spreads each over more SMs
@@ -296,6 +298,8 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<int>& S, c
     K2Class k;
     if (!k2_pick_class(S[i], h->Q, single, &k)) FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
     h->cls[i] = k;
+    if (!k2_pick_class(S[i], h->Q, true, &h->bcls[i]) || h->bcls[i].NS != k.NS)
+      FAIL(h, UNIAP_ERR_ARG, "no traceback class for |S|=%d Q=%d", S[i], h->Q);
     CfgDev& d = h->cfg[i];
     const int NSP = round4(k.NS);
     d.deg = deg[i]; d.c = c[i]; d.S = S[i]; d.NSP = NSP; d.g = g[i]; d.skip = skipc[i];
@@ -783,10 +787,10 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     R.max_deg = std::max(R.max_deg, std::min(d.deg, h->L));
     int g = -1;
     for (size_t j = 0; j < R.bgrp.size(); ++j)
-      if (class_key(R.bgrp[j].cls) == class_key(h->cls[i])) g = (int)j;
+      if (class_key(R.bgrp[j].cls) == class_key(h->bcls[i])) g = (int)j;
     if (g < 0) {
       g = (int)R.bgrp.size();
-      R.bgrp.push_back(K2Group{0, 0, h->cls[i], 0.0, 0});
+      R.bgrp.push_back(K2Group{0, 0, h->bcls[i], 0.0, 0});
     }
     R.bgrp[g].max_inst = std::max(R.bgrp[g].max_inst, bound);
     cls_of_cfg[i] = g;
