@@ -148,28 +148,27 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   // yields A' + min_k'(D + R) directly and the shift is a plain shifted copy.
   // (D <= INF = 2^30, R' <= 2^23: no overflow; the INF-initialised
   // accumulator clamps every E at INF.)
-  auto a_prime = [&](int u, int k) -> int32_t {
-    int32_t a = __ldg(gA + (int64_t)u * NSP + k);
-    if (ks >= 0 && u >= skip + 2) a += __ldg(gRs + ((int64_t)u * NSP + ks) * NSP + k);
-    return a;
-  };
-  auto stage_word = [&](int u, int e, int w) -> int32_t {
-    if (w < NS * NSP) return __ldg(gR + (int64_t)e * NSP * NSP + w) + a_prime(u, w / NSP);
-    const int x = w - NS * NSP, k = x >> 1;
-    if (x & 1) {
-      int32_t m = min(__ldg(gM + (int64_t)u * NSP + k), MBIG);
-      if (ks >= 0 && u == skip && k != ks) m = MBIG;
-      return m;
-    }
-    return a_prime(u, k);
-  };
-  int32_t pre[PER];
+  // Raw words are loaded two layers ahead and combined only when stored one
+  // layer ahead, so no arithmetic waits on an in-flight load (the loads go
+  // to L2: every cluster barrier invalidates L1).
+  int32_t pre_x[PER], pre_a[PER], pre_s[PER];  // R or M word, A, Rskip
+  int pre_u = 0;                                // layer of the fetched stage
   auto fetch_stage = [&](int step, int u_next) {  // global -> registers (issued early)
     const int e = in.dir > 0 ? u_next - 1 : u_next;
+    const bool sk = ks >= 0 && u_next >= skip + 2;
+    pre_u = u_next;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int w = t + i * T;
-      pre[i] = (w < SW && step < in.n) ? stage_word(u_next, e, w) : 0;
+      pre_x[i] = pre_a[i] = pre_s[i] = 0;
+      if (w < SW && step < in.n) {
+        const bool isR = w < NS * NSP;
+        const int x = w - NS * NSP;
+        const int k = isR ? w / NSP : (x >> 1);
+        pre_x[i] = isR ? __ldg(gR + (int64_t)e * NSP * NSP + w) : ((x & 1) ? __ldg(gM + (int64_t)u_next * NSP + k) : 0);
+        pre_a[i] = (isR || !(x & 1)) ? __ldg(gA + (int64_t)u_next * NSP + k) : 0;
+        pre_s[i] = (sk && (isR || !(x & 1))) ? __ldg(gRs + ((int64_t)u_next * NSP + ks) * NSP + k) : 0;
+      }
     }
   };
   auto store_stage = [&](int step) {  // registers -> shared (before the barrier)
@@ -177,7 +176,21 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int w = t + i * T;
-      if (w < SW) dst[w] = pre[i];
+      if (w < SW) {
+        int32_t v;
+        if (w < NS * NSP) {
+          v = pre_x[i] + pre_a[i] + pre_s[i];  // R' = R + A' of the destination
+        } else {
+          const int x = w - NS * NSP, k = x >> 1;
+          if (x & 1) {
+            v = min(pre_x[i], MBIG);
+            if (ks >= 0 && pre_u == skip && k != ks) v = MBIG;
+          } else {
+            v = pre_a[i] + pre_s[i];
+          }
+        }
+        dst[w] = v;
+      }
     }
   };
 
