@@ -314,9 +314,18 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       if constexpr (CL) mmax = max(mmax, am.y <= cap ? am.y : 0);  // forbidden rows are all INF
       const int32_t bk = (k * ROW + t - am.y) * 4;  // byte offset of bucket t - M in row k
       const int32_t gk = k * ROW * 4 - 4;          // the row's guard word
+      if (V > 1 && am.y <= T) {
+        // (warp-uniform) only j = 0 can fall below the row start: the other
+        // buckets read at constant offsets from one clamped base
+        const char* base = Ec + bk;
+        d[k][0] = *reinterpret_cast<const int32_t*>(Ec + max(bk, gk));
 #pragma unroll
-      for (int j = 0; j < V; ++j)
-        d[k][j] = *reinterpret_cast<const int32_t*>(Ec + __viaddmax_s32(bk, j * T * 4, gk));
+        for (int j = 1; j < V; ++j) d[k][j] = *reinterpret_cast<const int32_t*>(base + j * T * 4);
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          d[k][j] = *reinterpret_cast<const int32_t*>(Ec + __viaddmax_s32(bk, j * T * 4, gk));
+      }
     }
     if constexpr (CL) {
       // buckets whose shifted source q - M lies in a lower CTA's range: the
