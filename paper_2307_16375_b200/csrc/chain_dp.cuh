@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       if constexpr (CL) mmax = max(mmax, am.y <= cap ? am.y : 0);  // forbidden rows are all INF
       const int32_t bk = (k * ROW + t - am.y) * 4;  // byte offset of bucket t - M in row k
       const int32_t gk = k * ROW * 4 - 4;          // the row's guard word
-      if (V > 1 && am.y <= T) {
+      if (V > 1 && am.y <= T && !(args.flags & 2)) {
         // (warp-uniform) only j = 0 can fall below the row start: the other
         // buckets read at constant offsets from one clamped base
         const char* base = Ec + bk;

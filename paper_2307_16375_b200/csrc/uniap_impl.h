@@ -56,7 +56,8 @@ struct K2Args {
   int32_t* P;
   int32_t* G;
   int32_t L, cap, skip;
-  int32_t flags;  // experiments only (UNIAP_K2_FLAGS): bit 0 = relaxed cluster arrive (NOT memory-model safe)
+  int32_t flags;  // experiments only (UNIAP_K2_FLAGS): bit 0 = relaxed cluster arrive (NOT memory-model
+                  // safe), bit 1 = always clamp every shifted read
 };
 
 // Kernel class: template shape of K2.
