@@ -67,6 +67,8 @@ struct RunPlan {
   const uniap_record* rec = nullptr;
   std::vector<int32_t> local;
   std::vector<K2Group> fgrp, bgrp;
+  std::vector<std::pair<int, int>> k4range;  // per forward group: its configs in `local`
+  std::pair<int, int> k4rest{0, 0};          // configs without chain-DP work (deg > L)
   int max_deg = 0;
 };
 
@@ -106,6 +108,7 @@ struct uniap_handle {
   std::vector<cudaStream_t> side;          // K2 classes run concurrently
   std::vector<cudaEvent_t> side_ev;
   cudaEvent_t fork_ev = nullptr;
+  std::vector<cudaEvent_t> k2_end;         // per forward group: end of its K2 (timing)
   RunPlan plan;                            // launch plan of the last (rank, world)
   DevBuf<int32_t> clsid;
   DevBuf<BwPlan> bwp;
@@ -272,6 +275,7 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   for (auto e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto e : h->side_ev) cudaEventDestroy(e);
+  for (auto e : h->k2_end) cudaEventDestroy(e);
   for (auto x : h->side) cudaStreamDestroy(x);
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   if (h->own_stream) cudaStreamDestroy(h->st);
@@ -709,11 +713,19 @@ static uniap_status ensure_side_streams(uniap_handle* h, size_t n) {
 }
 
 // Enqueue K2 launches of `grp` (instances at `dinst`) on h->st with fork/join.
+// Per-group follow-up on the group's stream (K4 of the group's configs).
+struct GroupTail {
+  const std::vector<std::pair<int, int>>* ranges;  // [group] -> (li0, count) in the local config list
+  bool timing;                                     // record the K2 end event of every group
+};
+
+static uniap_status enqueue_k4_range(uniap_handle* h, int li0, int cnt, cudaStream_t st);
+
 static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp, const Inst* dinst,
-                               const int32_t* dcount_per_class, int32_t* Pdev) {
-  const bool fork = grp.size() > 1;
+                               const int32_t* dcount_per_class, int32_t* Pdev, const GroupTail* tail = nullptr) {
+  const bool fork = grp.size() > 1 || tail;
   if (fork) {
-    uniap_status s = ensure_side_streams(h, grp.size());
+    uniap_status s = ensure_side_streams(h, std::max<size_t>(grp.size(), 1));
     if (s != UNIAP_OK) return s;
     CK(h, cudaEventRecord(h->fork_ev, h->st));
   }
@@ -727,6 +739,13 @@ static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp,
     CK(h, k2_launch(grp[g].cls, args, n, st));
     h->launches++;
     h->k2_launches++;
+    if (tail) {
+      if (tail->timing)
+        CK(h, cudaEventRecordWithFlags(h->k2_end[g], st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+      const auto& r = (*tail->ranges)[g];
+      uniap_status s = enqueue_k4_range(h, r.first, r.second, st);
+      if (s != UNIAP_OK) return s;
+    }
     if (fork) CK(h, cudaEventRecord(h->side_ev[g], st));
   }
   if (fork)
@@ -774,6 +793,32 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     for (auto& x : cv) h->cells_canon += (uint64_t)x.n * h->cfg[i].S * h->Q;
   }
   group_instances(h, fw, R.fgrp);
+  // local configs ordered by forward group, so each group's K4 takes a range
+  {
+    std::vector<int32_t> ordered;
+    std::vector<char> used(h->ncfg, 0);
+    R.k4range.assign(R.fgrp.size(), {0, 0});
+    for (size_t g = 0; g < R.fgrp.size(); ++g) {
+      const int start = (int)ordered.size();
+      for (int i : R.local)
+        if (!used[i] && class_key(h->cls[i]) == class_key(R.fgrp[g].cls)) {
+          bool has = false;
+          for (size_t j = R.fgrp[g].s; j < R.fgrp[g].e && !has; ++j) has = fw[j].cfg == i;
+          if (has) { ordered.push_back(i); used[i] = 1; }
+        }
+      R.k4range[g] = {start, (int)ordered.size() - start};
+    }
+    const int rest0 = (int)ordered.size();
+    for (int i : R.local)
+      if (!used[i]) ordered.push_back(i);
+    R.k4rest = {rest0, (int)ordered.size() - rest0};
+    R.local.swap(ordered);
+  }
+  while (h->k2_end.size() < R.fgrp.size()) {
+    cudaEvent_t e;
+    CK(h, cudaEventCreate(&e));
+    h->k2_end.push_back(e);
+  }
   // backward: one device-sized launch per kernel class of the local configs
   std::vector<int32_t> cls_of_cfg(h->ncfg, 0);
   R.bgrp.clear();
@@ -825,6 +870,14 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   return UNIAP_OK;
 }
 
+static uniap_status enqueue_k4_range(uniap_handle* h, int li0, int cnt, cudaStream_t st) {
+  if (cnt <= 0) return UNIAP_OK;
+  CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, li0, cnt, h->L, h->thetas.p, h->ntheta.p, h->vals.p,
+                  h->cfgopt.p, st));
+  h->launches++;
+  return UNIAP_OK;
+}
+
 // The whole path for this rank, enqueued on h->st with no host
 // synchronisation (so it can be captured as one CUDA graph).
 static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
@@ -838,17 +891,19 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   h->launches++;
   CK(h, cudaEventRecordWithFlags(h->ev[1], h->st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
   {
-    uniap_status s = enqueue_k2(h, R.fgrp, h->inst.p, nullptr, h->P.p);
+    // K2 per class on side streams, each followed by the K4 of its configs
+    GroupTail tail{&R.k4range, true};
+    uniap_status s = enqueue_k2(h, R.fgrp, h->inst.p, nullptr, h->P.p, R.fgrp.empty() ? nullptr : &tail);
+    if (s != UNIAP_OK) return s;
+    s = enqueue_k4_range(h, R.k4rest.first, R.k4rest.second, h->st);
     if (s != UNIAP_OK) return s;
   }
   CK(h, cudaEventRecordWithFlags(h->ev[2], h->st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
-  CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
-                  h->cfgopt.p, h->st));
   RecordArgs ra{rec, h->cells, h->relax, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
                 h->binst.p, h->bwp.p};
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
                    h->cfgopt.p, h->scratch.p, h->win.p, ra, h->st));
-  h->launches += nl > 0 ? 2 : 1;
+  h->launches += 1;
   // traceback: backward sweeps sized on the device, then the strategy walk
   {
     uniap_status s = enqueue_k2(h, R.bgrp, h->binst.p, h->bwp.p->count, h->P.p);
@@ -928,7 +983,11 @@ extern "C" uniap_status uniap_fetch(uniap_handle* h, uniap_result* out) {
   }
   if (h->timed) {
     CK(h, cudaStreamSynchronize(h->st));
-    cudaEventElapsedTime(&h->ms_dp, h->ev[1], h->ev[2]);
+    h->ms_dp = 0.f;
+    for (size_t g = 0; g < h->plan.fgrp.size() && g < h->k2_end.size(); ++g) {
+      float x = 0.f;
+      if (cudaEventElapsedTime(&x, h->ev[1], h->k2_end[g]) == cudaSuccess) h->ms_dp = std::max(h->ms_dp, x);
+    }
     cudaEventElapsedTime(&h->ms_total, h->ev[0], h->ev[3]);
     h->timed = false;
   }

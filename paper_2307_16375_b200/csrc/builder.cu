@@ -202,20 +202,29 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
       for (int p = 0; p <= 61; ++p)
         if (okp[p]) { q = (int64_t)1 << p; break; }
     bb.qcfg[blockIdx.x] = q;
-    // the last config block to finish sets the global quantum = max over the
-    // configs (every check is monotone in q), or flags "no quantum fits"
     __threadfence();
     unsigned int* done = reinterpret_cast<unsigned int*>(bb.qglob + 2);
-    if (atomicAdd(done, 1u) == gridDim.x - 1) {
-      __threadfence();
-      int64_t g = 1;
-      for (int i = 0; i < (int)gridDim.x; ++i) {
-        const int64_t x = *reinterpret_cast<volatile int64_t*>(bb.qcfg + i);
-        if (x < 0) { atomicOr(reinterpret_cast<unsigned long long*>(bb.qglob + 1), 2ull); g = -1; break; }
-        g = max(g, x);
-      }
-      bb.qglob[0] = g;
-      *done = 0u;  // ready for the next run (graph replays)
+    okp[0] = atomicAdd(done, 1u) == gridDim.x - 1;  // this block finished last
+  }
+  __syncthreads();
+  // the last config block sets the global quantum = max over the configs
+  // (every check is monotone in q), or flags "no quantum fits"
+  if (okp[0]) {
+    __threadfence();
+    __shared__ long long red[64];
+    long long g = 1;
+    for (int i = t; i < (int)gridDim.x; i += blockDim.x) {
+      const long long x = *reinterpret_cast<volatile long long*>(bb.qcfg + i);
+      g = (x < 0 || g < 0) ? -1 : max(g, x);
+    }
+    red[t] = g;
+    __syncthreads();
+    if (t == 0) {
+      long long r = 1;
+      for (int i = 0; i < (int)blockDim.x; ++i) r = (red[i] < 0 || r < 0) ? -1 : max(r, red[i]);
+      if (r < 0) atomicOr(reinterpret_cast<unsigned long long*>(bb.qglob + 1), 2ull);
+      bb.qglob[0] = r;
+      *reinterpret_cast<unsigned int*>(bb.qglob + 2) = 0u;  // ready for the next run (graph replays)
     }
   }
 }

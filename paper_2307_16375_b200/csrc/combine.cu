@@ -172,7 +172,7 @@ struct K4Smem {
 
 __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
                                                    const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
-                                                   int L, int32_t* __restrict__ thetas,
+                                                   int li0, int L, int32_t* __restrict__ thetas,
                                                    int32_t* __restrict__ ntheta, int64_t* __restrict__ vals,
                                                    int64_t* __restrict__ cfg_opt) {
   extern __shared__ __align__(16) unsigned char k4raw[];
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
   int& s_hi = S.s_hi;
   unsigned long long& s_best = S.s_best;
   auto g = S.g;
-  const int li = blockIdx.x;
+  const int li = li0 + blockIdx.x;
   const CfgDev cf = cfgs[cfg_list[li]];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // K3 fused: the sorted distinct theta candidates (also kept for K5a)
@@ -261,8 +261,9 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
   }
 }
 
-cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
-                      int L, int32_t* thetas, int32_t* ntheta, int64_t* vals, int64_t* cfg_opt, cudaStream_t st) {
+cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int li0,
+                      int n_local, int L, int32_t* thetas, int32_t* ntheta, int64_t* vals, int64_t* cfg_opt,
+                      cudaStream_t st) {
   if (n_local <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -270,7 +271,7 @@ cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P,
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k4_vals<<<n_local, K4W * 32, sizeof(K4Smem), st>>>(cfg, arena, P, cfg_list, L, thetas, ntheta, vals, cfg_opt);
+  k4_vals<<<n_local, K4W * 32, sizeof(K4Smem), st>>>(cfg, arena, P, cfg_list, li0, L, thetas, ntheta, vals, cfg_opt);
   return cudaGetLastError();
 }
 
