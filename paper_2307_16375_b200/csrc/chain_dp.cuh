@@ -332,7 +332,18 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       // local read above returned the guard (INF); fetch the value over DSMEM
       const uint32_t tok = cl_wait_tok();
       const int wbase = t & ~31;
-      if (rank > 0 && wbase < mmax) {  // warp-uniform: only the low warps of a CTA
+      if (rank > 0 && wbase < mmax && mmax <= T && !(args.flags & 4)) {
+        // common case (every shift <= T): only bucket j = 0 of threads t < M_k
+        // needs a fix-up, and its source is bucket B + t - M_k of CTA rank-1:
+        // one mapped base per layer, one predicated load per row
+        // (generic loads: ordered after the wait by its memory clobber)
+        const int32_t* rb = map_rank(Eb + B + t, (uint32_t)rank - 1);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const int mk = Tb[NS * NSP + 2 * k + 1];  // > cap >= T when forbidden
+          if (t < mk && mk <= T) d[k][0] = rb[k * ROW - mk];
+        }
+      } else if (rank > 0 && wbase < mmax) {  // warp-uniform: only the low warps of a CTA
         // predicated loads, all in flight together: a cell that needs no
         // fix-up reads its own E word (shared::cluster window, own rank)
         const uint32_t ebase = (uint32_t)__cvta_generic_to_shared(Eb) + tok;
