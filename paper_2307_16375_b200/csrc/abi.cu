@@ -59,6 +59,7 @@ struct K2Group {
   K2Class cls;
   double crit;
   int max_inst;  // device-sized launches (backward): grid bound
+  int priority = 0;  // launch priority (cluster classes and long critical paths first)
 };
 
 struct RunPlan {
@@ -112,6 +113,7 @@ struct uniap_handle {
   RunPlan plan;                            // launch plan of the last (rank, world)
   DevBuf<int32_t> clsid;
   DevBuf<BwPlan> bwp;
+  DevBuf<unsigned long long> trace;        // UNIAP_TRACE: K2 per-CTA timeline (diagnostics)
   cudaGraphExec_t graph_exec = nullptr;    // the captured pipeline of `plan`
   uint32_t graph_launches = 0, graph_k2 = 0;
   bool capturing = false, timed = false;
@@ -127,7 +129,7 @@ static void update_signature(uniap_handle* h) {
     const CfgDev& d = h->cfg[i];
     const K2Class& k = h->cls[i];
     for (int64_t x : {(int64_t)d.deg, (int64_t)d.c, (int64_t)d.S, (int64_t)d.NSP, (int64_t)d.skip, d.offA, d.offP,
-                      (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C, (int64_t)k.DB})
+                      (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C, (int64_t)k.DB, (int64_t)k.G})
       sg.push_back(x);
   }
   if (h->level2) {
@@ -668,7 +670,7 @@ extern "C" uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32
 // per-layer synchronisation) -- so it starts on free SMs.
 // ---------------------------------------------------------------------------
 
-static int class_key(const K2Class& k) { return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C + (k.DB ? 0 : 50000); }
+static int class_key(const K2Class& k) { return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C + (k.DB ? 0 : 50000) + k.G * 10000; }
 
 static void group_instances(const uniap_handle* h, std::vector<Inst>& all, std::vector<K2Group>& grp) {
   std::vector<int> key(all.size());
@@ -697,6 +699,21 @@ static void group_instances(const uniap_handle* h, std::vector<Inst>& all, std::
     s = e;
   }
   std::stable_sort(grp.begin(), grp.end(), [](const K2Group& a, const K2Group& b) { return a.crit > b.crit; });
+  // Launch priorities: a cluster launch needs C free SMs of one GPC at once,
+  // so once one-CTA classes hold the SMs it starves until they drain; cluster
+  // classes therefore get the highest priority, then the longest critical
+  // paths (UNIAP_K2_PRIO=0 disables).
+  static const bool prio_ok = !getenv("UNIAP_K2_PRIO") || atoi(getenv("UNIAP_K2_PRIO")) != 0;
+  int least = 0, greatest = 0;
+  if (prio_ok && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess && greatest < least) {
+    std::vector<size_t> ord(grp.size());
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+      if ((grp[a].cls.C > 1) != (grp[b].cls.C > 1)) return grp[a].cls.C > 1;
+      return grp[a].crit > grp[b].crit;
+    });
+    for (size_t r = 0; r < ord.size(); ++r) grp[ord[r]].priority = std::min(greatest + (int)r, least);
+  }
   all.swap(sorted);
 }
 
@@ -736,7 +753,14 @@ static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp,
     K2Args args{dcount_per_class ? dinst : dinst + grp[g].s,
                 dcount_per_class ? dcount_per_class + g : nullptr,
                 h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip, k2_flags()};
-    CK(h, k2_launch(grp[g].cls, args, n, st));
+    if (h->trace.p) {  // diagnostics: tag = class shape | forward/backward | group
+      const K2Class& k = grp[g].cls;
+      args.trace = h->trace.p;
+      args.tag = (uint32_t)k.NS | (uint32_t)k.V << 6 | (uint32_t)(k.T / 32) << 10 | (uint32_t)k.C << 16 |
+                 (uint32_t)k.G << 21 | (uint32_t)k.DB << 24 | (uint32_t)(dcount_per_class ? 1 : 0) << 25 |
+                 (uint32_t)(g & 31) << 26;
+    }
+    CK(h, k2_launch(grp[g].cls, args, n, st, grp[g].priority));
     h->launches++;
     h->k2_launches++;
     if (tail) {
@@ -883,6 +907,7 @@ static uniap_status enqueue_k4_range(uniap_handle* h, int li0, int cnt, cudaStre
 static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   const RunPlan& R = h->plan;
   const int L = h->L, nl = (int)R.local.size();
+  if (h->trace.p) CK(h, cudaMemsetAsync(h->trace.p, 0, 8, h->st));
   if (h->level2) {
     CK(h, launch_k1(h->cl, build_bufs(h), h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
     h->launches += 3;
@@ -931,6 +956,11 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
     uniap_status s = make_plan(h, rank, world, rec);
     if (s != UNIAP_OK) return s;
   }
+  if (getenv("UNIAP_TRACE") && !h->trace.p) {  // diagnostics: allocated before any capture
+    CK(h, h->trace.ensure(4 + 4 * (size_t)TRACE_CAP));
+    const unsigned long long hdr[2] = {0ull, (unsigned long long)TRACE_CAP};
+    CK(h, cudaMemcpy(h->trace.p, hdr, sizeof hdr, cudaMemcpyHostToDevice));
+  }
   const bool use_graph = !env_flag("UNIAP_NO_GRAPH");
   CK(h, cudaEventRecord(h->ev[0], h->st));
   if (use_graph) {
@@ -945,7 +975,7 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
       cudaError_t e = cudaStreamEndCapture(h->st, &g);
       if (s != UNIAP_OK) { if (g) cudaGraphDestroy(g); return s; }
       CK(h, e);
-      e = cudaGraphInstantiate(&h->graph_exec, g, 0);
+      e = cudaGraphInstantiate(&h->graph_exec, g, cudaGraphInstantiateFlagUseNodePriority);  // K2 launch priorities
       cudaGraphDestroy(g);
       CK(h, e);
       h->graph_launches = h->launches - l0;
@@ -990,6 +1020,20 @@ extern "C" uniap_status uniap_fetch(uniap_handle* h, uniap_result* out) {
     }
     cudaEventElapsedTime(&h->ms_total, h->ev[0], h->ev[3]);
     h->timed = false;
+  }
+  if (h->trace.p) {  // diagnostics: append this run's K2 timeline to $UNIAP_TRACE
+    CK(h, cudaStreamSynchronize(h->st));
+    unsigned long long n = 0;
+    CK(h, cudaMemcpy(&n, h->trace.p, 8, cudaMemcpyDeviceToHost));
+    n = std::min<unsigned long long>(n, TRACE_CAP);
+    std::vector<unsigned long long> r(4 * n);
+    if (n) CK(h, cudaMemcpy(r.data(), h->trace.p + 4, 32 * n, cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(getenv("UNIAP_TRACE"), "a")) {
+      fprintf(f, "run %llu\n", n);
+      for (unsigned long long i = 0; i < n; ++i)
+        fprintf(f, "%llu %llu %llu %llu\n", r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+      fclose(f);
+    }
   }
   int64_t* keep = out->cfg_objective;
   memset(out, 0, sizeof *out);

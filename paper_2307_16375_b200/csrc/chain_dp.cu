@@ -7,7 +7,7 @@
 namespace uniap {
 
 #define UNIAP_NS_LIST(X) X(1) X(2) X(3) X(4) X(6) X(8) X(10) X(12) X(15) X(16) X(21) X(24) X(32)
-#define UNIAP_EXTERN(N) extern template k2_fn k2_get<N>(int, int, bool, bool);
+#define UNIAP_EXTERN(N) extern template k2_fn k2_get<N>(int, int, bool, bool, int);
 UNIAP_NS_LIST(UNIAP_EXTERN)
 #undef UNIAP_EXTERN
 
@@ -45,6 +45,23 @@ static int env_int(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
+// One CTA per instance: the segmented schedule (chain_dp.cuh) overlaps the
+// shifted shared-memory reads with the E-step.  2 bucket slots per segment;
+// G = 2 needs the double-buffered E, G >= 3 works with a single buffer.
+// UNIAP_K2_SEG=0 keeps the phase-separated schedule (experiments).
+static void seg_class(K2Class* c) {
+  static const int seg_ok = env_int("UNIAP_K2_SEG", 1);
+  if (!seg_ok) return;
+  if (c->V == 8 && c->T == 512 && c->NS <= 10) {  // 4 segments, one E buffer
+    c->DB = false;
+    c->G = 4;
+  } else if (c->V == 4 && c->DB && c->NS <= (c->T == 512 ? 12 : 16)) {
+    c->G = 2;
+  } else if (c->V == 4 && c->T == 512 && !c->DB && c->NS > 12 && c->NS <= 24) {
+    c->G = 4;
+  }
+}
+
 bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   const int NS = k2_ns_round(S);
   if (NS < 0 || Q < 1 || Q > UNIAP_MAX_Q) return false;
@@ -78,7 +95,9 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
     const bool shape = (Bs == 4096 && NS > 6 && NS <= 10) || (Bs == 2048 && NS > 12 && NS <= 24) ||
                        (Bs == 1024 && NS > 24);
     if (shape && smem_words(NS, Bs, 1) * 4 <= lim) {
-      *out = K2Class{NS, Bs / 512, 512, 1, false};
+      K2Class c{NS, Bs / 512, 512, 1, false};
+      seg_class(&c);
+      *out = c;
       return true;
     }
   }
@@ -88,6 +107,7 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   if (B == 32) { c.V = 1; c.T = 32; }
   if (B == 2048) { c.V = 4; c.T = 512; }
   if (B == 4096) { c.V = 8; c.T = 512; }
+  if (C == 1) seg_class(&c);
   *out = c;
   return true;
 }
@@ -96,7 +116,7 @@ static k2_fn k2_lookup(const K2Class& c) {
   const bool CL = c.C > 1;
   switch (c.NS) {
 #define UNIAP_CASE(N) \
-  case N: return k2_get<N>(c.V, c.T, CL, c.DB);
+  case N: return k2_get<N>(c.V, c.T, CL, c.DB, c.G);
     UNIAP_NS_LIST(UNIAP_CASE)
 #undef UNIAP_CASE
     default: return nullptr;
@@ -131,7 +151,7 @@ int k2_selftest(int* S_out, int* Q_out, int* single_out) {
   return 0;
 }
 
-cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st) {
+cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st, int priority) {
   if (n_inst <= 0) return cudaSuccess;
   k2_fn fn = k2_lookup(c);
   if (!fn) return cudaErrorInvalidDeviceFunction;
@@ -156,15 +176,20 @@ cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStre
   cfg.blockDim = dim3((unsigned)c.T);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   cfg.attrs = attr;
   cfg.numAttrs = 0;
   if (c.C > 1) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)c.C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.numAttrs = 1;
+    attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+    attr[cfg.numAttrs].val.clusterDim.x = (unsigned)c.C;
+    attr[cfg.numAttrs].val.clusterDim.y = 1;
+    attr[cfg.numAttrs].val.clusterDim.z = 1;
+    cfg.numAttrs++;
+  }
+  if (priority != 0) {  // the block scheduler serves pending CTAs of higher priority first
+    attr[cfg.numAttrs].id = cudaLaunchAttributePriority;
+    attr[cfg.numAttrs].val.priority = priority;
+    cfg.numAttrs++;
   }
   return cudaLaunchKernelEx(&cfg, fn, args);
 }

@@ -95,6 +95,15 @@ __device__ __forceinline__ int32_t lds32(uint32_t addr) {
   return v;
 }
 
+// Compile-time loop: f(integral_constant<int, I>) for I = B .. E-1.
+template <int I, int E, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < E) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, E>(f);
+  }
+}
+
 __device__ __forceinline__ int comp(const int4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
 // Shared-memory words of one "table stage" (the tables of one layer step):
@@ -105,9 +114,10 @@ struct Stage {
   static constexpr int WORDS = NS * NSP + 2 * NSP;
 };
 
-template <int NS, int V, int T, bool CL, bool DB = true>
+template <int NS, int V, int T, bool CL, bool DB = true, int G = 0>
 __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   static_assert(DB || !CL, "single-buffered E only without clusters");
+  static_assert(G == 0 || !CL, "segmented schedule only without clusters");
   constexpr int B = T * V;          // buckets per CTA
   constexpr int ROW = B + 4;        // 4 guard words + B buckets
   constexpr int NE = DB ? 2 : 1;    // E buffers (single: a second barrier per layer)
@@ -126,6 +136,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     ii = blockIdx.x / (int)cl_size();
   }
   if (args.n_inst && ii >= *args.n_inst) return;  // device-sized launch: spare CTA (whole cluster)
+  const unsigned long long t_start = args.trace ? gtimer() : 0ull;
   const Inst in = args.inst[ii];
   const CfgDev cf = args.cfg[in.cfg];
   const int32_t* __restrict__ gA = args.arena + cf.offA;
@@ -245,6 +256,150 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   __syncthreads();
   emit(u);
 
+  if constexpr (G > 0) {
+    // ---- segmented schedule (one CTA per instance) -----------------------
+    // The bucket slots j are split into G segments of VS slots.  Phase g of
+    // a layer computes E of segment g (ALU) while the shifted reads of
+    // segment g-1 of the same layer (or of segment G-1 of the previous layer,
+    // for g = 0) are in flight (shared memory): a shift only reads lower
+    // buckets, so segment g-1's shift needs E of segments <= g-1, complete at
+    // the previous phase's barrier.  The per-layer shared-memory traffic thus
+    // overlaps the E-step inside each warp's instruction stream instead of
+    // forming a phase of its own.  With one E buffer (NE = 1, G >= 3) the
+    // only hazard is the deferred shift of segment G-1 reading segment 0 while
+    // phase 0 of the next layer overwrites it: possible only when a shift
+    // exceeds (G-2) segments; such a layer shifts segment G-1 at its end.
+    constexpr int VS = V / G;
+    constexpr int SEGB = VS * T;
+    static_assert(V % G == 0 && (NE == 2 || G >= 3), "segment shape");
+    auto shift_seg = [&](int g, const int32_t* Ebuf, const int32_t* Tst) {
+      const char* Ec = reinterpret_cast<const char*>(Ebuf);
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const int mk = Tst[NS * NSP + 2 * k + 1];
+        const int32_t bk = (k * ROW + t - mk) * 4;
+        const int32_t gk = k * ROW * 4 - 4;
+#pragma unroll
+        for (int jj = 0; jj < VS; ++jj) {
+          const int j = g * VS + jj;
+          if (j > 0 && mk <= j * T)  // warp-uniform: the source is inside the row
+            d[k][j] = *reinterpret_cast<const int32_t*>(Ec + bk + j * T * 4);
+          else
+            d[k][j] = *reinterpret_cast<const int32_t*>(Ec + __viaddmax_s32(bk, j * T * 4, gk));
+        }
+      }
+    };
+    auto estep_seg = [&](int g, int32_t* Ebuf, const int32_t* Tst) {
+      int32_t* Et = Ebuf + t;
+      auto rows = [&](auto rrc, int k) {
+        constexpr int RR = decltype(rrc)::value;
+        int32_t acc[RR][VS];
+#pragma unroll
+        for (int r = 0; r < RR; ++r)
+#pragma unroll
+          for (int jj = 0; jj < VS; ++jj) acc[r][jj] = INF;
+#pragma unroll
+        for (int c = 0; c < NSP / 4; ++c) {
+          int4 x[RR];
+#pragma unroll
+          for (int r = 0; r < RR; ++r) x[r] = reinterpret_cast<const int4*>(Tst + (k + r) * NSP)[c];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (4 * c + i < NS)
+#pragma unroll
+              for (int r = 0; r < RR; ++r)
+#pragma unroll
+                for (int jj = 0; jj < VS; ++jj)
+                  acc[r][jj] = addmin(d[4 * c + i][g * VS + jj], comp(x[r], i), acc[r][jj]);
+        }
+#pragma unroll
+        for (int r = 0; r < RR; ++r)
+#pragma unroll
+          for (int jj = 0; jj < VS; ++jj) Et[(k + r) * ROW + (g * VS + jj) * T] = acc[r][jj];
+      };
+      constexpr int RR = 4;
+      constexpr int RRC = RR < NS ? RR : NS;
+      constexpr int NFULL = NS / RRC * RRC;
+      if constexpr (NS <= KUNROLL) {
+#pragma unroll
+        for (int k = 0; k < NFULL; k += RRC) rows(std::integral_constant<int, RRC>{}, k);
+      } else {
+#pragma unroll 1
+        for (int k = 0; k < NFULL; k += RRC) rows(std::integral_constant<int, RRC>{}, k);
+      }
+      if constexpr (NS - NFULL > 0) rows(std::integral_constant<int, NS - NFULL>{}, NFULL);
+    };
+    // stage optimum / backward table of layer uu for the slots of segment g
+    auto emit_seg = [&](int uu, int g) {
+      if (in.emit != 0) {
+        const int jc = cap / T, tc = cap - jc * T;  // C = 1: cap < B
+        if (jc / VS == g && t == tc) {
+          int32_t v = INF;
+#pragma unroll
+          for (int jj = 0; jj < VS; ++jj)
+            if (g * VS + jj == jc)
+#pragma unroll
+              for (int k = 0; k < NS; ++k) v = min(v, d[k][g * VS + jj]);
+          sProw[uu] = v;
+        }
+      } else {
+        const int lo = in.a - in.n + 1;
+        int32_t* gp = args.G + in.gofs + (int64_t)(uu - lo) * NSP * Q;
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+          for (int jj = 0; jj < VS; ++jj) {
+            const int q = (g * VS + jj) * T + t;
+            if (q < Q) gp[(int64_t)k * Q + q] = d[k][g * VS + jj];
+          }
+      }
+    };
+    bool pend = false;  // the shift of segment G-1 of the previous layer
+    for (int step = 1; step < in.n; ++step) {
+      u += in.dir;
+      int32_t* Eb = sE + (NE == 2 ? (step & 1) * NS * ROW : 0) + 4;
+      const int32_t* Ep = sE + (NE == 2 ? ((step - 1) & 1) * NS * ROW : 0) + 4;
+      const int32_t* Tb = sT + (step % 3) * SW;
+      const int32_t* Tp = sT + ((step + 2) % 3) * SW;  // the previous layer's stage
+      static_for<0, G>([&](auto gc) {
+        constexpr int g = decltype(gc)::value;
+        if (g == 0) {
+          if (pend) shift_seg(G - 1, Ep, Tp);
+        } else {
+          shift_seg(g - 1, Eb, Tb);
+        }
+        estep_seg(g, Eb, Tb);
+        if (g == 0) {
+          if (pend) emit_seg(u - in.dir, G - 1);
+          if (step + 1 < in.n) store_stage(step + 1);
+          if (step + 2 < in.n) fetch_stage(step + 2, u + 2 * in.dir);
+        } else {
+          emit_seg(u, g - 1);
+        }
+        __syncthreads();
+      });
+      pend = true;
+      if constexpr (NE == 1) {
+        int32_t mmax = 0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const int mk = Tb[NS * NSP + 2 * k + 1];
+          mmax = max(mmax, mk <= cap ? mk : 0);  // forbidden rows read only the guard
+        }
+        if (mmax > (G - 2) * SEGB) {
+          shift_seg(G - 1, Eb, Tb);
+          emit_seg(u, G - 1);
+          __syncthreads();
+          pend = false;
+        }
+      }
+    }
+    if (pend) {
+      const int step = in.n - 1;
+      shift_seg(G - 1, sE + (NE == 2 ? (step & 1) * NS * ROW : 0) + 4, sT + (step % 3) * SW);
+      emit_seg(u, G - 1);
+    }
+  } else
   for (int step = 1; step < in.n; ++step) {
     u += in.dir;
     int32_t* Eb = sE + (DB ? (step & 1) * NS * ROW : 0) + 4;  // row 0, bucket 0
@@ -376,6 +531,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     }
   }
   if constexpr (CL) cl_sync();  // keep this CTA's E alive for remote readers
+  if (args.trace && t == 0) trace_put(args.trace, args.tag, t_start, rank, ii, in.n);
 }
 
 template <int NS>
@@ -388,7 +544,15 @@ constexpr size_t k2_smem(int B, int ne = 2) {
 typedef void (*k2_fn)(const K2Args);
 
 template <int NS>
-k2_fn k2_get(int V, int T, bool CL, bool DB) {
+k2_fn k2_get(int V, int T, bool CL, bool DB, int G = 0) {
+  if (G > 0) {  // segmented schedule, one CTA per instance
+    if (CL) return nullptr;
+    if constexpr (NS <= 10) if (V == 8 && T == 512 && !DB && G == 4) return k2_chain<NS, 8, 512, false, false, 4>;
+    if constexpr (NS <= 12) if (V == 4 && T == 512 && DB && G == 2) return k2_chain<NS, 4, 512, false, true, 2>;
+    if constexpr (NS > 12 && NS <= 24) if (V == 4 && T == 512 && !DB && G == 4) return k2_chain<NS, 4, 512, false, false, 4>;
+    if constexpr (NS <= 16) if (V == 4 && T == 256 && DB && G == 2) return k2_chain<NS, 4, 256, false, true, 2>;
+    return nullptr;
+  }
   if (!DB) {  // single-buffered E, one CTA per instance (large B without a cluster)
     if (CL) return nullptr;
     if constexpr (NS > 24 && k2_smem<NS>(1024, 1) <= 200 * 1024) if (V == 2 && T == 512) return k2_chain<NS, 2, 512, false, false>;

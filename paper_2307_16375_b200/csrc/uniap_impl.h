@@ -58,7 +58,33 @@ struct K2Args {
   int32_t L, cap, skip;
   int32_t flags;  // experiments only (UNIAP_K2_FLAGS): bit 0 = relaxed cluster arrive (NOT memory-model
                   // safe), bit 1 = always clamp every shifted read
+  // diagnostics (UNIAP_TRACE): per-CTA timeline records, or nullptr
+  unsigned long long* trace = nullptr;
+  uint32_t tag = 0;
 };
+
+// Timeline record of one CTA (UNIAP_TRACE): trace[0] = record count, trace[1]
+// = capacity, records of 4 words from trace[4]:
+//   {tag, %globaltimer at start, at end, smid | ctarank << 8 | inst << 16 | n << 40}
+constexpr int TRACE_CAP = 1 << 15;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_put(unsigned long long* tr, uint32_t tag, unsigned long long t0, uint32_t rank,
+                                          uint32_t inst, uint32_t n) {
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  const unsigned long long i = atomicAdd(tr, 1ull);
+  if (i < tr[1]) {
+    unsigned long long* r = tr + 4 + 4 * i;
+    r[0] = tag;
+    r[1] = t0;
+    r[2] = gtimer();
+    r[3] = sm | (rank << 8) | ((unsigned long long)inst << 16) | ((unsigned long long)n << 40);
+  }
+}
 
 // Kernel class: template shape of K2.
 struct K2Class {
@@ -67,6 +93,7 @@ struct K2Class {
   int T;       // threads per CTA
   int C;       // CTAs per cluster
   bool DB;     // double-buffered E (one barrier per layer); single: two
+  int G = 0;   // > 0: segmented schedule with G bucket segments (C = 1)
 };
 
 // chain_dp.cu
@@ -75,7 +102,9 @@ struct K2Class {
 bool k2_pick_class(int S, int Q, bool single, K2Class* out);
 int k2_ns_round(int S);
 size_t k2_smem_bytes(const K2Class& c);
-cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st);
+// priority: launch priority (0 = default; lower = served first, see
+// cudaDeviceGetStreamPriorityRange)
+cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st, int priority = 0);
 int k2_selftest(int* S_out, int* Q_out, int* single_out);
 
 // Winner of the combine step (written by K5a, read by the host and K5c).
