@@ -48,9 +48,10 @@ static int env_int(const char* name, int dflt) {
 // One CTA per instance: the segmented schedule (chain_dp.cuh) overlaps the
 // shifted shared-memory reads with the E-step.  2 bucket slots per segment;
 // G = 2 needs the double-buffered E, G >= 3 works with a single buffer.
-// UNIAP_K2_SEG=0 keeps the phase-separated schedule (experiments).
+// Measured slower than the phase-separated schedule on B200 (the R rows are
+// re-read per segment): off unless UNIAP_K2_SEG=1 (experiments).
 static void seg_class(K2Class* c) {
-  static const int seg_ok = env_int("UNIAP_K2_SEG", 1);
+  static const int seg_ok = env_int("UNIAP_K2_SEG", 0);
   if (!seg_ok) return;
   if (c->V == 8 && c->T == 512 && c->NS <= 10) {  // 4 segments, one E buffer
     c->DB = false;
