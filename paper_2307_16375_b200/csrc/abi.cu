@@ -9,6 +9,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -242,6 +243,15 @@ extern "C" uniap_status uniap_create(uniap_handle** out, int device, void* strea
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return UNIAP_ERR_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return UNIAP_ERR_CUDA;
+  {
+    static std::mutex mu;
+    static bool done = false;
+    std::lock_guard<std::mutex> g(mu);
+    if (!done) {
+      if (combine_init() != cudaSuccess || builder_init() != cudaSuccess) return UNIAP_ERR_CUDA;
+      done = true;
+    }
+  }
   uniap_handle* h = new uniap_handle();
   h->device = device;
   if (stream) {
@@ -909,10 +919,19 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   const int L = h->L, nl = (int)R.local.size();
   if (h->trace.p) CK(h, cudaMemsetAsync(h->trace.p, 0, 8, h->st));
   if (h->level2) {
+    // the P fill overlaps the builder (side stream, joined before K2)
+    uniap_status s = ensure_side_streams(h, 1);
+    if (s != UNIAP_OK) return s;
+    CK(h, cudaEventRecord(h->fork_ev, h->st));
+    CK(h, cudaStreamWaitEvent(h->side[0], h->fork_ev, 0));
+    CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->side[0]));
+    CK(h, cudaEventRecord(h->side_ev[0], h->side[0]));
     CK(h, launch_k1(h->cl, build_bufs(h), h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
+    CK(h, cudaStreamWaitEvent(h->st, h->side_ev[0], 0));
     h->launches += 3;
+  } else {
+    CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
   }
-  CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
   h->launches++;
   CK(h, cudaEventRecordWithFlags(h->ev[1], h->st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
   {
@@ -960,6 +979,8 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
     CK(h, h->trace.ensure(4 + 4 * (size_t)TRACE_CAP));
     const unsigned long long hdr[2] = {0ull, (unsigned long long)TRACE_CAP};
     CK(h, cudaMemcpy(h->trace.p, hdr, sizeof hdr, cudaMemcpyHostToDevice));
+    CK(h, combine_trace(h->trace.p));
+    CK(h, builder_trace(h->trace.p));
   }
   const bool use_graph = !env_flag("UNIAP_NO_GRAPH");
   CK(h, cudaEventRecord(h->ev[0], h->st));

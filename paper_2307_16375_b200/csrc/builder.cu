@@ -19,15 +19,61 @@ namespace uniap {
 typedef unsigned __int128 u128;
 constexpr int64_t NS_LIM = (int64_t)1 << 62;
 
-// ceil(x / y), exact; the common case (both below 2^64) takes the much
-// cheaper 64-bit division
+// (u1 * 2^64 + u0) / v for u1 < v (quotient < 2^64), remainder in *r:
+// two-digit long division in base 2^32 with normalised divisor (Knuth's
+// algorithm D as in Hacker's Delight, divlu) -- a few 64-bit operations
+// instead of the generic 128-bit division routine.
+__device__ __forceinline__ uint64_t divlu(uint64_t u1, uint64_t u0, uint64_t v, uint64_t* r) {
+  const uint64_t b = 1ull << 32;
+  const int s = __clzll(v);
+  v <<= s;
+  const uint64_t vn1 = v >> 32, vn0 = v & 0xffffffffull;
+  const uint64_t un32 = (u1 << s) | (s ? (u0 >> (64 - s)) : 0);
+  const uint64_t un10 = u0 << s;
+  const uint64_t un1 = un10 >> 32, un0 = un10 & 0xffffffffull;
+  uint64_t q1 = un32 / vn1, rhat = un32 - q1 * vn1;
+  while (q1 >= b || q1 * vn0 > b * rhat + un1) {
+    --q1;
+    rhat += vn1;
+    if (rhat >= b) break;
+  }
+  const uint64_t un21 = un32 * b + un1 - q1 * v;
+  uint64_t q0 = un21 / vn1;
+  rhat = un21 - q0 * vn1;
+  while (q0 >= b || q0 * vn0 > b * rhat + un0) {
+    --q0;
+    rhat += vn1;
+    if (rhat >= b) break;
+  }
+  *r = (un21 * b + un0 - q0 * v) >> s;
+  return q1 * b + q0;
+}
+
+// ceil(x / y), exact; both below 2^64: one 64-bit division; y below 2^64:
+// a 64-bit division of the high word and divlu for the low word
 __device__ __forceinline__ u128 cdiv128(u128 x, u128 y) {
-  if (((x | y) >> 64) == 0) {
-    const uint64_t a = (uint64_t)x, b = (uint64_t)y;
-    const uint64_t q = a / b;
-    return (u128)(q + (a - q * b != 0));
+  if ((y >> 64) == 0) {
+    const uint64_t yy = (uint64_t)y, hi = (uint64_t)(x >> 64), lo = (uint64_t)x;
+    if (hi == 0) {
+      const uint64_t q = lo / yy;
+      return (u128)(q + (lo - q * yy != 0));
+    }
+    const uint64_t qh = hi / yy;
+    uint64_t rem;
+    const uint64_t ql = divlu(hi - qh * yy, lo, yy, &rem);
+    return (((u128)qh << 64) | ql) + (rem != 0);
   }
   return (x + y - 1) / y;
+}
+
+// floor(x / y), exact, y < 2^64
+__device__ __forceinline__ u128 fdiv128(u128 x, uint64_t y) {
+  const uint64_t hi = (uint64_t)(x >> 64), lo = (uint64_t)x;
+  if (hi == 0) return (u128)(lo / y);
+  const uint64_t qh = hi / y;
+  uint64_t rem;
+  const uint64_t ql = divlu(hi - qh * y, lo, y, &rem);
+  return ((u128)qh << 64) | ql;
 }
 
 struct Coll {
@@ -90,7 +136,7 @@ __device__ void k1a_layers(const ClusterDev& cl, const BuildBufs& bb, const CfgD
   const u128 comp = 3 * fp;                                          // fp + bp, bp = 2 fp
   const u128 tpc = 3 * co.allreduce((u128)bl * bb.tpc[u], t, 1);     // TP collectives fwd + 2x bwd
   const u128 mn = comp < tpc ? comp : tpc;
-  const u128 ov = comp + tpc - (u128)cl.ccoc * mn / 1000;            // CCOC overlap (A-23)
+  const u128 ov = comp + tpc - fdiv128((u128)cl.ccoc * mn, 1000);   // CCOC overlap (A-23)
   const u128 ps_t = cdiv128((u128)ps, (u128)t), ps_tf = cdiv128((u128)ps, (u128)(t * f));
   const u128 fsdp = f > 1 ? 2 * co.allgather(ps_t, f, t) : 0;        // parameter gathers fwd + bwd
   const u128 sync = co.allreduce(ps_tf, d, t * f) + (f > 1 ? co.allgather(ps_t, f, t) : 0);
@@ -102,29 +148,31 @@ __device__ void k1a_layers(const ClusterDev& cl, const BuildBufs& bb, const CfgD
   amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + u) * 4, A[idx]);
 }
 
-// K1b: R (edge e = u->u+1), Rskip (edge skip->v) in ns, original [k][l] layout.
-__device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* __restrict__ cfgs, int L, int bx) {
+// K1b: R (edge e = u->u+1), Rskip (edge skip->v) in ns, original [k][l] layout
+// (nb blocks per config, grid-stride over the config's entries).
+__device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* __restrict__ cfgs, int L, int bx,
+                            int nb) {
   const CfgDev cf = cfgs[blockIdx.y];
   const int NSP = cf.NSP, n2 = NSP * NSP;
-  const int idx = bx * blockDim.x + threadIdx.x;
   const int nR = (L - 1) * n2, nS = L * n2;
-  if (idx >= nR + nS) return;
-  const bool isR = idx < nR;
-  const int j = isR ? idx : idx - nR;
-  const int e = j / n2, k = (j - e * n2) / NSP, l = j - e * n2 - k * NSP;
-  const int64_t b = cl.B / cf.c;
-  int64_t v = 0;
-  if (k < cf.S && l < cf.S) {
-    const int64_t tb = isR ? bb.chain[e] : bb.skipb[e];
-    if (tb >= 0) {
-      const Coll co{cl};
-      v = checked(co.reshard(bb.cat[blockIdx.y].tfd + 3 * k, bb.cat[blockIdx.y].tfd + 3 * l, (u128)b * tb), bb.qglob + 1);
+  for (int idx = bx * blockDim.x + threadIdx.x; idx < nR + nS; idx += nb * blockDim.x) {
+    const bool isR = idx < nR;
+    const int j = isR ? idx : idx - nR;
+    const int e = j / n2, k = (j - e * n2) / NSP, l = j - e * n2 - k * NSP;
+    const int64_t b = cl.B / cf.c;
+    int64_t v = 0;
+    if (k < cf.S && l < cf.S) {
+      const int64_t tb = isR ? bb.chain[e] : bb.skipb[e];
+      if (tb >= 0) {
+        const Coll co{cl};
+        v = checked(co.reshard(bb.cat[blockIdx.y].tfd + 3 * k, bb.cat[blockIdx.y].tfd + 3 * l, (u128)b * tb), bb.qglob + 1);
+      }
     }
+    (bb.ns + (isR ? cf.offRf : cf.offRs))[j] = v;
+    // per-layer maxima for the quantum: R of edge e goes into layer e+1
+    if (v > 0 && (isR || (cf.skip >= 0 && e >= cf.skip + 2)))
+      amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + (isR ? e + 1 : e)) * 4 + (isR ? 1 : 2), v);
   }
-  (bb.ns + (isR ? cf.offRf : cf.offRs))[j] = v;
-  // per-layer maxima for the quantum: R of edge e goes into layer e+1
-  if (v > 0 && (isR || (cf.skip >= 0 && e >= cf.skip + 2)))
-    amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + (isR ? e + 1 : e)) * 4 + (isR ? 1 : 2), v);
 }
 
 // K1c: cut costs: every edge crossing the cut after layer e, fwd + bwd P2P
@@ -154,9 +202,10 @@ __device__ void k1c_cuts(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
 constexpr int K1T = 256;
 __global__ void __launch_bounds__(K1T) k1_costs(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L,
                                                 int nbA, int nbR) {
+  TraceScope tr(TR_K1);
   const int bx = blockIdx.x;
   if (bx < nbA) k1a_layers(cl, bb, cfgs, L, bx);
-  else if (bx < nbA + nbR) k1b_reshard(cl, bb, cfgs, L, bx - nbA);
+  else if (bx < nbA + nbR) k1b_reshard(cl, bb, cfgs, L, bx - nbA, nbR);
   else k1c_cuts(cl, bb, cfgs, L);
 }
 
@@ -164,6 +213,7 @@ __global__ void __launch_bounds__(K1T) k1_costs(ClusterDev cl, BuildBufs bb, con
 // every ceil(x/q) <= 2^22 and sum_u (max A + max R into u + max Rskip into u)
 // <= 2^28, sum_e O <= 2^28.  An explicit quantum is checked as given.
 __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int skip) {
+  TraceScope tr(TR_K1D);
   __shared__ int64_t mx[MAXL * 4];
   __shared__ int okp[64];
   (void)cfgs;
@@ -231,6 +281,7 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
 
 // K1f: quantise into the int32 device layout (A, M buckets, Rt, Rf, Rs, O).
 __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int32_t* arena) {
+  TraceScope tr(TR_K1F);
   const CfgDev cf = cfgs[blockIdx.y];
   const int NSP = cf.NSP, n2 = NSP * NSP;
   const int64_t q = bb.qglob[0] > 0 ? bb.qglob[0] : 1;
@@ -272,11 +323,21 @@ cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* c
   e = cudaMemsetAsync(bb.qmax, 0, (size_t)ncfg * MAXL * 4 * sizeof(int64_t), st);
   if (e != cudaSuccess) return e;
   const int nbA = (L * 32 + K1T - 1) / K1T;
-  const int nbR = ((2 * L - 1) * 32 * 32 + K1T - 1) / K1T;
+  const int nbR = 16;  // grid-stride over (2L-1) NSP^2 entries per config
   k1_costs<<<dim3(nbA + nbR + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR);
   k1d_quantum<<<ncfg, 64, 0, st>>>(cl, bb, cfg, L, skip);
   k1f_quantise<<<dim3(16, ncfg), 256, 0, st>>>(cl, bb, cfg, L, arena);
   return cudaGetLastError();
+}
+
+cudaError_t builder_trace(unsigned long long* p) { return cudaMemcpyToSymbol(g_trace, &p, sizeof p); }
+
+cudaError_t builder_init() {
+  for (const void* f : {(const void*)k1_costs, (const void*)k1d_quantum, (const void*)k1f_quantise}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace uniap

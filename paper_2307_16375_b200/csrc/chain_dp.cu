@@ -169,6 +169,8 @@ cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStre
       if (e != cudaSuccess) return e;
       e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
       done.push_back(fn);
     }
   }

@@ -18,7 +18,10 @@
 
 namespace uniap {
 
+
+
 __global__ void k_fill(int32_t* p, int64_t n, int32_t v) {
+  TraceScope tr(TR_FILL);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
 }
@@ -36,25 +39,69 @@ cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st) {
 constexpr int K3T = 1024;
 typedef cub::BlockScan<int, K3T> K3Scan;
 // Sorted distinct theta candidates of config `cf` into v[0..n) (returns n):
-// valid P[a][b] < INF and every O[e]; bitonic sort + dedupe in shared memory.
+// valid P[a][b] < INF and every O[e].  The values are first de-duplicated in
+// an open-addressing hash set in v (identical layers make most of them
+// equal), compacted with a block scan, then sorted: by rank counting when
+// few (<= 64), else bitonic.  The config's P block and O row are copied to
+// sP / sO on the way (K4 reads them from shared memory).
+constexpr int32_t EMPTY = 0x7fffffff;
+__device__ __forceinline__ void hset_insert(int32_t* v, int32_t x) {
+  uint32_t h = ((uint32_t)x * 2654435761u) >> (32 - 12);  // SORTN = 4096 slots
+  for (;;) {
+    const int32_t old = atomicCAS(v + h, EMPTY, x);
+    if (old == EMPTY || old == x) return;
+    h = (h + 1) & (SORTN - 1);
+  }
+}
 __device__ int sort_thetas(const CfgDev& cf, const int32_t* __restrict__ arena, const int32_t* __restrict__ P, int L,
-                           int32_t* v, int32_t* cnt, typename K3Scan::TempStorage& scan_tmp) {
+                           int32_t* v, int32_t* sP, int32_t* sO, typename K3Scan::TempStorage& scan_tmp) {
+  static_assert(SORTN == 4 * K3T, "4 hash slots per thread");
   const int t = threadIdx.x;
-  if (t == 0) *cnt = 0;
-  for (int i = t; i < SORTN; i += K3T) v[i] = 0x7fffffff;
+  for (int i = t; i < SORTN; i += K3T) v[i] = EMPTY;
   __syncthreads();
   const int32_t* Pc = P + cf.offP;
   for (int idx = t; idx < L * L; idx += K3T) {
     const int a = idx / L, b = idx - a * L;
     const int32_t x = Pc[idx];
-    if (a <= b && x < INF) v[atomicAdd(cnt, 1)] = x;
+    sP[idx] = x;
+    if (a <= b && x < INF) hset_insert(v, x);
   }
   const int32_t* O = arena + cf.offO;
-  for (int e = t; e < L - 1; e += K3T) v[atomicAdd(cnt, 1)] = O[e];
+  for (int e = t; e < L - 1; e += K3T) {
+    const int32_t x = O[e];
+    sO[e] = x;
+    hset_insert(v, x);
+  }
   __syncthreads();
-  const int n = *cnt;
+  int flags[4], c = 0;
+  int32_t vals[4];
+  for (int r = 0; r < 4; ++r) {
+    vals[r] = v[4 * t + r];
+    flags[r] = vals[r] != EMPTY;
+    c += flags[r];
+  }
+  int pos, n;
+  K3Scan(scan_tmp).ExclusiveSum(c, pos, n);
+  __syncthreads();  // every read of v above is done before the compaction writes
+  for (int r = 0; r < 4; ++r)
+    if (flags[r]) v[pos++] = vals[r];
+  __syncthreads();
+  if (n <= 64) {  // rank counting (values are distinct)
+    int32_t x = EMPTY;
+    int rank = 0;
+    if (t < n) {
+      x = v[t];
+      for (int j = 0; j < n; ++j) rank += v[j] < x;
+    }
+    __syncthreads();
+    if (t < n) v[rank] = x;
+    __syncthreads();
+    return n;
+  }
   int N = 2;
   while (N < n) N <<= 1;
+  for (int i = n + t; i < N; i += K3T) v[i] = EMPTY;
+  __syncthreads();
   for (int k = 2; k <= N; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = t; i < N; i += K3T) {
@@ -70,81 +117,100 @@ __device__ int sort_thetas(const CfgDev& cf, const int32_t* __restrict__ arena, 
       }
       __syncthreads();
     }
-  int flags[4], c = 0;
-  int32_t vals[4];
-  for (int r = 0; r < 4; ++r) {
-    const int i = 4 * t + r;
-    vals[r] = i < SORTN ? v[i] : 0;
-    flags[r] = (i < n) && (i == 0 || v[i] != v[i - 1]);
-    c += flags[r];
-  }
-  int pos, total;
-  K3Scan(scan_tmp).ExclusiveSum(c, pos, total);
-  __syncthreads();  // every read of v above is done before the compaction writes
-  for (int r = 0; r < 4; ++r)
-    if (flags[r]) v[pos++] = vals[r];
-  __syncthreads();
-  return total;
+  return n;
 }
 
 // ---------------------------------------------------------------------------
 // Placement DPs by one warp over (stage i, end b); lanes own b (b = lane,
 // lane + 32).  Stage i = [a, b] with i-1 <= a <= b <= L-1-(deg-i); the last
-// stage ends at L-1.  sP: the config's P[L][L] in shared memory, sO: O[L-1],
-// g: 128 words of warp-private scratch.
-//  warp_F:   F_theta = min sum P + sum O over placements with every P, O <=
-//            theta (theta = INF: no limit)   -- (min, +) semiring
-//  warp_Bmm: the bottleneck min over placements of max(P u O), i.e. the
-//            smallest theta with a feasible placement -- (min, max) semiring
-// The a-loop is branch-free (predicated) and unrolled for ILP.
+// stage ends at L-1.  sP: the config's P[L][L] in shared memory (INF for
+// a > b and for intervals no placement uses), sO: O[L-1], g: 128 words of
+// warp-private scratch holding w[a] = (best placement of stages < i ending
+// at a-1) (+) O[a-1], double-buffered by stage parity.
+//  F:          F_theta = min sum P + sum O over placements with every P, O <=
+//              theta (theta = INF: no limit)   -- (min, +) semiring
+//  BOTTLENECK: the bottleneck min over placements of max(P u O), i.e. the
+//              smallest theta with a feasible placement -- (min, max) semiring
+// The a-loop reads one broadcast w and one conflict-free P word per lane
+// and accumulates with one DPX op (unsigned: INF + INF = 2^31 fits), two
+// accumulators per column for ILP.
 // ---------------------------------------------------------------------------
-template <bool BOTTLENECK>
+template <bool BOTTLENECK, bool MASK>
 __device__ int32_t warp_dp(const int32_t* sP, const int32_t* sO, int32_t* g, int L, int deg, int32_t theta) {
   const int lane = threadIdx.x & 31;
-  int32_t* cur = g;
-  int32_t* nxt = g + 64;
-  for (int b = lane; b < L; b += 32) {
-    const int32_t p = sP[b];
-    cur[b] = (b <= L - deg && p <= theta) ? p : INF;
-  }
-  __syncwarp();
   const int b0 = lane, b1 = lane + 32;
+  auto mask = [&](int32_t p) { return (MASK && p > theta) ? INF : p; };
+  // w of the next stage from this stage's value c at column b (stage ends at b)
+  auto put_w = [&](int32_t* w, int b, int32_t c) {
+    if (b + 1 < L) {
+      const int32_t o = sO[b];
+      int32_t x;
+      if (BOTTLENECK) x = max(c, o);
+      else x = (c < INF && !(MASK && o > theta)) ? c + o : INF;
+      w[b + 1] = x;
+    }
+  };
+  int32_t c0 = INF, c1 = INF;
+  {  // stage 1 = [0, b], b <= L - deg
+    if (b0 < L && b0 <= L - deg) c0 = mask(sP[b0]);
+    if (b1 < L && b1 <= L - deg) c1 = mask(sP[b1]);
+    if (deg > 1) {
+      if (b0 < L) put_w(g, b0, c0);
+      if (b1 < L) put_w(g, b1, c1);
+    }
+  }
   for (int i = 2; i <= deg; ++i) {
+    __syncwarp();
+    const int32_t* w = g + ((i & 1) ? 64 : 0);  // written by stage i-1
+    int32_t* wn = g + ((i & 1) ? 0 : 64);
     const int blo = (i == deg) ? L - 1 : i - 1, bhi = L - 1 - (deg - i);
-    const bool v0 = b0 >= blo && b0 <= bhi, v1 = b1 >= blo && b1 <= bhi && b1 < L;
-    int32_t best0 = INF, best1 = INF;
-#pragma unroll 4
-    for (int a = i - 1; a <= bhi; ++a) {  // stage i-1 ends at a-1
-      const int32_t gp = cur[a - 1];
-      const int32_t o = sO[a - 1];
-      const int32_t p0 = (v0 && b0 >= a) ? sP[a * L + b0] : INF;
-      const int32_t p1 = (v1 && b1 >= a) ? sP[a * L + b1] : INF;
+    uint32_t x0 = INF, y0 = INF, x1 = INF, y1 = INF;  // two accumulators per column
+    const bool two = L > 32;
+    int a = i - 1;
+    for (; a + 1 <= bhi; a += 2) {
+      const uint32_t wa = (uint32_t)w[a], wb = (uint32_t)w[a + 1];
+      const uint32_t pa0 = (uint32_t)mask(sP[a * L + b0]), pb0 = (uint32_t)mask(sP[(a + 1) * L + b0]);
       if (BOTTLENECK) {
-        const int32_t base = max(gp, o);
-        best0 = min(best0, max(base, p0));
-        best1 = min(best1, max(base, p1));
+        x0 = min(x0, max(wa, pa0));
+        y0 = min(y0, max(wb, pb0));
       } else {
-        const bool ok = gp < INF && o <= theta;  // then gp + o < 2^29 + 2^22
-        const int32_t base = gp + o;
-        best0 = min(best0, (ok && p0 <= theta) ? base + p0 : INF);
-        best1 = min(best1, (ok && p1 <= theta) ? base + p1 : INF);
+        x0 = __viaddmin_u32(wa, pa0, x0);
+        y0 = __viaddmin_u32(wb, pb0, y0);
+      }
+      if (two) {
+        const uint32_t pa1 = (uint32_t)mask(sP[a * L + b1]), pb1 = (uint32_t)mask(sP[(a + 1) * L + b1]);
+        if (BOTTLENECK) {
+          x1 = min(x1, max(wa, pa1));
+          y1 = min(y1, max(wb, pb1));
+        } else {
+          x1 = __viaddmin_u32(wa, pa1, x1);
+          y1 = __viaddmin_u32(wb, pb1, y1);
+        }
       }
     }
-    __syncwarp();
-    if (b0 < L) nxt[b0] = min(best0, INF);
-    if (b1 < L) nxt[b1] = min(best1, INF);
-    __syncwarp();
-    int32_t* tmp = cur;
-    cur = nxt;
-    nxt = tmp;
+    if (a <= bhi) {
+      const uint32_t wa = (uint32_t)w[a];
+      const uint32_t pa0 = (uint32_t)mask(sP[a * L + b0]);
+      x0 = BOTTLENECK ? min(x0, max(wa, pa0)) : __viaddmin_u32(wa, pa0, x0);
+      if (two) {
+        const uint32_t pa1 = (uint32_t)mask(sP[a * L + b1]);
+        x1 = BOTTLENECK ? min(x1, max(wa, pa1)) : __viaddmin_u32(wa, pa1, x1);
+      }
+    }
+    c0 = (b0 >= blo && b0 <= bhi) ? (int32_t)min(min(x0, y0), (uint32_t)INF) : INF;
+    c1 = (b1 < L && b1 >= blo && b1 <= bhi) ? (int32_t)min(min(x1, y1), (uint32_t)INF) : INF;
+    if (i < deg) {
+      if (b0 < L) put_w(wn, b0, c0);
+      if (b1 < L) put_w(wn, b1, c1);
+    }
   }
-  const int32_t F = cur[L - 1];
+  const int32_t F = __shfl_sync(0xffffffffu, (L - 1) < 32 ? c0 : c1, (L - 1) & 31);
   __syncwarp();
   return F;
 }
 __device__ __forceinline__ int32_t warp_F(const int32_t* sP, const int32_t* sO, int32_t* g, int L, int deg,
                                           int32_t theta) {
-  return warp_dp<false>(sP, sO, g, L, deg, theta);
+  return theta >= INF ? warp_dp<false, false>(sP, sO, g, L, deg, INF) : warp_dp<false, true>(sP, sO, g, L, deg, theta);
 }
 
 // ---------------------------------------------------------------------------
@@ -175,6 +241,7 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
                                                    int li0, int L, int32_t* __restrict__ thetas,
                                                    int32_t* __restrict__ ntheta, int64_t* __restrict__ vals,
                                                    int64_t* __restrict__ cfg_opt) {
+  TraceScope tr(TR_K4 | (uint32_t)li0 << 8);
   extern __shared__ __align__(16) unsigned char k4raw[];
   K4Smem& S = *reinterpret_cast<K4Smem*>(k4raw);
   int32_t* sP = S.sP;
@@ -187,7 +254,7 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
   const CfgDev cf = cfgs[cfg_list[li]];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // K3 fused: the sorted distinct theta candidates (also kept for K5a)
-  const int nt = sort_thetas(cf, arena, P, L, S.v, &S.cnt, S.scan_tmp);
+  const int nt = sort_thetas(cf, arena, P, L, S.v, sP, sO, S.scan_tmp);
   for (int i = threadIdx.x; i < nt; i += blockDim.x) thetas[(int64_t)li * TMAX + i] = S.v[i];
   if (threadIdx.x == 0) ntheta[li] = nt;
   int64_t* V = vals + (int64_t)li * (TMAX + 2);  // [0..nt) Val, [TMAX] F_inf, [TMAX+1] opt
@@ -197,16 +264,36 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
     if (threadIdx.x == 0) { V[TMAX] = INT64_MAX; cfg_opt[cfg_list[li]] = INT64_MAX; }
     return;
   }
-  for (int i = threadIdx.x; i < L * L; i += blockDim.x) sP[i] = P[cf.offP + i];
-  for (int i = threadIdx.x; i < L - 1; i += blockDim.x) sO[i] = arena[cf.offO + i];
-  __syncthreads();
   const int64_t cm1 = cf.c - 1;
+  if (nt <= K4W && cf.c > 1) {
+    // few candidates: every F_theta in one round, one warp each (the
+    // largest theta bounds every P and O, so F of it is F_inf)
+    if (w < nt) {
+      const int32_t F = warp_F(sP, sO, g[w], L, cf.deg, w == nt - 1 ? INF : S.v[w]);
+      if (lane == 0) probeF[w] = F;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int32_t Finf = probeF[nt - 1];
+      int64_t best = INT64_MAX;
+      for (int i = 0; i < nt; ++i)
+        if (Finf < INF && probeF[i] < INF) {
+          const int64_t val = (int64_t)probeF[i] + cm1 * S.v[i];
+          V[i] = val;
+          best = min(best, val);
+        }
+      V[TMAX] = Finf >= INF ? INT64_MAX : (int64_t)Finf;
+      cfg_opt[cfg_list[li]] = Finf >= INF ? INT64_MAX : best;
+      tr.extra = (uint32_t)nt | (uint32_t)nt << 12;
+    }
+    return;
+  }
   // 1. F_inf (warp 0) and the bottleneck theta_min (warp 1)
   if (w == 0) {
     const int32_t F = warp_F(sP, sO, g[0], L, cf.deg, INF);
     if (lane == 0) probeF[0] = F;
   } else if (w == 1) {
-    const int32_t Bm = warp_dp<true>(sP, sO, g[1], L, cf.deg, INF);
+    const int32_t Bm = warp_dp<true, false>(sP, sO, g[1], L, cf.deg, INF);
     if (lane == 0) probeF[1] = Bm;
   }
   __syncthreads();
@@ -242,12 +329,15 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
   }
   __syncthreads();
   const int64_t U = (int64_t)s_best;
+  if (threadIdx.x == 0) S.cnt = 0;
+  __syncthreads();
   for (int i = imin + 1 + w; i < nt; i += K4W) {
     const int32_t theta = th[i];
     const int64_t lb = (int64_t)Finf + cm1 * theta;
     if (lb > U) break;  // ascending thetas: every later one is worse too
     if ((unsigned long long)lb > *(volatile unsigned long long*)&s_best) continue;
     const int32_t F = warp_F(sP, sO, g[w], L, cf.deg, theta);
+    if (g_trace && lane == 0) atomicAdd(&S.cnt, 1);  // diagnostics: thetas evaluated
     if (F < INF && lane == 0) {
       const int64_t val = (int64_t)F + cm1 * theta;
       V[i] = val;
@@ -258,6 +348,7 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
   if (threadIdx.x == 0) {
     V[TMAX] = Finf;
     cfg_opt[cfg_list[li]] = (int64_t)s_best;
+    tr.extra = (uint32_t)S.cnt | (uint32_t)nt << 12 | (uint32_t)(nt - imin) << 24;
   }
 }
 
@@ -287,6 +378,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
                                                   const int32_t* __restrict__ ntheta, const int64_t* __restrict__ vals,
                                                   const int64_t* __restrict__ cfg_opt, int32_t* __restrict__ scratch,
                                                   Winner* __restrict__ win, RecordArgs ra) {
+  TraceScope tr(TR_K5A);
   __shared__ int32_t sP[MAXL * MAXL];
   __shared__ int32_t sO[MAXL];
   __shared__ int32_t stars[TMAX];
@@ -495,6 +587,7 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
                                                  const int32_t* __restrict__ G, const BwPlan* __restrict__ bw,
                                                  const Winner* __restrict__ win, int L, int cap,
                                                  uniap_record* __restrict__ rec) {
+  TraceScope tr(TR_K5C);
   __shared__ int32_t vec[32][MAXL];
   __shared__ int32_t mem[32];
   __shared__ int32_t okw[32];
@@ -576,6 +669,18 @@ cudaError_t launch_k5c_grid(int max_deg, const CfgDev* cfg, const int32_t* arena
   if (max_deg <= 0) return cudaSuccess;
   k5c_walk<<<max_deg, 1024, 0, st>>>(cfg, arena, G, bw, win, L, cap, rec);
   return cudaGetLastError();
+}
+
+cudaError_t combine_trace(unsigned long long* p) { return cudaMemcpyToSymbol(g_trace, &p, sizeof p); }
+
+// Every kernel of the step prefers the maximum shared-memory carveout, as K2
+// needs it: no L1/shared reconfiguration between the kernels of the step.
+cudaError_t combine_init() {
+  for (const void* f : {(const void*)k_fill, (const void*)k4_vals, (const void*)k5a_winner, (const void*)k5c_walk}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace uniap

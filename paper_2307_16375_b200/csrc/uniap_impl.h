@@ -85,6 +85,24 @@ __device__ __forceinline__ void trace_put(unsigned long long* tr, uint32_t tag, 
     r[3] = sm | (rank << 8) | ((unsigned long long)inst << 16) | ((unsigned long long)n << 40);
   }
 }
+// The non-K2 kernels record through a per-translation-unit pointer (set by
+// combine_trace / builder_trace); tag bit 31 marks them, bits 0-7 the kernel.
+enum TraceKind : uint32_t { TR_K1 = 1, TR_K1D = 2, TR_K1F = 3, TR_FILL = 4, TR_K4 = 5, TR_K5A = 6, TR_K5C = 7 };
+static __device__ unsigned long long* g_trace = nullptr;
+struct TraceScope {  // one record per CTA, written by thread 0 when the kernel returns
+  uint32_t tag, extra;  // extra: a kernel-defined count (default blockIdx.y)
+  unsigned long long t0 = 0;
+  __device__ explicit TraceScope(uint32_t k) : tag(0x80000000u | k), extra(blockIdx.y) {
+    if (g_trace && threadIdx.x == 0) t0 = gtimer();
+  }
+  __device__ ~TraceScope() {
+    if (g_trace && threadIdx.x == 0) trace_put(g_trace, tag, t0, 0, blockIdx.x, extra);
+  }
+};
+cudaError_t combine_trace(unsigned long long* p);
+cudaError_t builder_trace(unsigned long long* p);
+cudaError_t combine_init();  // kernel attributes (once per process)
+cudaError_t builder_init();
 
 // Kernel class: template shape of K2.
 struct K2Class {

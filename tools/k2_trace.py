@@ -33,12 +33,15 @@ lines = open(path).read().split("\n")
 recs = [tuple(int(x) for x in ln.split()) for ln in lines[1:] if ln.strip()]
 
 
+KIND = {1: "K1 costs", 2: "K1d quantum", 3: "K1f quantise", 4: "fill", 5: "K4", 6: "K5a", 7: "K5c", 8: "K4 sorted", 9: "K4 loaded", 10: "K4 dp done"}
+
+
 def shape(tag):
     return dict(NS=tag & 63, V=(tag >> 6) & 15, T=((tag >> 10) & 63) * 32, C=(tag >> 16) & 31, G=(tag >> 21) & 7,
                 DB=(tag >> 24) & 1, bw=(tag >> 25) & 1, grp=(tag >> 26) & 31)
 
 
-t00 = min(r[1] for r in recs)
+t00 = min(r[1] for r in recs if not r[0] >> 31)  # time 0 = first K2 CTA
 by = collections.defaultdict(list)
 for tag, t0, t1, packed in recs:
     by[tag].append(((t0 - t00) / 1e3, (t1 - t00) / 1e3, packed & 255, (packed >> 40) & 0xFFFFFF))
@@ -46,7 +49,11 @@ out = []
 for tag, v in sorted(by.items(), key=lambda kv: min(x[0] for x in kv[1])):
     s = shape(tag)
     d = sorted(x[1] - x[0] for x in v)
-    row = dict(cls=f"NS{s['NS']} V{s['V']} T{s['T']} C{s['C']} G{s['G']} DB{s['DB']}" + (" bw" if s["bw"] else ""),
+    if tag >> 31:
+        name = KIND.get(tag & 255, "?") + (f" li0={(tag >> 8) & 0xFFFF}" if tag & 255 in (5, 8, 9, 10) else "")
+    else:
+        name = f"NS{s['NS']} V{s['V']} T{s['T']} C{s['C']} G{s['G']} DB{s['DB']}" + (" bw" if s["bw"] else "")
+    row = dict(cls=name,
                ctas=len(v), start=round(min(x[0] for x in v), 1), end=round(max(x[1] for x in v), 1),
                dur_max=round(d[-1], 1), dur_med=round(d[len(d) // 2], 1), sm_us=round(sum(d), 1),
                us_per_layer=round(max((x[1] - x[0]) / max(x[3] - 1, 1) for x in v), 2))
@@ -57,10 +64,12 @@ end = max(r[2] for r in recs)
 nb = int((end - t00) / 1e4) + 1
 busy = [set() for _ in range(nb)]
 for tag, t0, t1, packed in recs:
+    if t0 < t00:
+        continue
     for b in range(int((t0 - t00) / 1e4), int((t1 - t00) / 1e4) + 1):
         busy[b].add(packed & 255)
 occ = [len(b) for b in busy]
-total = sum(x[1] - x[0] for v in by.values() for x in v)
+total = sum(x[1] - x[0] for tag, v in by.items() for x in v if not tag >> 31)
 print("busy SMs per 10us:", occ)
 print(f"span {(end - t00) / 1e3:.1f} us, CTA-us {total:.0f}, CTA-us / 148 = {total / 148:.1f} us")
 if len(sys.argv) > 2:
