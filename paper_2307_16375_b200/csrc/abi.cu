@@ -110,11 +110,11 @@ struct uniap_handle {
   std::vector<cudaStream_t> side;          // K2 classes run concurrently
   std::vector<cudaEvent_t> side_ev;
   cudaEvent_t fork_ev = nullptr;
-  std::vector<cudaEvent_t> k2_end;         // per forward group: end of its K2 (timing)
   RunPlan plan;                            // launch plan of the last (rank, world)
   DevBuf<int32_t> clsid;
   DevBuf<BwPlan> bwp;
   DevBuf<unsigned long long> trace;        // UNIAP_TRACE: K2 per-CTA timeline (diagnostics)
+  DevBuf<unsigned long long> tim;          // forward K2 phase clock (see K2Args::tim)
   cudaGraphExec_t graph_exec = nullptr;    // the captured pipeline of `plan`
   uint32_t graph_launches = 0, graph_k2 = 0;
   bool capturing = false, timed = false;
@@ -287,7 +287,6 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   for (auto e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto e : h->side_ev) cudaEventDestroy(e);
-  for (auto e : h->k2_end) cudaEventDestroy(e);
   for (auto x : h->side) cudaStreamDestroy(x);
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   if (h->own_stream) cudaStreamDestroy(h->st);
@@ -743,7 +742,6 @@ static uniap_status ensure_side_streams(uniap_handle* h, size_t n) {
 // Per-group follow-up on the group's stream (K4 of the group's configs).
 struct GroupTail {
   const std::vector<std::pair<int, int>>* ranges;  // [group] -> (li0, count) in the local config list
-  bool timing;                                     // record the K2 end event of every group
 };
 
 static uniap_status enqueue_k4_range(uniap_handle* h, int li0, int cnt, cudaStream_t st);
@@ -763,6 +761,7 @@ static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp,
     K2Args args{dcount_per_class ? dinst : dinst + grp[g].s,
                 dcount_per_class ? dcount_per_class + g : nullptr,
                 h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip, k2_flags()};
+    if (!dcount_per_class) args.tim = h->tim.p;  // forward launches: phase clock
     if (h->trace.p) {  // diagnostics: tag = class shape | forward/backward | group
       const K2Class& k = grp[g].cls;
       args.trace = h->trace.p;
@@ -774,8 +773,6 @@ static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp,
     h->launches++;
     h->k2_launches++;
     if (tail) {
-      if (tail->timing)
-        CK(h, cudaEventRecordWithFlags(h->k2_end[g], st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
       const auto& r = (*tail->ranges)[g];
       uniap_status s = enqueue_k4_range(h, r.first, r.second, st);
       if (s != UNIAP_OK) return s;
@@ -848,11 +845,7 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     R.k4rest = {rest0, (int)ordered.size() - rest0};
     R.local.swap(ordered);
   }
-  while (h->k2_end.size() < R.fgrp.size()) {
-    cudaEvent_t e;
-    CK(h, cudaEventCreate(&e));
-    h->k2_end.push_back(e);
-  }
+  CK(h, h->tim.ensure(2));
   // backward: one device-sized launch per kernel class of the local configs
   std::vector<int32_t> cls_of_cfg(h->ncfg, 0);
   R.bgrp.clear();
@@ -924,25 +917,27 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     if (s != UNIAP_OK) return s;
     CK(h, cudaEventRecord(h->fork_ev, h->st));
     CK(h, cudaStreamWaitEvent(h->side[0], h->fork_ev, 0));
+    CK(h, cudaMemsetAsync(h->tim.p, 0, 2 * sizeof(unsigned long long), h->side[0]));  // forward phase clock
     CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->side[0]));
     CK(h, cudaEventRecord(h->side_ev[0], h->side[0]));
     CK(h, launch_k1(h->cl, build_bufs(h), h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
     CK(h, cudaStreamWaitEvent(h->st, h->side_ev[0], 0));
     h->launches += 3;
   } else {
+    CK(h, cudaMemsetAsync(h->tim.p, 0, 2 * sizeof(unsigned long long), h->st));  // forward phase clock
     CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
   }
   h->launches++;
-  CK(h, cudaEventRecordWithFlags(h->ev[1], h->st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+
   {
     // K2 per class on side streams, each followed by the K4 of its configs
-    GroupTail tail{&R.k4range, true};
+    GroupTail tail{&R.k4range};
     uniap_status s = enqueue_k2(h, R.fgrp, h->inst.p, nullptr, h->P.p, R.fgrp.empty() ? nullptr : &tail);
     if (s != UNIAP_OK) return s;
     s = enqueue_k4_range(h, R.k4rest.first, R.k4rest.second, h->st);
     if (s != UNIAP_OK) return s;
   }
-  CK(h, cudaEventRecordWithFlags(h->ev[2], h->st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+
   RecordArgs ra{rec, h->cells, h->relax, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
                 h->binst.p, h->bwp.p};
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
@@ -1035,10 +1030,9 @@ extern "C" uniap_status uniap_fetch(uniap_handle* h, uniap_result* out) {
   if (h->timed) {
     CK(h, cudaStreamSynchronize(h->st));
     h->ms_dp = 0.f;
-    for (size_t g = 0; g < h->plan.fgrp.size() && g < h->k2_end.size(); ++g) {
-      float x = 0.f;
-      if (cudaEventElapsedTime(&x, h->ev[1], h->k2_end[g]) == cudaSuccess) h->ms_dp = std::max(h->ms_dp, x);
-    }
+    unsigned long long tm[2] = {0ull, 0ull};
+    if (h->tim.p) CK(h, cudaMemcpy(tm, h->tim.p, sizeof tm, cudaMemcpyDeviceToHost));
+    if (tm[0] && tm[1] >= ~tm[0]) h->ms_dp = (float)((double)(tm[1] - ~tm[0]) * 1e-6);
     cudaEventElapsedTime(&h->ms_total, h->ev[0], h->ev[3]);
     h->timed = false;
   }

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     ii = blockIdx.x / (int)cl_size();
   }
   if (args.n_inst && ii >= *args.n_inst) return;  // device-sized launch: spare CTA (whole cluster)
-  const unsigned long long t_start = args.trace ? gtimer() : 0ull;
+  const unsigned long long t_start = (args.trace || args.tim) ? gtimer() : 0ull;
   const Inst in = args.inst[ii];
   const CfgDev cf = args.cfg[in.cfg];
   const int32_t* __restrict__ gA = args.arena + cf.offA;
@@ -532,6 +532,10 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   }
   if constexpr (CL) cl_sync();  // keep this CTA's E alive for remote readers
   if (args.trace && t == 0) trace_put(args.trace, args.tag, t_start, rank, ii, in.n);
+  if (args.tim && t == 0) {  // the forward phase's device time (uniap_fetch: ms_gpu_dp)
+    atomicMax(args.tim, ~t_start);
+    atomicMax(args.tim + 1, gtimer());
+  }
 }
 
 template <int NS>

@@ -61,6 +61,9 @@ struct K2Args {
   // diagnostics (UNIAP_TRACE): per-CTA timeline records, or nullptr
   unsigned long long* trace = nullptr;
   uint32_t tag = 0;
+  // forward-phase clock (%globaltimer, ns): tim[0] = max of ~start, tim[1] =
+  // max of end over the launch's CTAs (both reset to 0 per run), or nullptr
+  unsigned long long* tim = nullptr;
 };
 
 // Timeline record of one CTA (UNIAP_TRACE): trace[0] = record count, trace[1]
