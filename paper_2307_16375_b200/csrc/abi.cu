@@ -118,6 +118,7 @@ struct uniap_handle {
   cudaGraphExec_t graph_exec = nullptr;    // the captured pipeline of `plan`
   uint32_t graph_launches = 0, graph_k2 = 0;
   bool capturing = false, timed = false;
+  bool no_compact = false;  // uniap_build_tables: keep every strategy in the tables
   std::vector<int64_t> sig;                // what the captured graph depends on
 };
 
@@ -298,9 +299,14 @@ static void plan_instances(int L, int i, int deg, int S, int skip, bool all_inte
 // ---------------------------------------------------------------------------
 // Layout of the configs in the device arena.
 // ---------------------------------------------------------------------------
-static uniap_status layout_configs(uniap_handle* h, const std::vector<int>& S, const std::vector<int>& deg,
+// keep[i]: the strategies of config i that can be feasible (ascending caller
+// indices); the tables, kernels and plan use only these (S = keep size).
+static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vector<int>>& keep,
+                                   const std::vector<int>& Sfull, const std::vector<int>& deg,
                                    const std::vector<int>& c, const std::vector<int>& g, const std::vector<int>& skipc) {
   const int L = h->L;
+  std::vector<int> S(h->ncfg);
+  for (int i = 0; i < h->ncfg; ++i) S[i] = (int)keep[i].size();
   h->cfg.assign(h->ncfg, CfgDev{});
   h->cls.assign(h->ncfg, K2Class{});
   h->bcls.assign(h->ncfg, K2Class{});
@@ -318,6 +324,12 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<int>& S, c
     CfgDev& d = h->cfg[i];
     const int NSP = round4(k.NS);
     d.deg = deg[i]; d.c = c[i]; d.S = S[i]; d.NSP = NSP; d.g = g[i]; d.skip = skipc[i];
+    d.Sfull = Sfull[i];
+    for (int j = 0; j < UNIAP_MAX_STRAT; ++j) d.orig[j] = d.comp[j] = -1;
+    for (int k = 0; k < S[i]; ++k) {
+      d.orig[k] = (int8_t)keep[i][k];
+      d.comp[keep[i][k]] = (int8_t)k;
+    }
     d.offA = off; off += (int64_t)L * NSP;
     d.offM = off; off += (int64_t)L * NSP;
     d.offRt = off; off += (int64_t)(L - 1) * NSP * NSP;
@@ -347,6 +359,7 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
   if (t->n_cfg < 1 || t->n_cfg > UNIAP_MAX_CFG) FAIL(h, UNIAP_ERR_ARG, "n_cfg=%d", t->n_cfg);
   h->L = L; h->cap = t->cap; h->Q = t->cap + 1; h->skip = t->skip_src; h->ncfg = t->n_cfg; h->level2 = false;
   std::vector<int> S(h->ncfg), deg(h->ncfg), c(h->ncfg), g(h->ncfg, 0), skc(h->ncfg);
+  std::vector<std::vector<int>> keep(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i) {
     const uniap_config& x = t->cfg[i];
     if (x.deg < 1 || x.c < 1 || x.n_strat < 1 || x.n_strat > UNIAP_MAX_STRAT)
@@ -385,31 +398,40 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
     if (sum > UNIAP_MAX_SUM || osum > UNIAP_MAX_SUM) FAIL(h, UNIAP_ERR_RANGE, "config %d: sum bound exceeds 2^28", i);
     S[i] = s; deg[i] = x.deg; c[i] = x.c;
     skc[i] = (x.Rskip && t->skip_src >= 0) ? t->skip_src : -1;
+    // strategies with M > cap at every layer can never be part of a solution
+    for (int k = 0; k < s; ++k) {
+      bool ok = false;
+      for (int u = 0; u < L && !ok; ++u) ok = x.M[u * s + k] <= t->cap;
+      if (ok || h->no_compact) keep[i].push_back(k);
+    }
+    if (keep[i].empty()) keep[i].push_back(0);  // all forbidden: the config is infeasible
   }
-  uniap_status st = layout_configs(h, S, deg, c, g, skc);
+  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc);
   if (st != UNIAP_OK) return st;
   // pack the host tables into the device layout (pads: A 0, M cap+1, R 0)
   std::vector<int32_t> a(h->arena_words, 0);
   for (int i = 0; i < h->ncfg; ++i) {
     const uniap_config& x = t->cfg[i];
     const CfgDev& d = h->cfg[i];
-    const int s = x.n_strat, N = d.NSP;
+    const int s = x.n_strat, N = d.NSP, sc = d.S;
+    const std::vector<int>& kp = keep[i];
     for (int u = 0; u < L; ++u)
       for (int k = 0; k < N; ++k) {
-        a[d.offA + u * N + k] = k < s ? x.A[u * s + k] : 0;
-        a[d.offM + u * N + k] = k < s ? std::min(x.M[u * s + k], h->cap + 1) : h->cap + 1;
+        a[d.offA + u * N + k] = k < sc ? x.A[u * s + kp[k]] : 0;
+        a[d.offM + u * N + k] = k < sc ? std::min(x.M[u * s + kp[k]], h->cap + 1) : h->cap + 1;
       }
     for (int e = 0; e + 1 < L; ++e)
-      for (int k = 0; k < s; ++k)
-        for (int l = 0; l < s; ++l) {
-          const int32_t r = x.R[((int64_t)e * s + k) * s + l];
+      for (int k = 0; k < sc; ++k)
+        for (int l = 0; l < sc; ++l) {
+          const int32_t r = x.R[((int64_t)e * s + kp[k]) * s + kp[l]];
           a[d.offRf + ((int64_t)e * N + k) * N + l] = r;
           a[d.offRt + ((int64_t)e * N + l) * N + k] = r;
         }
     if (d.skip >= 0)
       for (int v = d.skip + 2; v < L; ++v)
-        for (int k = 0; k < s; ++k)
-          for (int l = 0; l < s; ++l) a[d.offRs + ((int64_t)v * N + k) * N + l] = x.Rskip[((int64_t)v * s + k) * s + l];
+        for (int k = 0; k < sc; ++k)
+          for (int l = 0; l < sc; ++l)
+            a[d.offRs + ((int64_t)v * N + k) * N + l] = x.Rskip[((int64_t)v * s + kp[k]) * s + kp[l]];
     if (x.O)
       for (int e = 0; e + 1 < L; ++e) a[d.offO + e] = x.O[e];
   }
@@ -502,13 +524,19 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   h->L = L; h->Q = o->Q; h->cap = o->Q - 1; h->skip = skip; h->ncfg = (int)cand.size() / 2; h->level2 = true;
   std::vector<int> S(h->ncfg), deg(h->ncfg), c(h->ncfg), g(h->ncfg), skc(h->ncfg, skip);
   h->cat.assign(h->ncfg, CatDev{});
+  std::vector<std::vector<int>> keep(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i) {
     deg[i] = cand[2 * i]; c[i] = cand[2 * i + 1]; g[i] = n / deg[i];
     S[i] = uniap_catalogue(g[i], nullptr, 0);
     if (S[i] > UNIAP_MAX_STRAT) FAIL(h, UNIAP_ERR_RANGE, "|S(%d)| = %d > 32", g[i], S[i]);
     uniap_catalogue(g[i], h->cat[i].tfd, UNIAP_MAX_STRAT);
+    // b mod (f d) != 0 forbids a strategy at every layer (reading A-7)
+    const int b = o->B / c[i];
+    for (int k = 0; k < S[i]; ++k)
+      if (h->no_compact || b % (h->cat[i].tfd[3 * k + 1] * h->cat[i].tfd[3 * k + 2]) == 0) keep[i].push_back(k);
+    if (keep[i].empty()) keep[i].push_back(0);
   }
-  uniap_status st = layout_configs(h, S, deg, c, g, skc);
+  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc);
   if (st != UNIAP_OK) return st;
   h->cl = ClusterDev{cl->n_dev, cl->node_size, cl->ccoc_permille, o->B, o->precision, o->Q, NT, 0,
                      cl->mem_bytes, cl->mem_reserve_bytes, cl->bw_intra_Bps, cl->bw_inter_Bps, cl->p2p_Bps,
@@ -615,7 +643,7 @@ static void forward_instances(const uniap_handle* h, int i, bool all_intervals, 
   else plan_fast(h->L, i, d.deg, d.S, d.skip, out);
 }
 
-// LPT over configs by chain-DP work (sum over instances of n |S|^2 Q); ties
+// LPT over configs by executed chain-DP work (sum over the sweeps of n |S|^2 Q); ties
 // keep the candidate order, the least-loaded (then lowest) rank takes the next.
 static void lpt_shapes(int L, int Q, const std::vector<int>& deg, const std::vector<int>& S,
                        const std::vector<int>& skip, int world, std::vector<int>& owner) {
@@ -624,7 +652,7 @@ static void lpt_shapes(int L, int Q, const std::vector<int>& deg, const std::vec
   std::vector<double> w(n);
   for (int i = 0; i < n; ++i) {
     std::vector<Inst> v;
-    plan_instances(L, i, deg[i], S[i], skip[i], false, v);
+    plan_fast(L, i, deg[i], S[i], skip[i], v);  // the executed sweeps
     double x = 1.0;  // + the combine
     for (auto& e : v) x += (double)e.n * S[i] * S[i] * Q;
     order[i] = i;
@@ -653,8 +681,17 @@ extern "C" uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world,
   std::vector<int> deg(t->n_cfg), S(t->n_cfg), sk(t->n_cfg), owner;
   for (int i = 0; i < t->n_cfg; ++i) {
     deg[i] = t->cfg[i].deg;
-    S[i] = t->cfg[i].n_strat;
-    sk[i] = (t->cfg[i].Rskip && t->skip_src >= 0) ? t->skip_src : -1;
+    // the strategy count the prepared tables hold (strategies feasible at some layer)
+    const uniap_config& x = t->cfg[i];
+    if (!x.M || x.n_strat < 1) return UNIAP_ERR_ARG;
+    S[i] = 0;
+    for (int k = 0; k < x.n_strat; ++k) {
+      bool ok = false;
+      for (int u = 0; u < t->L && !ok; ++u) ok = x.M[u * x.n_strat + k] <= t->cap;
+      S[i] += ok;
+    }
+    S[i] = std::max(S[i], 1);
+    sk[i] = (x.Rskip && t->skip_src >= 0) ? t->skip_src : -1;
   }
   lpt_shapes(t->L, t->cap + 1, deg, S, sk, world, owner);
   for (int i = 0; i < t->n_cfg; ++i) owner_out[i] = owner[i];
@@ -820,8 +857,8 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   h->cells_canon = 0;
   for (int i : R.local) {
     std::vector<Inst> cv;
-    plan_instances(h->L, i, h->cfg[i].deg, h->cfg[i].S, h->cfg[i].skip, false, cv);
-    for (auto& x : cv) h->cells_canon += (uint64_t)x.n * h->cfg[i].S * h->Q;
+    plan_instances(h->L, i, h->cfg[i].deg, h->cfg[i].Sfull, h->cfg[i].skip, false, cv);
+    for (auto& x : cv) h->cells_canon += (uint64_t)x.n * h->cfg[i].Sfull * h->Q;
   }
   group_instances(h, fw, R.fgrp);
   // local configs ordered by forward group, so each group's K4 takes a range
@@ -1120,7 +1157,9 @@ extern "C" uniap_status uniap_interval_table(uniap_handle* h, const uniap_tables
 extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
                                            const uniap_options* o, int32_t* buf, int64_t buf_len, int64_t* words,
                                            int32_t* n_cfg, int32_t* skip_src, int64_t* quantum_ns) {
+  h->no_compact = true;  // the documented layout holds every catalogue strategy
   uniap_status s = uniap_prepare(h, m, cl, o);
+  h->no_compact = false;
   if (s != UNIAP_OK) return s;
   const int L = h->L;
   int64_t need = 0;

@@ -125,7 +125,7 @@ __device__ void k1a_layers(const ClusterDev& cl, const BuildBufs& bb, const CfgD
   int64_t* M = bb.ns + cf.offM;
   const int64_t b = cl.B / cf.c;
   if (k >= cf.S) { A[idx] = 0; M[idx] = -1; return; }
-  const int32_t* s = bb.cat[blockIdx.y].tfd + 3 * k;
+  const int32_t* s = bb.cat[blockIdx.y].tfd + 3 * cf.orig[k];  // table strategy k = catalogue orig[k]
   const int64_t t = s[0], f = s[1], d = s[2], r = f * d;
   if (b % r) { A[idx] = 0; M[idx] = -1; return; }  // reading A-7
   const int64_t bl = b / r;
@@ -152,23 +152,33 @@ __device__ void k1a_layers(const ClusterDev& cl, const BuildBufs& bb, const CfgD
 // (nb blocks per config, grid-stride over the config's entries).
 __device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* __restrict__ cfgs, int L, int bx,
                             int nb) {
-  const CfgDev cf = cfgs[blockIdx.y];
-  const int NSP = cf.NSP, n2 = NSP * NSP;
-  const int nR = (L - 1) * n2, nS = L * n2;
+  const CfgDev& cf = cfgs[blockIdx.y];
+  // every catalogue pair (j, i): the quantum's maxima include the pairs of
+  // dropped strategies (reading A-9 over the whole catalogue); the table
+  // stores the pairs of kept ones at their compacted place (pads stay 0)
+  const int SF = cf.Sfull, NSP = cf.NSP, f2 = SF * SF;
+  const int nR = (L - 1) * f2, nS = L * f2;
+  {  // pad rows / columns of the compacted layout: R = 0
+    const int n2 = NSP * NSP, pR = (L - 1) * n2, pS = L * n2;
+    for (int idx = bx * blockDim.x + threadIdx.x; idx < pR + pS; idx += nb * blockDim.x) {
+      const int jx = idx < pR ? idx : idx - pR;
+      const int r = jx % n2;
+      if (r / NSP >= cf.S || r % NSP >= cf.S) (bb.ns + (idx < pR ? cf.offRf : cf.offRs))[jx] = 0;
+    }
+  }
   for (int idx = bx * blockDim.x + threadIdx.x; idx < nR + nS; idx += nb * blockDim.x) {
     const bool isR = idx < nR;
-    const int j = isR ? idx : idx - nR;
-    const int e = j / n2, k = (j - e * n2) / NSP, l = j - e * n2 - k * NSP;
+    const int jx = isR ? idx : idx - nR;
+    const int e = jx / f2, k = (jx - e * f2) / SF, l = jx - e * f2 - k * SF;
     const int64_t b = cl.B / cf.c;
     int64_t v = 0;
-    if (k < cf.S && l < cf.S) {
-      const int64_t tb = isR ? bb.chain[e] : bb.skipb[e];
-      if (tb >= 0) {
-        const Coll co{cl};
-        v = checked(co.reshard(bb.cat[blockIdx.y].tfd + 3 * k, bb.cat[blockIdx.y].tfd + 3 * l, (u128)b * tb), bb.qglob + 1);
-      }
+    const int64_t tb = isR ? bb.chain[e] : bb.skipb[e];
+    if (tb >= 0) {
+      const Coll co{cl};
+      v = checked(co.reshard(bb.cat[blockIdx.y].tfd + 3 * k, bb.cat[blockIdx.y].tfd + 3 * l, (u128)b * tb), bb.qglob + 1);
     }
-    (bb.ns + (isR ? cf.offRf : cf.offRs))[j] = v;
+    const int kc = cf.comp[k], lc = cf.comp[l];
+    if (kc >= 0 && lc >= 0) (bb.ns + (isR ? cf.offRf : cf.offRs))[((int64_t)e * NSP + kc) * NSP + lc] = v;
     // per-layer maxima for the quantum: R of edge e goes into layer e+1
     if (v > 0 && (isR || (cf.skip >= 0 && e >= cf.skip + 2)))
       amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + (isR ? e + 1 : e)) * 4 + (isR ? 1 : 2), v);

@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
       rec->status = UNIAP_ERR_INTERNAL;
     } else {
       for (int u = a; u <= b; ++u) {
-        rec->strategy_of[u] = vec[bw][u];
+        rec->strategy_of[u] = cfgs[W.cfg].orig[vec[bw][u]];  // caller's strategy index
         rec->stage_of[u] = stage;
       }
       rec->stage_mem[stage] = mem[bw];

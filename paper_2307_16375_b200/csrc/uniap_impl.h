@@ -31,6 +31,12 @@ struct CfgDev {
   int32_t deg, c, S, NSP, g, skip;        // skip: skip source of this config's tables (-1 none)
   int64_t offA, offM, offRt, offRf, offRs, offO;  // word offsets into the arena
   int64_t offP;                            // word offset into the P arena
+  // Strategy compaction: the tables hold only the S strategies that can be
+  // feasible; orig[k] is the catalogue / caller index of
+  // table strategy k, comp[j] the table index of catalogue strategy j (-1:
+  // dropped), Sfull the catalogue size (the canonical work counts use it).
+  int32_t Sfull, pad_;
+  int8_t orig[UNIAP_MAX_STRAT], comp[UNIAP_MAX_STRAT];
 };
 
 // One chain sweep of K2.
