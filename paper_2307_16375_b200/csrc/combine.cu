@@ -388,25 +388,32 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
   __shared__ int64_t s_opt[1];
   __shared__ int32_t s_win;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  // 2. winner by (objective, deg, c)
-  if (t == 0) {
-    int wi = -1;
+  // 2. winner by (objective, deg, c): warp 0, lanes over the local configs,
+  //    then a shuffle argmin on the key tuple
+  if (w == 0) {
+    int wi = -1, bd = 0, bc = 0;
     int64_t best = INT64_MAX;
-    for (int li = 0; li < n_local; ++li) {
+    for (int li = lane; li < n_local; li += 32) {
       const int ci = cfg_list[li];
       const int64_t v = cfg_opt[ci];
-      if (v == INT64_MAX) continue;
-      const CfgDev a = cfgs[ci];
-      bool take = wi < 0 || v < best;
-      if (!take && v == best) {
-        const CfgDev b = cfgs[cfg_list[wi]];
-        take = a.deg < b.deg || (a.deg == b.deg && a.c < b.c);
+      const int dg = cfgs[ci].deg, cc = cfgs[ci].c;
+      if (v != INT64_MAX && (wi < 0 || v < best || (v == best && (dg < bd || (dg == bd && cc < bc))))) {
+        wi = li; best = v; bd = dg; bc = cc;
       }
-      if (take) { wi = li; best = v; }
     }
-    s_win = wi;
-    s_opt[0] = best;
-    nstar = 0;
+    for (int off = 16; off > 0; off >>= 1) {
+      const int owi = __shfl_down_sync(0xffffffffu, wi, off), obd = __shfl_down_sync(0xffffffffu, bd, off),
+                obc = __shfl_down_sync(0xffffffffu, bc, off);
+      const int64_t ob = __shfl_down_sync(0xffffffffu, best, off);
+      if (owi >= 0 && (wi < 0 || ob < best || (ob == best && (obd < bd || (obd == bd && obc < bc))))) {
+        wi = owi; best = ob; bd = obd; bc = obc;
+      }
+    }
+    if (lane == 0) {
+      s_win = wi;
+      s_opt[0] = best;
+      nstar = 0;
+    }
   }
   __syncthreads();
   const int wl = s_win;
@@ -617,8 +624,9 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
     for (int u = a; u <= b && ok; ++u) {
       const int k = lane;
       bool c = false;
-      int32_t edge = 0, ap = 0;
+      int32_t edge = 0, ap = 0, mk = 0;
       if (k < S) {
+        mk = M[u * NSP + k];  // per lane, with the other loads: one global round trip per layer
         const int32_t gv = g[((int64_t)(u - a) * NSP + k) * Q + q];
         edge = (u > a) ? Rf[((int64_t)(u - 1) * NSP + kprev) * NSP + k] : 0;
         ap = A[u * NSP + k] + ((ks >= 0 && u >= skip + 2) ? Rs[((int64_t)u * NSP + ks) * NSP + k] : 0);
@@ -629,7 +637,7 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
       const int kk = __ffs(m) - 1;
       const int32_t e2 = __shfl_sync(0xffffffffu, edge, kk);
       const int32_t a2 = __shfl_sync(0xffffffffu, ap, kk);
-      const int32_t m2 = M[u * NSP + kk];
+      const int32_t m2 = __shfl_sync(0xffffffffu, mk, kk);
       rest -= (int64_t)e2 + a2;
       q -= m2;
       msum += m2;
