@@ -91,7 +91,7 @@ struct uniap_handle {
   int n_edges = 0;
   // device buffers
   DevBuf<int32_t> arena, P, thetas, ntheta, cfglist, scratch, G;
-  DevBuf<int64_t> ns, vals, cfgopt, qcfg, qglob, gofs, qmax;
+  DevBuf<int64_t> ns, vals, cfgopt, qcfg, qglob, gofs, qmax, gstore;
   DevBuf<int64_t> fwd, act, ps, ctx, tpc, chain, skipb, edges;
   DevBuf<CfgDev> dcfg;
   DevBuf<CatDev> dcat;
@@ -273,7 +273,7 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->st);
   for (auto* b : {&h->arena, &h->P, &h->thetas, &h->ntheta, &h->cfglist, &h->scratch, &h->G}) b->release();
-  for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->qglob, &h->gofs, &h->qmax, &h->fwd, &h->act, &h->ps, &h->ctx,
+  for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->qglob, &h->gofs, &h->qmax, &h->gstore, &h->fwd, &h->act, &h->ps, &h->ctx,
                   &h->tpc, &h->chain, &h->skipb, &h->edges})
     b->release();
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
@@ -624,7 +624,15 @@ static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>&
       out.push_back(Inst{i, a, n, -1, +1, 1, 0, a, bmax});
     }
   };
-  if (deg == 1) { fwd(0, L - 1); return; }
+  if (deg == 1) {
+    // the whole chain as ONE backward sweep from L-1 that also keeps its G
+    // tables: the traceback of a deg = 1 winner then needs no sweep of its
+    // own (gofs assigned by make_plan).  With the skip source inside, the
+    // |S| conditioned copies would keep |S| tables: plain forward sweep.
+    if (skip >= 0 && skip + 2 <= L - 1) fwd(0, L - 1);
+    else out.push_back(Inst{i, L - 1, L, -1, -1, 5, -1, 0, 0});
+    return;
+  }
   fwd(0, L - deg);                                               // stage 1: prefixes
   for (int a = 1; a <= L - 2 && deg >= 3; ++a)                   // middle stages
     fwd(a, L - 1 - deg + std::min(a + 1, deg - 1));
@@ -905,6 +913,24 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     cls_of_cfg[i] = g;
   }
   if ((int)R.bgrp.size() > MAXCLS) FAIL(h, UNIAP_ERR_ARG, "too many kernel classes");
+  // G blocks kept from the forward phase (deg = 1 whole-chain sweeps), after
+  // the traceback's own blocks
+  std::vector<int64_t> gstore(h->ncfg, -1);
+  {
+    int64_t off = gmax;
+    for (auto& x : fw)
+      if (x.emit & 4) {
+        const CfgDev& d = h->cfg[x.cfg];
+        if (gstore[x.cfg] < 0) {
+          gstore[x.cfg] = off;
+          off += (int64_t)(d.skip >= 0 && d.skip + 2 <= h->L - 1 ? d.S : 1) * h->L * d.NSP * h->Q;
+        }
+        x.gofs = gstore[x.cfg] + (int64_t)(x.ks < 0 ? 0 : x.ks) * h->L * d.NSP * h->Q;
+      }
+    gmax = off;
+  }
+  CK(h, h->gstore.ensure(h->ncfg));
+  CK(h, h2d(h, h->gstore.p, gstore.data(), h->ncfg * 8));
   int max_bw = 1;
   for (auto& g : R.bgrp) max_bw = std::max(max_bw, g.max_inst);
   // device buffers + uploads (outside any graph)
@@ -976,7 +1002,7 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   }
 
   RecordArgs ra{rec, h->cells, h->relax, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
-                h->binst.p, h->bwp.p};
+                h->binst.p, h->bwp.p, h->gstore.p};
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
                    h->cfgopt.p, h->scratch.p, h->win.p, ra, h->st));
   h->launches += 1;

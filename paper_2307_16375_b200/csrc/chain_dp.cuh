@@ -206,8 +206,9 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   };
 
   int32_t d[NS][V];
+  const bool eP = (in.emit & 3) != 0, eG = in.emit == 0 || (in.emit & 4) != 0;  // Inst::emit
   auto emit = [&](int u) {
-    if (in.emit != 0) {
+    if (eP) {
       const int rc = cap / B;
       if (rank == rc) {
         const int lc = cap - rc * B, jc = lc / T, tc = lc - jc * T;
@@ -222,7 +223,8 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
                          // outstanding at the per-layer cluster barrier)
         }
       }
-    } else {
+    }
+    if (eG) {
       const int lo = in.a - in.n + 1;
       int32_t* g = args.G + in.gofs + (int64_t)(u - lo) * NSP * Q;
 #pragma unroll
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     };
     // stage optimum / backward table of layer uu for the slots of segment g
     auto emit_seg = [&](int uu, int g) {
-      if (in.emit != 0) {
+      if (eP) {
         const int jc = cap / T, tc = cap - jc * T;  // C = 1: cap < B
         if (jc / VS == g && t == tc) {
           int32_t v = INF;
@@ -342,7 +344,8 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
               for (int k = 0; k < NS; ++k) v = min(v, d[k][g * VS + jj]);
           sProw[uu] = v;
         }
-      } else {
+      }
+      if (eG) {
         const int lo = in.a - in.n + 1;
         int32_t* gp = args.G + in.gofs + (int64_t)(uu - lo) * NSP * Q;
 #pragma unroll
@@ -522,11 +525,11 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     emit(u);
   }
   // the forward sweep's stage optima P[a][a..a+n-1], from its owner thread
-  if (in.emit != 0 && rank == cap / B && t == (cap - (cap / B) * B) % T) {
+  if (eP && rank == cap / B && t == (cap - (cap / B) * B) % T) {
     int32_t* Pc = args.P + cf.offP;
     for (int uu = in.elo; uu <= in.ehi; ++uu) {
       int32_t* dst = in.dir > 0 ? Pc + (int64_t)in.a * L + uu : Pc + (int64_t)uu * L + in.a;
-      if (in.emit == 2) atomicMin(dst, sProw[uu]);
+      if ((in.emit & 3) == 2) atomicMin(dst, sProw[uu]);
       else *dst = sProw[uu];
     }
   }

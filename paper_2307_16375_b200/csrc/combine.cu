@@ -565,7 +565,12 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     for (int i = 0; i < deg && have && r->status == 0; ++i) {
       const int b = best_end[i], len = b - a + 1;
       const bool cond = cf.skip >= 0 && a <= cf.skip && cf.skip + 2 <= b;
+      const int64_t kept = ra.gstore[ci];  // deg = 1: the forward phase's sweep kept its tables
       for (int ks = cond ? 0 : -1; ks < (cond ? cf.S : 0); ++ks) {
+        if (kept >= 0) {
+          ra.bw->gofs[i * 33 + ks + 1] = kept + (int64_t)(ks < 0 ? 0 : ks) * L * cf.NSP * (ra.cap + 1);
+          continue;
+        }
         ra.bw->gofs[i * 33 + ks + 1] = goff;
         ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1};
         goff += (int64_t)len * cf.NSP * (ra.cap + 1);

@@ -46,8 +46,10 @@ struct Inst {
   int32_t n;     // number of layers swept (>= 1)
   int32_t ks;    // skip-source conditioning (-1 = none)
   int32_t dir;   // +1 forward (emit P[a][u]), -1 backward (store G[u])
-  int32_t emit;  // 1: P plain store, 2: P atomicMin (several copies), 0: store G (traceback)
-  int64_t gofs;  // emit 0: word offset of this sweep's G block (layers a-n+1..a)
+  int32_t emit;  // 1: P plain store, 2: P atomicMin (several copies), 0: store G (traceback);
+                 // 5 / 6: as 1 / 2 and store G too (the whole-chain sweep of a deg = 1 config,
+                 // kept for its traceback)
+  int64_t gofs;  // G stores: word offset of this sweep's G block (layers a-n+1..a)
   // emit 1/2: P entries of the layers u in [elo, ehi] only -- P[a][u] for a
   // forward sweep (intervals starting at a), P[u][a] for a backward sweep
   // (intervals ending at a: the suffix sweep of the last stage)
@@ -156,6 +158,10 @@ struct RecordArgs {          // what K5a writes into the record besides the winn
   const int32_t* cls_of_cfg; // kernel class id per config
   Inst* bw_inst;             // out: backward instances of the winner
   BwPlan* bw;                // out
+  // per config: word offset in G of the whole-chain backward sweep's tables
+  // kept from the forward phase (deg = 1; per skip conditioning ks consecutive
+  // blocks of L * NSP * Q words), or -1 (the traceback runs its own sweep)
+  const int64_t* gstore;
 };
 
 // combine.cu
