@@ -90,14 +90,8 @@ struct Coll {
     return cdiv128((u128)(G - 1) * V * 1000000000ull, (u128)G * bw(G, stride)) + (u128)(G - 1) * c.lat;
   }
   __device__ u128 p2p(u128 V) const { return cdiv128(V * 1000000000ull, (u128)c.p2p) + (u128)c.lat; }
-  __device__ u128 reshard(const int32_t* s1, const int32_t* s2, u128 V) const {
-    const int64_t t1 = s1[0], r1 = (int64_t)s1[1] * s1[2], t2 = s2[0], r2 = (int64_t)s2[1] * s2[2];
-    if (t1 == t2 && r1 == r2) return 0;  // identical layouts
-    int64_t G = 1;
-    if (t1 != t2) G = max(G, t1 > t2 ? (t1 + t2 - 1) / t2 : (t2 + t1 - 1) / t1);
-    if (r1 != r2) G = max(G, r1 > r2 ? (r1 + r2 - 1) / r2 : (r2 + r1 - 1) / r1);
-    return 2 * allreduce(V, G, 1);  // forward + backward
-  }
+  // resharding over a group of G devices: forward + backward all-reduce
+  __device__ u128 reshard_G(u128 V, int64_t G) const { return G <= 1 ? 0 : 2 * allreduce(V, G, 1); }
 };
 
 __device__ __forceinline__ int lg2(int x) { return 31 - __clz(x); }
@@ -148,41 +142,56 @@ __device__ void k1a_layers(const ClusterDev& cl, const BuildBufs& bb, const CfgD
   amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + u) * 4, A[idx]);
 }
 
-// K1b: R (edge e = u->u+1), Rskip (edge skip->v) in ns, original [k][l] layout
-// (nb blocks per config, grid-stride over the config's entries).
-__device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* __restrict__ cfgs, int L, int bx,
-                            int nb) {
+// K1b: R (edge e = u->u+1), Rskip (edge skip->v) in ns, compacted [k][l]
+// layout; one block per (edge slot, config).  The resharding cost of a pair
+// depends only on its group size G (reading A-15) for the edge's volume, so
+// the block first evaluates 2 allreduce(b * tensor, G) for every G in 2..g
+// (one exact division per G, in parallel) and then fills the pairs by lookup.
+// Every catalogue pair enters the quantum's maxima (reading A-9 over the
+// whole catalogue); the table stores the pairs of kept strategies (pads 0).
+constexpr int K1G = 1024;  // largest group size with a lookup table
+__device__ __forceinline__ int64_t reshard_group(const int32_t* s1, const int32_t* s2) {
+  const int64_t t1 = s1[0], r1 = (int64_t)s1[1] * s1[2], t2 = s2[0], r2 = (int64_t)s2[1] * s2[2];
+  if (t1 == t2 && r1 == r2) return 1;  // identical layouts: no resharding
+  int64_t G = 1;
+  if (t1 != t2) G = max(G, t1 > t2 ? (t1 + t2 - 1) / t2 : (t2 + t1 - 1) / t1);
+  if (r1 != r2) G = max(G, r1 > r2 ? (r1 + r2 - 1) / r2 : (r2 + r1 - 1) / r1);
+  return G;
+}
+__device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* __restrict__ cfgs, int L, int slot) {
+  __shared__ int64_t tab[K1G + 1];
   const CfgDev& cf = cfgs[blockIdx.y];
-  // every catalogue pair (j, i): the quantum's maxima include the pairs of
-  // dropped strategies (reading A-9 over the whole catalogue); the table
-  // stores the pairs of kept ones at their compacted place (pads stay 0)
-  const int SF = cf.Sfull, NSP = cf.NSP, f2 = SF * SF;
-  const int nR = (L - 1) * f2, nS = L * f2;
-  {  // pad rows / columns of the compacted layout: R = 0
-    const int n2 = NSP * NSP, pR = (L - 1) * n2, pS = L * n2;
-    for (int idx = bx * blockDim.x + threadIdx.x; idx < pR + pS; idx += nb * blockDim.x) {
-      const int jx = idx < pR ? idx : idx - pR;
-      const int r = jx % n2;
-      if (r / NSP >= cf.S || r % NSP >= cf.S) (bb.ns + (idx < pR ? cf.offRf : cf.offRs))[jx] = 0;
-    }
+  const int SF = cf.Sfull, NSP = cf.NSP, n2 = NSP * NSP;
+  const bool isR = slot < L - 1;
+  const int e = isR ? slot : slot - (L - 1);  // R: edge e -> e+1; Rskip: destination v = e
+  int64_t* dst = bb.ns + (isR ? cf.offRf : cf.offRs) + (int64_t)e * n2;
+  const int64_t tb = isR ? bb.chain[e] : bb.skipb[e];
+  const int32_t* tfd = bb.cat[blockIdx.y].tfd;
+  if (tb < 0) {  // no such edge: all zero
+    for (int j = threadIdx.x; j < n2; j += blockDim.x) dst[j] = 0;
+    return;
   }
-  for (int idx = bx * blockDim.x + threadIdx.x; idx < nR + nS; idx += nb * blockDim.x) {
-    const bool isR = idx < nR;
-    const int jx = isR ? idx : idx - nR;
-    const int e = jx / f2, k = (jx - e * f2) / SF, l = jx - e * f2 - k * SF;
-    const int64_t b = cl.B / cf.c;
-    int64_t v = 0;
-    const int64_t tb = isR ? bb.chain[e] : bb.skipb[e];
-    if (tb >= 0) {
-      const Coll co{cl};
-      v = checked(co.reshard(bb.cat[blockIdx.y].tfd + 3 * k, bb.cat[blockIdx.y].tfd + 3 * l, (u128)b * tb), bb.qglob + 1);
-    }
+  const int64_t b = cl.B / cf.c;
+  const Coll co{cl};
+  const int gmax = min(cf.g, K1G);
+  for (int G = 2 + threadIdx.x; G <= gmax; G += blockDim.x)
+    tab[G] = checked(co.reshard_G((u128)b * tb, G), bb.qglob + 1);
+  if (threadIdx.x == 0) tab[1] = 0;
+  __syncthreads();
+  int64_t mx = 0;
+  for (int j = threadIdx.x; j < SF * SF; j += blockDim.x) {
+    const int k = j / SF, l = j - k * SF;
+    const int64_t G = reshard_group(tfd + 3 * k, tfd + 3 * l);
+    const int64_t v = G <= gmax ? tab[G] : checked(co.reshard_G((u128)b * tb, G), bb.qglob + 1);
+    mx = max(mx, v);
     const int kc = cf.comp[k], lc = cf.comp[l];
-    if (kc >= 0 && lc >= 0) (bb.ns + (isR ? cf.offRf : cf.offRs))[((int64_t)e * NSP + kc) * NSP + lc] = v;
-    // per-layer maxima for the quantum: R of edge e goes into layer e+1
-    if (v > 0 && (isR || (cf.skip >= 0 && e >= cf.skip + 2)))
-      amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + (isR ? e + 1 : e)) * 4 + (isR ? 1 : 2), v);
+    if (kc >= 0 && lc >= 0) dst[kc * NSP + lc] = v;
   }
+  for (int j = threadIdx.x; j < n2; j += blockDim.x)  // pad rows / columns
+    if (j / NSP >= cf.S || j % NSP >= cf.S) dst[j] = 0;
+  // per-layer maxima for the quantum: R of edge e goes into layer e+1
+  if (mx > 0 && (isR || (cf.skip >= 0 && e >= cf.skip + 2)))
+    amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + (isR ? e + 1 : e)) * 4 + (isR ? 1 : 2), mx);
 }
 
 // K1c: cut costs: every edge crossing the cut after layer e, fwd + bwd P2P
@@ -215,7 +224,7 @@ __global__ void __launch_bounds__(K1T) k1_costs(ClusterDev cl, BuildBufs bb, con
   TraceScope tr(TR_K1);
   const int bx = blockIdx.x;
   if (bx < nbA) k1a_layers(cl, bb, cfgs, L, bx);
-  else if (bx < nbA + nbR) k1b_reshard(cl, bb, cfgs, L, bx - nbA, nbR);
+  else if (bx < nbA + nbR) k1b_reshard(cl, bb, cfgs, L, bx - nbA);
   else k1c_cuts(cl, bb, cfgs, L);
 }
 
@@ -333,7 +342,7 @@ cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* c
   e = cudaMemsetAsync(bb.qmax, 0, (size_t)ncfg * MAXL * 4 * sizeof(int64_t), st);
   if (e != cudaSuccess) return e;
   const int nbA = (L * 32 + K1T - 1) / K1T;
-  const int nbR = 16;  // grid-stride over (2L-1) NSP^2 entries per config
+  const int nbR = 2 * L - 1;  // one block per edge slot: L-1 chain edges, L skip destinations
   k1_costs<<<dim3(nbA + nbR + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR);
   k1d_quantum<<<ncfg, 64, 0, st>>>(cl, bb, cfg, L, skip);
   k1f_quantise<<<dim3(16, ncfg), 256, 0, st>>>(cl, bb, cfg, L, arena);
