@@ -629,7 +629,7 @@ static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>&
     // tables: the traceback of a deg = 1 winner then needs no sweep of its
     // own (gofs assigned by make_plan).  With the skip source inside, the
     // |S| conditioned copies would keep |S| tables: plain forward sweep.
-    if (skip >= 0 && skip + 2 <= L - 1) fwd(0, L - 1);
+    if ((skip >= 0 && skip + 2 <= L - 1) || S == 1) fwd(0, L - 1);  // |S| = 1: closed form, no G
     else out.push_back(Inst{i, L - 1, L, -1, -1, 5, -1, 0, 0});
     return;
   }
@@ -859,6 +859,7 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   h->cells = h->relax = 0;
   for (auto& x : fw) {
     const uint64_t S = h->cfg[x.cfg].S;
+    if (S == 1) continue;  // closed form (k2_closed_s1): no DP cells
     h->cells += (uint64_t)x.n * S * h->Q;
     h->relax += (uint64_t)(x.n - 1) * S * S * h->Q;
   }

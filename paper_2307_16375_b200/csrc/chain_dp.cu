@@ -152,8 +152,46 @@ int k2_selftest(int* S_out, int* Q_out, int* single_out) {
   return 0;
 }
 
+// |S| = 1: a sweep has no choice to make, so the stage optimum of an interval
+// is its plain sum (Eq. 3 with the single strategy) when its memory fits
+// (Eq. 5): sum over v in [lo, hi] of A[v] (+ Rskip[v] when the skip source
+// lo <= s is inside and v >= s + 2) plus R of the edges inside, INF when
+// sum M > cap.  One warp per sweep writes exactly the P entries the sweep
+// would emit (same interval set, same combine).  Exact: every sum is below
+// the 2^28 bound, so the chain DP's INF clamp never acts.
+__global__ void k2_closed_s1(const K2Args args, int n_inst) {
+  const int ii = blockIdx.x;
+  if (ii >= n_inst) return;
+  const Inst in = args.inst[ii];
+  const CfgDev& cf = args.cfg[in.cfg];
+  const int NSP = cf.NSP, L = args.L, skip = cf.skip;
+  const int32_t* A = args.arena + cf.offA;
+  const int32_t* M = args.arena + cf.offM;
+  const int32_t* Rf = args.arena + cf.offRf;
+  const int32_t* Rs = args.arena + cf.offRs;
+  int32_t* Pc = args.P + cf.offP;
+  for (int uu = in.elo + (int)threadIdx.x; uu <= in.ehi; uu += blockDim.x) {
+    const int lo = in.dir > 0 ? in.a : uu, hi = in.dir > 0 ? uu : in.a;
+    int64_t cost = 0, mem = 0;
+    for (int v = lo; v <= hi; ++v) {
+      cost += A[(int64_t)v * NSP];
+      if (skip >= 0 && lo <= skip && v >= skip + 2) cost += Rs[(int64_t)v * NSP * NSP];
+      if (v > lo) cost += Rf[(int64_t)(v - 1) * NSP * NSP];
+      mem += M[(int64_t)v * NSP];
+    }
+    const int32_t val = mem <= args.cap ? (int32_t)min(cost, (int64_t)INF) : INF;
+    int32_t* dst = in.dir > 0 ? Pc + (int64_t)in.a * L + uu : Pc + (int64_t)uu * L + in.a;
+    if ((in.emit & 3) == 2) atomicMin(dst, val);
+    else *dst = val;
+  }
+}
+
 cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st, int priority) {
   if (n_inst <= 0) return cudaSuccess;
+  if (c.NS == 1 && !args.n_inst && !getenv("UNIAP_NO_CLOSED_S1")) {  // forward |S| = 1 sweeps: closed form
+    k2_closed_s1<<<n_inst, 32, 0, st>>>(args, n_inst);
+    return cudaGetLastError();
+  }
   k2_fn fn = k2_lookup(c);
   if (!fn) return cudaErrorInvalidDeviceFunction;
   const size_t smem = k2_smem_bytes(c);
