@@ -551,6 +551,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   CK(h, h->qmax.ensure((size_t)h->ncfg * MAXL * 4));
   CK(h, h->qglob.ensure(3));
   CK(h, cudaMemsetAsync(h->qglob.p, 0, 3 * sizeof(int64_t), h->st));
+  CK(h, cudaMemsetAsync(h->qmax.p, 0, (size_t)h->ncfg * MAXL * 4 * sizeof(int64_t), h->st));
   CK(h, h->fwd.ensure(fwd.size()));
   CK(h, h->act.ensure(act.size()));
   CK(h, h->ps.ensure(L));

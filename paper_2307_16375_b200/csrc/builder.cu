@@ -238,7 +238,11 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
   (void)cfgs;
   (void)skip;
   const int t = threadIdx.x;
-  for (int i = t; i < L * 4; i += blockDim.x) mx[i] = bb.qmax[(int64_t)blockIdx.x * MAXL * 4 + i];
+  for (int i = t; i < L * 4; i += blockDim.x) {
+    int64_t* q = bb.qmax + (int64_t)blockIdx.x * MAXL * 4 + i;
+    mx[i] = *q;
+    *q = 0;  // zero for the next run's atomics (no memset node in the graph)
+  }
   __syncthreads();
   if (t < 64) {
     const bool expl = cl.quantum > 0;
@@ -337,10 +341,8 @@ __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restri
 
 cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* cfg, int ncfg, int L, int skip,
                       int32_t* arena, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(bb.qglob, 0, 2 * sizeof(int64_t), st);  // [2] = done counter (reset by K1d)
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(bb.qmax, 0, (size_t)ncfg * MAXL * 4 * sizeof(int64_t), st);
-  if (e != cudaSuccess) return e;
+  // qmax / qglob are zeroed by uniap_prepare and left zeroed by K1d (qmax,
+  // done counter); the range flags qglob[1] are sticky for the prepared input
   const int nbA = (L * 32 + K1T - 1) / K1T;
   const int nbR = 2 * L - 1;  // one block per edge slot: L-1 chain edges, L skip destinations
   k1_costs<<<dim3(nbA + nbR + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR);

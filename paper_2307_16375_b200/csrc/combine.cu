@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
                                                   const int64_t* __restrict__ cfg_opt, int32_t* __restrict__ scratch,
                                                   Winner* __restrict__ win, RecordArgs ra) {
   TraceScope tr(TR_K5A);
-  __shared__ int32_t sP[MAXL * MAXL];
+  __shared__ int32_t sP[MAXL * (MAXL + 1)];  // P[a][b] at a * PP + b, odd pitch: lanes over a or b conflict-free
   __shared__ int32_t sO[MAXL];
   __shared__ int32_t stars[TMAX];
   __shared__ int32_t nstar;
@@ -449,7 +449,8 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
   const int64_t* V = vals + (int64_t)wl * (TMAX + 2);
   const int32_t* th = thetas + (int64_t)wl * TMAX;
   const int nt = ntheta[wl];
-  for (int i = t; i < L * L; i += K5T) sP[i] = P[cf.offP + i];
+  const int PP = L | 1;
+  for (int i = t; i < L * L; i += K5T) sP[(i / L) * PP + i % L] = P[cf.offP + i];
   for (int i = t; i < L - 1; i += K5T) sO[i] = arena[cf.offO + i];
   // 3. Theta*: every theta with Val = OPT (c > 1); the unconstrained one (c = 1)
   if (cf.c == 1) {
@@ -476,19 +477,34 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
       // H_deg[a] = P[a][L-1]
       for (int a = lane; a <= L; a += 32) {
         int32_t v = INF;
-        if (a < L) { const int32_t p = sP[a * L + L - 1]; v = p <= theta ? p : INF; }
+        if (a < L) { const int32_t p = sP[a * PP + L - 1]; v = p <= theta ? p : INF; }
         H[deg * (MAXL + 1) + a] = v;
       }
       __syncwarp();
       for (int i = deg - 1; i >= 1; --i) {
+        // H_i[a] = min_b P[a][b] + (O[b] + H_{i+1}[b+1]); the bracket is
+        // lane-independent (broadcast), P[a][b] read transposed
+        const int bhi = L - 1 - (deg - i);
+        const int32_t* Hn = H + (i + 1) * (MAXL + 1);
         for (int a = lane; a <= L; a += 32) {
-          int32_t best = INF;
-          if (a < L)
-            for (int b = a; b <= L - 1 - (deg - i); ++b) {
-              const int32_t p = sP[a * L + b], o = sO[b], h = H[(i + 1) * (MAXL + 1) + b + 1];
-              if (p <= theta && o <= theta && h < INF) best = min(best, p + o + h);
+          uint32_t x = INF, y = INF;
+          if (a < L) {
+            int b = a;
+            for (; b + 1 <= bhi; b += 2) {
+              const int32_t p0 = sP[a * PP + b], p1 = sP[a * PP + b + 1];
+              const int32_t o0 = sO[b], o1 = sO[b + 1], h0 = Hn[b + 1], h1 = Hn[b + 2];
+              const uint32_t w0 = (o0 <= theta && h0 < INF) ? (uint32_t)(o0 + h0) : INF;
+              const uint32_t w1 = (o1 <= theta && h1 < INF) ? (uint32_t)(o1 + h1) : INF;
+              x = __viaddmin_u32(w0, p0 <= theta ? (uint32_t)p0 : INF, x);
+              y = __viaddmin_u32(w1, p1 <= theta ? (uint32_t)p1 : INF, y);
             }
-          H[i * (MAXL + 1) + a] = min(best, INF);
+            if (b <= bhi) {
+              const int32_t p0 = sP[a * PP + b], o0 = sO[b], h0 = Hn[b + 1];
+              const uint32_t w0 = (o0 <= theta && h0 < INF) ? (uint32_t)(o0 + h0) : INF;
+              x = __viaddmin_u32(w0, p0 <= theta ? (uint32_t)p0 : INF, x);
+            }
+          }
+          H[i * (MAXL + 1) + a] = (int32_t)min(min(x, y), (uint32_t)INF);
         }
         __syncwarp();
       }
@@ -502,7 +518,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
           const int b = b0 - lane;
           bool c = false;
           if (b >= a) {
-            const int32_t p = sP[a * L + b], o = sO[b], h = H[(i + 1) * (MAXL + 1) + b + 1];
+            const int32_t p = sP[a * PP + b], o = sO[b], h = H[(i + 1) * (MAXL + 1) + b + 1];
             c = p <= theta && o <= theta && h < INF && pre + p + o + h == F_target;
           }
           const unsigned m = __ballot_sync(0xffffffffu, c);
@@ -510,7 +526,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
         }
         if (found < 0) { ok = false; break; }
         if (lane == 0) mine[i - 1] = found;
-        pre += sP[a * L + found] + sO[found];
+        pre += sP[a * PP + found] + sO[found];
         a = found + 1;
       }
       if (lane == 0) mine[deg - 1] = L - 1;
@@ -547,7 +563,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     for (int i = 0; i < deg; ++i) {
       const int b = have ? best_end[i] : L - 1;
       win->end[i] = b;
-      win->p[i] = sP[a * L + b];
+      win->p[i] = sP[a * PP + b];
       win->o[i] = (i + 1 < deg) ? sO[b] : 0;
       a = b + 1;
     }

@@ -33,7 +33,7 @@ lines = open(path).read().split("\n")
 recs = [tuple(int(x) for x in ln.split()) for ln in lines[1:] if ln.strip()]
 
 
-KIND = {1: "K1 costs", 2: "K1d quantum", 3: "K1f quantise", 4: "fill", 5: "K4", 6: "K5a", 7: "K5c", 8: "K4 sorted", 9: "K4 loaded", 10: "K4 dp done"}
+KIND = {1: "K1 costs", 2: "K1d quantum", 3: "K1f quantise", 4: "fill", 5: "K4", 6: "K5a", 7: "K5c", 8: "K4 sorted", 9: "K4 loaded", 10: "K4 dp done", 11: "K5a winner", 12: "K5a stars", 13: "K5a ends"}
 
 
 def shape(tag):
