@@ -161,21 +161,32 @@ def _tables(t):
     return uniap_tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs), keep
 
 
+_LAYER_DT = np.dtype([("fwd", np.uint64), ("param", np.int64), ("act", np.uint64), ("ctx", np.int64),
+                      ("tpc", np.int64)])
+_EDGE_DT = np.dtype([("src", np.int32), ("dst", np.int32), ("bytes", np.int64)])
+
+
 def _profile(p):
-    keep = []
+    """Marshal a profile dict into the ABI structs (vectorised: one numpy
+    array per field, the struct arrays filled column-wise)."""
     m = p["model"]
     L = m["L"]
-    layers = (uniap_layer * L)()
-    for u, ly in enumerate(m["layers"]):
-        f = np.ascontiguousarray(ly["fwd_ns_per_sample"], dtype=np.int64)
-        a = np.ascontiguousarray(ly["act_bytes_per_sample"], dtype=np.int64)
-        keep += [f, a]
-        layers[u] = uniap_layer(f.ctypes.data_as(_P64), ly["param_bytes"], a.ctypes.data_as(_P64),
-                                ly["ctx_bytes"], ly["tp_comm_bytes_per_sample"])
+    ls = m["layers"]
+    fwd = np.ascontiguousarray([ly["fwd_ns_per_sample"] for ly in ls], dtype=np.int64)
+    act = np.ascontiguousarray([ly["act_bytes_per_sample"] for ly in ls], dtype=np.int64)
+    assert C.sizeof(uniap_layer) == _LAYER_DT.itemsize and C.sizeof(uniap_edge) == _EDGE_DT.itemsize
+    lay = np.zeros(L, _LAYER_DT)
+    lay["fwd"] = fwd.ctypes.data + np.arange(L, dtype=np.uint64) * np.uint64(fwd.strides[0])
+    lay["act"] = act.ctypes.data + np.arange(L, dtype=np.uint64) * np.uint64(act.strides[0])
+    lay["param"] = [ly["param_bytes"] for ly in ls]
+    lay["ctx"] = [ly["ctx_bytes"] for ly in ls]
+    lay["tpc"] = [ly["tp_comm_bytes_per_sample"] for ly in ls]
     E = len(m["edges"])
-    edges = (uniap_edge * max(E, 1))()
-    for i, e in enumerate(m["edges"]):
-        edges[i] = uniap_edge(e["src"], e["dst"], e["tensor_bytes_per_sample"])
+    ed = np.zeros(max(E, 1), _EDGE_DT)
+    if E:
+        ed["src"] = [e["src"] for e in m["edges"]]
+        ed["dst"] = [e["dst"] for e in m["edges"]]
+        ed["bytes"] = [e["tensor_bytes_per_sample"] for e in m["edges"]]
     cl = p["cluster"]
     cluster = uniap_cluster(cl["n_dev"], cl["node_size"], cl["mem_bytes"], cl["mem_reserve_bytes"],
                             cl["bw_intra_Bps"], cl["bw_inter_Bps"], cl["p2p_Bps"], cl["lat_ns"],
@@ -186,8 +197,10 @@ def _profile(p):
         cand = np.ascontiguousarray(np.array(o["cand"], dtype=np.int32).reshape(-1))
     opts = uniap_options(o["B"], o["precision"], o["Q"], o.get("quantum_ns", 0), _p32(cand),
                          0 if cand is None else len(cand) // 2)
-    keep += [layers, edges, cand]
-    return uniap_model(L, layers, E, edges), cluster, opts, keep
+    keep = [fwd, act, lay, ed, cand]
+    model = uniap_model(L, C.cast(lay.ctypes.data, C.POINTER(uniap_layer)), E,
+                        C.cast(ed.ctypes.data, C.POINTER(uniap_edge)))
+    return model, cluster, opts, keep
 
 
 def _result_dict(r, n_cfg, cfg_obj):
@@ -337,8 +350,8 @@ class Handle:
         self._keep = _profile(p)
         model, cluster, opts, _ = self._keep
         self._check(lib().uniap_prepare(self._h, C.byref(model), C.byref(cluster), C.byref(opts)), "prepare")
-        self.n_cfg = len(candidates(p["cluster"]["n_dev"], p["options"]["B"])) if not p["options"].get("cand") \
-            else len(p["options"]["cand"])
+        self.n_cfg = lib().uniap_candidates(p["cluster"]["n_dev"], p["options"]["B"], None, 0) \
+            if not p["options"].get("cand") else len(p["options"]["cand"])
 
     def prepare_tables(self, t):
         tb, keep = _tables(t)

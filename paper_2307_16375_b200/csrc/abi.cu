@@ -21,6 +21,11 @@ using namespace uniap;
 namespace {
 
 template <class T>
+struct View {  // non-owning device pointer
+  T* p = nullptr;
+};
+
+template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
@@ -92,9 +97,13 @@ struct uniap_handle {
   // device buffers
   DevBuf<int32_t> arena, P, thetas, ntheta, cfglist, scratch, G;
   DevBuf<int64_t> ns, vals, cfgopt, qcfg, qglob, gofs, qmax, gstore;
-  DevBuf<int64_t> fwd, act, ps, ctx, tpc, chain, skipb, edges;
-  DevBuf<CfgDev> dcfg;
-  DevBuf<CatDev> dcat;
+  // the level-2 profile, config and catalogue arrays: views into ONE device
+  // blob filled by one DMA per prepare
+  DevBuf<char> upb;
+  View<int64_t> fwd, act, ps, ctx, tpc, chain, skipb, edges;
+  View<CfgDev> dcfg;
+  View<CatDev> dcat;
+  DevBuf<CfgDev> dcfg1;  // level 1: the config array (the arena is its own buffer)
   DevBuf<Inst> inst, binst;
   DevBuf<Winner> win;
   DevBuf<uniap_record> rec;
@@ -119,6 +128,18 @@ struct uniap_handle {
   uint32_t graph_launches = 0, graph_k2 = 0;
   bool capturing = false, timed = false;
   bool no_compact = false;  // uniap_build_tables: keep every strategy in the tables
+  // pinned host staging of the uploads of one prepare (one DMA each, no
+  // stream sync; stage_ev: the previous prepare's copies have read it) and
+  // of the reads of one fetch
+  char* stage = nullptr;
+  size_t stage_n = 0, stage_off = 0;
+  cudaEvent_t stage_ev = nullptr;
+  struct FetchBlock {
+    uniap_record rec;
+    int64_t qg[2];
+    unsigned long long tm[2];
+    int64_t cfgopt[UNIAP_MAX_CFG];
+  }* fb = nullptr;
   std::vector<int64_t> sig;                // what the captured graph depends on
 };
 
@@ -158,6 +179,38 @@ static void update_signature(uniap_handle* h) {
 static cudaError_t h2d(uniap_handle* h, void* dst, const void* src, size_t bytes) {
   h->h2d += bytes;
   return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->st);
+}
+static cudaError_t stage_begin(uniap_handle* h, size_t bytes) {
+  if (h->stage_ev) {
+    cudaError_t e = cudaEventSynchronize(h->stage_ev);
+    if (e != cudaSuccess) return e;
+  }
+  if (bytes > h->stage_n) {
+    if (h->stage) cudaFreeHost(h->stage);
+    h->stage = nullptr;
+    h->stage_n = 0;
+    cudaError_t e = cudaMallocHost((void**)&h->stage, bytes);
+    if (e != cudaSuccess) return e;
+    h->stage_n = bytes;
+  }
+  h->stage_off = 0;
+  return cudaSuccess;
+}
+static cudaError_t stage_put(uniap_handle* h, void* dst, const void* src, size_t bytes) {
+  if (h->stage_off + bytes > h->stage_n) return cudaErrorInvalidValue;
+  memcpy(h->stage + h->stage_off, src, bytes);
+  h->h2d += bytes;
+  cudaError_t e = cudaMemcpyAsync(dst, h->stage + h->stage_off, bytes, cudaMemcpyHostToDevice, h->st);
+  h->stage_off += (bytes + 15) & ~(size_t)15;
+  return e;
+}
+static size_t staged(size_t bytes) { return (bytes + 15) & ~(size_t)15; }
+static cudaError_t stage_end(uniap_handle* h) {
+  if (!h->stage_ev) {
+    cudaError_t e = cudaEventCreateWithFlags(&h->stage_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaEventRecord(h->stage_ev, h->st);
 }
 static cudaError_t d2h(uniap_handle* h, void* dst, const void* src, size_t bytes) {
   h->d2h += bytes;
@@ -273,14 +326,12 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->st);
   for (auto* b : {&h->arena, &h->P, &h->thetas, &h->ntheta, &h->cfglist, &h->scratch, &h->G}) b->release();
-  for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->qglob, &h->gofs, &h->qmax, &h->gstore, &h->fwd, &h->act, &h->ps, &h->ctx,
-                  &h->tpc, &h->chain, &h->skipb, &h->edges})
-    b->release();
+  for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->qglob, &h->gofs, &h->qmax, &h->gstore}) b->release();
+  h->upb.release();
+  h->dcfg1.release();
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   h->clsid.release();
   h->bwp.release();
-  h->dcfg.release();
-  h->dcat.release();
   h->inst.release();
   h->binst.release();
   h->win.release();
@@ -288,6 +339,9 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   for (auto e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto e : h->side_ev) cudaEventDestroy(e);
+  if (h->stage_ev) cudaEventDestroy(h->stage_ev);
+  if (h->stage) cudaFreeHost(h->stage);
+  if (h->fb) cudaFreeHost(h->fb);
   for (auto x : h->side) cudaStreamDestroy(x);
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   if (h->own_stream) cudaStreamDestroy(h->st);
@@ -437,10 +491,13 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
   }
   CK(h, cudaSetDevice(h->device));
   CK(h, h->arena.ensure(h->arena_words));
-  CK(h, h->dcfg.ensure(h->ncfg));
-  CK(h, h2d(h, h->arena.p, a.data(), a.size() * 4));
-  CK(h, h2d(h, h->dcfg.p, h->cfg.data(), h->ncfg * sizeof(CfgDev)));
-  CK(h, cudaStreamSynchronize(h->st));
+  CK(h, h->dcfg1.ensure(h->ncfg));
+  h->dcfg.p = h->dcfg1.p;
+  h->dcat.p = nullptr;
+  CK(h, stage_begin(h, staged(a.size() * 4) + staged(h->ncfg * sizeof(CfgDev))));
+  CK(h, stage_put(h, h->arena.p, a.data(), a.size() * 4));
+  CK(h, stage_put(h, h->dcfg.p, h->cfg.data(), h->ncfg * sizeof(CfgDev)));
+  CK(h, stage_end(h));
   update_signature(h);
   h->ready = true;
   return UNIAP_OK;
@@ -545,33 +602,33 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   CK(h, cudaSetDevice(h->device));
   CK(h, h->arena.ensure(h->arena_words));
   CK(h, h->ns.ensure(h->arena_words));
-  CK(h, h->dcfg.ensure(h->ncfg));
-  CK(h, h->dcat.ensure(h->ncfg));
   CK(h, h->qcfg.ensure(h->ncfg));
   CK(h, h->qmax.ensure((size_t)h->ncfg * MAXL * 4));
   CK(h, h->qglob.ensure(3));
   CK(h, cudaMemsetAsync(h->qglob.p, 0, 3 * sizeof(int64_t), h->st));
   CK(h, cudaMemsetAsync(h->qmax.p, 0, (size_t)h->ncfg * MAXL * 4 * sizeof(int64_t), h->st));
-  CK(h, h->fwd.ensure(fwd.size()));
-  CK(h, h->act.ensure(act.size()));
-  CK(h, h->ps.ensure(L));
-  CK(h, h->ctx.ensure(L));
-  CK(h, h->tpc.ensure(L));
-  CK(h, h->chain.ensure(L));
-  CK(h, h->skipb.ensure(L));
-  CK(h, h->edges.ensure(std::max<size_t>(ed.size(), 3)));
-  auto up = [&](void* d, const void* s, size_t bytes) { return h2d(h, d, s, bytes); };
-  CK(h, up(h->fwd.p, fwd.data(), fwd.size() * 8));
-  CK(h, up(h->act.p, act.data(), act.size() * 8));
-  CK(h, up(h->ps.p, ps.data(), L * 8));
-  CK(h, up(h->ctx.p, ctx.data(), L * 8));
-  CK(h, up(h->tpc.p, tpc.data(), L * 8));
-  CK(h, up(h->chain.p, chain.data(), L * 8));
-  CK(h, up(h->skipb.p, skipb.data(), L * 8));
-  if (!ed.empty()) CK(h, up(h->edges.p, ed.data(), ed.size() * 8));
-  CK(h, up(h->dcfg.p, h->cfg.data(), h->ncfg * sizeof(CfgDev)));
-  CK(h, up(h->dcat.p, h->cat.data(), h->ncfg * sizeof(CatDev)));
-  CK(h, cudaStreamSynchronize(h->st));
+  {  // one pinned staging block -> one device blob, one DMA
+    const size_t sz[10] = {fwd.size() * 8, act.size() * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8,
+                           (size_t)L * 8, std::max<size_t>(ed.size(), 3) * 8, h->ncfg * sizeof(CfgDev),
+                           h->ncfg * sizeof(CatDev)};
+    const void* src[10] = {fwd.data(), act.data(), ps.data(), ctx.data(), tpc.data(), chain.data(), skipb.data(),
+                           ed.data(), h->cfg.data(), h->cat.data()};
+    size_t off[10], tot = 0;
+    for (int i = 0; i < 10; ++i) { off[i] = tot; tot += staged(sz[i]); }
+    CK(h, h->upb.ensure(tot));
+    CK(h, stage_begin(h, tot));
+    memset(h->stage, 0, tot);
+    for (int i = 0; i < 10; ++i)
+      if (src[i]) memcpy(h->stage + off[i], src[i], i == 7 ? ed.size() * 8 : sz[i]);
+    h->h2d += tot;
+    CK(h, cudaMemcpyAsync(h->upb.p, h->stage, tot, cudaMemcpyHostToDevice, h->st));
+    char* b = h->upb.p;
+    h->fwd.p = (int64_t*)(b + off[0]); h->act.p = (int64_t*)(b + off[1]); h->ps.p = (int64_t*)(b + off[2]);
+    h->ctx.p = (int64_t*)(b + off[3]); h->tpc.p = (int64_t*)(b + off[4]); h->chain.p = (int64_t*)(b + off[5]);
+    h->skipb.p = (int64_t*)(b + off[6]); h->edges.p = (int64_t*)(b + off[7]);
+    h->dcfg.p = (CfgDev*)(b + off[8]); h->dcat.p = (CatDev*)(b + off[9]);
+  }
+  CK(h, stage_end(h));
   update_signature(h);
   h->ready = true;
   return UNIAP_OK;
@@ -1080,24 +1137,23 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
 extern "C" uniap_status uniap_fetch(uniap_handle* h, uniap_result* out) {
   if (!h || !out) return UNIAP_ERR_ARG;
   CK(h, cudaSetDevice(h->device));
-  uniap_record R;
   const uniap_record* src = h->last_rec;
   if (!src) FAIL(h, UNIAP_ERR_ARG, "nothing has run on this handle");
-  CK(h, d2h(h, &R, src, sizeof R));
-  if (h->level2) {
-    int64_t qg[2];
-    CK(h, d2h(h, qg, h->qglob.p, 16));
-    CK(h, cudaStreamSynchronize(h->st));
-    h->quantum = qg[0];
-  } else {
-    h->quantum = 0;
-  }
+  // every read of the fetch: async copies into pinned memory, one sync
+  if (!h->fb) CK(h, cudaMallocHost((void**)&h->fb, sizeof(*h->fb)));
+  auto* fb = h->fb;
+  int64_t* keep = out->cfg_objective;
+  CK(h, d2h(h, &fb->rec, src, sizeof fb->rec));
+  if (h->level2) CK(h, d2h(h, fb->qg, h->qglob.p, 16));
+  if (h->timed && h->tim.p) CK(h, cudaMemcpyAsync(fb->tm, h->tim.p, 16, cudaMemcpyDeviceToHost, h->st));
+  if (keep) CK(h, d2h(h, fb->cfgopt, h->cfgopt.p, h->ncfg * 8));
+  CK(h, cudaStreamSynchronize(h->st));
+  const uniap_record& R = fb->rec;
+  h->quantum = h->level2 ? fb->qg[0] : 0;
   if (h->timed) {
-    CK(h, cudaStreamSynchronize(h->st));
     h->ms_dp = 0.f;
-    unsigned long long tm[2] = {0ull, 0ull};
-    if (h->tim.p) CK(h, cudaMemcpy(tm, h->tim.p, sizeof tm, cudaMemcpyDeviceToHost));
-    if (tm[0] && tm[1] >= ~tm[0]) h->ms_dp = (float)((double)(tm[1] - ~tm[0]) * 1e-6);
+    const unsigned long long* tm = fb->tm;
+    if (h->tim.p && tm[0] && tm[1] >= ~tm[0]) h->ms_dp = (float)((double)(tm[1] - ~tm[0]) * 1e-6);
     cudaEventElapsedTime(&h->ms_total, h->ev[0], h->ev[3]);
     h->timed = false;
   }
@@ -1115,11 +1171,9 @@ extern "C" uniap_status uniap_fetch(uniap_handle* h, uniap_result* out) {
       fclose(f);
     }
   }
-  int64_t* keep = out->cfg_objective;
   memset(out, 0, sizeof *out);
   out->cfg_objective = keep;
-  if (keep) CK(h, d2h(h, keep, h->cfgopt.p, h->ncfg * 8));
-  CK(h, cudaStreamSynchronize(h->st));
+  if (keep) memcpy(keep, fb->cfgopt, h->ncfg * 8);
   out->objective = R.objective;
   out->cfg_index = R.cfg_index;
   out->deg = R.deg;
