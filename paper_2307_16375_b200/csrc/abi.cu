@@ -349,6 +349,7 @@ extern "C" void uniap_destroy(uniap_handle* h) {
 }
 
 static void plan_instances(int L, int i, int deg, int S, int skip, bool all_intervals, std::vector<Inst>& out);
+static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>& out);
 
 // ---------------------------------------------------------------------------
 // Layout of the configs in the device arena.
@@ -367,9 +368,13 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
   int64_t off = 0;
   for (int i = 0; i < h->ncfg; ++i) {
     // a config with only a few (long) chains spreads each over more SMs
+    // (deg = 1: the whole chain, or its |S| skip-conditioned copies, is the
+    // critical path of the step; measured: giving deg = 2's prefix + suffix
+    // sweeps the same treatment starves the many-sweep classes of SMs)
     std::vector<Inst> v;
-    plan_instances(L, i, deg[i], S[i], skipc[i], false, v);
-    const bool single = !v.empty() && v.size() <= 4;
+    plan_fast(L, i, deg[i], S[i], skipc[i], v);
+    static const int nsingle = getenv("UNIAP_K2_SINGLE_N") ? atoi(getenv("UNIAP_K2_SINGLE_N")) : 1;
+    const bool single = !v.empty() && (deg[i] == 1 || (int)v.size() <= nsingle);
     K2Class k;
     if (!k2_pick_class(S[i], h->Q, single, &k)) FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
     h->cls[i] = k;

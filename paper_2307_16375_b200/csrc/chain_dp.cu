@@ -76,9 +76,16 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   int C = pow2ceil((Q + B - 1) / B);
   static const int single_ok = env_int("UNIAP_K2_SINGLE", 1);  // tuning knob (experiments)
   if (single && single_ok) {
-    const int cmax = 8;
-    while (C < cmax && B > 128) {
-      B /= 2;
+    // a config with few (long) sweeps: at least 256 buckets per CTA (4
+    // warps), the bucket axis over a cluster of up to 8 CTAs (measured on the
+    // bench workloads: C = 4 x 256 beats C = 8 x 128 at Q = 1024; at 4096,
+    // 16-CTA clusters starve the other classes, which need whole GPCs free)
+    static const int bs = env_int("UNIAP_K2_SINGLE_B", 256);  // tuning knob (experiments)
+    static const int cs = env_int("UNIAP_K2_SINGLE_C", 8);
+    B = std::min(B, std::max(32, bs));
+    C = pow2ceil((Q + B - 1) / B);
+    while (C > cs && B < Bmax) {
+      B *= 2;
       C = pow2ceil((Q + B - 1) / B);
     }
   }

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
         }
       }
     }
-    if (eG) {
+    if (eG && !(args.flags & 8)) {
       const int lo = in.a - in.n + 1;
       int32_t* g = args.G + in.gofs + (int64_t)(u - lo) * NSP * Q;
 #pragma unroll
