@@ -97,7 +97,6 @@ struct uniap_handle {
   // device buffers
   DevBuf<int32_t> arena, P, thetas, ntheta, cfglist, scratch, G;
   DevBuf<int64_t> ns, vals, cfgopt, qcfg, qglob, gofs, qmax, gstore;
-  DevBuf<int32_t> mitm_ctr;  // split deg = 1 chains: arrival counter per config (K2Args::mitm_ctr)
   // the level-2 profile, config and catalogue arrays: views into ONE device
   // blob filled by one DMA per prepare
   DevBuf<char> upb;
@@ -332,7 +331,6 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   h->dcfg1.release();
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   h->clsid.release();
-  h->mitm_ctr.release();
   h->bwp.release();
   h->inst.release();
   h->binst.release();
@@ -370,15 +368,13 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
   int64_t off = 0;
   for (int i = 0; i < h->ncfg; ++i) {
     // a config with only a few (long) chains spreads each over more SMs
-    // (deg = 1: its two halves, or the skip-conditioned copies of one, are a
-    // critical path of the step; so are deg = 2's prefix + suffix sweeps at
-    // Q <= 2048.  Measured: at Q = 4096 the many-sweep classes bind instead
-    // (the step is throughput-bound) and spreading deg = 2 starves them.)
+    // (deg = 1: the whole chain, or its |S| skip-conditioned copies, is the
+    // critical path of the step; measured: giving deg = 2's prefix + suffix
+    // sweeps the same treatment starves the many-sweep classes of SMs)
     std::vector<Inst> v;
     plan_fast(L, i, deg[i], S[i], skipc[i], v);
-    static const int nsingle = getenv("UNIAP_K2_SINGLE_N") ? atoi(getenv("UNIAP_K2_SINGLE_N")) : 4;
-    static const int qsingle = getenv("UNIAP_K2_SINGLE_Q") ? atoi(getenv("UNIAP_K2_SINGLE_Q")) : 2048;
-    const bool single = !v.empty() && (deg[i] == 1 || ((int)v.size() <= nsingle && h->Q <= qsingle));
+    static const int nsingle = getenv("UNIAP_K2_SINGLE_N") ? atoi(getenv("UNIAP_K2_SINGLE_N")) : 1;
+    const bool single = !v.empty() && (deg[i] == 1 || (int)v.size() <= nsingle);
     K2Class k;
     if (!k2_pick_class(S[i], h->Q, single, &k)) FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
     h->cls[i] = k;
@@ -692,17 +688,12 @@ static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>&
     }
   };
   if (deg == 1) {
-    // only P[0][L-1] is needed: the chain split in two halves that run
-    // concurrently (forward 0..m, backward L-1..m+1; chain_dp.cuh,
-    // mitm_combine), so the critical path is about L/2 layers.  With the
-    // skip source s inside, m = s and the backward half runs one copy per
-    // strategy of s.  (gofs assigned by make_plan; |S| = 1: closed form.)
-    if (S == 1) { fwd(0, L - 1); return; }
-    if (L == 1) { out.push_back(Inst{i, 0, 1, -1, +1, 1, 0, 0, 0}); return; }
-    const bool sk = skip >= 0 && skip + 2 <= L - 1;
-    const int m = sk ? skip : L / 2 - 1;
-    out.push_back(Inst{i, 0, m + 1, -1, +1, 8, -1, 1, 0});
-    for (int ks = 0; ks < (sk ? S : 1); ++ks) out.push_back(Inst{i, L - 1, L - 1 - m, sk ? ks : -1, -1, 8, -1, 1, 0});
+    // the whole chain as ONE backward sweep from L-1 that also keeps its G
+    // tables: the traceback of a deg = 1 winner then needs no sweep of its
+    // own (gofs assigned by make_plan).  With the skip source inside, the
+    // |S| conditioned copies would keep |S| tables: plain forward sweep.
+    if ((skip >= 0 && skip + 2 <= L - 1) || S == 1) fwd(0, L - 1);  // |S| = 1: closed form, no G
+    else out.push_back(Inst{i, L - 1, L, -1, -1, 5, -1, 0, 0});
     return;
   }
   fwd(0, L - deg);                                               // stage 1: prefixes
@@ -796,9 +787,7 @@ extern "C" uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32
 // per-layer synchronisation) -- so it starts on free SMs.
 // ---------------------------------------------------------------------------
 
-static int class_key(const K2Class& k) {
-  return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C + (k.DB ? 0 : 50000) + k.G * 10000 + (k.excl ? 500000000 : 0);
-}
+static int class_key(const K2Class& k) { return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C + (k.DB ? 0 : 50000) + k.G * 10000; }
 
 static void group_instances(const uniap_handle* h, std::vector<Inst>& all, std::vector<K2Group>& grp) {
   std::vector<int> key(all.size());
@@ -880,10 +869,7 @@ static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp,
     K2Args args{dcount_per_class ? dinst : dinst + grp[g].s,
                 dcount_per_class ? dcount_per_class + g : nullptr,
                 h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip, k2_flags()};
-    if (!dcount_per_class) {
-      args.tim = h->tim.p;  // forward launches: phase clock
-      args.mitm_ctr = h->mitm_ctr.p;
-    }
+    if (!dcount_per_class) args.tim = h->tim.p;  // forward launches: phase clock
     if (h->trace.p) {  // diagnostics: tag = class shape | forward/backward | group
       const K2Class& k = grp[g].cls;
       args.trace = h->trace.p;
@@ -939,7 +925,6 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     if (S == 1) continue;  // closed form (k2_closed_s1): no DP cells
     h->cells += (uint64_t)x.n * S * h->Q;
     h->relax += (uint64_t)(x.n - 1) * S * S * h->Q;
-    if ((x.emit & 8) && x.dir > 0) h->relax += S * S * h->Q;  // the split chain's combine (one more step)
   }
   h->cells_canon = 0;
   for (int i : R.local) {
@@ -1006,24 +991,10 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
         }
         x.gofs = gstore[x.cfg] + (int64_t)(x.ks < 0 ? 0 : x.ks) * h->L * d.NSP * h->Q;
       }
-    // final states of the split deg = 1 halves: per config [forward][backward copy 0..]
-    std::vector<int64_t> mitm(h->ncfg, -1);
-    for (auto& x : fw)
-      if (x.emit & 8) {
-        const CfgDev& d = h->cfg[x.cfg];
-        const int64_t blk = (int64_t)d.NSP * h->Q;
-        if (mitm[x.cfg] < 0) {
-          mitm[x.cfg] = off;
-          off += (int64_t)(1 + (d.skip >= 0 && d.skip + 2 <= h->L - 1 ? d.S : 1)) * blk;
-        }
-        x.gofs = mitm[x.cfg] + (x.dir > 0 ? 0 : (int64_t)(1 + (x.ks < 0 ? 0 : x.ks)) * blk);
-      }
     gmax = off;
   }
   CK(h, h->gstore.ensure(h->ncfg));
   CK(h, h2d(h, h->gstore.p, gstore.data(), h->ncfg * 8));
-  CK(h, h->mitm_ctr.ensure(h->ncfg));
-  CK(h, cudaMemsetAsync(h->mitm_ctr.p, 0, h->ncfg * sizeof(int32_t), h->st));
   int max_bw = 1;
   for (auto& g : R.bgrp) max_bw = std::max(max_bw, g.max_inst);
   // device buffers + uploads (outside any graph)

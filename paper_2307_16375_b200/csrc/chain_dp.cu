@@ -24,10 +24,7 @@ static size_t smem_words(int NS, int B, int ne = 2) {
   return (size_t)ne * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP) + MAXL;
 }
 
-size_t k2_smem_bytes(const K2Class& c) {
-  const size_t b = smem_words(c.NS, c.T * c.V, c.DB ? 2 : 1) * sizeof(int32_t);
-  return c.excl ? std::max<size_t>(b, 200 * 1024) : b;
-}
+size_t k2_smem_bytes(const K2Class& c) { return smem_words(c.NS, c.T * c.V, c.DB ? 2 : 1) * sizeof(int32_t); }
 
 static int pow2ceil(int x) {
   int p = 1;
@@ -114,8 +111,6 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   }
   static const int pref_v = env_int("UNIAP_K2_V", 0);
   K2Class c{NS, 2, B / 2, C, true};
-  static const int excl = env_int("UNIAP_K2_EXCL", 1);  // tuning knob (experiments)
-  if (single && single_ok && excl) c.excl = 1;
   if (B == 1024 && NS <= 16 && (pref_v == 4 || (pref_v == 0 && C == 1))) { c.V = 4; c.T = 256; }
   if (B == 32) { c.V = 1; c.T = 32; }
   if (B == 2048) { c.V = 4; c.T = 512; }
@@ -215,7 +210,7 @@ cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStre
     bool seen = false;
     for (auto f : done) seen |= (f == fn);
     if (!seen) {
-      cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);  // + static (mitm flag)
+      cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       if (e != cudaSuccess) return e;
       e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;

@@ -114,119 +114,6 @@ struct Stage {
   static constexpr int WORDS = NS * NSP + 2 * NSP;
 };
 
-// Split deg = 1 chain ("meet in the middle"; Inst::emit & 8).  A deg = 1
-// config needs only P[0][L-1], the optimum of the whole chain (Eq. 3 under
-// Eq. 5).  The chain is swept as two halves that run concurrently: forward
-// over layers 0..m (final state Df[k][q]: best cost of 0..m ending on k with
-// memory <= q) and backward over L-1..m+1 (final state Gb[k'][q]: best cost
-// of m+1..L-1 starting on k').  Then exactly
-//   P[0][L-1] = min_{k, k', x} Df[k][cap - x] + R[m][k][k'] + Gb[k'][x]
-// (a split x of the memory budget: both tables are "<= q" minima, so every
-// feasible assignment is covered and every combination is feasible).  With
-// the skip source s inside, m = s and the backward half runs one copy per
-// strategy ks of s (the skip-edge terms Rskip[v][ks][.] of Eq. 3 all lie in
-// m+1..L-1); copy ks combines with Df[ks] only.  Each half stores its final
-// state at G + gofs (block [1 + copy] after the forward block); the last of
-// the 1 + copies arrivals (a per-config counter) combines, its CTAs splitting
-// the x range like the sweep's buckets, and atomicMin's P[0][L-1].
-// The combine of the last arrival (not inlined: it runs once per sweep and
-// must not disturb the sweep loop's register allocation).  Unrolled over the
-// strategies so every thread has all its loads in flight at once.  Pad
-// strategies (k >= S) hold INF rows and zero R entries: no effect.
-template <int NS, int V, int T>
-__device__ __noinline__ void mitm_combine_body(const K2Args& args, const CfgDev& cf, int m, bool sk, int64_t base,
-                                               int x0, int L, int cap) {
-  const int Q = cap + 1, NSP = cf.NSP;
-  const int64_t blk = (int64_t)NSP * Q;
-  const int32_t* Df = args.G + base;
-  const int32_t* Rr = args.arena + cf.offRf + (int64_t)m * NSP * NSP;  // R[m][k][k']
-  int64_t best = INF;
-  if (!sk) {
-    const int32_t* Gb = args.G + base + blk;
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int x = x0 + j * T;
-      if (x < Q) {
-        int32_t gb[NS], f[NS];
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          gb[k] = __ldcg(Gb + (int64_t)k * Q + x);
-          f[k] = __ldcg(Df + (int64_t)k * Q + (cap - x));
-        }
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          int32_t e = INF;
-#pragma unroll
-          for (int k2 = 0; k2 < NS; ++k2) e = min(e, __ldg(Rr + k * NSP + k2) + gb[k2]);
-          best = min(best, (int64_t)f[k] + e);
-        }
-      }
-    }
-  } else {
-#pragma unroll 2
-    for (int c = 0; c < cf.S; ++c) {  // copy c: the skip source s = m on strategy c
-      const int32_t* Gb = args.G + base + (int64_t)(1 + c) * blk;
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const int x = x0 + j * T;
-        if (x < Q) {
-          int32_t gb[NS];
-#pragma unroll
-          for (int k2 = 0; k2 < NS; ++k2) gb[k2] = __ldcg(Gb + (int64_t)k2 * Q + x);
-          const int32_t f = __ldcg(Df + (int64_t)c * Q + (cap - x));
-          int32_t e = INF;
-#pragma unroll
-          for (int k2 = 0; k2 < NS; ++k2) e = min(e, __ldg(Rr + c * NSP + k2) + gb[k2]);
-          best = min(best, (int64_t)f + e);
-        }
-      }
-    }
-  }
-  int32_t v = (int32_t)min(best, (int64_t)INF);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if ((threadIdx.x & 31) == 0 && v < INF) atomicMin(args.P + cf.offP + (L - 1), v);  // P[0][L-1]
-}
-
-template <int NS, int V, int T, bool CL>
-__device__ __forceinline__ void mitm_combine(const K2Args& args, const Inst& in, const CfgDev& cf, const int32_t (&d)[NS][V],
-                                             int rank, int L, int cap) {
-  constexpr int B = T * V;
-  const int t = threadIdx.x, Q = cap + 1;
-  const int64_t blk = (int64_t)cf.NSP * Q;
-  const int m = in.dir > 0 ? in.a + in.n - 1 : in.a - in.n;  // the forward half's last layer
-  const bool sk = cf.skip >= 0 && cf.skip == m && cf.skip + 2 <= L - 1;
-  const int copies = sk ? cf.S : 1;
-  const int64_t base = in.gofs - (in.dir > 0 ? 0 : (int64_t)(1 + (in.ks < 0 ? 0 : in.ks)) * blk);
-  int32_t* mine = args.G + in.gofs;
-#pragma unroll
-  for (int k = 0; k < NS; ++k)
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int q = rank * B + j * T + t;
-      if (q < Q) mine[(int64_t)k * Q + q] = d[k][j];
-    }
-  __threadfence();
-  __shared__ int s_last;
-  if constexpr (CL) cl_sync(); else __syncthreads();
-  if (rank == 0 && t == 0) {
-    const int old = atomicAdd(args.mitm_ctr + in.cfg, 1);
-    s_last = old == copies;  // copies + 1 arrivals
-    if (old == copies) args.mitm_ctr[in.cfg] = 0;  // ready for the next run
-  }
-  bool last;
-  if constexpr (CL) {
-    cl_sync();
-    last = *map_rank(&s_last, 0) != 0;
-  } else {
-    __syncthreads();
-    last = s_last != 0;
-  }
-  if (!last) return;
-  __threadfence();
-  mitm_combine_body<NS, V, T>(args, cf, m, sk, base, rank * B + t, L, cap);
-}
-
 template <int NS, int V, int T, bool CL, bool DB = true, int G = 0>
 __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   static_assert(DB || !CL, "single-buffered E only without clusters");
@@ -646,7 +533,6 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       else *dst = sProw[uu];
     }
   }
-  if (in.emit & 8) mitm_combine<NS, V, T, CL>(args, in, cf, d, rank, L, cap);
   if constexpr (CL) cl_sync();  // keep this CTA's E alive for remote readers
   if (args.trace && t == 0) trace_put(args.trace, args.tag, t_start, rank, ii, in.n);
   if (args.tim && t == 0) {  // the forward phase's device time (uniap_fetch: ms_gpu_dp)

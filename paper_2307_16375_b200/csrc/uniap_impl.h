@@ -48,8 +48,7 @@ struct Inst {
   int32_t dir;   // +1 forward (emit P[a][u]), -1 backward (store G[u])
   int32_t emit;  // 1: P plain store, 2: P atomicMin (several copies), 0: store G (traceback);
                  // 5 / 6: as 1 / 2 and store G too (the whole-chain sweep of a deg = 1 config,
-                 // kept for its traceback); 8: one half of a split deg = 1 chain (store the
-                 // final state at G + gofs; the last half to finish combines P[0][L-1])
+                 // kept for its traceback)
   int64_t gofs;  // G stores: word offset of this sweep's G block (layers a-n+1..a)
   // emit 1/2: P entries of the layers u in [elo, ehi] only -- P[a][u] for a
   // forward sweep (intervals starting at a), P[u][a] for a backward sweep
@@ -73,9 +72,6 @@ struct K2Args {
   // forward-phase clock (%globaltimer, ns): tim[0] = max of ~start, tim[1] =
   // max of end over the launch's CTAs (both reset to 0 per run), or nullptr
   unsigned long long* tim = nullptr;
-  // split deg = 1 chains (Inst::emit & 8): per config arrival counter of the
-  // two halves (zero between runs: the last arrival resets it)
-  int32_t* mitm_ctr = nullptr;
 };
 
 // Timeline record of one CTA (UNIAP_TRACE): trace[0] = record count, trace[1]
@@ -127,8 +123,6 @@ struct K2Class {
   int C;       // CTAs per cluster
   bool DB;     // double-buffered E (one barrier per layer); single: two
   int G = 0;   // > 0: segmented schedule with G bucket segments (C = 1)
-  int excl = 0;  // 1: the CTAs take an SM to themselves (critical-path sweeps: shared memory
-                 // padded so that no other K2 CTA is co-resident and steals issue slots)
 };
 
 // chain_dp.cu
