@@ -6,5 +6,6 @@ GPU (so the ABI can be inspected), but creating a ``Handle`` requires a
 compute-capability 10.x device and the built library.
 """
 from .binding import (  # noqa: F401
-    EXPORTS, INT64_MAX, LIB_PATH, RECORD_BYTES, UNIAP_INF, Handle, UniapError, candidates, catalogue, lib, pick, selftest, shard_tables,
+    EXPORTS, INT64_MAX, LIB_PATH, RECORD_BYTES, UNIAP_INF, Handle, Profile, UniapError, candidates, catalogue, lib, pick,
+    selftest, shard_tables,
 )

@@ -204,6 +204,30 @@ def _profile(p):
     return model, cluster, opts, keep
 
 
+class Profile:
+    """A profile marshalled once into the ABI structs (uniap_model /
+    uniap_cluster / uniap_options over host arrays it owns).  Pass it to
+    Handle.prepare / Handle.plan instead of the dict to skip the per-call
+    dict -> struct conversion; every call still validates and uploads the
+    host arrays (uniap_prepare).  The arrays can be edited in place
+    (`fwd`, `act`: int64 [L][1+log2 n]) between calls."""
+
+    def __init__(self, p):
+        self.model, self.cluster, self.opts, self.keep = _profile(p)
+        self.fwd, self.act = self.keep[0], self.keep[1]
+        o = p["options"]
+        self.n_cfg = len(o["cand"]) if o.get("cand") else len(candidates(p["cluster"]["n_dev"], o["B"]))
+
+
+def _structs(p):
+    if isinstance(p, Profile):
+        return p.model, p.cluster, p.opts, p.keep, p.n_cfg
+    model, cluster, opts, keep = _profile(p)
+    o = p["options"]
+    n = len(o["cand"]) if o.get("cand") else len(candidates(p["cluster"]["n_dev"], o["B"]))
+    return model, cluster, opts, keep, n
+
+
 def _result_dict(r, n_cfg, cfg_obj):
     deg = r.deg
     L = r.L
@@ -309,9 +333,8 @@ class Handle:
         return P.reshape(L, L)
 
     def plan(self, p):
-        model, cluster, opts, keep = _profile(p)
-        n = len(candidates(p["cluster"]["n_dev"], p["options"]["B"])) if not p["options"].get("cand") \
-            else len(p["options"]["cand"])
+        """p: a profile dict or a Profile."""
+        model, cluster, opts, keep, n = _structs(p)
         cfg_obj = (C.c_int64 * n)()
         r = uniap_result()
         r.cfg_objective = cfg_obj
@@ -348,11 +371,10 @@ class Handle:
 
     # ---- split pipeline ----
     def prepare(self, p):
-        self._keep = _profile(p)
-        model, cluster, opts, _ = self._keep
+        """p: a profile dict or a Profile (validated and uploaded on every call)."""
+        self._keep = _structs(p)
+        model, cluster, opts, _, self.n_cfg = self._keep
         self._check(lib().uniap_prepare(self._h, C.byref(model), C.byref(cluster), C.byref(opts)), "prepare")
-        self.n_cfg = lib().uniap_candidates(p["cluster"]["n_dev"], p["options"]["B"], None, 0) \
-            if not p["options"].get("cand") else len(p["options"]["cand"])
 
     def prepare_tables(self, t):
         tb, keep = _tables(t)

@@ -108,6 +108,26 @@ def test_models_full_size(h, orc, name):
     assert got["quantum_ns"] == qn
 
 
+def test_prepared_profile_object(h, orc):
+    """pkg.Profile (marshalled once, reused; arrays edited in place) gives the
+    oracle's answer on every call, like the dict path."""
+    import paper_2307_16375_b200 as pkg
+    p = profiles.make_profile("vit")
+    prof = pkg.Profile(p)
+    want, _ = orc.plan(p)
+    for _ in range(2):
+        h.prepare(prof)
+        h.run()
+        _same(h.fetch(), want, "vit Profile")
+    # edit in place: halve every forward time; the dict path of the edited
+    # profile is the reference
+    prof.fwd[:] = prof.fwd // 2
+    for ly, row in zip(p["model"]["layers"], prof.fwd):
+        ly["fwd_ns_per_sample"] = [int(x) for x in row]
+    want2, _ = orc.plan(p)
+    _same(h.plan(prof), want2, "vit Profile edited")
+
+
 def test_models_nojitter_ties(h, orc):
     for name in ("bert", "vit"):
         p = profiles.make_profile(name, jitter=False)
