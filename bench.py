@@ -245,14 +245,14 @@ def main():
         if ws > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        h.prepare(prof)                         # validation + H2D of the profile
-        h.run(rank, ws, rec.data_ptr())
         if ws > 1:
+            h.prepare(prof)                     # validation + H2D of the profile
+            h.run(rank, ws, rec.data_ptr())
             dist.all_gather_into_tensor(all_recs, rec)
             host = all_recs.cpu().numpy().tobytes()   # D2H of every rank's record
             st, res = pkg.pick(host, ws)
         else:
-            res = h.fetch()                     # D2H of the record + per-config optima
+            res = h.plan(prof)                  # uniap_plan: prepare (H2D) + run + fetch (D2H)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if i > 0:
@@ -289,7 +289,8 @@ def main():
             "cells_executed_per_step": r["dp_cells"], "cells_canonical_per_step": r["dp_cells_canonical"],
             "e2e": {"value": cells / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d_per_step,
                     "d2h_bytes_per_step": d2h_per_step, "seconds_per_step": e2e_s,
-                    "path": "uniap_prepare (validate + H2D of the ABI profile) + uniap_run + uniap_fetch (D2H + sync)",
+                    "path": "uniap_plan = uniap_prepare (validate + H2D of the ABI profile) + uniap_run + uniap_fetch "
+                            "(D2H + sync); N > 1: + NCCL all_gather of the records and uniap_pick",
                     "python_marshal_us": statistics.median(marshal_us)},
             "gpu_launches": launches_per_step,
             "roofline": {"bound": "alu", "kernel": "k2_chain (VIADDMNMX min-plus)", "achieved": achieved,
