@@ -139,7 +139,7 @@ struct uniap_handle {
     int64_t qg[2];
     unsigned long long tm[2];
     int64_t cfgopt[UNIAP_MAX_CFG];
-  }* fb = nullptr;
+  }* fb = nullptr, *fb_dev = nullptr;  // mapped pinned block (host / device address), written by k_publish
   std::vector<int64_t> sig;                // what the captured graph depends on
 };
 
@@ -1077,6 +1077,11 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   }
   CK(h, launch_k5c_grid(R.max_deg, h->dcfg.p, h->arena.p, h->G.p, h->bwp.p, h->win.p, L, h->cap, rec, h->st));
   if (R.max_deg > 0) h->launches++;
+  // the results into the mapped host block (uniap_fetch: one sync, no copies)
+  auto* fd = h->fb_dev;
+  CK(h, launch_publish(reinterpret_cast<int32_t*>(&fd->rec), rec, fd->qg, h->level2 ? h->qglob.p : nullptr, fd->tm,
+                       h->tim.p, fd->cfgopt, h->cfgopt.p, h->ncfg, h->st));
+  h->launches++;
   return UNIAP_OK;
 }
 
@@ -1092,6 +1097,10 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
     rec = h->rec.p;
   }
   h->last_rec = rec;
+  if (!h->fb) {  // before any capture: the graph's k_publish writes here
+    CK(h, cudaHostAlloc((void**)&h->fb, sizeof(*h->fb), cudaHostAllocMapped));
+    CK(h, cudaHostGetDevicePointer((void**)&h->fb_dev, h->fb, 0));
+  }
   if (!h->plan.valid || h->plan.rank != rank || h->plan.world != world || h->plan.rec != rec) {
     if (h->graph_exec) { cudaGraphExecDestroy(h->graph_exec); h->graph_exec = nullptr; }
     uniap_status s = make_plan(h, rank, world, rec);
@@ -1144,15 +1153,13 @@ extern "C" uniap_status uniap_fetch(uniap_handle* h, uniap_result* out) {
   CK(h, cudaSetDevice(h->device));
   const uniap_record* src = h->last_rec;
   if (!src) FAIL(h, UNIAP_ERR_ARG, "nothing has run on this handle");
-  // every read of the fetch: async copies into pinned memory, one sync
-  if (!h->fb) CK(h, cudaMallocHost((void**)&h->fb, sizeof(*h->fb)));
+  // every result of the run is already on its way into the mapped block
+  // (k_publish, the last kernel of the run): one sync, no copies
+  (void)src;
   auto* fb = h->fb;
   int64_t* keep = out->cfg_objective;
-  CK(h, d2h(h, &fb->rec, src, sizeof fb->rec));
-  if (h->level2) CK(h, d2h(h, fb->qg, h->qglob.p, 16));
-  if (h->timed && h->tim.p) CK(h, cudaMemcpyAsync(fb->tm, h->tim.p, 16, cudaMemcpyDeviceToHost, h->st));
-  if (keep) CK(h, d2h(h, fb->cfgopt, h->cfgopt.p, h->ncfg * 8));
   CK(h, cudaStreamSynchronize(h->st));
+  h->d2h += sizeof fb->rec + (h->level2 ? 16 : 0) + (keep ? h->ncfg * 8 : 0);  // device -> host bytes
   const uniap_record& R = fb->rec;
   h->quantum = h->level2 ? fb->qg[0] : 0;
   if (h->timed) {

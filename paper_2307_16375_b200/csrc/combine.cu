@@ -26,6 +26,31 @@ __global__ void k_fill(int32_t* p, int64_t n, int32_t v) {
     p[i] = v;
 }
 
+// Publish: copy the run's results (record, builder flags, phase clock,
+// per-config optima) into the handle's mapped pinned host block with plain
+// (zero-copy) stores, so a fetch is one stream sync and no DMA round trips.
+__global__ void k_publish(int32_t* __restrict__ d_rec, const int32_t* __restrict__ rec, int rec_words,
+                          int64_t* __restrict__ d_qg, const int64_t* __restrict__ qg,
+                          unsigned long long* __restrict__ d_tm, const unsigned long long* __restrict__ tm,
+                          int64_t* __restrict__ d_cfg, const int64_t* __restrict__ cfgopt, int ncfg) {
+  const int t = threadIdx.x;
+  for (int i = t; i < rec_words; i += blockDim.x) d_rec[i] = rec[i];
+  if (t < 2) {
+    d_qg[t] = qg ? qg[t] : 0;
+    d_tm[t] = tm ? tm[t] : 0ull;
+  }
+  for (int i = t; i < ncfg; i += blockDim.x) d_cfg[i] = cfgopt[i];
+}
+
+cudaError_t launch_publish(int32_t* d_rec, const uniap_record* rec, int64_t* d_qg, const int64_t* qg,
+                           unsigned long long* d_tm, const unsigned long long* tm, int64_t* d_cfg,
+                           const int64_t* cfgopt, int ncfg, cudaStream_t st) {
+  static_assert(sizeof(uniap_record) % 4 == 0, "record words");
+  k_publish<<<1, 256, 0, st>>>(d_rec, reinterpret_cast<const int32_t*>(rec), (int)(sizeof(uniap_record) / 4), d_qg,
+                               qg, d_tm, tm, d_cfg, cfgopt, ncfg);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);

@@ -166,6 +166,9 @@ struct RecordArgs {          // what K5a writes into the record besides the winn
 
 // combine.cu
 cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st);
+cudaError_t launch_publish(int32_t* d_rec, const uniap_record* rec, int64_t* d_qg, const int64_t* qg,
+                           unsigned long long* d_tm, const unsigned long long* tm, int64_t* d_cfg,
+                           const int64_t* cfgopt, int ncfg, cudaStream_t st);
 // K3 (theta candidates) is fused into K4.
 cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int li0,
                       int n_local, int L, int32_t* thetas, int32_t* ntheta, int64_t* vals,
