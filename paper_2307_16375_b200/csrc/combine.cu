@@ -397,6 +397,7 @@ cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P,
 // (= lexicographically smallest stage_of, reading A-11).  One CTA.
 // ---------------------------------------------------------------------------
 constexpr int K5T = 1024;
+constexpr int K5A_DYN = (MAXL + 1) * (MAXL + 1) * 4;  // K5a's shared suffix table (dynamic: static is near 48 KB)
 __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
                                                   const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
                                                   int n_local, int L, const int32_t* __restrict__ thetas,
@@ -493,7 +494,75 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
   int32_t* mine = ends[w];
   int32_t best_end[MAXL];
   bool have = false;
-  for (int base = 0; base < ns; base += 32) {
+  // Few theta* (the usual case: one): the whole CTA per theta, H in shared
+  // memory -- stages sequential (one barrier each), warps over the start a,
+  // lanes over the end b with a warp min.  Many: one warp per theta below.
+  constexpr int HP = MAXL + 1;
+  extern __shared__ int32_t sH[];  // dynamic, K5A_DYN bytes: [i][a], i = 1..deg, a = 0..L
+  for (int si = 0; si < ns && ns <= 4; ++si) {
+    const int32_t theta = stars[si] < 0 ? INF : th[stars[si]];
+    const int64_t F_target = stars[si] < 0 ? OPT : OPT - (int64_t)(cf.c - 1) * theta;
+    for (int a = t; a <= L; a += K5T) {
+      int32_t v = INF;
+      if (a < L) { const int32_t p = sP[a * PP + L - 1]; v = p <= theta ? p : INF; }
+      sH[deg * HP + a] = v;
+    }
+    __syncthreads();
+    for (int i = deg - 1; i >= 1; --i) {
+      // H_i[a] = min_b P[a][b] + O[b] + H_{i+1}[b+1], b <= L-1-(deg-i)
+      const int bhi = L - 1 - (deg - i);
+      for (int a = w; a <= L; a += K5T / 32) {
+        uint32_t v = INF;
+        for (int b = a + lane; b <= bhi && a < L; b += 32) {
+          const int32_t p = sP[a * PP + b], o = sO[b], hh = sH[(i + 1) * HP + b + 1];
+          if (p <= theta && o <= theta && hh < INF) v = min(v, (uint32_t)p + (uint32_t)o + (uint32_t)hh);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, off));
+        if (lane == 0) sH[i * HP + a] = (int32_t)min(v, (uint32_t)INF);
+      }
+      __syncthreads();
+    }
+    bool ok = (int64_t)sH[1 * HP + 0] == F_target;
+    if (w == 0) {  // greedy: the largest feasible end of each stage
+      int64_t pre = 0;
+      int a = 0;
+      for (int i = 1; i < deg && ok; ++i) {
+        int found = -1;
+        for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
+          const int b = b0 - lane;
+          bool c = false;
+          if (b >= a) {
+            const int32_t p = sP[a * PP + b], o = sO[b], hh = sH[(i + 1) * HP + b + 1];
+            c = p <= theta && o <= theta && hh < INF && pre + p + o + hh == F_target;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, c);
+          if (m) found = b0 - (__ffs(m) - 1);
+        }
+        if (found < 0) { ok = false; break; }
+        if (lane == 0) ends[0][i - 1] = found;
+        pre += sP[a * PP + found] + sO[found];
+        a = found + 1;
+      }
+      if (lane == 0) {
+        ends[0][deg - 1] = L - 1;
+        okw[0] = ok;
+      }
+    }
+    __syncthreads();
+    if (t == 0 && okw[0]) {  // lexicographically largest end vector over theta*
+      bool better = !have;
+      for (int i = 0; i < deg && !better; ++i) {
+        if (ends[0][i] != best_end[i]) { better = ends[0][i] > best_end[i]; break; }
+      }
+      if (better) {
+        for (int i = 0; i < deg; ++i) best_end[i] = ends[0][i];
+        have = true;
+      }
+    }
+    __syncthreads();
+  }
+  for (int base = 0; base < ns && ns > 4; base += 32) {
     const int si = base + w;
     bool ok = false;
     if (si < ns) {
@@ -625,7 +694,8 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
 cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
                        int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals, const int64_t* cfg_opt,
                        int32_t* scratch, Winner* win, const RecordArgs& ra, cudaStream_t st) {
-  k5a_winner<<<1, K5T, 0, st>>>(cfg, arena, P, cfg_list, n_local, L, thetas, ntheta, vals, cfg_opt, scratch, win, ra);
+  k5a_winner<<<1, K5T, K5A_DYN, st>>>(cfg, arena, P, cfg_list, n_local, L, thetas, ntheta, vals, cfg_opt, scratch,
+                                      win, ra);
   return cudaGetLastError();
 }
 
@@ -734,7 +804,7 @@ cudaError_t combine_init() {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
   }
-  return cudaSuccess;
+  return cudaFuncSetAttribute((const void*)k5a_winner, cudaFuncAttributeMaxDynamicSharedMemorySize, K5A_DYN);
 }
 
 }  // namespace uniap
