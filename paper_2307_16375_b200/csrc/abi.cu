@@ -375,8 +375,11 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     plan_fast(L, i, deg[i], S[i], skipc[i], v);
     static const int nsingle = getenv("UNIAP_K2_SINGLE_N") ? atoi(getenv("UNIAP_K2_SINGLE_N")) : 1;
     const bool single = !v.empty() && (deg[i] == 1 || (int)v.size() <= nsingle);
+    static const int nfew = getenv("UNIAP_K2_FEW_N") ? atoi(getenv("UNIAP_K2_FEW_N")) : 4;
+    const bool few = !v.empty() && (int)v.size() <= nfew;  // deg = 2 (prefix + suffix): keep clusters
     K2Class k;
-    if (!k2_pick_class(S[i], h->Q, single, &k)) FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
+    if (!k2_pick_class(S[i], h->Q, single, &k, few))
+      FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
     h->cls[i] = k;
     if (!k2_pick_class(S[i], h->Q, true, &h->bcls[i]) || h->bcls[i].NS != k.NS)
       FAIL(h, UNIAP_ERR_ARG, "no traceback class for |S|=%d Q=%d", S[i], h->Q);

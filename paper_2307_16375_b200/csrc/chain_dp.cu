@@ -63,7 +63,7 @@ static void seg_class(K2Class* c) {
   }
 }
 
-bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
+bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few) {
   const int NS = k2_ns_round(S);
   if (NS < 0 || Q < 1 || Q > UNIAP_MAX_Q) return false;
   const size_t lim = 200 * 1024;
@@ -98,7 +98,7 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out) {
   // layer instead of DSMEM and cluster barriers) when the whole bucket range
   // fits one CTA: |S| <= 10 up to 4096 buckets, <= 24 up to 2048, 32 up to 1024.
   static const int sb_ok = env_int("UNIAP_K2_SB", 1);
-  if (C > 1 && !single && sb_ok) {
+  if (C > 1 && !single && !few && sb_ok) {
     const int Bs = std::max(32, pow2ceil(Q));
     const bool shape = (Bs == 4096 && NS > 6 && NS <= 10) || (Bs == 2048 && NS > 12 && NS <= 24) ||
                        (Bs == 1024 && NS > 24);
@@ -136,9 +136,9 @@ static k2_fn k2_lookup(const K2Class& c) {
 int k2_selftest(int* S_out, int* Q_out, int* single_out) {
   for (int S = 1; S <= UNIAP_MAX_STRAT; ++S)
     for (int Q = 1; Q <= UNIAP_MAX_Q; Q += (Q < 64 ? 1 : Q < 1100 ? 7 : 61))
-      for (int single = 0; single < 2; ++single) {
+      for (int single = 0; single < 3; ++single) {  // 2: few sweeps
         K2Class c;
-        if (!k2_pick_class(S, Q, single, &c) || !k2_lookup(c)) {
+        if (!k2_pick_class(S, Q, single == 1, &c, single == 2) || !k2_lookup(c)) {
           *S_out = S;
           *Q_out = Q;
           *single_out = single;
@@ -147,9 +147,9 @@ int k2_selftest(int* S_out, int* Q_out, int* single_out) {
       }
   for (int S = 1; S <= UNIAP_MAX_STRAT; ++S)
     for (int Q : {2048, 4096, 8192})
-      for (int single = 0; single < 2; ++single) {
+      for (int single = 0; single < 3; ++single) {  // 2: few sweeps
         K2Class c;
-        if (!k2_pick_class(S, Q, single, &c) || !k2_lookup(c)) {
+        if (!k2_pick_class(S, Q, single == 1, &c, single == 2) || !k2_lookup(c)) {
           *S_out = S;
           *Q_out = Q;
           *single_out = single;

@@ -128,7 +128,10 @@ struct K2Class {
 // chain_dp.cu
 // single = the config has one long chain (deg = 1): spread its buckets over
 // more SMs (a wider cluster) to shorten the critical path.
-bool k2_pick_class(int S, int Q, bool single, K2Class* out);
+// few = the config has only a few sweeps (deg = 2: prefix + suffix): each is
+// a critical path, so a bucket range that needs a cluster keeps it rather
+// than folding into one single-buffered CTA (which halves the SMs per sweep).
+bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few = false);
 int k2_ns_round(int S);
 size_t k2_smem_bytes(const K2Class& c);
 // priority: launch priority (0 = default; lower = served first, see

@@ -59,6 +59,9 @@ for tag, v in sorted(by.items(), key=lambda kv: min(x[0] for x in kv[1])):
                us_per_layer=round(max((x[1] - x[0]) / max(x[3] - 1, 1) for x in v), 2))
     out.append(row)
     print(row)
+    if os.environ.get("K2_TRACE_TOP") and not tag >> 31:  # the longest CTAs: (n layers, us)
+        top = sorted(v, key=lambda x: x[0] - x[1])[:8]
+        print("   longest (n, us, start):", [(x[3], round(x[1] - x[0], 1), round(x[0], 1)) for x in top])
 # SM occupancy over time (10 us bins)
 end = max(r[2] for r in recs)
 nb = int((end - t00) / 1e4) + 1
