@@ -76,6 +76,22 @@ def test_interval_table_elementwise(h, orc, Q):
         assert np.array_equal(got[iu], want[iu]), (Q, S, skip)
 
 
+@pytest.mark.parametrize("L,S,Q", [(64, 32, 256), (4, 32, 8192), (64, 21, 64), (3, 24, 8192)])
+def test_maximum_sizes(h, orc, L, S, Q):
+    """The ABI's maxima (L = 64 layers, |S| = 32 strategies, Q = 8192
+    buckets: the widest cluster class) element by element, then the whole
+    solve over deg 1 / 2 / L."""
+    cands = [(1, 1), (2, 2), (L, 3)]
+    t = tables.large_random_tables(L * 1000 + S, L, [S, S, S], Q - 1, cands, skip_src=min(5, L - 3) if L >= 3 else -1,
+                                   mem_max=max(1, (2 * Q) // max(L // 2, 1)))
+    got = h.interval_table(t, 0).astype(np.int64)
+    want = orc.interval_table(t, 0)
+    want = np.where(want == (1 << 63) - 1, 0x40000000, want)
+    iu = np.triu_indices(L)
+    assert np.array_equal(got[iu], want[iu]), (L, S, Q)
+    _same(h.solve_tables(t), orc.solve_tables(t, n_threads=0), (L, S, Q))
+
+
 @pytest.mark.parametrize("dist", ["uniform", "ties"])
 def test_random_gpu_sized(h, orc, dist):
     """Several configs of mixed |S|, L = 24, Q = 1000 (ragged), skip edges."""
