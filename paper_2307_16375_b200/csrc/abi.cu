@@ -141,6 +141,10 @@ struct uniap_handle {
     int64_t cfgopt[UNIAP_MAX_CFG];
   }* fb = nullptr, *fb_dev = nullptr;  // mapped pinned block (host / device address), written by k_publish
   std::vector<int64_t> sig;                // what the captured graph depends on
+  // per (config, layer): min over the config's strategies of M (buckets,
+  // cap + 1 = none fits) -- the plan stops a forward sweep where the running
+  // sum exceeds cap (every later interval is infeasible, Eq. 5)
+  std::vector<int32_t> minM;
 };
 
 // A prepared problem keeps the launch plan and the captured graph when
@@ -155,6 +159,7 @@ static void update_signature(uniap_handle* h) {
                       (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C, (int64_t)k.DB, (int64_t)k.G})
       sg.push_back(x);
   }
+  for (int32_t m : h->minM) sg.push_back(m);  // the plan's sweep lengths depend on them
   if (h->level2) {
     const int64_t* c = reinterpret_cast<const int64_t*>(&h->cl);
     for (size_t i = 0; i < sizeof(ClusterDev) / 8; ++i) sg.push_back(c[i]);
@@ -468,6 +473,15 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
     }
     if (keep[i].empty()) keep[i].push_back(0);  // all forbidden: the config is infeasible
   }
+  h->minM.assign((size_t)h->ncfg * L, t->cap + 1);
+  for (int i = 0; i < h->ncfg; ++i) {
+    const uniap_config& x = t->cfg[i];
+    for (int u = 0; u < L; ++u) {
+      int32_t mn = t->cap + 1;
+      for (int k : keep[i]) mn = std::min(mn, x.M[u * x.n_strat + k]);
+      h->minM[(size_t)i * L + u] = mn;
+    }
+  }
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc);
   if (st != UNIAP_OK) return st;
   // pack the host tables into the device layout (pads: A 0, M cap+1, R 0)
@@ -603,6 +617,46 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   }
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc);
   if (st != UNIAP_OK) return st;
+  {
+    // A lower bound of the builder's memory term (Eq. 1 + activations + ctx,
+    // in buckets; reading A-8) per (layer, strategy), minimised per config:
+    // the plan trims sweeps with it, so a lower bound only trims less.  c b / r
+    // = B / r, so M depends on the stage size g and the strategy, not on c:
+    // evaluated once per distinct g, in double precision (floor of the
+    // quotient <= the builder's exact ceiling).
+    const int64_t cap = o->Q - 1;
+    const double inv_unit = 1.0 / (double)((cl->mem_bytes - cl->mem_reserve_bytes) / cap);
+    const double cdt = o->precision ? 8.0 : 4.0;
+    std::vector<int> gs;
+    std::vector<std::vector<int32_t>> mg;  // per distinct g: [u][catalogue k]
+    h->minM.assign((size_t)h->ncfg * L, (int32_t)cap + 1);
+    for (int i = 0; i < h->ncfg; ++i) {
+      int gi = 0;
+      while (gi < (int)gs.size() && gs[gi] != g[i]) ++gi;
+      const int32_t* tfd = h->cat[i].tfd;
+      if (gi == (int)gs.size()) {
+        gs.push_back(g[i]);
+        std::vector<int32_t> m((size_t)L * S[i]);
+        for (int u = 0; u < L; ++u)
+          for (int k = 0; k < S[i]; ++k) {
+            const int tt = tfd[3 * k], ff = tfd[3 * k + 1], r = ff * tfd[3 * k + 2];
+            int lt = 0;
+            while ((1 << lt) < tt) ++lt;
+            const double mem = cdt * (double)ps[u] / (tt * ff) + (double)(o->B / r) * (double)act[u * NT + lt] + (double)ctx[u];
+            const double q = mem * inv_unit;
+            m[(size_t)u * S[i] + k] = q >= (double)cap + 2.0 ? (int32_t)cap + 1 : std::max(0, (int32_t)q - 1);
+          }
+        mg.push_back(std::move(m));
+      }
+      const std::vector<int32_t>& m = mg[gi];
+      for (int u = 0; u < L; ++u) {  // keep[i]: the strategies with (B / c) mod (f d) = 0 (reading A-7)
+        const int32_t* row = m.data() + (size_t)u * S[i];
+        int32_t mn = (int32_t)cap + 1;
+        for (int k : keep[i]) mn = std::min(mn, row[k]);
+        h->minM[(size_t)i * L + u] = mn;
+      }
+    }
+  }
   h->cl = ClusterDev{cl->n_dev, cl->node_size, cl->ccoc_permille, o->B, o->precision, o->Q, NT, 0,
                      cl->mem_bytes, cl->mem_reserve_bytes, cl->bw_intra_Bps, cl->bw_inter_Bps, cl->p2p_Bps,
                      cl->lat_ns, o->quantum_ns};
@@ -713,8 +767,30 @@ static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>&
 
 static void forward_instances(const uniap_handle* h, int i, bool all_intervals, std::vector<Inst>& out) {
   const CfgDev& d = h->cfg[i];
+  const size_t first = out.size();
   if (all_intervals || env_flag("UNIAP_CANONICAL_PLAN")) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, out);
   else plan_fast(h->L, i, d.deg, d.S, d.skip, out);
+  // Stop each forward P sweep where it becomes infeasible: the memory sum of
+  // Eq. 5 over the layers swept is at least the running sum of the per-layer
+  // minima, so past the first layer where that exceeds cap every state is INF
+  // and the interval optima stay INF from the fill (exact).  The emitted
+  // range shrinks with it; G-storing sweeps (deg = 1's kept tables) run in full.
+  static const bool trim_ok = !env_flag("UNIAP_NO_TRIM");
+  if (all_intervals || !trim_ok || h->minM.empty()) return;
+  const int L = h->L;
+  for (size_t j = first; j < out.size(); ++j) {
+    Inst& x = out[j];
+    if (x.emit != 1 && x.emit != 2) continue;
+    int64_t sum = 0;
+    int n = 0;
+    for (; n < x.n; ++n) {
+      sum += h->minM[(size_t)i * L + x.a + x.dir * n];
+      if (sum > h->cap) break;
+    }
+    x.n = std::max(n, 1);
+    if (x.dir > 0) x.ehi = std::min(x.ehi, x.a + x.n - 1);
+    else x.elo = std::max(x.elo, x.a - x.n + 1);
+  }
 }
 
 // LPT over configs by executed chain-DP work (sum over the sweeps of n |S|^2 Q); ties

@@ -76,12 +76,13 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few) {
   int C = pow2ceil((Q + B - 1) / B);
   static const int single_ok = env_int("UNIAP_K2_SINGLE", 1);  // tuning knob (experiments)
   if (single && single_ok) {
-    // a config with few (long) sweeps: at least 256 buckets per CTA (4
-    // warps), the bucket axis over a cluster of up to 8 CTAs (measured on the
-    // bench workloads: C = 4 x 256 beats C = 8 x 128 at Q = 1024; at 4096,
-    // 16-CTA clusters starve the other classes, which need whole GPCs free)
+    // a deg = 1 config (one long chain, or its skip copies): at least 256
+    // buckets per CTA (4 warps), the bucket axis over a cluster of up to 16
+    // CTAs (measured on the bench workloads: C = 4 x 256 beats C = 8 x 128 at
+    // Q = 1024; at Q = 4096 the Llama chain takes 109 us at C = 16 x 256
+    // against 133 us at C = 8 x 512)
     static const int bs = env_int("UNIAP_K2_SINGLE_B", 256);  // tuning knob (experiments)
-    static const int cs = env_int("UNIAP_K2_SINGLE_C", 8);
+    static const int cs = env_int("UNIAP_K2_SINGLE_C", 16);
     B = std::min(B, std::max(32, bs));
     C = pow2ceil((Q + B - 1) / B);
     while (C > cs && B < Bmax) {
