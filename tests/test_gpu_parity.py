@@ -167,6 +167,31 @@ def test_builder_random_profiles(h, orc):
         _same(h.plan(p), orc.solve_tables(t), seed)
 
 
+@pytest.mark.parametrize("L,Q", [(None, None), (24, 1024), (40, 4096)])
+def test_plan_random_profiles(h, orc, L, Q):
+    """Level 2 end to end (GPU builder, plan-time sweep trim from the host
+    memory bound, solve) = the oracle's builder' + solve, on random profiles
+    whose memory often binds; out-of-range profiles fail with the same status."""
+    import paper_2307_16375_b200 as pkg
+    checked = 0
+    for seed in range({None: 40, 24: 12, 40: 6}[L]):
+        p = profiles.random_profile(1000 * (L or 1) + seed, L=L, Q=Q)
+        try:
+            want, _ = orc.plan(p)
+        except orc.OracleError as e:
+            with pytest.raises(pkg.UniapError) as ei:
+                h.plan(p)
+            assert ei.value.status == e.status
+            continue
+        got = h.plan(p)
+        for k in ("objective", "deg", "c", "quantum_ns", "cfg_objective"):
+            assert got[k] == want[k], (seed, k)
+        if want["objective"] != (1 << 63) - 1:
+            assert got["stage_of"] == want["stage_of"] and got["strategy_of"] == want["strategy_of"], seed
+        checked += 1
+    assert checked > 0
+
+
 def test_edge_cases(h, orc):
     # L = 1; deg = L; deg > L; cap = 0; everything infeasible
     for seed in range(40):
