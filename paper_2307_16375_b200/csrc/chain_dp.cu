@@ -116,6 +116,8 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few) {
   if (B == 32) { c.V = 1; c.T = 32; }
   if (B == 2048) { c.V = 4; c.T = 512; }
   if (B == 4096) { c.V = 8; c.T = 512; }
+  static const int sv1 = env_int("UNIAP_K2_SV1", 0);  // experiment: one bucket per thread for deg = 1 chains
+  if (single && sv1 && C > 1 && B >= 128 && B <= 512) { c.V = 1; c.T = B; }
   if (C == 1) seg_class(&c);
   *out = c;
   return true;

@@ -574,6 +574,9 @@ k2_fn k2_get(int V, int T, bool CL, bool DB, int G = 0) {
     return nullptr;                                                         \
   }
   if (V == 1 && T == 32) return CL ? nullptr : k2_chain<NS, 1, 32, false>;
+  UNIAP_SHAPE(1, 128)
+  UNIAP_SHAPE(1, 256)
+  UNIAP_SHAPE(1, 512)
   UNIAP_SHAPE(2, 32)
   UNIAP_SHAPE(2, 64)
   UNIAP_SHAPE(2, 128)

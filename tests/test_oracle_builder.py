@@ -137,3 +137,117 @@ def test_all_models_build_and_solve(orc):
         t, qn, buf = orc.build_tables(p)
         assert len(t["cfgs"]) == {"bert": 16, "vit": 29, "swin": 25, "llama": 31}[name]
         assert buf.dtype == np.int32
+
+
+# ---------------------------------------------------------------------------
+# Hand-derived pins of the builder' terms that the SPEC examples above do not
+# reach (all-gather, FSDP gathers, DP/FSDP gradient sync / c, TP collectives
+# with the CCOC overlap, and the intra- vs inter-node bandwidth choice).
+# Every expected integer below is worked out by hand in the docstring from
+# the formulas of DESIGN.md Sec. 2 (PAPER.md:44-46 TP all-reduce / FSDP
+# all-gather + reduce-scatter; PAPER.md:88 collective efficiency per device
+# subset; PAPER.md:95 time cost model; SPEC.md:146 ring all-reduce,
+# SPEC.md:156 p2p, SPEC.md:166 CCOC overlap), so a plausible misreading --
+# a wrong (G-1)/G, a wrong group stride, a missing / c, intra and inter
+# swapped, min and max swapped in the overlap -- changes one of them.
+# ---------------------------------------------------------------------------
+
+def _one_layer(n, B, fwd_by_t, ps, tpcomm, node, bw_intra, bw_inter, lat, ccoc, cand, quantum=100):
+    p = _profile(L=1, n=n, B=B, fwd=fwd_by_t, ps=ps, tpcomm=tpcomm, cand=cand, quantum=quantum,
+                 lat=lat, ccoc=ccoc, node=node, Q=8192, mem=1 << 40)
+    p["cluster"]["bw_intra_Bps"] = bw_intra
+    p["cluster"]["bw_inter_Bps"] = bw_inter
+    return p
+
+
+def test_allgather_ring_model(orc):
+    """Ring all-gather / reduce-scatter over G ranks moves (G-1)/G of V per
+    rank and pays G-1 hops: ag(V,G) = ceil((G-1) V 1e9 / (G bw)) + (G-1) lat.
+    V = 1e9 B, bw = 1e9 B/s, lat = 10 us: G=2 -> 0.5 s + 10 us = 500_010_000 ns;
+    G=4 -> 0.75 s + 30 us = 750_030_000 ns; G=1 -> 0.  Rounding is up:
+    V=1, G=3, bw=1e9, lat=0 -> ceil(2/3) = 1 ns.  (An all-reduce is twice
+    the same volume and hop count: 1_000_020_000 at G=2, which the SPEC
+    example pins at lat = 0.)"""
+    assert orc.allgather_ns(10 ** 9, 1, GB, 10_000) == 0
+    assert orc.allgather_ns(10 ** 9, 2, GB, 10_000) == 500_010_000
+    assert orc.allgather_ns(10 ** 9, 4, GB, 10_000) == 750_030_000
+    assert orc.allgather_ns(1, 3, GB, 0) == 1
+    assert orc.allreduce_ns(10 ** 9, 2, GB, 10_000) == 1_000_020_000
+
+
+def test_fsdp_and_gradient_sync_terms_by_hand(orc):
+    """One layer, n = 8 devices in one stage (cand (1,1): g = 8, b = B = 8,
+    c = 1), strategy (t,f,d) = (2,2,2): r = 4, bl = 2.  fwd[t=2] = 1e6 ns,
+    no TP traffic, ps = 4e9 B, lat = 1000 ns, bw_intra 1e11, bw_inter 1e10.
+      comp  = 3 * bl * fwd = 6_000_000                      (bp = 2 fp)
+      tpc   = 3 * ar(0, t=2) = 3 * 2 * 1 * 1000 = 6_000     (the TP all-reduces, PAPER.md:44,
+              pay their hop latency even with no volume; ccoc = 0: ov = 6_006_000)
+      ag(ceil(ps/t) = 2e9, f=2) at stride t = 2, span 4 <= node 8 -> intra:
+            = ceil(1 * 2e9 * 1e9 / (2 * 1e11)) + 1 * 1000 = 10_001_000
+      fsdp  = 2 * ag = 20_002_000                           (gathers in FP and BP, PAPER.md:46)
+      ar(ceil(ps/(t f)) = 1e9, d=2) at stride t f = 4, span 8 <= 8 -> intra:
+            = ceil(2 * 1 * 1e9 * 1e9 / (2 * 1e11)) + 2 * 1 * 1000 = 10_002_000
+      sync  = ar + ag (FSDP reduce-scatter) = 20_003_000
+      A     = ov + fsdp + ceil(sync / c) = 46_011_000 ns.
+    node_size = 4: the DP group now spans 8 > 4 devices -> inter (1e10):
+      ar = ceil(2e18 / 2e10) + 2000 = 100_002_000; the FSDP group (span 4)
+      and the TP group (span 2) stay intra:
+      A = 6_006_000 + 20_002_000 + 100_002_000 + 10_001_000 = 136_011_000.
+    c = 2 (cand (1,2), B = 16: b = 8, bl = 2 unchanged): the per-iteration
+    sync is divided by c (reading A-14): A = 6_006_000 + 20_002_000 +
+      ceil(20_003_000 / 2) = 36_009_500.
+    (The first draft of this derivation forgot the latency of the empty TP
+    all-reduce; the oracle's 46_011_000 exposed it.)
+    Memory (Eq. 1, FP32 c_dtype 4): ceil(4 * 4e9 / (t f = 4)) = 4e9 B."""
+    fwd = [2_000_000, 1_000_000, 600_000, 400_000]  # t = 1, 2, 4, 8
+    k = orc.catalogue(8).index((2, 2, 2))
+    # explicit quanta (every entry of the config must fit 2^22 quanta; the
+    # inter-node case has 700 ms entries) that divide the expected value
+    for node, B, cand, q, want in ((8, 8, [(1, 1)], 100, 46_011_000), (4, 8, [(1, 1)], 1000, 136_011_000),
+                                   (8, 16, [(1, 2)], 100, 36_009_500)):
+        p = _one_layer(8, B, fwd, 4 * 10 ** 9, 0, node, 10 ** 11, 10 ** 10, 1000, 0, cand, quantum=q)
+        t, qn, _ = orc.build_tables(p)
+        assert qn == q and want % q == 0
+        assert int(t["cfgs"][0]["A"][0, k]) == want // q, (node, B, cand)
+    # M in bytes: unit = (2^40 - 0) // 8191 B per bucket -> ceil(4e9 / unit)
+    unit = (1 << 40) // 8191
+    assert int(t["cfgs"][0]["M"][0, k]) == -(-4 * 10 ** 9 // unit)
+
+
+def test_pure_dp_sync_without_fsdp(orc):
+    """(t,f,d) = (1,1,8), same layer: no gathers; sync = ar(ps = 4e9, 8) at
+    stride 1, span 8 <= node 8 -> intra: ceil(2 * 7 * 4e9 * 1e9 / (8 * 1e11))
+    + 2 * 7 * 1000 = 70_000_000 + 14_000 = 70_014_000; bl = 1:
+    A = 3 * 2e6 + 70_014_000 = 76_014_000.  (t,f,d) = (1,8,1): no DP group;
+    fsdp = 2 ag(4e9, 8) = 2 (ceil(7 * 4e9 * 1e9 / 8e11) + 7000) = 70_014_000,
+    sync = ag = 35_007_000: A = 6e6 + 70_014_000 + 35_007_000 = 111_021_000."""
+    fwd = [2_000_000, 1_000_000, 600_000, 400_000]
+    p = _one_layer(8, 8, fwd, 4 * 10 ** 9, 0, 8, 10 ** 11, 10 ** 10, 1000, 0, [(1, 1)])
+    t, _, _ = orc.build_tables(p)
+    cat = orc.catalogue(8)
+    assert int(t["cfgs"][0]["A"][0, cat.index((1, 1, 8))]) == 76_014_000 // 100
+    assert int(t["cfgs"][0]["A"][0, cat.index((1, 8, 1))]) == 111_021_000 // 100
+
+
+def test_tp_collectives_with_ccoc_overlap(orc):
+    """TP all-reduces in FP and BP overlapped with computation
+    by the CCOC.  n = 8, cand (1,1), B = 8,
+    strategy (2,1,4): bl = 2, fwd[2] = 20_000 ns -> comp = 3 * 2 * 20_000 =
+    120_000; tpcomm = 1e6 B/sample -> ar(2e6, 2) at stride 1 (intra 1e11,
+    lat 0) = ceil(2 * 2e6 * 1e9 / 2e11) = 20_000; tpc = 3 * ar = 60_000 (one
+    all-reduce in FP, two in BP); ps = 0 -> no sync, no gathers.
+      ccoc = 0    -> 120_000 + 60_000 = 180_000
+      ccoc = 500  -> 180_000 - floor(500 * min(120_000, 60_000) / 1000) = 150_000
+      ccoc = 1000 -> 180_000 - 60_000 = 120_000 = max(comp, tpc)."""
+    fwd = [40_000, 20_000, 12_000, 8_000]
+    k = orc.catalogue(8).index((2, 1, 4))
+    for ccoc, want in ((0, 180_000), (500, 150_000), (1000, 120_000)):
+        p = _one_layer(8, 8, fwd, 0, 10 ** 6, 8, 10 ** 11, 10 ** 10, 0, ccoc, [(1, 1)], quantum=1)
+        t, _, _ = orc.build_tables(p)
+        assert int(t["cfgs"][0]["A"][0, k]) == want, ccoc
+    # the TP group never spans nodes here (stride 1); with node_size = 1 it
+    # does: ar = ceil(2 * 2e6 * 1e9 / (2 * 1e10)) = 200_000, tpc = 600_000,
+    # ccoc 500: 120_000 + 600_000 - 60_000 = 660_000
+    p = _one_layer(8, 8, fwd, 0, 10 ** 6, 1, 10 ** 11, 10 ** 10, 0, 500, [(1, 1)], quantum=2)
+    t, _, _ = orc.build_tables(p)
+    assert int(t["cfgs"][0]["A"][0, k]) == 660_000 // 2
