@@ -13,8 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# UNIAP_LIB: another build of the same library (A/B experiments only; tools/gpu_ab.sh)
-LIB_PATH = os.environ.get("UNIAP_LIB") or os.path.join(HERE, "libuniap.so")
+LIB_PATH = os.path.join(HERE, "libuniap.so")
 INT64_MAX = (1 << 63) - 1
 MAX_L = 64
 

@@ -47,11 +47,6 @@ struct DevBuf {
 
 int round4(int x) { return (x + 3) & ~3; }
 
-int k2_flags() {
-  static const int f = getenv("UNIAP_K2_FLAGS") ? atoi(getenv("UNIAP_K2_FLAGS")) : 0;
-  return f;
-}
-
 bool env_flag(const char* name) {
   const char* v = getenv(name);
   return v && *v && *v != '0';
@@ -105,6 +100,8 @@ struct uniap_handle {
   View<CatDev> dcat;
   DevBuf<CfgDev> dcfg1;  // level 1: the config array (the arena is its own buffer)
   DevBuf<Inst> inst, binst;
+  DevBuf<Inst> iinst;                      // uniap_interval_table's own instance list (not in any graph)
+  DevBuf<int32_t> iP;                      // uniap_interval_table's own P block
   DevBuf<Winner> win;
   DevBuf<uniap_record> rec;
   // last run
@@ -156,7 +153,7 @@ static void update_signature(uniap_handle* h) {
     const CfgDev& d = h->cfg[i];
     const K2Class& k = h->cls[i];
     for (int64_t x : {(int64_t)d.deg, (int64_t)d.c, (int64_t)d.S, (int64_t)d.NSP, (int64_t)d.skip, d.offA, d.offP,
-                      (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C, (int64_t)k.DB, (int64_t)k.G})
+                      (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C, (int64_t)k.DB})
       sg.push_back(x);
   }
   for (int32_t m : h->minM) sg.push_back(m);  // the plan's sweep lengths depend on them
@@ -303,12 +300,13 @@ extern "C" uniap_status uniap_create(uniap_handle** out, int device, void* strea
   if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return UNIAP_ERR_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return UNIAP_ERR_CUDA;
   {
+    // kernel attributes are per device: set them once for every device used
     static std::mutex mu;
-    static bool done = false;
+    static std::vector<int> done;
     std::lock_guard<std::mutex> g(mu);
-    if (!done) {
+    if (std::find(done.begin(), done.end(), device) == done.end()) {
       if (combine_init() != cudaSuccess || builder_init() != cudaSuccess) return UNIAP_ERR_CUDA;
-      done = true;
+      done.push_back(device);
     }
   }
   uniap_handle* h = new uniap_handle();
@@ -339,6 +337,8 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   h->bwp.release();
   h->inst.release();
   h->binst.release();
+  h->iinst.release();
+  h->iP.release();
   h->win.release();
   h->rec.release();
   for (auto e : h->ev)
@@ -378,10 +378,8 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     // sweeps the same treatment starves the many-sweep classes of SMs)
     std::vector<Inst> v;
     plan_fast(L, i, deg[i], S[i], skipc[i], v);
-    static const int nsingle = getenv("UNIAP_K2_SINGLE_N") ? atoi(getenv("UNIAP_K2_SINGLE_N")) : 1;
-    const bool single = !v.empty() && (deg[i] == 1 || (int)v.size() <= nsingle);
-    static const int nfew = getenv("UNIAP_K2_FEW_N") ? atoi(getenv("UNIAP_K2_FEW_N")) : 4;
-    const bool few = !v.empty() && (int)v.size() <= nfew;  // deg = 2 (prefix + suffix): keep clusters
+    const bool single = !v.empty() && (deg[i] == 1 || v.size() <= 1);
+    const bool few = !v.empty() && v.size() <= 4;  // deg = 2 (prefix + suffix): keep clusters
     K2Class k;
     if (!k2_pick_class(S[i], h->Q, single, &k, few))
       FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
@@ -768,15 +766,14 @@ static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>&
 static void forward_instances(const uniap_handle* h, int i, bool all_intervals, std::vector<Inst>& out) {
   const CfgDev& d = h->cfg[i];
   const size_t first = out.size();
-  if (all_intervals || env_flag("UNIAP_CANONICAL_PLAN")) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, out);
+  if (all_intervals) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, out);
   else plan_fast(h->L, i, d.deg, d.S, d.skip, out);
   // Stop each forward P sweep where it becomes infeasible: the memory sum of
   // Eq. 5 over the layers swept is at least the running sum of the per-layer
   // minima, so past the first layer where that exceeds cap every state is INF
   // and the interval optima stay INF from the fill (exact).  The emitted
   // range shrinks with it; G-storing sweeps (deg = 1's kept tables) run in full.
-  static const bool trim_ok = !env_flag("UNIAP_NO_TRIM");
-  if (all_intervals || !trim_ok || h->minM.empty()) return;
+  if (all_intervals || h->minM.empty()) return;
   const int L = h->L;
   for (size_t j = first; j < out.size(); ++j) {
     Inst& x = out[j];
@@ -866,7 +863,7 @@ extern "C" uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32
 // per-layer synchronisation) -- so it starts on free SMs.
 // ---------------------------------------------------------------------------
 
-static int class_key(const K2Class& k) { return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C + (k.DB ? 0 : 50000) + k.G * 10000; }
+static int class_key(const K2Class& k) { return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C + (k.DB ? 0 : 50000); }
 
 static void group_instances(const uniap_handle* h, std::vector<Inst>& all, std::vector<K2Group>& grp) {
   std::vector<int> key(all.size());
@@ -898,10 +895,9 @@ static void group_instances(const uniap_handle* h, std::vector<Inst>& all, std::
   // Launch priorities: a cluster launch needs C free SMs of one GPC at once,
   // so once one-CTA classes hold the SMs it starves until they drain; cluster
   // classes therefore get the highest priority, then the longest critical
-  // paths (UNIAP_K2_PRIO=0 disables).
-  static const bool prio_ok = !getenv("UNIAP_K2_PRIO") || atoi(getenv("UNIAP_K2_PRIO")) != 0;
+  // paths.
   int least = 0, greatest = 0;
-  if (prio_ok && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess && greatest < least) {
+  if (cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess && greatest < least) {
     std::vector<size_t> ord(grp.size());
     std::iota(ord.begin(), ord.end(), 0);
     std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
@@ -947,13 +943,13 @@ static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp,
     const int n = dcount_per_class ? grp[g].max_inst : (int)(grp[g].e - grp[g].s);
     K2Args args{dcount_per_class ? dinst : dinst + grp[g].s,
                 dcount_per_class ? dcount_per_class + g : nullptr,
-                h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip, k2_flags()};
+                h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip};
     if (!dcount_per_class) args.tim = h->tim.p;  // forward launches: phase clock
     if (h->trace.p) {  // diagnostics: tag = class shape | forward/backward | group
       const K2Class& k = grp[g].cls;
       args.trace = h->trace.p;
       args.tag = (uint32_t)k.NS | (uint32_t)k.V << 6 | (uint32_t)(k.T / 32) << 10 | (uint32_t)k.C << 16 |
-                 (uint32_t)k.G << 21 | (uint32_t)k.DB << 24 | (uint32_t)(dcount_per_class ? 1 : 0) << 25 |
+                 (uint32_t)k.DB << 24 | (uint32_t)(dcount_per_class ? 1 : 0) << 25 |
                  (uint32_t)(g & 31) << 26;
     }
     CK(h, k2_launch(grp[g].cls, args, n, st, grp[g].priority));
@@ -989,6 +985,7 @@ static BuildBufs build_bufs(uniap_handle* h) {
 // ---------------------------------------------------------------------------
 static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_record* rec) {
   RunPlan& R = h->plan;
+  R.valid = false;  // set again only when every field and upload below succeeded
   std::vector<int> owner;
   lpt(h, world, owner);
   R.local.clear();
@@ -1313,15 +1310,18 @@ extern "C" uniap_status uniap_interval_table(uniap_handle* h, const uniap_tables
   uniap_status s = uniap_prepare_tables(h, t);
   if (s != UNIAP_OK) return s;
   if (cfg < 0 || cfg >= h->ncfg || !P_out) FAIL(h, UNIAP_ERR_ARG, "cfg index %d", cfg);
+  // Own buffers: the captured pipeline graph of the prepared tables bakes in
+  // the addresses of h->inst / h->P / h->G, so this call must not reallocate
+  // them (a later solve on the same tables replays that graph).  Only the
+  // emitted P entries are written (K2 does not store G for emit 1 / 2).
   const int L = h->L;
   std::vector<Inst> fw;
   forward_instances(h, cfg, true, fw);
-  CK(h, h->P.ensure((size_t)h->ncfg * L * L));
-  CK(h, h->G.ensure(1));
-  CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
-  s = launch_k2_groups(h, fw, h->inst, h->P.p);
+  CK(h, h->iP.ensure((size_t)h->ncfg * L * L));
+  CK(h, launch_fill(h->iP.p, (int64_t)h->ncfg * L * L, INF, h->st));
+  s = launch_k2_groups(h, fw, h->iinst, h->iP.p);
   if (s != UNIAP_OK) return s;
-  CK(h, d2h(h, P_out, h->P.p + h->cfg[cfg].offP, (size_t)L * L * 4));
+  CK(h, d2h(h, P_out, h->iP.p + h->cfg[cfg].offP, (size_t)L * L * 4));
   CK(h, cudaStreamSynchronize(h->st));
   CK(h, cudaGetLastError());
   return UNIAP_OK;

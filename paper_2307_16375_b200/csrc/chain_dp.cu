@@ -1,13 +1,14 @@
 // chain_dp.cu -- K2 class selection and launch (see chain_dp.cuh for the kernel).
-#include <cstdlib>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "chain_dp.cuh"
 
 namespace uniap {
 
 #define UNIAP_NS_LIST(X) X(1) X(2) X(3) X(4) X(6) X(8) X(10) X(12) X(15) X(16) X(21) X(24) X(32)
-#define UNIAP_EXTERN(N) extern template k2_fn k2_get<N>(int, int, bool, bool, int);
+#define UNIAP_EXTERN(N) extern template k2_fn k2_get<N>(int, int, bool, bool);
 UNIAP_NS_LIST(UNIAP_EXTERN)
 #undef UNIAP_EXTERN
 
@@ -37,53 +38,27 @@ static int pow2ceil(int x) {
 // thread for B = 2048 / 4096) with E double-buffered in shared memory: B is
 // the largest span whose E fits 200 KB, so a cluster (DSMEM for the shifted
 // reads, one cluster barrier per layer) is used only when Q exceeds it.
-// A single long chain (deg = 1) is spread over a cluster of up to 8 CTAs
-// with B >= 128, even when it would fit one CTA: its critical
-// path is serial in the layers, so more SMs per layer shorten it.
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
-
-// One CTA per instance: the segmented schedule (chain_dp.cuh) overlaps the
-// shifted shared-memory reads with the E-step.  2 bucket slots per segment;
-// G = 2 needs the double-buffered E, G >= 3 works with a single buffer.
-// Measured slower than the phase-separated schedule on B200 (the R rows are
-// re-read per segment): off unless UNIAP_K2_SEG=1 (experiments).
-static void seg_class(K2Class* c) {
-  static const int seg_ok = env_int("UNIAP_K2_SEG", 0);
-  if (!seg_ok) return;
-  if (c->V == 8 && c->T == 512 && c->NS <= 10) {  // 4 segments, one E buffer
-    c->DB = false;
-    c->G = 4;
-  } else if (c->V == 4 && c->DB && c->NS <= (c->T == 512 ? 12 : 16)) {
-    c->G = 2;
-  } else if (c->V == 4 && c->T == 512 && !c->DB && c->NS > 12 && c->NS <= 24) {
-    c->G = 4;
-  }
-}
-
+// A single long chain (deg = 1) is spread over a cluster of up to 16 CTAs
+// with B >= 256, even when it would fit one CTA: its critical path is serial
+// in the layers, so more SMs per layer shorten it.
 bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few) {
   const int NS = k2_ns_round(S);
   if (NS < 0 || Q < 1 || Q > UNIAP_MAX_Q) return false;
   const size_t lim = 200 * 1024;
-  static const int cap_b = env_int("UNIAP_K2_BMAX", 4096);  // tuning knob (experiments)
   int Bmax = 32;
-  for (int B : {64, 128, 256, 512, 1024}) if (B <= cap_b && smem_words(NS, B) * 4 <= lim) Bmax = B;
-  if (NS <= 12 && 2048 <= cap_b && smem_words(NS, 2048) * 4 <= lim) Bmax = 2048;
-  if (NS <= 6 && 4096 <= cap_b && smem_words(NS, 4096) * 4 <= lim) Bmax = 4096;
+  for (int B : {64, 128, 256, 512, 1024}) if (smem_words(NS, B) * 4 <= lim) Bmax = B;
+  if (NS <= 12 && smem_words(NS, 2048) * 4 <= lim) Bmax = 2048;
+  if (NS <= 6 && smem_words(NS, 4096) * 4 <= lim) Bmax = 4096;
   int B = std::min(Bmax, std::max(32, pow2ceil(Q)));
   int C = pow2ceil((Q + B - 1) / B);
-  static const int single_ok = env_int("UNIAP_K2_SINGLE", 1);  // tuning knob (experiments)
-  if (single && single_ok) {
+  if (single) {
     // a deg = 1 config (one long chain, or its skip copies): at least 256
     // buckets per CTA (4 warps), the bucket axis over a cluster of up to 16
     // CTAs (measured on the bench workloads: C = 4 x 256 beats C = 8 x 128 at
     // Q = 1024; at Q = 4096 the Llama chain takes 109 us at C = 16 x 256
     // against 133 us at C = 8 x 512)
-    static const int bs = env_int("UNIAP_K2_SINGLE_B", 256);  // tuning knob (experiments)
-    static const int cs = env_int("UNIAP_K2_SINGLE_C", 16);
-    B = std::min(B, std::max(32, bs));
+    constexpr int bs = 256, cs = 16;
+    B = std::min(B, bs);
     C = pow2ceil((Q + B - 1) / B);
     while (C > cs && B < Bmax) {
       B *= 2;
@@ -98,27 +73,20 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few) {
   // A cluster is avoidable with a single-buffered E (two CTA barriers per
   // layer instead of DSMEM and cluster barriers) when the whole bucket range
   // fits one CTA: |S| <= 10 up to 4096 buckets, <= 24 up to 2048, 32 up to 1024.
-  static const int sb_ok = env_int("UNIAP_K2_SB", 1);
-  if (C > 1 && !single && !few && sb_ok) {
+  if (C > 1 && !single && !few) {
     const int Bs = std::max(32, pow2ceil(Q));
     const bool shape = (Bs == 4096 && NS > 6 && NS <= 10) || (Bs == 2048 && NS > 12 && NS <= 24) ||
                        (Bs == 1024 && NS > 24);
     if (shape && smem_words(NS, Bs, 1) * 4 <= lim) {
-      K2Class c{NS, Bs / 512, 512, 1, false};
-      seg_class(&c);
-      *out = c;
+      *out = K2Class{NS, Bs / 512, 512, 1, false};
       return true;
     }
   }
-  static const int pref_v = env_int("UNIAP_K2_V", 0);
   K2Class c{NS, 2, B / 2, C, true};
-  if (B == 1024 && NS <= 16 && (pref_v == 4 || (pref_v == 0 && C == 1))) { c.V = 4; c.T = 256; }
+  if (B == 1024 && NS <= 16 && C == 1) { c.V = 4; c.T = 256; }
   if (B == 32) { c.V = 1; c.T = 32; }
   if (B == 2048) { c.V = 4; c.T = 512; }
   if (B == 4096) { c.V = 8; c.T = 512; }
-  static const int sv1 = env_int("UNIAP_K2_SV1", 0);  // experiment: one bucket per thread for deg = 1 chains
-  if (single && sv1 && C > 1 && B >= 128 && B <= 512) { c.V = 1; c.T = B; }
-  if (C == 1) seg_class(&c);
   *out = c;
   return true;
 }
@@ -127,7 +95,7 @@ static k2_fn k2_lookup(const K2Class& c) {
   const bool CL = c.C > 1;
   switch (c.NS) {
 #define UNIAP_CASE(N) \
-  case N: return k2_get<N>(c.V, c.T, CL, c.DB, c.G);
+  case N: return k2_get<N>(c.V, c.T, CL, c.DB);
     UNIAP_NS_LIST(UNIAP_CASE)
 #undef UNIAP_CASE
     default: return nullptr;
@@ -198,7 +166,7 @@ __global__ void k2_closed_s1(const K2Args args, int n_inst) {
 
 cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st, int priority) {
   if (n_inst <= 0) return cudaSuccess;
-  if (c.NS == 1 && !args.n_inst && !getenv("UNIAP_NO_CLOSED_S1")) {  // forward |S| = 1 sweeps: closed form
+  if (c.NS == 1 && !args.n_inst) {  // forward |S| = 1 sweeps: closed form
     k2_closed_s1<<<n_inst, 32, 0, st>>>(args, n_inst);
     return cudaGetLastError();
   }
@@ -206,12 +174,16 @@ cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStre
   if (!fn) return cudaErrorInvalidDeviceFunction;
   const size_t smem = k2_smem_bytes(c);
   {
-    // raise the dynamic shared-memory limit (and allow 16-CTA clusters) once per kernel
+    // raise the dynamic shared-memory limit (and allow 16-CTA clusters) once
+    // per (device, kernel): function attributes are per device
     static std::mutex mu;
-    static std::vector<k2_fn> done;
+    static std::vector<std::pair<int, k2_fn>> done;
+    int dev = 0;
+    cudaError_t de = cudaGetDevice(&dev);
+    if (de != cudaSuccess) return de;
     std::lock_guard<std::mutex> g(mu);
     bool seen = false;
-    for (auto f : done) seen |= (f == fn);
+    for (auto& f : done) seen |= (f.first == dev && f.second == fn);
     if (!seen) {
       cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       if (e != cudaSuccess) return e;
@@ -219,7 +191,7 @@ cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStre
       if (e != cudaSuccess) return e;
       e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       if (e != cudaSuccess) return e;
-      done.push_back(fn);
+      done.push_back({dev, fn});
     }
   }
   cudaLaunchConfig_t cfg = {};

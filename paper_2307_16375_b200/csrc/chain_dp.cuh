@@ -114,10 +114,9 @@ struct Stage {
   static constexpr int WORDS = NS * NSP + 2 * NSP;
 };
 
-template <int NS, int V, int T, bool CL, bool DB = true, int G = 0>
+template <int NS, int V, int T, bool CL, bool DB = true>
 __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   static_assert(DB || !CL, "single-buffered E only without clusters");
-  static_assert(G == 0 || !CL, "segmented schedule only without clusters");
   constexpr int B = T * V;          // buckets per CTA
   constexpr int ROW = B + 4;        // 4 guard words + B buckets
   constexpr int NE = DB ? 2 : 1;    // E buffers (single: a second barrier per layer)
@@ -224,7 +223,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
         }
       }
     }
-    if (eG && !(args.flags & 8)) {
+    if (eG) {
       const int lo = in.a - in.n + 1;
       int32_t* g = args.G + in.gofs + (int64_t)(u - lo) * NSP * Q;
 #pragma unroll
@@ -258,151 +257,6 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   __syncthreads();
   emit(u);
 
-  if constexpr (G > 0) {
-    // ---- segmented schedule (one CTA per instance) -----------------------
-    // The bucket slots j are split into G segments of VS slots.  Phase g of
-    // a layer computes E of segment g (ALU) while the shifted reads of
-    // segment g-1 of the same layer (or of segment G-1 of the previous layer,
-    // for g = 0) are in flight (shared memory): a shift only reads lower
-    // buckets, so segment g-1's shift needs E of segments <= g-1, complete at
-    // the previous phase's barrier.  The per-layer shared-memory traffic thus
-    // overlaps the E-step inside each warp's instruction stream instead of
-    // forming a phase of its own.  With one E buffer (NE = 1, G >= 3) the
-    // only hazard is the deferred shift of segment G-1 reading segment 0 while
-    // phase 0 of the next layer overwrites it: possible only when a shift
-    // exceeds (G-2) segments; such a layer shifts segment G-1 at its end.
-    constexpr int VS = V / G;
-    constexpr int SEGB = VS * T;
-    static_assert(V % G == 0 && (NE == 2 || G >= 3), "segment shape");
-    auto shift_seg = [&](int g, const int32_t* Ebuf, const int32_t* Tst) {
-      const char* Ec = reinterpret_cast<const char*>(Ebuf);
-#pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const int mk = Tst[NS * NSP + 2 * k + 1];
-        const int32_t bk = (k * ROW + t - mk) * 4;
-        const int32_t gk = k * ROW * 4 - 4;
-#pragma unroll
-        for (int jj = 0; jj < VS; ++jj) {
-          const int j = g * VS + jj;
-          if (j > 0 && mk <= j * T)  // warp-uniform: the source is inside the row
-            d[k][j] = *reinterpret_cast<const int32_t*>(Ec + bk + j * T * 4);
-          else
-            d[k][j] = *reinterpret_cast<const int32_t*>(Ec + __viaddmax_s32(bk, j * T * 4, gk));
-        }
-      }
-    };
-    auto estep_seg = [&](int g, int32_t* Ebuf, const int32_t* Tst) {
-      int32_t* Et = Ebuf + t;
-      auto rows = [&](auto rrc, int k) {
-        constexpr int RR = decltype(rrc)::value;
-        int32_t acc[RR][VS];
-#pragma unroll
-        for (int r = 0; r < RR; ++r)
-#pragma unroll
-          for (int jj = 0; jj < VS; ++jj) acc[r][jj] = INF;
-#pragma unroll
-        for (int c = 0; c < NSP / 4; ++c) {
-          int4 x[RR];
-#pragma unroll
-          for (int r = 0; r < RR; ++r) x[r] = reinterpret_cast<const int4*>(Tst + (k + r) * NSP)[c];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (4 * c + i < NS)
-#pragma unroll
-              for (int r = 0; r < RR; ++r)
-#pragma unroll
-                for (int jj = 0; jj < VS; ++jj)
-                  acc[r][jj] = addmin(d[4 * c + i][g * VS + jj], comp(x[r], i), acc[r][jj]);
-        }
-#pragma unroll
-        for (int r = 0; r < RR; ++r)
-#pragma unroll
-          for (int jj = 0; jj < VS; ++jj) Et[(k + r) * ROW + (g * VS + jj) * T] = acc[r][jj];
-      };
-      constexpr int RR = 4;
-      constexpr int RRC = RR < NS ? RR : NS;
-      constexpr int NFULL = NS / RRC * RRC;
-      if constexpr (NS <= KUNROLL) {
-#pragma unroll
-        for (int k = 0; k < NFULL; k += RRC) rows(std::integral_constant<int, RRC>{}, k);
-      } else {
-#pragma unroll 1
-        for (int k = 0; k < NFULL; k += RRC) rows(std::integral_constant<int, RRC>{}, k);
-      }
-      if constexpr (NS - NFULL > 0) rows(std::integral_constant<int, NS - NFULL>{}, NFULL);
-    };
-    // stage optimum / backward table of layer uu for the slots of segment g
-    auto emit_seg = [&](int uu, int g) {
-      if (eP) {
-        const int jc = cap / T, tc = cap - jc * T;  // C = 1: cap < B
-        if (jc / VS == g && t == tc) {
-          int32_t v = INF;
-#pragma unroll
-          for (int jj = 0; jj < VS; ++jj)
-            if (g * VS + jj == jc)
-#pragma unroll
-              for (int k = 0; k < NS; ++k) v = min(v, d[k][g * VS + jj]);
-          sProw[uu] = v;
-        }
-      }
-      if (eG) {
-        const int lo = in.a - in.n + 1;
-        int32_t* gp = args.G + in.gofs + (int64_t)(uu - lo) * NSP * Q;
-#pragma unroll
-        for (int k = 0; k < NS; ++k)
-#pragma unroll
-          for (int jj = 0; jj < VS; ++jj) {
-            const int q = (g * VS + jj) * T + t;
-            if (q < Q) gp[(int64_t)k * Q + q] = d[k][g * VS + jj];
-          }
-      }
-    };
-    bool pend = false;  // the shift of segment G-1 of the previous layer
-    for (int step = 1; step < in.n; ++step) {
-      u += in.dir;
-      int32_t* Eb = sE + (NE == 2 ? (step & 1) * NS * ROW : 0) + 4;
-      const int32_t* Ep = sE + (NE == 2 ? ((step - 1) & 1) * NS * ROW : 0) + 4;
-      const int32_t* Tb = sT + (step % 3) * SW;
-      const int32_t* Tp = sT + ((step + 2) % 3) * SW;  // the previous layer's stage
-      static_for<0, G>([&](auto gc) {
-        constexpr int g = decltype(gc)::value;
-        if (g == 0) {
-          if (pend) shift_seg(G - 1, Ep, Tp);
-        } else {
-          shift_seg(g - 1, Eb, Tb);
-        }
-        estep_seg(g, Eb, Tb);
-        if (g == 0) {
-          if (pend) emit_seg(u - in.dir, G - 1);
-          if (step + 1 < in.n) store_stage(step + 1);
-          if (step + 2 < in.n) fetch_stage(step + 2, u + 2 * in.dir);
-        } else {
-          emit_seg(u, g - 1);
-        }
-        __syncthreads();
-      });
-      pend = true;
-      if constexpr (NE == 1) {
-        int32_t mmax = 0;
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          const int mk = Tb[NS * NSP + 2 * k + 1];
-          mmax = max(mmax, mk <= cap ? mk : 0);  // forbidden rows read only the guard
-        }
-        if (mmax > (G - 2) * SEGB) {
-          shift_seg(G - 1, Eb, Tb);
-          emit_seg(u, G - 1);
-          __syncthreads();
-          pend = false;
-        }
-      }
-    }
-    if (pend) {
-      const int step = in.n - 1;
-      shift_seg(G - 1, sE + (NE == 2 ? (step & 1) * NS * ROW : 0) + 4, sT + (step % 3) * SW);
-      emit_seg(u, G - 1);
-    }
-  } else
   for (int step = 1; step < in.n; ++step) {
     u += in.dir;
     int32_t* Eb = sE + (DB ? (step & 1) * NS * ROW : 0) + 4;  // row 0, bucket 0
@@ -454,10 +308,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     // table fetch (after the release, so its fence does not wait for it),
     // sync the CTA, shift from the local E while the other CTAs catch up,
     // then wait (acquire) before the few reads from a lower CTA's range.
-    if constexpr (CL) {
-      if (args.flags & 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-      else cl_arrive();
-    }
+    if constexpr (CL) cl_arrive();
     if (step + 2 < in.n) fetch_stage(step + 2, u + 2 * in.dir);
     __syncthreads();
     // ---- shift by the layer's memory, add A' ----
@@ -472,7 +323,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       if constexpr (CL) mmax = max(mmax, am.y <= cap ? am.y : 0);  // forbidden rows are all INF
       const int32_t bk = (k * ROW + t - am.y) * 4;  // byte offset of bucket t - M in row k
       const int32_t gk = k * ROW * 4 - 4;          // the row's guard word
-      if (V > 1 && am.y <= T && !(args.flags & 2)) {
+      if (V > 1 && am.y <= T) {
         // (warp-uniform) only j = 0 can fall below the row start: the other
         // buckets read at constant offsets from one clamped base
         const char* base = Ec + bk;
@@ -490,7 +341,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       // local read above returned the guard (INF); fetch the value over DSMEM
       const uint32_t tok = cl_wait_tok();
       const int wbase = t & ~31;
-      if (rank > 0 && wbase < mmax && mmax <= T && !(args.flags & 4)) {
+      if (rank > 0 && wbase < mmax && mmax <= T) {
         // common case (every shift <= T): only bucket j = 0 of threads t < M_k
         // needs a fix-up, and its source is bucket B + t - M_k of CTA rank-1:
         // one mapped base per layer, one predicated load per row
@@ -551,15 +402,7 @@ constexpr size_t k2_smem(int B, int ne = 2) {
 typedef void (*k2_fn)(const K2Args);
 
 template <int NS>
-k2_fn k2_get(int V, int T, bool CL, bool DB, int G = 0) {
-  if (G > 0) {  // segmented schedule, one CTA per instance
-    if (CL) return nullptr;
-    if constexpr (NS <= 10) if (V == 8 && T == 512 && !DB && G == 4) return k2_chain<NS, 8, 512, false, false, 4>;
-    if constexpr (NS <= 12) if (V == 4 && T == 512 && DB && G == 2) return k2_chain<NS, 4, 512, false, true, 2>;
-    if constexpr (NS > 12 && NS <= 24) if (V == 4 && T == 512 && !DB && G == 4) return k2_chain<NS, 4, 512, false, false, 4>;
-    if constexpr (NS <= 16) if (V == 4 && T == 256 && DB && G == 2) return k2_chain<NS, 4, 256, false, true, 2>;
-    return nullptr;
-  }
+k2_fn k2_get(int V, int T, bool CL, bool DB) {
   if (!DB) {  // single-buffered E, one CTA per instance (large B without a cluster)
     if (CL) return nullptr;
     if constexpr (NS > 24 && k2_smem<NS>(1024, 1) <= 200 * 1024) if (V == 2 && T == 512) return k2_chain<NS, 2, 512, false, false>;
@@ -574,9 +417,6 @@ k2_fn k2_get(int V, int T, bool CL, bool DB, int G = 0) {
     return nullptr;                                                         \
   }
   if (V == 1 && T == 32) return CL ? nullptr : k2_chain<NS, 1, 32, false>;
-  UNIAP_SHAPE(1, 128)
-  UNIAP_SHAPE(1, 256)
-  UNIAP_SHAPE(1, 512)
   UNIAP_SHAPE(2, 32)
   UNIAP_SHAPE(2, 64)
   UNIAP_SHAPE(2, 128)

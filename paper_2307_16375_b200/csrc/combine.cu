@@ -381,12 +381,6 @@ cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P,
                       int n_local, int L, int32_t* thetas, int32_t* ntheta, int64_t* vals, int64_t* cfg_opt,
                       cudaStream_t st) {
   if (n_local <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k4_vals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4Smem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
   k4_vals<<<n_local, K4W * 32, sizeof(K4Smem), st>>>(cfg, arena, P, cfg_list, li0, L, thetas, ntheta, vals, cfg_opt);
   return cudaGetLastError();
 }
@@ -797,6 +791,8 @@ cudaError_t launch_k5c_grid(int max_deg, const CfgDev* cfg, const int32_t* arena
 
 cudaError_t combine_trace(unsigned long long* p) { return cudaMemcpyToSymbol(g_trace, &p, sizeof p); }
 
+// Kernel attributes of this translation unit on the CURRENT device (function
+// attributes are per device; uniap_create calls this once per device).
 // Every kernel of the step prefers the maximum shared-memory carveout, as K2
 // needs it: no L1/shared reconfiguration between the kernels of the step.
 cudaError_t combine_init() {
@@ -804,6 +800,8 @@ cudaError_t combine_init() {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
   }
+  cudaError_t e = cudaFuncSetAttribute((const void*)k4_vals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4Smem));
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute((const void*)k5a_winner, cudaFuncAttributeMaxDynamicSharedMemorySize, K5A_DYN);
 }
 

@@ -64,8 +64,6 @@ struct K2Args {
   int32_t* P;
   int32_t* G;
   int32_t L, cap, skip;
-  int32_t flags;  // experiments only (UNIAP_K2_FLAGS): bit 0 = relaxed cluster arrive (NOT memory-model
-                  // safe), bit 1 = always clamp every shifted read
   // diagnostics (UNIAP_TRACE): per-CTA timeline records, or nullptr
   unsigned long long* trace = nullptr;
   uint32_t tag = 0;
@@ -112,7 +110,7 @@ struct TraceScope {  // one record per CTA, written by thread 0 when the kernel 
 };
 cudaError_t combine_trace(unsigned long long* p);
 cudaError_t builder_trace(unsigned long long* p);
-cudaError_t combine_init();  // kernel attributes (once per process)
+cudaError_t combine_init();  // kernel attributes on the current device (once per device)
 cudaError_t builder_init();
 
 // Kernel class: template shape of K2.
@@ -122,7 +120,6 @@ struct K2Class {
   int T;       // threads per CTA
   int C;       // CTAs per cluster
   bool DB;     // double-buffered E (one barrier per layer); single: two
-  int G = 0;   // > 0: segmented schedule with G bucket segments (C = 1)
 };
 
 // chain_dp.cu

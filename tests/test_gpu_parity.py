@@ -236,3 +236,20 @@ def test_world_size_invariance(h):
         for k in ("objective", "deg", "c", "cfg_index", "stage_of", "strategy_of", "stage_cost", "cut_cost",
                   "stage_mem", "dp_cells", "dp_relax", "dp_cells_canonical"):
             assert r[k] == ref[k], (world, k)
+
+
+def test_interval_table_between_solves_keeps_the_captured_plan(h, orc):
+    """solve -> interval_table -> solve on the SAME tables: the second solve
+    replays the captured graph of the first, so the all-intervals call must
+    not reallocate any buffer that graph uses."""
+    for seed, (L, S, Q) in enumerate([(12, 6, 300), (20, 10, 1025), (6, 3, 8192)]):
+        t = tables.large_random_tables(9000 + seed, L, [S, S], Q - 1, [(1, 1), (2, 2)], skip_src=2,
+                                       mem_max=max(1, (3 * Q) // L))
+        want = orc.solve_tables(t)
+        _same(h.solve_tables(t), want, ("first", seed))
+        P = h.interval_table(t, 1).astype(np.int64)
+        ref = orc.interval_table(t, 1)
+        ref = np.where(ref == (1 << 63) - 1, 0x40000000, ref)
+        iu = np.triu_indices(L)
+        assert np.array_equal(P[iu], ref[iu])
+        _same(h.solve_tables(t), want, ("second", seed))
