@@ -223,8 +223,13 @@ def toy_profile():
             "cluster": cluster, "options": dict(B=2, precision=0, Q=8, quantum_ns=0, cand=None)}
 
 
-def random_profile(seed, L=None, n=None, B=None, Q=None, skip=None):
-    """Random small profile for builder / end-to-end parity tests."""
+def random_profile(seed, L=None, n=None, B=None, Q=None, skip=None, mat_dim=None, space=0):
+    """Random small profile for builder / end-to-end parity tests.
+
+    ``mat_dim``: if given, about half of the edges carry a random resharding
+    matrix of that order (``reshard_ns_per_sample``, ns per sample in
+    [0, 2^20]; the caller passes |Cat| of the strategy space); ``space``: the
+    options' strategy space."""
     rng = np.random.default_rng(seed)
     L = int(rng.integers(1, 9)) if L is None else L
     n = int(rng.choice([1, 2, 4, 6, 8, 12, 16])) if n is None else n
@@ -253,6 +258,11 @@ def random_profile(seed, L=None, n=None, B=None, Q=None, skip=None):
                    bw_inter_Bps=int(rng.integers(1 << 27, 1 << 34)),
                    p2p_Bps=int(rng.integers(1 << 27, 1 << 36)),
                    lat_ns=int(rng.integers(0, 50_000)), ccoc_permille=int(rng.integers(0, 1001)))
-    opts = dict(B=B, precision=int(rng.integers(0, 2)), Q=Q, quantum_ns=0, cand=None)
+    if mat_dim:
+        mrng = np.random.default_rng(seed + 7_000_000)  # separate stream: the rest of the profile is unchanged
+        for e in edges:
+            if mrng.random() < 0.5:
+                e["reshard_ns_per_sample"] = mrng.integers(0, 1 << 20, size=(mat_dim, mat_dim), dtype=np.int64)
+    opts = dict(B=B, precision=int(rng.integers(0, 2)), Q=Q, quantum_ns=0, cand=None, strategy_space=space)
     return {"name": f"rand{seed}", "model": {"L": L, "layers": layers, "edges": edges},
             "cluster": cluster, "options": opts}

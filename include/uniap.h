@@ -136,7 +136,18 @@ typedef struct {
 typedef struct {
   int32_t src, dst;                   /* src < dst; dst == src+1 (chain) or a skip edge from
                                          the single skip source to dst >= src+2               */
-  int64_t tensor_bytes_per_sample;    /* activation bytes crossing the edge per sample         */
+  int64_t tensor_bytes_per_sample;    /* activation bytes crossing the edge per sample (the
+                                         cut cost o_j, Eq. 4 with a constant R', reading A-1)  */
+  const int64_t* reshard_ns_per_sample; /* NULL, or the edge's resharding matrix R_uv
+                                         (the quadratic term of Eq. 3) in ns per
+                                         sample, row-major [|Cat|][|Cat|]: row = the strategy of
+                                         src, column = the strategy of dst, both indices into
+                                         Cat = S(g) of every divisor g of n_dev in ascending
+                                         order, concatenated (uniap_catalogue order, the
+                                         options' strategy space).  A stage of g devices with
+                                         micro-batch b pays b * value.  Entries in [0, 2^46];
+                                         borrowed for the call.  NULL: the built-in resharding
+                                         formula (reading A-15)                              */
 } uniap_edge;
 
 typedef struct {
@@ -161,6 +172,9 @@ typedef struct {
   int64_t quantum_ns;                 /* 0 = auto (smallest feasible power of two, A-9)        */
   const int32_t* cand;                /* NULL = Algorithm 1's list; else n_cand (deg,c) pairs   */
   int32_t n_cand;
+  int32_t strategy_space;             /* 0 = every (t,f,d) triple (reading A-6); 1 = SPEC's
+                                         (dp, tp) pairs with an FSDP flag: the
+                                         triples with f = 1 or d = 1                            */
 } uniap_options;
 
 /* Algorithm 1 end to end: cost model on the GPU (K1), then the solve. */
@@ -215,9 +229,10 @@ uniap_status uniap_pick(const uniap_record* recs, int32_t world, uniap_result* o
  * Returns 0, or 1 with the first failing (S, Q, single-chain flag). */
 int32_t uniap_selftest(int32_t* S, int32_t* Q, int32_t* single);
 
-/* Candidate list of Algorithm 1 and the strategy catalogue (host only). */
+/* Candidate list of Algorithm 1 and the strategy catalogue S(g) of a
+ * strategy space (0 / 1, see uniap_options) as (t,f,d) triples (host only). */
 int32_t uniap_candidates(int32_t n, int32_t B, int32_t* pairs_out, int32_t cap);
-int32_t uniap_catalogue(int32_t g, int32_t* tfd_out, int32_t cap);
+int32_t uniap_catalogue(int32_t g, int32_t space, int32_t* tfd_out, int32_t cap);
 
 #ifdef __cplusplus
 }

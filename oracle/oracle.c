@@ -492,7 +492,7 @@ int orc_interval_table(const orc_tables* t, int cfg, int64_t* P) {
  * degree triple (t,f,d) with t*f*d = g, t a profiled TP size (power of two);
  * ordered t ascending then f ascending, so index 0 is pure DP, as in
  * Appendix D's S_{l0}.  Reading A-6. */
-int orc_catalogue(int32_t g, int32_t* tfd, int32_t cap) {
+int orc_catalogue(int32_t g, int32_t space, int32_t* tfd, int32_t cap) {
   int n = 0;
   if (g < 1) return 0;
   for (int t = 1; t <= g; t *= 2) {
@@ -500,6 +500,9 @@ int orc_catalogue(int32_t g, int32_t* tfd, int32_t cap) {
     for (int f = 1; f <= g / t; ++f) {
       if ((g / t) % f) continue;
       int d = g / t / f;
+      /* SPEC's space (StrategySpace): a (dp, tp) pair with the
+       * dp axis either plain DP (f = 1) or fully FSDP-sharded (d = 1) */
+      if (space == 1 && f != 1 && d != 1) continue;
       if (n < cap) { tfd[3 * n] = t; tfd[3 * n + 1] = f; tfd[3 * n + 2] = d; }
       ++n;
     }
@@ -570,6 +573,15 @@ static u128 t_reshard(const orc_cluster* cl, const int32_t* s1, const int32_t* s
   return 2 * t_allreduce(cl, V, G, 1);
 }
 
+/* Offset of S(g) in the concatenation of S(g') over the divisors g' of n in
+ * ascending order (g = n + 1: the total length |Cat|). */
+static int64_t cat_offset(int n, int g, int space) {
+  int64_t off = 0;
+  for (int x = 1; x < g && x <= n; ++x)
+    if (n % x == 0) off += orc_catalogue(x, space, NULL, 0);
+  return off;
+}
+
 int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, int32_t* buf,
               int64_t buf_len, int32_t* n_cfg_out, int32_t* skip_out, int64_t* quantum_out,
               int64_t* words_out) {
@@ -621,6 +633,21 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
       skip_tb[ed->dst] = ed->tensor_bytes;
     }
   }
+  if (o->strategy_space != 0 && o->strategy_space != 1) return ORC_ERR_ARG;
+  /* the concatenated catalogue Cat of the per-edge resharding matrices:
+   * S(g) of every divisor g of n, ascending */
+  const int64_t ncat = cat_offset(n, n + 1, o->strategy_space);
+  const int64_t* chain_mat[ORC_MAX_L];
+  const int64_t* skip_mat[ORC_MAX_L];
+  for (int u = 0; u < L; ++u) chain_mat[u] = skip_mat[u] = NULL;
+  for (int e = 0; e < m->n_edges; ++e) {
+    const orc_edge* ed = &m->edges[e];
+    if (!ed->reshard_ns) continue;
+    for (int64_t j = 0; j < (int64_t)ncat * ncat; ++j)
+      if (ed->reshard_ns[j] < 0 || ed->reshard_ns[j] > LIM) return ORC_ERR_ARG;
+    if (ed->dst == ed->src + 1) chain_mat[ed->src] = ed->reshard_ns;
+    else skip_mat[ed->dst] = ed->reshard_ns;
+  }
   int32_t cand_buf[2 * 4096];
   int n_cand;
   const int32_t* cand;
@@ -644,7 +671,7 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
   int Ss[4096];
   for (int i = 0; i < n_cand; ++i) {
     int g = n / cand[2 * i];
-    Ss[i] = orc_catalogue(g, NULL, 0);
+    Ss[i] = orc_catalogue(g, o->strategy_space, NULL, 0);
     if (Ss[i] > ORC_MAX_S) return ORC_ERR_RANGE;
     int S = Ss[i];
     words += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1);
@@ -662,7 +689,8 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
     int deg = cand[2 * i], c = cand[2 * i + 1], g = n / deg, S = Ss[i];
     int64_t b = o->B / c; /* micro-batch size b = B / c (Algorithm 1) */
     int32_t cat[3 * ORC_MAX_S];
-    orc_catalogue(g, cat, ORC_MAX_S);
+    orc_catalogue(g, o->strategy_space, cat, ORC_MAX_S);
+    const int64_t co = cat_offset(n, g, o->strategy_space); /* this stage size's block of the edge matrices */
     int64_t* blk = ns + off;
     blk[0] = deg; blk[1] = c; blk[2] = S; blk[3] = g;
     int64_t* A = blk + 4;
@@ -696,17 +724,23 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
         M[u * S + k] = (int64_t)mem;
       }
     }
+    /* same-stage resharding R_uv (the quadratic term of Eq. 3): the caller's
+     * per-edge matrix (per sample, times b) when given, else reading A-15 */
     for (int u = 0; u + 1 < L && st == ORC_OK; ++u)
       for (int k = 0; k < S; ++k)
         for (int l = 0; l < S; ++l) {
-          u128 v = has_chain[u] ? t_reshard(cl, &cat[3 * k], &cat[3 * l], (u128)b * chain_tb[u]) : 0;
+          u128 v = !has_chain[u] ? 0
+                   : chain_mat[u] ? (u128)b * (u128)chain_mat[u][(co + k) * ncat + co + l]
+                                  : t_reshard(cl, &cat[3 * k], &cat[3 * l], (u128)b * chain_tb[u]);
           if (v >= NS_LIMIT) st = ORC_ERR_RANGE;
           R[((int64_t)u * S + k) * S + l] = (int64_t)v;
         }
     for (int v = 0; v < L && st == ORC_OK; ++v)
       for (int k = 0; k < S; ++k)
         for (int l = 0; l < S; ++l) {
-          u128 x = has_skip[v] ? t_reshard(cl, &cat[3 * k], &cat[3 * l], (u128)b * skip_tb[v]) : 0;
+          u128 x = !has_skip[v] ? 0
+                   : skip_mat[v] ? (u128)b * (u128)skip_mat[v][(co + k) * ncat + co + l]
+                                 : t_reshard(cl, &cat[3 * k], &cat[3 * l], (u128)b * skip_tb[v]);
           if (x >= NS_LIMIT) st = ORC_ERR_RANGE;
           Rs[((int64_t)v * S + k) * S + l] = (int64_t)x;
         }

@@ -71,7 +71,13 @@ typedef struct {
   int64_t ctx_bytes;         /* m_c                                                  */
   int64_t tpcomm_bytes;      /* TP collective bytes per sample per forward           */
 } orc_layer;
-typedef struct { int32_t src, dst; int64_t tensor_bytes; } orc_edge;
+typedef struct {
+  int32_t src, dst;
+  int64_t tensor_bytes;      /* activation bytes per sample crossing the edge            */
+  const int64_t* reshard_ns; /* NULL, or the edge's resharding matrix R_uv per sample
+                                (PAPER.md:134): [|Cat|][|Cat|] ns, Cat = S(g) of every
+                                divisor g of n ascending, concatenated; R = b * value   */
+} orc_edge;
 typedef struct {
   int32_t n_dev, node_size;
   int64_t mem_bytes, mem_reserve, bw_intra, bw_inter, p2p_bw, lat_ns;
@@ -83,6 +89,7 @@ typedef struct {
   int64_t quantum_ns;        /* 0 = auto (reading A-9) */
   const int32_t* cand;       /* NULL = Algorithm 1; else n_cand (deg,c) pairs */
   int32_t n_cand;
+  int32_t strategy_space;    /* 0 = (t,f,d) triples, 1 = SPEC's (dp,tp)+FSDP-flag pairs */
 } orc_options;
 
 /* Builder': writes, per candidate config in order, the block
@@ -92,8 +99,10 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o,
               int32_t* buf, int64_t buf_len, int32_t* n_cfg, int32_t* skip_src,
               int64_t* quantum_ns, int64_t* words);
 
-/* Strategy catalogue S(g) (reading A-6): writes (t,f,d) triples, returns count. */
-int orc_catalogue(int32_t g, int32_t* tfd, int32_t cap);
+/* Strategy catalogue S(g) (reading A-6): writes (t,f,d) triples, returns count.
+ * space 0: every (t,f,d) with t*f*d = g, t a power of two; space 1:
+ * only f = 1 (DP) or d = 1 (FSDP over the whole replica axis).  (t, f) ascending. */
+int orc_catalogue(int32_t g, int32_t space, int32_t* tfd, int32_t cap);
 
 /* Candidate list of Algorithm 1: writes (deg,c) pairs. */
 int orc_candidates(int32_t n, int32_t B, int32_t* pairs, int32_t cap);

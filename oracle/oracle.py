@@ -56,7 +56,8 @@ class _Layer(C.Structure):
 
 
 class _Edge(C.Structure):
-    _fields_ = [("src", C.c_int32), ("dst", C.c_int32), ("tensor_bytes", C.c_int64)]
+    _fields_ = [("src", C.c_int32), ("dst", C.c_int32), ("tensor_bytes", C.c_int64),
+                ("reshard_ns", C.POINTER(C.c_int64))]
 
 
 class _Cluster(C.Structure):
@@ -72,7 +73,7 @@ class _Model(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("B", C.c_int32), ("precision", C.c_int32), ("Q", C.c_int32), ("quantum_ns", C.c_int64),
-                ("cand", C.POINTER(C.c_int32)), ("n_cand", C.c_int32)]
+                ("cand", C.POINTER(C.c_int32)), ("n_cand", C.c_int32), ("strategy_space", C.c_int32)]
 
 
 _lib = None
@@ -88,7 +89,7 @@ def lib():
         _lib.orc_build.argtypes = [C.POINTER(_Model), C.POINTER(_Cluster), C.POINTER(_Options),
                                    C.POINTER(C.c_int32), C.c_int64, C.POINTER(C.c_int32),
                                    C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
-        _lib.orc_catalogue.argtypes = [C.c_int32, C.POINTER(C.c_int32), C.c_int32]
+        _lib.orc_catalogue.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32]
         _lib.orc_candidates.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32]
         for f in ("orc_allreduce_ns", "orc_allgather_ns"):
             getattr(_lib, f).argtypes = [C.c_int64] * 4
@@ -179,9 +180,9 @@ def overlap_ns(comp, comm, ccoc_permille):
     return lib().orc_overlap_ns(comp, comm, ccoc_permille)
 
 
-def catalogue(g):
+def catalogue(g, space=0):
     buf = (C.c_int32 * (3 * 64))()
-    n = lib().orc_catalogue(g, buf, 64)
+    n = lib().orc_catalogue(g, space, buf, 64)
     return [tuple(buf[3 * i:3 * i + 3]) for i in range(min(n, 64))]
 
 
@@ -206,7 +207,13 @@ def _marshal_profile(p):
     E = len(m["edges"])
     edges = (_Edge * max(E, 1))()
     for i, e in enumerate(m["edges"]):
-        edges[i] = _Edge(e["src"], e["dst"], e["tensor_bytes_per_sample"])
+        mat = e.get("reshard_ns_per_sample")
+        ptr = None
+        if mat is not None:
+            mat = np.ascontiguousarray(mat, dtype=np.int64).reshape(-1)
+            keep.append(mat)
+            ptr = mat.ctypes.data_as(C.POINTER(C.c_int64))
+        edges[i] = _Edge(e["src"], e["dst"], e["tensor_bytes_per_sample"], ptr)
     model = _Model(L, layers, E, edges)
     cl = p["cluster"]
     cluster = _Cluster(cl["n_dev"], cl["node_size"], cl["mem_bytes"], cl["mem_reserve_bytes"],
@@ -217,7 +224,7 @@ def _marshal_profile(p):
         cand = np.ascontiguousarray(np.array(o["cand"], dtype=np.int32).reshape(-1))
         keep.append(cand)
     opts = _Options(o["B"], o["precision"], o["Q"], o.get("quantum_ns", 0),
-                    _ptr32(cand), 0 if cand is None else len(cand) // 2)
+                    _ptr32(cand), 0 if cand is None else len(cand) // 2, o.get("strategy_space", 0))
     keep += [layers, edges]
     return model, cluster, opts, keep
 

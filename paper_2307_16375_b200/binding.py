@@ -52,7 +52,8 @@ class uniap_layer(C.Structure):
 
 
 class uniap_edge(C.Structure):
-    _fields_ = [("src", C.c_int32), ("dst", C.c_int32), ("tensor_bytes_per_sample", C.c_int64)]
+    _fields_ = [("src", C.c_int32), ("dst", C.c_int32), ("tensor_bytes_per_sample", C.c_int64),
+                ("reshard_ns_per_sample", _P64)]
 
 
 class uniap_cluster(C.Structure):
@@ -68,7 +69,7 @@ class uniap_model(C.Structure):
 
 class uniap_options(C.Structure):
     _fields_ = [("B", C.c_int32), ("precision", C.c_int32), ("Q", C.c_int32), ("quantum_ns", C.c_int64),
-                ("cand", _P32), ("n_cand", C.c_int32)]
+                ("cand", _P32), ("n_cand", C.c_int32), ("strategy_space", C.c_int32)]
 
 
 class uniap_record(C.Structure):
@@ -121,7 +122,7 @@ def lib():
         L.uniap_shard_tables.argtypes = [C.POINTER(uniap_tables), C.c_int32, _P32]
         L.uniap_pick.argtypes = [C.POINTER(uniap_record), C.c_int32, C.POINTER(uniap_result)]
         L.uniap_candidates.argtypes = [C.c_int32, C.c_int32, _P32, C.c_int32]
-        L.uniap_catalogue.argtypes = [C.c_int32, _P32, C.c_int32]
+        L.uniap_catalogue.argtypes = [C.c_int32, C.c_int32, _P32, C.c_int32]
         L.uniap_selftest.argtypes = [_P32, _P32, _P32]
         for f in EXPORTS:
             if f not in ("uniap_destroy", "uniap_last_error", "uniap_status_string", "uniap_version"):
@@ -163,7 +164,7 @@ def _tables(t):
 
 _LAYER_DT = np.dtype([("fwd", np.uint64), ("param", np.int64), ("act", np.uint64), ("ctx", np.int64),
                       ("tpc", np.int64)])
-_EDGE_DT = np.dtype([("src", np.int32), ("dst", np.int32), ("bytes", np.int64)])
+_EDGE_DT = np.dtype([("src", np.int32), ("dst", np.int32), ("bytes", np.int64), ("mat", np.uint64)])
 
 
 def _profile(p):
@@ -183,10 +184,16 @@ def _profile(p):
     lay["tpc"] = [ly["tp_comm_bytes_per_sample"] for ly in ls]
     E = len(m["edges"])
     ed = np.zeros(max(E, 1), _EDGE_DT)
+    mats = []
     if E:
         ed["src"] = [e["src"] for e in m["edges"]]
         ed["dst"] = [e["dst"] for e in m["edges"]]
         ed["bytes"] = [e["tensor_bytes_per_sample"] for e in m["edges"]]
+        for i, e in enumerate(m["edges"]):  # optional per-edge resharding matrix (uniap_edge)
+            if e.get("reshard_ns_per_sample") is not None:
+                mat = np.ascontiguousarray(e["reshard_ns_per_sample"], dtype=np.int64).reshape(-1)
+                mats.append(mat)
+                ed["mat"][i] = mat.ctypes.data
     cl = p["cluster"]
     cluster = uniap_cluster(cl["n_dev"], cl["node_size"], cl["mem_bytes"], cl["mem_reserve_bytes"],
                             cl["bw_intra_Bps"], cl["bw_inter_Bps"], cl["p2p_Bps"], cl["lat_ns"],
@@ -196,8 +203,8 @@ def _profile(p):
     if o.get("cand"):
         cand = np.ascontiguousarray(np.array(o["cand"], dtype=np.int32).reshape(-1))
     opts = uniap_options(o["B"], o["precision"], o["Q"], o.get("quantum_ns", 0), _p32(cand),
-                         0 if cand is None else len(cand) // 2)
-    keep = [fwd, act, lay, ed, cand]
+                         0 if cand is None else len(cand) // 2, o.get("strategy_space", 0))
+    keep = [fwd, act, lay, ed, cand, mats]
     model = uniap_model(L, C.cast(lay.ctypes.data, C.POINTER(uniap_layer)), E,
                         C.cast(ed.ctypes.data, C.POINTER(uniap_edge)))
     return model, cluster, opts, keep
@@ -258,10 +265,10 @@ def selftest():
     return rc, (a.value, b.value, c.value)
 
 
-def catalogue(g):
-    k = lib().uniap_catalogue(g, None, 0)
+def catalogue(g, space=0):
+    k = lib().uniap_catalogue(g, space, None, 0)
     buf = (C.c_int32 * (3 * max(k, 1)))()
-    lib().uniap_catalogue(g, buf, k)
+    lib().uniap_catalogue(g, space, buf, k)
     return [tuple(buf[3 * i:3 * i + 3]) for i in range(k)]
 
 

@@ -95,7 +95,7 @@ struct uniap_handle {
   // the level-2 profile, config and catalogue arrays: views into ONE device
   // blob filled by one DMA per prepare
   DevBuf<char> upb;
-  View<int64_t> fwd, act, ps, ctx, tpc, chain, skipb, edges;
+  View<int64_t> fwd, act, ps, ctx, tpc, chain, skipb, edges, rmat, chain_mat, skip_mat;
   View<CfgDev> dcfg;
   View<CatDev> dcat;
   DevBuf<CfgDev> dcfg1;  // level 1: the config array (the arena is its own buffer)
@@ -106,7 +106,7 @@ struct uniap_handle {
   DevBuf<uniap_record> rec;
   // last run
   uniap_record rec_host{};
-  uint64_t cells = 0, relax = 0, cells_canon = 0;
+  uint64_t cells_canon = 0;
   float ms_dp = 0.f, ms_total = 0.f;
   int64_t quantum = 0;
   cudaEvent_t ev[4] = {};
@@ -138,10 +138,6 @@ struct uniap_handle {
     int64_t cfgopt[UNIAP_MAX_CFG];
   }* fb = nullptr, *fb_dev = nullptr;  // mapped pinned block (host / device address), written by k_publish
   std::vector<int64_t> sig;                // what the captured graph depends on
-  // per (config, layer): min over the config's strategies of M (buckets,
-  // cap + 1 = none fits) -- the plan stops a forward sweep where the running
-  // sum exceeds cap (every later interval is infeasible, Eq. 5)
-  std::vector<int32_t> minM;
 };
 
 // A prepared problem keeps the launch plan and the captured graph when
@@ -156,7 +152,6 @@ static void update_signature(uniap_handle* h) {
                       (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C, (int64_t)k.DB})
       sg.push_back(x);
   }
-  for (int32_t m : h->minM) sg.push_back(m);  // the plan's sweep lengths depend on them
   if (h->level2) {
     const int64_t* c = reinterpret_cast<const int64_t*>(&h->cl);
     for (size_t i = 0; i < sizeof(ClusterDev) / 8; ++i) sg.push_back(c[i]);
@@ -165,7 +160,8 @@ static void update_signature(uniap_handle* h) {
                         (const void*)h->fwd.p, (const void*)h->act.p, (const void*)h->ps.p, (const void*)h->ctx.p,
                         (const void*)h->tpc.p, (const void*)h->chain.p, (const void*)h->skipb.p,
                         (const void*)h->edges.p, (const void*)h->qcfg.p, (const void*)h->qmax.p,
-                        (const void*)h->qglob.p})
+                        (const void*)h->qglob.p, (const void*)h->rmat.p, (const void*)h->chain_mat.p,
+                        (const void*)h->skip_mat.p})
     sg.push_back(reinterpret_cast<int64_t>(p));
   if (sg != h->sig) {
     h->sig.swap(sg);
@@ -257,14 +253,16 @@ extern "C" int32_t uniap_candidates(int32_t n, int32_t B, int32_t* pairs, int32_
   return k;
 }
 
-extern "C" int32_t uniap_catalogue(int32_t g, int32_t* tfd, int32_t cap) {
+extern "C" int32_t uniap_catalogue(int32_t g, int32_t space, int32_t* tfd, int32_t cap) {
   // SD[deg] (reading A-6): (t,f,d) with t*f*d = g, t a
-  // power of two; t ascending then f ascending (index 0 = pure DP).
+  // power of two; t ascending then f ascending (index 0 = pure DP).  Space 1
+  // (SPEC.md:42-64): a (dp, tp) pair whose dp axis is plain DP (f = 1) or
+  // fully FSDP-sharded (d = 1).
   int32_t k = 0;
-  if (g < 1) return 0;
+  if (g < 1 || space < 0 || space > 1) return 0;
   for (int32_t t = 1; t <= g && g % t == 0; t *= 2)
     for (int32_t f = 1; f <= g / t; ++f)
-      if ((g / t) % f == 0) {
+      if ((g / t) % f == 0 && (space == 0 || f == 1 || f == g / t)) {
         if (k < cap && tfd) { tfd[3 * k] = t; tfd[3 * k + 1] = f; tfd[3 * k + 2] = g / t / f; }
         ++k;
       }
@@ -471,15 +469,6 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
     }
     if (keep[i].empty()) keep[i].push_back(0);  // all forbidden: the config is infeasible
   }
-  h->minM.assign((size_t)h->ncfg * L, t->cap + 1);
-  for (int i = 0; i < h->ncfg; ++i) {
-    const uniap_config& x = t->cfg[i];
-    for (int u = 0; u < L; ++u) {
-      int32_t mn = t->cap + 1;
-      for (int k : keep[i]) mn = std::min(mn, x.M[u * x.n_strat + k]);
-      h->minM[(size_t)i * L + u] = mn;
-    }
-  }
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc);
   if (st != UNIAP_OK) return st;
   // pack the host tables into the device layout (pads: A 0, M cap+1, R 0)
@@ -538,7 +527,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
       cl->lat_ns < 0 || cl->ccoc_permille < 0 || cl->ccoc_permille > 1000)
     FAIL(h, UNIAP_ERR_ARG, "bad cluster record");
   if (o->B < 1 || o->B > 65536 || o->Q < 2 || o->Q > UNIAP_MAX_Q || (o->precision != 0 && o->precision != 1) ||
-      o->quantum_ns < 0 || o->quantum_ns > ((int64_t)1 << 61))
+      o->quantum_ns < 0 || o->quantum_ns > ((int64_t)1 << 61) || (o->strategy_space != 0 && o->strategy_space != 1))
     FAIL(h, UNIAP_ERR_ARG, "bad options");
   if (cl->mem_reserve_bytes < 0 || cl->mem_bytes <= cl->mem_reserve_bytes) FAIL(h, UNIAP_ERR_ARG, "memory <= reserve");
   if ((cl->mem_bytes - cl->mem_reserve_bytes) / (o->Q - 1) < 1) FAIL(h, UNIAP_ERR_ARG, "memory unit < 1 byte");
@@ -564,8 +553,14 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
     }
     ps[u] = y.param_bytes; ctx[u] = y.ctx_bytes; tpc[u] = y.tp_comm_bytes_per_sample;
   }
+  // Cat = S(g) of every divisor g of n ascending: the index space of the
+  // caller's per-edge resharding matrices (uniap_edge)
+  std::vector<int32_t> cat_off(n + 2, 0);
+  for (int g = 1; g <= n; ++g)
+    cat_off[g + 1] = cat_off[g] + (n % g == 0 ? uniap_catalogue(g, o->strategy_space, nullptr, 0) : 0);
+  const int64_t ncat = cat_off[n + 1];
   int skip = -1;
-  std::vector<int64_t> ed;
+  std::vector<int64_t> ed, rmat, chain_mat(L, -1), skip_mat(L, -1);
   for (int i = 0; i < m->n_edges; ++i) {
     const uniap_edge& e = m->edges[i];
     if (e.src < 0 || e.dst >= L || e.src >= e.dst || e.tensor_bytes_per_sample < 0 || e.tensor_bytes_per_sample > LIM)
@@ -580,6 +575,15 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
       skipb[e.dst] = e.tensor_bytes_per_sample;
     }
     ed.push_back(e.src); ed.push_back(e.dst); ed.push_back(e.tensor_bytes_per_sample);
+    if (e.reshard_ns_per_sample) {
+      if (ncat * ncat > ((int64_t)1 << 24)) FAIL(h, UNIAP_ERR_ARG, "resharding matrix too large (|Cat| = %lld)", (long long)ncat);
+      (e.dst == e.src + 1 ? chain_mat[e.src] : skip_mat[e.dst]) = (int64_t)rmat.size();
+      for (int64_t j = 0; j < ncat * ncat; ++j) {
+        const int64_t v = e.reshard_ns_per_sample[j];
+        if (v < 0 || v > LIM) FAIL(h, UNIAP_ERR_ARG, "edge %d: resharding matrix entry out of [0, 2^46]", i);
+        rmat.push_back(v);
+      }
+    }
   }
   // candidate list (Algorithm 1 or explicit)
   std::vector<int32_t> cand;
@@ -604,9 +608,11 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   std::vector<std::vector<int>> keep(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i) {
     deg[i] = cand[2 * i]; c[i] = cand[2 * i + 1]; g[i] = n / deg[i];
-    S[i] = uniap_catalogue(g[i], nullptr, 0);
+    S[i] = uniap_catalogue(g[i], o->strategy_space, nullptr, 0);
     if (S[i] > UNIAP_MAX_STRAT) FAIL(h, UNIAP_ERR_RANGE, "|S(%d)| = %d > 32", g[i], S[i]);
-    uniap_catalogue(g[i], h->cat[i].tfd, UNIAP_MAX_STRAT);
+    uniap_catalogue(g[i], o->strategy_space, h->cat[i].tfd, UNIAP_MAX_STRAT);
+    h->cat[i].co = cat_off[g[i]];
+    h->cat[i].ncat = (int32_t)ncat;
     // b mod (f d) != 0 forbids a strategy at every layer (reading A-7)
     const int b = o->B / c[i];
     for (int k = 0; k < S[i]; ++k)
@@ -615,46 +621,6 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   }
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc);
   if (st != UNIAP_OK) return st;
-  {
-    // A lower bound of the builder's memory term (Eq. 1 + activations + ctx,
-    // in buckets; reading A-8) per (layer, strategy), minimised per config:
-    // the plan trims sweeps with it, so a lower bound only trims less.  c b / r
-    // = B / r, so M depends on the stage size g and the strategy, not on c:
-    // evaluated once per distinct g, in double precision (floor of the
-    // quotient <= the builder's exact ceiling).
-    const int64_t cap = o->Q - 1;
-    const double inv_unit = 1.0 / (double)((cl->mem_bytes - cl->mem_reserve_bytes) / cap);
-    const double cdt = o->precision ? 8.0 : 4.0;
-    std::vector<int> gs;
-    std::vector<std::vector<int32_t>> mg;  // per distinct g: [u][catalogue k]
-    h->minM.assign((size_t)h->ncfg * L, (int32_t)cap + 1);
-    for (int i = 0; i < h->ncfg; ++i) {
-      int gi = 0;
-      while (gi < (int)gs.size() && gs[gi] != g[i]) ++gi;
-      const int32_t* tfd = h->cat[i].tfd;
-      if (gi == (int)gs.size()) {
-        gs.push_back(g[i]);
-        std::vector<int32_t> m((size_t)L * S[i]);
-        for (int u = 0; u < L; ++u)
-          for (int k = 0; k < S[i]; ++k) {
-            const int tt = tfd[3 * k], ff = tfd[3 * k + 1], r = ff * tfd[3 * k + 2];
-            int lt = 0;
-            while ((1 << lt) < tt) ++lt;
-            const double mem = cdt * (double)ps[u] / (tt * ff) + (double)(o->B / r) * (double)act[u * NT + lt] + (double)ctx[u];
-            const double q = mem * inv_unit;
-            m[(size_t)u * S[i] + k] = q >= (double)cap + 2.0 ? (int32_t)cap + 1 : std::max(0, (int32_t)q - 1);
-          }
-        mg.push_back(std::move(m));
-      }
-      const std::vector<int32_t>& m = mg[gi];
-      for (int u = 0; u < L; ++u) {  // keep[i]: the strategies with (B / c) mod (f d) = 0 (reading A-7)
-        const int32_t* row = m.data() + (size_t)u * S[i];
-        int32_t mn = (int32_t)cap + 1;
-        for (int k : keep[i]) mn = std::min(mn, row[k]);
-        h->minM[(size_t)i * L + u] = mn;
-      }
-    }
-  }
   h->cl = ClusterDev{cl->n_dev, cl->node_size, cl->ccoc_permille, o->B, o->precision, o->Q, NT, 0,
                      cl->mem_bytes, cl->mem_reserve_bytes, cl->bw_intra_Bps, cl->bw_inter_Bps, cl->p2p_Bps,
                      cl->lat_ns, o->quantum_ns};
@@ -668,18 +634,22 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   CK(h, cudaMemsetAsync(h->qglob.p, 0, 3 * sizeof(int64_t), h->st));
   CK(h, cudaMemsetAsync(h->qmax.p, 0, (size_t)h->ncfg * MAXL * 4 * sizeof(int64_t), h->st));
   {  // one pinned staging block -> one device blob, one DMA
-    const size_t sz[10] = {fwd.size() * 8, act.size() * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8,
+    constexpr int NB = 13;
+    const size_t sz[NB] = {fwd.size() * 8, act.size() * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8,
                            (size_t)L * 8, std::max<size_t>(ed.size(), 3) * 8, h->ncfg * sizeof(CfgDev),
-                           h->ncfg * sizeof(CatDev)};
-    const void* src[10] = {fwd.data(), act.data(), ps.data(), ctx.data(), tpc.data(), chain.data(), skipb.data(),
-                           ed.data(), h->cfg.data(), h->cat.data()};
-    size_t off[10], tot = 0;
-    for (int i = 0; i < 10; ++i) { off[i] = tot; tot += staged(sz[i]); }
+                           h->ncfg * sizeof(CatDev), std::max<size_t>(rmat.size(), 1) * 8, (size_t)L * 8,
+                           (size_t)L * 8};
+    const size_t used[NB] = {sz[0], sz[1], sz[2], sz[3], sz[4], sz[5], sz[6], ed.size() * 8, sz[8], sz[9],
+                             rmat.size() * 8, sz[11], sz[12]};
+    const void* src[NB] = {fwd.data(), act.data(), ps.data(), ctx.data(), tpc.data(), chain.data(), skipb.data(),
+                           ed.data(), h->cfg.data(), h->cat.data(), rmat.data(), chain_mat.data(), skip_mat.data()};
+    size_t off[NB], tot = 0;
+    for (int i = 0; i < NB; ++i) { off[i] = tot; tot += staged(sz[i]); }
     CK(h, h->upb.ensure(tot));
     CK(h, stage_begin(h, tot));
     memset(h->stage, 0, tot);
-    for (int i = 0; i < 10; ++i)
-      if (src[i]) memcpy(h->stage + off[i], src[i], i == 7 ? ed.size() * 8 : sz[i]);
+    for (int i = 0; i < NB; ++i)
+      if (src[i] && used[i]) memcpy(h->stage + off[i], src[i], used[i]);
     h->h2d += tot;
     CK(h, cudaMemcpyAsync(h->upb.p, h->stage, tot, cudaMemcpyHostToDevice, h->st));
     char* b = h->upb.p;
@@ -687,6 +657,8 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
     h->ctx.p = (int64_t*)(b + off[3]); h->tpc.p = (int64_t*)(b + off[4]); h->chain.p = (int64_t*)(b + off[5]);
     h->skipb.p = (int64_t*)(b + off[6]); h->edges.p = (int64_t*)(b + off[7]);
     h->dcfg.p = (CfgDev*)(b + off[8]); h->dcat.p = (CatDev*)(b + off[9]);
+    h->rmat.p = (int64_t*)(b + off[10]); h->chain_mat.p = (int64_t*)(b + off[11]);
+    h->skip_mat.p = (int64_t*)(b + off[12]);
   }
   CK(h, stage_end(h));
   update_signature(h);
@@ -764,30 +736,11 @@ static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>&
 }
 
 static void forward_instances(const uniap_handle* h, int i, bool all_intervals, std::vector<Inst>& out) {
+  // (each P-emitting sweep stops at its feasible prefix inside K2, from the
+  // quantised memory table: k2_feasible_len)
   const CfgDev& d = h->cfg[i];
-  const size_t first = out.size();
   if (all_intervals) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, out);
   else plan_fast(h->L, i, d.deg, d.S, d.skip, out);
-  // Stop each forward P sweep where it becomes infeasible: the memory sum of
-  // Eq. 5 over the layers swept is at least the running sum of the per-layer
-  // minima, so past the first layer where that exceeds cap every state is INF
-  // and the interval optima stay INF from the fill (exact).  The emitted
-  // range shrinks with it; G-storing sweeps (deg = 1's kept tables) run in full.
-  if (all_intervals || h->minM.empty()) return;
-  const int L = h->L;
-  for (size_t j = first; j < out.size(); ++j) {
-    Inst& x = out[j];
-    if (x.emit != 1 && x.emit != 2) continue;
-    int64_t sum = 0;
-    int n = 0;
-    for (; n < x.n; ++n) {
-      sum += h->minM[(size_t)i * L + x.a + x.dir * n];
-      if (sum > h->cap) break;
-    }
-    x.n = std::max(n, 1);
-    if (x.dir > 0) x.ehi = std::min(x.ehi, x.a + x.n - 1);
-    else x.elo = std::max(x.elo, x.a - x.n + 1);
-  }
 }
 
 // LPT over configs by executed chain-DP work (sum over the sweeps of n |S|^2 Q); ties
@@ -977,7 +930,8 @@ static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, De
 
 static BuildBufs build_bufs(uniap_handle* h) {
   return BuildBufs{h->fwd.p, h->act.p, h->ps.p, h->ctx.p, h->tpc.p, h->chain.p, h->skipb.p, h->edges.p,
-                   h->n_edges, h->dcat.p, h->ns.p, h->qcfg.p, h->qmax.p, h->qglob.p};
+                   h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->dcat.p, h->ns.p, h->qcfg.p, h->qmax.p,
+                   h->qglob.p};
 }
 
 // ---------------------------------------------------------------------------
@@ -995,13 +949,9 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   // forward instances
   std::vector<Inst> fw;
   for (int i : R.local) forward_instances(h, i, false, fw);
-  h->cells = h->relax = 0;
-  for (auto& x : fw) {
-    const uint64_t S = h->cfg[x.cfg].S;
-    if (S == 1) continue;  // closed form (k2_closed_s1): no DP cells
-    h->cells += (uint64_t)x.n * S * h->Q;
-    h->relax += (uint64_t)(x.n - 1) * S * S * h->Q;
-  }
+  // executed cells / relaxations are counted by the K2 launches themselves
+  // (the feasible-prefix trim is decided on the device); the canonical count
+  // is the workload size
   h->cells_canon = 0;
   for (int i : R.local) {
     std::vector<Inst> cv;
@@ -1030,7 +980,7 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     R.k4rest = {rest0, (int)ordered.size() - rest0};
     R.local.swap(ordered);
   }
-  CK(h, h->tim.ensure(2));
+  CK(h, h->tim.ensure(4));
   // backward: one device-sized launch per kernel class of the local configs
   std::vector<int32_t> cls_of_cfg(h->ncfg, 0);
   R.bgrp.clear();
@@ -1120,14 +1070,14 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     if (s != UNIAP_OK) return s;
     CK(h, cudaEventRecord(h->fork_ev, h->st));
     CK(h, cudaStreamWaitEvent(h->side[0], h->fork_ev, 0));
-    CK(h, cudaMemsetAsync(h->tim.p, 0, 2 * sizeof(unsigned long long), h->side[0]));  // forward phase clock
+    CK(h, cudaMemsetAsync(h->tim.p, 0, 4 * sizeof(unsigned long long), h->side[0]));  // forward phase clock + work
     CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->side[0]));
     CK(h, cudaEventRecord(h->side_ev[0], h->side[0]));
     CK(h, launch_k1(h->cl, build_bufs(h), h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
     CK(h, cudaStreamWaitEvent(h->st, h->side_ev[0], 0));
     h->launches += 3;
   } else {
-    CK(h, cudaMemsetAsync(h->tim.p, 0, 2 * sizeof(unsigned long long), h->st));  // forward phase clock
+    CK(h, cudaMemsetAsync(h->tim.p, 0, 4 * sizeof(unsigned long long), h->st));  // forward phase clock + work
     CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
   }
   h->launches++;
@@ -1141,7 +1091,7 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     if (s != UNIAP_OK) return s;
   }
 
-  RecordArgs ra{rec, h->cells, h->relax, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
+  RecordArgs ra{rec, h->tim.p + 2, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
                 h->binst.p, h->bwp.p, h->gstore.p};
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
                    h->cfgopt.p, h->scratch.p, h->win.p, ra, h->st));

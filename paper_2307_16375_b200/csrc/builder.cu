@@ -173,16 +173,27 @@ __device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const Cfg
   }
   const int64_t b = cl.B / cf.c;
   const Coll co{cl};
+  // the caller's matrix of this edge ("R_uv"; b * per-sample
+  // value, the block of S(g)), else the built-in formula (reading A-15)
+  const int64_t mo = isR ? bb.chain_mat[e] : bb.skip_mat[e];
+  const CatDev& cd = bb.cat[blockIdx.y];
   const int gmax = min(cf.g, K1G);
-  for (int G = 2 + threadIdx.x; G <= gmax; G += blockDim.x)
-    tab[G] = checked(co.reshard_G((u128)b * tb, G), bb.qglob + 1);
-  if (threadIdx.x == 0) tab[1] = 0;
+  if (mo < 0) {
+    for (int G = 2 + threadIdx.x; G <= gmax; G += blockDim.x)
+      tab[G] = checked(co.reshard_G((u128)b * tb, G), bb.qglob + 1);
+    if (threadIdx.x == 0) tab[1] = 0;
+  }
   __syncthreads();
   int64_t mx = 0;
   for (int j = threadIdx.x; j < SF * SF; j += blockDim.x) {
     const int k = j / SF, l = j - k * SF;
-    const int64_t G = reshard_group(tfd + 3 * k, tfd + 3 * l);
-    const int64_t v = G <= gmax ? tab[G] : checked(co.reshard_G((u128)b * tb, G), bb.qglob + 1);
+    int64_t v;
+    if (mo >= 0) {
+      v = checked((u128)b * (u128)bb.rmat[mo + (int64_t)(cd.co + k) * cd.ncat + cd.co + l], bb.qglob + 1);
+    } else {
+      const int64_t G = reshard_group(tfd + 3 * k, tfd + 3 * l);
+      v = G <= gmax ? tab[G] : checked(co.reshard_G((u128)b * tb, G), bb.qglob + 1);
+    }
     mx = max(mx, v);
     const int kc = cf.comp[k], lc = cf.comp[l];
     if (kc >= 0 && lc >= 0) dst[kc * NSP + lc] = v;

@@ -455,8 +455,8 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     r->L = ra.L;
     r->status = (ra.qglob && ra.qglob[1] != 0) ? UNIAP_ERR_RANGE : 0;
     r->n_cfg_local = ra.n_local;
-    r->dp_cells = ra.cells;
-    r->dp_relax = ra.relax;
+    r->dp_cells = ra.work[0];
+    r->dp_relax = ra.work[1];
     r->dp_cells_canonical = ra.cells_canon;
   }
   if (wl < 0) {

@@ -68,7 +68,8 @@ struct K2Args {
   unsigned long long* trace = nullptr;
   uint32_t tag = 0;
   // forward-phase clock (%globaltimer, ns): tim[0] = max of ~start, tim[1] =
-  // max of end over the launch's CTAs (both reset to 0 per run), or nullptr
+  // max of end over the launch's CTAs; tim[2], tim[3] = executed cells and
+  // relaxations (all reset to 0 per run), or nullptr
   unsigned long long* tim = nullptr;
 };
 
@@ -152,7 +153,8 @@ struct BwPlan {
 };
 struct RecordArgs {          // what K5a writes into the record besides the winner
   uniap_record* rec;
-  uint64_t cells, relax, cells_canon;
+  const unsigned long long* work;  // forward-phase cells, relaxations (accumulated by the K2 launches)
+  uint64_t cells_canon;
   int32_t n_local, L, cap;
   const int64_t* qglob;      // builder flags (level 2) or nullptr
   const int32_t* cls_of_cfg; // kernel class id per config
@@ -188,6 +190,7 @@ struct ClusterDev {
 };
 struct CatDev {  // per config: catalogue (t,f,d) of its strategies
   int32_t tfd[UNIAP_MAX_STRAT * 3];
+  int32_t co, ncat;  // block offset of S(g) in the per-edge resharding matrices, their order |Cat|
 };
 struct BuildBufs {
   const int64_t* fwd;     // [L][NT]
@@ -199,6 +202,9 @@ struct BuildBufs {
   const int64_t* skipb;   // [L] tensor bytes of edge skip->v, -1 none
   const int64_t* esrc_dst_bytes;  // [E][3]
   int32_t n_edges;
+  const int64_t* rmat;    // caller resharding matrices (ns per sample), concatenated
+  const int64_t* chain_mat;  // [L] word offset into rmat of edge u->u+1's matrix, -1 none
+  const int64_t* skip_mat;   // [L] word offset of edge skip->v's matrix, -1 none
   const CatDev* cat;      // [ncfg]
   int64_t* ns;            // int64 scratch arena, same offsets as the int32 arena
   int64_t* qcfg;          // [ncfg] smallest passing quantum per config

@@ -61,7 +61,8 @@ def test_candidates_and_catalogue_match_the_oracle(orc):
         for B in (1, 2, 6, 8, 32, 64, 128):
             assert pkg.candidates(n, B) == orc.candidates(n, B)
     for g in (1, 2, 3, 4, 6, 8, 12, 16, 32):
-        assert pkg.catalogue(g) == orc.catalogue(g)
+        for space in (0, 1):
+            assert pkg.catalogue(g, space) == orc.catalogue(g, space)
     assert len(pkg.candidates(8, 32)) == 16 and len(pkg.candidates(4, 6)) == 7
 
 

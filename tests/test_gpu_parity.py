@@ -253,3 +253,28 @@ def test_interval_table_between_solves_keeps_the_captured_plan(h, orc):
         iu = np.triu_indices(L)
         assert np.array_equal(P[iu], ref[iu])
         _same(h.solve_tables(t), want, ("second", seed))
+
+
+@pytest.mark.parametrize("space", [0, 1])
+def test_builder_reshard_matrices_and_strategy_space(h, orc, space):
+    """Per-edge resharding matrices (uniap_edge.reshard_ns_per_sample) and
+    SPEC's strategy space (uniap_options.strategy_space): K1's tables are
+    bit-equal to builder''s and the plan equals the oracle's."""
+    import paper_2307_16375_b200 as pkg
+    checked = 0
+    for seed in range(40):
+        n = [1, 2, 4, 6, 8, 12, 16][seed % 7]
+        dim = sum(len(orc.catalogue(g, space)) for g in range(1, n + 1) if n % g == 0)
+        p = profiles.random_profile(5000 + seed, n=n, mat_dim=dim, space=space)
+        try:
+            t, qn, buf = orc.build_tables(p)
+        except orc.OracleError as e:
+            with pytest.raises(pkg.UniapError) as ei:
+                h.build_tables(p)
+            assert ei.value.status == e.status
+            continue
+        gt, gq, gbuf = h.build_tables(p)
+        assert gq == qn and np.array_equal(gbuf, buf), seed
+        _same(h.plan(p), orc.solve_tables(t), seed)
+        checked += 1
+    assert checked > 10

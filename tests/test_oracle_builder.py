@@ -251,3 +251,110 @@ def test_tp_collectives_with_ccoc_overlap(orc):
     p = _one_layer(8, 8, fwd, 0, 10 ** 6, 1, 10 ** 11, 10 ** 10, 0, 500, [(1, 1)], quantum=2)
     t, _, _ = orc.build_tables(p)
     assert int(t["cfgs"][0]["A"][0, k]) == 660_000 // 2
+
+
+# ---------------------------------------------------------------------------
+# The caller's per-edge resharding matrix (north_star "a resharding matrix per
+# edge"; PAPER.md:134 R_uv) and SPEC's strategy space.
+# ---------------------------------------------------------------------------
+
+def _cat_dim(orc, n, space):
+    return sum(len(orc.catalogue(g, space)) for g in range(1, n + 1) if n % g == 0)
+
+
+def test_spec_strategy_space_pairs_with_fsdp_flag(orc):
+    """SPEC.md:59-64: g=1 -> (dp1,tp1); g=2 -> (1,2,F),(2,1,F),(2,1,T); g=4 ->
+    (1,4,F),(2,2,F),(2,2,T),(4,1,F),(4,1,T).  As (t,f,d): FSDP flag off ->
+    (tp, 1, dp), on -> (tp, dp, 1).  |S(2^k)| = 2k+1 (SPEC's "3k" at
+    SPEC.md:89 is wrong for k >= 2, reading A-6); order (t, f) ascending as
+    in space 0, of which it is a subsequence."""
+    def spec(dp, tp, fsdp):
+        return (tp, dp, 1) if fsdp else (tp, 1, dp)
+    assert orc.catalogue(1, 1) == [spec(1, 1, False)]
+    assert set(orc.catalogue(2, 1)) == {spec(1, 2, False), spec(2, 1, False), spec(2, 1, True)}
+    assert set(orc.catalogue(4, 1)) == {spec(1, 4, False), spec(2, 2, False), spec(2, 2, True), spec(4, 1, False),
+                                        spec(4, 1, True)}
+    for k in range(6):
+        c1, c0 = orc.catalogue(2 ** k, 1), orc.catalogue(2 ** k, 0)
+        assert len(c1) == 2 * k + 1
+        assert c1 == [x for x in c0 if x in c1]
+
+
+def test_reshard_matrix_is_b_times_the_callers_value(orc):
+    """R_uv[k][l] = b * value[co+k][co+l] with co the offset of S(g) in Cat
+    (S(1) ++ S(2) for n = 2).  n = 2, B = 4: config (1,1) has g = 2, b = 4,
+    co = 1; config (2,2) has g = 1, b = 2, co = 0.  An asymmetric value
+    100 (row+1) + (col+1) makes a transposed read visible."""
+    dim = _cat_dim(orc, 2, 0)
+    assert dim == 4
+    val = np.array([[100 * (r + 1) + (c + 1) for c in range(dim)] for r in range(dim)], dtype=np.int64)
+    p = _profile(L=2, n=2, B=4, edges=[(0, 1, 1000)], cand=[(1, 1), (2, 2)], quantum=1, fwd=[1000, 600])
+    p["model"]["edges"][0]["reshard_ns_per_sample"] = val
+    t, _, _ = orc.build_tables(p)
+    R1 = t["cfgs"][0]["R"][0]
+    for k in range(3):
+        for l in range(3):
+            assert int(R1[k, l]) == 4 * (100 * (k + 2) + (l + 2))
+    assert int(t["cfgs"][1]["R"][0][0, 0]) == 2 * 101
+
+
+def test_reshard_matrix_reproducing_the_formula_gives_the_same_tables(orc):
+    """With lat = 0 and volumes that divide evenly, the built-in resharding
+    (reading A-15) is linear in b, so a matrix holding its per-sample values
+    must give identical tables at any b -- for the chain edge and a skip
+    edge, both strategy spaces (an orientation or offset slip breaks it)."""
+    for space in (0, 1):
+        n = 4
+        dim = _cat_dim(orc, n, space)
+        edges = [(0, 1, 10 ** 6), (1, 2, 10 ** 6), (2, 3, 10 ** 6), (0, 2, 2 * 10 ** 6), (0, 3, 2 * 10 ** 6)]
+        base = _profile(L=4, n=n, B=1, edges=edges, quantum=1, fwd=[1000, 600, 400], bw=10 ** 12, p2p=10 ** 12)
+        base["options"]["strategy_space"] = space
+        base["options"]["cand"] = [(1, 1), (2, 1), (4, 1)]  # g = 4, 2, 1 at b = B
+        t1, _, _ = orc.build_tables(base)           # b = 1: per-sample values
+        mats = {}
+        for (src, dst, _) in edges[:2] + edges[4:]:  # edges 0->1, 1->2 and the skip edge 0->3
+            mat = np.zeros((dim, dim), dtype=np.int64)
+            for ci, g in ((0, 4), (1, 2), (2, 1)):
+                cat = orc.catalogue(g, space)
+                co = sum(len(orc.catalogue(x, space)) for x in range(1, g) if n % x == 0)
+                blk = t1["cfgs"][ci]["R"][src] if dst == src + 1 else t1["cfgs"][ci]["Rskip"][dst]
+                mat[co:co + len(cat), co:co + len(cat)] = blk
+            mats[(src, dst)] = mat
+        for B in (4, 8):
+            pf = _profile(L=4, n=n, B=B, edges=edges, quantum=1, fwd=[1000, 600, 400], bw=10 ** 12, p2p=10 ** 12)
+            pf["options"].update(strategy_space=space, cand=[(1, 1), (2, 1), (4, 1)])
+            pm = _profile(L=4, n=n, B=B, edges=edges, quantum=1, fwd=[1000, 600, 400], bw=10 ** 12, p2p=10 ** 12)
+            pm["options"].update(strategy_space=space, cand=[(1, 1), (2, 1), (4, 1)])
+            for e in pm["model"]["edges"]:
+                if (e["src"], e["dst"]) in mats:
+                    e["reshard_ns_per_sample"] = mats[(e["src"], e["dst"])]
+            tf, _, _ = orc.build_tables(pf)
+            tm, _, _ = orc.build_tables(pm)
+            for a, b in zip(tf["cfgs"], tm["cfgs"]):
+                assert np.array_equal(a["R"], b["R"]) and np.array_equal(a["Rskip"], b["Rskip"]), (space, B)
+                assert np.array_equal(a["A"], b["A"]) and np.array_equal(a["O"], b["O"])
+
+
+def test_strategy_space_restricts_the_search(orc):
+    """Space 1 is a subset of space 0 with the same per-strategy costs, so the
+    space-0 optimum is never worse (and the tables agree strategy by strategy)."""
+    for seed in range(20):
+        p0 = profiles.random_profile(seed, n=8, B=8, Q=64)
+        p1 = profiles.random_profile(seed, n=8, B=8, Q=64, space=1)
+        t0, _, _ = orc.build_tables(p0)
+        t1, _, _ = orc.build_tables(p1)
+        for c0, c1 in zip(t0["cfgs"], t1["cfgs"]):
+            g = c0["g"]
+            idx = [orc.catalogue(g, 0).index(x) for x in orc.catalogue(g, 1)]
+            if t0["cap"] == t1["cap"]:
+                assert np.array_equal(c0["M"][:, idx], c1["M"])
+        try:
+            r0 = orc.solve_tables(t0)["objective"]
+        except orc.OracleError:
+            continue
+        # the quantum may differ between the spaces; compare in ns
+        q0 = orc.build_tables(p0)[1]
+        q1 = orc.build_tables(p1)[1]
+        r1 = orc.solve_tables(t1)["objective"]
+        if r0 != (1 << 63) - 1 and r1 != (1 << 63) - 1 and q0 == q1:
+            assert r0 <= r1
