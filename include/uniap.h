@@ -123,6 +123,14 @@ uniap_status uniap_solve_tables(uniap_handle* h, const uniap_tables* t, uniap_re
  * placement can use).  P_out has L*L int32; entries a > b are UNIAP_INF. */
 uniap_status uniap_interval_table(uniap_handle* h, const uniap_tables* t, int32_t cfg, int32_t* P_out);
 
+/* The interval optima the LAST run computed (for parity tests of the plan
+ * that actually runs: prefix / middle / suffix sweeps, skip-conditioned
+ * copies, the feasible-prefix trim): P_out[(i*L + a)*L + b] for config i in
+ * candidate order, UNIAP_INF where infeasible OR not needed by any
+ * placement of config i (and for configs another rank owns).  P_len must be
+ * >= n_cfg*L*L.  Synchronises the handle's stream. */
+uniap_status uniap_fetch_intervals(uniap_handle* h, int32_t* P_out, int64_t P_len);
+
 /* ---- level 2: profiles (the paper's problem statement) -- */
 typedef struct {
   const int64_t* fwd_ns_per_sample;   /* [1+log2(maxTP)] forward ns per sample, TP size 1,2,4,..

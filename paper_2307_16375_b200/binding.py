@@ -86,7 +86,7 @@ RECORD_BYTES = C.sizeof(uniap_record)
 EXPORTS = ("uniap_create", "uniap_destroy", "uniap_last_error", "uniap_status_string", "uniap_version",
            "uniap_solve_tables", "uniap_interval_table", "uniap_plan", "uniap_build_tables", "uniap_prepare",
            "uniap_prepare_tables", "uniap_run", "uniap_fetch", "uniap_shard_assign", "uniap_shard_tables",
-           "uniap_pick", "uniap_selftest",
+           "uniap_pick", "uniap_selftest", "uniap_fetch_intervals",
            "uniap_candidates", "uniap_catalogue")
 
 _lib = None
@@ -118,6 +118,7 @@ def lib():
         L.uniap_prepare_tables.argtypes = [H, C.POINTER(uniap_tables)]
         L.uniap_run.argtypes = [H, C.c_int32, C.c_int32, C.c_void_p]
         L.uniap_fetch.argtypes = [H, C.POINTER(uniap_result)]
+        L.uniap_fetch_intervals.argtypes = [H, _P32, C.c_int64]
         L.uniap_shard_assign.argtypes = [H, C.c_int32, _P32]
         L.uniap_shard_tables.argtypes = [C.POINTER(uniap_tables), C.c_int32, _P32]
         L.uniap_pick.argtypes = [C.POINTER(uniap_record), C.c_int32, C.POINTER(uniap_result)]
@@ -302,6 +303,7 @@ class Handle:
         if st != UNIAP_OK:
             raise UniapError(st, f"uniap_create(device={device}) failed: needs a compute-capability 10.x GPU")
         self.n_cfg = 0
+        self.device = device
 
     def close(self):
         if self._h:
@@ -321,7 +323,7 @@ class Handle:
 
     def solve_tables(self, t):
         tb, keep = _tables(t)
-        n = len(t["cfgs"])
+        n = self.n_cfg = len(t["cfgs"])
         cfg_obj = (C.c_int64 * n)()
         r = uniap_result()
         r.cfg_objective = cfg_obj
@@ -341,6 +343,7 @@ class Handle:
     def plan(self, p):
         """p: a profile dict or a Profile."""
         model, cluster, opts, keep, n = _structs(p)
+        self.n_cfg = n
         cfg_obj = (C.c_int64 * n)()
         r = uniap_result()
         r.cfg_objective = cfg_obj
@@ -398,6 +401,43 @@ class Handle:
         out = _result_dict(r, self.n_cfg, cfg_obj)
         out["status"] = st
         return out
+
+    def plan_distributed(self, p, group=None):
+        """Multi-GPU plan, one process per GPU: this rank runs
+        its LPT share of the candidate configs (uniap_run(rank, world)) on its
+        device, writing its best record into a device buffer; ONE all_gather of
+        the fixed-size records over the process group (NCCL over NVLink: the
+        device buffers directly; gloo: through host memory); uniap_pick on the
+        host.  Returns the picked result dict (every rank gets the same) plus
+        this rank's local per-config optima.  torch supplies only the memory
+        and the process group."""
+        import torch
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        self.prepare(p)
+        dev = torch.device("cuda", self.device)
+        rec = torch.zeros(RECORD_BYTES, dtype=torch.uint8, device=dev)
+        self.run(rank, world, rec.data_ptr())
+        local = self.fetch()  # synchronises the handle's stream: rec is complete
+        if dist.get_backend(group) == "nccl":
+            allr = torch.empty(world * RECORD_BYTES, dtype=torch.uint8, device=dev)
+            dist.all_gather_into_tensor(allr, rec, group=group)
+            host = allr.cpu().numpy().tobytes()
+        else:
+            parts = [torch.empty(RECORD_BYTES, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, rec.cpu(), group=group)
+            host = b"".join(x.numpy().tobytes() for x in parts)
+        st, out = pick(host, world)
+        out["status"] = st
+        out["cfg_objective_local"] = local.get("cfg_objective")
+        out["quantum_ns"] = local["quantum_ns"]
+        return out
+
+    def fetch_intervals(self, L):
+        """The last run's interval optima [n_cfg][L][L] (UNIAP_INF = infeasible or not needed)."""
+        P = np.zeros(self.n_cfg * L * L, dtype=np.int32)
+        self._check(lib().uniap_fetch_intervals(self._h, P.ctypes.data_as(_P32), P.size), "fetch_intervals")
+        return P.reshape(self.n_cfg, L, L)
 
     def shard_assign(self, world):
         owner = (C.c_int32 * max(self.n_cfg, 1))()

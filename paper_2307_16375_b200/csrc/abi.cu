@@ -71,6 +71,7 @@ struct RunPlan {
   std::vector<K2Group> fgrp, bgrp;
   std::vector<std::pair<int, int>> k4range;  // per forward group: its configs in `local`
   std::pair<int, int> k4rest{0, 0};          // configs without chain-DP work (deg > L)
+  int n_fw = 0;                              // forward instances (uploaded to h->inst)
   int max_deg = 0;
 };
 
@@ -106,7 +107,7 @@ struct uniap_handle {
   DevBuf<uniap_record> rec;
   // last run
   uniap_record rec_host{};
-  uint64_t cells_canon = 0;
+  uint64_t cells = 0, relax = 0, cells_canon = 0;
   float ms_dp = 0.f, ms_total = 0.f;
   int64_t quantum = 0;
   cudaEvent_t ev[4] = {};
@@ -121,6 +122,7 @@ struct uniap_handle {
   DevBuf<BwPlan> bwp;
   DevBuf<unsigned long long> trace;        // UNIAP_TRACE: K2 per-CTA timeline (diagnostics)
   DevBuf<unsigned long long> tim;          // forward K2 phase clock (see K2Args::tim)
+  DevBuf<unsigned long long> work;         // level 2: per config executed {cells, relax} (k1f_trim)
   cudaGraphExec_t graph_exec = nullptr;    // the captured pipeline of `plan`
   uint32_t graph_launches = 0, graph_k2 = 0;
   bool capturing = false, timed = false;
@@ -138,6 +140,11 @@ struct uniap_handle {
     int64_t cfgopt[UNIAP_MAX_CFG];
   }* fb = nullptr, *fb_dev = nullptr;  // mapped pinned block (host / device address), written by k_publish
   std::vector<int64_t> sig;                // what the captured graph depends on
+  // level 1 only: per (config, layer) the smallest M of the caller's tables
+  // over the config's strategies (cap + 1 = none fits); the plan stops each
+  // forward P sweep at its feasible prefix (Eq. 5).  Level 2: K1f does it on
+  // the device from the builder's M (k1f_trim).
+  std::vector<int32_t> minM;
 };
 
 // A prepared problem keeps the launch plan and the captured graph when
@@ -145,6 +152,7 @@ struct uniap_handle {
 // kernel-parameter values of the builder); otherwise both are rebuilt.
 static void update_signature(uniap_handle* h) {
   std::vector<int64_t> sg = {h->L, h->Q, h->ncfg, h->skip, h->level2, h->n_edges, h->arena_words};
+  for (int32_t m : h->minM) sg.push_back(m);  // level 1: the plan's sweep lengths depend on them
   for (int i = 0; i < h->ncfg; ++i) {
     const CfgDev& d = h->cfg[i];
     const K2Class& k = h->cls[i];
@@ -339,6 +347,9 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   h->iP.release();
   h->win.release();
   h->rec.release();
+  h->tim.release();
+  h->work.release();
+  h->trace.release();
   for (auto e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto e : h->side_ev) cudaEventDestroy(e);
@@ -468,6 +479,12 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
       if (ok || h->no_compact) keep[i].push_back(k);
     }
     if (keep[i].empty()) keep[i].push_back(0);  // all forbidden: the config is infeasible
+  }
+  h->minM.assign((size_t)h->ncfg * L, t->cap + 1);  // (min over given integers: no cost model)
+  for (int i = 0; i < h->ncfg; ++i) {
+    const uniap_config& x = t->cfg[i];
+    for (int u = 0; u < L; ++u)
+      for (int k : keep[i]) h->minM[(size_t)i * L + u] = std::min(h->minM[(size_t)i * L + u], x.M[u * x.n_strat + k]);
   }
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc);
   if (st != UNIAP_OK) return st;
@@ -621,6 +638,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   }
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc);
   if (st != UNIAP_OK) return st;
+  h->minM.clear();  // the sweep trim runs on the device (k1f_trim)
   h->cl = ClusterDev{cl->n_dev, cl->node_size, cl->ccoc_permille, o->B, o->precision, o->Q, NT, 0,
                      cl->mem_bytes, cl->mem_reserve_bytes, cl->bw_intra_Bps, cl->bw_inter_Bps, cl->p2p_Bps,
                      cl->lat_ns, o->quantum_ns};
@@ -736,11 +754,32 @@ static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>&
 }
 
 static void forward_instances(const uniap_handle* h, int i, bool all_intervals, std::vector<Inst>& out) {
-  // (each P-emitting sweep stops at its feasible prefix inside K2, from the
-  // quantised memory table: k2_feasible_len)
   const CfgDev& d = h->cfg[i];
+  const size_t first = out.size();
   if (all_intervals) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, out);
   else plan_fast(h->L, i, d.deg, d.S, d.skip, out);
+  for (size_t j = first; j < out.size(); ++j) out[j].n0 = out[j].n;
+  // Level 1: stop each forward P sweep where it becomes infeasible -- the
+  // memory sum of Eq. 5 over the layers swept is at least the running sum of
+  // the per-layer minima of the caller's M, so past the first layer where
+  // that exceeds cap every state is INF and the interval optima stay INF
+  // from the fill (exact; K2 clamps its emitted range to the n it sweeps).
+  // G-storing sweeps (deg = 1's kept tables) run in full.  Level 2: K1f.
+  if (all_intervals || h->minM.empty()) return;
+  const int L = h->L;
+  for (size_t j = first; j < out.size(); ++j) {
+    Inst& x = out[j];
+    if (x.emit != 1 && x.emit != 2) continue;
+    int64_t sum = 0;
+    int n = 0;
+    for (; n < x.n; ++n) {
+      sum += h->minM[(size_t)i * L + x.a + x.dir * n];  // (a lower bound also at a conditioned skip layer)
+      if (sum > h->cap) break;
+    }
+    x.n = std::max(n, 1);
+    if (x.dir > 0) x.ehi = std::min(x.ehi, x.a + x.n - 1);  // emit only the layers swept
+    else x.elo = std::max(x.elo, x.a - x.n + 1);
+  }
 }
 
 // LPT over configs by executed chain-DP work (sum over the sweeps of n |S|^2 Q); ties
@@ -930,8 +969,8 @@ static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, De
 
 static BuildBufs build_bufs(uniap_handle* h) {
   return BuildBufs{h->fwd.p, h->act.p, h->ps.p, h->ctx.p, h->tpc.p, h->chain.p, h->skipb.p, h->edges.p,
-                   h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->dcat.p, h->ns.p, h->qcfg.p, h->qmax.p,
-                   h->qglob.p};
+                   h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->dcat.p, nullptr, 0, nullptr, h->ns.p,
+                   h->qcfg.p, h->qmax.p, h->qglob.p};
 }
 
 // ---------------------------------------------------------------------------
@@ -949,9 +988,16 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   // forward instances
   std::vector<Inst> fw;
   for (int i : R.local) forward_instances(h, i, false, fw);
-  // executed cells / relaxations are counted by the K2 launches themselves
-  // (the feasible-prefix trim is decided on the device); the canonical count
-  // is the workload size
+  // executed cells / relaxations: level 1 from the host-trimmed plan, level 2
+  // counted by K1f where it trims (k1f_trim); the canonical count is the
+  // workload size
+  h->cells = h->relax = 0;
+  for (auto& x : fw) {
+    const uint64_t S = h->cfg[x.cfg].S;
+    if (S == 1) continue;  // closed form (k2_closed_s1): no DP cells
+    h->cells += (uint64_t)x.n * S * h->Q;
+    h->relax += (uint64_t)(x.n - 1) * S * S * h->Q;
+  }
   h->cells_canon = 0;
   for (int i : R.local) {
     std::vector<Inst> cv;
@@ -959,6 +1005,7 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     for (auto& x : cv) h->cells_canon += (uint64_t)x.n * h->cfg[i].Sfull * h->Q;
   }
   group_instances(h, fw, R.fgrp);
+  R.n_fw = (int)fw.size();
   // local configs ordered by forward group, so each group's K4 takes a range
   {
     std::vector<int32_t> ordered;
@@ -980,7 +1027,8 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     R.k4rest = {rest0, (int)ordered.size() - rest0};
     R.local.swap(ordered);
   }
-  CK(h, h->tim.ensure(4));
+  CK(h, h->tim.ensure(2));
+  CK(h, h->work.ensure(2 * (size_t)h->ncfg));
   // backward: one device-sized launch per kernel class of the local configs
   std::vector<int32_t> cls_of_cfg(h->ncfg, 0);
   R.bgrp.clear();
@@ -1070,14 +1118,18 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     if (s != UNIAP_OK) return s;
     CK(h, cudaEventRecord(h->fork_ev, h->st));
     CK(h, cudaStreamWaitEvent(h->side[0], h->fork_ev, 0));
-    CK(h, cudaMemsetAsync(h->tim.p, 0, 4 * sizeof(unsigned long long), h->side[0]));  // forward phase clock + work
+    CK(h, cudaMemsetAsync(h->tim.p, 0, 2 * sizeof(unsigned long long), h->side[0]));  // forward phase clock
     CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->side[0]));
     CK(h, cudaEventRecord(h->side_ev[0], h->side[0]));
-    CK(h, launch_k1(h->cl, build_bufs(h), h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
+    BuildBufs bb = build_bufs(h);
+    bb.inst = h->inst.p;  // K1f trims the forward sweeps of this plan (k1f_trim)
+    bb.n_inst = R.n_fw;
+    bb.work = h->work.p;
+    CK(h, launch_k1(h->cl, bb, h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
     CK(h, cudaStreamWaitEvent(h->st, h->side_ev[0], 0));
     h->launches += 3;
   } else {
-    CK(h, cudaMemsetAsync(h->tim.p, 0, 4 * sizeof(unsigned long long), h->st));  // forward phase clock + work
+    CK(h, cudaMemsetAsync(h->tim.p, 0, 2 * sizeof(unsigned long long), h->st));  // forward phase clock
     CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
   }
   h->launches++;
@@ -1091,7 +1143,7 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     if (s != UNIAP_OK) return s;
   }
 
-  RecordArgs ra{rec, h->tim.p + 2, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
+  RecordArgs ra{rec, h->cells, h->relax, h->level2 ? h->work.p : nullptr, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
                 h->binst.p, h->bwp.p, h->gstore.p};
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
                    h->cfgopt.p, h->scratch.p, h->win.p, ra, h->st));
@@ -1274,6 +1326,17 @@ extern "C" uniap_status uniap_interval_table(uniap_handle* h, const uniap_tables
   CK(h, d2h(h, P_out, h->iP.p + h->cfg[cfg].offP, (size_t)L * L * 4));
   CK(h, cudaStreamSynchronize(h->st));
   CK(h, cudaGetLastError());
+  return UNIAP_OK;
+}
+
+extern "C" uniap_status uniap_fetch_intervals(uniap_handle* h, int32_t* P_out, int64_t P_len) {
+  if (!h || !P_out) return UNIAP_ERR_ARG;
+  if (!h->last_rec || !h->plan.valid || !h->P.p) FAIL(h, UNIAP_ERR_ARG, "nothing has run on this handle");
+  const int64_t n = (int64_t)h->ncfg * h->L * h->L;
+  if (P_len < n) FAIL(h, UNIAP_ERR_ARG, "P_len %lld < %lld", (long long)P_len, (long long)n);
+  CK(h, cudaSetDevice(h->device));
+  CK(h, d2h(h, P_out, h->P.p, (size_t)n * 4));
+  CK(h, cudaStreamSynchronize(h->st));
   return UNIAP_OK;
 }
 

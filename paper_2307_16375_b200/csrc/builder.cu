@@ -313,10 +313,92 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
   }
 }
 
-// K1f: quantise into the int32 device layout (A, M buckets, Rt, Rf, Rs, O).
+// Memory bucket of a byte count (reading A-8): ceil(bytes / unit), cap + 1
+// (= forbidden) when it does not fit or the strategy is forbidden (bytes < 0).
+__device__ __forceinline__ int32_t mem_bucket(int64_t byt, int64_t unit, int cap) {
+  const int64_t bk = byt < 0 ? (int64_t)cap + 1 : (byt + unit - 1) / unit;
+  return (int32_t)(bk > cap ? cap + 1 : bk);
+}
+
+// K1f role of the last block column: the feasible prefix of every forward
+// P-emitting sweep of config blockIdx.y (one warp per sweep, lanes over its
+// layers).  Eq. 5 bounds the memory of every state at the i-th layer swept
+// by cap, and that memory is at least the running sum of each swept layer's
+// smallest bucket (only M[s][ks] at the skip source of a conditioned copy);
+// past the first layer where the sum exceeds cap every state is INF, so the
+// sweep stops there (Inst::n) and the later interval optima stay INF from
+// the fill.  Exact; computed from the builder's own M, rewritten every run
+// from the planned length n0.
+__device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev& cf, int cfg_id) {
+  __shared__ unsigned long long wsum[2];
+  const int cap = cl.Q - 1;
+  const int64_t unit = (cl.mem_bytes - cl.mem_reserve) / cap;
+  const int64_t* M = bb.ns + cf.offM;
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (threadIdx.x < 2) wsum[threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned long long S = cf.S, Qw = cl.Q;
+  for (int j = threadIdx.x >> 5; j < bb.n_inst; j += nw) {
+    const Inst in = bb.inst[j];
+    if (in.cfg != cfg_id) continue;
+    if (in.emit != 1 && in.emit != 2) {  // a G-keeping sweep runs in full
+      if (lane == 0 && S > 1) {          // (|S| = 1: the closed form, no DP cells)
+        atomicAdd(&wsum[0], (unsigned long long)in.n0 * S * Qw);
+        atomicAdd(&wsum[1], (unsigned long long)(in.n0 - 1) * S * S * Qw);
+      }
+      continue;
+    }
+    int pre = 0, first = in.n0;
+    for (int h = 0; h * 32 < in.n0; ++h) {
+      const int i = h * 32 + lane;
+      int mn = 0;
+      if (i < in.n0) {
+        const int u = in.a + in.dir * i;
+        mn = cap + 1;
+        if (in.ks >= 0 && u == cf.skip) {
+          mn = mem_bucket(M[u * cf.NSP + in.ks], unit, cap);
+        } else {
+          for (int k = 0; k < cf.S; ++k) mn = min(mn, mem_bucket(M[u * cf.NSP + k], unit, cap));
+        }
+      }
+      int x = mn;  // inclusive scan over this half's layers
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      x += pre;
+      const unsigned bad = __ballot_sync(0xffffffffu, i < in.n0 && x > cap);
+      if (bad && first == in.n0) first = h * 32 + __ffs(bad) - 1;
+      pre = __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) {
+      const int n = max(first, 1);
+      bb.inst[j].n = n;
+      // the emitted range within the layers swept (planned: forward elo = a,
+      // ehi = a + n0 - 1; backward elo = a - n0 + 1)
+      if (in.dir > 0) bb.inst[j].ehi = in.a + n - 1;
+      else bb.inst[j].elo = in.a - n + 1;
+      if (S > 1) {
+        atomicAdd(&wsum[0], (unsigned long long)n * S * Qw);
+        atomicAdd(&wsum[1], (unsigned long long)(n - 1) * S * S * Qw);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) bb.work[2 * cfg_id + threadIdx.x] = wsum[threadIdx.x];
+}
+
+// K1f: quantise into the int32 device layout (A, M buckets, Rt, Rf, Rs, O);
+// the last block column trims the forward sweeps (k1f_trim).
 __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int32_t* arena) {
   TraceScope tr(TR_K1F);
   const CfgDev cf = cfgs[blockIdx.y];
+  if (blockIdx.x == gridDim.x - 1) {
+    if (bb.inst) k1f_trim(cl, bb, cf, blockIdx.y);
+    return;
+  }
+  const int nqb = gridDim.x - 1;  // quantising blocks
   const int NSP = cf.NSP, n2 = NSP * NSP;
   const int64_t q = bb.qglob[0] > 0 ? bb.qglob[0] : 1;
   const int cap = cl.Q - 1;
@@ -325,14 +407,12 @@ __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restri
   const bool pow2 = (q & (q - 1)) == 0;
   const int sh = __ffsll(q) - 1;
   auto qt = [&](int64_t x) { return (int32_t)(pow2 ? (x + q - 1) >> sh : (x + q - 1) / q); };
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nA + nR + nS + nO; idx += gridDim.x * blockDim.x) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nA + nR + nS + nO; idx += nqb * blockDim.x) {
     int j = idx;
     if (j < nA) { arena[cf.offA + j] = qt(bb.ns[cf.offA + j]); continue; }
     j -= nA;
     if (j < nA) {
-      const int64_t byt = bb.ns[cf.offM + j];
-      int64_t bk = byt < 0 ? (int64_t)cap + 1 : (byt + unit - 1) / unit;
-      arena[cf.offM + j] = (int32_t)(bk > cap ? cap + 1 : bk);
+      arena[cf.offM + j] = mem_bucket(bb.ns[cf.offM + j], unit, cap);
       continue;
     }
     j -= nA;
@@ -358,7 +438,7 @@ cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* c
   const int nbR = 2 * L - 1;  // one block per edge slot: L-1 chain edges, L skip destinations
   k1_costs<<<dim3(nbA + nbR + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR);
   k1d_quantum<<<ncfg, 64, 0, st>>>(cl, bb, cfg, L, skip);
-  k1f_quantise<<<dim3(16, ncfg), 256, 0, st>>>(cl, bb, cfg, L, arena);
+  k1f_quantise<<<dim3(16 + 1, ncfg), 256, 0, st>>>(cl, bb, cfg, L, arena);
   return cudaGetLastError();
 }
 

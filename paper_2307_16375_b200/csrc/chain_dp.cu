@@ -22,7 +22,7 @@ int k2_ns_round(int S) {
 
 static size_t smem_words(int NS, int B, int ne = 2) {
   const int NSP = (NS + 3) & ~3;
-  return (size_t)ne * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP) + MAXL + 4;  // + the sweep-length word
+  return (size_t)ne * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP) + MAXL;
 }
 
 size_t k2_smem_bytes(const K2Class& c) { return smem_words(c.NS, c.T * c.V, c.DB ? 2 : 1) * sizeof(int32_t); }

@@ -114,49 +114,6 @@ struct Stage {
   static constexpr int WORDS = NS * NSP + 2 * NSP;
 };
 
-// Feasible prefix of a P-emitting sweep (warp-collective, lanes over the
-// swept layers; exact).  Eq. 5 bounds the memory of every state at the i-th
-// layer swept by cap, and that memory is at least the running sum of each
-// swept layer's smallest M (only M[s][ks] at the skip source of a
-// conditioned copy); past the first layer where that sum exceeds cap every
-// state is INF, so the sweep stops there and the later interval optima stay
-// INF from the fill.  Computed from the quantised M on the device, so the
-// host plan holds no cost-model arithmetic.  Returns the number of layers to
-// sweep (>= 1).
-template <int NS>
-__device__ __forceinline__ int k2_feasible_len(int a, int n, int dir, int ks, const int32_t* __restrict__ gM, int skip,
-                                                int cap) {
-  constexpr int NSP = (NS + 3) & ~3;
-  const int lane = threadIdx.x & 31;
-  int pre = 0, first = n;  // running sum, first infeasible step
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int i = h * 32 + lane;
-    int mn = 0;
-    if (i < n) {
-      const int u = a + dir * i;
-      mn = cap + 1;
-      if (ks >= 0 && u == skip) {
-        mn = min(mn, __ldg(gM + (int64_t)u * NSP + ks));
-      } else {
-#pragma unroll
-        for (int k = 0; k < NS; ++k) mn = min(mn, __ldg(gM + (int64_t)u * NSP + k));
-      }
-    }
-    int x = mn;  // inclusive scan over the 32 layers of this half
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    x += pre;
-    const unsigned bad = __ballot_sync(0xffffffffu, i < n && x > cap);
-    if (bad && first == n) first = h * 32 + __ffs(bad) - 1;
-    pre = __shfl_sync(0xffffffffu, x, 31);
-  }
-  return max(first, 1);
-}
-
 template <int NS, int V, int T, bool CL, bool DB = true>
 __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   static_assert(DB || !CL, "single-buffered E only without clusters");
@@ -171,8 +128,6 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   int32_t* sE = reinterpret_cast<int32_t*>(smem4);  // [2][NS][ROW]
   int32_t* sT = sE + NE * NS * ROW;                 // [3][SW] staged tables
   int32_t* sProw = sT + 3 * SW;                     // [MAXL] this instance's P[a][.]
-  int& s_len = *reinterpret_cast<int*>(sProw + MAXL);  // the sweep length (dynamic shared memory: no
-                                                        // static shared, so the full opt-in size is available)
   const int t = threadIdx.x;
   int rank = 0, ii = blockIdx.x;
   if constexpr (CL) {
@@ -192,12 +147,6 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   const int L = args.L;
 
   for (int r = t; r < NE * NS; r += T) *reinterpret_cast<int4*>(sE + r * ROW) = make_int4(INF, INF, INF, INF);
-  // sweep length: a P-emitting sweep stops at its feasible prefix; a sweep
-  // that keeps its G tables (traceback) runs in full
-  if (t < 32) {
-    const int nl = (in.emit == 1 || in.emit == 2) ? k2_feasible_len<NS>(in.a, in.n, in.dir, in.ks, gM, skip, cap) : in.n;
-    if (t == 0) s_len = nl;
-  }
 
   // ---- tables of one layer step, staged by the whole CTA ----------------
   // word w of a stage: R rows (w < NS*NSP), then (A', M) pairs.  A' adds the
@@ -307,10 +256,8 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   if (in.n > 2) fetch_stage(2, u + 2 * in.dir);
   __syncthreads();
   emit(u);
-  // s_len (the trimmed length) is re-read from shared memory where used,
-  // after the barriers, so it holds no register across the main loop
 
-  for (int step = 1; step < s_len; ++step) {
+  for (int step = 1; step < in.n; ++step) {
     u += in.dir;
     int32_t* Eb = sE + (DB ? (step & 1) * NS * ROW : 0) + 4;  // row 0, bucket 0
     const int32_t* Tb = sT + (step % 3) * SW;
@@ -356,13 +303,13 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       if constexpr (NS - NFULL > 0) rows(std::integral_constant<int, NS - NFULL>{}, NFULL);
     }
     // stage the tables of the step after next, then one barrier per layer
-    if (step + 1 < s_len) store_stage(step + 1);
+    if (step + 1 < in.n) store_stage(step + 1);
     // Split-phase: arrive on the cluster barrier (release E), issue the next
     // table fetch (after the release, so its fence does not wait for it),
     // sync the CTA, shift from the local E while the other CTAs catch up,
     // then wait (acquire) before the few reads from a lower CTA's range.
     if constexpr (CL) cl_arrive();
-    if (step + 2 < s_len) fetch_stage(step + 2, u + 2 * in.dir);
+    if (step + 2 < in.n) fetch_stage(step + 2, u + 2 * in.dir);
     __syncthreads();
     // ---- shift by the layer's memory, add A' ----
     // Byte addresses in the shared window: row k's bucket x sits at
@@ -431,10 +378,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   // the forward sweep's stage optima P[a][a..a+n-1], from its owner thread
   if (eP && rank == cap / B && t == (cap - (cap / B) * B) % T) {
     int32_t* Pc = args.P + cf.offP;
-    // the layers swept: a .. a + s_len - 1 (forward) or a - s_len + 1 .. a
-    const int lo = in.dir > 0 ? in.elo : max(in.elo, in.a - s_len + 1);
-    const int hi = in.dir > 0 ? min(in.ehi, in.a + s_len - 1) : in.ehi;
-    for (int uu = lo; uu <= hi; ++uu) {
+    for (int uu = in.elo; uu <= in.ehi; ++uu) {  // (the trim keeps [elo, ehi] inside the layers swept)
       int32_t* dst = in.dir > 0 ? Pc + (int64_t)in.a * L + uu : Pc + (int64_t)uu * L + in.a;
       if ((in.emit & 3) == 2) atomicMin(dst, sProw[uu]);
       else *dst = sProw[uu];
@@ -445,17 +389,12 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   if (args.tim && t == 0) {  // the forward phase's device time (uniap_fetch: ms_gpu_dp)
     atomicMax(args.tim, ~t_start);
     atomicMax(args.tim + 1, gtimer());
-    if (rank == 0) {  // executed work of the forward phase: cells and relaxations (|S| of the config)
-      const unsigned long long S = (unsigned long long)cf.S, Qw = (unsigned long long)Q;
-      atomicAdd(args.tim + 2, (unsigned long long)s_len * S * Qw);
-      atomicAdd(args.tim + 3, (unsigned long long)(s_len - 1) * S * S * Qw);
-    }
   }
 }
 
 template <int NS>
 constexpr size_t k2_smem(int B, int ne = 2) {
-  return (size_t)(ne * NS * (B + 4) + 3 * Stage<NS>::WORDS + MAXL + 4) * sizeof(int32_t);
+  return (size_t)(ne * NS * (B + 4) + 3 * Stage<NS>::WORDS + MAXL) * sizeof(int32_t);
 }
 
 // Instantiation helper used by the per-NS translation units: only the shapes

@@ -455,8 +455,17 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     r->L = ra.L;
     r->status = (ra.qglob && ra.qglob[1] != 0) ? UNIAP_ERR_RANGE : 0;
     r->n_cfg_local = ra.n_local;
-    r->dp_cells = ra.work[0];
-    r->dp_relax = ra.work[1];
+    r->dp_cells = ra.cells;
+    r->dp_relax = ra.relax;
+    if (ra.work) {  // level 2: the counts K1f made where it trimmed the sweeps
+      unsigned long long c = 0, x = 0;
+      for (int li = 0; li < ra.n_local; ++li) {
+        c += ra.work[2 * cfg_list[li]];
+        x += ra.work[2 * cfg_list[li] + 1];
+      }
+      r->dp_cells = c;
+      r->dp_relax = x;
+    }
     r->dp_cells_canonical = ra.cells_canon;
   }
   if (wl < 0) {
@@ -676,7 +685,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
           continue;
         }
         ra.bw->gofs[i * 33 + ks + 1] = goff;
-        ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1};
+        ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1, len};
         goff += (int64_t)len * cf.NSP * (ra.cap + 1);
       }
       a = b + 1;

@@ -43,7 +43,9 @@ struct CfgDev {
 struct Inst {
   int32_t cfg;   // config index
   int32_t a;     // first layer swept
-  int32_t n;     // number of layers swept (>= 1)
+  int32_t n;     // number of layers swept (>= 1): a P-emitting sweep's feasible prefix of n0
+                 // (Eq. 5: past it every state is INF), set by the host (level 1) or K1f (level 2),
+                 // which also shrink [elo, ehi] to the layers swept
   int32_t ks;    // skip-source conditioning (-1 = none)
   int32_t dir;   // +1 forward (emit P[a][u]), -1 backward (store G[u])
   int32_t emit;  // 1: P plain store, 2: P atomicMin (several copies), 0: store G (traceback);
@@ -54,6 +56,7 @@ struct Inst {
   // forward sweep (intervals starting at a), P[u][a] for a backward sweep
   // (intervals ending at a: the suffix sweep of the last stage)
   int32_t elo, ehi;
+  int32_t n0;    // the planned length (the layers a placement can use)
 };
 
 struct K2Args {
@@ -68,8 +71,7 @@ struct K2Args {
   unsigned long long* trace = nullptr;
   uint32_t tag = 0;
   // forward-phase clock (%globaltimer, ns): tim[0] = max of ~start, tim[1] =
-  // max of end over the launch's CTAs; tim[2], tim[3] = executed cells and
-  // relaxations (all reset to 0 per run), or nullptr
+  // max of end over the launch's CTAs (both reset to 0 per run), or nullptr
   unsigned long long* tim = nullptr;
 };
 
@@ -153,7 +155,8 @@ struct BwPlan {
 };
 struct RecordArgs {          // what K5a writes into the record besides the winner
   uniap_record* rec;
-  const unsigned long long* work;  // forward-phase cells, relaxations (accumulated by the K2 launches)
+  uint64_t cells, relax;           // executed forward-phase work (level 1: the host plan), or
+  const unsigned long long* work;  // level 2: per config {cells, relax} written by K1f (k1f_trim)
   uint64_t cells_canon;
   int32_t n_local, L, cap;
   const int64_t* qglob;      // builder flags (level 2) or nullptr
@@ -206,6 +209,9 @@ struct BuildBufs {
   const int64_t* chain_mat;  // [L] word offset into rmat of edge u->u+1's matrix, -1 none
   const int64_t* skip_mat;   // [L] word offset of edge skip->v's matrix, -1 none
   const CatDev* cat;      // [ncfg]
+  Inst* inst;             // the forward instances of the run (K1f writes each P sweep's feasible length)
+  int32_t n_inst;
+  unsigned long long* work;  // [ncfg][2] executed cells, relaxations of each config's forward sweeps
   int64_t* ns;            // int64 scratch arena, same offsets as the int32 arena
   int64_t* qcfg;          // [ncfg] smallest passing quantum per config
   int64_t* qmax;          // [ncfg][MAXL][4] per layer: max A, max R into u, max Rskip into u, O[u]

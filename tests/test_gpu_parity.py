@@ -217,13 +217,19 @@ def test_bad_tables_rejected(h):
     assert e.value.status == 3
 
 
-def test_world_size_invariance(h):
+@pytest.mark.parametrize("name", ["vit", "t5"])
+def test_world_size_invariance(h, orc, name):
     """Shards of world 2/4/8 run one after another on one GPU ("fake world"),
-    records picked on the host == the world-1 answer."""
+    records picked on the host == the ORACLE's plan (the a-8 exchange path
+    against the independent answer) and == the world-1 work counters
+    (SURVEY.md T4)."""
     import torch
     import paper_2307_16375_b200 as pkg
-    p = profiles.make_profile("vit")
+    p = profiles.make_profile(name)
+    want, _ = orc.plan(p, n_threads=0)
     ref = h.plan(p)
+    for k in ("objective", "deg", "c", "cfg_index", "stage_of", "strategy_of", "stage_cost", "cut_cost", "stage_mem"):
+        assert ref[k] == want[k], (1, k)
     for world in (2, 4, 8):
         h.prepare(p)
         recs = b""
@@ -234,7 +240,9 @@ def test_world_size_invariance(h):
             recs += buf.cpu().numpy().tobytes()
         st, r = pkg.pick(recs, world)
         for k in ("objective", "deg", "c", "cfg_index", "stage_of", "strategy_of", "stage_cost", "cut_cost",
-                  "stage_mem", "dp_cells", "dp_relax", "dp_cells_canonical"):
+                  "stage_mem"):
+            assert r[k] == want[k], (world, k)
+        for k in ("dp_cells", "dp_relax", "dp_cells_canonical"):
             assert r[k] == ref[k], (world, k)
 
 
