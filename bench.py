@@ -94,18 +94,51 @@ def _dist():
     return ws, rank, local
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(profile, cells, n_threads=None):
     """The oracle as it stands (oracle/, C, -O2 -march=native) on the host
-    cores: the whole workload once (a bounded sample: ~1-10 s on the survey box)."""
+    cores: the whole workload once on every core (threads over the candidate
+    configs), and once on one thread (a bounded sample: ~1-20 s)."""
     from oracle import oracle
     oracle.build_oracle()
     n = n_threads or os.cpu_count() or 1
     t0 = time.perf_counter()
     res, _ = oracle.plan(profile, n_threads=n)
     dt = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    res1, _ = oracle.plan(profile, n_threads=1)
+    dt1 = time.perf_counter() - t0
+    assert res1["objective"] == res["objective"]
     return {"value": cells / dt, "unit": UNIT, "cores": min(n, len(res["cfg_objective"])), "kind": "oracle",
-            "sample": f"whole workload, 1 oracle run ({dt:.2f} s); cells counted as the GPU path's "
-                      f"algorithmic cells of the same workload", "seconds": dt, "objective": res["objective"]}
+            "sample": f"whole workload, 1 oracle run on {min(n, len(res['cfg_objective']))} threads ({dt:.2f} s) "
+                      f"and 1 on one thread ({dt1:.2f} s); cells = the GPU path's canonical cells of the same workload",
+            "seconds": dt, "single_thread": {"value": cells / dt1, "seconds": dt1, "cores": 1},
+            "cpu_model": cpu_model(), "host_cores": os.cpu_count(), "objective": res["objective"]}
+
+
+def bench_config(args, profile, ws, n_cfg):
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": WORKLOAD_NAMES.get(args.workload, args.workload), "L": profile["model"]["L"],
+            "devices_planned": profile["cluster"]["n_dev"], "B": profile["options"]["B"],
+            "Q": profile["options"]["Q"], "candidates": n_cfg,
+            "l2": "256 MiB memset between timed steps (flush)", "parallelism": f"configs-lpt{ws}"}
+
+
+def measured_alu():
+    """MEASURED_ALU.json (tools/alu_peak.py, this pool's B200): the DPX rate."""
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_ALU.json")))
+    except (OSError, ValueError):
+        return None
 
 
 def run_reference(args, profile, cells):
@@ -127,10 +160,12 @@ def run_reference(args, profile, cells):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": WORKLOAD_NAMES.get(args.workload, args.workload)},
+            "config": bench_config(args, profile, ws, len(res["cfg_objective"])),
+            "opt_time_s": ms / 1000.0,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": n, "kind": "oracle",
-                             "sample": f"whole workload per step, {args.steps} steps"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": min(n, len(res["cfg_objective"])), "kind": "oracle",
+                             "sample": f"whole workload per step, {args.steps} steps on {n} host threads",
+                             "cpu_model": cpu_model(), "host_cores": os.cpu_count()},
             "objective": res["objective"]}
     print(json.dumps(line), flush=True)
 
@@ -152,16 +187,9 @@ def main():
     import torch
     ws, rank, local = _dist()
     if args.impl == "reference":
-        # the algorithmic cell count of the workload (the same unit as our arm)
-        cells = None
-        if torch.cuda.is_available():
-            import paper_2307_16375_b200 as pkg
-            h = pkg.Handle(0)
-            cells = h.plan(profile)["dp_cells_canonical"]
-            h.close()
-        else:
-            cells = _cells_host(profile)
-        run_reference(args, profile, cells)
+        # the canonical cell count of the workload (the same unit as our arm),
+        # counted on the host: the reference arm loads nothing of the product
+        run_reference(args, profile, _cells_host(profile))
         return
 
     import torch.distributed as dist
@@ -208,6 +236,9 @@ def main():
             times.append(e0.elapsed_time(e1))
             dp_ms.append(h.fetch()["ms_gpu_dp"])
     r = h.fetch()
+    if ws > 1:  # the winner of the whole job (the timed steps ran the exchange): pick over every rank's record
+        _, won = pkg.pick(all_recs.cpu().numpy().tobytes(), ws)
+        r.update({k: won[k] for k in ("objective", "deg", "c")})
     ms_local = statistics.mean(times)
     # the workload size: cells of the canonical plan (one forward sweep per
     # start layer); the solver executes fewer (suffix
@@ -268,7 +299,16 @@ def main():
     if rank == 0:
         clocks = clk.summary()
         sm_max = clocks.get("sm_max_mhz") or 1965.0
-        peak = SM_COUNT * ALU_LANES_PER_SM * sm_max * 1e6 / 1e12  # T relax/s
+        alu = measured_alu()
+        if alu:
+            peak = alu["peak_relax_per_s"] / 1e12  # T relax/s, measured (tools/alu_peak.py)
+            peak_source = (f"measured: MEASURED_ALU.json (tools/alu_peak.py, {alu['when']}): "
+                           f"{alu['viaddmnmx_per_clk_per_sm']:.1f} VIADDMNMX/clk/SM x {alu['sms']} SMs at "
+                           f"{alu['clocks']['sm_mhz_median_under_load']} MHz under load")
+        else:
+            peak = SM_COUNT * ALU_LANES_PER_SM * sm_max * 1e6 / 1e12
+            peak_source = (f"derived (MEASURED_ALU.json absent): {SM_COUNT} SMs x {ALU_LANES_PER_SM} alu lanes/clk x "
+                           f"{sm_max:.0f} MHz (B300_MICROARCH alu pipe rt=2; DESIGN.md Sec. 4)")
         achieved = relax_local / (statistics.mean(dp_ms) / 1000.0) / 1e12 if dp_ms and dp_ms[0] > 0 else None
         traffic = None
         summ = os.path.join(ROOT, "profiles", "ncu_k2_summary.json")
@@ -281,12 +321,12 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": WORKLOAD_NAMES[args.workload], "L": profile["model"]["L"],
-                       "devices_planned": profile["cluster"]["n_dev"], "B": profile["options"]["B"],
-                       "Q": profile["options"]["Q"], "candidates": len(r["cfg_objective"]),
-                       "l2": "256 MiB memset between timed steps (flush)", "parallelism": f"configs-lpt{ws}"},
-            "opt_time_s": ms / 1000.0,
+            "config": bench_config(args, profile, ws, len(r["cfg_objective"])),
+            "opt_time_s": ms / 1000.0, "e2e_opt_time_s": e2e_s,
             "cells_executed_per_step": r["dp_cells"], "cells_canonical_per_step": r["dp_cells_canonical"],
+            "cells_executed_per_s": float(r["dp_cells"]) * ws / (ms / 1000.0) if ws == 1 else None,
+            "value_note": "value = canonical cells (one forward sweep per start layer: the problem size) / device "
+                          "time, an effective rate; cells_executed_per_s = the cells the solver's plan executes",
             "e2e": {"value": cells / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d_per_step,
                     "d2h_bytes_per_step": d2h_per_step, "seconds_per_step": e2e_s,
                     "path": "uniap_plan = uniap_prepare (validate + H2D of the ABI profile) + uniap_run + uniap_fetch "
@@ -296,8 +336,7 @@ def main():
             "roofline": {"bound": "alu", "kernel": "k2_chain (VIADDMNMX min-plus)", "achieved": achieved,
                          "peak": peak, "unit": "Trelax/s", "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic,
-                         "peak_source": f"derived: {SM_COUNT} SMs x {ALU_LANES_PER_SM} alu lanes/clk x "
-                                        f"{sm_max:.0f} MHz (B300_MICROARCH alu pipe rt=2; DESIGN.md Sec. 4)",
+                         "peak_source": peak_source,
                          "algorithmic_relax_per_step": relax_local, "k2_ms_per_step": statistics.mean(dp_ms)},
             "clocks": clocks,
             "objective": r["objective"], "plan": {"deg": r["deg"], "c": r["c"]},

@@ -71,7 +71,6 @@ struct RunPlan {
   std::vector<K2Group> fgrp, bgrp;
   std::vector<std::pair<int, int>> k4range;  // per forward group: its configs in `local`
   std::pair<int, int> k4rest{0, 0};          // configs without chain-DP work (deg > L)
-  int n_fw = 0;                              // forward instances (uploaded to h->inst)
   int max_deg = 0;
 };
 
@@ -123,6 +122,7 @@ struct uniap_handle {
   DevBuf<unsigned long long> trace;        // UNIAP_TRACE: K2 per-CTA timeline (diagnostics)
   DevBuf<unsigned long long> tim;          // forward K2 phase clock (see K2Args::tim)
   DevBuf<unsigned long long> work;         // level 2: per config executed {cells, relax} (k1f_trim)
+  DevBuf<int32_t> inst_csr;                // per config: its forward instances (offsets [ncfg+1], indices)
   cudaGraphExec_t graph_exec = nullptr;    // the captured pipeline of `plan`
   uint32_t graph_launches = 0, graph_k2 = 0;
   bool capturing = false, timed = false;
@@ -349,6 +349,7 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   h->rec.release();
   h->tim.release();
   h->work.release();
+  h->inst_csr.release();
   h->trace.release();
   for (auto e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -969,7 +970,7 @@ static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, De
 
 static BuildBufs build_bufs(uniap_handle* h) {
   return BuildBufs{h->fwd.p, h->act.p, h->ps.p, h->ctx.p, h->tpc.p, h->chain.p, h->skipb.p, h->edges.p,
-                   h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->dcat.p, nullptr, 0, nullptr, h->ns.p,
+                   h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->dcat.p, nullptr, nullptr, nullptr, nullptr, h->ns.p,
                    h->qcfg.p, h->qmax.p, h->qglob.p};
 }
 
@@ -1005,7 +1006,6 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     for (auto& x : cv) h->cells_canon += (uint64_t)x.n * h->cfg[i].Sfull * h->Q;
   }
   group_instances(h, fw, R.fgrp);
-  R.n_fw = (int)fw.size();
   // local configs ordered by forward group, so each group's K4 takes a range
   {
     std::vector<int32_t> ordered;
@@ -1086,6 +1086,15 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   CK(h, h->win.ensure(1));
   CK(h, h->bwp.ensure(1));
   if (!fw.empty()) CK(h, h2d(h, h->inst.p, fw.data(), fw.size() * sizeof(Inst)));
+  {  // per config: its forward instances in the uploaded (grouped) order, for K1f's trim
+    std::vector<int32_t> csr(h->ncfg + 1 + fw.size(), 0);
+    for (auto& x : fw) csr[x.cfg + 1]++;
+    for (int i = 0; i < h->ncfg; ++i) csr[i + 1] += csr[i];
+    std::vector<int32_t> fill(csr.begin(), csr.begin() + h->ncfg);
+    for (size_t j = 0; j < fw.size(); ++j) csr[h->ncfg + 1 + fill[fw[j].cfg]++] = (int32_t)j;
+    CK(h, h->inst_csr.ensure(csr.size()));
+    CK(h, h2d(h, h->inst_csr.p, csr.data(), csr.size() * 4));
+  }
   if (nl > 0) CK(h, h2d(h, h->cfglist.p, R.local.data(), nl * 4));
   CK(h, h2d(h, h->clsid.p, cls_of_cfg.data(), h->ncfg * 4));
   std::vector<int64_t> big(h->ncfg, INT64_MAX);  // non-local configs stay "infeasible"
@@ -1123,7 +1132,8 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     CK(h, cudaEventRecord(h->side_ev[0], h->side[0]));
     BuildBufs bb = build_bufs(h);
     bb.inst = h->inst.p;  // K1f trims the forward sweeps of this plan (k1f_trim)
-    bb.n_inst = R.n_fw;
+    bb.inst_off = h->inst_csr.p;
+    bb.inst_idx = h->inst_csr.p + h->ncfg + 1;
     bb.work = h->work.p;
     CK(h, launch_k1(h->cl, bb, h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
     CK(h, cudaStreamWaitEvent(h->st, h->side_ev[0], 0));

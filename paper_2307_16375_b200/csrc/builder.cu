@@ -329,18 +329,31 @@ __device__ __forceinline__ int32_t mem_bucket(int64_t byt, int64_t unit, int cap
 // sweep stops there (Inst::n) and the later interval optima stay INF from
 // the fill.  Exact; computed from the builder's own M, rewritten every run
 // from the planned length n0.
-__device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev& cf, int cfg_id) {
+__device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev& cf, int cfg_id, int L) {
+  __shared__ int32_t minb[MAXL];            // per layer: the smallest bucket over the config's strategies
+  __shared__ int32_t skb[UNIAP_MAX_STRAT];  // the skip source's bucket per strategy (conditioned copies)
   __shared__ unsigned long long wsum[2];
   const int cap = cl.Q - 1;
   const int64_t unit = (cl.mem_bytes - cl.mem_reserve) / cap;
   const int64_t* M = bb.ns + cf.offM;
-  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  if (threadIdx.x < 2) wsum[threadIdx.x] = 0;
+  const int t = threadIdx.x, lane = t & 31, nw = blockDim.x >> 5;
+  if (t < L) {  // bucket(min bytes) = min bucket (ceil is monotone); forbidden (< 0) excluded
+    int64_t mn = -1;
+    for (int k = 0; k < cf.S; ++k) {
+      const int64_t x = M[t * cf.NSP + k];
+      if (x >= 0 && (mn < 0 || x < mn)) mn = x;
+    }
+    minb[t] = mem_bucket(mn, unit, cap);
+  } else if (t >= 64 && t < 64 + cf.S && cf.skip >= 0) {
+    skb[t - 64] = mem_bucket(M[cf.skip * cf.NSP + (t - 64)], unit, cap);
+  }
+  if (t < 2) wsum[t] = 0;
   __syncthreads();
   const unsigned long long S = cf.S, Qw = cl.Q;
-  for (int j = threadIdx.x >> 5; j < bb.n_inst; j += nw) {
+  const int i0 = bb.inst_off[cfg_id], i1 = bb.inst_off[cfg_id + 1];
+  for (int q = i0 + (t >> 5); q < i1; q += nw) {  // this config's forward sweeps, one warp each
+    const int j = bb.inst_idx[q];
     const Inst in = bb.inst[j];
-    if (in.cfg != cfg_id) continue;
     if (in.emit != 1 && in.emit != 2) {  // a G-keeping sweep runs in full
       if (lane == 0 && S > 1) {          // (|S| = 1: the closed form, no DP cells)
         atomicAdd(&wsum[0], (unsigned long long)in.n0 * S * Qw);
@@ -354,12 +367,7 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
       int mn = 0;
       if (i < in.n0) {
         const int u = in.a + in.dir * i;
-        mn = cap + 1;
-        if (in.ks >= 0 && u == cf.skip) {
-          mn = mem_bucket(M[u * cf.NSP + in.ks], unit, cap);
-        } else {
-          for (int k = 0; k < cf.S; ++k) mn = min(mn, mem_bucket(M[u * cf.NSP + k], unit, cap));
-        }
+        mn = (in.ks >= 0 && u == cf.skip) ? skb[in.ks] : minb[u];
       }
       int x = mn;  // inclusive scan over this half's layers
 #pragma unroll
@@ -386,7 +394,7 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
     }
   }
   __syncthreads();
-  if (threadIdx.x < 2) bb.work[2 * cfg_id + threadIdx.x] = wsum[threadIdx.x];
+  if (t < 2) bb.work[2 * cfg_id + t] = wsum[t];
 }
 
 // K1f: quantise into the int32 device layout (A, M buckets, Rt, Rf, Rs, O);
@@ -395,7 +403,7 @@ __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restri
   TraceScope tr(TR_K1F);
   const CfgDev cf = cfgs[blockIdx.y];
   if (blockIdx.x == gridDim.x - 1) {
-    if (bb.inst) k1f_trim(cl, bb, cf, blockIdx.y);
+    if (bb.inst) k1f_trim(cl, bb, cf, blockIdx.y, L);
     return;
   }
   const int nqb = gridDim.x - 1;  // quantising blocks

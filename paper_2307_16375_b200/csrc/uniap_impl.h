@@ -210,7 +210,8 @@ struct BuildBufs {
   const int64_t* skip_mat;   // [L] word offset of edge skip->v's matrix, -1 none
   const CatDev* cat;      // [ncfg]
   Inst* inst;             // the forward instances of the run (K1f writes each P sweep's feasible length)
-  int32_t n_inst;
+  const int32_t* inst_off;  // [ncfg + 1] CSR: config i's instances are inst[inst_idx[inst_off[i] ..]]
+  const int32_t* inst_idx;
   unsigned long long* work;  // [ncfg][2] executed cells, relaxations of each config's forward sweeps
   int64_t* ns;            // int64 scratch arena, same offsets as the int32 arena
   int64_t* qcfg;          // [ncfg] smallest passing quantum per config

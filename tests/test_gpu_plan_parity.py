@@ -8,7 +8,7 @@ sweep, every P sweep trimmed on the device at its feasible prefix).  Here the
 interval optima the solver's own run left in its P arena
 (uniap_fetch_intervals) are compared with the oracle's interval table on
 every entry some placement of the config can use -- and every other entry
-must be untouched (UNIAP_INF).  An over-estimated P entry off the optimal
+must be untouched (UNIAP_INF) or exact as well.  An over-estimated P entry off the optimal
 path cannot hide: it is compared directly.
 """
 import numpy as np
@@ -59,7 +59,11 @@ def check(h, orc, t, P, what):
         bad = np.argwhere(m & (got != want))
         assert bad.size == 0, (what, i, cfg["deg"], cfg["c"], bad[:5].tolist(),
                                [(int(got[a, b]), int(want[a, b])) for a, b in bad[:5]])
-        assert np.all(got[~m] == INF), (what, i, "entry outside the plan was written")
+        # entries no placement needs may still be computed by a sweep (e.g. a
+        # deg = 1 chain with the skip source inside runs as a forward sweep
+        # and emits every prefix): each is either untouched or exact
+        off = ~m & (got != INF)
+        assert np.array_equal(got[off], want[off]), (what, i, "an extra entry is wrong")
 
 
 @pytest.mark.parametrize("name", ["bert", "t5", "vit", "swin", "llama"])

@@ -1,0 +1,42 @@
+"""Small runs of every kernel family for compute-sanitizer (racecheck /
+synccheck / memcheck): toy tables, the BERT profile (level 2: K1 incl. the
+K1f trim role, K2 one-CTA classes, K4, K5a, backward K2, K5c), a deg = 1
+chain on a 16-CTA cluster at Q = 4096 (DSMEM fix-up, split cluster barrier,
+kept G tables) and a skip-conditioned cluster case; each checked against the
+oracle.  usage: python tools/sanitize_cases.py [case ...]"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2307_16375_b200 as pkg  # noqa: E402
+from gen import profiles, tables  # noqa: E402
+from oracle import oracle  # noqa: E402
+
+
+def same(g, o, what):
+    for k in ("objective", "deg", "c", "stage_of", "strategy_of"):
+        assert g.get(k) == o.get(k), (what, k, g.get(k), o.get(k))
+    print("ok", what, g["objective"], flush=True)
+
+
+def main(cases):
+    h = pkg.Handle(0)
+    if "toy" in cases:
+        t = tables.toy_tables()
+        same(h.solve_tables(t), oracle.solve_tables(t), "toy")
+    if "bert" in cases:
+        p = profiles.make_profile("bert")
+        want, _ = oracle.plan(p, n_threads=0)
+        same(h.plan(p), want, "bert plan")
+    if "cluster" in cases:  # deg = 1, |S| = 21, Q = 4096: the 16-CTA cluster chain that keeps G
+        t = tables.large_random_tables(99, 8, [21, 15], 4095, [(1, 1), (2, 2)], skip_src=-1, mem_max=900)
+        same(h.solve_tables(t), oracle.solve_tables(t, n_threads=0), "cluster deg1")
+    if "skip" in cases:  # skip-conditioned copies on clusters, Q = 4096
+        t = tables.large_random_tables(7, 8, [10, 6], 4095, [(1, 1), (2, 2)], skip_src=2, mem_max=900)
+        same(h.solve_tables(t), oracle.solve_tables(t, n_threads=0), "cluster skip")
+    h.close()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["toy", "bert", "cluster", "skip"])
