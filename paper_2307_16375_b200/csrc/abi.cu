@@ -71,6 +71,7 @@ struct RunPlan {
   std::vector<K2Group> fgrp, bgrp;
   std::vector<std::pair<int, int>> k4range;  // per forward group: its configs in `local`
   std::pair<int, int> k4rest{0, 0};          // configs without chain-DP work (deg > L)
+  int n_trim = 1;                            // K1f trim blocks per config (8 sweeps per block and pass)
   int max_deg = 0;
 };
 
@@ -970,7 +971,7 @@ static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, De
 
 static BuildBufs build_bufs(uniap_handle* h) {
   return BuildBufs{h->fwd.p, h->act.p, h->ps.p, h->ctx.p, h->tpc.p, h->chain.p, h->skipb.p, h->edges.p,
-                   h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->dcat.p, nullptr, nullptr, nullptr, nullptr, h->ns.p,
+                   h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->dcat.p, nullptr, nullptr, nullptr, 0, nullptr, h->ns.p,
                    h->qcfg.p, h->qmax.p, h->qglob.p};
 }
 
@@ -1092,6 +1093,9 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     for (int i = 0; i < h->ncfg; ++i) csr[i + 1] += csr[i];
     std::vector<int32_t> fill(csr.begin(), csr.begin() + h->ncfg);
     for (size_t j = 0; j < fw.size(); ++j) csr[h->ncfg + 1 + fill[fw[j].cfg]++] = (int32_t)j;
+    int most = 1;
+    for (int i = 0; i < h->ncfg; ++i) most = std::max(most, csr[i + 1] - csr[i]);
+    R.n_trim = std::min(64, (most + 7) / 8);  // about one sweep per warp
     CK(h, h->inst_csr.ensure(csr.size()));
     CK(h, h2d(h, h->inst_csr.p, csr.data(), csr.size() * 4));
   }
@@ -1134,6 +1138,7 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     bb.inst = h->inst.p;  // K1f trims the forward sweeps of this plan (k1f_trim)
     bb.inst_off = h->inst_csr.p;
     bb.inst_idx = h->inst_csr.p + h->ncfg + 1;
+    bb.n_trim = R.n_trim;
     bb.work = h->work.p;
     CK(h, launch_k1(h->cl, bb, h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
     CK(h, cudaStreamWaitEvent(h->st, h->side_ev[0], 0));

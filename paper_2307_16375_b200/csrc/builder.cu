@@ -254,6 +254,7 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
     mx[i] = *q;
     *q = 0;  // zero for the next run's atomics (no memset node in the graph)
   }
+  if (bb.work && t < 2) bb.work[2 * blockIdx.x + t] = 0;  // K1f's trim accumulates this run's work here
   __syncthreads();
   if (t < 64) {
     const bool expl = cl.quantum > 0;
@@ -329,7 +330,8 @@ __device__ __forceinline__ int32_t mem_bucket(int64_t byt, int64_t unit, int cap
 // sweep stops there (Inst::n) and the later interval optima stay INF from
 // the fill.  Exact; computed from the builder's own M, rewritten every run
 // from the planned length n0.
-__device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev& cf, int cfg_id, int L) {
+__device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev& cf, int cfg_id, int L, int tb,
+                         int ntb) {
   __shared__ int32_t minb[MAXL];            // per layer: the smallest bucket over the config's strategies
   __shared__ int32_t skb[UNIAP_MAX_STRAT];  // the skip source's bucket per strategy (conditioned copies)
   __shared__ unsigned long long wsum[2];
@@ -351,7 +353,8 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
   __syncthreads();
   const unsigned long long S = cf.S, Qw = cl.Q;
   const int i0 = bb.inst_off[cfg_id], i1 = bb.inst_off[cfg_id + 1];
-  for (int q = i0 + (t >> 5); q < i1; q += nw) {  // this config's forward sweeps, one warp each
+  // this config's forward sweeps, one warp each, over the ntb trim blocks
+  for (int q = i0 + tb * nw + (t >> 5); q < i1; q += ntb * nw) {
     const int j = bb.inst_idx[q];
     const Inst in = bb.inst[j];
     if (in.emit != 1 && in.emit != 2) {  // a G-keeping sweep runs in full
@@ -394,7 +397,7 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
     }
   }
   __syncthreads();
-  if (t < 2) bb.work[2 * cfg_id + t] = wsum[t];
+  if (t < 2 && (wsum[t] || tb == 0)) atomicAdd(bb.work + 2 * cfg_id + t, wsum[t]);  // (zeroed by K1d)
 }
 
 // K1f: quantise into the int32 device layout (A, M buckets, Rt, Rf, Rs, O);
@@ -402,11 +405,11 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
 __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int32_t* arena) {
   TraceScope tr(TR_K1F);
   const CfgDev cf = cfgs[blockIdx.y];
-  if (blockIdx.x == gridDim.x - 1) {
-    if (bb.inst) k1f_trim(cl, bb, cf, blockIdx.y, L);
+  const int nqb = gridDim.x - bb.n_trim;  // quantising blocks; then the trim blocks
+  if ((int)blockIdx.x >= nqb) {
+    k1f_trim(cl, bb, cf, blockIdx.y, L, blockIdx.x - nqb, bb.n_trim);
     return;
   }
-  const int nqb = gridDim.x - 1;  // quantising blocks
   const int NSP = cf.NSP, n2 = NSP * NSP;
   const int64_t q = bb.qglob[0] > 0 ? bb.qglob[0] : 1;
   const int cap = cl.Q - 1;
@@ -446,7 +449,7 @@ cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* c
   const int nbR = 2 * L - 1;  // one block per edge slot: L-1 chain edges, L skip destinations
   k1_costs<<<dim3(nbA + nbR + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR);
   k1d_quantum<<<ncfg, 64, 0, st>>>(cl, bb, cfg, L, skip);
-  k1f_quantise<<<dim3(16 + 1, ncfg), 256, 0, st>>>(cl, bb, cfg, L, arena);
+  k1f_quantise<<<dim3(16 + (bb.inst ? bb.n_trim : 0), ncfg), 256, 0, st>>>(cl, bb, cfg, L, arena);
   return cudaGetLastError();
 }
 

@@ -212,6 +212,7 @@ struct BuildBufs {
   Inst* inst;             // the forward instances of the run (K1f writes each P sweep's feasible length)
   const int32_t* inst_off;  // [ncfg + 1] CSR: config i's instances are inst[inst_idx[inst_off[i] ..]]
   const int32_t* inst_idx;
+  int32_t n_trim;           // K1f trim blocks per config (0 when inst is null)
   unsigned long long* work;  // [ncfg][2] executed cells, relaxations of each config's forward sweeps
   int64_t* ns;            // int64 scratch arena, same offsets as the int32 arena
   int64_t* qcfg;          // [ncfg] smallest passing quantum per config
