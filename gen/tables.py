@@ -72,12 +72,14 @@ def _draw_cfg(rng, L, S, cap, skip_src, dist, forbid_p, with_O):
 
 
 def random_tables(seed, L=None, S_max=3, cap=None, n_cfg=None, dist=None,
-                  skip_p=0.4, forbid_p=None, deg_max=None):
+                  skip_p=0.4, forbid_p=None, deg_max=None, stage_caps=False):
     """Random tiny instance for brute-force checks (SURVEY.md Sec. 4 tier T0).
 
     L <= 6, |S| <= 3, cap <= 7 by default; skip edges in ``skip_p`` of the
     instances; cut costs O != 0; 'uniform' or tie-heavy ('ties') values;
-    forbidden entries (M = cap+1).
+    forbidden entries (M = cap+1).  ``stage_caps``: every config also gets a
+    per-stage memory cap (``stage_cap``, drawn in [0, cap]; heterogeneous
+    devices).
     """
     rng = np.random.default_rng(seed)
     L = int(rng.integers(1, 7)) if L is None else L
@@ -98,11 +100,15 @@ def random_tables(seed, L=None, S_max=3, cap=None, n_cfg=None, dist=None,
         d = _draw_cfg(rng, L, S, cap, skip_src, dist, forbid_p, with_O=rng.random() < 0.8)
         d.update({"deg": deg, "c": c, "n_strat": S})
         cfgs.append(d)
+    if stage_caps:
+        crng = np.random.default_rng(seed + 12_345_678)  # separate stream: the tables above are unchanged
+        for d in cfgs:
+            d["stage_cap"] = crng.integers(max(cap - 3, 0), cap + 1, size=d["deg"]).astype(np.int32)
     return {"L": L, "cap": cap, "skip_src": skip_src, "cfgs": cfgs}
 
 
 def large_random_tables(seed, L, S_list, cap, cands, skip_src=-1, dist="uniform",
-                        forbid_p=0.05, vmax=1 << 20, mem_max=None):
+                        forbid_p=0.05, vmax=1 << 20, mem_max=None, stage_caps=False):
     """Random instance at GPU-parity sizes (several tiles and a ragged tail).
 
     ``S_list[i]`` strategies for candidate ``cands[i] = (deg, c)``; entries of
@@ -135,4 +141,8 @@ def large_random_tables(seed, L, S_list, cap, cands, skip_src=-1, dist="uniform"
                      "R": R.astype(np.int32),
                      "Rskip": None if Rskip is None else Rskip.astype(np.int32),
                      "O": O.astype(np.int32)})
+    if stage_caps:  # per-stage caps from at most 3 distinct device sizes (heterogeneous devices)
+        crng = np.random.default_rng(seed + 12_345_678)
+        for d in cfgs:
+            d["stage_cap"] = crng.choice([cap, cap - cap // 4, cap // 2], size=d["deg"]).astype(np.int32)
     return {"L": L, "cap": cap, "skip_src": skip_src, "cfgs": cfgs}

@@ -8,7 +8,8 @@ For tiny instances only.  Enumerates, for every candidate config (deg, c):
 and evaluates literally
   p_i = sum_{u in i} A_u[k_u] + sum_{<u,v> in E, u,v in i} R_uv[k_u][k_v]   (Eq. 3)
   o_j = O[last layer of stage j]                                            (Eq. 4, scalar R')
-  mem_i = sum_{u in i} M_u[k_u] <= cap                                      (Eq. 5)
+  mem_i = sum_{u in i} M_u[k_u] <= cap_i (the stage's cap, = cap unless the
+          config gives per-stage caps: heterogeneous devices)   (Eq. 5)
   tpi = sum p + sum o + (c-1) * max(P u O)                                  (Eq. 2)
 and returns the minimum of the key (tpi, deg, c, stage_of, strategy_of).
 """
@@ -46,6 +47,7 @@ def solve_cfg(t, cfg, guard=2_000_000):
     R = np.asarray(cfg["R"], dtype=np.int64).reshape(max(L - 1, 0), S, S) if L > 1 else None
     Rs = None if cfg.get("Rskip") is None or s < 0 else np.asarray(cfg["Rskip"], dtype=np.int64).reshape(L, S, S)
     O = np.zeros(max(L - 1, 0), dtype=np.int64) if cfg.get("O") is None else np.asarray(cfg["O"], dtype=np.int64)
+    caps = [cap] * deg if cfg.get("stage_cap") is None else [int(x) for x in cfg["stage_cap"]]
     places = sorted(placements(L, deg))
     if not places:
         return None
@@ -72,7 +74,7 @@ def solve_cfg(t, cfg, guard=2_000_000):
                 for v in range(max(s + 2, a), b + 1):
                     p = p + Rs[v, K[:, s], K[:, v]]
             mem = Mu[:, a:b + 1].sum(axis=1)
-            feas &= mem <= cap
+            feas &= mem <= caps[i]
             total += p
             mx = np.maximum(mx, p)
             if i + 1 < deg:

@@ -72,6 +72,9 @@ static int validate_tables(const orc_tables* t) {
         if (c->O[e] < 0 || c->O[e] > ENTRY_MAX) return ORC_ERR_RANGE;
         osum += c->O[e];
       }
+    if (c->stage_cap)
+      for (int i = 0; i < c->deg; ++i)
+        if (c->stage_cap[i] < 0 || c->stage_cap[i] > t->cap) return ORC_ERR_ARG;
     if (sum > SUM_MAX || osum > SUM_MAX) return ORC_ERR_RANGE;
   }
   return ORC_OK;
@@ -277,34 +280,48 @@ static void stage_strategies(const orc_tables* t, const orc_cfg* c, int a, int b
 /* ======================================================================== */
 /* One candidate config: the MIQP of Sec. 3.3 solved exactly                */
 /* ======================================================================== */
+/* Memory cap of stage i (0-based): Eq. (5) with the stage's own m_i when the
+ * devices are heterogeneous, else the common cap. */
+static int stage_cap(const orc_tables* t, const orc_cfg* c, int i) { return c->stage_cap ? c->stage_cap[i] : t->cap; }
+
 static void solve_cfg(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
   int L = t->L, deg = c->deg;
   sol->obj = INF;
   sol->status = ORC_OK;
   if (deg > L) return; /* Eq. (7b) cannot hold (reading A-22) */
-  int64_t* P = (int64_t*)malloc(sizeof(int64_t) * L * L);
-  interval_table(t, c, P);
+  /* P_i[a][b]: the stage optimum of [a,b] under stage i's cap -- the
+   * interval table of the same tables with cap = cap_i, per stage index */
+  int64_t* Pall = (int64_t*)malloc(sizeof(int64_t) * (size_t)deg * L * L);
+  for (int i = 0; i < deg; ++i) {
+    int j = 0;
+    while (j < i && stage_cap(t, c, j) != stage_cap(t, c, i)) ++j;
+    if (j < i) { memcpy(Pall + (size_t)i * L * L, Pall + (size_t)j * L * L, sizeof(int64_t) * L * L); continue; }
+    orc_tables ti = *t;
+    ti.cap = stage_cap(t, c, i);
+    interval_table(&ti, c, Pall + (size_t)i * L * L);
+  }
+#define PI(i, a, b) Pall[((size_t)((i) - 1) * L + (a)) * L + (b)] /* stage i = 1..deg */
   /* Set(i,a), i = 1..deg (index i-1), a = 0..L-1 */
   pset* sets = (pset*)calloc((size_t)deg * L, sizeof(pset));
 #define SET(i, a) sets[(size_t)((i) - 1) * L + (a)]
   for (int a = 0; a < L; ++a) {
     pset* s = &SET(deg, a);
-    if (P[a * L + L - 1] < INF) {
+    if (PI(deg, a, L - 1) < INF) {
       s->v = (pair_t*)malloc(sizeof(pair_t));
-      s->v[0].sig = P[a * L + L - 1];
-      s->v[0].mx = P[a * L + L - 1];
+      s->v[0].sig = PI(deg, a, L - 1);
+      s->v[0].mx = PI(deg, a, L - 1);
       s->n = 1;
     }
   }
   for (int i = deg - 1; i >= 1; --i)
     for (int a = 0; a < L; ++a) {
       int cnt = 0;
-      for (int b = a; b + 1 < L; ++b) if (P[a * L + b] < INF) cnt += SET(i + 1, b + 1).n;
+      for (int b = a; b + 1 < L; ++b) if (PI(i, a, b) < INF) cnt += SET(i + 1, b + 1).n;
       pset* s = &SET(i, a);
       if (!cnt) continue;
       s->v = (pair_t*)malloc(sizeof(pair_t) * cnt);
       for (int b = a; b + 1 < L; ++b) {
-        int64_t p = P[a * L + b];
+        int64_t p = PI(i, a, b);
         if (p >= INF) continue;
         int64_t o = Ocut(c, b);
         const pset* nx = &SET(i + 1, b + 1);
@@ -327,7 +344,7 @@ static void solve_cfg(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
     for (int i = 1; i < deg; ++i) {
       int chosen = -1;
       for (int b = L - 2; b >= a && chosen < 0; --b) {
-        int64_t p = P[a * L + b];
+        int64_t p = PI(i, a, b);
         if (p >= INF) continue;
         int64_t o = Ocut(c, b);
         const pset* nx = &SET(i + 1, b + 1);
@@ -338,7 +355,7 @@ static void solve_cfg(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
           }
       }
       if (chosen < 0) { sol->status = ORC_ERR_INTERNAL; break; }
-      int64_t p = P[a * L + chosen], o = Ocut(c, chosen);
+      int64_t p = PI(i, a, chosen), o = Ocut(c, chosen);
       sig += p + o;
       mx = max64(mx, max64(p, o));
       sol->end[i - 1] = chosen;
@@ -347,18 +364,21 @@ static void solve_cfg(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
       a = chosen + 1;
     }
     sol->end[deg - 1] = L - 1;
-    sol->p[deg - 1] = P[a * L + L - 1];
-    /* strategies per stage */
+    sol->p[deg - 1] = PI(deg, a, L - 1);
+    /* strategies per stage, under the stage's own cap */
     int start = 0;
     for (int i = 0; i < deg && sol->status == ORC_OK; ++i) {
-      stage_strategies(t, c, start, sol->end[i], sol->p[i], sol->strat);
+      orc_tables ti = *t;
+      ti.cap = stage_cap(t, c, i);
+      stage_strategies(&ti, c, start, sol->end[i], sol->p[i], sol->strat);
       start = sol->end[i] + 1;
     }
   }
   for (int i = 0; i < deg * L; ++i) free(sets[i].v);
 #undef SET
+#undef PI
   free(sets);
-  free(P);
+  free(Pall);
 }
 
 /* Literal re-evaluation of Eqs. (2), (3), (5) from (stage_of, strategy_of). */
@@ -378,7 +398,7 @@ static int check_solution(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
       if (u < b) p += Rchain(c, u, k, sol->strat[u + 1]);
       if (c->Rskip && s >= 0 && start <= s && u >= s + 2) p += c->Rskip[((size_t)u * S + sol->strat[s]) * S + k];
     }
-    if (mem > t->cap || p != sol->p[i]) return ORC_ERR_INTERNAL;
+    if (mem > stage_cap(t, c, i) || p != sol->p[i]) return ORC_ERR_INTERNAL;
     sol->mem[i] = (int32_t)mem;
     sum += p;
     mx = max64(mx, p);
@@ -596,6 +616,9 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
   if (cl->mem_bytes <= cl->mem_reserve || cl->mem_reserve < 0) return ORC_ERR_ARG;
   int64_t unit = (cl->mem_bytes - cl->mem_reserve) / cap; /* reading A-8 */
   if (unit < 1) return ORC_ERR_ARG;
+  if (cl->dev_mem)
+    for (int d = 0; d < cl->n_dev; ++d)
+      if (cl->dev_mem[d] <= cl->mem_reserve || cl->dev_mem[d] > cl->mem_bytes) return ORC_ERR_ARG;
   int maxtp = 1;
   while (n % (maxtp * 2) == 0) maxtp *= 2;
   const int64_t LIM = (int64_t)1 << 46;
@@ -674,7 +697,7 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
     Ss[i] = orc_catalogue(g, o->strategy_space, NULL, 0);
     if (Ss[i] > ORC_MAX_S) return ORC_ERR_RANGE;
     int S = Ss[i];
-    words += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1);
+    words += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + cand[2 * i];
   }
   *words_out = words;
   *n_cfg_out = n_cand;
@@ -755,7 +778,17 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
       if (sum >= NS_LIMIT) st = ORC_ERR_RANGE;
       O[e] = (int64_t)sum;
     }
-    off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1);
+    /* per-stage memory caps in buckets (Eq. 5 with m_i): the
+     * smallest device memory among the stage's g devices */
+    int64_t* SC = O + (L - 1);
+    for (int st = 0; st < deg; ++st) {
+      int64_t m = cl->mem_bytes;
+      if (cl->dev_mem)
+        for (int d = st * g; d < (st + 1) * g; ++d) m = cl->dev_mem[d] < m ? cl->dev_mem[d] : m;
+      int64_t cp = (m - cl->mem_reserve) / unit;
+      SC[st] = cp > cap ? cap : cp;
+    }
+    off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + deg;
   }
   /* time quantum (reading A-9): smallest power of two such that every entry
    * fits 2^22 and every config's sums fit 2^28 (or the caller's quantum). */
@@ -786,7 +819,7 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
         osum += x;
       }
       if (sum > SUM_MAX || osum > SUM_MAX) ok = 0;
-      off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1);
+      off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + cand[2 * i];
     }
     if (ok) break;
     if (o->quantum_ns) { st = ORC_ERR_RANGE; break; }
@@ -809,7 +842,8 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
       }
       int64_t rest = (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1);
       for (int64_t j = 0; j < rest; ++j) out[4 + 2 * nA + j] = (int32_t)((blk[4 + 2 * nA + j] + qn - 1) / qn);
-      off += 4 + 2 * nA + rest;
+      for (int st = 0; st < cand[2 * i]; ++st) out[4 + 2 * nA + rest + st] = (int32_t)blk[4 + 2 * nA + rest + st];
+      off += 4 + 2 * nA + rest + cand[2 * i];
     }
   }
   free(ns);

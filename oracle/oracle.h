@@ -40,6 +40,9 @@ typedef struct {
   const int32_t* R;      /* [L-1][S][S] R_{u,u+1}[k][l]  (Eq. 3)         */
   const int32_t* Rskip;  /* [L][S][S]   R_{s,v}[k_s][k_v] for v >= s+2, or NULL        */
   const int32_t* O;      /* [L-1]       cut cost after layer e, or NULL (=0)           */
+  const int32_t* stage_cap; /* [deg] memory cap of stage i (0..cap), or NULL (= cap):
+                               heterogeneous devices, PAPER.md:161 ("the value of m varies
+                               in the case of heterogeneous computing devices")          */
 } orc_cfg;
 
 typedef struct {
@@ -82,6 +85,10 @@ typedef struct {
   int32_t n_dev, node_size;
   int64_t mem_bytes, mem_reserve, bw_intra, bw_inter, p2p_bw, lat_ns;
   int32_t ccoc_permille;
+  const int64_t* dev_mem;    /* NULL, or [n_dev] memory of each device (heterogeneous):
+                                stage i of a (deg, g) config runs on devices i*g .. i*g+g-1 and
+                                its cap is floor((min of their memory - reserve) / unit);
+                                each in (reserve, mem_bytes] (mem_bytes sets the unit)   */
 } orc_cluster;
 typedef struct { int32_t L; const orc_layer* layers; int32_t n_edges; const orc_edge* edges; } orc_model;
 typedef struct {
@@ -93,7 +100,7 @@ typedef struct {
 } orc_options;
 
 /* Builder': writes, per candidate config in order, the block
- *   [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1]]
+ *   [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1], stage_cap[deg]]
  * into buf (int32).  *n_cfg, *skip_src, *quantum_ns, *words are outputs. */
 int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o,
               int32_t* buf, int64_t buf_len, int32_t* n_cfg, int32_t* skip_src,

@@ -35,7 +35,8 @@ def build_oracle(force=False):
 class _Cfg(C.Structure):
     _fields_ = [("deg", C.c_int32), ("c", C.c_int32), ("n_strat", C.c_int32),
                 ("A", C.POINTER(C.c_int32)), ("M", C.POINTER(C.c_int32)), ("R", C.POINTER(C.c_int32)),
-                ("Rskip", C.POINTER(C.c_int32)), ("O", C.POINTER(C.c_int32))]
+                ("Rskip", C.POINTER(C.c_int32)), ("O", C.POINTER(C.c_int32)),
+                ("stage_cap", C.POINTER(C.c_int32))]
 
 
 class _Tables(C.Structure):
@@ -63,7 +64,8 @@ class _Edge(C.Structure):
 class _Cluster(C.Structure):
     _fields_ = [("n_dev", C.c_int32), ("node_size", C.c_int32), ("mem_bytes", C.c_int64),
                 ("mem_reserve", C.c_int64), ("bw_intra", C.c_int64), ("bw_inter", C.c_int64),
-                ("p2p_bw", C.c_int64), ("lat_ns", C.c_int64), ("ccoc_permille", C.c_int32)]
+                ("p2p_bw", C.c_int64), ("lat_ns", C.c_int64), ("ccoc_permille", C.c_int32),
+                ("dev_mem", C.POINTER(C.c_int64))]
 
 
 class _Model(C.Structure):
@@ -128,8 +130,9 @@ def _marshal_tables(t):
         O = _i32(c["O"]).reshape(max(L - 1, 0)) if c.get("O") is not None else None
         if O is not None and O.size == 0:
             O = np.zeros(1, np.int32)
-        keep += [A, M, R, Rs, O]
-        cfgs[i] = _Cfg(c["deg"], c["c"], S, _ptr32(A), _ptr32(M), _ptr32(R), _ptr32(Rs), _ptr32(O))
+        SC = _i32(c["stage_cap"]).reshape(c["deg"]) if c.get("stage_cap") is not None else None
+        keep += [A, M, R, Rs, O, SC]
+        cfgs[i] = _Cfg(c["deg"], c["c"], S, _ptr32(A), _ptr32(M), _ptr32(R), _ptr32(Rs), _ptr32(O), _ptr32(SC))
     tb = _Tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs)
     keep.append(cfgs)
     return tb, keep
@@ -216,8 +219,13 @@ def _marshal_profile(p):
         edges[i] = _Edge(e["src"], e["dst"], e["tensor_bytes_per_sample"], ptr)
     model = _Model(L, layers, E, edges)
     cl = p["cluster"]
+    dm = None
+    if cl.get("dev_mem_bytes") is not None:
+        dm = np.ascontiguousarray(cl["dev_mem_bytes"], dtype=np.int64)
+        keep.append(dm)
     cluster = _Cluster(cl["n_dev"], cl["node_size"], cl["mem_bytes"], cl["mem_reserve_bytes"],
-                       cl["bw_intra_Bps"], cl["bw_inter_Bps"], cl["p2p_Bps"], cl["lat_ns"], cl["ccoc_permille"])
+                       cl["bw_intra_Bps"], cl["bw_inter_Bps"], cl["p2p_Bps"], cl["lat_ns"], cl["ccoc_permille"],
+                       None if dm is None else dm.ctypes.data_as(C.POINTER(C.c_int64)))
     o = p["options"]
     cand = None
     if o.get("cand"):
@@ -256,8 +264,9 @@ def unpack_buffer(buf, L, cap, skip_src, n_cfg):
         R = buf[off:off + (L - 1) * S * S].reshape(L - 1, S, S); off += (L - 1) * S * S
         Rs = buf[off:off + L * S * S].reshape(L, S, S); off += L * S * S
         O = buf[off:off + L - 1]; off += L - 1
+        SC = buf[off:off + deg]; off += deg
         cfgs.append({"deg": deg, "c": c, "n_strat": S, "g": g, "A": A, "M": M, "R": R,
-                     "Rskip": Rs if skip_src >= 0 else None, "O": O})
+                     "Rskip": Rs if skip_src >= 0 else None, "O": O, "stage_cap": SC})
     return {"L": L, "cap": cap, "skip_src": skip_src, "cfgs": cfgs}
 
 

@@ -81,3 +81,31 @@ def test_threads_do_not_change_result(orc):
     for seed in range(50):
         t = tables.random_tables(seed, n_cfg=4)
         assert orc.solve_tables(t, n_threads=1) == orc.solve_tables(t, n_threads=4)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: per-stage memory limits m_i (heterogeneous devices, PAPER.md:161
+# "the value of m varies in the case of heterogeneous computing devices";
+# PAPER.md:603).  Eq. (5) per stage with its own cap.
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("chunk", range(3))
+def test_oracle_equals_brute_force_with_stage_caps(orc, chunk):
+    """The whole key against the literal enumeration with mem_i <= cap_i."""
+    n = 0
+    for seed in range(chunk * 500, (chunk + 1) * 500):
+        t = tables.random_tables(700_000 + seed, stage_caps=True)
+        _same(orc.solve_tables(t), brute.solve_tables(t))
+        n += 1
+    assert n == 500
+
+
+def test_stage_caps_equal_to_cap_change_nothing_and_lower_caps_never_help(orc):
+    for seed in range(300):
+        t = tables.random_tables(800_000 + seed, stage_caps=True)
+        base = dict(t, cfgs=[{k: v for k, v in c.items() if k != "stage_cap"} for c in t["cfgs"]])
+        full = dict(t, cfgs=[dict(c, stage_cap=np.full(c["deg"], t["cap"], np.int32)) for c in base["cfgs"]])
+        r0, r1, r2 = orc.solve_tables(base), orc.solve_tables(full), orc.solve_tables(t)
+        assert r0 == r1
+        for a, b in zip(r0["cfg_objective"], r2["cfg_objective"]):
+            assert b >= a  # restricting a stage's memory can only raise the optimum

@@ -358,3 +358,27 @@ def test_strategy_space_restricts_the_search(orc):
         r1 = orc.solve_tables(t1)["objective"]
         if r0 != (1 << 63) - 1 and r1 != (1 << 63) - 1 and q0 == q1:
             assert r0 <= r1
+
+
+def test_per_device_memory_gives_per_stage_caps(orc):
+    """Heterogeneous devices: stage i of a (deg, g) config runs
+    on devices i*g .. i*g+g-1 and its cap is floor((min memory - reserve) /
+    unit), unit = floor((mem_bytes - reserve) / (Q-1)).  n = 4, Q = 101,
+    mem_bytes = 1100, reserve = 100 -> unit = 10; devices 1100, 900, 700, 1050:
+    deg 2 (g 2): stages min(1100,900) -> 80, min(700,1050) -> 60;
+    deg 4 (g 1): 100, 80, 60, 95; deg 1: min over all 4 -> 60.
+    Without per-device memory every stage cap is Q-1 = 100."""
+    p = _profile(L=4, n=4, B=4, Q=101, mem=1100, cand=[(1, 1), (2, 2), (4, 4)], quantum=1, fwd=[1000, 600, 400])
+    p["cluster"]["mem_reserve_bytes"] = 100
+    t, _, _ = orc.build_tables(p)
+    assert [list(c["stage_cap"]) for c in t["cfgs"]] == [[100], [100, 100], [100] * 4]
+    p["cluster"]["dev_mem_bytes"] = [1100, 900, 700, 1050]
+    t, _, _ = orc.build_tables(p)
+    assert [list(c["stage_cap"]) for c in t["cfgs"]] == [[60], [80, 60], [100, 80, 60, 95]]
+    p["cluster"]["dev_mem_bytes"] = [1100, 900, 100, 1050]  # a device with no memory above the reserve
+    try:
+        orc.build_tables(p)
+        raised = False
+    except orc.OracleError as e:
+        raised = e.status == 1
+    assert raised
