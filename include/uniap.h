@@ -41,6 +41,7 @@ extern "C" {
 #define UNIAP_MAX_STRAT 32
 #define UNIAP_MAX_Q 8192            /* memory buckets (cap + 1) */
 #define UNIAP_MAX_CFG 4096
+#define UNIAP_MAX_LEVELS 4          /* distinct per-stage memory caps per config (NEXT-2)   */
 
 typedef enum {
   UNIAP_OK = 0,
@@ -102,6 +103,11 @@ typedef struct {
                                 edge skip_src->v, v >= skip_src+2 (other rows ignored)        */
   const int32_t* O;          /* [L-1] or NULL (= 0): cost of a cut after layer e (Eq. 4 with a
                                 constant R', reading A-1)                                     */
+  const int32_t* stage_cap;  /* [deg] or NULL (= cap): the memory cap of pipeline stage i,
+                                0..cap -- heterogeneous devices, Eq. 5 with a per-stage m_i
+                                ("the value of m varies in the case of
+                                heterogeneous computing devices").  At most
+                                UNIAP_MAX_LEVELS distinct values per config (else _RANGE)    */
 } uniap_config;
 
 typedef struct {
@@ -125,11 +131,15 @@ uniap_status uniap_interval_table(uniap_handle* h, const uniap_tables* t, int32_
 
 /* The interval optima the LAST run computed (for parity tests of the plan
  * that actually runs: prefix / middle / suffix sweeps, skip-conditioned
- * copies, the feasible-prefix trim): P_out[(i*L + a)*L + b] for config i in
- * candidate order, UNIAP_INF where infeasible OR not needed by any
- * placement of config i (and for configs another rank owns).  P_len must be
- * >= n_cfg*L*L.  Synchronises the handle's stream. */
-uniap_status uniap_fetch_intervals(uniap_handle* h, int32_t* P_out, int64_t P_len);
+ * copies, the feasible-prefix trim): per config i in candidate order, one
+ * L*L block per distinct stage cap of the config (levels in order of first
+ * appearance over the stages; one block without per-stage caps):
+ * P_out[off_i + (lev*L + a)*L + b], off_i = L*L * (levels of configs < i),
+ * UNIAP_INF where infeasible OR not needed by any placement of config i (and
+ * for configs another rank owns).  *P_words (if not NULL) receives the
+ * total; P_out == NULL only queries it; else P_len must cover every block.
+ * Synchronises the handle's stream. */
+uniap_status uniap_fetch_intervals(uniap_handle* h, int32_t* P_out, int64_t P_len, int64_t* P_words);
 
 /* ---- level 2: profiles (the paper's problem statement) -- */
 typedef struct {
@@ -164,6 +174,12 @@ typedef struct {
   int64_t bw_intra_Bps, bw_inter_Bps, p2p_Bps;  /* collective / P2P bandwidths, >= 1         */
   int64_t lat_ns;                     /* per-hop latency                                       */
   int32_t ccoc_permille;              /* CCOC in 0..1000                          */
+  const int64_t* dev_mem_bytes;       /* NULL, or [n_dev] memory of each device (heterogeneous,
+                                         PAPER.md:161): stage i of a (deg, g = n/deg) config runs
+                                         on devices i*g .. i*g+g-1 and its cap is
+                                         floor((their smallest memory - reserve) / unit), unit
+                                         from mem_bytes (reading A-8); each entry in
+                                         (mem_reserve_bytes, mem_bytes]                        */
 } uniap_cluster;                      /* SPEC.md:115-120 as an alpha-beta record               */
 
 typedef struct {
@@ -191,7 +207,7 @@ uniap_status uniap_plan(uniap_handle* h, const uniap_model* m, const uniap_clust
 
 /* The builder's tables (for builder parity tests), per candidate config in
  * order, as int32 blocks
- *    [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1]]
+ *    [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1], stage_cap[deg]]
  * Call with buf == NULL to get *words; then with buf_len >= *words. */
 uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
                                 const uniap_options* o, int32_t* buf, int64_t buf_len, int64_t* words,

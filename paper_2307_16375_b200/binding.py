@@ -27,7 +27,7 @@ _P64 = C.POINTER(C.c_int64)
 
 class uniap_config(C.Structure):
     _fields_ = [("deg", C.c_int32), ("c", C.c_int32), ("n_strat", C.c_int32), ("A", _P32), ("M", _P32),
-                ("R", _P32), ("Rskip", _P32), ("O", _P32)]
+                ("R", _P32), ("Rskip", _P32), ("O", _P32), ("stage_cap", _P32)]
 
 
 class uniap_tables(C.Structure):
@@ -59,7 +59,8 @@ class uniap_edge(C.Structure):
 class uniap_cluster(C.Structure):
     _fields_ = [("n_dev", C.c_int32), ("node_size", C.c_int32), ("mem_bytes", C.c_int64),
                 ("mem_reserve_bytes", C.c_int64), ("bw_intra_Bps", C.c_int64), ("bw_inter_Bps", C.c_int64),
-                ("p2p_Bps", C.c_int64), ("lat_ns", C.c_int64), ("ccoc_permille", C.c_int32)]
+                ("p2p_Bps", C.c_int64), ("lat_ns", C.c_int64), ("ccoc_permille", C.c_int32),
+                ("dev_mem_bytes", _P64)]
 
 
 class uniap_model(C.Structure):
@@ -118,7 +119,7 @@ def lib():
         L.uniap_prepare_tables.argtypes = [H, C.POINTER(uniap_tables)]
         L.uniap_run.argtypes = [H, C.c_int32, C.c_int32, C.c_void_p]
         L.uniap_fetch.argtypes = [H, C.POINTER(uniap_result)]
-        L.uniap_fetch_intervals.argtypes = [H, _P32, C.c_int64]
+        L.uniap_fetch_intervals.argtypes = [H, _P32, C.c_int64, _P64]
         L.uniap_shard_assign.argtypes = [H, C.c_int32, _P32]
         L.uniap_shard_tables.argtypes = [C.POINTER(uniap_tables), C.c_int32, _P32]
         L.uniap_pick.argtypes = [C.POINTER(uniap_record), C.c_int32, C.POINTER(uniap_result)]
@@ -157,8 +158,9 @@ def _tables(t):
         R = _i32(c["R"]).reshape(L - 1, S, S) if L > 1 else np.zeros((1, S, S), np.int32)
         Rs = _i32(c["Rskip"]).reshape(L, S, S) if c.get("Rskip") is not None else None
         O = _i32(c["O"]).reshape(L - 1) if c.get("O") is not None and L > 1 else None
-        keep += [A, M, R, Rs, O]
-        cfgs[i] = uniap_config(c["deg"], c["c"], S, _p32(A), _p32(M), _p32(R), _p32(Rs), _p32(O))
+        SC = _i32(c["stage_cap"]).reshape(c["deg"]) if c.get("stage_cap") is not None else None
+        keep += [A, M, R, Rs, O, SC]
+        cfgs[i] = uniap_config(c["deg"], c["c"], S, _p32(A), _p32(M), _p32(R), _p32(Rs), _p32(O), _p32(SC))
     keep.append(cfgs)
     return uniap_tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs), keep
 
@@ -196,9 +198,13 @@ def _profile(p):
                 mats.append(mat)
                 ed["mat"][i] = mat.ctypes.data
     cl = p["cluster"]
+    dm = None
+    if cl.get("dev_mem_bytes") is not None:  # optional per-device memory (heterogeneous devices)
+        dm = np.ascontiguousarray(cl["dev_mem_bytes"], dtype=np.int64)
+        mats.append(dm)
     cluster = uniap_cluster(cl["n_dev"], cl["node_size"], cl["mem_bytes"], cl["mem_reserve_bytes"],
                             cl["bw_intra_Bps"], cl["bw_inter_Bps"], cl["p2p_Bps"], cl["lat_ns"],
-                            cl["ccoc_permille"])
+                            cl["ccoc_permille"], None if dm is None else dm.ctypes.data_as(_P64))
     o = p["options"]
     cand = None
     if o.get("cand"):
@@ -370,7 +376,7 @@ class Handle:
             off += 4
             blk = {}
             for name, shape in (("A", (L, S)), ("M", (L, S)), ("R", (L - 1, S, S)), ("Rskip", (L, S, S)),
-                                ("O", (L - 1,))):
+                                ("O", (L - 1,)), ("stage_cap", (deg,))):
                 size = int(np.prod(shape))
                 blk[name] = buf[off:off + size].reshape(shape)
                 off += size
@@ -433,11 +439,14 @@ class Handle:
         out["quantum_ns"] = local["quantum_ns"]
         return out
 
-    def fetch_intervals(self, L):
-        """The last run's interval optima [n_cfg][L][L] (UNIAP_INF = infeasible or not needed)."""
-        P = np.zeros(self.n_cfg * L * L, dtype=np.int32)
-        self._check(lib().uniap_fetch_intervals(self._h, P.ctypes.data_as(_P32), P.size), "fetch_intervals")
-        return P.reshape(self.n_cfg, L, L)
+    def fetch_intervals(self):
+        """The last run's interval tables, flat: per config, one L*L block per
+        cap level (uniap_fetch_intervals; UNIAP_INF = infeasible or not needed)."""
+        n = C.c_int64()
+        self._check(lib().uniap_fetch_intervals(self._h, None, 0, C.byref(n)), "fetch_intervals(size)")
+        P = np.zeros(n.value, dtype=np.int32)
+        self._check(lib().uniap_fetch_intervals(self._h, P.ctypes.data_as(_P32), P.size, None), "fetch_intervals")
+        return P
 
     def shard_assign(self, world):
         owner = (C.c_int32 * max(self.n_cfg, 1))()

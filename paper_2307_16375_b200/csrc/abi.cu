@@ -54,6 +54,31 @@ bool env_flag(const char* name) {
 
 }  // namespace
 
+// Per-stage memory caps of one config (NEXT-2): the distinct caps in order
+// of first appearance over the stages, and each stage's level.
+struct Levels {
+  int nlev = 1;
+  int32_t lcap[MAXLEV] = {0, 0, 0, 0};
+  std::vector<int8_t> lev_of;  // [deg]
+};
+// caps: [deg] per-stage caps (empty = every stage at cap).  false if more
+// than MAXLEV distinct values.
+static bool make_levels(int deg, int cap, const std::vector<int32_t>& caps, Levels& lv) {
+  lv.nlev = 0;
+  lv.lev_of.assign(std::max(deg, 1), 0);
+  for (int i = 0; i < std::max(deg, 1); ++i) {
+    const int32_t c = caps.empty() ? cap : caps[i];
+    int l = 0;
+    while (l < lv.nlev && lv.lcap[l] != c) ++l;
+    if (l == lv.nlev) {
+      if (lv.nlev == MAXLEV) return false;
+      lv.lcap[lv.nlev++] = c;
+    }
+    lv.lev_of[i] = (int8_t)l;
+  }
+  return true;
+}
+
 // one K2 launch: instances of one kernel class
 struct K2Group {
   size_t s, e;  // [s, e) in the uploaded instance array
@@ -146,6 +171,10 @@ struct uniap_handle {
   // forward P sweep at its feasible prefix (Eq. 5).  Level 2: K1f does it on
   // the device from the builder's M (k1f_trim).
   std::vector<int32_t> minM;
+  // per-stage memory caps (NEXT-2): per config its levels and stage caps
+  std::vector<Levels> lev;
+  std::vector<std::vector<int32_t>> scap;
+  int64_t P_words = 0;  // interval tables of every config and cap level
 };
 
 // A prepared problem keeps the launch plan and the captured graph when
@@ -364,31 +393,38 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   delete h;
 }
 
-static void plan_instances(int L, int i, int deg, int S, int skip, bool all_intervals, std::vector<Inst>& out);
-static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>& out);
+static void plan_instances(int L, int i, int deg, int S, int skip, bool all_intervals, int ecap, std::vector<Inst>& out);
+static void plan_fast(int L, int i, int deg, int S, int skip, const Levels& lv, std::vector<Inst>& out);
 
 // ---------------------------------------------------------------------------
 // Layout of the configs in the device arena.
 // ---------------------------------------------------------------------------
 // keep[i]: the strategies of config i that can be feasible (ascending caller
 // indices); the tables, kernels and plan use only these (S = keep size).
+// caps[i]: the per-stage caps of config i ([deg], or empty = all at cap).
 static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vector<int>>& keep,
                                    const std::vector<int>& Sfull, const std::vector<int>& deg,
-                                   const std::vector<int>& c, const std::vector<int>& g, const std::vector<int>& skipc) {
+                                   const std::vector<int>& c, const std::vector<int>& g, const std::vector<int>& skipc,
+                                   const std::vector<std::vector<int32_t>>& caps) {
   const int L = h->L;
   std::vector<int> S(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i) S[i] = (int)keep[i].size();
   h->cfg.assign(h->ncfg, CfgDev{});
   h->cls.assign(h->ncfg, K2Class{});
   h->bcls.assign(h->ncfg, K2Class{});
-  int64_t off = 0;
+  h->lev.assign(h->ncfg, Levels{});
+  h->scap = caps;
+  int64_t off = 0, poff = 0;
+  for (int i = 0; i < h->ncfg; ++i)
+    if (!make_levels(deg[i], h->cap, caps[i], h->lev[i]))
+      FAIL(h, UNIAP_ERR_RANGE, "config %d: more than %d distinct per-stage caps", i, MAXLEV);
   for (int i = 0; i < h->ncfg; ++i) {
     // a config with only a few (long) chains spreads each over more SMs
     // (deg = 1: the whole chain, or its |S| skip-conditioned copies, is the
     // critical path of the step; measured: giving deg = 2's prefix + suffix
     // sweeps the same treatment starves the many-sweep classes of SMs)
     std::vector<Inst> v;
-    plan_fast(L, i, deg[i], S[i], skipc[i], v);
+    plan_fast(L, i, deg[i], S[i], skipc[i], h->lev[i], v);
     const bool single = !v.empty() && (deg[i] == 1 || v.size() <= 1);
     const bool few = !v.empty() && v.size() <= 4;  // deg = 2 (prefix + suffix): keep clusters
     K2Class k;
@@ -412,9 +448,14 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     d.offRf = off; off += (int64_t)(L - 1) * NSP * NSP;
     d.offRs = off; off += (int64_t)L * NSP * NSP;
     d.offO = off; off += std::max(4, round4(L - 1));
-    d.offP = (int64_t)i * L * L;
+    const Levels& lv = h->lev[i];
+    d.nlev = lv.nlev;
+    for (int l = 0; l < MAXLEV; ++l) d.lcap[l] = l < lv.nlev ? lv.lcap[l] : h->cap;
+    for (int st = 0; st < MAXL; ++st) d.lev_of[st] = st < (int)lv.lev_of.size() ? lv.lev_of[st] : 0;
+    d.offP = poff; poff += (int64_t)lv.nlev * L * L;  // one L*L interval table per cap level
   }
   h->arena_words = off;
+  h->P_words = poff;
   return UNIAP_OK;
 }
 
@@ -488,7 +529,16 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
     for (int u = 0; u < L; ++u)
       for (int k : keep[i]) h->minM[(size_t)i * L + u] = std::min(h->minM[(size_t)i * L + u], x.M[u * x.n_strat + k]);
   }
-  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc);
+  std::vector<std::vector<int32_t>> caps(h->ncfg);
+  for (int i = 0; i < h->ncfg; ++i)
+    if (t->cfg[i].stage_cap) {
+      for (int st = 0; st < t->cfg[i].deg; ++st) {
+        const int32_t v = t->cfg[i].stage_cap[st];
+        if (v < 0 || v > t->cap) FAIL(h, UNIAP_ERR_ARG, "config %d: stage_cap[%d] = %d out of 0..cap", i, st, v);
+        caps[i].push_back(v);
+      }
+    }
+  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps);
   if (st != UNIAP_OK) return st;
   // pack the host tables into the device layout (pads: A 0, M cap+1, R 0)
   std::vector<int32_t> a(h->arena_words, 0);
@@ -638,7 +688,24 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
       if (h->no_compact || b % (h->cat[i].tfd[3 * k + 1] * h->cat[i].tfd[3 * k + 2]) == 0) keep[i].push_back(k);
     if (keep[i].empty()) keep[i].push_back(0);
   }
-  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc);
+  // per-stage caps from the per-device memory (NEXT-2): stage
+  // i of (deg, g) runs on devices i*g .. i*g+g-1; its cap in buckets is
+  // floor((their smallest memory - reserve) / unit), the capacity side of
+  // reading A-8 (bucket-feasible => byte-feasible on every device)
+  std::vector<std::vector<int32_t>> caps(h->ncfg);
+  if (cl->dev_mem_bytes) {
+    for (int d = 0; d < n; ++d)
+      if (cl->dev_mem_bytes[d] <= cl->mem_reserve_bytes || cl->dev_mem_bytes[d] > cl->mem_bytes)
+        FAIL(h, UNIAP_ERR_ARG, "dev_mem_bytes[%d] outside (reserve, mem_bytes]", d);
+    const int64_t unit = (cl->mem_bytes - cl->mem_reserve_bytes) / (o->Q - 1);
+    for (int i = 0; i < h->ncfg; ++i)
+      for (int stg = 0; stg < deg[i]; ++stg) {
+        int64_t m = cl->mem_bytes;
+        for (int d = stg * g[i]; d < (stg + 1) * g[i]; ++d) m = std::min(m, cl->dev_mem_bytes[d]);
+        caps[i].push_back((int32_t)std::min<int64_t>((m - cl->mem_reserve_bytes) / unit, o->Q - 1));
+      }
+  }
+  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps);
   if (st != UNIAP_OK) return st;
   h->minM.clear();  // the sweep trim runs on the device (k1f_trim)
   h->cl = ClusterDev{cl->n_dev, cl->node_size, cl->ccoc_permille, o->B, o->precision, o->Q, NT, 0,
@@ -696,7 +763,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
 // Canonical plan (the survey's work definition; also the all-intervals mode
 // of uniap_interval_table): one forward sweep per start layer a, over every
 // interval [a, b] a deg-stage ordered placement can use.
-static void plan_instances(int L, int i, int deg, int S, int skip, bool all_intervals, std::vector<Inst>& out) {
+static void plan_instances(int L, int i, int deg, int S, int skip, bool all_intervals, int ecap, std::vector<Inst>& out) {
   if (!all_intervals && deg > L) return;
   for (int a = 0; a < L; ++a) {
     int bmax;
@@ -706,9 +773,9 @@ static void plan_instances(int L, int i, int deg, int S, int skip, bool all_inte
     if (bmax < a) continue;
     const int n = bmax - a + 1;
     if (skip >= 0 && a <= skip && bmax >= skip + 2) {
-      for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0, a, bmax});
+      for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0, a, bmax, n, 0, ecap});
     } else {
-      out.push_back(Inst{i, a, n, -1, +1, 1, 0, a, bmax});
+      out.push_back(Inst{i, a, n, -1, +1, 1, 0, a, bmax, n, 0, ecap});
     }
   }
 }
@@ -723,15 +790,19 @@ static void plan_instances(int L, int i, int deg, int S, int skip, bool all_inte
 // source s inside a sweep, one copy per strategy ks of s (Eq. 3 couples it
 // with later layers); a suffix sweep emits the conditioned copies for a <= s
 // and an unconditioned sweep for a > s.
-static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>& out) {
+// With per-stage caps (NEXT-2) a sweep emits the optima under ONE cap level
+// (column ecap of its state): the prefix sweep under stage 1's, the suffix
+// sweep under the last stage's, and the middle sweeps once per distinct
+// level among the middle stages, starting where a stage of that level can.
+static void plan_fast(int L, int i, int deg, int S, int skip, const Levels& lv, std::vector<Inst>& out) {
   if (deg > L) return;
-  auto fwd = [&](int a, int bmax) {
+  auto fwd = [&](int a, int bmax, int lev) {
     if (bmax < a) return;
-    const int n = bmax - a + 1;
+    const int n = bmax - a + 1, ec = lv.lcap[lev];
     if (skip >= 0 && a <= skip && bmax >= skip + 2) {
-      for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0, a, bmax});
+      for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0, a, bmax, n, lev, ec});
     } else {
-      out.push_back(Inst{i, a, n, -1, +1, 1, 0, a, bmax});
+      out.push_back(Inst{i, a, n, -1, +1, 1, 0, a, bmax, n, lev, ec});
     }
   };
   if (deg == 1) {
@@ -739,28 +810,34 @@ static void plan_fast(int L, int i, int deg, int S, int skip, std::vector<Inst>&
     // tables: the traceback of a deg = 1 winner then needs no sweep of its
     // own (gofs assigned by make_plan).  With the skip source inside, the
     // |S| conditioned copies would keep |S| tables: plain forward sweep.
-    if ((skip >= 0 && skip + 2 <= L - 1) || S == 1) fwd(0, L - 1);  // |S| = 1: closed form, no G
-    else out.push_back(Inst{i, L - 1, L, -1, -1, 5, -1, 0, 0});
+    const int l0 = lv.lev_of[0];
+    if ((skip >= 0 && skip + 2 <= L - 1) || S == 1) fwd(0, L - 1, l0);  // |S| = 1: closed form, no G
+    else out.push_back(Inst{i, L - 1, L, -1, -1, 5, -1, 0, 0, L, l0, lv.lcap[l0]});
     return;
   }
-  fwd(0, L - deg);                                               // stage 1: prefixes
-  for (int a = 1; a <= L - 2 && deg >= 3; ++a)                   // middle stages
-    fwd(a, L - 1 - deg + std::min(a + 1, deg - 1));
+  fwd(0, L - deg, lv.lev_of[0]);                                 // stage 1: prefixes
+  for (int l = 0; l < lv.nlev && deg >= 3; ++l)                  // middle stages, per cap level:
+    for (int a = 1; a <= L - 2; ++a) {                           // stage i (0-based 1..deg-2) can
+      int im = -1;                                               // start at a >= i and end at
+      for (int st = 1; st <= std::min(a, deg - 2); ++st)         // b <= L - deg + i
+        if (lv.lev_of[st] == l) im = st;
+      if (im >= 0) fwd(a, L - deg + im, l);
+    }
   const int amin = deg - 1, b = L - 1;                           // last stage: suffixes
+  const int ll = lv.lev_of[deg - 1], ec = lv.lcap[ll];
   if (skip >= 0 && amin <= skip && b >= skip + 2) {
-    for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, b, b - amin + 1, ks, -1, 2, 0, amin, skip});
-    if (skip + 1 <= b) out.push_back(Inst{i, b, b - skip, -1, -1, 1, 0, skip + 1, b});
+    for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, b, b - amin + 1, ks, -1, 2, 0, amin, skip, b - amin + 1, ll, ec});
+    if (skip + 1 <= b) out.push_back(Inst{i, b, b - skip, -1, -1, 1, 0, skip + 1, b, b - skip, ll, ec});
   } else {
-    out.push_back(Inst{i, b, b - amin + 1, -1, -1, 1, 0, amin, b});
+    out.push_back(Inst{i, b, b - amin + 1, -1, -1, 1, 0, amin, b, b - amin + 1, ll, ec});
   }
 }
 
 static void forward_instances(const uniap_handle* h, int i, bool all_intervals, std::vector<Inst>& out) {
   const CfgDev& d = h->cfg[i];
   const size_t first = out.size();
-  if (all_intervals) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, out);
-  else plan_fast(h->L, i, d.deg, d.S, d.skip, out);
-  for (size_t j = first; j < out.size(); ++j) out[j].n0 = out[j].n;
+  if (all_intervals) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, h->cap, out);
+  else plan_fast(h->L, i, d.deg, d.S, d.skip, h->lev[i], out);
   // Level 1: stop each forward P sweep where it becomes infeasible -- the
   // memory sum of Eq. 5 over the layers swept is at least the running sum of
   // the per-layer minima of the caller's M, so past the first layer where
@@ -776,7 +853,7 @@ static void forward_instances(const uniap_handle* h, int i, bool all_intervals, 
     int n = 0;
     for (; n < x.n; ++n) {
       sum += h->minM[(size_t)i * L + x.a + x.dir * n];  // (a lower bound also at a conditioned skip layer)
-      if (sum > h->cap) break;
+      if (sum > x.ecap) break;
     }
     x.n = std::max(n, 1);
     if (x.dir > 0) x.ehi = std::min(x.ehi, x.a + x.n - 1);  // emit only the layers swept
@@ -787,13 +864,14 @@ static void forward_instances(const uniap_handle* h, int i, bool all_intervals, 
 // LPT over configs by executed chain-DP work (sum over the sweeps of n |S|^2 Q); ties
 // keep the candidate order, the least-loaded (then lowest) rank takes the next.
 static void lpt_shapes(int L, int Q, const std::vector<int>& deg, const std::vector<int>& S,
-                       const std::vector<int>& skip, int world, std::vector<int>& owner) {
+                       const std::vector<int>& skip, const std::vector<Levels>& lev, int world,
+                       std::vector<int>& owner) {
   const int n = (int)deg.size();
   std::vector<int> order(n);
   std::vector<double> w(n);
   for (int i = 0; i < n; ++i) {
     std::vector<Inst> v;
-    plan_fast(L, i, deg[i], S[i], skip[i], v);  // the executed sweeps
+    plan_fast(L, i, deg[i], S[i], skip[i], lev[i], v);  // the executed sweeps
     double x = 1.0;  // + the combine
     for (auto& e : v) x += (double)e.n * S[i] * S[i] * Q;
     order[i] = i;
@@ -814,14 +892,18 @@ static void lpt_shapes(int L, int Q, const std::vector<int>& deg, const std::vec
 static void lpt(const uniap_handle* h, int world, std::vector<int>& owner) {
   std::vector<int> deg(h->ncfg), S(h->ncfg), sk(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i) { deg[i] = h->cfg[i].deg; S[i] = h->cfg[i].S; sk[i] = h->cfg[i].skip; }
-  lpt_shapes(h->L, h->Q, deg, S, sk, world, owner);
+  lpt_shapes(h->L, h->Q, deg, S, sk, h->lev, world, owner);
 }
 
 extern "C" uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world, int32_t* owner_out) {
   if (!t || !t->cfg || !owner_out || world < 1 || t->n_cfg < 1 || t->L < 1) return UNIAP_ERR_ARG;
   std::vector<int> deg(t->n_cfg), S(t->n_cfg), sk(t->n_cfg), owner;
+  std::vector<Levels> lev(t->n_cfg);
   for (int i = 0; i < t->n_cfg; ++i) {
     deg[i] = t->cfg[i].deg;
+    std::vector<int32_t> caps;
+    if (t->cfg[i].stage_cap) caps.assign(t->cfg[i].stage_cap, t->cfg[i].stage_cap + deg[i]);
+    if (!make_levels(deg[i], t->cap, caps, lev[i])) return UNIAP_ERR_RANGE;
     // the strategy count the prepared tables hold (strategies feasible at some layer)
     const uniap_config& x = t->cfg[i];
     if (!x.M || x.n_strat < 1) return UNIAP_ERR_ARG;
@@ -834,7 +916,7 @@ extern "C" uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world,
     S[i] = std::max(S[i], 1);
     sk[i] = (x.Rskip && t->skip_src >= 0) ? t->skip_src : -1;
   }
-  lpt_shapes(t->L, t->cap + 1, deg, S, sk, world, owner);
+  lpt_shapes(t->L, t->cap + 1, deg, S, sk, lev, world, owner);
   for (int i = 0; i < t->n_cfg; ++i) owner_out[i] = owner[i];
   return UNIAP_OK;
 }
@@ -1003,7 +1085,7 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   h->cells_canon = 0;
   for (int i : R.local) {
     std::vector<Inst> cv;
-    plan_instances(h->L, i, h->cfg[i].deg, h->cfg[i].Sfull, h->cfg[i].skip, false, cv);
+    plan_instances(h->L, i, h->cfg[i].deg, h->cfg[i].Sfull, h->cfg[i].skip, false, h->cap, cv);
     for (auto& x : cv) h->cells_canon += (uint64_t)x.n * h->cfg[i].Sfull * h->Q;
   }
   group_instances(h, fw, R.fgrp);
@@ -1073,7 +1155,7 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   int max_bw = 1;
   for (auto& g : R.bgrp) max_bw = std::max(max_bw, g.max_inst);
   // device buffers + uploads (outside any graph)
-  CK(h, h->P.ensure((size_t)h->ncfg * h->L * h->L));
+  CK(h, h->P.ensure((size_t)h->P_words));
   CK(h, h->inst.ensure(std::max<size_t>(fw.size(), 1)));
   CK(h, h->binst.ensure(max_bw));
   CK(h, h->G.ensure(gmax));
@@ -1132,7 +1214,7 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     CK(h, cudaEventRecord(h->fork_ev, h->st));
     CK(h, cudaStreamWaitEvent(h->side[0], h->fork_ev, 0));
     CK(h, cudaMemsetAsync(h->tim.p, 0, 2 * sizeof(unsigned long long), h->side[0]));  // forward phase clock
-    CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->side[0]));
+    CK(h, launch_fill(h->P.p, h->P_words, INF, h->side[0]));
     CK(h, cudaEventRecord(h->side_ev[0], h->side[0]));
     BuildBufs bb = build_bufs(h);
     bb.inst = h->inst.p;  // K1f trims the forward sweeps of this plan (k1f_trim)
@@ -1145,7 +1227,7 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     h->launches += 3;
   } else {
     CK(h, cudaMemsetAsync(h->tim.p, 0, 2 * sizeof(unsigned long long), h->st));  // forward phase clock
-    CK(h, launch_fill(h->P.p, (int64_t)h->ncfg * L * L, INF, h->st));
+    CK(h, launch_fill(h->P.p, h->P_words, INF, h->st));
   }
   h->launches++;
 
@@ -1334,8 +1416,8 @@ extern "C" uniap_status uniap_interval_table(uniap_handle* h, const uniap_tables
   const int L = h->L;
   std::vector<Inst> fw;
   forward_instances(h, cfg, true, fw);
-  CK(h, h->iP.ensure((size_t)h->ncfg * L * L));
-  CK(h, launch_fill(h->iP.p, (int64_t)h->ncfg * L * L, INF, h->st));
+  CK(h, h->iP.ensure((size_t)h->P_words));
+  CK(h, launch_fill(h->iP.p, h->P_words, INF, h->st));
   s = launch_k2_groups(h, fw, h->iinst, h->iP.p);
   if (s != UNIAP_OK) return s;
   CK(h, d2h(h, P_out, h->iP.p + h->cfg[cfg].offP, (size_t)L * L * 4));
@@ -1344,10 +1426,12 @@ extern "C" uniap_status uniap_interval_table(uniap_handle* h, const uniap_tables
   return UNIAP_OK;
 }
 
-extern "C" uniap_status uniap_fetch_intervals(uniap_handle* h, int32_t* P_out, int64_t P_len) {
-  if (!h || !P_out) return UNIAP_ERR_ARG;
+extern "C" uniap_status uniap_fetch_intervals(uniap_handle* h, int32_t* P_out, int64_t P_len, int64_t* P_words) {
+  if (!h) return UNIAP_ERR_ARG;
   if (!h->last_rec || !h->plan.valid || !h->P.p) FAIL(h, UNIAP_ERR_ARG, "nothing has run on this handle");
-  const int64_t n = (int64_t)h->ncfg * h->L * h->L;
+  const int64_t n = h->P_words;
+  if (P_words) *P_words = n;
+  if (!P_out) return UNIAP_OK;
   if (P_len < n) FAIL(h, UNIAP_ERR_ARG, "P_len %lld < %lld", (long long)P_len, (long long)n);
   CK(h, cudaSetDevice(h->device));
   CK(h, d2h(h, P_out, h->P.p, (size_t)n * 4));
@@ -1364,7 +1448,8 @@ extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m
   if (s != UNIAP_OK) return s;
   const int L = h->L;
   int64_t need = 0;
-  for (auto& d : h->cfg) need += 4 + 2 * (int64_t)L * d.S + (int64_t)(L - 1) * d.S * d.S + (int64_t)L * d.S * d.S + (L - 1);
+  for (auto& d : h->cfg)
+    need += 4 + 2 * (int64_t)L * d.S + (int64_t)(L - 1) * d.S * d.S + (int64_t)L * d.S * d.S + (L - 1) + d.deg;
   if (words) *words = need;
   if (n_cfg) *n_cfg = h->ncfg;
   if (skip_src) *skip_src = h->skip;
@@ -1395,6 +1480,7 @@ extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m
       for (int k = 0; k < S; ++k)
         for (int l = 0; l < S; ++l) buf[w++] = a[d.offRs + ((int64_t)v * N + k) * N + l];
     for (int e = 0; e + 1 < L; ++e) buf[w++] = a[d.offO + e];
+    for (int st = 0; st < d.deg; ++st) buf[w++] = h->scap[i].empty() ? h->cap : h->scap[i][st];
   }
   return UNIAP_OK;
 }

@@ -22,7 +22,7 @@ int k2_ns_round(int S) {
 
 static size_t smem_words(int NS, int B, int ne = 2) {
   const int NSP = (NS + 3) & ~3;
-  return (size_t)ne * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP) + MAXL;
+  return (size_t)ne * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP) + MAXL + 4;  // + the emission words
 }
 
 size_t k2_smem_bytes(const K2Class& c) { return smem_words(c.NS, c.T * c.V, c.DB ? 2 : 1) * sizeof(int32_t); }
@@ -147,7 +147,7 @@ __global__ void k2_closed_s1(const K2Args args, int n_inst) {
   const int32_t* M = args.arena + cf.offM;
   const int32_t* Rf = args.arena + cf.offRf;
   const int32_t* Rs = args.arena + cf.offRs;
-  int32_t* Pc = args.P + cf.offP;
+  int32_t* Pc = args.P + cf.offP + (int64_t)in.lev * L * L;
   for (int uu = in.elo + (int)threadIdx.x; uu <= in.ehi; uu += blockDim.x) {
     const int lo = in.dir > 0 ? in.a : uu, hi = in.dir > 0 ? uu : in.a;
     int64_t cost = 0, mem = 0;
@@ -157,7 +157,7 @@ __global__ void k2_closed_s1(const K2Args args, int n_inst) {
       if (v > lo) cost += Rf[(int64_t)(v - 1) * NSP * NSP];
       mem += M[(int64_t)v * NSP];
     }
-    const int32_t val = mem <= args.cap ? (int32_t)min(cost, (int64_t)INF) : INF;
+    const int32_t val = mem <= in.ecap ? (int32_t)min(cost, (int64_t)INF) : INF;
     int32_t* dst = in.dir > 0 ? Pc + (int64_t)in.a * L + uu : Pc + (int64_t)uu * L + in.a;
     if ((in.emit & 3) == 2) atomicMin(dst, val);
     else *dst = val;

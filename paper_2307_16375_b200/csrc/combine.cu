@@ -84,9 +84,9 @@ __device__ int sort_thetas(const CfgDev& cf, const int32_t* __restrict__ arena, 
   const int t = threadIdx.x;
   for (int i = t; i < SORTN; i += K3T) v[i] = EMPTY;
   __syncthreads();
-  const int32_t* Pc = P + cf.offP;
-  for (int idx = t; idx < L * L; idx += K3T) {
-    const int a = idx / L, b = idx - a * L;
+  const int32_t* Pc = P + cf.offP;  // one L*L table per cap level (NEXT-2)
+  for (int idx = t; idx < cf.nlev * L * L; idx += K3T) {
+    const int r = idx % (L * L), a = r / L, b = r - a * L;
     const int32_t x = Pc[idx];
     sP[idx] = x;
     if (a <= b && x < INF) hset_insert(v, x);
@@ -160,8 +160,11 @@ __device__ int sort_thetas(const CfgDev& cf, const int32_t* __restrict__ arena, 
 // and accumulates with one DPX op (unsigned: INF + INF = 2^31 fits), two
 // accumulators per column for ILP.
 // ---------------------------------------------------------------------------
+// slev[i]: the cap level of stage i (0-based; NEXT-2): stage i reads the
+// interval table sP + slev[i] * L * L.
 template <bool BOTTLENECK, bool MASK>
-__device__ int32_t warp_dp(const int32_t* sP, const int32_t* sO, int32_t* g, int L, int deg, int32_t theta) {
+__device__ int32_t warp_dp(const int32_t* sPall, const int32_t* slev, const int32_t* sO, int32_t* g, int L, int deg,
+                           int32_t theta) {
   const int lane = threadIdx.x & 31;
   const int b0 = lane, b1 = lane + 32;
   auto mask = [&](int32_t p) { return (MASK && p > theta) ? INF : p; };
@@ -177,6 +180,7 @@ __device__ int32_t warp_dp(const int32_t* sP, const int32_t* sO, int32_t* g, int
   };
   int32_t c0 = INF, c1 = INF;
   {  // stage 1 = [0, b], b <= L - deg
+    const int32_t* sP = sPall + slev[0] * L * L;
     if (b0 < L && b0 <= L - deg) c0 = mask(sP[b0]);
     if (b1 < L && b1 <= L - deg) c1 = mask(sP[b1]);
     if (deg > 1) {
@@ -186,6 +190,7 @@ __device__ int32_t warp_dp(const int32_t* sP, const int32_t* sO, int32_t* g, int
   }
   for (int i = 2; i <= deg; ++i) {
     __syncwarp();
+    const int32_t* sP = sPall + slev[i - 1] * L * L;
     const int32_t* w = g + ((i & 1) ? 64 : 0);  // written by stage i-1
     int32_t* wn = g + ((i & 1) ? 0 : 64);
     const int blo = (i == deg) ? L - 1 : i - 1, bhi = L - 1 - (deg - i);
@@ -233,9 +238,10 @@ __device__ int32_t warp_dp(const int32_t* sP, const int32_t* sO, int32_t* g, int
   __syncwarp();
   return F;
 }
-__device__ __forceinline__ int32_t warp_F(const int32_t* sP, const int32_t* sO, int32_t* g, int L, int deg,
-                                          int32_t theta) {
-  return theta >= INF ? warp_dp<false, false>(sP, sO, g, L, deg, INF) : warp_dp<false, true>(sP, sO, g, L, deg, theta);
+__device__ __forceinline__ int32_t warp_F(const int32_t* sP, const int32_t* slev, const int32_t* sO, int32_t* g, int L,
+                                          int deg, int32_t theta) {
+  return theta >= INF ? warp_dp<false, false>(sP, slev, sO, g, L, deg, INF)
+                      : warp_dp<false, true>(sP, slev, sO, g, L, deg, theta);
 }
 
 // ---------------------------------------------------------------------------
@@ -252,7 +258,8 @@ __device__ __forceinline__ int32_t warp_F(const int32_t* sP, const int32_t* sO, 
 constexpr int K4W = 32;
 struct K4Smem {
   int32_t v[SORTN];  // sorted distinct thetas (K3)
-  int32_t sP[MAXL * MAXL];
+  int32_t sP[MAXLEV * MAXL * MAXL];  // the config's interval tables, one per cap level
+  int32_t slev[MAXL];                // cap level of each stage
   int32_t sO[MAXL];
   int32_t g[K4W][128];
   int32_t probeF[K4W];
@@ -279,7 +286,10 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
   const CfgDev cf = cfgs[cfg_list[li]];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // K3 fused: the sorted distinct theta candidates (also kept for K5a)
+  for (int i = threadIdx.x; i < MAXL; i += blockDim.x)  // (from global: no local copy of cf; visible after
+    S.slev[i] = cfgs[cfg_list[li]].lev_of[i];           //  sort_thetas' first barrier)
   const int nt = sort_thetas(cf, arena, P, L, S.v, sP, sO, S.scan_tmp);
+  const int32_t* slev = S.slev;
   for (int i = threadIdx.x; i < nt; i += blockDim.x) thetas[(int64_t)li * TMAX + i] = S.v[i];
   if (threadIdx.x == 0) ntheta[li] = nt;
   int64_t* V = vals + (int64_t)li * (TMAX + 2);  // [0..nt) Val, [TMAX] F_inf, [TMAX+1] opt
@@ -294,7 +304,7 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
     // few candidates: every F_theta in one round, one warp each (the
     // largest theta bounds every P and O, so F of it is F_inf)
     if (w < nt) {
-      const int32_t F = warp_F(sP, sO, g[w], L, cf.deg, w == nt - 1 ? INF : S.v[w]);
+      const int32_t F = warp_F(sP, slev, sO, g[w], L, cf.deg, w == nt - 1 ? INF : S.v[w]);
       if (lane == 0) probeF[w] = F;
     }
     __syncthreads();
@@ -315,10 +325,10 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
   }
   // 1. F_inf (warp 0) and the bottleneck theta_min (warp 1)
   if (w == 0) {
-    const int32_t F = warp_F(sP, sO, g[0], L, cf.deg, INF);
+    const int32_t F = warp_F(sP, slev, sO, g[0], L, cf.deg, INF);
     if (lane == 0) probeF[0] = F;
   } else if (w == 1) {
-    const int32_t Bm = warp_dp<true, false>(sP, sO, g[1], L, cf.deg, INF);
+    const int32_t Bm = warp_dp<true, false>(sP, slev, sO, g[1], L, cf.deg, INF);
     if (lane == 0) probeF[1] = Bm;
   }
   __syncthreads();
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
   const int imin = s_hi;
   // 3. U = Val(theta_min); evaluate theta_min .. theta_hi
   if (w == 0) {
-    const int32_t F = warp_F(sP, sO, g[0], L, cf.deg, th[imin]);
+    const int32_t F = warp_F(sP, slev, sO, g[0], L, cf.deg, th[imin]);
     if (lane == 0) {
       const int64_t U = (int64_t)F + cm1 * th[imin];
       V[imin] = U;
@@ -361,7 +371,7 @@ __global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ c
     const int64_t lb = (int64_t)Finf + cm1 * theta;
     if (lb > U) break;  // ascending thetas: every later one is worse too
     if ((unsigned long long)lb > *(volatile unsigned long long*)&s_best) continue;
-    const int32_t F = warp_F(sP, sO, g[w], L, cf.deg, theta);
+    const int32_t F = warp_F(sP, slev, sO, g[w], L, cf.deg, theta);
     if (g_trace && lane == 0) atomicAdd(&S.cnt, 1);  // diagnostics: thetas evaluated
     if (F < INF && lane == 0) {
       const int64_t val = (int64_t)F + cm1 * theta;
@@ -391,7 +401,10 @@ cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P,
 // (= lexicographically smallest stage_of, reading A-11).  One CTA.
 // ---------------------------------------------------------------------------
 constexpr int K5T = 1024;
-constexpr int K5A_DYN = (MAXL + 1) * (MAXL + 1) * 4;  // K5a's shared suffix table (dynamic: static is near 48 KB)
+constexpr int K5PP = MAXL + 1;  // odd pitch of K5a's interval tables
+// K5a's dynamic shared memory: the suffix table H, then the winner's interval
+// tables (one per cap level)
+constexpr int K5A_DYN = (MAXL + 1) * (MAXL + 1) * 4 + MAXLEV * MAXL * K5PP * 4;
 __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
                                                   const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
                                                   int n_local, int L, const int32_t* __restrict__ thetas,
@@ -399,7 +412,6 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
                                                   const int64_t* __restrict__ cfg_opt, int32_t* __restrict__ scratch,
                                                   Winner* __restrict__ win, RecordArgs ra) {
   TraceScope tr(TR_K5A);
-  __shared__ int32_t sP[MAXL * (MAXL + 1)];  // P[a][b] at a * PP + b, odd pitch: lanes over a or b conflict-free
   __shared__ int32_t sO[MAXL];
   __shared__ int32_t stars[TMAX];
   __shared__ int32_t nstar;
@@ -478,8 +490,19 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
   const int64_t* V = vals + (int64_t)wl * (TMAX + 2);
   const int32_t* th = thetas + (int64_t)wl * TMAX;
   const int nt = ntheta[wl];
+  // the winner's interval tables P_lev[a][b] at lev * L * PP + a * PP + b
+  // (odd pitch: lanes over a or b conflict-free), in dynamic shared memory
+  // after the suffix table sH
+  extern __shared__ int32_t k5dyn[];
+  int32_t* sPl = k5dyn + (MAXL + 1) * (MAXL + 1);
   const int PP = L | 1;
-  for (int i = t; i < L * L; i += K5T) sP[(i / L) * PP + i % L] = P[cf.offP + i];
+  for (int i = t; i < cf.nlev * L * L; i += K5T) {
+    const int lv = i / (L * L), r = i - lv * L * L;
+    sPl[lv * L * PP + (r / L) * PP + r % L] = P[cf.offP + i];
+  }
+  // stage i (1-based) reads the table of its cap level
+  const int8_t* lev_of = cfgs[ci].lev_of;  // (global: no local copy of cf)
+  auto SPs = [&](int i) { return sPl + lev_of[i - 1] * L * PP; };
   for (int i = t; i < L - 1; i += K5T) sO[i] = arena[cf.offO + i];
   // 3. Theta*: every theta with Val = OPT (c > 1); the unconstrained one (c = 1)
   if (cf.c == 1) {
@@ -501,19 +524,20 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
   // memory -- stages sequential (one barrier each), warps over the start a,
   // lanes over the end b with a warp min.  Many: one warp per theta below.
   constexpr int HP = MAXL + 1;
-  extern __shared__ int32_t sH[];  // dynamic, K5A_DYN bytes: [i][a], i = 1..deg, a = 0..L
+  int32_t* sH = k5dyn;  // [i][a], i = 1..deg, a = 0..L
   for (int si = 0; si < ns && ns <= 4; ++si) {
     const int32_t theta = stars[si] < 0 ? INF : th[stars[si]];
     const int64_t F_target = stars[si] < 0 ? OPT : OPT - (int64_t)(cf.c - 1) * theta;
     for (int a = t; a <= L; a += K5T) {
       int32_t v = INF;
-      if (a < L) { const int32_t p = sP[a * PP + L - 1]; v = p <= theta ? p : INF; }
+      if (a < L) { const int32_t p = SPs(deg)[a * PP + L - 1]; v = p <= theta ? p : INF; }
       sH[deg * HP + a] = v;
     }
     __syncthreads();
     for (int i = deg - 1; i >= 1; --i) {
-      // H_i[a] = min_b P[a][b] + O[b] + H_{i+1}[b+1], b <= L-1-(deg-i)
+      // H_i[a] = min_b P_i[a][b] + O[b] + H_{i+1}[b+1], b <= L-1-(deg-i)
       const int bhi = L - 1 - (deg - i);
+      const int32_t* sP = SPs(i);
       for (int a = w; a <= L; a += K5T / 32) {
         uint32_t v = INF;
         for (int b = a + lane; b <= bhi && a < L; b += 32) {
@@ -531,6 +555,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
       int64_t pre = 0;
       int a = 0;
       for (int i = 1; i < deg && ok; ++i) {
+        const int32_t* sP = SPs(i);
         int found = -1;
         for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
           const int b = b0 - lane;
@@ -574,7 +599,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
       // H_deg[a] = P[a][L-1]
       for (int a = lane; a <= L; a += 32) {
         int32_t v = INF;
-        if (a < L) { const int32_t p = sP[a * PP + L - 1]; v = p <= theta ? p : INF; }
+        if (a < L) { const int32_t p = SPs(deg)[a * PP + L - 1]; v = p <= theta ? p : INF; }
         H[deg * (MAXL + 1) + a] = v;
       }
       __syncwarp();
@@ -583,6 +608,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
         // lane-independent (broadcast), P[a][b] read transposed
         const int bhi = L - 1 - (deg - i);
         const int32_t* Hn = H + (i + 1) * (MAXL + 1);
+        const int32_t* sP = SPs(i);
         for (int a = lane; a <= L; a += 32) {
           uint32_t x = INF, y = INF;
           if (a < L) {
@@ -610,6 +636,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
       int64_t pre = 0;
       int a = 0;
       for (int i = 1; i < deg && ok; ++i) {
+        const int32_t* sP = SPs(i);
         int found = -1;
         for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
           const int b = b0 - lane;
@@ -660,7 +687,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     for (int i = 0; i < deg; ++i) {
       const int b = have ? best_end[i] : L - 1;
       win->end[i] = b;
-      win->p[i] = sP[a * PP + b];
+      win->p[i] = SPs(i + 1)[a * PP + b];
       win->o[i] = (i + 1 < deg) ? sO[b] : 0;
       a = b + 1;
     }
@@ -737,7 +764,7 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
     const int ks = cond ? w : -1;
     const int32_t* g = G + bw->gofs[stage * 33 + (ks + 1)];
     int64_t rest = W.p[stage];
-    int q = cap, kprev = -1;
+    int q = cfgs[W.cfg].lcap[cfgs[W.cfg].lev_of[stage]], kprev = -1;  // the stage's own memory cap (NEXT-2)
     int32_t msum = 0;
     ok = true;
     for (int u = a; u <= b && ok; ++u) {

@@ -26,6 +26,7 @@ constexpr int32_t INF = UNIAP_INF;
 constexpr int MAXL = UNIAP_MAX_LAYERS;
 constexpr int TMAX = 2176;   // >= L(L+1)/2 + L - 1 theta candidates for L <= 64
 constexpr int SORTN = 4096;  // bitonic size (power of two >= TMAX)
+constexpr int MAXLEV = UNIAP_MAX_LEVELS;  // distinct per-stage caps of a config (NEXT-2)
 
 struct CfgDev {
   int32_t deg, c, S, NSP, g, skip;        // skip: skip source of this config's tables (-1 none)
@@ -35,8 +36,13 @@ struct CfgDev {
   // feasible; orig[k] is the catalogue / caller index of
   // table strategy k, comp[j] the table index of catalogue strategy j (-1:
   // dropped), Sfull the catalogue size (the canonical work counts use it).
-  int32_t Sfull, pad_;
+  int32_t Sfull, nlev;
   int8_t orig[UNIAP_MAX_STRAT], comp[UNIAP_MAX_STRAT];
+  // Per-stage memory caps (NEXT-2): the config's distinct caps
+  // lcap[0..nlev), stage i uses level lev_of[i]; the P block of the config
+  // holds one L*L table per level (P_lev[a][b] = optimum of [a,b] under lcap).
+  int32_t lcap[MAXLEV];
+  int8_t lev_of[MAXL];
 };
 
 // One chain sweep of K2.
@@ -57,6 +63,8 @@ struct Inst {
   // (intervals ending at a: the suffix sweep of the last stage)
   int32_t elo, ehi;
   int32_t n0;    // the planned length (the layers a placement can use)
+  int32_t lev;   // the config's cap level this sweep emits (P block lev, column ecap)
+  int32_t ecap;  // = lcap[lev]: the bucket whose state min_k D[k][ecap] is the stage optimum
 };
 
 struct K2Args {

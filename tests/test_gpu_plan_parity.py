@@ -29,41 +29,62 @@ def h():
     hd.close()
 
 
-def covered(L, deg):
-    """Intervals [a, b] a deg-stage ordered placement can use (SURVEY.md 8a,
-    the solver's sweep plan): stage 1 a prefix, the last stage a suffix,
-    middle stages inside."""
+def stage_intervals(L, deg, i):
+    """Intervals [a, b] stage i (0-based) of a deg-stage ordered placement can
+    be: i layers before it, deg-1-i after it."""
     m = np.zeros((L, L), dtype=bool)
     if deg > L:
         return m
-    if deg == 1:
-        m[0, L - 1] = True
-        return m
-    m[0, :L - deg + 1] = True                       # prefixes [0, b], b <= L - deg
-    m[deg - 1:, L - 1] = True                       # suffixes [a, L-1], a >= deg - 1
-    for a in range(1, L - 1) if deg >= 3 else ():   # middle stages i = 2..deg-1
-        bmax = L - 1 - deg + min(a + 1, deg - 1)
-        m[a, a:bmax + 1] = True
+    for a in range(i, L):
+        for b in range(a, L - (deg - 1 - i)):
+            if (i == 0 and a != 0) or (i == deg - 1 and b != L - 1):
+                continue
+            m[a, b] = True
     return m
 
 
+def levels(t, cfg):
+    """The config's distinct stage caps in order of first appearance (the
+    library's cap levels) and each stage's level."""
+    caps = [t["cap"]] * cfg["deg"] if cfg.get("stage_cap") is None else [int(x) for x in cfg["stage_cap"]]
+    lcap = []
+    for c in caps:
+        if c not in lcap:
+            lcap.append(c)
+    return lcap, [lcap.index(c) for c in caps]
+
+
 def check(h, orc, t, P, what):
+    """P: the flat fetch_intervals array (per config, one L*L block per cap level)."""
     import concurrent.futures as cf
     L = t["L"]
-    with cf.ThreadPoolExecutor() as ex:  # ctypes releases the GIL: one oracle call per config in parallel
-        tabs = list(ex.map(lambda i: orc.interval_table(t, i), range(len(t["cfgs"]))))
+    jobs, off = [], 0
     for i, cfg in enumerate(t["cfgs"]):
-        want = np.where(tabs[i] == BIG, INF, tabs[i])
-        m = covered(L, cfg["deg"])
-        got = P[i].astype(np.int64)
+        lcap, lev_of = levels(t, cfg)
+        for lv, cap in enumerate(lcap):
+            jobs.append((i, lv, cap, off))
+            off += L * L
+    assert off == P.size, (what, off, P.size)
+    plain = dict(t, cfgs=[{k: v for k, v in c.items() if k != "stage_cap"} for c in t["cfgs"]])
+    with cf.ThreadPoolExecutor() as ex:  # ctypes releases the GIL: one oracle call per table in parallel
+        tabs = list(ex.map(lambda j: orc.interval_table(dict(plain, cap=j[2]), j[0]), jobs))
+    for (i, lv, cap, o), want in zip(jobs, tabs):
+        cfg = t["cfgs"][i]
+        want = np.where(want == BIG, INF, want)
+        _, lev_of = levels(t, cfg)
+        m = np.zeros((L, L), dtype=bool)
+        for st, l in enumerate(lev_of if cfg["deg"] <= L else []):
+            if l == lv:
+                m |= stage_intervals(L, cfg["deg"], st)
+        got = P[o:o + L * L].reshape(L, L).astype(np.int64)
         bad = np.argwhere(m & (got != want))
-        assert bad.size == 0, (what, i, cfg["deg"], cfg["c"], bad[:5].tolist(),
+        assert bad.size == 0, (what, i, lv, cfg["deg"], cfg["c"], bad[:5].tolist(),
                                [(int(got[a, b]), int(want[a, b])) for a, b in bad[:5]])
         # entries no placement needs may still be computed by a sweep (e.g. a
         # deg = 1 chain with the skip source inside runs as a forward sweep
         # and emits every prefix): each is either untouched or exact
-        off = ~m & (got != INF)
-        assert np.array_equal(got[off], want[off]), (what, i, "an extra entry is wrong")
+        extra = ~m & (got != INF)
+        assert np.array_equal(got[extra], want[extra]), (what, i, lv, "an extra entry is wrong")
 
 
 @pytest.mark.parametrize("name", ["bert", "t5", "vit", "swin", "llama"])
@@ -71,9 +92,9 @@ def test_production_plan_intervals_full_size(h, orc, name):
     p = profiles.make_profile(name)
     t, qn, _ = orc.build_tables(p)
     h.plan(p)                                   # level 2: K1 + the production solve
-    check(h, orc, t, h.fetch_intervals(t["L"]), name + " plan")
+    check(h, orc, t, h.fetch_intervals(), name + " plan")
     h.solve_tables(t)                           # level 1: the same tables
-    check(h, orc, t, h.fetch_intervals(t["L"]), name + " tables")
+    check(h, orc, t, h.fetch_intervals(), name + " tables")
 
 
 def test_production_plan_intervals_random_skip_tables(h, orc):
@@ -89,8 +110,7 @@ def test_production_plan_intervals_random_skip_tables(h, orc):
         t = tables.large_random_tables(40_000 + seed, L, S, Q - 1, cands, skip_src=skip,
                                        mem_max=max(1, (4 * Q) // L))
         h.solve_tables(t)
-        check(h, orc, t, h.fetch_intervals(L), ("random", seed, L, Q, skip))
-        _ = orc.solve_tables(t)
+        check(h, orc, t, h.fetch_intervals(), ("random", seed, L, Q, skip))
 
 
 def test_level2_swin50_llama_envc_llama13b(h, orc):
@@ -104,4 +124,59 @@ def test_level2_swin50_llama_envc_llama13b(h, orc):
         if want["objective"] != BIG:
             for k in ("stage_of", "strategy_of", "stage_cost", "cut_cost", "stage_mem"):
                 assert got[k] == want[k], (name, k)
-        check(h, orc, t, h.fetch_intervals(t["L"]), name)
+        check(h, orc, t, h.fetch_intervals(), name)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: per-stage memory limits (heterogeneous devices)
+# ---------------------------------------------------------------------------
+
+KEYS = ("objective", "cfg_index", "deg", "c", "cfg_objective")
+ASSIGN = ("stage_of", "strategy_of", "stage_cost", "cut_cost", "stage_mem")
+
+
+def _same(g, o, what=""):
+    for k in KEYS:
+        assert g[k] == o[k], (what, k, g[k], o[k])
+    if o["objective"] != BIG:
+        for k in ASSIGN:
+            assert g[k] == o[k], (what, k, g[k], o[k])
+
+
+def test_stage_caps_tiny_brute_checked(h, orc):
+    """The brute-force-pinned tiny instances with per-stage caps, GPU = oracle."""
+    for seed in range(1500):
+        t = tables.random_tables(700_000 + seed, stage_caps=True)
+        _same(h.solve_tables(t), orc.solve_tables(t), seed)
+
+
+def test_stage_caps_large_tables_and_intervals(h, orc):
+    rng = np.random.default_rng(77)
+    for seed in range(16):
+        L = int(rng.integers(4, 20))
+        Q = int(rng.choice([64, 300, 1025, 4096]))
+        cands = sorted({(int(d), int(c)) for d, c in zip(rng.integers(1, 9, 4), rng.integers(1, 5, 4))})
+        S = [int(rng.choice([1, 3, 6, 10, 15])) for _ in cands]
+        skip = int(rng.integers(-1, L - 2))
+        t = tables.large_random_tables(60_000 + seed, L, S, Q - 1, cands, skip_src=skip,
+                                       mem_max=max(1, (3 * Q) // L), stage_caps=True)
+        _same(h.solve_tables(t), orc.solve_tables(t, n_threads=0), ("large", seed))
+        check(h, orc, t, h.fetch_intervals(), ("large", seed))
+
+
+@pytest.mark.parametrize("name", ["llama", "t5"])
+def test_heterogeneous_device_memory_profiles(h, orc, name):
+    """Level 2 with per-device memory: half of the devices with 60 % of the
+    memory (alternating blocks of 4), K1 tables incl. stage caps bit-equal,
+    plan = oracle plan, interval tables element by element."""
+    p = profiles.make_profile(name)
+    cl = p["cluster"]
+    n = cl["n_dev"]
+    small = cl["mem_reserve_bytes"] + (cl["mem_bytes"] - cl["mem_reserve_bytes"]) * 6 // 10
+    cl["dev_mem_bytes"] = [small if (d // 4) % 2 else cl["mem_bytes"] for d in range(n)]
+    t, qn, buf = orc.build_tables(p)
+    gt, gq, gbuf = h.build_tables(p)
+    assert gq == qn and np.array_equal(gbuf, buf)
+    want = orc.solve_tables(t, n_threads=0)
+    _same(h.plan(p), want, name)
+    check(h, orc, t, h.fetch_intervals(), name + " hetero")
