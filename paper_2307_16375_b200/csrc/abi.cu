@@ -86,6 +86,7 @@ struct K2Group {
   double crit;
   int max_inst;  // device-sized launches (backward): grid bound
   int priority = 0;  // launch priority (cluster classes and long critical paths first)
+  int ecap = -1;     // emission bucket of every sweep of the launch (K2Args::ecap; -1: the cap)
 };
 
 struct RunPlan {
@@ -941,9 +942,15 @@ extern "C" uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32
 
 static int class_key(const K2Class& k) { return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C + (k.DB ? 0 : 50000); }
 
+// launches group sweeps by kernel class and emission bucket (per-stage caps:
+// a launch emits one cap level's column, a kernel parameter)
+static int64_t group_key(const uniap_handle* h, const Inst& x) {
+  return (int64_t)class_key(h->cls[x.cfg]) * 16384 + x.ecap;
+}
+
 static void group_instances(const uniap_handle* h, std::vector<Inst>& all, std::vector<K2Group>& grp) {
-  std::vector<int> key(all.size());
-  for (size_t j = 0; j < all.size(); ++j) key[j] = class_key(h->cls[all[j].cfg]);
+  std::vector<int64_t> key(all.size());
+  for (size_t j = 0; j < all.size(); ++j) key[j] = group_key(h, all[j]);
   std::vector<size_t> idx(all.size());
   std::iota(idx.begin(), idx.end(), 0);
   std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
@@ -955,16 +962,16 @@ static void group_instances(const uniap_handle* h, std::vector<Inst>& all, std::
   grp.clear();
   for (size_t s = 0; s < sorted.size();) {
     size_t e = s;
-    const int id = class_key(h->cls[sorted[s].cfg]);
+    const int64_t id = group_key(h, sorted[s]);
     double c = 0;
-    while (e < sorted.size() && class_key(h->cls[sorted[e].cfg]) == id) {
+    while (e < sorted.size() && group_key(h, sorted[e]) == id) {
       const K2Class& k = h->cls[sorted[e].cfg];
       const double step = (double)k.NS * k.NS * k.T * k.V / (64.0 * std::min(1.0, k.T / 512.0)) + 3000.0 +
                           (k.C > 1 ? 3000.0 : 0.0);
       c = std::max(c, (double)sorted[e].n * step);
       ++e;
     }
-    grp.push_back(K2Group{s, e, h->cls[sorted[s].cfg], c, 0});
+    grp.push_back(K2Group{s, e, h->cls[sorted[s].cfg], c, 0, 0, sorted[s].ecap});
     s = e;
   }
   std::stable_sort(grp.begin(), grp.end(), [](const K2Group& a, const K2Group& b) { return a.crit > b.crit; });
@@ -1019,7 +1026,8 @@ static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp,
     const int n = dcount_per_class ? grp[g].max_inst : (int)(grp[g].e - grp[g].s);
     K2Args args{dcount_per_class ? dinst : dinst + grp[g].s,
                 dcount_per_class ? dcount_per_class + g : nullptr,
-                h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip};
+                h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip,
+                grp[g].ecap >= 0 ? grp[g].ecap : h->cap};
     if (!dcount_per_class) args.tim = h->tim.p;  // forward launches: phase clock
     if (h->trace.p) {  // diagnostics: tag = class shape | forward/backward | group
       const K2Class& k = grp[g].cls;
@@ -1089,19 +1097,22 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
     for (auto& x : cv) h->cells_canon += (uint64_t)x.n * h->cfg[i].Sfull * h->Q;
   }
   group_instances(h, fw, R.fgrp);
-  // local configs ordered by forward group, so each group's K4 takes a range
+  // local configs ordered by forward group, so each group's K4 takes a range;
+  // a config whose sweeps span several groups (several cap levels) runs its
+  // K4 after the join (k4rest)
   {
-    std::vector<int32_t> ordered;
+    std::vector<int32_t> ordered, grp_of(h->ncfg, -1);
     std::vector<char> used(h->ncfg, 0);
+    for (size_t g = 0; g < R.fgrp.size(); ++g)
+      for (size_t j = R.fgrp[g].s; j < R.fgrp[g].e; ++j) {
+        int32_t& x = grp_of[fw[j].cfg];
+        x = (x == -1 || x == (int32_t)g) ? (int32_t)g : -2;
+      }
     R.k4range.assign(R.fgrp.size(), {0, 0});
     for (size_t g = 0; g < R.fgrp.size(); ++g) {
       const int start = (int)ordered.size();
       for (int i : R.local)
-        if (!used[i] && class_key(h->cls[i]) == class_key(R.fgrp[g].cls)) {
-          bool has = false;
-          for (size_t j = R.fgrp[g].s; j < R.fgrp[g].e && !has; ++j) has = fw[j].cfg == i;
-          if (has) { ordered.push_back(i); used[i] = 1; }
-        }
+        if (!used[i] && grp_of[i] == (int32_t)g) { ordered.push_back(i); used[i] = 1; }
       R.k4range[g] = {start, (int)ordered.size() - start};
     }
     const int rest0 = (int)ordered.size();

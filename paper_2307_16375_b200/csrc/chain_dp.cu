@@ -22,7 +22,7 @@ int k2_ns_round(int S) {
 
 static size_t smem_words(int NS, int B, int ne = 2) {
   const int NSP = (NS + 3) & ~3;
-  return (size_t)ne * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP) + MAXL + 4;  // + the emission words
+  return (size_t)ne * NS * (B + 4) + 3 * (NS * NSP + 2 * NSP) + MAXL;
 }
 
 size_t k2_smem_bytes(const K2Class& c) { return smem_words(c.NS, c.T * c.V, c.DB ? 2 : 1) * sizeof(int32_t); }
@@ -157,7 +157,7 @@ __global__ void k2_closed_s1(const K2Args args, int n_inst) {
       if (v > lo) cost += Rf[(int64_t)(v - 1) * NSP * NSP];
       mem += M[(int64_t)v * NSP];
     }
-    const int32_t val = mem <= in.ecap ? (int32_t)min(cost, (int64_t)INF) : INF;
+    const int32_t val = mem <= args.ecap ? (int32_t)min(cost, (int64_t)INF) : INF;
     int32_t* dst = in.dir > 0 ? Pc + (int64_t)in.a * L + uu : Pc + (int64_t)uu * L + in.a;
     if ((in.emit & 3) == 2) atomicMin(dst, val);
     else *dst = val;

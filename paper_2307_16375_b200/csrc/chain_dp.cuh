@@ -128,9 +128,6 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   int32_t* sE = reinterpret_cast<int32_t*>(smem4);  // [2][NS][ROW]
   int32_t* sT = sE + NE * NS * ROW;                 // [3][SW] staged tables
   int32_t* sProw = sT + 3 * SW;                     // [MAXL] this instance's P[a][.]
-  // the sweep's emission bucket (its cap level's cap) and P block, kept in
-  // shared memory and re-read where used: no register across the main loop
-  volatile int32_t* sEm = sProw + MAXL;             // [0] ecap, [1] lev
   const int t = threadIdx.x;
   int rank = 0, ii = blockIdx.x;
   if constexpr (CL) {
@@ -150,7 +147,6 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   const int L = args.L;
 
   for (int r = t; r < NE * NS; r += T) *reinterpret_cast<int4*>(sE + r * ROW) = make_int4(INF, INF, INF, INF);
-  if (t == 0) { sEm[0] = in.ecap; sEm[1] = in.lev; }  // (visible after the first barrier)
 
   // ---- tables of one layer step, staged by the whole CTA ----------------
   // word w of a stage: R rows (w < NS*NSP), then (A', M) pairs.  A' adds the
@@ -211,11 +207,10 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   int32_t d[NS][V];
   const bool eP = (in.emit & 3) != 0, eG = in.emit == 0 || (in.emit & 4) != 0;  // Inst::emit
   auto emit = [&](int u) {
-    if (eP) {  // the stage optimum under the sweep's cap level: min_k D[k][ecap]
-      const int ecap = sEm[0];
-      const int rc = ecap / B;
+    if (eP) {  // the stage optimum under the launch's cap level: min_k D[k][ecap] (a kernel parameter)
+      const int rc = args.ecap / B;
       if (rank == rc) {
-        const int lc = ecap - rc * B, jc = lc / T, tc = lc - jc * T;
+        const int lc = args.ecap - rc * B, jc = lc / T, tc = lc - jc * T;
         if (t == tc) {
           int32_t v = INF;
 #pragma unroll
@@ -381,8 +376,8 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
     emit(u);
   }
   // the forward sweep's stage optima P[a][a..a+n-1], from its owner thread
-  if (eP && rank == sEm[0] / B && t == (sEm[0] - (sEm[0] / B) * B) % T) {
-    int32_t* Pc = args.P + cf.offP + (int64_t)sEm[1] * L * L;
+  if (eP && rank == args.ecap / B && t == (args.ecap - (args.ecap / B) * B) % T) {
+    int32_t* Pc = args.P + cf.offP + (int64_t)args.inst[ii].lev * L * L;  // (read here: not live in the loop)
     for (int uu = in.elo; uu <= in.ehi; ++uu) {  // (the trim keeps [elo, ehi] inside the layers swept)
       int32_t* dst = in.dir > 0 ? Pc + (int64_t)in.a * L + uu : Pc + (int64_t)uu * L + in.a;
       if ((in.emit & 3) == 2) atomicMin(dst, sProw[uu]);
@@ -399,7 +394,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
 
 template <int NS>
 constexpr size_t k2_smem(int B, int ne = 2) {
-  return (size_t)(ne * NS * (B + 4) + 3 * Stage<NS>::WORDS + MAXL + 4) * sizeof(int32_t);
+  return (size_t)(ne * NS * (B + 4) + 3 * Stage<NS>::WORDS + MAXL) * sizeof(int32_t);
 }
 
 // Instantiation helper used by the per-NS translation units: only the shapes

@@ -75,6 +75,7 @@ struct K2Args {
   int32_t* P;
   int32_t* G;
   int32_t L, cap, skip;
+  int32_t ecap;  // emission bucket of this launch's sweeps (their cap level's cap; Inst::ecap)
   // diagnostics (UNIAP_TRACE): per-CTA timeline records, or nullptr
   unsigned long long* trace = nullptr;
   uint32_t tag = 0;
