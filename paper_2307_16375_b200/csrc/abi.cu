@@ -117,7 +117,7 @@ struct uniap_handle {
   ClusterDev cl{};
   int n_edges = 0;
   // device buffers
-  DevBuf<int32_t> arena, P, thetas, ntheta, cfglist, scratch, G, ends;
+  DevBuf<int32_t> arena, P, thetas, ntheta, cfglist, scratch, G;
   DevBuf<int64_t> ns, vals, cfgopt, qcfg, qglob, gofs, qmax, gstore;
   // the level-2 profile, config and catalogue arrays: views into ONE device
   // blob filled by one DMA per prepare
@@ -365,7 +365,7 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->st);
-  for (auto* b : {&h->arena, &h->P, &h->thetas, &h->ntheta, &h->cfglist, &h->scratch, &h->G, &h->ends}) b->release();
+  for (auto* b : {&h->arena, &h->P, &h->thetas, &h->ntheta, &h->cfglist, &h->scratch, &h->G}) b->release();
   for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->qglob, &h->gofs, &h->qmax, &h->gstore}) b->release();
   h->upb.release();
   h->dcfg1.release();
@@ -1176,12 +1176,7 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   CK(h, h->ntheta.ensure(std::max(nl, 1)));
   CK(h, h->vals.ensure((size_t)std::max(nl, 1) * (TMAX + 2)));
   CK(h, h->cfgopt.ensure(h->ncfg));
-  {  // K4's stage-end search with many tied thetas: one slot per SM (k4_vals)
-    int nsm = 0;
-    CK(h, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
-    CK(h, h->scratch.ensure((size_t)nsm * 32 * (MAXL + 1) * (MAXL + 1)));
-  }
-  CK(h, h->ends.ensure((size_t)std::max(nl, 1) * (MAXL + 1)));
+  CK(h, h->scratch.ensure((size_t)32 * (MAXL + 1) * (MAXL + 1)));
   CK(h, h->win.ensure(1));
   CK(h, h->bwp.ensure(1));
   if (!fw.empty()) CK(h, h2d(h, h->inst.p, fw.data(), fw.size() * sizeof(Inst)));
@@ -1212,7 +1207,7 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
 static uniap_status enqueue_k4_range(uniap_handle* h, int li0, int cnt, cudaStream_t st) {
   if (cnt <= 0) return UNIAP_OK;
   CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, li0, cnt, h->L, h->thetas.p, h->ntheta.p, h->vals.p,
-                  h->cfgopt.p, h->ends.p, h->scratch.p, st));
+                  h->cfgopt.p, st));
   h->launches++;
   return UNIAP_OK;
 }
@@ -1258,7 +1253,8 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
 
   RecordArgs ra{rec, h->cells, h->relax, h->level2 ? h->work.p : nullptr, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
                 h->binst.p, h->bwp.p, h->gstore.p};
-  CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->cfgopt.p, h->ends.p, h->win.p, ra, h->st));
+  CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
+                   h->cfgopt.p, h->scratch.p, h->win.p, ra, h->st));
   h->launches += 1;
   // traceback: backward sweeps sized on the device, then the strategy walk
   {

@@ -263,20 +263,19 @@ struct K4Smem {
   int32_t sO[MAXL];
   int32_t g[K4W][128];
   int32_t probeF[K4W];
-  int32_t cnt, s_hi, nstar;
+  int32_t cnt, s_hi;
   unsigned long long s_best;
-  int64_t opt;                          // the config's optimum (INT64_MAX: infeasible)
-  int32_t H[(MAXL + 1) * (MAXL + 1)];   // suffix table of the stage-end search (few theta*)
-  int32_t wends[K4W][MAXL];             // per-warp end vectors (many theta*)
-  int32_t okw[K4W];
   typename K3Scan::TempStorage scan_tmp;
 };
 
-// K4 part 1: Val(theta) and the config optimum S.opt (every return is CTA-uniform).
-__device__ void k4_values(K4Smem& S, TraceScope& tr, const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
-                          const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list, int li0, int L,
-                          int32_t* __restrict__ thetas, int32_t* __restrict__ ntheta, int64_t* __restrict__ vals,
-                          int64_t* __restrict__ cfg_opt) {
+__global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
+                                                   const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
+                                                   int li0, int L, int32_t* __restrict__ thetas,
+                                                   int32_t* __restrict__ ntheta, int64_t* __restrict__ vals,
+                                                   int64_t* __restrict__ cfg_opt) {
+  TraceScope tr(TR_K4 | (uint32_t)li0 << 8);
+  extern __shared__ __align__(16) unsigned char k4raw[];
+  K4Smem& S = *reinterpret_cast<K4Smem*>(k4raw);
   int32_t* sP = S.sP;
   int32_t* sO = S.sO;
   int32_t* probeF = S.probeF;
@@ -296,7 +295,6 @@ __device__ void k4_values(K4Smem& S, TraceScope& tr, const CfgDev* __restrict__ 
   int64_t* V = vals + (int64_t)li * (TMAX + 2);  // [0..nt) Val, [TMAX] F_inf, [TMAX+1] opt
   const int32_t* th = S.v;
   for (int i = threadIdx.x; i < nt; i += blockDim.x) V[i] = INT64_MAX;
-  if (threadIdx.x == 0) S.opt = INT64_MAX;
   if (cf.deg > L || nt == 0) {  // Eq. 7b cannot hold (reading A-22)
     if (threadIdx.x == 0) { V[TMAX] = INT64_MAX; cfg_opt[cfg_list[li]] = INT64_MAX; }
     return;
@@ -320,7 +318,7 @@ __device__ void k4_values(K4Smem& S, TraceScope& tr, const CfgDev* __restrict__ 
           best = min(best, val);
         }
       V[TMAX] = Finf >= INF ? INT64_MAX : (int64_t)Finf;
-      cfg_opt[cfg_list[li]] = S.opt = Finf >= INF ? INT64_MAX : best;
+      cfg_opt[cfg_list[li]] = Finf >= INF ? INT64_MAX : best;
       tr.extra = (uint32_t)nt | (uint32_t)nt << 12;
     }
     return;
@@ -338,7 +336,7 @@ __device__ void k4_values(K4Smem& S, TraceScope& tr, const CfgDev* __restrict__ 
   if (Finf >= INF || cf.c == 1) {
     if (threadIdx.x == 0) {
       V[TMAX] = Finf >= INF ? INT64_MAX : (int64_t)Finf;
-      cfg_opt[cfg_list[li]] = S.opt = V[TMAX];
+      cfg_opt[cfg_list[li]] = V[TMAX];
     }
     return;
   }
@@ -384,242 +382,46 @@ __device__ void k4_values(K4Smem& S, TraceScope& tr, const CfgDev* __restrict__ 
   __syncthreads();
   if (threadIdx.x == 0) {
     V[TMAX] = Finf;
-    cfg_opt[cfg_list[li]] = S.opt = (int64_t)s_best;
+    cfg_opt[cfg_list[li]] = (int64_t)s_best;
     tr.extra = (uint32_t)S.cnt | (uint32_t)nt << 12 | (uint32_t)(nt - imin) << 24;
   }
 }
 
-// K4 part 2: the lexicographically largest stage-end vector over the optimal
-// placements of this config (= lexicographically smallest stage_of, reading
-// A-11), written to ends_out = [status, e_1 .. e_deg] (status 1 found, 0 the
-// config is infeasible, -1 none found: a bug).  Theta* = every theta with
-// Val(theta) = OPT (c > 1) or the unconstrained one (c = 1); per theta a
-// suffix DP H_i[a] = min_b P_i[a][b] + O[b] + H_{i+1}[b+1] (cover [a, L-1]
-// with stages i..deg, every P and O <= theta), then the largest feasible end
-// of each stage in turn.  Few theta* (the usual case): the whole CTA per
-// theta, H in shared memory; many: one warp per theta, H in global scratch.
-// Runs per config right after its Val(theta), so only the last config's
-// search is on the step's critical path (the global argmin, K5a, only reads
-// the winner's vector).
-__device__ void k4_ends(K4Smem& S, const int32_t* __restrict__ O, int L, int deg, int c, int nt,
-                        const int64_t* __restrict__ V, int32_t* __restrict__ ends_out, int32_t* __restrict__ gH) {
-  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  const int64_t OPT = S.opt;
-  if (OPT == INT64_MAX) {
-    if (t == 0) ends_out[0] = 0;
-    return;
-  }
-  const int32_t* sO = S.sO;
-  const int32_t* th = S.v;
-  int32_t* stars = &S.g[0][0];  // (the DP scratch of part 1 is free now)
-  if (t == 0) S.nstar = 0;
-  __syncthreads();
-  if (c == 1) {
-    if (t == 0) { stars[0] = -1; S.nstar = 1; }
-  } else {
-    for (int i = t; i < nt; i += blockDim.x)
-      if (V[i] == OPT) stars[atomicAdd(&S.nstar, 1)] = i;
-  }
-  __syncthreads();
-  const int ns = S.nstar;
-  // stage i (1-based) reads the interval table of its cap level
-  auto Pt = [&](int i) { return S.sP + S.slev[i - 1] * L * L; };
-  int32_t best_end[MAXL];
-  bool have = false;
-  constexpr int HP = MAXL + 1;
-  int32_t* sH = S.H;
-  for (int si = 0; si < ns && ns <= 4; ++si) {
-    const int32_t theta = stars[si] < 0 ? INF : th[stars[si]];
-    const int64_t F_target = stars[si] < 0 ? OPT : OPT - (int64_t)(c - 1) * theta;
-    for (int a = t; a <= L; a += blockDim.x) {
-      int32_t v = INF;
-      if (a < L) { const int32_t p = Pt(deg)[a * L + L - 1]; v = p <= theta ? p : INF; }
-      sH[deg * HP + a] = v;
-    }
-    __syncthreads();
-    for (int i = deg - 1; i >= 1; --i) {
-      const int bhi = L - 1 - (deg - i);
-      const int32_t* sP = Pt(i);
-      for (int a = w; a <= L; a += K4W) {
-        uint32_t v = INF;
-        for (int b = a + lane; b <= bhi && a < L; b += 32) {
-          const int32_t p = sP[a * L + b], o = sO[b], hh = sH[(i + 1) * HP + b + 1];
-          if (p <= theta && o <= theta && hh < INF) v = min(v, (uint32_t)p + (uint32_t)o + (uint32_t)hh);
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, off));
-        if (lane == 0) sH[i * HP + a] = (int32_t)min(v, (uint32_t)INF);
-      }
-      __syncthreads();
-    }
-    bool ok = (int64_t)sH[1 * HP + 0] == F_target;
-    if (w == 0) {  // greedy: the largest feasible end of each stage
-      int64_t pre = 0;
-      int a = 0;
-      for (int i = 1; i < deg && ok; ++i) {
-        const int32_t* sP = Pt(i);
-        int found = -1;
-        for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
-          const int b = b0 - lane;
-          bool cc = false;
-          if (b >= a) {
-            const int32_t p = sP[a * L + b], o = sO[b], hh = sH[(i + 1) * HP + b + 1];
-            cc = p <= theta && o <= theta && hh < INF && pre + p + o + hh == F_target;
-          }
-          const unsigned m = __ballot_sync(0xffffffffu, cc);
-          if (m) found = b0 - (__ffs(m) - 1);
-        }
-        if (found < 0) { ok = false; break; }
-        if (lane == 0) S.wends[0][i - 1] = found;
-        pre += sP[a * L + found] + sO[found];
-        a = found + 1;
-      }
-      if (lane == 0) {
-        S.wends[0][deg - 1] = L - 1;
-        S.okw[0] = ok;
-      }
-    }
-    __syncthreads();
-    if (t == 0 && S.okw[0]) {  // lexicographically largest end vector over theta*
-      bool better = !have;
-      for (int i = 0; i < deg && !better; ++i)
-        if (S.wends[0][i] != best_end[i]) { better = S.wends[0][i] > best_end[i]; break; }
-      if (better) {
-        for (int i = 0; i < deg; ++i) best_end[i] = S.wends[0][i];
-        have = true;
-      }
-    }
-    __syncthreads();
-  }
-  for (int base = 0; base < ns && ns > 4; base += K4W) {
-    const int si = base + w;
-    bool ok = false;
-    int32_t* H = gH + (int64_t)w * HP * HP;
-    if (si < ns) {
-      const int32_t theta = stars[si] < 0 ? INF : th[stars[si]];
-      const int64_t F_target = stars[si] < 0 ? OPT : OPT - (int64_t)(c - 1) * theta;
-      for (int a = lane; a <= L; a += 32) {
-        int32_t v = INF;
-        if (a < L) { const int32_t p = Pt(deg)[a * L + L - 1]; v = p <= theta ? p : INF; }
-        H[deg * HP + a] = v;
-      }
-      __syncwarp();
-      for (int i = deg - 1; i >= 1; --i) {
-        const int bhi = L - 1 - (deg - i);
-        const int32_t* Hn = H + (i + 1) * HP;
-        const int32_t* sP = Pt(i);
-        for (int a = lane; a <= L; a += 32) {
-          uint32_t x = INF;
-          for (int b = a; b <= bhi && a < L; ++b) {
-            const int32_t p0 = sP[a * L + b], o0 = sO[b], h0 = Hn[b + 1];
-            const uint32_t w0 = (o0 <= theta && h0 < INF) ? (uint32_t)(o0 + h0) : INF;
-            x = __viaddmin_u32(w0, p0 <= theta ? (uint32_t)p0 : INF, x);
-          }
-          H[i * HP + a] = (int32_t)min(x, (uint32_t)INF);
-        }
-        __syncwarp();
-      }
-      ok = (int64_t)H[1 * HP + 0] == F_target;
-      int64_t pre = 0;
-      int a = 0;
-      for (int i = 1; i < deg && ok; ++i) {
-        const int32_t* sP = Pt(i);
-        int found = -1;
-        for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
-          const int b = b0 - lane;
-          bool cc = false;
-          if (b >= a) {
-            const int32_t p = sP[a * L + b], o = sO[b], hh = H[(i + 1) * HP + b + 1];
-            cc = p <= theta && o <= theta && hh < INF && pre + p + o + hh == F_target;
-          }
-          const unsigned m = __ballot_sync(0xffffffffu, cc);
-          if (m) found = b0 - (__ffs(m) - 1);
-        }
-        if (found < 0) { ok = false; break; }
-        if (lane == 0) S.wends[w][i - 1] = found;
-        pre += sP[a * L + found] + sO[found];
-        a = found + 1;
-      }
-      if (lane == 0) S.wends[w][deg - 1] = L - 1;
-      __syncwarp();
-    }
-    if (lane == 0) S.okw[w] = ok;
-    __syncthreads();
-    if (t == 0)  // lexicographically largest end vector (theta order is deterministic)
-      for (int j = 0; j < K4W && base + j < ns; ++j) {
-        if (!S.okw[j]) continue;
-        bool better = !have;
-        for (int i = 0; i < deg && !better; ++i)
-          if (S.wends[j][i] != best_end[i]) { better = S.wends[j][i] > best_end[i]; break; }
-        if (better) {
-          for (int i = 0; i < deg; ++i) best_end[i] = S.wends[j][i];
-          have = true;
-        }
-      }
-    __syncthreads();
-  }
-  if (t == 0) {
-    ends_out[0] = have ? 1 : -1;
-    for (int i = 0; i < deg && have; ++i) ends_out[1 + i] = best_end[i];
-  }
-  (void)O;
-}
-
-__global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
-                                                   const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
-                                                   int li0, int L, int32_t* __restrict__ thetas,
-                                                   int32_t* __restrict__ ntheta, int64_t* __restrict__ vals,
-                                                   int64_t* __restrict__ cfg_opt, int32_t* __restrict__ cfg_ends,
-                                                   int32_t* __restrict__ scratch) {
-  TraceScope tr(TR_K4 | (uint32_t)li0 << 8);
-  extern __shared__ __align__(16) unsigned char k4raw[];
-  K4Smem& S = *reinterpret_cast<K4Smem*>(k4raw);
-  const int li = li0 + blockIdx.x;
-  k4_values(S, tr, cfgs, arena, P, cfg_list, li0, L, thetas, ntheta, vals, cfg_opt);
-  __syncthreads();
-  const CfgDev* cfp = cfgs + cfg_list[li];
-  const int deg = cfp->deg;
-  if (deg > L) {
-    if (threadIdx.x == 0) cfg_ends[(int64_t)li * (MAXL + 1)] = 0;
-    return;
-  }
-  // many tied thetas: per-warp suffix tables in global scratch, one slot per
-  // SM -- K4's shared memory admits one K4 CTA per SM (static_assert below),
-  // so no two CTAs use a slot at once
-  uint32_t sm;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-  k4_ends(S, arena + cfp->offO, L, deg, cfp->c, ntheta[li], vals + (int64_t)li * (TMAX + 2),
-          cfg_ends + (int64_t)li * (MAXL + 1), scratch + (int64_t)sm * K4W * (MAXL + 1) * (MAXL + 1));
-}
-static_assert(sizeof(K4Smem) > 114 * 1024, "one K4 CTA per SM (the scratch slot is the SM id)");
-
 cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int li0,
                       int n_local, int L, int32_t* thetas, int32_t* ntheta, int64_t* vals, int64_t* cfg_opt,
-                      int32_t* cfg_ends, int32_t* scratch, cudaStream_t st) {
+                      cudaStream_t st) {
   if (n_local <= 0) return cudaSuccess;
-  k4_vals<<<n_local, K4W * 32, sizeof(K4Smem), st>>>(cfg, arena, P, cfg_list, li0, L, thetas, ntheta, vals, cfg_opt,
-                                                      cfg_ends, scratch);
+  k4_vals<<<n_local, K4W * 32, sizeof(K4Smem), st>>>(cfg, arena, P, cfg_list, li0, L, thetas, ntheta, vals, cfg_opt);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
-// K5a: global (objective, deg, c) argmin over the local configs, the
-// winner's stage ends (found per config by K4, k4_ends), its stage and cut
-// costs, the record header and the device-side plan of the traceback's
-// backward sweeps.  One CTA; only small reads.
+// K5a: per-config optimum, global (objective, deg, c) argmin, and the
+// lexicographically largest stage-end vector over the optimal placements
+// (= lexicographically smallest stage_of, reading A-11).  One CTA.
 // ---------------------------------------------------------------------------
-constexpr int K5T = 256;
+constexpr int K5T = 1024;
+constexpr int K5PP = MAXL + 1;  // odd pitch of K5a's interval tables
+// K5a's dynamic shared memory: the suffix table H, then the winner's interval
+// tables (one per cap level)
+constexpr int K5A_DYN = (MAXL + 1) * (MAXL + 1) * 4 + MAXLEV * MAXL * K5PP * 4;
 __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
                                                   const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
-                                                  int n_local, int L, const int64_t* __restrict__ cfg_opt,
-                                                  const int32_t* __restrict__ cfg_ends, Winner* __restrict__ win,
-                                                  RecordArgs ra) {
+                                                  int n_local, int L, const int32_t* __restrict__ thetas,
+                                                  const int32_t* __restrict__ ntheta, const int64_t* __restrict__ vals,
+                                                  const int64_t* __restrict__ cfg_opt, int32_t* __restrict__ scratch,
+                                                  Winner* __restrict__ win, RecordArgs ra) {
   TraceScope tr(TR_K5A);
+  __shared__ int32_t sO[MAXL];
+  __shared__ int32_t stars[TMAX];
+  __shared__ int32_t nstar;
+  __shared__ int32_t ends[32][MAXL];
+  __shared__ int32_t okw[32];
   __shared__ int64_t s_opt[1];
   __shared__ int32_t s_win;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  // winner by (objective, deg, c): warp 0, lanes over the local configs,
-  // then a shuffle argmin on the key tuple
+  // 2. winner by (objective, deg, c): warp 0, lanes over the local configs,
+  //    then a shuffle argmin on the key tuple
   if (w == 0) {
     int wi = -1, bd = 0, bc = 0;
     int64_t best = INT64_MAX;
@@ -642,8 +444,11 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     if (lane == 0) {
       s_win = wi;
       s_opt[0] = best;
+      nstar = 0;
     }
   }
+  __syncthreads();
+  const int wl = s_win;
   // the record header: every field K5c does not write (assignment arrays zeroed)
   if (t < UNIAP_MAX_LAYERS) {
     uniap_record* r = ra.rec;
@@ -654,8 +459,6 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     r->stage_mem[t] = 0;
   }
   if (t < MAXCLS) ra.bw->count[t] = 0;
-  __syncthreads();
-  const int wl = s_win;
   if (t == 0) {
     uniap_record* r = ra.rec;
     r->objective = INT64_MAX;
@@ -681,62 +484,248 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     if (t == 0) { win->objective = INT64_MAX; win->cfg = -1; win->status = 0; }
     return;
   }
-  if (t != 0) return;
   const int ci = cfg_list[wl];
-  const CfgDev* cf = cfgs + ci;
-  const int deg = cf->deg;
-  const int32_t* E = cfg_ends + (int64_t)wl * (MAXL + 1);
-  const bool have = E[0] == 1;
+  const CfgDev cf = cfgs[ci];
   const int64_t OPT = s_opt[0];
-  win->objective = OPT;
-  win->cfg = ci;
-  win->deg = deg;
-  win->c = cf->c;
-  win->S = cf->S;
-  win->NSP = cf->NSP;
-  win->n_theta_star = 0;
-  win->status = have ? 0 : 99;
-  int a = 0;
-  for (int i = 0; i < deg; ++i) {
-    const int b = have ? E[1 + i] : L - 1;
-    win->end[i] = b;
-    win->p[i] = P[cf->offP + (int64_t)cf->lev_of[i] * L * L + a * L + b];  // the stage's cap level
-    win->o[i] = (i + 1 < deg) ? arena[cf->offO + b] : 0;
-    a = b + 1;
+  const int64_t* V = vals + (int64_t)wl * (TMAX + 2);
+  const int32_t* th = thetas + (int64_t)wl * TMAX;
+  const int nt = ntheta[wl];
+  // the winner's interval tables P_lev[a][b] at lev * L * PP + a * PP + b
+  // (odd pitch: lanes over a or b conflict-free), in dynamic shared memory
+  // after the suffix table sH
+  extern __shared__ int32_t k5dyn[];
+  int32_t* sPl = k5dyn + (MAXL + 1) * (MAXL + 1);
+  const int PP = L | 1;
+  for (int i = t; i < cf.nlev * L * L; i += K5T) {
+    const int lv = i / (L * L), r = i - lv * L * L;
+    sPl[lv * L * PP + (r / L) * PP + r % L] = P[cf.offP + i];
   }
-  uniap_record* r = ra.rec;
-  if (!have) r->status = UNIAP_ERR_INTERNAL;
-  r->objective = OPT;
-  r->cfg_index = ci;
-  r->deg = deg;
-  r->c = cf->c;
-  // the backward sweeps of the traceback: one per stage, one per skip
-  // conditioning ks when the stage contains the skip source and an edge of it
-  int n = 0;
-  int64_t goff = 0;
-  a = 0;
-  for (int i = 0; i < deg && have && r->status == 0; ++i) {
-    const int b = E[1 + i], len = b - a + 1;
-    const bool cond = cf->skip >= 0 && a <= cf->skip && cf->skip + 2 <= b;
-    const int64_t kept = ra.gstore[ci];  // deg = 1: the forward phase's sweep kept its tables
-    for (int ks = cond ? 0 : -1; ks < (cond ? cf->S : 0); ++ks) {
-      if (kept >= 0) {
-        ra.bw->gofs[i * 33 + ks + 1] = kept + (int64_t)(ks < 0 ? 0 : ks) * L * cf->NSP * (ra.cap + 1);
-        continue;
-      }
-      ra.bw->gofs[i * 33 + ks + 1] = goff;
-      ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1, len, 0, 0};
-      goff += (int64_t)len * cf->NSP * (ra.cap + 1);
+  // stage i (1-based) reads the table of its cap level
+  const int8_t* lev_of = cfgs[ci].lev_of;  // (global: no local copy of cf)
+  auto SPs = [&](int i) { return sPl + lev_of[i - 1] * L * PP; };
+  for (int i = t; i < L - 1; i += K5T) sO[i] = arena[cf.offO + i];
+  // 3. Theta*: every theta with Val = OPT (c > 1); the unconstrained one (c = 1)
+  if (cf.c == 1) {
+    if (t == 0) { stars[0] = -1; nstar = 1; }
+  } else {
+    for (int i = t; i < nt; i += K5T)
+      if (V[i] == OPT) stars[atomicAdd(&nstar, 1)] = i;
+  }
+  __syncthreads();
+  const int ns = nstar;
+  const int deg = cf.deg;
+  // 4. per theta in Theta*: suffix DP H_i[a] (cover [a, L-1] with stages i..deg)
+  //    then the greedy largest end per stage.
+  int32_t* H = scratch + (int64_t)w * (MAXL + 1) * (MAXL + 1);  // [i][a], i = 1..deg, a = 0..L
+  int32_t* mine = ends[w];
+  int32_t best_end[MAXL];
+  bool have = false;
+  // Few theta* (the usual case: one): the whole CTA per theta, H in shared
+  // memory -- stages sequential (one barrier each), warps over the start a,
+  // lanes over the end b with a warp min.  Many: one warp per theta below.
+  constexpr int HP = MAXL + 1;
+  int32_t* sH = k5dyn;  // [i][a], i = 1..deg, a = 0..L
+  for (int si = 0; si < ns && ns <= 4; ++si) {
+    const int32_t theta = stars[si] < 0 ? INF : th[stars[si]];
+    const int64_t F_target = stars[si] < 0 ? OPT : OPT - (int64_t)(cf.c - 1) * theta;
+    for (int a = t; a <= L; a += K5T) {
+      int32_t v = INF;
+      if (a < L) { const int32_t p = SPs(deg)[a * PP + L - 1]; v = p <= theta ? p : INF; }
+      sH[deg * HP + a] = v;
     }
-    a = b + 1;
+    __syncthreads();
+    for (int i = deg - 1; i >= 1; --i) {
+      // H_i[a] = min_b P_i[a][b] + O[b] + H_{i+1}[b+1], b <= L-1-(deg-i)
+      const int bhi = L - 1 - (deg - i);
+      const int32_t* sP = SPs(i);
+      for (int a = w; a <= L; a += K5T / 32) {
+        uint32_t v = INF;
+        for (int b = a + lane; b <= bhi && a < L; b += 32) {
+          const int32_t p = sP[a * PP + b], o = sO[b], hh = sH[(i + 1) * HP + b + 1];
+          if (p <= theta && o <= theta && hh < INF) v = min(v, (uint32_t)p + (uint32_t)o + (uint32_t)hh);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, off));
+        if (lane == 0) sH[i * HP + a] = (int32_t)min(v, (uint32_t)INF);
+      }
+      __syncthreads();
+    }
+    bool ok = (int64_t)sH[1 * HP + 0] == F_target;
+    if (w == 0) {  // greedy: the largest feasible end of each stage
+      int64_t pre = 0;
+      int a = 0;
+      for (int i = 1; i < deg && ok; ++i) {
+        const int32_t* sP = SPs(i);
+        int found = -1;
+        for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
+          const int b = b0 - lane;
+          bool c = false;
+          if (b >= a) {
+            const int32_t p = sP[a * PP + b], o = sO[b], hh = sH[(i + 1) * HP + b + 1];
+            c = p <= theta && o <= theta && hh < INF && pre + p + o + hh == F_target;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, c);
+          if (m) found = b0 - (__ffs(m) - 1);
+        }
+        if (found < 0) { ok = false; break; }
+        if (lane == 0) ends[0][i - 1] = found;
+        pre += sP[a * PP + found] + sO[found];
+        a = found + 1;
+      }
+      if (lane == 0) {
+        ends[0][deg - 1] = L - 1;
+        okw[0] = ok;
+      }
+    }
+    __syncthreads();
+    if (t == 0 && okw[0]) {  // lexicographically largest end vector over theta*
+      bool better = !have;
+      for (int i = 0; i < deg && !better; ++i) {
+        if (ends[0][i] != best_end[i]) { better = ends[0][i] > best_end[i]; break; }
+      }
+      if (better) {
+        for (int i = 0; i < deg; ++i) best_end[i] = ends[0][i];
+        have = true;
+      }
+    }
+    __syncthreads();
   }
-  ra.bw->count[ra.cls_of_cfg[ci]] = n;
+  for (int base = 0; base < ns && ns > 4; base += 32) {
+    const int si = base + w;
+    bool ok = false;
+    if (si < ns) {
+      const int32_t theta = stars[si] < 0 ? INF : th[stars[si]];
+      const int64_t F_target = stars[si] < 0 ? OPT : OPT - (int64_t)(cf.c - 1) * theta;
+      // H_deg[a] = P[a][L-1]
+      for (int a = lane; a <= L; a += 32) {
+        int32_t v = INF;
+        if (a < L) { const int32_t p = SPs(deg)[a * PP + L - 1]; v = p <= theta ? p : INF; }
+        H[deg * (MAXL + 1) + a] = v;
+      }
+      __syncwarp();
+      for (int i = deg - 1; i >= 1; --i) {
+        // H_i[a] = min_b P[a][b] + (O[b] + H_{i+1}[b+1]); the bracket is
+        // lane-independent (broadcast), P[a][b] read transposed
+        const int bhi = L - 1 - (deg - i);
+        const int32_t* Hn = H + (i + 1) * (MAXL + 1);
+        const int32_t* sP = SPs(i);
+        for (int a = lane; a <= L; a += 32) {
+          uint32_t x = INF, y = INF;
+          if (a < L) {
+            int b = a;
+            for (; b + 1 <= bhi; b += 2) {
+              const int32_t p0 = sP[a * PP + b], p1 = sP[a * PP + b + 1];
+              const int32_t o0 = sO[b], o1 = sO[b + 1], h0 = Hn[b + 1], h1 = Hn[b + 2];
+              const uint32_t w0 = (o0 <= theta && h0 < INF) ? (uint32_t)(o0 + h0) : INF;
+              const uint32_t w1 = (o1 <= theta && h1 < INF) ? (uint32_t)(o1 + h1) : INF;
+              x = __viaddmin_u32(w0, p0 <= theta ? (uint32_t)p0 : INF, x);
+              y = __viaddmin_u32(w1, p1 <= theta ? (uint32_t)p1 : INF, y);
+            }
+            if (b <= bhi) {
+              const int32_t p0 = sP[a * PP + b], o0 = sO[b], h0 = Hn[b + 1];
+              const uint32_t w0 = (o0 <= theta && h0 < INF) ? (uint32_t)(o0 + h0) : INF;
+              x = __viaddmin_u32(w0, p0 <= theta ? (uint32_t)p0 : INF, x);
+            }
+          }
+          H[i * (MAXL + 1) + a] = (int32_t)min(min(x, y), (uint32_t)INF);
+        }
+        __syncwarp();
+      }
+      ok = (int64_t)H[1 * (MAXL + 1) + 0] == F_target;
+      // greedy: the largest feasible end of each stage
+      int64_t pre = 0;
+      int a = 0;
+      for (int i = 1; i < deg && ok; ++i) {
+        const int32_t* sP = SPs(i);
+        int found = -1;
+        for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
+          const int b = b0 - lane;
+          bool c = false;
+          if (b >= a) {
+            const int32_t p = sP[a * PP + b], o = sO[b], h = H[(i + 1) * (MAXL + 1) + b + 1];
+            c = p <= theta && o <= theta && h < INF && pre + p + o + h == F_target;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, c);
+          if (m) found = b0 - (__ffs(m) - 1);
+        }
+        if (found < 0) { ok = false; break; }
+        if (lane == 0) mine[i - 1] = found;
+        pre += sP[a * PP + found] + sO[found];
+        a = found + 1;
+      }
+      if (lane == 0) mine[deg - 1] = L - 1;
+      __syncwarp();
+    }
+    if (lane == 0) okw[w] = ok;
+    __syncthreads();
+    // lexicographically largest end vector (theta order is deterministic)
+    if (t == 0) {
+      for (int j = 0; j < 32 && base + j < ns; ++j) {
+        if (!okw[j]) continue;
+        bool better = !have;
+        for (int i = 0; i < deg && !better; ++i) {
+          if (ends[j][i] != best_end[i]) { better = ends[j][i] > best_end[i]; break; }
+        }
+        if (better) {
+          for (int i = 0; i < deg; ++i) best_end[i] = ends[j][i];
+          have = true;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    win->objective = OPT;
+    win->cfg = ci;
+    win->deg = deg;
+    win->c = cf.c;
+    win->S = cf.S;
+    win->NSP = cf.NSP;
+    win->n_theta_star = ns;
+    win->status = have ? 0 : 99;
+    int a = 0;
+    for (int i = 0; i < deg; ++i) {
+      const int b = have ? best_end[i] : L - 1;
+      win->end[i] = b;
+      win->p[i] = SPs(i + 1)[a * PP + b];
+      win->o[i] = (i + 1 < deg) ? sO[b] : 0;
+      a = b + 1;
+    }
+    uniap_record* r = ra.rec;
+    if (!have) r->status = UNIAP_ERR_INTERNAL;
+    r->objective = OPT;
+    r->cfg_index = ci;
+    r->deg = deg;
+    r->c = cf.c;
+    // the backward sweeps of the traceback: one per stage, one per skip
+    // conditioning ks when the stage contains the skip source and an edge of it
+    int n = 0;
+    int64_t goff = 0;
+    a = 0;
+    for (int i = 0; i < deg && have && r->status == 0; ++i) {
+      const int b = best_end[i], len = b - a + 1;
+      const bool cond = cf.skip >= 0 && a <= cf.skip && cf.skip + 2 <= b;
+      const int64_t kept = ra.gstore[ci];  // deg = 1: the forward phase's sweep kept its tables
+      for (int ks = cond ? 0 : -1; ks < (cond ? cf.S : 0); ++ks) {
+        if (kept >= 0) {
+          ra.bw->gofs[i * 33 + ks + 1] = kept + (int64_t)(ks < 0 ? 0 : ks) * L * cf.NSP * (ra.cap + 1);
+          continue;
+        }
+        ra.bw->gofs[i * 33 + ks + 1] = goff;
+        ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1, len};
+        goff += (int64_t)len * cf.NSP * (ra.cap + 1);
+      }
+      a = b + 1;
+    }
+    ra.bw->count[ra.cls_of_cfg[ci]] = n;
+  }
 }
 
 cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
-                       int L, const int64_t* cfg_opt, const int32_t* cfg_ends, Winner* win, const RecordArgs& ra,
-                       cudaStream_t st) {
-  k5a_winner<<<1, K5T, 0, st>>>(cfg, arena, P, cfg_list, n_local, L, cfg_opt, cfg_ends, win, ra);
+                       int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals, const int64_t* cfg_opt,
+                       int32_t* scratch, Winner* win, const RecordArgs& ra, cudaStream_t st) {
+  k5a_winner<<<1, K5T, K5A_DYN, st>>>(cfg, arena, P, cfg_list, n_local, L, thetas, ntheta, vals, cfg_opt, scratch,
+                                      win, ra);
   return cudaGetLastError();
 }
 
@@ -847,7 +836,9 @@ cudaError_t combine_init() {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
   }
-  return cudaFuncSetAttribute((const void*)k4_vals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4Smem));
+  cudaError_t e = cudaFuncSetAttribute((const void*)k4_vals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4Smem));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute((const void*)k5a_winner, cudaFuncAttributeMaxDynamicSharedMemorySize, K5A_DYN);
 }
 
 }  // namespace uniap

@@ -184,14 +184,13 @@ cudaError_t launch_publish(int32_t* d_rec, const uniap_record* rec, int64_t* d_q
                            unsigned long long* d_tm, const unsigned long long* tm, int64_t* d_cfg,
                            const int64_t* cfgopt, int ncfg, cudaStream_t st);
 // K3 (theta candidates) is fused into K4.
-// K4 also searches its config's stage ends (cfg_ends: [n_local][MAXL+1],
-// scratch: [n_local][32][(MAXL+1)^2] for many tied thetas)
 cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int li0,
                       int n_local, int L, int32_t* thetas, int32_t* ntheta, int64_t* vals,
-                      int64_t* cfg_opt, int32_t* cfg_ends, int32_t* scratch, cudaStream_t st);
+                      int64_t* cfg_opt, cudaStream_t st);
 cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
-                       int n_local, int L, const int64_t* cfg_opt, const int32_t* cfg_ends, Winner* win,
-                       const RecordArgs& ra, cudaStream_t st);
+                       int n_local, int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals,
+                       const int64_t* cfg_opt, int32_t* scratch, Winner* win, const RecordArgs& ra,
+                       cudaStream_t st);
 cudaError_t launch_k5c_grid(int max_deg, const CfgDev* cfg, const int32_t* arena, const int32_t* G,
                             const BwPlan* bw, const Winner* win, int L, int cap, uniap_record* rec,
                             cudaStream_t st);
