@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(K1T) k1_costs(ClusterDev cl, BuildBufs bb, con
 // every ceil(x/q) <= 2^22 and sum_u (max A + max R into u + max Rskip into u)
 // <= 2^28, sum_e O <= 2^28.  An explicit quantum is checked as given.
 __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int skip) {
+  pdl_wait();  // K1's maxima (PDL: launched while K1 drains)
   TraceScope tr(TR_K1D);
   __shared__ int64_t mx[MAXL * 4];
   __shared__ int okp[64];
@@ -403,6 +404,7 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
 // K1f: quantise into the int32 device layout (A, M buckets, Rt, Rf, Rs, O);
 // the last block column trims the forward sweeps (k1f_trim).
 __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int32_t* arena) {
+  pdl_wait();  // K1d's quantum (PDL)
   TraceScope tr(TR_K1F);
   const CfgDev cf = cfgs[blockIdx.y];
   const int nqb = gridDim.x - bb.n_trim;  // quantising blocks; then the trim blocks
@@ -448,8 +450,10 @@ cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* c
   const int nbA = (L * 32 + K1T - 1) / K1T;
   const int nbR = 2 * L - 1;  // one block per edge slot: L-1 chain edges, L skip destinations
   k1_costs<<<dim3(nbA + nbR + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR);
-  k1d_quantum<<<ncfg, 64, 0, st>>>(cl, bb, cfg, L, skip);
-  k1f_quantise<<<dim3(16 + (bb.inst ? bb.n_trim : 0), ncfg), 256, 0, st>>>(cl, bb, cfg, L, arena);
+  cudaError_t e = pdl_launch(k1d_quantum, dim3(ncfg), dim3(64), 0, st, cl, bb, cfg, L, skip);
+  if (e != cudaSuccess) return e;
+  e = pdl_launch(k1f_quantise, dim3(16 + (bb.inst ? bb.n_trim : 0), ncfg), dim3(256), 0, st, cl, bb, cfg, L, arena);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

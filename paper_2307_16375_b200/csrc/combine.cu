@@ -33,6 +33,7 @@ __global__ void k_publish(int32_t* __restrict__ d_rec, const int32_t* __restrict
                           int64_t* __restrict__ d_qg, const int64_t* __restrict__ qg,
                           unsigned long long* __restrict__ d_tm, const unsigned long long* __restrict__ tm,
                           int64_t* __restrict__ d_cfg, const int64_t* __restrict__ cfgopt, int ncfg) {
+  pdl_wait();  // K5c's record (PDL)
   const int t = threadIdx.x;
   for (int i = t; i < rec_words; i += blockDim.x) d_rec[i] = rec[i];
   if (t < 2) {
@@ -46,8 +47,9 @@ cudaError_t launch_publish(int32_t* d_rec, const uniap_record* rec, int64_t* d_q
                            unsigned long long* d_tm, const unsigned long long* tm, int64_t* d_cfg,
                            const int64_t* cfgopt, int ncfg, cudaStream_t st) {
   static_assert(sizeof(uniap_record) % 4 == 0, "record words");
-  k_publish<<<1, 256, 0, st>>>(d_rec, reinterpret_cast<const int32_t*>(rec), (int)(sizeof(uniap_record) / 4), d_qg,
-                               qg, d_tm, tm, d_cfg, cfgopt, ncfg);
+  cudaError_t e = pdl_launch(k_publish, dim3(1), dim3(256), 0, st, d_rec, reinterpret_cast<const int32_t*>(rec),
+                             (int)(sizeof(uniap_record) / 4), d_qg, qg, d_tm, tm, d_cfg, cfgopt, ncfg);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -740,6 +742,7 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
                                                  const int32_t* __restrict__ G, const BwPlan* __restrict__ bw,
                                                  const Winner* __restrict__ win, int L, int cap,
                                                  uniap_record* __restrict__ rec) {
+  pdl_wait();  // the backward sweeps' tables (PDL when one launch precedes on the stream)
   TraceScope tr(TR_K5C);
   __shared__ int32_t vec[32][MAXL];
   __shared__ int32_t mem[32];
@@ -821,7 +824,8 @@ cudaError_t launch_k5c_grid(int max_deg, const CfgDev* cfg, const int32_t* arena
                             const BwPlan* bw, const Winner* win, int L, int cap, uniap_record* rec,
                             cudaStream_t st) {
   if (max_deg <= 0) return cudaSuccess;
-  k5c_walk<<<max_deg, 1024, 0, st>>>(cfg, arena, G, bw, win, L, cap, rec);
+  cudaError_t e = pdl_launch(k5c_walk, dim3(max_deg), dim3(1024), 0, st, cfg, arena, G, bw, win, L, cap, rec);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

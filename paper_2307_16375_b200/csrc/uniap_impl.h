@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "uniap.h"
@@ -106,6 +107,26 @@ __device__ __forceinline__ void trace_put(unsigned long long* tr, uint32_t tag, 
     r[3] = sm | (rank << 8) | ((unsigned long long)inst << 16) | ((unsigned long long)n << 40);
   }
 }
+// Programmatic dependent launch (PDL): a kernel launched with pdl_launch may
+// start while its same-stream predecessor finishes; it waits here before it
+// reads anything the predecessor wrote (griddepcontrol, sm_90+).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 // The non-K2 kernels record through a per-translation-unit pointer (set by
 // combine_trace / builder_trace); tag bit 31 marks them, bits 0-7 the kernel.
 enum TraceKind : uint32_t { TR_K1 = 1, TR_K1D = 2, TR_K1F = 3, TR_FILL = 4, TR_K4 = 5, TR_K5A = 6, TR_K5C = 7 };
