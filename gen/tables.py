@@ -72,14 +72,15 @@ def _draw_cfg(rng, L, S, cap, skip_src, dist, forbid_p, with_O):
 
 
 def random_tables(seed, L=None, S_max=3, cap=None, n_cfg=None, dist=None,
-                  skip_p=0.4, forbid_p=None, deg_max=None, stage_caps=False):
+                  skip_p=0.4, forbid_p=None, deg_max=None, stage_caps=False, rcut=False):
     """Random tiny instance for brute-force checks (SURVEY.md Sec. 4 tier T0).
 
     L <= 6, |S| <= 3, cap <= 7 by default; skip edges in ``skip_p`` of the
     instances; cut costs O != 0; 'uniform' or tie-heavy ('ties') values;
     forbidden entries (M = cap+1).  ``stage_caps``: every config also gets a
     per-stage memory cap (``stage_cap``, drawn in [0, cap]; heterogeneous
-    devices).
+    devices).  ``rcut``: every config also gets a strategy-dependent cut cost
+    ``Rcut[e][k][l]`` (Eq. 4 with R' per strategy pair), values like O's.
     """
     rng = np.random.default_rng(seed)
     L = int(rng.integers(1, 7)) if L is None else L
@@ -104,6 +105,12 @@ def random_tables(seed, L=None, S_max=3, cap=None, n_cfg=None, dist=None,
         crng = np.random.default_rng(seed + 12_345_678)  # separate stream: the tables above are unchanged
         for d in cfgs:
             d["stage_cap"] = crng.integers(max(cap - 3, 0), cap + 1, size=d["deg"]).astype(np.int32)
+    if rcut:
+        rrng = np.random.default_rng(seed + 23_456_789)
+        for d in cfgs:
+            S = d["n_strat"]
+            hi = 2 if dist == "ties" else 5
+            d["Rcut"] = rrng.integers(0, hi, size=(max(L - 1, 0), S, S)).astype(np.int32)
     return {"L": L, "cap": cap, "skip_src": skip_src, "cfgs": cfgs}
 
 

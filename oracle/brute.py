@@ -7,11 +7,14 @@ For tiny instances only.  Enumerates, for every candidate config (deg, c):
   * every strategy vector S satisfying Eq. (8) (PAPER.md:194-201);
 and evaluates literally
   p_i = sum_{u in i} A_u[k_u] + sum_{<u,v> in E, u,v in i} R_uv[k_u][k_v]   (Eq. 3)
-  o_j = O[last layer of stage j]                                            (Eq. 4, scalar R')
+  o_j = O[e_j] (+ Rcut[e_j][k_{e_j}][k_{e_j+1}] when the config gives the
+        strategy-dependent cut cost, Eq. 4 with R'; e_j = last layer of stage j)
   mem_i = sum_{u in i} M_u[k_u] <= cap_i (the stage's cap, = cap unless the
           config gives per-stage caps: heterogeneous devices)   (Eq. 5)
   tpi = sum p + sum o + (c-1) * max(P u O)                                  (Eq. 2)
-and returns the minimum of the key (tpi, deg, c, stage_of, strategy_of).
+and returns the minimum of the key (tpi, deg, c, stage_of, strategy_of) --
+with Rcut: (tpi, deg, c, stage_of, boundary vector, strategy_of), the
+boundary vector (k_{e_1}, k_{e_1+1}, k_{e_2}, k_{e_2+1}, ...) (reading A-31).
 """
 from __future__ import annotations
 
@@ -48,6 +51,7 @@ def solve_cfg(t, cfg, guard=2_000_000):
     Rs = None if cfg.get("Rskip") is None or s < 0 else np.asarray(cfg["Rskip"], dtype=np.int64).reshape(L, S, S)
     O = np.zeros(max(L - 1, 0), dtype=np.int64) if cfg.get("O") is None else np.asarray(cfg["O"], dtype=np.int64)
     caps = [cap] * deg if cfg.get("stage_cap") is None else [int(x) for x in cfg["stage_cap"]]
+    RC = None if cfg.get("Rcut") is None else np.asarray(cfg["Rcut"], dtype=np.int64).reshape(L - 1, S, S)
     places = sorted(placements(L, deg))
     if not places:
         return None
@@ -78,7 +82,7 @@ def solve_cfg(t, cfg, guard=2_000_000):
             total += p
             mx = np.maximum(mx, p)
             if i + 1 < deg:
-                o = O[b]
+                o = O[b] + (RC[b, K[:, b], K[:, b + 1]] if RC is not None else 0)
                 total += o
                 mx = np.maximum(mx, o)
         f = total + (c - 1) * mx
@@ -86,6 +90,10 @@ def solve_cfg(t, cfg, guard=2_000_000):
         j = int(np.argmin(f))            # first = lexicographically smallest strategy vector
         if f[j] == INT64_MAX:
             continue
+        if RC is not None:               # reading A-31: the boundary vector before strategy_of
+            cand = np.nonzero(f == f[j])[0]
+            bidx = [x for e in ends[:-1] for x in (e, e + 1)]
+            j = int(min(cand, key=lambda r: (tuple(K[r, bidx]), tuple(K[r]))))
         if best is None or f[j] < best[0]:   # placements in lexicographic order: keep first
             best = (int(f[j]), list(map(int, so)), list(map(int, K[j])))
     return best

@@ -75,6 +75,20 @@ static int validate_tables(const orc_tables* t) {
     if (c->stage_cap)
       for (int i = 0; i < c->deg; ++i)
         if (c->stage_cap[i] < 0 || c->stage_cap[i] > t->cap) return ORC_ERR_ARG;
+    if (c->Rcut) {
+      if (c->stage_cap) return ORC_ERR_ARG; /* NEXT-1 and NEXT-2 are not combined */
+      int64_t csum = 0;
+      for (int e = 0; e < L - 1; ++e) {
+        int64_t mx = 0;
+        for (int k = 0; k < S * S; ++k) {
+          int32_t r = c->Rcut[(size_t)e * S * S + k];
+          if (r < 0 || r > ENTRY_MAX) return ORC_ERR_RANGE;
+          mx = max64(mx, r);
+        }
+        csum += mx + (c->O ? c->O[e] : 0);
+      }
+      if (csum > SUM_MAX) return ORC_ERR_RANGE; /* every cut's o_j <= O[e] + max Rcut[e] */
+    }
     if (sum > SUM_MAX || osum > SUM_MAX) return ORC_ERR_RANGE;
   }
   return ORC_OK;
@@ -403,7 +417,7 @@ static int check_solution(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
     sum += p;
     mx = max64(mx, p);
     if (i + 1 < deg) {
-      int64_t o = Ocut(c, b);
+      int64_t o = Ocut(c, b) + (c->Rcut ? c->Rcut[((size_t)b * S + sol->strat[b]) * S + sol->strat[b + 1]] : 0);
       if (o != sol->o[i]) return ORC_ERR_INTERNAL;
       sum += o;
       mx = max64(mx, o);
@@ -414,6 +428,377 @@ static int check_solution(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
   if (tpi(sum, mx, c->c) != sol->obj) return ORC_ERR_INTERNAL;
   return ORC_OK;
 }
+
+/* ======================================================================== */
+/* NEXT-1: strategy-dependent cross-stage cost (Eq. 4 with R' per strategy) */
+/* ======================================================================== */
+/* o_j = O[e_j] + Rcut[e_j][k_{e_j}][k_{e_j + 1}]: Eq. (4) sums S_u^T R'_uv S_v
+ * over the edges from stage j to stage j+1; for the chain
+ * edge e_j -> e_j + 1 that is Rcut, the edges skipping past the cut keep the
+ * scalar part O (reading A-16).  The stage optimum now depends on the
+ * strategies at the stage's two ends, so the interval table grows to
+ * T[a][b][kf][kl]: the minimum of Eq. (3) over [a,b] under Eq. (5) with layer
+ * a on kf and layer b on kl. */
+static int32_t Rc(const orc_cfg* c, int e, int k, int l) {
+  int S = c->n_strat;
+  return c->Rcut[((size_t)e * S + k) * S + l];
+}
+static int64_t ocut(const orc_cfg* c, int e, int kl, int kf) { return Ocut(c, e) + Rc(c, e, kl, kf); }
+
+/* Strategy k allowed at layer u with the start layer a restricted to kf. */
+static int allowed_f(const orc_tables* t, const orc_cfg* c, int u, int k, int ks, int a, int kf) {
+  if (!allowed(t, c, u, k, ks)) return 0;
+  if (kf >= 0 && u == a && k != kf) return 0;
+  return 1;
+}
+
+/* The textbook forward DP of interval_row with the start layer on kf:
+ * rowk[b][kl] = min cost of [a,b] with layer b on kl (INF if infeasible). */
+static void interval_row_k(const orc_tables* t, const orc_cfg* c, int a, int ks, int kf, int64_t* rowk) {
+  int L = t->L, S = c->n_strat, Q = t->cap + 1;
+  int64_t* Dp = (int64_t*)malloc(sizeof(int64_t) * (size_t)S * Q);
+  int64_t* Dc = (int64_t*)malloc(sizeof(int64_t) * (size_t)S * Q);
+  for (int k = 0; k < S; ++k)
+    for (int q = 0; q < Q; ++q)
+      Dc[(size_t)k * Q + q] = (allowed_f(t, c, a, k, ks, a, kf) && c->M[a * S + k] <= q) ? A_cond(t, c, a, k, ks) : INF;
+  for (int u = a;; ++u) {
+    for (int k = 0; k < S; ++k) rowk[(size_t)u * S + k] = Dc[(size_t)k * Q + t->cap];
+    if (u + 1 >= L) break;
+    int64_t* tmp = Dp; Dp = Dc; Dc = tmp;
+    int v = u + 1;
+    for (int k = 0; k < S; ++k) {
+      int64_t* out = Dc + (size_t)k * Q;
+      for (int q = 0; q < Q; ++q) out[q] = INF;
+      if (!allowed_f(t, c, v, k, ks, a, kf)) continue;
+      int m = c->M[v * S + k];
+      int64_t av = A_cond(t, c, v, k, ks);
+      for (int kp = 0; kp < S; ++kp) {
+        int64_t r = Rchain(c, u, kp, k);
+        const int64_t* in = Dp + (size_t)kp * Q;
+        for (int q = m; q < Q; ++q) {
+          int64_t x = in[q - m] + r;
+          if (x < out[q]) out[q] = x;
+        }
+      }
+      for (int q = m; q < Q; ++q) out[q] = out[q] >= INF ? INF : out[q] + av;
+    }
+  }
+  free(Dp);
+  free(Dc);
+}
+
+/* T[((a*L + b)*S + kf)*S + kl] for every a <= b (min over the skip
+ * conditioning ks when the stage holds the skip source and one of its edges). */
+static void cut_tables(const orc_tables* t, const orc_cfg* c, int64_t* T) {
+  int L = t->L, S = c->n_strat, s = t->skip_src;
+  size_t n = (size_t)L * L * S * S;
+  for (size_t i = 0; i < n; ++i) T[i] = INF;
+  int64_t* rowk = (int64_t*)malloc(sizeof(int64_t) * (size_t)L * S);
+  for (int a = 0; a < L; ++a)
+    for (int kf = 0; kf < S; ++kf) {
+      int cond = (s >= 0 && c->Rskip && a <= s && s + 2 < L);
+      for (int ks = cond ? 0 : -1; ks < (cond ? S : 0); ++ks) {
+        interval_row_k(t, c, a, ks, kf, rowk);
+        for (int b = a; b < L; ++b)
+          for (int kl = 0; kl < S; ++kl) {
+            int64_t* d = &T[(((size_t)a * L + b) * S + kf) * S + kl];
+            *d = min64(*d, rowk[(size_t)b * S + kl]);
+          }
+      }
+    }
+  free(rowk);
+}
+#define TT(a, b, kf, kl) T[((((size_t)(a)) * L + (b)) * S + (kf)) * S + (kl)]
+
+static void pset_add(pset* p, int64_t sig, int64_t mx, int* cap) {
+  if (p->n == *cap) {
+    *cap = *cap ? 2 * *cap : 16;
+    p->v = (pair_t*)realloc(p->v, sizeof(pair_t) * (size_t)*cap);
+  }
+  p->v[p->n].sig = sig;
+  p->v[p->n].mx = mx;
+  p->n++;
+}
+/* exists (s2, m2) in set with sig + s2 + (c-1) max(mx, m2) == opt */
+static int pset_hits(const pset* p, int64_t sig, int64_t mx, int c, int64_t opt) {
+  for (int j = 0; j < p->n; ++j)
+    if (tpi(sig + p->v[j].sig, max64(mx, p->v[j].mx), c) == opt) return 1;
+  return 0;
+}
+
+/* Backward DP of stage_walk with the first layer restricted to kf and the
+ * last to kl (-1: free): the lexicographically smallest strategy vector of
+ * [a,b] reaching `target` (reading A-11 within the stage). */
+static int stage_walk_fl(const orc_tables* t, const orc_cfg* c, int a, int b, int ks, int kf, int kl, int64_t target,
+                         int32_t* out) {
+  int S = c->n_strat, Q = t->cap + 1, n = b - a + 1;
+  int64_t* G = (int64_t*)malloc(sizeof(int64_t) * (size_t)n * S * Q);
+#define GI(u, k, q) G[(((size_t)((u) - a) * S) + (k)) * Q + (q)]
+  for (int u = b; u >= a; --u)
+    for (int k = 0; k < S; ++k)
+      for (int q = 0; q < Q; ++q) {
+        int m = c->M[u * S + k];
+        int64_t v = INF;
+        int ok = allowed_f(t, c, u, k, ks, a, kf) && !(kl >= 0 && u == b && k != kl);
+        if (ok && m <= q) {
+          if (u == b) v = A_cond(t, c, u, k, ks);
+          else {
+            int64_t best = INF;
+            for (int k2 = 0; k2 < S; ++k2) best = min64(best, add_sat(Rchain(c, u, k, k2), GI(u + 1, k2, q - m)));
+            v = add_sat(best, A_cond(t, c, u, k, ks));
+          }
+        }
+        GI(u, k, q) = v;
+      }
+  int64_t rem = target;
+  int q = t->cap, found = 1, kprev = -1;
+  for (int u = a; u <= b && found; ++u) {
+    found = 0;
+    for (int k = 0; k < S; ++k) {
+      int64_t edge = (u > a) ? Rchain(c, u - 1, kprev, k) : 0;
+      if (GI(u, k, q) < INF && edge + GI(u, k, q) == rem) {
+        out[u] = k;
+        rem -= edge + A_cond(t, c, u, k, ks);
+        q -= c->M[u * S + k];
+        kprev = k;
+        found = 1;
+        break;
+      }
+    }
+  }
+#undef GI
+  free(G);
+  return found;
+}
+
+static int stage_strategies_fl(const orc_tables* t, const orc_cfg* c, int a, int b, int kf, int kl, int64_t target,
+                               int32_t* strat) {
+  int S = c->n_strat, s = t->skip_src;
+  int cond = (s >= 0 && c->Rskip && a <= s && s + 2 <= b);
+  int32_t best[ORC_MAX_L], cur[ORC_MAX_L];
+  int have = 0;
+  for (int ks = cond ? 0 : -1; ks < (cond ? S : 0); ++ks) {
+    if (!stage_walk_fl(t, c, a, b, ks, kf, kl, target, cur)) continue;
+    int less = !have;
+    for (int u = a; u <= b && !less; ++u)
+      if (cur[u] != best[u]) { less = cur[u] < best[u]; break; }
+    if (less) { memcpy(best + a, cur + a, sizeof(int32_t) * (b - a + 1)); have = 1; }
+  }
+  if (have) memcpy(strat + a, best + a, sizeof(int32_t) * (b - a + 1));
+  return have;
+}
+
+/* One candidate config with strategy-dependent cut costs, solved exactly:
+ * Pareto sets Set(i, a, kf) of (sigma, mx) over ways to cover [a, L-1] with
+ * stages i..deg when stage i starts at a on strategy kf; Eq. (2) from
+ * Set(1, 0, *).  Then the tie-break of reading A-31: the largest feasible end
+ * of each stage in turn (lexicographically smallest stage_of), then the
+ * boundary strategies (k_{e_1}, k_{e_1 + 1}, ...) smallest first, then the
+ * lexicographically smallest strategies inside each stage. */
+static void solve_cfg_cut(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
+  int L = t->L, deg = c->deg, S = c->n_strat, cc = c->c;
+  sol->obj = INF;
+  sol->status = ORC_OK;
+  if (deg > L) return;
+  int64_t* T = (int64_t*)malloc(sizeof(int64_t) * (size_t)L * L * S * S);
+  cut_tables(t, c, T);
+  /* Set(i, a, kf): index ((i-1)*L + a)*S + kf */
+  size_t nsets = (size_t)deg * L * S;
+  pset* sets = (pset*)calloc(nsets, sizeof(pset));
+#define SETF(i, a, kf) sets[(((size_t)((i) - 1) * L) + (a)) * S + (kf)]
+  for (int a = 0; a < L; ++a)
+    for (int kf = 0; kf < S; ++kf) {
+      int64_t v = INF;
+      for (int kl = 0; kl < S; ++kl) v = min64(v, TT(a, L - 1, kf, kl));
+      if (v < INF) {
+        int capn = 0;
+        pset_add(&SETF(deg, a, kf), v, v, &capn);
+      }
+    }
+  for (int i = deg - 1; i >= 1; --i)
+    for (int a = 0; a < L; ++a)
+      for (int kf = 0; kf < S; ++kf) {
+        pset* ps = &SETF(i, a, kf);
+        int capn = 0;
+        for (int b = a; b + 1 < L; ++b)
+          for (int kl = 0; kl < S; ++kl) {
+            int64_t p = TT(a, b, kf, kl);
+            if (p >= INF) continue;
+            for (int kf2 = 0; kf2 < S; ++kf2) {
+              const pset* nx = &SETF(i + 1, b + 1, kf2);
+              int64_t o = ocut(c, b, kl, kf2);
+              for (int j = 0; j < nx->n; ++j)
+                pset_add(ps, p + o + nx->v[j].sig, max64(max64(p, o), nx->v[j].mx), &capn);
+            }
+          }
+        if (ps->n) pareto(ps);
+      }
+  int64_t opt = INF;
+  for (int kf = 0; kf < S; ++kf)
+    for (int j = 0; j < SETF(1, 0, kf).n; ++j) opt = min64(opt, tpi(SETF(1, 0, kf).v[j].sig, SETF(1, 0, kf).v[j].mx, cc));
+  sol->obj = opt;
+  if (opt < INF) {
+    /* (a) stage ends: prefix Pareto sets per last strategy of the fixed stages */
+    pset pre[ORC_MAX_S], nxt[ORC_MAX_S];
+    int precap[ORC_MAX_S], nxtcap[ORC_MAX_S];
+    memset(pre, 0, sizeof pre);
+    memset(nxt, 0, sizeof nxt);
+    memset(precap, 0, sizeof precap);
+    memset(nxtcap, 0, sizeof nxtcap);
+    int a = 0;
+    for (int i = 1; i <= deg && sol->status == ORC_OK; ++i) {
+      int chosen = -1;
+      int blo = (i == deg) ? L - 1 : a, bhi = (i == deg) ? L - 1 : L - 2;
+      for (int b = bhi; b >= blo && chosen < 0; --b) {
+        int hit = 0;
+        for (int kf = 0; kf < S && !hit; ++kf)
+          for (int kl = 0; kl < S && !hit; ++kl) {
+            int64_t p = TT(a, b, kf, kl);
+            if (p >= INF) continue;
+            /* prefix pairs with the incoming cut (stage 1: none) */
+            for (int kp = 0; kp < (i == 1 ? 1 : S) && !hit; ++kp) {
+              const pset* pp = (i == 1) ? NULL : &pre[kp];
+              int np = (i == 1) ? 1 : pp->n;
+              for (int x = 0; x < np && !hit; ++x) {
+                int64_t s0 = (i == 1) ? 0 : pp->v[x].sig, m0 = (i == 1) ? 0 : pp->v[x].mx;
+                int64_t oin = (i == 1) ? 0 : ocut(c, a - 1, kp, kf);
+                int64_t sg = s0 + oin + p, mx = max64(max64(m0, oin), p);
+                if (i == deg) hit = tpi(sg, mx, cc) == opt;
+                else
+                  for (int kf2 = 0; kf2 < S && !hit; ++kf2) {
+                    int64_t o = ocut(c, b, kl, kf2);
+                    hit = pset_hits(&SETF(i + 1, b + 1, kf2), sg + o, max64(mx, o), cc, opt);
+                  }
+              }
+            }
+          }
+        if (hit) chosen = b;
+      }
+      if (chosen < 0) { sol->status = ORC_ERR_INTERNAL; break; }
+      sol->end[i - 1] = chosen;
+      /* the prefix sets through stage i, per its last strategy */
+      for (int kl = 0; kl < S; ++kl) nxt[kl].n = 0;
+      for (int kf = 0; kf < S; ++kf)
+        for (int kl = 0; kl < S; ++kl) {
+          int64_t p = TT(a, chosen, kf, kl);
+          if (p >= INF) continue;
+          for (int kp = 0; kp < (i == 1 ? 1 : S); ++kp) {
+            int np = (i == 1) ? 1 : pre[kp].n;
+            for (int x = 0; x < np; ++x) {
+              int64_t s0 = (i == 1) ? 0 : pre[kp].v[x].sig, m0 = (i == 1) ? 0 : pre[kp].v[x].mx;
+              int64_t oin = (i == 1) ? 0 : ocut(c, a - 1, kp, kf);
+              pset_add(&nxt[kl], s0 + oin + p, max64(max64(m0, oin), p), &nxtcap[kl]);
+            }
+          }
+        }
+      for (int kl = 0; kl < S; ++kl) {
+        if (nxt[kl].n) pareto(&nxt[kl]);
+        pset tmp = pre[kl]; pre[kl] = nxt[kl]; nxt[kl] = tmp;
+        int tc = precap[kl]; precap[kl] = nxtcap[kl]; nxtcap[kl] = tc;
+      }
+      a = chosen + 1;
+    }
+    for (int k = 0; k < S; ++k) { free(pre[k].v); free(nxt[k].v); }
+    /* (b) boundary strategies with the ends fixed: suffix sets SE(i, kf) of
+     * stages i..deg (stage i first on kf, later boundaries free), then the
+     * greedy (kl_1, kf_2, kl_2, ...) smallest first */
+    int32_t kfs[ORC_MAX_L], kls[ORC_MAX_L];
+    int st[ORC_MAX_L + 1];
+    st[0] = 0;
+    for (int i = 1; i < deg; ++i) st[i] = sol->end[i - 1] + 1;
+    pset* SE = (pset*)calloc((size_t)(deg + 1) * S, sizeof(pset));
+#define SEF(i, kf) SE[(size_t)(i) * S + (kf)]
+    for (int i = deg; i >= 1 && sol->status == ORC_OK; --i) {
+      int a0 = st[i - 1], b0 = sol->end[i - 1];
+      for (int kf = 0; kf < S; ++kf) {
+        pset* ps = &SEF(i, kf);
+        int capn = 0;
+        if (i == deg) {
+          int64_t v = INF;
+          for (int kl = 0; kl < S; ++kl) v = min64(v, TT(a0, b0, kf, kl));
+          if (v < INF) pset_add(ps, v, v, &capn);
+        } else {
+          for (int kl = 0; kl < S; ++kl) {
+            int64_t p = TT(a0, b0, kf, kl);
+            if (p >= INF) continue;
+            for (int kf2 = 0; kf2 < S; ++kf2) {
+              int64_t o = ocut(c, b0, kl, kf2);
+              const pset* nx = &SEF(i + 1, kf2);
+              for (int j = 0; j < nx->n; ++j)
+                pset_add(ps, p + o + nx->v[j].sig, max64(max64(p, o), nx->v[j].mx), &capn);
+            }
+          }
+          if (ps->n) pareto(ps);
+        }
+      }
+    }
+    /* prefix state: Pareto set of the fixed stages 1..j (stage 1's first
+     * strategy free), ending on kls[j-1] */
+    pset cur = {0}, nw = {0};
+    int curcap = 0, nwcap = 0;
+    for (int j = 1; j < deg && sol->status == ORC_OK; ++j) {
+      int a0 = st[j - 1], b0 = sol->end[j - 1];
+      /* candidates of stage j's pairs given its first strategy (fixed for j > 1) */
+      int chosen_kl = -1, chosen_kf = -1;
+      for (int kl = 0; kl < S && chosen_kl < 0; ++kl) {
+        nw.n = 0;
+        for (int kf = 0; kf < S; ++kf) {
+          if (j > 1 && kf != kfs[j - 1]) continue;
+          int64_t p = TT(a0, b0, kf, kl);
+          if (p >= INF) continue;
+          int np = (j == 1) ? 1 : cur.n;
+          for (int x = 0; x < np; ++x) {
+            int64_t s0 = (j == 1) ? 0 : cur.v[x].sig, m0 = (j == 1) ? 0 : cur.v[x].mx;
+            pset_add(&nw, s0 + p, max64(m0, p), &nwcap);
+          }
+        }
+        for (int x = 0; x < nw.n && chosen_kl < 0; ++x)
+          for (int kf2 = 0; kf2 < S && chosen_kl < 0; ++kf2) {
+            int64_t o = ocut(c, b0, kl, kf2);
+            if (pset_hits(&SEF(j + 1, kf2), nw.v[x].sig + o, max64(nw.v[x].mx, o), cc, opt)) chosen_kl = kl;
+          }
+      }
+      if (chosen_kl < 0) { sol->status = ORC_ERR_INTERNAL; break; }
+      /* nw holds stage j's prefix pairs ending on chosen_kl (the loop broke on it) */
+      for (int kf2 = 0; kf2 < S && chosen_kf < 0; ++kf2) {
+        int64_t o = ocut(c, b0, chosen_kl, kf2);
+        for (int x = 0; x < nw.n && chosen_kf < 0; ++x)
+          if (pset_hits(&SEF(j + 1, kf2), nw.v[x].sig + o, max64(nw.v[x].mx, o), cc, opt)) chosen_kf = kf2;
+      }
+      if (chosen_kf < 0) { sol->status = ORC_ERR_INTERNAL; break; }
+      kls[j - 1] = chosen_kl;
+      kfs[j] = chosen_kf;
+      /* prefix through the cut into stage j+1 (its own cost added next round) */
+      int64_t o = ocut(c, b0, chosen_kl, chosen_kf);
+      cur.n = 0;
+      for (int x = 0; x < nw.n; ++x) pset_add(&cur, nw.v[x].sig + o, max64(nw.v[x].mx, o), &curcap);
+      pareto(&cur);
+    }
+    free(cur.v);
+    free(nw.v);
+    for (size_t i = 0; i < (size_t)(deg + 1) * S; ++i) free(SE[i].v);
+    free(SE);
+#undef SEF
+    /* (c) strategies inside each stage, with the boundary strategies fixed;
+     * p_i = T for fixed ends strategies (minimised over a free first / last) */
+    for (int i = 0; i < deg && sol->status == ORC_OK; ++i) {
+      int a0 = st[i], b0 = sol->end[i];
+      int kf = i > 0 ? kfs[i] : -1, kl = i + 1 < deg ? kls[i] : -1;
+      int64_t v = INF;
+      for (int x = 0; x < S; ++x)
+        for (int y = 0; y < S; ++y)
+          if ((kf < 0 || x == kf) && (kl < 0 || y == kl)) v = min64(v, TT(a0, b0, x, y));
+      sol->p[i] = v;
+      if (i + 1 < deg) sol->o[i] = ocut(c, b0, kls[i], kfs[i + 1]);
+      if (v >= INF || !stage_strategies_fl(t, c, a0, b0, kf, kl, v, sol->strat)) sol->status = ORC_ERR_INTERNAL;
+    }
+  }
+  for (size_t i = 0; i < nsets; ++i) free(sets[i].v);
+#undef SETF
+  free(sets);
+  free(T);
+}
+#undef TT
 
 /* ======================================================================== */
 /* Algorithm 1 outer loop over candidates, optionally on host threads       */
@@ -432,7 +817,8 @@ static void* worker(void* arg) {
     int i = p->next++;
     pthread_mutex_unlock(&p->mu);
     if (i >= p->t->n_cfg) break;
-    solve_cfg(p->t, &p->t->cfg[i], &p->sols[i]);
+    if (p->t->cfg[i].Rcut) solve_cfg_cut(p->t, &p->t->cfg[i], &p->sols[i]);
+    else solve_cfg(p->t, &p->t->cfg[i], &p->sols[i]);
     if (p->sols[i].status == ORC_OK && p->sols[i].obj < INF)
       p->sols[i].status = check_solution(p->t, &p->t->cfg[i], &p->sols[i]);
   }

@@ -43,6 +43,12 @@ typedef struct {
   const int32_t* stage_cap; /* [deg] memory cap of stage i (0..cap), or NULL (= cap):
                                heterogeneous devices, PAPER.md:161 ("the value of m varies
                                in the case of heterogeneous computing devices")          */
+  const int32_t* Rcut;   /* [L-1][S][S] or NULL: the strategy-dependent cross-stage cost of
+                            the chain edge e -> e+1 when a cut follows layer e (Eq. 4,
+                            S_u^T R'_uv S_v): o_j = O[e] + Rcut[e][k_e][k_e+1].
+                            Not combined with stage_cap.  Tie-break key (reading A-31):
+                            (tpi, deg, c, stage_of, boundary vector, strategy_of) with the
+                            boundary vector (k_{e_1}, k_{e_1+1}, k_{e_2}, k_{e_2+1}, ...)    */
 } orc_cfg;
 
 typedef struct {

@@ -36,7 +36,7 @@ class _Cfg(C.Structure):
     _fields_ = [("deg", C.c_int32), ("c", C.c_int32), ("n_strat", C.c_int32),
                 ("A", C.POINTER(C.c_int32)), ("M", C.POINTER(C.c_int32)), ("R", C.POINTER(C.c_int32)),
                 ("Rskip", C.POINTER(C.c_int32)), ("O", C.POINTER(C.c_int32)),
-                ("stage_cap", C.POINTER(C.c_int32))]
+                ("stage_cap", C.POINTER(C.c_int32)), ("Rcut", C.POINTER(C.c_int32))]
 
 
 class _Tables(C.Structure):
@@ -131,8 +131,10 @@ def _marshal_tables(t):
         if O is not None and O.size == 0:
             O = np.zeros(1, np.int32)
         SC = _i32(c["stage_cap"]).reshape(c["deg"]) if c.get("stage_cap") is not None else None
-        keep += [A, M, R, Rs, O, SC]
-        cfgs[i] = _Cfg(c["deg"], c["c"], S, _ptr32(A), _ptr32(M), _ptr32(R), _ptr32(Rs), _ptr32(O), _ptr32(SC))
+        RC = _i32(c["Rcut"]).reshape(L - 1, S, S) if c.get("Rcut") is not None and L > 1 else None
+        keep += [A, M, R, Rs, O, SC, RC]
+        cfgs[i] = _Cfg(c["deg"], c["c"], S, _ptr32(A), _ptr32(M), _ptr32(R), _ptr32(Rs), _ptr32(O), _ptr32(SC),
+                       _ptr32(RC))
     tb = _Tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs)
     keep.append(cfgs)
     return tb, keep

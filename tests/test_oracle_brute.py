@@ -109,3 +109,27 @@ def test_stage_caps_equal_to_cap_change_nothing_and_lower_caps_never_help(orc):
         assert r0 == r1
         for a, b in zip(r0["cfg_objective"], r2["cfg_objective"]):
             assert b >= a  # restricting a stage's memory can only raise the optimum
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1: strategy-dependent cross-stage cost (Eq. 4, S_u^T R'_uv S_v for
+# the chain edge at each cut); tie-break reading A-31.
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_oracle_equals_brute_force_with_strategy_dependent_cut_cost(orc, chunk):
+    for seed in range(chunk * 500, (chunk + 1) * 500):
+        t = tables.random_tables(900_000 + seed, rcut=True)
+        _same(orc.solve_tables(t), brute.solve_tables(t))
+
+
+def test_zero_cut_matrix_keeps_the_objective_and_costs_only_add(orc):
+    """Rcut = 0 is Eq. 4 with a constant R' (the scalar path): same optimum;
+    Rcut >= 0 only adds to the objective."""
+    for seed in range(300):
+        t = tables.random_tables(950_000 + seed, rcut=True)
+        base = dict(t, cfgs=[{k: v for k, v in c.items() if k != "Rcut"} for c in t["cfgs"]])
+        zero = dict(t, cfgs=[dict(c, Rcut=np.zeros_like(c["Rcut"])) for c in t["cfgs"]])
+        r0, rz, r1 = orc.solve_tables(base), orc.solve_tables(zero), orc.solve_tables(t)
+        assert r0["cfg_objective"] == rz["cfg_objective"]
+        assert all(b >= a for a, b in zip(r0["cfg_objective"], r1["cfg_objective"]))
