@@ -108,6 +108,15 @@ typedef struct {
                                 ("the value of m varies in the case of
                                 heterogeneous computing devices").  At most
                                 UNIAP_MAX_LEVELS distinct values per config (else _RANGE)    */
+  const int32_t* Rcut;       /* [L-1][n_strat][n_strat] or NULL: the strategy-dependent cross-stage
+                                cost of the chain edge e -> e+1 when a cut follows layer e
+                                (Eq. 4, S_u^T R'_uv S_v): o_j = O[e_j] +
+                                Rcut[e_j][k_{e_j}][k_{e_j + 1}], entries 0..2^22, sum over e of
+                                (O[e] + max Rcut[e]) <= 2^28.  Ties are then broken by
+                                (tpi, deg, c, stage_of, boundary vector, strategy_of), the
+                                boundary vector (k_{e_1}, k_{e_1+1}, k_{e_2}, k_{e_2+1}, ...)
+                                (reading A-31).  Not combined with stage_cap (_ARG); its configs
+                                need Q <= 2048 (Q <= 1024 for |S| > 12), else _RANGE          */
 } uniap_config;
 
 typedef struct {

@@ -27,7 +27,7 @@ _P64 = C.POINTER(C.c_int64)
 
 class uniap_config(C.Structure):
     _fields_ = [("deg", C.c_int32), ("c", C.c_int32), ("n_strat", C.c_int32), ("A", _P32), ("M", _P32),
-                ("R", _P32), ("Rskip", _P32), ("O", _P32), ("stage_cap", _P32)]
+                ("R", _P32), ("Rskip", _P32), ("O", _P32), ("stage_cap", _P32), ("Rcut", _P32)]
 
 
 class uniap_tables(C.Structure):
@@ -159,8 +159,10 @@ def _tables(t):
         Rs = _i32(c["Rskip"]).reshape(L, S, S) if c.get("Rskip") is not None else None
         O = _i32(c["O"]).reshape(L - 1) if c.get("O") is not None and L > 1 else None
         SC = _i32(c["stage_cap"]).reshape(c["deg"]) if c.get("stage_cap") is not None else None
-        keep += [A, M, R, Rs, O, SC]
-        cfgs[i] = uniap_config(c["deg"], c["c"], S, _p32(A), _p32(M), _p32(R), _p32(Rs), _p32(O), _p32(SC))
+        RC = _i32(c["Rcut"]).reshape(L - 1, S, S) if c.get("Rcut") is not None and L > 1 else None
+        keep += [A, M, R, Rs, O, SC, RC]
+        cfgs[i] = uniap_config(c["deg"], c["c"], S, _p32(A), _p32(M), _p32(R), _p32(Rs), _p32(O), _p32(SC),
+                               _p32(RC))
     keep.append(cfgs)
     return uniap_tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs), keep
 

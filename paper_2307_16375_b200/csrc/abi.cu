@@ -176,6 +176,13 @@ struct uniap_handle {
   std::vector<Levels> lev;
   std::vector<std::vector<int32_t>> scap;
   int64_t P_words = 0;  // interval tables of every config and cap level
+  // NEXT-1: configs with a strategy-dependent cut cost (cut[i]), their
+  // boundary-strategy tables T and the K4c results / scratch
+  std::vector<char> cut;
+  int64_t T_words = 0;
+  DevBuf<int32_t> T, zscr;
+  DevBuf<char> cutres;
+  int64_t zstride = 0;
 };
 
 // A prepared problem keeps the launch plan and the captured graph when
@@ -188,7 +195,8 @@ static void update_signature(uniap_handle* h) {
     const CfgDev& d = h->cfg[i];
     const K2Class& k = h->cls[i];
     for (int64_t x : {(int64_t)d.deg, (int64_t)d.c, (int64_t)d.S, (int64_t)d.NSP, (int64_t)d.skip, d.offA, d.offP,
-                      (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C, (int64_t)k.DB})
+                      (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C, (int64_t)k.DB, (int64_t)k.TM,
+                      (int64_t)d.cut, d.offT})
       sg.push_back(x);
   }
   if (h->level2) {
@@ -342,7 +350,8 @@ extern "C" uniap_status uniap_create(uniap_handle** out, int device, void* strea
     static std::vector<int> done;
     std::lock_guard<std::mutex> g(mu);
     if (std::find(done.begin(), done.end(), device) == done.end()) {
-      if (combine_init() != cudaSuccess || builder_init() != cudaSuccess) return UNIAP_ERR_CUDA;
+      if (combine_init() != cudaSuccess || builder_init() != cudaSuccess || cutcombine_init() != cudaSuccess)
+        return UNIAP_ERR_CUDA;
       done.push_back(device);
     }
   }
@@ -374,6 +383,9 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   h->bwp.release();
   h->inst.release();
   h->binst.release();
+  h->T.release();
+  h->zscr.release();
+  h->cutres.release();
   h->iinst.release();
   h->iP.release();
   h->win.release();
@@ -395,7 +407,7 @@ extern "C" void uniap_destroy(uniap_handle* h) {
 }
 
 static void plan_instances(int L, int i, int deg, int S, int skip, bool all_intervals, int ecap, std::vector<Inst>& out);
-static void plan_fast(int L, int i, int deg, int S, int skip, const Levels& lv, std::vector<Inst>& out);
+static void plan_fast(int L, int i, int deg, int S, int skip, const Levels& lv, bool cut, std::vector<Inst>& out);
 
 // ---------------------------------------------------------------------------
 // Layout of the configs in the device arena.
@@ -415,6 +427,8 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
   h->bcls.assign(h->ncfg, K2Class{});
   h->lev.assign(h->ncfg, Levels{});
   h->scap = caps;
+  if ((int)h->cut.size() != h->ncfg) h->cut.assign(h->ncfg, 0);
+  h->T_words = 0;
   int64_t off = 0, poff = 0;
   for (int i = 0; i < h->ncfg; ++i)
     if (!make_levels(deg[i], h->cap, caps[i], h->lev[i]))
@@ -425,12 +439,17 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     // critical path of the step; measured: giving deg = 2's prefix + suffix
     // sweeps the same treatment starves the many-sweep classes of SMs)
     std::vector<Inst> v;
-    plan_fast(L, i, deg[i], S[i], skipc[i], h->lev[i], v);
+    plan_fast(L, i, deg[i], S[i], skipc[i], h->lev[i], h->cut[i], v);
     const bool single = !v.empty() && (deg[i] == 1 || v.size() <= 1);
     const bool few = !v.empty() && v.size() <= 4;  // deg = 2 (prefix + suffix): keep clusters
     K2Class k;
-    if (!k2_pick_class(S[i], h->Q, single, &k, few))
+    if (h->cut[i]) {  // NEXT-1: one-CTA per-strategy emission
+      if (!k2_pick_class_t(S[i], h->Q, &k))
+        FAIL(h, UNIAP_ERR_RANGE, "config %d: a strategy-dependent cut cost needs Q <= %d at |S| = %d", i,
+             S[i] > 12 ? 1024 : 2048, S[i]);
+    } else if (!k2_pick_class(S[i], h->Q, single, &k, few)) {
       FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
+    }
     h->cls[i] = k;
     if (!k2_pick_class(S[i], h->Q, true, &h->bcls[i]) || h->bcls[i].NS != k.NS)
       FAIL(h, UNIAP_ERR_ARG, "no traceback class for |S|=%d Q=%d", S[i], h->Q);
@@ -449,6 +468,9 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     d.offRf = off; off += (int64_t)(L - 1) * NSP * NSP;
     d.offRs = off; off += (int64_t)L * NSP * NSP;
     d.offO = off; off += std::max(4, round4(L - 1));
+    d.cut = h->cut[i];
+    d.offRc = off; off += h->cut[i] ? (int64_t)(L - 1) * NSP * NSP : 0;
+    d.offT = h->T_words; h->T_words += h->cut[i] ? (int64_t)L * L * (NSP + 1) * (NSP + 1) : 0;
     const Levels& lv = h->lev[i];
     d.nlev = lv.nlev;
     for (int l = 0; l < MAXLEV; ++l) d.lcap[l] = l < lv.nlev ? lv.lcap[l] : h->cap;
@@ -514,6 +536,20 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
         osum += x.O[e];
       }
     if (sum > UNIAP_MAX_SUM || osum > UNIAP_MAX_SUM) FAIL(h, UNIAP_ERR_RANGE, "config %d: sum bound exceeds 2^28", i);
+    if (x.Rcut && L > 1) {  // NEXT-1: every o_j <= O[e] + max Rcut[e]; the sum of those bounded like O's
+      if (x.stage_cap) FAIL(h, UNIAP_ERR_ARG, "config %d: Rcut with stage_cap is not supported", i);
+      int64_t csum = 0;
+      for (int e = 0; e < L - 1; ++e) {
+        int64_t mx = 0;
+        for (int k = 0; k < s * s; ++k) {
+          const int32_t r = x.Rcut[(int64_t)e * s * s + k];
+          if (r < 0 || r > UNIAP_MAX_ENTRY) FAIL(h, UNIAP_ERR_RANGE, "config %d: Rcut out of range at edge %d", i, e);
+          mx = std::max<int64_t>(mx, r);
+        }
+        csum += mx + (x.O ? x.O[e] : 0);
+      }
+      if (csum > UNIAP_MAX_SUM) FAIL(h, UNIAP_ERR_RANGE, "config %d: cut-cost sum bound exceeds 2^28", i);
+    }
     S[i] = s; deg[i] = x.deg; c[i] = x.c;
     skc[i] = (x.Rskip && t->skip_src >= 0) ? t->skip_src : -1;
     // strategies with M > cap at every layer can never be part of a solution
@@ -539,6 +575,8 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
         caps[i].push_back(v);
       }
     }
+  h->cut.assign(h->ncfg, 0);  // NEXT-1: a strategy-dependent cut cost matters only with cuts
+  for (int i = 0; i < h->ncfg; ++i) h->cut[i] = t->cfg[i].Rcut && L > 1 && deg[i] >= 2 && deg[i] <= L;
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps);
   if (st != UNIAP_OK) return st;
   // pack the host tables into the device layout (pads: A 0, M cap+1, R 0)
@@ -567,6 +605,11 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
             a[d.offRs + ((int64_t)v * N + k) * N + l] = x.Rskip[((int64_t)v * s + kp[k]) * s + kp[l]];
     if (x.O)
       for (int e = 0; e + 1 < L; ++e) a[d.offO + e] = x.O[e];
+    if (d.cut)
+      for (int e = 0; e + 1 < L; ++e)
+        for (int k = 0; k < sc; ++k)
+          for (int l = 0; l < sc; ++l)
+            a[d.offRc + ((int64_t)e * N + k) * N + l] = x.Rcut[((int64_t)e * s + kp[k]) * s + kp[l]];
   }
   CK(h, cudaSetDevice(h->device));
   CK(h, h->arena.ensure(h->arena_words));
@@ -706,6 +749,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
         caps[i].push_back((int32_t)std::min<int64_t>((m - cl->mem_reserve_bytes) / unit, o->Q - 1));
       }
   }
+  h->cut.assign(h->ncfg, 0);  // (level 2: the built-in cut cost is strategy-independent)
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps);
   if (st != UNIAP_OK) return st;
   h->minM.clear();  // the sweep trim runs on the device (k1f_trim)
@@ -795,15 +839,19 @@ static void plan_instances(int L, int i, int deg, int S, int skip, bool all_inte
 // (column ecap of its state): the prefix sweep under stage 1's, the suffix
 // sweep under the last stage's, and the middle sweeps once per distinct
 // level among the middle stages, starting where a stage of that level can.
-static void plan_fast(int L, int i, int deg, int S, int skip, const Levels& lv, std::vector<Inst>& out) {
+// NEXT-1 (cut): every middle sweep once per first strategy kf (T[a][b][kf][*]),
+// the prefix and suffix sweeps emit per strategy at their open end.
+static void plan_fast(int L, int i, int deg, int S, int skip, const Levels& lv, bool cut, std::vector<Inst>& out) {
   if (deg > L) return;
-  auto fwd = [&](int a, int bmax, int lev) {
+  auto fwd = [&](int a, int bmax, int lev, int kf = -1) {
     if (bmax < a) return;
     const int n = bmax - a + 1, ec = lv.lcap[lev];
     if (skip >= 0 && a <= skip && bmax >= skip + 2) {
-      for (int ks = 0; ks < S; ++ks) out.push_back(Inst{i, a, n, ks, +1, 2, 0, a, bmax, n, lev, ec});
+      for (int ks = 0; ks < S; ++ks)
+        if (kf < 0 || a != skip || ks == kf)  // (the first layer is the skip source: one strategy)
+          out.push_back(Inst{i, a, n, ks, +1, 2, 0, a, bmax, n, lev, ec, kf});
     } else {
-      out.push_back(Inst{i, a, n, -1, +1, 1, 0, a, bmax, n, lev, ec});
+      out.push_back(Inst{i, a, n, -1, +1, 1, 0, a, bmax, n, lev, ec, kf});
     }
   };
   if (deg == 1) {
@@ -822,7 +870,8 @@ static void plan_fast(int L, int i, int deg, int S, int skip, const Levels& lv, 
       int im = -1;                                               // start at a >= i and end at
       for (int st = 1; st <= std::min(a, deg - 2); ++st)         // b <= L - deg + i
         if (lv.lev_of[st] == l) im = st;
-      if (im >= 0) fwd(a, L - deg + im, l);
+      if (im >= 0)
+        for (int kf = cut ? 0 : -1; kf < (cut ? S : 0); ++kf) fwd(a, L - deg + im, l, kf);
     }
   const int amin = deg - 1, b = L - 1;                           // last stage: suffixes
   const int ll = lv.lev_of[deg - 1], ec = lv.lcap[ll];
@@ -838,7 +887,7 @@ static void forward_instances(const uniap_handle* h, int i, bool all_intervals, 
   const CfgDev& d = h->cfg[i];
   const size_t first = out.size();
   if (all_intervals) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, h->cap, out);
-  else plan_fast(h->L, i, d.deg, d.S, d.skip, h->lev[i], out);
+  else plan_fast(h->L, i, d.deg, d.S, d.skip, h->lev[i], h->cut[i], out);
   // Level 1: stop each forward P sweep where it becomes infeasible -- the
   // memory sum of Eq. 5 over the layers swept is at least the running sum of
   // the per-layer minima of the caller's M, so past the first layer where
@@ -865,14 +914,14 @@ static void forward_instances(const uniap_handle* h, int i, bool all_intervals, 
 // LPT over configs by executed chain-DP work (sum over the sweeps of n |S|^2 Q); ties
 // keep the candidate order, the least-loaded (then lowest) rank takes the next.
 static void lpt_shapes(int L, int Q, const std::vector<int>& deg, const std::vector<int>& S,
-                       const std::vector<int>& skip, const std::vector<Levels>& lev, int world,
-                       std::vector<int>& owner) {
+                       const std::vector<int>& skip, const std::vector<Levels>& lev, const std::vector<char>& cut,
+                       int world, std::vector<int>& owner) {
   const int n = (int)deg.size();
   std::vector<int> order(n);
   std::vector<double> w(n);
   for (int i = 0; i < n; ++i) {
     std::vector<Inst> v;
-    plan_fast(L, i, deg[i], S[i], skip[i], lev[i], v);  // the executed sweeps
+    plan_fast(L, i, deg[i], S[i], skip[i], lev[i], cut[i], v);  // the executed sweeps
     double x = 1.0;  // + the combine
     for (auto& e : v) x += (double)e.n * S[i] * S[i] * Q;
     order[i] = i;
@@ -893,18 +942,20 @@ static void lpt_shapes(int L, int Q, const std::vector<int>& deg, const std::vec
 static void lpt(const uniap_handle* h, int world, std::vector<int>& owner) {
   std::vector<int> deg(h->ncfg), S(h->ncfg), sk(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i) { deg[i] = h->cfg[i].deg; S[i] = h->cfg[i].S; sk[i] = h->cfg[i].skip; }
-  lpt_shapes(h->L, h->Q, deg, S, sk, h->lev, world, owner);
+  lpt_shapes(h->L, h->Q, deg, S, sk, h->lev, h->cut, world, owner);
 }
 
 extern "C" uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world, int32_t* owner_out) {
   if (!t || !t->cfg || !owner_out || world < 1 || t->n_cfg < 1 || t->L < 1) return UNIAP_ERR_ARG;
   std::vector<int> deg(t->n_cfg), S(t->n_cfg), sk(t->n_cfg), owner;
   std::vector<Levels> lev(t->n_cfg);
+  std::vector<char> cut(t->n_cfg);
   for (int i = 0; i < t->n_cfg; ++i) {
     deg[i] = t->cfg[i].deg;
     std::vector<int32_t> caps;
     if (t->cfg[i].stage_cap) caps.assign(t->cfg[i].stage_cap, t->cfg[i].stage_cap + deg[i]);
     if (!make_levels(deg[i], t->cap, caps, lev[i])) return UNIAP_ERR_RANGE;
+    cut[i] = t->cfg[i].Rcut && deg[i] >= 2 && deg[i] <= t->L;
     // the strategy count the prepared tables hold (strategies feasible at some layer)
     const uniap_config& x = t->cfg[i];
     if (!x.M || x.n_strat < 1) return UNIAP_ERR_ARG;
@@ -917,7 +968,7 @@ extern "C" uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world,
     S[i] = std::max(S[i], 1);
     sk[i] = (x.Rskip && t->skip_src >= 0) ? t->skip_src : -1;
   }
-  lpt_shapes(t->L, t->cap + 1, deg, S, sk, lev, world, owner);
+  lpt_shapes(t->L, t->cap + 1, deg, S, sk, lev, cut, world, owner);
   for (int i = 0; i < t->n_cfg; ++i) owner_out[i] = owner[i];
   return UNIAP_OK;
 }
@@ -940,7 +991,9 @@ extern "C" uniap_status uniap_shard_assign(uniap_handle* h, int32_t world, int32
 // per-layer synchronisation) -- so it starts on free SMs.
 // ---------------------------------------------------------------------------
 
-static int class_key(const K2Class& k) { return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C + (k.DB ? 0 : 50000); }
+static int class_key(const K2Class& k) {
+  return k.NS * 1000000 + k.V * 100000 + k.T * 10 + k.C + (k.DB ? 0 : 50000) + (k.TM ? 25000 : 0);
+}
 
 // launches group sweeps by kernel class and emission bucket (per-stage caps:
 // a launch emits one cap level's column, a kernel parameter)
@@ -1028,6 +1081,8 @@ static uniap_status enqueue_k2(uniap_handle* h, const std::vector<K2Group>& grp,
                 dcount_per_class ? dcount_per_class + g : nullptr,
                 h->dcfg.p, h->arena.p, Pdev, h->G.p, h->L, h->cap, h->skip,
                 grp[g].ecap >= 0 ? grp[g].ecap : h->cap};
+    args.tmode = grp[g].cls.TM;  // NEXT-1 launches emit into T
+    args.T = h->T.p;
     if (!dcount_per_class) args.tim = h->tim.p;  // forward launches: phase clock
     if (h->trace.p) {  // diagnostics: tag = class shape | forward/backward | group
       const K2Class& k = grp[g].cls;
@@ -1167,6 +1222,15 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   for (auto& g : R.bgrp) max_bw = std::max(max_bw, g.max_inst);
   // device buffers + uploads (outside any graph)
   CK(h, h->P.ensure((size_t)h->P_words));
+  if (h->T_words > 0) {  // NEXT-1: T tables, K4c results and suffix scratch
+    int maxdeg = 1;
+    for (int i = 0; i < h->ncfg; ++i)
+      if (h->cut[i]) maxdeg = std::max(maxdeg, h->cfg[i].deg);
+    h->zstride = (int64_t)(maxdeg + 2) * h->L * (UNIAP_MAX_STRAT + 1);
+    CK(h, h->T.ensure((size_t)h->T_words));
+    CK(h, h->zscr.ensure((size_t)std::max(nl, 1) * h->zstride));
+    CK(h, h->cutres.ensure((size_t)std::max(nl, 1) * sizeof(CutRes)));
+  }
   CK(h, h->inst.ensure(std::max<size_t>(fw.size(), 1)));
   CK(h, h->binst.ensure(max_bw));
   CK(h, h->G.ensure(gmax));
@@ -1206,8 +1270,13 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
 
 static uniap_status enqueue_k4_range(uniap_handle* h, int li0, int cnt, cudaStream_t st) {
   if (cnt <= 0) return UNIAP_OK;
-  CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, li0, cnt, h->L, h->thetas.p, h->ntheta.p, h->vals.p,
-                  h->cfgopt.p, st));
+  if (h->cut[h->plan.local[li0]]) {  // NEXT-1 configs (a group holds only such configs: class TM)
+    CK(h, launch_k4c(h->dcfg.p, h->arena.p, h->T.p, h->cfglist.p, li0, cnt, h->L, h->cfgopt.p, h->cutres.p,
+                     h->zscr.p, h->zstride, st));
+  } else {
+    CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, li0, cnt, h->L, h->thetas.p, h->ntheta.p, h->vals.p,
+                    h->cfgopt.p, st));
+  }
   h->launches++;
   return UNIAP_OK;
 }
@@ -1241,6 +1310,10 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     CK(h, launch_fill(h->P.p, h->P_words, INF, h->st));
   }
   h->launches++;
+  if (h->T_words > 0) {  // NEXT-1 boundary-strategy tables
+    CK(h, launch_fill(h->T.p, h->T_words, INF, h->st));
+    h->launches++;
+  }
 
   {
     // K2 per class on side streams, each followed by the K4 of its configs
@@ -1251,8 +1324,9 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     if (s != UNIAP_OK) return s;
   }
 
-  RecordArgs ra{rec, h->cells, h->relax, h->level2 ? h->work.p : nullptr, h->cells_canon, nl, L, h->cap, h->level2 ? h->qglob.p : nullptr, h->clsid.p,
-                h->binst.p, h->bwp.p, h->gstore.p};
+  RecordArgs ra{rec, h->cells, h->relax, h->level2 ? h->work.p : nullptr, h->cells_canon, nl, L, h->cap,
+                h->level2 ? h->qglob.p : nullptr, h->clsid.p, h->binst.p, h->bwp.p,
+                h->T_words > 0 ? reinterpret_cast<const CutRes*>(h->cutres.p) : nullptr, h->gstore.p};
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
                    h->cfgopt.p, h->scratch.p, h->win.p, ra, h->st));
   h->launches += 1;

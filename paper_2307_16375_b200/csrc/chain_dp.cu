@@ -8,7 +8,7 @@
 namespace uniap {
 
 #define UNIAP_NS_LIST(X) X(1) X(2) X(3) X(4) X(6) X(8) X(10) X(12) X(15) X(16) X(21) X(24) X(32)
-#define UNIAP_EXTERN(N) extern template k2_fn k2_get<N>(int, int, bool, bool);
+#define UNIAP_EXTERN(N) extern template k2_fn k2_get<N>(int, int, bool, bool, bool);
 UNIAP_NS_LIST(UNIAP_EXTERN)
 #undef UNIAP_EXTERN
 
@@ -91,11 +91,22 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few) {
   return true;
 }
 
+bool k2_pick_class_t(int S, int Q, K2Class* out) {
+  const int NS = k2_ns_round(S);
+  if (NS < 0 || Q < 1 || Q > 2048) return false;
+  const int B = std::max(32, pow2ceil(Q));
+  K2Class c{NS, B == 32 ? 1 : (B <= 1024 ? 2 : 4), 0, 1, true, true};
+  c.T = B / c.V;
+  if (smem_words(NS, B) * 4 + (size_t)MAXL * ((NS + 3) & ~3) * 4 > 200 * 1024) return false;
+  *out = c;
+  return true;
+}
+
 static k2_fn k2_lookup(const K2Class& c) {
   const bool CL = c.C > 1;
   switch (c.NS) {
 #define UNIAP_CASE(N) \
-  case N: return k2_get<N>(c.V, c.T, CL, c.DB);
+  case N: return k2_get<N>(c.V, c.T, CL, c.DB, c.TM);
     UNIAP_NS_LIST(UNIAP_CASE)
 #undef UNIAP_CASE
     default: return nullptr;
@@ -127,6 +138,16 @@ int k2_selftest(int* S_out, int* Q_out, int* single_out) {
           return 1;
         }
       }
+  for (int S = 1; S <= UNIAP_MAX_STRAT; ++S)  // NEXT-1 shapes
+    for (int Q = 1; Q <= 2048; Q += (Q < 64 ? 1 : 37)) {
+      K2Class c;
+      if (k2_pick_class_t(S, Q, &c) && !k2_lookup(c)) {
+        *S_out = S;
+        *Q_out = Q;
+        *single_out = 3;
+        return 1;
+      }
+    }
   return 0;
 }
 
@@ -166,13 +187,13 @@ __global__ void k2_closed_s1(const K2Args args, int n_inst) {
 
 cudaError_t k2_launch(const K2Class& c, const K2Args& args, int n_inst, cudaStream_t st, int priority) {
   if (n_inst <= 0) return cudaSuccess;
-  if (c.NS == 1 && !args.n_inst) {  // forward |S| = 1 sweeps: closed form
+  if (c.NS == 1 && !args.n_inst && !c.TM) {  // forward |S| = 1 sweeps: closed form
     k2_closed_s1<<<n_inst, 32, 0, st>>>(args, n_inst);
     return cudaGetLastError();
   }
   k2_fn fn = k2_lookup(c);
   if (!fn) return cudaErrorInvalidDeviceFunction;
-  const size_t smem = k2_smem_bytes(c);
+  const size_t smem = k2_smem_bytes(c) + (c.TM ? (size_t)MAXL * ((c.NS + 3) & ~3) * sizeof(int32_t) : 0);
   {
     // raise the dynamic shared-memory limit (and allow 16-CTA clusters) once
     // per (device, kernel): function attributes are per device

@@ -114,7 +114,9 @@ struct Stage {
   static constexpr int WORDS = NS * NSP + 2 * NSP;
 };
 
-template <int NS, int V, int T, bool CL, bool DB = true>
+// TM: a NEXT-1 launch (per-strategy emission into T, K2Args::tmode); only
+// one-CTA double-buffered shapes are instantiated with it.
+template <int NS, int V, int T, bool CL, bool DB = true, bool TM = false>
 __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   static_assert(DB || !CL, "single-buffered E only without clusters");
   constexpr int B = T * V;          // buckets per CTA
@@ -220,6 +222,14 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
               for (int k = 0; k < NS; ++k) v = min(v, d[k][j]);
           sProw[u] = v;  // written to global after the sweep (no global store
                          // outstanding at the per-layer cluster barrier)
+          if constexpr (TM) {  // NEXT-1: every strategy's state at ecap, flushed after the sweep
+            int32_t* row = sProw + MAXL + u * NSP;
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+              if (j == jc)
+#pragma unroll
+                for (int k = 0; k < NS; ++k) row[k] = d[k][j];
+          }
         }
       }
     }
@@ -247,6 +257,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
         if (u >= skip + 2) a += __ldg(gRs + ((int64_t)u * NSP + ks) * NSP + k);
         if (u == skip && k != ks) m = MBIG;
       }
+      if (in.kf >= 0 && k != in.kf) m = MBIG;  // NEXT-1: the first layer on strategy kf
 #pragma unroll
       for (int j = 0; j < V; ++j) d[k][j] = (rank * B + j * T + t >= m) ? a : INF;
     }
@@ -383,6 +394,21 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       if ((in.emit & 3) == 2) atomicMin(dst, sProw[uu]);
       else *dst = sProw[uu];
     }
+    if constexpr (TM) {  // NEXT-1: T[a][b][kf'][kl'] of the config, index NSP = that end free
+      constexpr int W = NSP + 1;
+      int32_t* Tc = args.T + cf.offT;
+      const int kf = args.inst[ii].kf;
+      for (int uu = in.elo; uu <= in.ehi; ++uu)
+        for (int k = 0; k < NS; ++k) {
+          // forward from a: first = kf (or free), last = k; backward (suffix) from
+          // L-1: first = k, last free
+          const int64_t i = in.dir > 0 ? (((int64_t)in.a * L + uu) * W + (kf < 0 ? NSP : kf)) * W + k
+                                       : (((int64_t)uu * L + in.a) * W + k) * W + NSP;
+          const int32_t v = sProw[MAXL + uu * NSP + k];
+          if ((in.emit & 3) == 2) atomicMin(Tc + i, v);
+          else Tc[i] = v;
+        }
+    }
   }
   if constexpr (CL) cl_sync();  // keep this CTA's E alive for remote readers
   if (args.trace && t == 0) trace_put(args.trace, args.tag, t_start, rank, ii, in.n);
@@ -396,13 +422,36 @@ template <int NS>
 constexpr size_t k2_smem(int B, int ne = 2) {
   return (size_t)(ne * NS * (B + 4) + 3 * Stage<NS>::WORDS + MAXL) * sizeof(int32_t);
 }
+// + the per-strategy rows of a NEXT-1 (tmode) launch
+template <int NS>
+constexpr size_t k2_smem_t() {
+  return (size_t)MAXL * Stage<NS>::NSP * sizeof(int32_t);
+}
 
 // Instantiation helper used by the per-NS translation units: only the shapes
 // the class chooser (chain_dp.cu, k2_pick_class) can return are instantiated.
 typedef void (*k2_fn)(const K2Args);
 
 template <int NS>
-k2_fn k2_get(int V, int T, bool CL, bool DB) {
+k2_fn k2_get(int V, int T, bool CL, bool DB, bool TM) {
+  if (TM) {  // NEXT-1 launches: one CTA per sweep, double-buffered (k2_pick_class_t)
+    if (CL || !DB) return nullptr;
+#define UNIAP_TSHAPE(VV, TT)                                                                   \
+  if (V == VV && T == TT) {                                                                    \
+    if constexpr (k2_smem<NS>(VV * TT) + k2_smem_t<NS>() <= 200 * 1024)                       \
+      return k2_chain<NS, VV, TT, false, true, true>;                                          \
+    return nullptr;                                                                            \
+  }
+    UNIAP_TSHAPE(1, 32)
+    UNIAP_TSHAPE(2, 32)
+    UNIAP_TSHAPE(2, 64)
+    UNIAP_TSHAPE(2, 128)
+    UNIAP_TSHAPE(2, 256)
+    UNIAP_TSHAPE(2, 512)
+    if constexpr (NS <= 12) { UNIAP_TSHAPE(4, 512) }
+#undef UNIAP_TSHAPE
+    return nullptr;
+  }
   if (!DB) {  // single-buffered E, one CTA per instance (large B without a cluster)
     if (CL) return nullptr;
     if constexpr (NS > 24 && k2_smem<NS>(1024, 1) <= 200 * 1024) if (V == 2 && T == 512) return k2_chain<NS, 2, 512, false, false>;

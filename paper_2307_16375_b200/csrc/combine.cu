@@ -487,6 +487,50 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     return;
   }
   const int ci = cfg_list[wl];
+  if (cfgs[ci].cut) {
+    // NEXT-1 winner: K4c found its stage ends and boundary strategies; the
+    // traceback sweeps start at each stage's last layer restricted to its
+    // last strategy, and K5c starts each walk on the stage's first strategy
+    if (t == 0) {
+      const CfgDev* cp = cfgs + ci;
+      const CutRes& X = ra.cutres[wl];
+      const int deg = cp->deg;
+      const bool have = X.status == 1;
+      win->objective = s_opt[0];
+      win->cfg = ci;
+      win->deg = deg;
+      win->c = cp->c;
+      win->S = cp->S;
+      win->NSP = cp->NSP;
+      win->n_theta_star = 0;
+      win->status = have ? 0 : 99;
+      uniap_record* r = ra.rec;
+      if (!have) r->status = X.status == UNIAP_ERR_RANGE ? UNIAP_ERR_RANGE : UNIAP_ERR_INTERNAL;
+      r->objective = s_opt[0];
+      r->cfg_index = ci;
+      r->deg = deg;
+      r->c = cp->c;
+      int n = 0, a = 0;
+      int64_t goff = 0;
+      for (int i = 0; i < deg && have; ++i) {
+        const int b = X.ends[i], len = b - a + 1;
+        win->end[i] = b;
+        win->p[i] = X.p[i];
+        win->o[i] = X.o[i];
+        win->kfirst[i] = X.kfirst[i];
+        win->klast[i] = X.klast[i];
+        const bool cond = cp->skip >= 0 && a <= cp->skip && cp->skip + 2 <= b;
+        for (int ks = cond ? 0 : -1; ks < (cond ? cp->S : 0); ++ks) {
+          ra.bw->gofs[i * 33 + ks + 1] = goff;
+          ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1, len, 0, 0, X.klast[i]};
+          goff += (int64_t)len * cp->NSP * (ra.cap + 1);
+        }
+        a = b + 1;
+      }
+      ra.bw->count[ra.cls_of_cfg[ci]] = n;
+    }
+    return;
+  }
   const CfgDev cf = cfgs[ci];
   const int64_t OPT = s_opt[0];
   const int64_t* V = vals + (int64_t)wl * (TMAX + 2);
@@ -677,6 +721,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     __syncthreads();
   }
   if (t == 0) {
+    for (int i = 0; i < MAXL; ++i) win->kfirst[i] = win->klast[i] = -1;
     win->objective = OPT;
     win->cfg = ci;
     win->deg = deg;
@@ -768,13 +813,14 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
     const int32_t* g = G + bw->gofs[stage * 33 + (ks + 1)];
     int64_t rest = W.p[stage];
     int q = cfgs[W.cfg].lcap[cfgs[W.cfg].lev_of[stage]], kprev = -1;  // the stage's own memory cap (NEXT-2)
+    const int kf0 = W.kfirst[stage];
     int32_t msum = 0;
     ok = true;
     for (int u = a; u <= b && ok; ++u) {
       const int k = lane;
       bool c = false;
       int32_t edge = 0, ap = 0, mk = 0;
-      if (k < S) {
+      if (k < S && (u != a || kf0 < 0 || k == kf0)) {  // (NEXT-1: the stage's first strategy forced)
         mk = M[u * NSP + k];  // per lane, with the other loads: one global round trip per layer
         const int32_t gv = g[((int64_t)(u - a) * NSP + k) * Q + q];
         edge = (u > a) ? Rf[((int64_t)(u - 1) * NSP + kprev) * NSP + k] : 0;

@@ -1,5 +1,5 @@
 // K2 instantiations for NS = 16 strategies (split per NS for parallel compilation).
 #include "chain_dp.cuh"
 namespace uniap {
-template k2_fn k2_get<16>(int, int, bool, bool);
+template k2_fn k2_get<16>(int, int, bool, bool, bool);
 }

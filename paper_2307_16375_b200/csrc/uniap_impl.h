@@ -44,6 +44,12 @@ struct CfgDev {
   // holds one L*L table per level (P_lev[a][b] = optimum of [a,b] under lcap).
   int32_t lcap[MAXLEV];
   int8_t lev_of[MAXL];
+  // NEXT-1 (strategy-dependent cut cost, Eq. 4): cut = 1 when the config has
+  // Rcut [L-1][NSP][NSP] at offRc; its stage tables are then
+  // T[a][b][kf][kl] ((NSP+1)^2 per interval, index NSP = that end free) at
+  // offT in the T arena instead of P
+  int32_t cut, pad2_;
+  int64_t offRc, offT;
 };
 
 // One chain sweep of K2.
@@ -66,6 +72,7 @@ struct Inst {
   int32_t n0;    // the planned length (the layers a placement can use)
   int32_t lev;   // the config's cap level this sweep emits (P block lev, column ecap)
   int32_t ecap;  // = lcap[lev]: the bucket whose state min_k D[k][ecap] is the stage optimum
+  int32_t kf = -1;  // NEXT-1: the first layer swept restricted to strategy kf (-1: free)
 };
 
 struct K2Args {
@@ -77,6 +84,10 @@ struct K2Args {
   int32_t* G;
   int32_t L, cap, skip;
   int32_t ecap;  // emission bucket of this launch's sweeps (their cap level's cap; Inst::ecap)
+  // NEXT-1 launches (tmode = 1): emit every strategy's state at ecap into the
+  // config's T table (CfgDev::offT) instead of the minimum into P
+  int32_t tmode = 0;
+  int32_t* T = nullptr;
   // diagnostics (UNIAP_TRACE): per-CTA timeline records, or nullptr
   unsigned long long* trace = nullptr;
   uint32_t tag = 0;
@@ -153,6 +164,7 @@ struct K2Class {
   int T;       // threads per CTA
   int C;       // CTAs per cluster
   bool DB;     // double-buffered E (one barrier per layer); single: two
+  bool TM = false;  // NEXT-1 launch (per-strategy emission into T)
 };
 
 // chain_dp.cu
@@ -162,6 +174,9 @@ struct K2Class {
 // a critical path, so a bucket range that needs a cluster keeps it rather
 // than folding into one single-buffered CTA (which halves the SMs per sweep).
 bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few = false);
+// The class of a NEXT-1 (tmode) sweep: one CTA of B = pow2ceil(Q) buckets;
+// false when that does not fit (|S| > 12 needs Q <= 1024, else Q <= 2048).
+bool k2_pick_class_t(int S, int Q, K2Class* out);
 int k2_ns_round(int S);
 size_t k2_smem_bytes(const K2Class& c);
 // priority: launch priority (0 = default; lower = served first, see
@@ -174,6 +189,14 @@ struct Winner {
   int64_t objective;  // INT64_MAX if none
   int32_t cfg, deg, c, S, NSP, n_theta_star, status;
   int32_t end[MAXL];
+  int64_t p[MAXL], o[MAXL];
+  int32_t kfirst[MAXL], klast[MAXL];  // NEXT-1: each stage's boundary strategies (-1: free)
+};
+
+// cutcombine.cu (K4c, NEXT-1): per local config the winner data K5a reads
+struct CutRes {
+  int32_t status;  // 1 found, 0 infeasible, UNIAP_ERR_RANGE / UNIAP_ERR_INTERNAL
+  int32_t ends[MAXL], kfirst[MAXL], klast[MAXL];  // stage ends, boundary strategies (-1: free end)
   int64_t p[MAXL], o[MAXL];
 };
 
@@ -193,6 +216,7 @@ struct RecordArgs {          // what K5a writes into the record besides the winn
   const int32_t* cls_of_cfg; // kernel class id per config
   Inst* bw_inst;             // out: backward instances of the winner
   BwPlan* bw;                // out
+  const CutRes* cutres;      // NEXT-1: per local config its K4c result, or nullptr
   // per config: word offset in G of the whole-chain backward sweep's tables
   // kept from the forward phase (deg = 1; per skip conditioning ks consecutive
   // blocks of L * NSP * Q words), or -1 (the traceback runs its own sweep)
@@ -215,6 +239,13 @@ cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P
 cudaError_t launch_k5c_grid(int max_deg, const CfgDev* cfg, const int32_t* arena, const int32_t* G,
                             const BwPlan* bw, const Winner* win, int L, int cap, uniap_record* rec,
                             cudaStream_t st);
+
+// cutcombine.cu (K4c, NEXT-1): CutRes (above) per local config
+cudaError_t launch_k4c(const CfgDev* cfg, const int32_t* arena, const int32_t* T, const int32_t* cfg_list, int li0,
+                       int n, int L, int64_t* cfg_opt, void* res, int32_t* zscratch, int64_t zstride,
+                       cudaStream_t st);
+size_t cut_result_bytes();
+cudaError_t cutcombine_init();
 
 // builder.cu (K1)
 struct ClusterDev {

@@ -42,7 +42,7 @@ def test_library_targets_sm100a_only():
 def test_k2_uses_dpx_viaddmnmx():
     """The chain DP's min-plus relaxation is one DPX VIADDMNMX on sm_100a."""
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
-                          "_ZN5uniap8k2_chainILi10ELi8ELi512ELb0ELb0EEEvNS_6K2ArgsE", pkg.LIB_PATH],
+                          "_ZN5uniap8k2_chainILi10ELi8ELi512ELb0ELb0ELb0EEEvNS_6K2ArgsE", pkg.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert out.count("VIADDMNMX") >= 50
 
