@@ -65,6 +65,7 @@ def test_cut_cost_t5_shaped(h, orc):
     t, qn, _ = orc.build_tables(p)
     rng = np.random.default_rng(5)
     for c in t["cfgs"]:
+        c.pop("stage_cap", None)  # (all at cap here; NEXT-1 is not combined with per-stage caps)
         s, O = c["n_strat"], np.asarray(c["O"], dtype=np.int64)
         c["Rcut"] = (rng.integers(0, 256, size=(t["L"] - 1, s, s)) * (O[:, None, None] // 1024 + 1)).astype(np.int32)
     _same(h.solve_tables(t), orc.solve_tables(t, n_threads=0), "t5 cut")
