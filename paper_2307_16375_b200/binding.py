@@ -244,6 +244,7 @@ def _structs(p):
 
 
 def _result_dict(r, n_cfg, cfg_obj):
+    # (slicing a ctypes array yields a list of Python ints)
     deg = r.deg
     L = r.L
     out = {"objective": r.objective, "cfg_index": r.cfg_index, "deg": deg, "c": r.c,
@@ -252,11 +253,13 @@ def _result_dict(r, n_cfg, cfg_obj):
            "ms_gpu_dp": r.ms_gpu_dp, "ms_gpu_total": r.ms_gpu_total, "h2d_bytes": r.h2d_bytes,
            "d2h_bytes": r.d2h_bytes, "n_launches": r.n_launches, "n_k2_launches": r.n_k2_launches}
     if cfg_obj is not None:
-        out["cfg_objective"] = [int(x) for x in cfg_obj[:n_cfg]]
+        out["cfg_objective"] = cfg_obj[:n_cfg]
     if r.objective != INT64_MAX:
-        out.update({"stage_of": list(r.stage_of[:L]), "strategy_of": list(r.strategy_of[:L]),
-                    "stage_cost": list(r.stage_cost[:deg]), "cut_cost": list(r.cut_cost[:max(deg - 1, 0)]),
-                    "stage_mem": list(r.stage_mem[:deg])})
+        out["stage_of"] = r.stage_of[:L]
+        out["strategy_of"] = r.strategy_of[:L]
+        out["stage_cost"] = r.stage_cost[:deg]
+        out["cut_cost"] = r.cut_cost[:max(deg - 1, 0)]
+        out["stage_mem"] = r.stage_mem[:deg]
     return out
 
 

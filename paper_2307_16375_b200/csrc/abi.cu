@@ -118,7 +118,8 @@ struct uniap_handle {
   int n_edges = 0;
   // device buffers
   DevBuf<int32_t> arena, P, thetas, ntheta, cfglist, scratch, G;
-  DevBuf<int64_t> ns, vals, cfgopt, qcfg, qglob, gofs, qmax, gstore;
+  DevBuf<int64_t> ns, vals, cfgopt, qcfg, gofs, qmax, gstore;
+  View<int64_t> qglob;  // [3] builder quantum / flags / counter: zeroed by each prepare's upload
   // the level-2 profile, config and catalogue arrays: views into ONE device
   // blob filled by one DMA per prepare
   DevBuf<char> upb;
@@ -375,7 +376,7 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->st);
   for (auto* b : {&h->arena, &h->P, &h->thetas, &h->ntheta, &h->cfglist, &h->scratch, &h->G}) b->release();
-  for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->qglob, &h->gofs, &h->qmax, &h->gstore}) b->release();
+  for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->gofs, &h->qmax, &h->gstore}) b->release();
   h->upb.release();
   h->dcfg1.release();
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
@@ -761,20 +762,22 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   CK(h, h->arena.ensure(h->arena_words));
   CK(h, h->ns.ensure(h->arena_words));
   CK(h, h->qcfg.ensure(h->ncfg));
-  CK(h, h->qmax.ensure((size_t)h->ncfg * MAXL * 4));
-  CK(h, h->qglob.ensure(3));
-  CK(h, cudaMemsetAsync(h->qglob.p, 0, 3 * sizeof(int64_t), h->st));
-  CK(h, cudaMemsetAsync(h->qmax.p, 0, (size_t)h->ncfg * MAXL * 4 * sizeof(int64_t), h->st));
+  {  // per-layer maxima of K1 (zeroed again by K1d after each use): zero when (re)allocated
+    int64_t* before = h->qmax.p;
+    CK(h, h->qmax.ensure((size_t)h->ncfg * MAXL * 4));
+    if (h->qmax.p != before) CK(h, cudaMemsetAsync(h->qmax.p, 0, h->qmax.n * sizeof(int64_t), h->st));
+  }
   {  // one pinned staging block -> one device blob, one DMA
-    constexpr int NB = 13;
+    constexpr int NB = 14;  // ... the last block: qglob, zeroed by the same copy (no memset node)
     const size_t sz[NB] = {fwd.size() * 8, act.size() * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8,
                            (size_t)L * 8, std::max<size_t>(ed.size(), 3) * 8, h->ncfg * sizeof(CfgDev),
                            h->ncfg * sizeof(CatDev), std::max<size_t>(rmat.size(), 1) * 8, (size_t)L * 8,
-                           (size_t)L * 8};
+                           (size_t)L * 8, 3 * 8};
     const size_t used[NB] = {sz[0], sz[1], sz[2], sz[3], sz[4], sz[5], sz[6], ed.size() * 8, sz[8], sz[9],
-                             rmat.size() * 8, sz[11], sz[12]};
+                             rmat.size() * 8, sz[11], sz[12], 0};
     const void* src[NB] = {fwd.data(), act.data(), ps.data(), ctx.data(), tpc.data(), chain.data(), skipb.data(),
-                           ed.data(), h->cfg.data(), h->cat.data(), rmat.data(), chain_mat.data(), skip_mat.data()};
+                           ed.data(), h->cfg.data(), h->cat.data(), rmat.data(), chain_mat.data(), skip_mat.data(),
+                           nullptr};
     size_t off[NB], tot = 0;
     for (int i = 0; i < NB; ++i) { off[i] = tot; tot += staged(sz[i]); }
     CK(h, h->upb.ensure(tot));
@@ -790,7 +793,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
     h->skipb.p = (int64_t*)(b + off[6]); h->edges.p = (int64_t*)(b + off[7]);
     h->dcfg.p = (CfgDev*)(b + off[8]); h->dcat.p = (CatDev*)(b + off[9]);
     h->rmat.p = (int64_t*)(b + off[10]); h->chain_mat.p = (int64_t*)(b + off[11]);
-    h->skip_mat.p = (int64_t*)(b + off[12]);
+    h->skip_mat.p = (int64_t*)(b + off[12]); h->qglob.p = (int64_t*)(b + off[13]);
   }
   CK(h, stage_end(h));
   update_signature(h);
