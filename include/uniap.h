@@ -115,8 +115,9 @@ typedef struct {
                                 (O[e] + max Rcut[e]) <= 2^28.  Ties are then broken by
                                 (tpi, deg, c, stage_of, boundary vector, strategy_of), the
                                 boundary vector (k_{e_1}, k_{e_1+1}, k_{e_2}, k_{e_2+1}, ...)
-                                (reading A-31).  Not combined with stage_cap (_ARG); its configs
-                                need Q <= 2048 (Q <= 1024 for |S| > 12), else _RANGE          */
+                                (reading A-31).  Not combined with per-stage caps other than
+                                cap (_ARG); its configs need Q <= 2048 (Q <= 1024 for |S| > 12),
+                                else _RANGE                                                    */
 } uniap_config;
 
 typedef struct {
@@ -175,6 +176,11 @@ typedef struct {
                                          micro-batch b pays b * value.  Entries in [0, 2^46];
                                          borrowed for the call.  NULL: the built-in resharding
                                          formula (reading A-15)                              */
+  const int64_t* cut_ns_per_sample;   /* NULL, or (chain edges only) the strategy-dependent
+                                         cross-stage cost R'_uv of a cut after src (Eq. 4,
+                                         PAPER.md:147-154), ns per sample, same indexing; a
+                                         config with cuts gets Rcut = b * value (NEXT-1, see
+                                         uniap_config.Rcut); not with dev_mem_bytes            */
 } uniap_edge;
 
 typedef struct {
@@ -216,7 +222,8 @@ uniap_status uniap_plan(uniap_handle* h, const uniap_model* m, const uniap_clust
 
 /* The builder's tables (for builder parity tests), per candidate config in
  * order, as int32 blocks
- *    [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1], stage_cap[deg]]
+ *    [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1], stage_cap[deg],
+ *     has_rcut, Rcut[L-1][S][S] if has_rcut]
  * Call with buf == NULL to get *words; then with buf_len >= *words. */
 uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
                                 const uniap_options* o, int32_t* buf, int64_t buf_len, int64_t* words,

@@ -76,7 +76,9 @@ static int validate_tables(const orc_tables* t) {
       for (int i = 0; i < c->deg; ++i)
         if (c->stage_cap[i] < 0 || c->stage_cap[i] > t->cap) return ORC_ERR_ARG;
     if (c->Rcut) {
-      if (c->stage_cap) return ORC_ERR_ARG; /* NEXT-1 and NEXT-2 are not combined */
+      if (c->stage_cap) /* NEXT-1 and NEXT-2 are not combined: caps must all be the common cap */
+        for (int i = 0; i < c->deg; ++i)
+          if (c->stage_cap[i] != t->cap) return ORC_ERR_ARG;
       int64_t csum = 0;
       for (int e = 0; e < L - 1; ++e) {
         int64_t mx = 0;
@@ -1048,9 +1050,18 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
   const int64_t ncat = cat_offset(n, n + 1, o->strategy_space);
   const int64_t* chain_mat[ORC_MAX_L];
   const int64_t* skip_mat[ORC_MAX_L];
-  for (int u = 0; u < L; ++u) chain_mat[u] = skip_mat[u] = NULL;
+  const int64_t* cut_mat[ORC_MAX_L];
+  int any_cut = 0;
+  for (int u = 0; u < L; ++u) chain_mat[u] = skip_mat[u] = cut_mat[u] = NULL;
   for (int e = 0; e < m->n_edges; ++e) {
     const orc_edge* ed = &m->edges[e];
+    if (ed->cut_ns) {
+      if (ed->dst != ed->src + 1) return ORC_ERR_ARG; /* a cut follows a chain edge */
+      for (int64_t j = 0; j < (int64_t)ncat * ncat; ++j)
+        if (ed->cut_ns[j] < 0 || ed->cut_ns[j] > LIM) return ORC_ERR_ARG;
+      cut_mat[ed->src] = ed->cut_ns;
+      any_cut = 1;
+    }
     if (!ed->reshard_ns) continue;
     for (int64_t j = 0; j < (int64_t)ncat * ncat; ++j)
       if (ed->reshard_ns[j] < 0 || ed->reshard_ns[j] > LIM) return ORC_ERR_ARG;
@@ -1075,6 +1086,8 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
     if (n_cand > 4096) return ORC_ERR_ARG;
     cand = cand_buf;
   }
+  /* NEXT-1: a config carries Rcut when some chain edge has a cut matrix and it has cuts */
+#define CUTS(i) (any_cut && cand[2 * (i)] >= 2 && cand[2 * (i)] <= L)
   /* pass 1: sizes and the int64 ns/byte values */
   int64_t words = 0;
   int Ss[4096];
@@ -1083,7 +1096,8 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
     Ss[i] = orc_catalogue(g, o->strategy_space, NULL, 0);
     if (Ss[i] > ORC_MAX_S) return ORC_ERR_RANGE;
     int S = Ss[i];
-    words += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + cand[2 * i];
+    words += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + cand[2 * i] + 1 +
+             (CUTS(i) ? (int64_t)(L - 1) * S * S : 0);
   }
   *words_out = words;
   *n_cfg_out = n_cand;
@@ -1174,7 +1188,21 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
       int64_t cp = (m - cl->mem_reserve) / unit;
       SC[st] = cp > cap ? cap : cp;
     }
-    off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + deg;
+    /* NEXT-1: the strategy-dependent cross-stage cost of each chain edge's
+     * cut, b * the caller's per-sample value (Eq. 4) */
+    int64_t* HR = SC + deg;
+    HR[0] = CUTS(i);
+    int64_t* RC = HR + 1;
+    if (CUTS(i))
+      for (int e = 0; e + 1 < L && st == ORC_OK; ++e)
+        for (int k = 0; k < S; ++k)
+          for (int l = 0; l < S; ++l) {
+            u128 v = cut_mat[e] ? (u128)b * (u128)cut_mat[e][(co + k) * ncat + co + l] : 0;
+            if (v >= NS_LIMIT) st = ORC_ERR_RANGE;
+            RC[((int64_t)e * S + k) * S + l] = (int64_t)v;
+          }
+    off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + deg + 1 +
+           (CUTS(i) ? (int64_t)(L - 1) * S * S : 0);
   }
   /* time quantum (reading A-9): smallest power of two such that every entry
    * fits 2^22 and every config's sums fit 2^28 (or the caller's quantum). */
@@ -1199,13 +1227,17 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
         if (ma > ENTRY_MAX || mr > ENTRY_MAX || ms > ENTRY_MAX) ok = 0;
         sum += ma + mr + ms;
       }
+      const int64_t* RC = O + (L - 1) + cand[2 * i] + 1;
       for (int e = 0; e + 1 < L; ++e) {
-        int64_t x = (O[e] + qn - 1) / qn;
-        if (x > ENTRY_MAX) ok = 0;
-        osum += x;
+        int64_t x = (O[e] + qn - 1) / qn, xr = 0;
+        if (CUTS(i))
+          for (int k = 0; k < S * S; ++k) xr = max64(xr, (RC[(int64_t)e * S * S + k] + qn - 1) / qn);
+        if (x > ENTRY_MAX || xr > ENTRY_MAX) ok = 0;
+        osum += x + xr; /* every o_j <= O + max Rcut (reading A-9 with NEXT-1) */
       }
       if (sum > SUM_MAX || osum > SUM_MAX) ok = 0;
-      off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + cand[2 * i];
+      off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + cand[2 * i] + 1 +
+             (CUTS(i) ? (int64_t)(L - 1) * S * S : 0);
     }
     if (ok) break;
     if (o->quantum_ns) { st = ORC_ERR_RANGE; break; }
@@ -1229,10 +1261,15 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
       int64_t rest = (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1);
       for (int64_t j = 0; j < rest; ++j) out[4 + 2 * nA + j] = (int32_t)((blk[4 + 2 * nA + j] + qn - 1) / qn);
       for (int st = 0; st < cand[2 * i]; ++st) out[4 + 2 * nA + rest + st] = (int32_t)blk[4 + 2 * nA + rest + st];
-      off += 4 + 2 * nA + rest + cand[2 * i];
+      int64_t x0 = 4 + 2 * nA + rest + cand[2 * i];
+      out[x0] = (int32_t)blk[x0]; /* has_rcut */
+      int64_t nrc = CUTS(i) ? (int64_t)(L - 1) * S * S : 0;
+      for (int64_t j = 0; j < nrc; ++j) out[x0 + 1 + j] = (int32_t)((blk[x0 + 1 + j] + qn - 1) / qn);
+      off += x0 + 1 + nrc;
     }
   }
   free(ns);
+#undef CUTS
   return st;
 }
 

@@ -86,6 +86,9 @@ typedef struct {
   const int64_t* reshard_ns; /* NULL, or the edge's resharding matrix R_uv per sample
                                 (PAPER.md:134): [|Cat|][|Cat|] ns, Cat = S(g) of every
                                 divisor g of n ascending, concatenated; R = b * value   */
+  const int64_t* cut_ns;     /* NULL, or (chain edges only) the edge's strategy-dependent
+                                cross-stage cost R'_uv per sample (Eq. 4),
+                                same indexing: a config gets Rcut = b * value (NEXT-1)      */
 } orc_edge;
 typedef struct {
   int32_t n_dev, node_size;
@@ -106,7 +109,9 @@ typedef struct {
 } orc_options;
 
 /* Builder': writes, per candidate config in order, the block
- *   [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1], stage_cap[deg]]
+ *   [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1], stage_cap[deg],
+ *    has_rcut, Rcut[L-1][S][S] if has_rcut]
+ * (has_rcut: some chain edge carries cut_ns and 2 <= deg <= L)
  * into buf (int32).  *n_cfg, *skip_src, *quantum_ns, *words are outputs. */
 int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o,
               int32_t* buf, int64_t buf_len, int32_t* n_cfg, int32_t* skip_src,

@@ -58,7 +58,7 @@ class _Layer(C.Structure):
 
 class _Edge(C.Structure):
     _fields_ = [("src", C.c_int32), ("dst", C.c_int32), ("tensor_bytes", C.c_int64),
-                ("reshard_ns", C.POINTER(C.c_int64))]
+                ("reshard_ns", C.POINTER(C.c_int64)), ("cut_ns", C.POINTER(C.c_int64))]
 
 
 class _Cluster(C.Structure):
@@ -211,14 +211,15 @@ def _marshal_profile(p):
                            ly["tp_comm_bytes_per_sample"])
     E = len(m["edges"])
     edges = (_Edge * max(E, 1))()
+    def _mat(x):
+        if x is None:
+            return None
+        x = np.ascontiguousarray(x, dtype=np.int64).reshape(-1)
+        keep.append(x)
+        return x.ctypes.data_as(C.POINTER(C.c_int64))
     for i, e in enumerate(m["edges"]):
-        mat = e.get("reshard_ns_per_sample")
-        ptr = None
-        if mat is not None:
-            mat = np.ascontiguousarray(mat, dtype=np.int64).reshape(-1)
-            keep.append(mat)
-            ptr = mat.ctypes.data_as(C.POINTER(C.c_int64))
-        edges[i] = _Edge(e["src"], e["dst"], e["tensor_bytes_per_sample"], ptr)
+        edges[i] = _Edge(e["src"], e["dst"], e["tensor_bytes_per_sample"], _mat(e.get("reshard_ns_per_sample")),
+                         _mat(e.get("cut_ns_per_sample")))
     model = _Model(L, layers, E, edges)
     cl = p["cluster"]
     dm = None
@@ -267,8 +268,12 @@ def unpack_buffer(buf, L, cap, skip_src, n_cfg):
         Rs = buf[off:off + L * S * S].reshape(L, S, S); off += L * S * S
         O = buf[off:off + L - 1]; off += L - 1
         SC = buf[off:off + deg]; off += deg
+        has_rcut = int(buf[off]); off += 1
+        RC = None
+        if has_rcut:
+            RC = buf[off:off + (L - 1) * S * S].reshape(L - 1, S, S); off += (L - 1) * S * S
         cfgs.append({"deg": deg, "c": c, "n_strat": S, "g": g, "A": A, "M": M, "R": R,
-                     "Rskip": Rs if skip_src >= 0 else None, "O": O, "stage_cap": SC})
+                     "Rskip": Rs if skip_src >= 0 else None, "O": O, "stage_cap": SC, "Rcut": RC})
     return {"L": L, "cap": cap, "skip_src": skip_src, "cfgs": cfgs}
 
 

@@ -53,7 +53,7 @@ class uniap_layer(C.Structure):
 
 class uniap_edge(C.Structure):
     _fields_ = [("src", C.c_int32), ("dst", C.c_int32), ("tensor_bytes_per_sample", C.c_int64),
-                ("reshard_ns_per_sample", _P64)]
+                ("reshard_ns_per_sample", _P64), ("cut_ns_per_sample", _P64)]
 
 
 class uniap_cluster(C.Structure):
@@ -169,7 +169,8 @@ def _tables(t):
 
 _LAYER_DT = np.dtype([("fwd", np.uint64), ("param", np.int64), ("act", np.uint64), ("ctx", np.int64),
                       ("tpc", np.int64)])
-_EDGE_DT = np.dtype([("src", np.int32), ("dst", np.int32), ("bytes", np.int64), ("mat", np.uint64)])
+_EDGE_DT = np.dtype([("src", np.int32), ("dst", np.int32), ("bytes", np.int64), ("mat", np.uint64),
+                     ("cut", np.uint64)])
 
 
 def _profile(p):
@@ -194,11 +195,12 @@ def _profile(p):
         ed["src"] = [e["src"] for e in m["edges"]]
         ed["dst"] = [e["dst"] for e in m["edges"]]
         ed["bytes"] = [e["tensor_bytes_per_sample"] for e in m["edges"]]
-        for i, e in enumerate(m["edges"]):  # optional per-edge resharding matrix (uniap_edge)
-            if e.get("reshard_ns_per_sample") is not None:
-                mat = np.ascontiguousarray(e["reshard_ns_per_sample"], dtype=np.int64).reshape(-1)
-                mats.append(mat)
-                ed["mat"][i] = mat.ctypes.data
+        for i, e in enumerate(m["edges"]):  # optional per-edge matrices (uniap_edge)
+            for key, col in (("reshard_ns_per_sample", "mat"), ("cut_ns_per_sample", "cut")):
+                if e.get(key) is not None:
+                    mat = np.ascontiguousarray(e[key], dtype=np.int64).reshape(-1)
+                    mats.append(mat)
+                    ed[col][i] = mat.ctypes.data
     cl = p["cluster"]
     dm = None
     if cl.get("dev_mem_bytes") is not None:  # optional per-device memory (heterogeneous devices)
@@ -385,6 +387,12 @@ class Handle:
                 size = int(np.prod(shape))
                 blk[name] = buf[off:off + size].reshape(shape)
                 off += size
+            has_rcut = int(buf[off])
+            off += 1
+            blk["Rcut"] = None
+            if has_rcut:
+                blk["Rcut"] = buf[off:off + (L - 1) * S * S].reshape(L - 1, S, S)
+                off += (L - 1) * S * S
             cfgs.append({"deg": deg, "c": c, "n_strat": S, "g": g, **blk,
                          "Rskip": blk["Rskip"] if skip.value >= 0 else None})
         return {"L": L, "cap": cap, "skip_src": skip.value, "cfgs": cfgs}, qn.value, buf

@@ -123,7 +123,7 @@ struct uniap_handle {
   // the level-2 profile, config and catalogue arrays: views into ONE device
   // blob filled by one DMA per prepare
   DevBuf<char> upb;
-  View<int64_t> fwd, act, ps, ctx, tpc, chain, skipb, edges, rmat, chain_mat, skip_mat;
+  View<int64_t> fwd, act, ps, ctx, tpc, chain, skipb, edges, rmat, chain_mat, skip_mat, cut_mat;
   View<CfgDev> dcfg;
   View<CatDev> dcat;
   DevBuf<CfgDev> dcfg1;  // level 1: the config array (the arena is its own buffer)
@@ -181,6 +181,7 @@ struct uniap_handle {
   // boundary-strategy tables T and the K4c results / scratch
   std::vector<char> cut;
   int64_t T_words = 0;
+  bool any_cut = false;  // level 2: some edge carries a cut matrix
   DevBuf<int32_t> T, zscr;
   DevBuf<char> cutres;
   int64_t zstride = 0;
@@ -209,7 +210,7 @@ static void update_signature(uniap_handle* h) {
                         (const void*)h->tpc.p, (const void*)h->chain.p, (const void*)h->skipb.p,
                         (const void*)h->edges.p, (const void*)h->qcfg.p, (const void*)h->qmax.p,
                         (const void*)h->qglob.p, (const void*)h->rmat.p, (const void*)h->chain_mat.p,
-                        (const void*)h->skip_mat.p})
+                        (const void*)h->skip_mat.p, (const void*)h->cut_mat.p, (const void*)(intptr_t)h->any_cut})
     sg.push_back(reinterpret_cast<int64_t>(p));
   if (sg != h->sig) {
     h->sig.swap(sg);
@@ -538,7 +539,8 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
       }
     if (sum > UNIAP_MAX_SUM || osum > UNIAP_MAX_SUM) FAIL(h, UNIAP_ERR_RANGE, "config %d: sum bound exceeds 2^28", i);
     if (x.Rcut && L > 1) {  // NEXT-1: every o_j <= O[e] + max Rcut[e]; the sum of those bounded like O's
-      if (x.stage_cap) FAIL(h, UNIAP_ERR_ARG, "config %d: Rcut with stage_cap is not supported", i);
+      for (int st = 0; x.stage_cap && st < x.deg; ++st)  // (per-stage caps other than cap: not combined)
+        if (x.stage_cap[st] != t->cap) FAIL(h, UNIAP_ERR_ARG, "config %d: Rcut with per-stage caps is not supported", i);
       int64_t csum = 0;
       for (int e = 0; e < L - 1; ++e) {
         int64_t mx = 0;
@@ -576,6 +578,7 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
         caps[i].push_back(v);
       }
     }
+  h->any_cut = false;
   h->cut.assign(h->ncfg, 0);  // NEXT-1: a strategy-dependent cut cost matters only with cuts
   for (int i = 0; i < h->ncfg; ++i) h->cut[i] = t->cfg[i].Rcut && L > 1 && deg[i] >= 2 && deg[i] <= L;
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps);
@@ -674,7 +677,8 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
     cat_off[g + 1] = cat_off[g] + (n % g == 0 ? uniap_catalogue(g, o->strategy_space, nullptr, 0) : 0);
   const int64_t ncat = cat_off[n + 1];
   int skip = -1;
-  std::vector<int64_t> ed, rmat, chain_mat(L, -1), skip_mat(L, -1);
+  std::vector<int64_t> ed, rmat, chain_mat(L, -1), skip_mat(L, -1), cut_mat(L, -1);
+  bool any_cut = false;
   for (int i = 0; i < m->n_edges; ++i) {
     const uniap_edge& e = m->edges[i];
     if (e.src < 0 || e.dst >= L || e.src >= e.dst || e.tensor_bytes_per_sample < 0 || e.tensor_bytes_per_sample > LIM)
@@ -689,6 +693,17 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
       skipb[e.dst] = e.tensor_bytes_per_sample;
     }
     ed.push_back(e.src); ed.push_back(e.dst); ed.push_back(e.tensor_bytes_per_sample);
+    if (e.cut_ns_per_sample) {  // NEXT-1: a cut after a chain edge only
+      if (e.dst != e.src + 1) FAIL(h, UNIAP_ERR_ARG, "edge %d: a cut matrix on a skip edge", i);
+      if (ncat * ncat > ((int64_t)1 << 24)) FAIL(h, UNIAP_ERR_ARG, "cut matrix too large (|Cat| = %lld)", (long long)ncat);
+      cut_mat[e.src] = (int64_t)rmat.size();
+      any_cut = true;
+      for (int64_t j = 0; j < ncat * ncat; ++j) {
+        const int64_t v = e.cut_ns_per_sample[j];
+        if (v < 0 || v > LIM) FAIL(h, UNIAP_ERR_ARG, "edge %d: cut matrix entry out of [0, 2^46]", i);
+        rmat.push_back(v);
+      }
+    }
     if (e.reshard_ns_per_sample) {
       if (ncat * ncat > ((int64_t)1 << 24)) FAIL(h, UNIAP_ERR_ARG, "resharding matrix too large (|Cat| = %lld)", (long long)ncat);
       (e.dst == e.src + 1 ? chain_mat[e.src] : skip_mat[e.dst]) = (int64_t)rmat.size();
@@ -750,7 +765,14 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
         caps[i].push_back((int32_t)std::min<int64_t>((m - cl->mem_reserve_bytes) / unit, o->Q - 1));
       }
   }
-  h->cut.assign(h->ncfg, 0);  // (level 2: the built-in cut cost is strategy-independent)
+  // NEXT-1 at level 2: configs with cuts get Rcut from the edges' cut matrices
+  h->cut.assign(h->ncfg, 0);
+  for (int i = 0; i < h->ncfg && any_cut; ++i) {
+    h->cut[i] = deg[i] >= 2 && deg[i] <= L;
+    for (size_t st = 0; h->cut[i] && st < caps[i].size(); ++st)
+      if (caps[i][st] != o->Q - 1) FAIL(h, UNIAP_ERR_ARG, "cut matrices with per-stage memory caps are not supported");
+  }
+  h->any_cut = any_cut;
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps);
   if (st != UNIAP_OK) return st;
   h->minM.clear();  // the sweep trim runs on the device (k1f_trim)
@@ -764,20 +786,20 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   CK(h, h->qcfg.ensure(h->ncfg));
   {  // per-layer maxima of K1 (zeroed again by K1d after each use): zero when (re)allocated
     int64_t* before = h->qmax.p;
-    CK(h, h->qmax.ensure((size_t)h->ncfg * MAXL * 4));
+    CK(h, h->qmax.ensure((size_t)h->ncfg * MAXL * 5));
     if (h->qmax.p != before) CK(h, cudaMemsetAsync(h->qmax.p, 0, h->qmax.n * sizeof(int64_t), h->st));
   }
   {  // one pinned staging block -> one device blob, one DMA
-    constexpr int NB = 14;  // ... the last block: qglob, zeroed by the same copy (no memset node)
+    constexpr int NB = 15;  // ... qglob, zeroed by the same copy (no memset node), then the cut offsets
     const size_t sz[NB] = {fwd.size() * 8, act.size() * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8,
                            (size_t)L * 8, std::max<size_t>(ed.size(), 3) * 8, h->ncfg * sizeof(CfgDev),
                            h->ncfg * sizeof(CatDev), std::max<size_t>(rmat.size(), 1) * 8, (size_t)L * 8,
-                           (size_t)L * 8, 3 * 8};
+                           (size_t)L * 8, 3 * 8, (size_t)L * 8};
     const size_t used[NB] = {sz[0], sz[1], sz[2], sz[3], sz[4], sz[5], sz[6], ed.size() * 8, sz[8], sz[9],
-                             rmat.size() * 8, sz[11], sz[12], 0};
+                             rmat.size() * 8, sz[11], sz[12], 0, sz[14]};
     const void* src[NB] = {fwd.data(), act.data(), ps.data(), ctx.data(), tpc.data(), chain.data(), skipb.data(),
                            ed.data(), h->cfg.data(), h->cat.data(), rmat.data(), chain_mat.data(), skip_mat.data(),
-                           nullptr};
+                           nullptr, cut_mat.data()};
     size_t off[NB], tot = 0;
     for (int i = 0; i < NB; ++i) { off[i] = tot; tot += staged(sz[i]); }
     CK(h, h->upb.ensure(tot));
@@ -794,6 +816,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
     h->dcfg.p = (CfgDev*)(b + off[8]); h->dcat.p = (CatDev*)(b + off[9]);
     h->rmat.p = (int64_t*)(b + off[10]); h->chain_mat.p = (int64_t*)(b + off[11]);
     h->skip_mat.p = (int64_t*)(b + off[12]); h->qglob.p = (int64_t*)(b + off[13]);
+    h->cut_mat.p = (int64_t*)(b + off[14]);
   }
   CK(h, stage_end(h));
   update_signature(h);
@@ -1119,8 +1142,8 @@ static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, De
 
 static BuildBufs build_bufs(uniap_handle* h) {
   return BuildBufs{h->fwd.p, h->act.p, h->ps.p, h->ctx.p, h->tpc.p, h->chain.p, h->skipb.p, h->edges.p,
-                   h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->dcat.p, nullptr, nullptr, nullptr, 0, nullptr, h->ns.p,
-                   h->qcfg.p, h->qmax.p, h->qglob.p};
+                   h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->any_cut ? h->cut_mat.p : nullptr,
+                   h->dcat.p, nullptr, nullptr, nullptr, 0, nullptr, h->ns.p, h->qcfg.p, h->qmax.p, h->qglob.p};
 }
 
 // ---------------------------------------------------------------------------
@@ -1537,7 +1560,8 @@ extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m
   const int L = h->L;
   int64_t need = 0;
   for (auto& d : h->cfg)
-    need += 4 + 2 * (int64_t)L * d.S + (int64_t)(L - 1) * d.S * d.S + (int64_t)L * d.S * d.S + (L - 1) + d.deg;
+    need += 4 + 2 * (int64_t)L * d.S + (int64_t)(L - 1) * d.S * d.S + (int64_t)L * d.S * d.S + (L - 1) + d.deg + 1 +
+            (d.cut ? (int64_t)(L - 1) * d.S * d.S : 0);
   if (words) *words = need;
   if (n_cfg) *n_cfg = h->ncfg;
   if (skip_src) *skip_src = h->skip;
@@ -1569,6 +1593,10 @@ extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m
         for (int l = 0; l < S; ++l) buf[w++] = a[d.offRs + ((int64_t)v * N + k) * N + l];
     for (int e = 0; e + 1 < L; ++e) buf[w++] = a[d.offO + e];
     for (int st = 0; st < d.deg; ++st) buf[w++] = h->scap[i].empty() ? h->cap : h->scap[i][st];
+    buf[w++] = d.cut;  // NEXT-1: has_rcut, then Rcut
+    for (int e = 0; d.cut && e + 1 < L; ++e)
+      for (int k = 0; k < S; ++k)
+        for (int l = 0; l < S; ++l) buf[w++] = a[d.offRc + ((int64_t)e * N + k) * N + l];
   }
   return UNIAP_OK;
 }

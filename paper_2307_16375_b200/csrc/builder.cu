@@ -18,6 +18,7 @@ namespace uniap {
 
 typedef unsigned __int128 u128;
 constexpr int64_t NS_LIM = (int64_t)1 << 62;
+constexpr int QMS = 5;  // per (config, layer) maxima: A, R into u, Rskip into u, O[u], max Rcut[u] (NEXT-1)
 
 // (u1 * 2^64 + u0) / v for u1 < v (quotient < 2^64), remainder in *r:
 // two-digit long division in base 2^32 with normalised divisor (Knuth's
@@ -139,7 +140,7 @@ __device__ void k1a_layers(const ClusterDev& cl, const BuildBufs& bb, const CfgD
   const u128 mem = cdiv128((u128)cdt * ps, (u128)(t * f)) + (u128)cf.c * bl * bb.act[u * cl.NT + lt] + (u128)bb.ctx[u];
   A[idx] = checked(a, bb.qglob + 1);
   M[idx] = checked(mem, bb.qglob + 1);
-  amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + u) * 4, A[idx]);
+  amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + u) * QMS, A[idx]);
 }
 
 // K1b: R (edge e = u->u+1), Rskip (edge skip->v) in ns, compacted [k][l]
@@ -202,7 +203,7 @@ __device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const Cfg
     if (j / NSP >= cf.S || j % NSP >= cf.S) dst[j] = 0;
   // per-layer maxima for the quantum: R of edge e goes into layer e+1
   if (mx > 0 && (isR || (cf.skip >= 0 && e >= cf.skip + 2)))
-    amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + (isR ? e + 1 : e)) * 4 + (isR ? 1 : 2), mx);
+    amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + (isR ? e + 1 : e)) * QMS + (isR ? 1 : 2), mx);
 }
 
 // K1c: cut costs: every edge crossing the cut after layer e, fwd + bwd P2P
@@ -223,19 +224,46 @@ __device__ void k1c_cuts(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
     }
     const int64_t v = checked(s, bb.qglob + 1);
     (bb.ns + cf.offO)[e] = v;
-    bb.qmax[((int64_t)blockIdx.y * MAXL + e) * 4 + 3] = v;
+    bb.qmax[((int64_t)blockIdx.y * MAXL + e) * QMS + 3] = v;
   }
 }
 
-// K1a-c in one launch: blockIdx.x selects the role (layers | reshards | cuts),
-// blockIdx.y the config.
+// K1e (NEXT-1): the strategy-dependent cross-stage cost Rcut of chain edge
+// e -> e+1 (Eq. 4): b times the caller's per-sample value
+// of the config's S(g) block (cut_ns_per_sample); 0 for an edge without one;
+// only for configs with cuts (CfgDev::cut).  Every catalogue pair enters the
+// quantum's maxima.
+__device__ void k1e_rcut(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* __restrict__ cfgs, int L, int e) {
+  const CfgDev& cf = cfgs[blockIdx.y];
+  if (!cf.cut) return;
+  const int SF = cf.Sfull, NSP = cf.NSP, n2 = NSP * NSP;
+  int64_t* dst = bb.ns + cf.offRc + (int64_t)e * n2;
+  const int64_t mo = bb.cut_mat[e];
+  const CatDev& cd = bb.cat[blockIdx.y];
+  const int64_t b = cl.B / cf.c;
+  int64_t mx = 0;
+  for (int j = threadIdx.x; j < n2; j += blockDim.x) dst[j] = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < SF * SF && mo >= 0; j += blockDim.x) {
+    const int k = j / SF, l = j - k * SF;
+    const int64_t v = checked((u128)b * (u128)bb.rmat[mo + (int64_t)(cd.co + k) * cd.ncat + cd.co + l], bb.qglob + 1);
+    mx = max(mx, v);
+    const int kc = cf.comp[k], lc = cf.comp[l];
+    if (kc >= 0 && lc >= 0) dst[kc * NSP + lc] = v;
+  }
+  if (mx > 0) amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + e) * QMS + 4, mx);
+}
+
+// K1a-c, K1e in one launch: blockIdx.x selects the role (layers | reshards |
+// cut costs | cuts), blockIdx.y the config.
 constexpr int K1T = 256;
 __global__ void __launch_bounds__(K1T) k1_costs(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L,
-                                                int nbA, int nbR) {
+                                                int nbA, int nbR, int nbE) {
   TraceScope tr(TR_K1);
   const int bx = blockIdx.x;
   if (bx < nbA) k1a_layers(cl, bb, cfgs, L, bx);
   else if (bx < nbA + nbR) k1b_reshard(cl, bb, cfgs, L, bx - nbA);
+  else if (bx < nbA + nbR + nbE) k1e_rcut(cl, bb, cfgs, L, bx - nbA - nbR);
   else k1c_cuts(cl, bb, cfgs, L);
 }
 
@@ -245,13 +273,13 @@ __global__ void __launch_bounds__(K1T) k1_costs(ClusterDev cl, BuildBufs bb, con
 __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int skip) {
   pdl_wait();  // K1's maxima (PDL: launched while K1 drains)
   TraceScope tr(TR_K1D);
-  __shared__ int64_t mx[MAXL * 4];
+  __shared__ int64_t mx[MAXL * QMS];
   __shared__ int okp[64];
   (void)cfgs;
   (void)skip;
   const int t = threadIdx.x;
-  for (int i = t; i < L * 4; i += blockDim.x) {
-    int64_t* q = bb.qmax + (int64_t)blockIdx.x * MAXL * 4 + i;
+  for (int i = t; i < L * QMS; i += blockDim.x) {
+    int64_t* q = bb.qmax + (int64_t)blockIdx.x * MAXL * QMS + i;
     mx[i] = *q;
     *q = 0;  // zero for the next run's atomics (no memset node in the graph)
   }
@@ -269,11 +297,11 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
         // ceil(x / q): a shift for the power-of-two candidates
         auto cq = [&](int64_t x) { return expl ? (x + q - 1) / q : (x + q - 1) >> t; };
         for (int u = 0; u < L; ++u) {
-          const int64_t a = cq(mx[4 * u]), r = cq(mx[4 * u + 1]), s = cq(mx[4 * u + 2]);
-          const int64_t o = u < L - 1 ? cq(mx[4 * u + 3]) : 0;
-          ok = ok && a <= EM && r <= EM && s <= EM && o <= EM;
+          const int64_t a = cq(mx[QMS * u]), r = cq(mx[QMS * u + 1]), s = cq(mx[QMS * u + 2]);
+          const int64_t o = u < L - 1 ? cq(mx[QMS * u + 3]) : 0, rc = u < L - 1 ? cq(mx[QMS * u + 4]) : 0;
+          ok = ok && a <= EM && r <= EM && s <= EM && o <= EM && rc <= EM;
           sum += a + r + s;
-          osum += o;
+          osum += o + rc;  // every o_j <= O + max Rcut (NEXT-1)
         }
         ok = ok && sum <= SM && osum <= SM;
         okp[t] = ok;
@@ -417,10 +445,11 @@ __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restri
   const int cap = cl.Q - 1;
   const int64_t unit = (cl.mem_bytes - cl.mem_reserve) / cap;  // reading A-8
   const int nA = L * NSP, nR = (L - 1) * n2, nS = L * n2, nO = ((L - 1) + 3) & ~3;
+  const int nRc = cf.cut ? (L - 1) * n2 : 0;  // NEXT-1 Rcut block
   const bool pow2 = (q & (q - 1)) == 0;
   const int sh = __ffsll(q) - 1;
   auto qt = [&](int64_t x) { return (int32_t)(pow2 ? (x + q - 1) >> sh : (x + q - 1) / q); };
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nA + nR + nS + nO; idx += nqb * blockDim.x) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nA + nR + nS + nO + nRc; idx += nqb * blockDim.x) {
     int j = idx;
     if (j < nA) { arena[cf.offA + j] = qt(bb.ns[cf.offA + j]); continue; }
     j -= nA;
@@ -439,7 +468,9 @@ __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restri
     j -= nR;
     if (j < nS) { arena[cf.offRs + j] = qt(bb.ns[cf.offRs + j]); continue; }
     j -= nS;
-    arena[cf.offO + j] = j < L - 1 ? qt(bb.ns[cf.offO + j]) : 0;
+    if (j < nO) { arena[cf.offO + j] = j < L - 1 ? qt(bb.ns[cf.offO + j]) : 0; continue; }
+    j -= nO;
+    arena[cf.offRc + j] = qt(bb.ns[cf.offRc + j]);  // NEXT-1 Rcut
   }
 }
 
@@ -449,7 +480,8 @@ cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* c
   // done counter); the range flags qglob[1] are sticky for the prepared input
   const int nbA = (L * 32 + K1T - 1) / K1T;
   const int nbR = 2 * L - 1;  // one block per edge slot: L-1 chain edges, L skip destinations
-  k1_costs<<<dim3(nbA + nbR + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR);
+  const int nbE = bb.cut_mat ? L - 1 : 0;  // NEXT-1 cut-cost blocks (per chain edge)
+  k1_costs<<<dim3(nbA + nbR + nbE + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR, nbE);
   cudaError_t e = pdl_launch(k1d_quantum, dim3(ncfg), dim3(64), 0, st, cl, bb, cfg, L, skip);
   if (e != cudaSuccess) return e;
   e = pdl_launch(k1f_quantise, dim3(16 + (bb.inst ? bb.n_trim : 0), ncfg), dim3(256), 0, st, cl, bb, cfg, L, arena);

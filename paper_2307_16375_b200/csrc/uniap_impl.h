@@ -269,6 +269,7 @@ struct BuildBufs {
   const int64_t* rmat;    // caller resharding matrices (ns per sample), concatenated
   const int64_t* chain_mat;  // [L] word offset into rmat of edge u->u+1's matrix, -1 none
   const int64_t* skip_mat;   // [L] word offset of edge skip->v's matrix, -1 none
+  const int64_t* cut_mat;    // [L] word offset of edge u->u+1's cut matrix (NEXT-1), -1 none; null: none at all
   const CatDev* cat;      // [ncfg]
   Inst* inst;             // the forward instances of the run (K1f writes each P sweep's feasible length)
   const int32_t* inst_off;  // [ncfg + 1] CSR: config i's instances are inst[inst_idx[inst_off[i] ..]]
@@ -277,7 +278,7 @@ struct BuildBufs {
   unsigned long long* work;  // [ncfg][2] executed cells, relaxations of each config's forward sweeps
   int64_t* ns;            // int64 scratch arena, same offsets as the int32 arena
   int64_t* qcfg;          // [ncfg] smallest passing quantum per config
-  int64_t* qmax;          // [ncfg][MAXL][4] per layer: max A, max R into u, max Rskip into u, O[u]
+  int64_t* qmax;          // [ncfg][MAXL][5] per layer: max A, max R into u, max Rskip into u, O[u], max Rcut[u]
   int64_t* qglob;         // [3]: quantum, error flags, completion counter of K1d
 };
 cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* cfg, int ncfg, int L, int skip,

@@ -69,3 +69,31 @@ def test_cut_cost_t5_shaped(h, orc):
         s, O = c["n_strat"], np.asarray(c["O"], dtype=np.int64)
         c["Rcut"] = (rng.integers(0, 256, size=(t["L"] - 1, s, s)) * (O[:, None, None] // 1024 + 1)).astype(np.int32)
     _same(h.solve_tables(t), orc.solve_tables(t, n_threads=0), "t5 cut")
+
+
+@pytest.mark.parametrize("space", [0, 1])
+def test_cut_matrices_at_profile_level(h, orc, space):
+    """uniap_edge.cut_ns_per_sample (R'_uv per sample on chain edges): K1's
+    tables incl. Rcut bit-equal to builder''s, the plan equal to the oracle's."""
+    import paper_2307_16375_b200 as pkg
+    checked = 0
+    for seed in range(30):
+        n = [2, 4, 8][seed % 3]
+        dim = sum(len(orc.catalogue(g, space)) for g in range(1, n + 1) if n % g == 0)
+        p = profiles.random_profile(7000 + seed, n=n, Q=int([16, 64, 256][seed % 3]), mat_dim=dim, space=space)
+        rng = np.random.default_rng(seed)
+        for e in p["model"]["edges"]:
+            if e["dst"] == e["src"] + 1 and rng.random() < 0.7:
+                e["cut_ns_per_sample"] = rng.integers(0, 1 << 20, size=(dim, dim), dtype=np.int64)
+        try:
+            t, qn, buf = orc.build_tables(p)
+        except orc.OracleError as e:
+            with pytest.raises(pkg.UniapError) as ei:
+                h.build_tables(p)
+            assert ei.value.status == e.status
+            continue
+        gt, gq, gbuf = h.build_tables(p)
+        assert gq == qn and np.array_equal(gbuf, buf), seed
+        _same(h.plan(p), orc.solve_tables(t, n_threads=0), seed)
+        checked += 1
+    assert checked > 10

@@ -382,3 +382,28 @@ def test_per_device_memory_gives_per_stage_caps(orc):
     except orc.OracleError as e:
         raised = e.status == 1
     assert raised
+
+
+def test_cut_matrix_gives_per_config_rcut(orc):
+    """NEXT-1 at the profile level: a chain edge's cut_ns_per_sample (R'_uv
+    per sample, Eq. 4) gives every config with cuts Rcut[e] = b * value of its
+    S(g) block; configs without cuts (deg = 1) carry none; the quantum keeps
+    every O + max Rcut within the sum bound.  n = 2, B = 4, cand (2, 2): g = 1,
+    b = 2, Cat = S(1) ++ S(2) -> S(1) block at offset 0: Rcut[0][0][0] =
+    2 * value[0][0]; cand (1, 1) has no cut."""
+    dim = _cat_dim(orc, 2, 0)
+    val = np.arange(dim * dim, dtype=np.int64).reshape(dim, dim) * 10 + 7
+    p = _profile(L=2, n=2, B=4, edges=[(0, 1, 1000)], cand=[(1, 1), (2, 2)], quantum=1, fwd=[1000, 600])
+    p["model"]["edges"][0]["cut_ns_per_sample"] = val
+    t, _, _ = orc.build_tables(p)
+    assert t["cfgs"][0]["Rcut"] is None
+    assert int(t["cfgs"][1]["Rcut"][0][0, 0]) == 2 * 7
+    # a skip edge cannot carry a cut matrix
+    q = _profile(L=3, n=1, B=1, edges=[(0, 1, 10), (1, 2, 10), (0, 2, 10)], quantum=1, fwd=[1000])
+    q["model"]["edges"][2]["cut_ns_per_sample"] = np.zeros((1, 1), dtype=np.int64)
+    try:
+        orc.build_tables(q)
+        raised = False
+    except orc.OracleError as e:
+        raised = e.status == 1
+    assert raised

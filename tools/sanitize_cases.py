@@ -35,8 +35,20 @@ def main(cases):
     if "skip" in cases:  # skip-conditioned copies on clusters, Q = 4096
         t = tables.large_random_tables(7, 8, [10, 6], 4095, [(1, 1), (2, 2)], skip_src=2, mem_max=900)
         same(h.solve_tables(t), oracle.solve_tables(t, n_threads=0), "cluster skip")
+    if "levels" in cases:  # NEXT-2: per-stage caps (cap levels, per-level launches, K4/K5a per level)
+        t = tables.large_random_tables(61, 10, [6, 10, 3], 1023, [(2, 2), (3, 4), (4, 2)], skip_src=3,
+                                       mem_max=300, stage_caps=True)
+        same(h.solve_tables(t), oracle.solve_tables(t, n_threads=0), "stage caps")
+    if "cut" in cases:  # NEXT-1: tmode K2, K4c, conditioned traceback
+        import numpy as np
+        t = tables.large_random_tables(62, 9, [6, 3, 5], 255, [(2, 2), (3, 4), (4, 2)], skip_src=2, mem_max=80,
+                                       vmax=1 << 16)
+        rng = np.random.default_rng(1)
+        for c in t["cfgs"]:
+            c["Rcut"] = rng.integers(0, 1 << 16, size=(8, c["n_strat"], c["n_strat"])).astype(np.int32)
+        same(h.solve_tables(t), oracle.solve_tables(t, n_threads=0), "cut cost")
     h.close()
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["toy", "bert", "cluster", "skip"])
+    main(sys.argv[1:] or ["toy", "bert", "cluster", "skip", "levels", "cut"])
