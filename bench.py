@@ -310,11 +310,11 @@ def main():
             peak_source = (f"derived (MEASURED_ALU.json absent): {SM_COUNT} SMs x {ALU_LANES_PER_SM} alu lanes/clk x "
                            f"{sm_max:.0f} MHz (B300_MICROARCH alu pipe rt=2; DESIGN.md Sec. 4)")
         achieved = relax_local / (statistics.mean(dp_ms) / 1000.0) / 1e12 if dp_ms and dp_ms[0] > 0 else None
-        traffic = None
-        summ = os.path.join(ROOT, "profiles", "ncu_k2_summary.json")
+        traffic = None  # DRAM bytes of one step's forward K2 launches (ncu --set full, profiles/r2)
+        summ = os.path.join(ROOT, "profiles", "r2", f"ncu_summary_{args.workload}.json")
         if os.path.exists(summ):
             try:
-                traffic = json.load(open(summ)).get(f"dram_bytes_per_launch_{args.workload}")
+                traffic = json.load(open(summ)).get(f"dram_bytes_forward_step_{args.workload}")
             except Exception:
                 traffic = None
         line = {
@@ -337,7 +337,9 @@ def main():
                          "peak": peak, "unit": "Trelax/s", "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic,
                          "peak_source": peak_source,
-                         "algorithmic_relax_per_step": relax_local, "k2_ms_per_step": statistics.mean(dp_ms)},
+                         "algorithmic_relax_per_step": relax_local, "k2_ms_per_step": statistics.mean(dp_ms),
+                         "traffic_unit": "DRAM bytes read + written by one step's forward K2 launches (ncu --set "
+                                         "full, cold cache: an upper bound; the tables + P a step needs are < 1 MB)"},
             "clocks": clocks,
             "objective": r["objective"], "plan": {"deg": r["deg"], "c": r["c"]},
         }

@@ -1,7 +1,8 @@
-"""Summarise an ncu --set full report of one bench step into profiles/<round>/.
+"""Summarise ncu --set full reports of one bench step into profiles/<round>/.
 
-usage: python tools/ncu_summary.py gpurun_out/prof_full_llama.ncu-rep profiles/r1/ncu_k2_summary.json llama
-Forward K2 launches = the k2_chain launches between the first k1_costs and the next k5a_winner.
+usage: python tools/ncu_summary.py OUT.json WORKLOAD K2_REPORT [REST_REPORT]
+K2_REPORT: the capture of one step's forward k2_chain launches only
+(tools/profile_r2.sh); REST_REPORT: its K1 / K4 / K5 kernels.
 """
 import csv
 import io
@@ -9,10 +10,21 @@ import json
 import subprocess
 import sys
 
-rep, out, workload = sys.argv[1], sys.argv[2], sys.argv[3]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(raw)))
-hdr, units, data = rows[0], rows[1], rows[2:]
+out, workload, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+rep = reps[0]
+
+
+def load(r):
+    raw = subprocess.run(["ncu", "-i", r, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    return rows[0], rows[1], rows[2:]
+
+
+hdr, units, data = load(rep)
+for r in reps[1:]:
+    h2, u2, d2 = load(r)
+    m = {h: i for i, h in enumerate(h2)}
+    data += [[d[m[h]] if h in m else "" for h in hdr] for d in d2]
 ix = {h: i for i, h in enumerate(hdr)}
 
 
@@ -43,21 +55,17 @@ for d in data:
         "issue_active_pct": f(d, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "warps_active_pct": f(d, "sm__warps_active.avg.pct_of_peak_sustained_active"),
         "top_stalls": {k: round(v, 2) for v, k in top}})
-# forward K2 of one step: k2 launches before the first k5a
-fwd, seen_k1 = [], False
-for k in kernels:
-    if "k1_costs" in k["kernel"]:
-        seen_k1 = True
-    elif "k5a" in k["kernel"] and seen_k1:
-        break
-    elif "k2_chain" in k["kernel"] and seen_k1:
-        fwd.append(k)
+# the first report holds exactly one step's forward k2_chain launches
+fwd = [k for k in kernels if "k2_chain" in k["kernel"]]
 summ = {
-    "workload": workload, "source": rep, "note": "ncu --set full --clock-control none, one bench step; times are "
+    "workload": workload, "source": reps, "note": "ncu --set full --clock-control none, one bench step; times are "
     "serialized and cold-cache (compare shares, not absolutes)",
     "forward_k2_launches": len(fwd),
     "forward_k2_us_serialized": sum(k["us"] for k in fwd),
-    f"dram_bytes_per_launch_{workload}": sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in fwd),
+    # one step's forward K2 launches together (the unit of bench.py's roofline.achieved)
+    f"dram_bytes_forward_step_{workload}": sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in fwd),
+    f"dram_bytes_per_forward_launch_{workload}": (sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in fwd)
+                                                 / max(len(fwd), 1)),
     "kernels": kernels}
 json.dump(summ, open(out, "w"), indent=1)
 print(json.dumps({k: v for k, v in summ.items() if k != "kernels"}))
