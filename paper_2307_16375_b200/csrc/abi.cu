@@ -785,9 +785,9 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   CK(h, h->ns.ensure(h->arena_words));
   CK(h, h->qcfg.ensure(h->ncfg));
   {  // per-layer maxima of K1 (zeroed again by K1d after each use): zero when (re)allocated
-    int64_t* before = h->qmax.p;
+    const size_t nbefore = h->qmax.n;  // (a reallocation may return the same address)
     CK(h, h->qmax.ensure((size_t)h->ncfg * MAXL * 5));
-    if (h->qmax.p != before) CK(h, cudaMemsetAsync(h->qmax.p, 0, h->qmax.n * sizeof(int64_t), h->st));
+    if (h->qmax.n != nbefore) CK(h, cudaMemsetAsync(h->qmax.p, 0, h->qmax.n * sizeof(int64_t), h->st));
   }
   {  // one pinned staging block -> one device blob, one DMA
     constexpr int NB = 15;  // ... qglob, zeroed by the same copy (no memset node), then the cut offsets
