@@ -87,6 +87,7 @@ struct K2Group {
   int max_inst;  // device-sized launches (backward): grid bound
   int priority = 0;  // launch priority (cluster classes and long critical paths first)
   int ecap = -1;     // emission bucket of every sweep of the launch (K2Args::ecap; -1: the cap)
+  int max_deg = 0;   // largest pipeline degree of the group's configs (its K4's stage count)
 };
 
 struct RunPlan {
@@ -117,7 +118,7 @@ struct uniap_handle {
   ClusterDev cl{};
   int n_edges = 0;
   // device buffers
-  DevBuf<int32_t> arena, P, thetas, ntheta, cfglist, scratch, G;
+  DevBuf<int32_t> arena, P, thetas, ends, cfglist, G;
   DevBuf<int64_t> ns, vals, cfgopt, qcfg, gofs, qmax, gstore;
   View<int64_t> qglob;  // [3] builder quantum / flags / counter: zeroed by each prepare's upload
   // the level-2 profile, config and catalogue arrays: views into ONE device
@@ -147,6 +148,7 @@ struct uniap_handle {
   RunPlan plan;                            // launch plan of the last (rank, world)
   DevBuf<int32_t> clsid;
   DevBuf<BwPlan> bwp;
+  DevBuf<long long> k4best;  // K4's running minimum objective of the run (k4_vals)
   DevBuf<unsigned long long> trace;        // UNIAP_TRACE: K2 per-CTA timeline (diagnostics)
   DevBuf<unsigned long long> tim;          // forward K2 phase clock (see K2Args::tim)
   DevBuf<unsigned long long> work;         // level 2: per config executed {cells, relax} (k1f_trim)
@@ -376,13 +378,14 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->st);
-  for (auto* b : {&h->arena, &h->P, &h->thetas, &h->ntheta, &h->cfglist, &h->scratch, &h->G}) b->release();
+  for (auto* b : {&h->arena, &h->P, &h->thetas, &h->ends, &h->cfglist, &h->G}) b->release();
   for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->gofs, &h->qmax, &h->gstore}) b->release();
   h->upb.release();
   h->dcfg1.release();
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   h->clsid.release();
   h->bwp.release();
+  h->k4best.release();
   h->inst.release();
   h->binst.release();
   h->T.release();
@@ -1051,13 +1054,16 @@ static void group_instances(const uniap_handle* h, std::vector<Inst>& all, std::
       ++e;
     }
     grp.push_back(K2Group{s, e, h->cls[sorted[s].cfg], c, 0, 0, sorted[s].ecap});
+    for (size_t x = s; x < e; ++x) grp.back().max_deg = std::max(grp.back().max_deg, h->cfg[sorted[x].cfg].deg);
     s = e;
   }
   std::stable_sort(grp.begin(), grp.end(), [](const K2Group& a, const K2Group& b) { return a.crit > b.crit; });
   // Launch priorities: a cluster launch needs C free SMs of one GPC at once,
   // so once one-CTA classes hold the SMs it starves until they drain; cluster
   // classes therefore get the highest priority, then the longest critical
-  // paths.
+  // paths.  (Running the group with the longest K4 -- the largest deg --
+  // first instead was measured: the bulk class then starts 36 us late and
+  // ends after the chain, Llama +11 %.)
   int least = 0, greatest = 0;
   if (cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess && greatest < least) {
     std::vector<size_t> ord(grp.size());
@@ -1263,10 +1269,14 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   CK(h, h->cfglist.ensure(std::max(nl, 1)));
   CK(h, h->clsid.ensure(h->ncfg));
   CK(h, h->thetas.ensure((size_t)std::max(nl, 1) * TMAX));
-  CK(h, h->ntheta.ensure(std::max(nl, 1)));
-  CK(h, h->vals.ensure((size_t)std::max(nl, 1) * (TMAX + 2)));
+  CK(h, h->ends.ensure((size_t)std::max(nl, 1) * (MAXL + 1)));
+  if (!h->k4best.p) {  // K4's running minimum objective (K5a resets it after every run)
+    CK(h, h->k4best.ensure(1));
+    const long long m = LLONG_MAX;
+    CK(h, h2d(h, h->k4best.p, &m, sizeof m));
+  }
+  CK(h, h->vals.ensure((size_t)std::max(nl, 1) * TMAX));
   CK(h, h->cfgopt.ensure(h->ncfg));
-  CK(h, h->scratch.ensure((size_t)32 * (MAXL + 1) * (MAXL + 1)));
   CK(h, h->win.ensure(1));
   CK(h, h->bwp.ensure(1));
   if (!fw.empty()) CK(h, h2d(h, h->inst.p, fw.data(), fw.size() * sizeof(Inst)));
@@ -1295,15 +1305,21 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
 }
 
 static uniap_status enqueue_k4_range(uniap_handle* h, int li0, int cnt, cudaStream_t st) {
-  if (cnt <= 0) return UNIAP_OK;
-  if (h->cut[h->plan.local[li0]]) {  // NEXT-1 configs (a group holds only such configs: class TM)
-    CK(h, launch_k4c(h->dcfg.p, h->arena.p, h->T.p, h->cfglist.p, li0, cnt, h->L, h->cfgopt.p, h->cutres.p,
-                     h->zscr.p, h->zstride, st));
-  } else {
-    CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, li0, cnt, h->L, h->thetas.p, h->ntheta.p, h->vals.p,
-                    h->cfgopt.p, st));
+  // runs of NEXT-1 configs (K4c over T) and of the others (K4 over P)
+  for (int s = li0, e; s < li0 + cnt; s = e) {
+    const bool cut = h->cut[h->plan.local[s]];
+    int nlev = 1;
+    for (e = s; e < li0 + cnt && (bool)h->cut[h->plan.local[e]] == cut; ++e)
+      nlev = std::max(nlev, h->cfg[h->plan.local[e]].nlev);
+    if (cut) {
+      CK(h, launch_k4c(h->dcfg.p, h->arena.p, h->T.p, h->cfglist.p, s, e - s, h->L, h->cfgopt.p, h->cutres.p,
+                       h->zscr.p, h->zstride, st));
+    } else {
+      CK(h, launch_k4(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, s, e - s, h->L, nlev, h->thetas.p, h->vals.p,
+                      h->ends.p, h->cfgopt.p, h->k4best.p, st));
+    }
+    h->launches++;
   }
-  h->launches++;
   return UNIAP_OK;
 }
 
@@ -1353,8 +1369,8 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   RecordArgs ra{rec, h->cells, h->relax, h->level2 ? h->work.p : nullptr, h->cells_canon, nl, L, h->cap,
                 h->level2 ? h->qglob.p : nullptr, h->clsid.p, h->binst.p, h->bwp.p,
                 h->T_words > 0 ? reinterpret_cast<const CutRes*>(h->cutres.p) : nullptr, h->gstore.p};
-  CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->thetas.p, h->ntheta.p, h->vals.p,
-                   h->cfgopt.p, h->scratch.p, h->win.p, ra, h->st));
+  CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->ends.p, h->cfgopt.p, h->win.p,
+                   h->k4best.p, ra, h->st));
   h->launches += 1;
   // traceback: backward sweeps sized on the device, then the strategy walk
   {

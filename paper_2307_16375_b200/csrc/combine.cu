@@ -12,8 +12,6 @@
 // Val(theta).  The optimal placements are exactly the argmin sets of F_theta
 // over theta with Val(theta) = OPT.  For c = 1, Val =
 // F_theta and the largest theta (no constraint) contains every argmin.
-#include <cub/block/block_scan.cuh>
-
 #include "uniap_impl.h"
 
 namespace uniap {
@@ -61,369 +59,385 @@ cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: sorted distinct theta candidates per config (one CTA per config).
+// K4's placement DPs, CTA-wide.  Placements of deg stages over [0, L-1]:
+// stage i = [a, b] with i-1 <= a <= b <= bhi(i) = L-1-(deg-i), the last
+// stage ends at L-1.  Every stage has n = L - deg + 1 candidate ends (and
+// starts), so a stage is one small min-plus product: thread groups of g
+// lanes own one target (an end b, or a start a), split its sources over the
+// g lanes and reduce with shuffles; one barrier per stage.  (A warp-serial
+// DP measured ~1000 cycles per stage on B200 -- tools/k4_micro.cu -- being
+// bound by the latency of its source loop; here a stage is a few loads and
+// log2(g) shuffles.)  The interval tables are in shared memory, pitch PP =
+// L | 1, one table per cap level (slev[i]: the level of stage i, NEXT-2).
+//  cta_lex: under "every P and O <= theta", the lexicographic minimum of
+//           (sum P + sum O, max(P u O)) over placements: F_theta and the
+//           smallest bottleneck m among its argmin placements.  (sum, max)
+//           pairs under (+, max) with the lexicographic min form a semiring
+//           (x <= y implies x (x) z <= y (x) z), so the stage DP is exact; a
+//           pair is one 64-bit key sum << 32 | max.  With BN it also returns
+//           theta_min = min over placements of max(P u O) (the (min, max)
+//           semiring, unconstrained), the smallest theta with a feasible
+//           placement.
+//  cta_suffix: H_i[a] = min cost of covering [a, L-1] with stages i..deg
+//           under theta (for the greedy of the stage ends).
 // ---------------------------------------------------------------------------
-constexpr int K3T = 1024;
-typedef cub::BlockScan<int, K3T> K3Scan;
-// Sorted distinct theta candidates of config `cf` into v[0..n) (returns n):
-// valid P[a][b] < INF and every O[e].  The values are first de-duplicated in
-// an open-addressing hash set in v (identical layers make most of them
-// equal), compacted with a block scan, then sorted: by rank counting when
-// few (<= 64), else bitonic.  The config's P block and O row are copied to
-// sP / sO on the way (K4 reads them from shared memory).
-constexpr int32_t EMPTY = 0x7fffffff;
-__device__ __forceinline__ void hset_insert(int32_t* v, int32_t x) {
-  uint32_t h = ((uint32_t)x * 2654435761u) >> (32 - 12);  // SORTN = 4096 slots
-  for (;;) {
-    const int32_t old = atomicCAS(v + h, EMPTY, x);
-    if (old == EMPTY || old == x) return;
-    h = (h + 1) & (SORTN - 1);
+__device__ __forceinline__ uint64_t lex_key(uint32_t sum, uint32_t mx) { return (uint64_t)sum << 32 | mx; }
+struct K4Geom {
+  int n, g, q, j;  // candidates per stage, lanes per target, this thread's target and lane in its group
+  __device__ K4Geom(int L, int deg) {
+    // as many lanes per target as the CTA allows (a stage is latency-bound:
+    // fewer sources per lane, a few more shuffle rounds); measured against
+    // an unrolled 8-source loop with 512 threads (issue-bound, 1.6x slower)
+    n = L - deg + 1;
+    g = 32;
+    while (g > 1 && g * n > (int)blockDim.x) g >>= 1;
+    q = threadIdx.x / g;
+    j = threadIdx.x % g;
   }
-}
-__device__ int sort_thetas(const CfgDev& cf, const int32_t* __restrict__ arena, const int32_t* __restrict__ P, int L,
-                           int32_t* v, int32_t* sP, int32_t* sO, typename K3Scan::TempStorage& scan_tmp) {
-  static_assert(SORTN == 4 * K3T, "4 hash slots per thread");
-  const int t = threadIdx.x;
-  for (int i = t; i < SORTN; i += K3T) v[i] = EMPTY;
-  __syncthreads();
-  const int32_t* Pc = P + cf.offP;  // one L*L table per cap level (NEXT-2)
-  for (int idx = t; idx < cf.nlev * L * L; idx += K3T) {
-    const int r = idx % (L * L), a = r / L, b = r - a * L;
-    const int32_t x = Pc[idx];
-    sP[idx] = x;
-    if (a <= b && x < INF) hset_insert(v, x);
-  }
-  const int32_t* O = arena + cf.offO;
-  for (int e = t; e < L - 1; e += K3T) {
-    const int32_t x = O[e];
-    sO[e] = x;
-    hset_insert(v, x);
-  }
-  __syncthreads();
-  int flags[4], c = 0;
-  int32_t vals[4];
-  for (int r = 0; r < 4; ++r) {
-    vals[r] = v[4 * t + r];
-    flags[r] = vals[r] != EMPTY;
-    c += flags[r];
-  }
-  int pos, n;
-  K3Scan(scan_tmp).ExclusiveSum(c, pos, n);
-  __syncthreads();  // every read of v above is done before the compaction writes
-  for (int r = 0; r < 4; ++r)
-    if (flags[r]) v[pos++] = vals[r];
-  __syncthreads();
-  if (n <= 64) {  // rank counting (values are distinct)
-    int32_t x = EMPTY;
-    int rank = 0;
-    if (t < n) {
-      x = v[t];
-      for (int j = 0; j < n; ++j) rank += v[j] < x;
-    }
-    __syncthreads();
-    if (t < n) v[rank] = x;
-    __syncthreads();
-    return n;
-  }
-  int N = 2;
-  while (N < n) N <<= 1;
-  for (int i = n + t; i < N; i += K3T) v[i] = EMPTY;
-  __syncthreads();
-  for (int k = 2; k <= N; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = t; i < N; i += K3T) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool up = (i & k) == 0;
-          const int32_t x = v[i], y = v[ixj];
-          if ((x > y) == up) {
-            v[i] = y;
-            v[ixj] = x;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  return n;
-}
-
-// ---------------------------------------------------------------------------
-// Placement DPs by one warp over (stage i, end b); lanes own b (b = lane,
-// lane + 32).  Stage i = [a, b] with i-1 <= a <= b <= L-1-(deg-i); the last
-// stage ends at L-1.  sP: the config's P[L][L] in shared memory (INF for
-// a > b and for intervals no placement uses), sO: O[L-1], g: 128 words of
-// warp-private scratch holding w[a] = (best placement of stages < i ending
-// at a-1) (+) O[a-1], double-buffered by stage parity.
-//  F:          F_theta = min sum P + sum O over placements with every P, O <=
-//              theta (theta = INF: no limit)   -- (min, +) semiring
-//  BOTTLENECK: the bottleneck min over placements of max(P u O), i.e. the
-//              smallest theta with a feasible placement -- (min, max) semiring
-// The a-loop reads one broadcast w and one conflict-free P word per lane
-// and accumulates with one DPX op (unsigned: INF + INF = 2^31 fits), two
-// accumulators per column for ILP.
-// ---------------------------------------------------------------------------
-// slev[i]: the cap level of stage i (0-based; NEXT-2): stage i reads the
-// interval table sP + slev[i] * L * L.
-template <bool BOTTLENECK, bool MASK>
-__device__ int32_t warp_dp(const int32_t* sPall, const int32_t* slev, const int32_t* sO, int32_t* g, int L, int deg,
-                           int32_t theta) {
-  const int lane = threadIdx.x & 31;
-  const int b0 = lane, b1 = lane + 32;
-  auto mask = [&](int32_t p) { return (MASK && p > theta) ? INF : p; };
-  // w of the next stage from this stage's value c at column b (stage ends at b)
-  auto put_w = [&](int32_t* w, int b, int32_t c) {
-    if (b + 1 < L) {
-      const int32_t o = sO[b];
-      int32_t x;
-      if (BOTTLENECK) x = max(c, o);
-      else x = (c < INF && !(MASK && o > theta)) ? c + o : INF;
-      w[b + 1] = x;
-    }
-  };
-  int32_t c0 = INF, c1 = INF;
-  {  // stage 1 = [0, b], b <= L - deg
-    const int32_t* sP = sPall + slev[0] * L * L;
-    if (b0 < L && b0 <= L - deg) c0 = mask(sP[b0]);
-    if (b1 < L && b1 <= L - deg) c1 = mask(sP[b1]);
-    if (deg > 1) {
-      if (b0 < L) put_w(g, b0, c0);
-      if (b1 < L) put_w(g, b1, c1);
-    }
-  }
-  for (int i = 2; i <= deg; ++i) {
-    __syncwarp();
-    const int32_t* sP = sPall + slev[i - 1] * L * L;
-    const int32_t* w = g + ((i & 1) ? 64 : 0);  // written by stage i-1
-    int32_t* wn = g + ((i & 1) ? 0 : 64);
-    const int blo = (i == deg) ? L - 1 : i - 1, bhi = L - 1 - (deg - i);
-    uint32_t x0 = INF, y0 = INF, x1 = INF, y1 = INF;  // two accumulators per column
-    const bool two = L > 32;
-    int a = i - 1;
-    for (; a + 1 <= bhi; a += 2) {
-      const uint32_t wa = (uint32_t)w[a], wb = (uint32_t)w[a + 1];
-      const uint32_t pa0 = (uint32_t)mask(sP[a * L + b0]), pb0 = (uint32_t)mask(sP[(a + 1) * L + b0]);
-      if (BOTTLENECK) {
-        x0 = min(x0, max(wa, pa0));
-        y0 = min(y0, max(wb, pb0));
-      } else {
-        x0 = __viaddmin_u32(wa, pa0, x0);
-        y0 = __viaddmin_u32(wb, pb0, y0);
-      }
-      if (two) {
-        const uint32_t pa1 = (uint32_t)mask(sP[a * L + b1]), pb1 = (uint32_t)mask(sP[(a + 1) * L + b1]);
-        if (BOTTLENECK) {
-          x1 = min(x1, max(wa, pa1));
-          y1 = min(y1, max(wb, pb1));
-        } else {
-          x1 = __viaddmin_u32(wa, pa1, x1);
-          y1 = __viaddmin_u32(wb, pb1, y1);
-        }
-      }
-    }
-    if (a <= bhi) {
-      const uint32_t wa = (uint32_t)w[a];
-      const uint32_t pa0 = (uint32_t)mask(sP[a * L + b0]);
-      x0 = BOTTLENECK ? min(x0, max(wa, pa0)) : __viaddmin_u32(wa, pa0, x0);
-      if (two) {
-        const uint32_t pa1 = (uint32_t)mask(sP[a * L + b1]);
-        x1 = BOTTLENECK ? min(x1, max(wa, pa1)) : __viaddmin_u32(wa, pa1, x1);
-      }
-    }
-    c0 = (b0 >= blo && b0 <= bhi) ? (int32_t)min(min(x0, y0), (uint32_t)INF) : INF;
-    c1 = (b1 < L && b1 >= blo && b1 <= bhi) ? (int32_t)min(min(x1, y1), (uint32_t)INF) : INF;
-    if (i < deg) {
-      if (b0 < L) put_w(wn, b0, c0);
-      if (b1 < L) put_w(wn, b1, c1);
-    }
-  }
-  const int32_t F = __shfl_sync(0xffffffffu, (L - 1) < 32 ? c0 : c1, (L - 1) & 31);
-  __syncwarp();
-  return F;
-}
-__device__ __forceinline__ int32_t warp_F(const int32_t* sP, const int32_t* slev, const int32_t* sO, int32_t* g, int L,
-                                          int deg, int32_t theta) {
-  return theta >= INF ? warp_dp<false, false>(sP, slev, sO, g, L, deg, INF)
-                      : warp_dp<false, true>(sP, slev, sO, g, L, deg, theta);
-}
-
-// ---------------------------------------------------------------------------
-// K4: Val(theta) of one config per CTA (32 warps), and the config's optimum.
-//  1. F_inf = F at the largest theta (no limit).  c = 1: OPT = F_inf.
-//  2. theta_min, the smallest theta with a feasible placement (F is finite
-//     exactly for theta >= theta_min): one bottleneck (min, max) DP.
-//  3. U = Val(theta_min) bounds OPT, so only theta <= (U - F_inf)/(c-1)
-//     can reach it (Val(theta) >= F_inf + (c-1) theta); those are evaluated
-//     in ascending order by the 32 warps, skipping theta once
-//     F_inf + (c-1) theta > best-so-far (strict: ties stay for the tie-break).
-// Unevaluated entries keep Val = INT64_MAX (> OPT, so never in Theta*).
-// ---------------------------------------------------------------------------
-constexpr int K4W = 32;
-struct K4Smem {
-  int32_t v[SORTN];  // sorted distinct thetas (K3)
-  int32_t sP[MAXLEV * MAXL * MAXL];  // the config's interval tables, one per cap level
-  int32_t slev[MAXL];                // cap level of each stage
-  int32_t sO[MAXL];
-  int32_t g[K4W][128];
-  int32_t probeF[K4W];
-  int32_t cnt, s_hi;
-  unsigned long long s_best;
-  typename K3Scan::TempStorage scan_tmp;
 };
-
-__global__ void __launch_bounds__(K4W * 32) k4_vals(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
-                                                   const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
-                                                   int li0, int L, int32_t* __restrict__ thetas,
-                                                   int32_t* __restrict__ ntheta, int64_t* __restrict__ vals,
-                                                   int64_t* __restrict__ cfg_opt) {
-  TraceScope tr(TR_K4 | (uint32_t)li0 << 8);
-  extern __shared__ __align__(16) unsigned char k4raw[];
-  K4Smem& S = *reinterpret_cast<K4Smem*>(k4raw);
-  int32_t* sP = S.sP;
-  int32_t* sO = S.sO;
-  int32_t* probeF = S.probeF;
-  int& s_hi = S.s_hi;
-  unsigned long long& s_best = S.s_best;
-  auto g = S.g;
-  const int li = li0 + blockIdx.x;
-  const CfgDev cf = cfgs[cfg_list[li]];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // K3 fused: the sorted distinct theta candidates (also kept for K5a)
-  for (int i = threadIdx.x; i < MAXL; i += blockDim.x)  // (from global: no local copy of cf; visible after
-    S.slev[i] = cfgs[cfg_list[li]].lev_of[i];           //  sort_thetas' first barrier)
-  const int nt = sort_thetas(cf, arena, P, L, S.v, sP, sO, S.scan_tmp);
-  const int32_t* slev = S.slev;
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) thetas[(int64_t)li * TMAX + i] = S.v[i];
-  if (threadIdx.x == 0) ntheta[li] = nt;
-  int64_t* V = vals + (int64_t)li * (TMAX + 2);  // [0..nt) Val, [TMAX] F_inf, [TMAX+1] opt
-  const int32_t* th = S.v;
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) V[i] = INT64_MAX;
-  if (cf.deg > L || nt == 0) {  // Eq. 7b cannot hold (reading A-22)
-    if (threadIdx.x == 0) { V[TMAX] = INT64_MAX; cfg_opt[cfg_list[li]] = INT64_MAX; }
-    return;
+template <typename T>
+__device__ __forceinline__ T group_min(T v, int g) {
+  for (int o = 1; o < g; o <<= 1) {
+    const T x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = x < v ? x : v;
   }
-  const int64_t cm1 = cf.c - 1;
-  if (nt <= K4W && cf.c > 1) {
-    // few candidates: every F_theta in one round, one warp each (the
-    // largest theta bounds every P and O, so F of it is F_inf)
-    if (w < nt) {
-      const int32_t F = warp_F(sP, slev, sO, g[w], L, cf.deg, w == nt - 1 ? INF : S.v[w]);
-      if (lane == 0) probeF[w] = F;
+  return v;
+}
+__device__ __forceinline__ int32_t group_max(int32_t v, int g) {
+  for (int o = 1; o < g; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// W: [2][MAXL + 1] keys (w of a stage: the best placement of the stages
+// before it ending at a - 1, plus O[a - 1]); Wb: [2][MAXL + 1] bottleneck
+// values (BN).  Returns (F, m), or (INF, INF) when infeasible; *tmin (BN).
+template <bool BN>
+__device__ int2 cta_lex(const int32_t* sPall, const int32_t* slev, const int32_t* sO, uint64_t* W, int32_t* Wb, int L,
+                        int PP, int deg, int32_t theta, int32_t* tmin) {
+  const K4Geom G(L, deg);
+  const uint32_t lim = (uint32_t)min(theta, INF - 1);  // P = INF: no interval
+  // An unusable w or P enters as sum INF: every key with sum >= INF (INF +
+  // INF < 2^32) is larger than every valid key and is dropped at the stage
+  // end, so the source loop is branch-free.
+  const uint64_t KBAD = lex_key(INF, 0);
+  __shared__ uint64_t s_res;
+  __shared__ int32_t s_bn;
+  auto put = [&](uint64_t* wn, int32_t* wbn, int b, uint64_t c, int32_t cb) {
+    // w of the next stage at b + 1 from this stage's key c at end b
+    const uint32_t o = (uint32_t)sO[b];
+    const uint32_t sum = (uint32_t)(c >> 32) + o;
+    wn[b + 1] = (o <= (uint32_t)theta && sum < (uint32_t)INF) ? lex_key(sum, max((uint32_t)c, o)) : KBAD;
+    if (BN) wbn[b + 1] = max(cb, sO[b]);
+  };
+  // stage 1 = [0, b], b <= L - deg
+  {
+    const int32_t* sP = sPall + slev[0] * L * PP;
+    for (int b = threadIdx.x; b <= L - deg; b += blockDim.x) {
+      const uint32_t p = (uint32_t)sP[b];
+      const uint64_t c = p <= lim ? lex_key(p, p) : KBAD;
+      if (deg > 1) put(W, Wb, b, c, sP[b]);
+      else if (b == L - 1) { s_res = c; if (BN) s_bn = sP[b]; }
+    }
+  }
+  __syncthreads();
+  for (int i = 2; i <= deg; ++i) {
+    const int32_t* sP = sPall + slev[i - 1] * L * PP;
+    const uint64_t* w = W + ((i & 1) ? MAXL + 1 : 0);  // written by stage i-1
+    uint64_t* wn = W + ((i & 1) ? 0 : MAXL + 1);
+    const int32_t* wb = Wb + ((i & 1) ? MAXL + 1 : 0);
+    int32_t* wbn = Wb + ((i & 1) ? 0 : MAXL + 1);
+    const int lo = i - 1;
+    // this group's end (the last stage ends at L-1: group 0 writes it); a
+    // thread of no group runs an empty source loop but joins the shuffles
+    const bool mine = G.q < G.n && (i < deg || G.q == 0);
+    const int b = (i == deg) ? L - 1 : lo + G.q;
+    const int aend = mine ? b : lo - 1;
+    uint64_t acc = KBAD;
+    int32_t accb = INF;
+    for (int a = lo + G.j; a <= aend; a += G.g) {
+      const uint64_t wa = w[a];
+      const int32_t p = sP[a * PP + b];
+      const uint32_t pe = (uint32_t)p <= lim ? (uint32_t)p : (uint32_t)INF;
+      acc = min(acc, lex_key((uint32_t)(wa >> 32) + pe, max((uint32_t)wa, pe)));
+      if (BN) accb = min(accb, max(wb[a], p));
+    }
+    acc = group_min(acc, G.g);
+    if (BN) accb = group_min(accb, G.g);
+    if (mine && G.j == 0) {
+      if ((acc >> 32) >= (uint64_t)INF) acc = KBAD;
+      if (i < deg) put(wn, wbn, b, acc, accb);
+      else { s_res = acc; if (BN) s_bn = accb; }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      const int32_t Finf = probeF[nt - 1];
-      int64_t best = INT64_MAX;
-      for (int i = 0; i < nt; ++i)
-        if (Finf < INF && probeF[i] < INF) {
-          const int64_t val = (int64_t)probeF[i] + cm1 * S.v[i];
-          V[i] = val;
-          best = min(best, val);
+  }
+  const uint64_t F = s_res;
+  if (BN) *tmin = s_bn;
+  __syncthreads();  // (s_res reused by the next call)
+  // sums reaching INF are infeasible (the builder's quantum keeps every
+  // placement sum of a valid input below it)
+  return (F >> 32) >= (uint64_t)INF ? make_int2(INF, INF) : make_int2((int32_t)(F >> 32), (int32_t)(uint32_t)F);
+}
+
+// H: [deg + 1][L + 1]; entries of stage i are written for a in [i-1, bhi(i)],
+// exactly the ones the greedy reads.
+__device__ void cta_suffix(const int32_t* sPall, const int32_t* slev, const int32_t* sO, int32_t* H, int L, int PP,
+                           int deg, int32_t theta) {
+  const K4Geom G(L, deg);
+  {
+    const int32_t* Pd = sPall + slev[deg - 1] * L * PP;
+    for (int a = deg - 1 + (int)threadIdx.x; a < L; a += blockDim.x) {
+      const int32_t p = Pd[a * PP + L - 1];
+      H[deg * (L + 1) + a] = p <= theta ? p : INF;
+    }
+  }
+  __syncthreads();
+  for (int i = deg - 1; i >= 1; --i) {
+    // H_i[a] = min_b P_i[a][b] + O[b] + H_{i+1}[b+1], a <= b <= bhi
+    const int bhi = L - 1 - (deg - i);
+    const int32_t* Pi = sPall + slev[i - 1] * L * PP;
+    const int32_t* Hn = H + (i + 1) * (L + 1);
+    const int a = i - 1 + G.q;  // (a > bhi for a thread of no group: empty loop, joins the shuffles)
+    uint32_t x = INF;
+    for (int b = a + G.j; b <= bhi; b += G.g) {
+      const int32_t p = Pi[a * PP + b], o = sO[b], h = Hn[b + 1];
+      const uint32_t wv = (o <= theta && h < INF) ? (uint32_t)(o + h) : INF;
+      x = __viaddmin_u32(wv, p <= theta ? (uint32_t)p : INF, x);
+    }
+    x = group_min(x, G.g);
+    if (G.q < G.n && G.j == 0) H[i * (L + 1) + a] = (int32_t)min(x, (uint32_t)INF);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4 (with K3): the config's optimum OPT = min over theta of Val(theta) =
+// F_theta + (c-1) theta, and its lexicographically largest stage-end vector
+// over the optimal placements (= smallest stage_of, reading A-11).  One CTA
+// per config, on the stream of the config's forward group, so every config's
+// ends are ready when K5a picks the winner.
+//
+// 1. Descent over the bottlenecks: theta_0 = INF; at theta_j, cta_lex gives
+//    F_j = F_{theta_j} and m_j <= theta_j, the smallest max(P u O) of a
+//    placement attaining F_j.  For theta in [m_j, theta_j] that placement is
+//    feasible and optimal, so F_theta = F_j and Val(theta) = F_j + (c-1)
+//    theta is smallest at theta = m_j (strictly, c > 1): record (m_j,
+//    Val(m_j)), then continue at theta_{j+1} = m_j - 1 (integer costs).
+//    Below theta_{j+1}, F_theta >= F_j and theta >= theta_min, so once
+//    F_j + (c-1) theta_min > best no theta below can reach OPT (strict: ties
+//    are kept for the tie-break).  The recorded m_j therefore include every
+//    theta with Val(theta) = OPT (Theta*) and each Val(m_j) is exact; no
+//    candidate list, sort or scan.  The number of steps is the number of
+//    (sum, max) Pareto points visited: 2 for every Llama-like config, <= 9 on
+//    the T5-like profile.  c = 1: Val = F_theta, OPT = F_INF, Theta* = {INF}.
+// 2. Per theta in Theta*: the suffix DP H (cta_suffix), then the greedy
+//    largest end of each stage (warp 0, a ballot over the ends) that still
+//    reaches F_theta = OPT - (c-1) theta; the lexicographically largest end
+//    vector over Theta* wins.
+// Out: cfg_opt[config]; ends[li] = {ok, end of stage 1, ..., end of stage deg};
+// thetas / vals: the descent's (m_j, Val(m_j)) (scratch).
+// Dynamic shared memory: the interval tables (one per cap level, odd pitch
+// L | 1), then H.
+// ---------------------------------------------------------------------------
+constexpr int K4T = 256;  // threads per K4 CTA
+constexpr int K4EW = MAXL + 1;  // words per config in `ends`
+// (+ 64 words of slack after H)
+size_t k4_smem(int L, int nlev) { return (size_t)(nlev * L * (L | 1) + (L + 1) * (L + 1) + 64) * sizeof(int32_t); }
+__device__ __forceinline__ void cp_async4(int32_t* dst, const int32_t* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__global__ void __launch_bounds__(K4T) k4_vals(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
+                                               const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
+                                               int li0, int L, int32_t* __restrict__ thetas,
+                                               int64_t* __restrict__ vals, int32_t* __restrict__ ends,
+                                               int64_t* __restrict__ cfg_opt, long long* __restrict__ best_obj) {
+  TraceScope tr(TR_K4 | (uint32_t)li0 << 8);
+  extern __shared__ __align__(16) int32_t k4dyn[];
+  __shared__ int32_t slev[MAXL], sO[MAXL], cur[MAXL];
+  __shared__ uint64_t W[2 * (MAXL + 1)];
+  __shared__ int32_t Wb[2 * (MAXL + 1)];
+  const int li = li0 + blockIdx.x;
+  const int ci = cfg_list[li];
+  const CfgDev& cf = cfgs[ci];
+  const int deg = cf.deg;
+  const int64_t cm1 = cf.c - 1;
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  int32_t* E = ends + (int64_t)li * K4EW;
+  int64_t* V = vals + (int64_t)li * TMAX;
+  int32_t* th = thetas + (int64_t)li * TMAX;
+  if (deg > L) {  // Eq. 7b cannot hold (reading A-22)
+    if (t == 0) { E[0] = 0; cfg_opt[ci] = INT64_MAX; }
+    return;
+  }
+  if (deg == 1) {  // one placement [0, L-1]: tpi = p + (c-1) p
+    if (t == 0) {
+      const int32_t p = P[cf.offP + (int64_t)cf.lev_of[0] * L * L + (L - 1)];
+      E[0] = p < INF;
+      E[1] = L - 1;
+      cfg_opt[ci] = p < INF ? (int64_t)p + cm1 * p : INT64_MAX;
+      tr.extra = 1;
+    }
+    return;
+  }
+  if (deg == L) {  // one placement, every layer a stage: tpi = sum P + sum O + (c-1) max(P u O)
+    if (w == 0) {
+      int64_t sum = 0;
+      int32_t mx = 0;
+      bool ok = true;
+      for (int a = lane; a < L; a += 32) {
+        const int32_t p = P[cf.offP + (int64_t)cf.lev_of[a] * L * L + (int64_t)a * L + a];
+        const int32_t o = a < L - 1 ? arena[cf.offO + a] : 0;
+        ok = ok && p < INF;
+        sum += (int64_t)p + o;
+        mx = max(mx, max(p, o));
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      ok = __all_sync(0xffffffffu, ok) && sum < INF;  // (a sum reaching INF is infeasible, as in cta_lex)
+      for (int a = lane; a < L; a += 32) E[1 + a] = a;
+      if (lane == 0) {
+        E[0] = ok;
+        cfg_opt[ci] = ok ? sum + cm1 * mx : INT64_MAX;
+        tr.extra = 1;
+      }
+    }
+    return;
+  }
+  const int PP = L | 1;
+  const int nlev = cf.nlev;
+  int32_t* sP = k4dyn;                   // [nlev][L][PP]
+  int32_t* H = k4dyn + nlev * L * PP;    // [deg + 1][L + 1]
+  {  // asynchronous copies (LDGSTS): every load of the tables in flight at once
+    const int32_t* Pc = P + cf.offP;
+    for (int r = w; r < nlev * L; r += K4T / 32)  // row r = level * L + a
+      for (int b = lane; b < L; b += 32) cp_async4(sP + r * PP + b, Pc + (int64_t)r * L + b);
+    for (int i = t; i < L - 1; i += K4T) cp_async4(sO + i, arena + cf.offO + i);
+  }
+  for (int i = t; i < MAXL; i += K4T) slev[i] = cf.lev_of[i];
+  cp_async_wait_all();
+  __syncthreads();
+  // diagnostics (UNIAP_TRACE): a record per phase, from the kernel's start
+  auto phase = [&](uint32_t kind) {
+    if (g_trace && t == 0) trace_put(g_trace, 0x80000000u | kind | (uint32_t)li0 << 8, tr.t0, 0, blockIdx.x, 0);
+  };
+  phase(9);  // tables loaded
+  // ---- 1. OPT and the candidates of Theta* ----
+  int32_t tmin = 0;
+  int2 fm = cm1 > 0 ? cta_lex<true>(sP, slev, sO, W, Wb, L, PP, deg, INF, &tmin)
+                    : cta_lex<false>(sP, slev, sO, W, Wb, L, PP, deg, INF, nullptr);
+  const int32_t Finf = fm.x;
+  int64_t best = Finf < INF ? (int64_t)Finf : INT64_MAX;
+  int n = 0;
+  if (Finf < INF && cm1 > 0) {
+    best = INT64_MAX;
+    for (;;) {  // (uniform: every thread holds the same fm)
+      const int64_t val = (int64_t)fm.x + cm1 * fm.y;
+      if (t == 0) { th[n] = fm.y; V[n] = val; }
+      ++n;
+      best = min(best, val);
+      if ((int64_t)fm.x + cm1 * tmin > best || fm.y <= tmin || n == TMAX) break;
+      fm = cta_lex<false>(sP, slev, sO, W, Wb, L, PP, deg, fm.y - 1, nullptr);
+      if (fm.x >= INF) break;
+    }
+  }
+  const int64_t OPT = best;
+  __shared__ int s_skip;
+  if (t == 0) {
+    cfg_opt[ci] = OPT;
+    tr.extra = (uint32_t)n;
+    // the running minimum over the configs whose K4 got here first: a config
+    // strictly worse than one of them cannot be the winner (K5a's key is
+    // (objective, deg, c)), so its stage ends are not needed.  The winner
+    // always finds the minimum >= its own objective and computes them.
+    s_skip = OPT == INT64_MAX || (long long)OPT > atomicMin(best_obj, (long long)OPT);
+  }
+  __syncthreads();
+  phase(10);  // OPT and Theta* known
+  if (s_skip) {
+    if (t == 0) E[0] = 0;
+    return;
+  }
+  // ---- 2. the lexicographically largest stage ends over Theta* ----
+  const int nst = cm1 > 0 ? n : 1;
+  bool have = false;  // (thread 0: the best vector so far is E[1..deg])
+  for (int j = 0; j < nst; ++j) {
+    __syncthreads();  // th / V of the descent (thread 0) visible; H free
+    if (cm1 > 0 && V[j] != OPT) continue;  // (uniform)
+    const int32_t theta = cm1 > 0 ? th[j] : INF;
+    const int64_t F_target = OPT - cm1 * (cm1 > 0 ? theta : 0);
+    cta_suffix(sP, slev, sO, H, L, PP, deg, theta);
+    phase(14);  // H of this theta
+    if (w == 0) {
+      bool ok = (int64_t)H[1 * (L + 1) + 0] == F_target;
+      // greedy: the largest end of each stage that still reaches F_target
+      int64_t pre = 0;
+      int a = 0;
+      for (int i = 1; i < deg && ok; ++i) {
+        const int32_t* Pi = sP + slev[i - 1] * L * PP;
+        const int32_t* Hn = H + (i + 1) * (L + 1);
+        int found = -1;
+        for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
+          const int b = b0 - lane;
+          bool c = false;
+          if (b >= a) {
+            const int32_t p = Pi[a * PP + b], o = sO[b], hh = Hn[b + 1];
+            c = p <= theta && o <= theta && hh < INF && pre + p + o + hh == F_target;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, c);
+          if (m) found = b0 - (__ffs(m) - 1);
         }
-      V[TMAX] = Finf >= INF ? INT64_MAX : (int64_t)Finf;
-      cfg_opt[cfg_list[li]] = Finf >= INF ? INT64_MAX : best;
-      tr.extra = (uint32_t)nt | (uint32_t)nt << 12;
+        if (found < 0) { ok = false; break; }
+        if (lane == 0) cur[i - 1] = found;
+        pre += Pi[a * PP + found] + sO[found];
+        a = found + 1;
+      }
+      __syncwarp();
+      if (lane == 0 && ok) {  // keep the lexicographically largest end vector
+        cur[deg - 1] = L - 1;
+        bool better = !have;
+        for (int i = 0; i < deg && !better; ++i)
+          if (cur[i] != E[1 + i]) { better = cur[i] > E[1 + i]; break; }
+        if (better)
+          for (int i = 0; i < deg; ++i) E[1 + i] = cur[i];
+        have = true;
+      }
     }
-    return;
+    phase(15);  // ends of this theta
   }
-  // 1. F_inf (warp 0) and the bottleneck theta_min (warp 1)
-  if (w == 0) {
-    const int32_t F = warp_F(sP, slev, sO, g[0], L, cf.deg, INF);
-    if (lane == 0) probeF[0] = F;
-  } else if (w == 1) {
-    const int32_t Bm = warp_dp<true, false>(sP, slev, sO, g[1], L, cf.deg, INF);
-    if (lane == 0) probeF[1] = Bm;
-  }
-  __syncthreads();
-  const int32_t Finf = probeF[0];
-  if (Finf >= INF || cf.c == 1) {
-    if (threadIdx.x == 0) {
-      V[TMAX] = Finf >= INF ? INT64_MAX : (int64_t)Finf;
-      cfg_opt[cfg_list[li]] = V[TMAX];
-    }
-    return;
-  }
-  // 2. the index of theta_min in the sorted candidates (it is one of them)
-  if (threadIdx.x == 0) {
-    const int32_t tm = probeF[1];
-    int lo = 0, hi = nt - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (th[mid] < tm) lo = mid + 1;
-      else hi = mid;
-    }
-    s_hi = lo;
-  }
-  __syncthreads();
-  const int imin = s_hi;
-  // 3. U = Val(theta_min); evaluate theta_min .. theta_hi
-  if (w == 0) {
-    const int32_t F = warp_F(sP, slev, sO, g[0], L, cf.deg, th[imin]);
-    if (lane == 0) {
-      const int64_t U = (int64_t)F + cm1 * th[imin];
-      V[imin] = U;
-      s_best = (unsigned long long)U;
-    }
-  }
-  __syncthreads();
-  const int64_t U = (int64_t)s_best;
-  if (threadIdx.x == 0) S.cnt = 0;
-  __syncthreads();
-  for (int i = imin + 1 + w; i < nt; i += K4W) {
-    const int32_t theta = th[i];
-    const int64_t lb = (int64_t)Finf + cm1 * theta;
-    if (lb > U) break;  // ascending thetas: every later one is worse too
-    if ((unsigned long long)lb > *(volatile unsigned long long*)&s_best) continue;
-    const int32_t F = warp_F(sP, slev, sO, g[w], L, cf.deg, theta);
-    if (g_trace && lane == 0) atomicAdd(&S.cnt, 1);  // diagnostics: thetas evaluated
-    if (F < INF && lane == 0) {
-      const int64_t val = (int64_t)F + cm1 * theta;
-      V[i] = val;
-      atomicMin(&s_best, (unsigned long long)val);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    V[TMAX] = Finf;
-    cfg_opt[cfg_list[li]] = (int64_t)s_best;
-    tr.extra = (uint32_t)S.cnt | (uint32_t)nt << 12 | (uint32_t)(nt - imin) << 24;
-  }
+  if (t == 0) E[0] = have;
 }
 
 cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int li0,
-                      int n_local, int L, int32_t* thetas, int32_t* ntheta, int64_t* vals, int64_t* cfg_opt,
-                      cudaStream_t st) {
+                      int n_local, int L, int nlev, int32_t* thetas, int64_t* vals, int32_t* ends, int64_t* cfg_opt,
+                      long long* best_obj, cudaStream_t st) {
   if (n_local <= 0) return cudaSuccess;
-  k4_vals<<<n_local, K4W * 32, sizeof(K4Smem), st>>>(cfg, arena, P, cfg_list, li0, L, thetas, ntheta, vals, cfg_opt);
+  k4_vals<<<n_local, K4T, k4_smem(L, nlev), st>>>(cfg, arena, P, cfg_list, li0, L, thetas, vals, ends, cfg_opt,
+                                                   best_obj);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
-// K5a: per-config optimum, global (objective, deg, c) argmin, and the
-// lexicographically largest stage-end vector over the optimal placements
-// (= lexicographically smallest stage_of, reading A-11).  One CTA.
+// K5a: global (objective, deg, c) argmin over the local configs, the record
+// header, the winner's stages (its ends from K4 / K4c) and the device-side
+// plan of the traceback's backward sweeps.  One CTA.
 // ---------------------------------------------------------------------------
-constexpr int K5T = 1024;
-constexpr int K5PP = MAXL + 1;  // odd pitch of K5a's interval tables
-// K5a's dynamic shared memory: the suffix table H, then the winner's interval
-// tables (one per cap level)
-constexpr int K5A_DYN = (MAXL + 1) * (MAXL + 1) * 4 + MAXLEV * MAXL * K5PP * 4;
+constexpr int K5T = 256;
 __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
                                                   const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
-                                                  int n_local, int L, const int32_t* __restrict__ thetas,
-                                                  const int32_t* __restrict__ ntheta, const int64_t* __restrict__ vals,
-                                                  const int64_t* __restrict__ cfg_opt, int32_t* __restrict__ scratch,
-                                                  Winner* __restrict__ win, RecordArgs ra) {
+                                                  int n_local, int L, const int32_t* __restrict__ ends,
+                                                  const int64_t* __restrict__ cfg_opt, Winner* __restrict__ win,
+                                                  long long* __restrict__ best_obj, RecordArgs ra) {
   TraceScope tr(TR_K5A);
-  __shared__ int32_t sO[MAXL];
-  __shared__ int32_t stars[TMAX];
-  __shared__ int32_t nstar;
-  __shared__ int32_t ends[32][MAXL];
-  __shared__ int32_t okw[32];
+  if (threadIdx.x == 0) *best_obj = LLONG_MAX;  // K4's running minimum, ready for the next run (every K4 is done)
   __shared__ int64_t s_opt[1];
   __shared__ int32_t s_win;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  // 2. winner by (objective, deg, c): warp 0, lanes over the local configs,
-  //    then a shuffle argmin on the key tuple
+  // winner by (objective, deg, c): warp 0, lanes over the local configs,
+  // then a shuffle argmin on the key tuple
   if (w == 0) {
     int wi = -1, bd = 0, bc = 0;
     int64_t best = INT64_MAX;
@@ -446,21 +460,21 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     if (lane == 0) {
       s_win = wi;
       s_opt[0] = best;
-      nstar = 0;
     }
   }
-  __syncthreads();
-  const int wl = s_win;
   // the record header: every field K5c does not write (assignment arrays zeroed)
-  if (t < UNIAP_MAX_LAYERS) {
+  for (int i = t; i < UNIAP_MAX_LAYERS; i += K5T) {
     uniap_record* r = ra.rec;
-    r->stage_of[t] = 0;
-    r->strategy_of[t] = 0;
-    r->stage_cost[t] = 0;
-    r->cut_cost[t] = 0;
-    r->stage_mem[t] = 0;
+    r->stage_of[i] = 0;
+    r->strategy_of[i] = 0;
+    r->stage_cost[i] = 0;
+    r->cut_cost[i] = 0;
+    r->stage_mem[i] = 0;
   }
   if (t < MAXCLS) ra.bw->count[t] = 0;
+  if (t < MAXL) win->kfirst[t] = win->klast[t] = -1;
+  __syncthreads();
+  const int wl = s_win;
   if (t == 0) {
     uniap_record* r = ra.rec;
     r->objective = INT64_MAX;
@@ -481,12 +495,11 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
       r->dp_relax = x;
     }
     r->dp_cells_canonical = ra.cells_canon;
+    if (wl < 0) { win->objective = INT64_MAX; win->cfg = -1; win->status = 0; }
   }
-  if (wl < 0) {
-    if (t == 0) { win->objective = INT64_MAX; win->cfg = -1; win->status = 0; }
-    return;
-  }
+  if (wl < 0) return;
   const int ci = cfg_list[wl];
+  __syncthreads();  // the header is written before the winner's fields
   if (cfgs[ci].cut) {
     // NEXT-1 winner: K4c found its stage ends and boundary strategies; the
     // traceback sweeps start at each stage's last layer restricted to its
@@ -531,213 +544,28 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     }
     return;
   }
-  const CfgDev cf = cfgs[ci];
-  const int64_t OPT = s_opt[0];
-  const int64_t* V = vals + (int64_t)wl * (TMAX + 2);
-  const int32_t* th = thetas + (int64_t)wl * TMAX;
-  const int nt = ntheta[wl];
-  // the winner's interval tables P_lev[a][b] at lev * L * PP + a * PP + b
-  // (odd pitch: lanes over a or b conflict-free), in dynamic shared memory
-  // after the suffix table sH
-  extern __shared__ int32_t k5dyn[];
-  int32_t* sPl = k5dyn + (MAXL + 1) * (MAXL + 1);
-  const int PP = L | 1;
-  for (int i = t; i < cf.nlev * L * L; i += K5T) {
-    const int lv = i / (L * L), r = i - lv * L * L;
-    sPl[lv * L * PP + (r / L) * PP + r % L] = P[cf.offP + i];
-  }
-  // stage i (1-based) reads the table of its cap level
-  const int8_t* lev_of = cfgs[ci].lev_of;  // (global: no local copy of cf)
-  auto SPs = [&](int i) { return sPl + lev_of[i - 1] * L * PP; };
-  for (int i = t; i < L - 1; i += K5T) sO[i] = arena[cf.offO + i];
-  // 3. Theta*: every theta with Val = OPT (c > 1); the unconstrained one (c = 1)
-  if (cf.c == 1) {
-    if (t == 0) { stars[0] = -1; nstar = 1; }
-  } else {
-    for (int i = t; i < nt; i += K5T)
-      if (V[i] == OPT) stars[atomicAdd(&nstar, 1)] = i;
-  }
-  __syncthreads();
-  const int ns = nstar;
+  // the winner's stages from K4: stage i = [end[i-1] + 1, end[i]]
+  const CfgDev& cf = cfgs[ci];
   const int deg = cf.deg;
-  // 4. per theta in Theta*: suffix DP H_i[a] (cover [a, L-1] with stages i..deg)
-  //    then the greedy largest end per stage.
-  int32_t* H = scratch + (int64_t)w * (MAXL + 1) * (MAXL + 1);  // [i][a], i = 1..deg, a = 0..L
-  int32_t* mine = ends[w];
-  int32_t best_end[MAXL];
-  bool have = false;
-  // Few theta* (the usual case: one): the whole CTA per theta, H in shared
-  // memory -- stages sequential (one barrier each), warps over the start a,
-  // lanes over the end b with a warp min.  Many: one warp per theta below.
-  constexpr int HP = MAXL + 1;
-  int32_t* sH = k5dyn;  // [i][a], i = 1..deg, a = 0..L
-  for (int si = 0; si < ns && ns <= 4; ++si) {
-    const int32_t theta = stars[si] < 0 ? INF : th[stars[si]];
-    const int64_t F_target = stars[si] < 0 ? OPT : OPT - (int64_t)(cf.c - 1) * theta;
-    for (int a = t; a <= L; a += K5T) {
-      int32_t v = INF;
-      if (a < L) { const int32_t p = SPs(deg)[a * PP + L - 1]; v = p <= theta ? p : INF; }
-      sH[deg * HP + a] = v;
-    }
-    __syncthreads();
-    for (int i = deg - 1; i >= 1; --i) {
-      // H_i[a] = min_b P_i[a][b] + O[b] + H_{i+1}[b+1], b <= L-1-(deg-i)
-      const int bhi = L - 1 - (deg - i);
-      const int32_t* sP = SPs(i);
-      for (int a = w; a <= L; a += K5T / 32) {
-        uint32_t v = INF;
-        for (int b = a + lane; b <= bhi && a < L; b += 32) {
-          const int32_t p = sP[a * PP + b], o = sO[b], hh = sH[(i + 1) * HP + b + 1];
-          if (p <= theta && o <= theta && hh < INF) v = min(v, (uint32_t)p + (uint32_t)o + (uint32_t)hh);
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, off));
-        if (lane == 0) sH[i * HP + a] = (int32_t)min(v, (uint32_t)INF);
-      }
-      __syncthreads();
-    }
-    bool ok = (int64_t)sH[1 * HP + 0] == F_target;
-    if (w == 0) {  // greedy: the largest feasible end of each stage
-      int64_t pre = 0;
-      int a = 0;
-      for (int i = 1; i < deg && ok; ++i) {
-        const int32_t* sP = SPs(i);
-        int found = -1;
-        for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
-          const int b = b0 - lane;
-          bool c = false;
-          if (b >= a) {
-            const int32_t p = sP[a * PP + b], o = sO[b], hh = sH[(i + 1) * HP + b + 1];
-            c = p <= theta && o <= theta && hh < INF && pre + p + o + hh == F_target;
-          }
-          const unsigned m = __ballot_sync(0xffffffffu, c);
-          if (m) found = b0 - (__ffs(m) - 1);
-        }
-        if (found < 0) { ok = false; break; }
-        if (lane == 0) ends[0][i - 1] = found;
-        pre += sP[a * PP + found] + sO[found];
-        a = found + 1;
-      }
-      if (lane == 0) {
-        ends[0][deg - 1] = L - 1;
-        okw[0] = ok;
-      }
-    }
-    __syncthreads();
-    if (t == 0 && okw[0]) {  // lexicographically largest end vector over theta*
-      bool better = !have;
-      for (int i = 0; i < deg && !better; ++i) {
-        if (ends[0][i] != best_end[i]) { better = ends[0][i] > best_end[i]; break; }
-      }
-      if (better) {
-        for (int i = 0; i < deg; ++i) best_end[i] = ends[0][i];
-        have = true;
-      }
-    }
-    __syncthreads();
-  }
-  for (int base = 0; base < ns && ns > 4; base += 32) {
-    const int si = base + w;
-    bool ok = false;
-    if (si < ns) {
-      const int32_t theta = stars[si] < 0 ? INF : th[stars[si]];
-      const int64_t F_target = stars[si] < 0 ? OPT : OPT - (int64_t)(cf.c - 1) * theta;
-      // H_deg[a] = P[a][L-1]
-      for (int a = lane; a <= L; a += 32) {
-        int32_t v = INF;
-        if (a < L) { const int32_t p = SPs(deg)[a * PP + L - 1]; v = p <= theta ? p : INF; }
-        H[deg * (MAXL + 1) + a] = v;
-      }
-      __syncwarp();
-      for (int i = deg - 1; i >= 1; --i) {
-        // H_i[a] = min_b P[a][b] + (O[b] + H_{i+1}[b+1]); the bracket is
-        // lane-independent (broadcast), P[a][b] read transposed
-        const int bhi = L - 1 - (deg - i);
-        const int32_t* Hn = H + (i + 1) * (MAXL + 1);
-        const int32_t* sP = SPs(i);
-        for (int a = lane; a <= L; a += 32) {
-          uint32_t x = INF, y = INF;
-          if (a < L) {
-            int b = a;
-            for (; b + 1 <= bhi; b += 2) {
-              const int32_t p0 = sP[a * PP + b], p1 = sP[a * PP + b + 1];
-              const int32_t o0 = sO[b], o1 = sO[b + 1], h0 = Hn[b + 1], h1 = Hn[b + 2];
-              const uint32_t w0 = (o0 <= theta && h0 < INF) ? (uint32_t)(o0 + h0) : INF;
-              const uint32_t w1 = (o1 <= theta && h1 < INF) ? (uint32_t)(o1 + h1) : INF;
-              x = __viaddmin_u32(w0, p0 <= theta ? (uint32_t)p0 : INF, x);
-              y = __viaddmin_u32(w1, p1 <= theta ? (uint32_t)p1 : INF, y);
-            }
-            if (b <= bhi) {
-              const int32_t p0 = sP[a * PP + b], o0 = sO[b], h0 = Hn[b + 1];
-              const uint32_t w0 = (o0 <= theta && h0 < INF) ? (uint32_t)(o0 + h0) : INF;
-              x = __viaddmin_u32(w0, p0 <= theta ? (uint32_t)p0 : INF, x);
-            }
-          }
-          H[i * (MAXL + 1) + a] = (int32_t)min(min(x, y), (uint32_t)INF);
-        }
-        __syncwarp();
-      }
-      ok = (int64_t)H[1 * (MAXL + 1) + 0] == F_target;
-      // greedy: the largest feasible end of each stage
-      int64_t pre = 0;
-      int a = 0;
-      for (int i = 1; i < deg && ok; ++i) {
-        const int32_t* sP = SPs(i);
-        int found = -1;
-        for (int b0 = L - 1 - (deg - i); b0 >= a && found < 0; b0 -= 32) {
-          const int b = b0 - lane;
-          bool c = false;
-          if (b >= a) {
-            const int32_t p = sP[a * PP + b], o = sO[b], h = H[(i + 1) * (MAXL + 1) + b + 1];
-            c = p <= theta && o <= theta && h < INF && pre + p + o + h == F_target;
-          }
-          const unsigned m = __ballot_sync(0xffffffffu, c);
-          if (m) found = b0 - (__ffs(m) - 1);
-        }
-        if (found < 0) { ok = false; break; }
-        if (lane == 0) mine[i - 1] = found;
-        pre += sP[a * PP + found] + sO[found];
-        a = found + 1;
-      }
-      if (lane == 0) mine[deg - 1] = L - 1;
-      __syncwarp();
-    }
-    if (lane == 0) okw[w] = ok;
-    __syncthreads();
-    // lexicographically largest end vector (theta order is deterministic)
-    if (t == 0) {
-      for (int j = 0; j < 32 && base + j < ns; ++j) {
-        if (!okw[j]) continue;
-        bool better = !have;
-        for (int i = 0; i < deg && !better; ++i) {
-          if (ends[j][i] != best_end[i]) { better = ends[j][i] > best_end[i]; break; }
-        }
-        if (better) {
-          for (int i = 0; i < deg; ++i) best_end[i] = ends[j][i];
-          have = true;
-        }
-      }
-    }
-    __syncthreads();
+  const int32_t* E = ends + (int64_t)wl * (MAXL + 1);
+  const bool have = E[0] != 0;
+  if (t < deg) {
+    const int b = have ? E[1 + t] : L - 1;
+    const int a = t == 0 ? 0 : (have ? E[t] + 1 : L - 1);
+    win->end[t] = b;
+    win->p[t] = P[cf.offP + (int64_t)cf.lev_of[t] * L * L + (int64_t)a * L + b];
+    win->o[t] = (t + 1 < deg) ? arena[cf.offO + b] : 0;
   }
   if (t == 0) {
-    for (int i = 0; i < MAXL; ++i) win->kfirst[i] = win->klast[i] = -1;
+    const int64_t OPT = s_opt[0];
     win->objective = OPT;
     win->cfg = ci;
     win->deg = deg;
     win->c = cf.c;
     win->S = cf.S;
     win->NSP = cf.NSP;
-    win->n_theta_star = ns;
+    win->n_theta_star = 0;
     win->status = have ? 0 : 99;
-    int a = 0;
-    for (int i = 0; i < deg; ++i) {
-      const int b = have ? best_end[i] : L - 1;
-      win->end[i] = b;
-      win->p[i] = SPs(i + 1)[a * PP + b];
-      win->o[i] = (i + 1 < deg) ? sO[b] : 0;
-      a = b + 1;
-    }
     uniap_record* r = ra.rec;
     if (!have) r->status = UNIAP_ERR_INTERNAL;
     r->objective = OPT;
@@ -748,11 +576,11 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     // conditioning ks when the stage contains the skip source and an edge of it
     int n = 0;
     int64_t goff = 0;
-    a = 0;
+    int a = 0;
+    const int64_t kept = ra.gstore[ci];  // deg = 1: the forward phase's sweep kept its tables
     for (int i = 0; i < deg && have && r->status == 0; ++i) {
-      const int b = best_end[i], len = b - a + 1;
+      const int b = E[1 + i], len = b - a + 1;
       const bool cond = cf.skip >= 0 && a <= cf.skip && cf.skip + 2 <= b;
-      const int64_t kept = ra.gstore[ci];  // deg = 1: the forward phase's sweep kept its tables
       for (int ks = cond ? 0 : -1; ks < (cond ? cf.S : 0); ++ks) {
         if (kept >= 0) {
           ra.bw->gofs[i * 33 + ks + 1] = kept + (int64_t)(ks < 0 ? 0 : ks) * L * cf.NSP * (ra.cap + 1);
@@ -769,10 +597,9 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
 }
 
 cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
-                       int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals, const int64_t* cfg_opt,
-                       int32_t* scratch, Winner* win, const RecordArgs& ra, cudaStream_t st) {
-  k5a_winner<<<1, K5T, K5A_DYN, st>>>(cfg, arena, P, cfg_list, n_local, L, thetas, ntheta, vals, cfg_opt, scratch,
-                                      win, ra);
+                       int L, const int32_t* ends, const int64_t* cfg_opt, Winner* win, long long* best_obj,
+                       const RecordArgs& ra, cudaStream_t st) {
+  k5a_winner<<<1, K5T, 0, st>>>(cfg, arena, P, cfg_list, n_local, L, ends, cfg_opt, win, best_obj, ra);
   return cudaGetLastError();
 }
 
@@ -886,9 +713,8 @@ cudaError_t combine_init() {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
   }
-  cudaError_t e = cudaFuncSetAttribute((const void*)k4_vals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4Smem));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute((const void*)k5a_winner, cudaFuncAttributeMaxDynamicSharedMemorySize, K5A_DYN);
+  return cudaFuncSetAttribute((const void*)k4_vals, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)k4_smem(MAXL, MAXLEV));
 }
 
 }  // namespace uniap

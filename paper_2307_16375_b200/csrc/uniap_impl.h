@@ -228,14 +228,15 @@ cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st);
 cudaError_t launch_publish(int32_t* d_rec, const uniap_record* rec, int64_t* d_qg, const int64_t* qg,
                            unsigned long long* d_tm, const unsigned long long* tm, int64_t* d_cfg,
                            const int64_t* cfgopt, int ncfg, cudaStream_t st);
-// K3 (theta candidates) is fused into K4.
+// K3 (theta candidates) is fused into K4; K4 also finds each config's stage
+// ends (ends[li] = {ok, end_1, ..., end_deg}, MAXL + 1 words per config).
+size_t k4_smem(int L, int nlev);
 cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int li0,
-                      int n_local, int L, int32_t* thetas, int32_t* ntheta, int64_t* vals,
-                      int64_t* cfg_opt, cudaStream_t st);
+                      int n_local, int L, int nlev, int32_t* thetas, int64_t* vals, int32_t* ends,
+                      int64_t* cfg_opt, long long* best_obj, cudaStream_t st);
 cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list,
-                       int n_local, int L, const int32_t* thetas, const int32_t* ntheta, const int64_t* vals,
-                       const int64_t* cfg_opt, int32_t* scratch, Winner* win, const RecordArgs& ra,
-                       cudaStream_t st);
+                       int n_local, int L, const int32_t* ends, const int64_t* cfg_opt, Winner* win,
+                       long long* best_obj, const RecordArgs& ra, cudaStream_t st);
 cudaError_t launch_k5c_grid(int max_deg, const CfgDev* cfg, const int32_t* arena, const int32_t* G,
                             const BwPlan* bw, const Winner* win, int L, int cap, uniap_record* rec,
                             cudaStream_t st);

@@ -33,7 +33,7 @@ lines = open(path).read().split("\n")
 recs = [tuple(int(x) for x in ln.split()) for ln in lines[1:] if ln.strip()]
 
 
-KIND = {1: "K1 costs", 2: "K1d quantum", 3: "K1f quantise", 4: "fill", 5: "K4", 6: "K5a", 7: "K5c", 8: "K4 sorted", 9: "K4 loaded", 10: "K4 dp done", 11: "K5a winner", 12: "K5a stars", 13: "K5a ends"}
+KIND = {1: "K1 costs", 2: "K1d quantum", 3: "K1f quantise", 4: "fill", 5: "K4", 6: "K5a", 7: "K5c", 8: "K4 sorted", 9: "K4 loaded", 10: "K4 dp done", 11: "K5a winner", 12: "K5a stars", 13: "K5a ends", 14: "K4 H", 15: "K4 ends"}
 
 
 def shape(tag):
@@ -50,7 +50,7 @@ for tag, v in sorted(by.items(), key=lambda kv: min(x[0] for x in kv[1])):
     s = shape(tag)
     d = sorted(x[1] - x[0] for x in v)
     if tag >> 31:
-        name = KIND.get(tag & 255, "?") + (f" li0={(tag >> 8) & 0xFFFF}" if tag & 255 in (5, 8, 9, 10) else "")
+        name = KIND.get(tag & 255, "?") + (f" li0={(tag >> 8) & 0xFFFF}" if tag & 255 in (5, 8, 9, 10, 14, 15) else "")
     else:
         name = f"NS{s['NS']} V{s['V']} T{s['T']} C{s['C']} G{s['G']} DB{s['DB']}" + (" bw" if s["bw"] else "")
     row = dict(cls=name,
