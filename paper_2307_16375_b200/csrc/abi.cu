@@ -47,6 +47,13 @@ struct DevBuf {
 
 int round4(int x) { return (x + 3) & ~3; }
 
+// Buckets per CTA of the traceback's backward sweeps (k2_pick_class single
+// mode: the bucket axis over a cluster of up to 16 CTAs).  Measured (A/B on
+// the five workloads): up to 1024 buckets one CTA without a cluster is
+// fastest (T5 / Swin / ViT -1.2 to -2.4 % per plan against 4 x 256), at
+// 4096 buckets 16 x 256 beats 4 x 1024 (Llama +1.2 % with the latter).
+static int tb_buckets(int Q) { return Q <= 1024 ? 1024 : 256; }
+
 bool env_flag(const char* name) {
   const char* v = getenv(name);
   return v && *v && *v != '0';
@@ -456,7 +463,7 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
       FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
     }
     h->cls[i] = k;
-    if (!k2_pick_class(S[i], h->Q, true, &h->bcls[i]) || h->bcls[i].NS != k.NS)
+    if (!k2_pick_class(S[i], h->Q, true, &h->bcls[i], false, tb_buckets(h->Q)) || h->bcls[i].NS != k.NS)
       FAIL(h, UNIAP_ERR_ARG, "no traceback class for |S|=%d Q=%d", S[i], h->Q);
     CfgDev& d = h->cfg[i];
     const int NSP = round4(k.NS);

@@ -41,7 +41,7 @@ static int pow2ceil(int x) {
 // A single long chain (deg = 1) is spread over a cluster of up to 16 CTAs
 // with B >= 256, even when it would fit one CTA: its critical path is serial
 // in the layers, so more SMs per layer shorten it.
-bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few) {
+bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few, int single_b) {
   const int NS = k2_ns_round(S);
   if (NS < 0 || Q < 1 || Q > UNIAP_MAX_Q) return false;
   const size_t lim = 200 * 1024;
@@ -57,7 +57,8 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few) {
     // CTAs (measured on the bench workloads: C = 4 x 256 beats C = 8 x 128 at
     // Q = 1024; at Q = 4096 the Llama chain takes 109 us at C = 16 x 256
     // against 133 us at C = 8 x 512)
-    constexpr int bs = 256, cs = 16;
+    const int bs = single_b;
+    constexpr int cs = 16;
     B = std::min(B, bs);
     C = pow2ceil((Q + B - 1) / B);
     while (C > cs && B < Bmax) {
@@ -118,9 +119,10 @@ static k2_fn k2_lookup(const K2Class& c) {
 int k2_selftest(int* S_out, int* Q_out, int* single_out) {
   for (int S = 1; S <= UNIAP_MAX_STRAT; ++S)
     for (int Q = 1; Q <= UNIAP_MAX_Q; Q += (Q < 64 ? 1 : Q < 1100 ? 7 : 61))
-      for (int single = 0; single < 3; ++single) {  // 2: few sweeps
+      for (int single = 0; single < 4; ++single) {  // 2: few sweeps, 3: a traceback of <= 1024 buckets
         K2Class c;
-        if (!k2_pick_class(S, Q, single == 1, &c, single == 2) || !k2_lookup(c)) {
+        if (!k2_pick_class(S, Q, single == 1 || single == 3, &c, single == 2, single == 3 ? 1024 : 256) ||
+            !k2_lookup(c)) {
           *S_out = S;
           *Q_out = Q;
           *single_out = single;
@@ -129,9 +131,10 @@ int k2_selftest(int* S_out, int* Q_out, int* single_out) {
       }
   for (int S = 1; S <= UNIAP_MAX_STRAT; ++S)
     for (int Q : {2048, 4096, 8192})
-      for (int single = 0; single < 3; ++single) {  // 2: few sweeps
+      for (int single = 0; single < 4; ++single) {  // 2: few sweeps, 3: a traceback of <= 1024 buckets
         K2Class c;
-        if (!k2_pick_class(S, Q, single == 1, &c, single == 2) || !k2_lookup(c)) {
+        if (!k2_pick_class(S, Q, single == 1 || single == 3, &c, single == 2, single == 3 ? 1024 : 256) ||
+            !k2_lookup(c)) {
           *S_out = S;
           *Q_out = Q;
           *single_out = single;

@@ -434,37 +434,58 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
   TraceScope tr(TR_K5A);
   if (threadIdx.x == 0) *best_obj = LLONG_MAX;  // K4's running minimum, ready for the next run (every K4 is done)
   __shared__ int64_t s_opt[1];
-  __shared__ int32_t s_win;
+  __shared__ int32_t s_win, s_ci;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  uniap_record* r = ra.rec;
   // winner by (objective, deg, c): warp 0, lanes over the local configs,
   // then a shuffle argmin on the key tuple
   if (w == 0) {
-    int wi = -1, bd = 0, bc = 0;
+    int wi = -1, bd = 0, bc = 0, bci = -1;
     int64_t best = INT64_MAX;
     for (int li = lane; li < n_local; li += 32) {
       const int ci = cfg_list[li];
       const int64_t v = cfg_opt[ci];
       const int dg = cfgs[ci].deg, cc = cfgs[ci].c;
       if (v != INT64_MAX && (wi < 0 || v < best || (v == best && (dg < bd || (dg == bd && cc < bc))))) {
-        wi = li; best = v; bd = dg; bc = cc;
+        wi = li; best = v; bd = dg; bc = cc; bci = ci;
       }
     }
     for (int off = 16; off > 0; off >>= 1) {
       const int owi = __shfl_down_sync(0xffffffffu, wi, off), obd = __shfl_down_sync(0xffffffffu, bd, off),
-                obc = __shfl_down_sync(0xffffffffu, bc, off);
+                obc = __shfl_down_sync(0xffffffffu, bc, off), oci = __shfl_down_sync(0xffffffffu, bci, off);
       const int64_t ob = __shfl_down_sync(0xffffffffu, best, off);
       if (owi >= 0 && (wi < 0 || ob < best || (ob == best && (obd < bd || (obd == bd && obc < bc))))) {
-        wi = owi; best = ob; bd = obd; bc = obc;
+        wi = owi; best = ob; bd = obd; bc = obc; bci = oci;
       }
     }
     if (lane == 0) {
       s_win = wi;
+      s_ci = bci;
       s_opt[0] = best;
     }
+  } else if (w == 1) {  // the record's work counts (level 2: K1f's, where it trimmed the sweeps)
+    unsigned long long c = 0, x = 0;
+    if (ra.work)
+      for (int li = lane; li < ra.n_local; li += 32) {
+        c += ra.work[2 * cfg_list[li]];
+        x += ra.work[2 * cfg_list[li] + 1];
+      }
+    for (int off = 16; off > 0; off >>= 1) {
+      c += __shfl_xor_sync(0xffffffffu, c, off);
+      x += __shfl_xor_sync(0xffffffffu, x, off);
+    }
+    if (lane == 0) {
+      r->n_cfg_local = ra.n_local;
+      r->L = ra.L;
+      r->dp_cells = ra.work ? c : ra.cells;
+      r->dp_relax = ra.work ? x : ra.relax;
+      r->dp_cells_canonical = ra.cells_canon;
+    }
+  } else if (t == 64) {
+    r->status = (ra.qglob && ra.qglob[1] != 0) ? UNIAP_ERR_RANGE : 0;
   }
   // the record header: every field K5c does not write (assignment arrays zeroed)
   for (int i = t; i < UNIAP_MAX_LAYERS; i += K5T) {
-    uniap_record* r = ra.rec;
     r->stage_of[i] = 0;
     r->strategy_of[i] = 0;
     r->stage_cost[i] = 0;
@@ -476,29 +497,13 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
   __syncthreads();
   const int wl = s_win;
   if (t == 0) {
-    uniap_record* r = ra.rec;
     r->objective = INT64_MAX;
     r->cfg_index = -1;
     r->deg = r->c = 0;
-    r->L = ra.L;
-    r->status = (ra.qglob && ra.qglob[1] != 0) ? UNIAP_ERR_RANGE : 0;
-    r->n_cfg_local = ra.n_local;
-    r->dp_cells = ra.cells;
-    r->dp_relax = ra.relax;
-    if (ra.work) {  // level 2: the counts K1f made where it trimmed the sweeps
-      unsigned long long c = 0, x = 0;
-      for (int li = 0; li < ra.n_local; ++li) {
-        c += ra.work[2 * cfg_list[li]];
-        x += ra.work[2 * cfg_list[li] + 1];
-      }
-      r->dp_cells = c;
-      r->dp_relax = x;
-    }
-    r->dp_cells_canonical = ra.cells_canon;
     if (wl < 0) { win->objective = INT64_MAX; win->cfg = -1; win->status = 0; }
   }
   if (wl < 0) return;
-  const int ci = cfg_list[wl];
+  const int ci = s_ci;
   __syncthreads();  // the header is written before the winner's fields
   if (cfgs[ci].cut) {
     // NEXT-1 winner: K4c found its stage ends and boundary strategies; the
@@ -566,7 +571,9 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     win->NSP = cf.NSP;
     win->n_theta_star = 0;
     win->status = have ? 0 : 99;
-    uniap_record* r = ra.rec;
+    const int64_t kept = ra.gstore[ci];  // deg = 1: the forward phase's sweep kept its tables
+    const int cls = ra.cls_of_cfg[ci];
+    const bool st_ok = have && r->status == 0;
     if (!have) r->status = UNIAP_ERR_INTERNAL;
     r->objective = OPT;
     r->cfg_index = ci;
@@ -577,8 +584,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     int n = 0;
     int64_t goff = 0;
     int a = 0;
-    const int64_t kept = ra.gstore[ci];  // deg = 1: the forward phase's sweep kept its tables
-    for (int i = 0; i < deg && have && r->status == 0; ++i) {
+    for (int i = 0; i < deg && st_ok; ++i) {
       const int b = E[1 + i], len = b - a + 1;
       const bool cond = cf.skip >= 0 && a <= cf.skip && cf.skip + 2 <= b;
       for (int ks = cond ? 0 : -1; ks < (cond ? cf.S : 0); ++ks) {
@@ -592,7 +598,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
       }
       a = b + 1;
     }
-    ra.bw->count[ra.cls_of_cfg[ci]] = n;
+    ra.bw->count[cls] = n;
   }
 }
 

@@ -173,7 +173,9 @@ struct K2Class {
 // few = the config has only a few sweeps (deg = 2: prefix + suffix): each is
 // a critical path, so a bucket range that needs a cluster keeps it rather
 // than folding into one single-buffered CTA (which halves the SMs per sweep).
-bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few = false);
+// single: a long chain on a cluster, at least single_b buckets per CTA (a
+// power of two >= 32)
+bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few = false, int single_b = 256);
 // The class of a NEXT-1 (tmode) sweep: one CTA of B = pow2ceil(Q) buckets;
 // false when that does not fit (|S| > 12 needs Q <= 1024, else Q <= 2048).
 bool k2_pick_class_t(int S, int Q, K2Class* out);
