@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["toy_tables", "random_tables", "large_random_tables", "TOY_GRID"]
+__all__ = ["toy_tables", "random_tables", "large_random_tables", "with_1f1b", "TOY_GRID"]
 
 TOY_GRID = [(1, 1), (1, 2), (2, 1), (2, 2)]
 
@@ -153,3 +153,28 @@ def large_random_tables(seed, L, S_list, cap, cands, skip_src=-1, dist="uniform"
         for d in cfgs:
             d["stage_cap"] = crng.choice([cap, cap - cap // 4, cap // 2], size=d["deg"]).astype(np.int32)
     return {"L": L, "cap": cap, "skip_src": skip_src, "cfgs": cfgs}
+
+
+def with_1f1b(t, seed, act_max=None):
+    """The same tables with 1F1B-shaped per-stage memory (reading A-32).
+
+    Every config gets a weight part Mw and a per-micro-batch activation part
+    Ma (drawn, [L, S]); stage i of deg holds min(c, deg - i) micro-batches,
+    so ``M_stage[i] = Mw + min(c, deg - i) * Ma``, and ``M`` becomes GPipe's
+    ``Mw + c * Ma`` (all c in flight).  Entries forbidden in the input (M >
+    cap) stay forbidden in every stage.  Returns a new dict; ``t`` is untouched.
+    """
+    rng = np.random.default_rng(seed + 34_567_890)
+    L, cap = t["L"], t["cap"]
+    out = dict(t, cfgs=[])
+    for d in t["cfgs"]:
+        S, deg, c = d["n_strat"], d["deg"], d["c"]
+        amax = max(1, cap // (2 * max(L, 1) * max(c, 1))) if act_max is None else act_max
+        wmax = max(1, cap // max(L, 1))
+        Mw = rng.integers(0, wmax + 1, size=(L, S))
+        Ma = rng.integers(0, amax + 1, size=(L, S))
+        bad = np.asarray(d["M"]) > cap
+        M = np.where(bad, cap + 1, np.minimum(Mw + c * Ma, cap + 1))
+        MS = np.stack([np.where(bad, cap + 1, np.minimum(Mw + min(c, deg - i) * Ma, cap + 1)) for i in range(deg)])
+        out["cfgs"].append(dict(d, M=M.astype(np.int32), M_stage=MS.astype(np.int32)))
+    return out

@@ -10,7 +10,9 @@ and evaluates literally
   o_j = O[e_j] (+ Rcut[e_j][k_{e_j}][k_{e_j+1}] when the config gives the
         strategy-dependent cut cost, Eq. 4 with R'; e_j = last layer of stage j)
   mem_i = sum_{u in i} M_u[k_u] <= cap_i (the stage's cap, = cap unless the
-          config gives per-stage caps: heterogeneous devices)   (Eq. 5)
+          config gives per-stage caps: heterogeneous devices, PAPER.md:161;
+          M = the stage's own table M_stage[i] when the config gives one: the
+          1F1B schedule, footnote of PAPER.md:122, reading A-32)            (Eq. 5)
   tpi = sum p + sum o + (c-1) * max(P u O)                                  (Eq. 2)
 and returns the minimum of the key (tpi, deg, c, stage_of, strategy_of) --
 with Rcut: (tpi, deg, c, stage_of, boundary vector, strategy_of), the
@@ -46,7 +48,9 @@ def solve_cfg(t, cfg, guard=2_000_000):
     L, cap, s = t["L"], t["cap"], t.get("skip_src", -1)
     S, deg, c = cfg["n_strat"], cfg["deg"], cfg["c"]
     A = np.asarray(cfg["A"], dtype=np.int64).reshape(L, S)
-    M = np.asarray(cfg["M"], dtype=np.int64).reshape(L, S)
+    MS = cfg.get("M_stage")
+    Ms = ([np.asarray(cfg["M"], dtype=np.int64).reshape(L, S)] * deg if MS is None
+          else list(np.asarray(MS, dtype=np.int64).reshape(deg, L, S)))
     R = np.asarray(cfg["R"], dtype=np.int64).reshape(max(L - 1, 0), S, S) if L > 1 else None
     Rs = None if cfg.get("Rskip") is None or s < 0 else np.asarray(cfg["Rskip"], dtype=np.int64).reshape(L, S, S)
     O = np.zeros(max(L - 1, 0), dtype=np.int64) if cfg.get("O") is None else np.asarray(cfg["O"], dtype=np.int64)
@@ -61,7 +65,7 @@ def solve_cfg(t, cfg, guard=2_000_000):
     K = np.array(list(itertools.product(range(S), repeat=L)), dtype=np.int64).reshape(-1, L)
     idx = np.arange(L)
     Au = A[idx, K]                      # [N, L]  A_u[k_u]
-    Mu = M[idx, K]                      # [N, L]
+    Mu = [Mi[idx, K] for Mi in Ms]      # per stage [N, L]
     Ru = R[idx[:-1], K[:, :-1], K[:, 1:]] if L > 1 else np.zeros((len(K), 0), np.int64)  # chain edge u->u+1
     best = None
     for so in places:
@@ -77,7 +81,7 @@ def solve_cfg(t, cfg, guard=2_000_000):
             if Rs is not None and a <= s:
                 for v in range(max(s + 2, a), b + 1):
                     p = p + Rs[v, K[:, s], K[:, v]]
-            mem = Mu[:, a:b + 1].sum(axis=1)
+            mem = Mu[i][:, a:b + 1].sum(axis=1)
             feas &= mem <= caps[i]
             total += p
             mx = np.maximum(mx, p)

@@ -41,7 +41,7 @@ static int validate_tables(const orc_tables* t) {
   for (int i = 0; i < t->n_cfg; ++i) {
     const orc_cfg* c = &t->cfg[i];
     if (c->deg < 1 || c->c < 1 || c->n_strat < 1 || c->n_strat > ORC_MAX_S) return ORC_ERR_ARG;
-    if (!c->A || !c->M || (L > 1 && !c->R)) return ORC_ERR_ARG;
+    if (!c->A || (!c->M && !c->M_stage) || (L > 1 && !c->R)) return ORC_ERR_ARG;
     for (int j = 0; j < i; ++j)
       if (t->cfg[j].deg == c->deg && t->cfg[j].c == c->c) return ORC_ERR_ARG;
     int S = c->n_strat;
@@ -49,7 +49,7 @@ static int validate_tables(const orc_tables* t) {
     for (int u = 0; u < L; ++u) {
       int64_t ma = 0, mr = 0, ms = 0;
       for (int k = 0; k < S; ++k) {
-        int32_t a = c->A[u * S + k], m = c->M[u * S + k];
+        int32_t a = c->A[u * S + k], m = c->M ? c->M[u * S + k] : 0;
         if (a < 0 || a > ENTRY_MAX || m < 0) return ORC_ERR_RANGE;
         ma = max64(ma, a);
       }
@@ -75,6 +75,11 @@ static int validate_tables(const orc_tables* t) {
     if (c->stage_cap)
       for (int i = 0; i < c->deg; ++i)
         if (c->stage_cap[i] < 0 || c->stage_cap[i] > t->cap) return ORC_ERR_ARG;
+    if (c->M_stage) { /* stage-indexed memory (1F1B, reading A-32): entries >= 0, not with Rcut */
+      if (c->Rcut) return ORC_ERR_ARG;
+      for (int64_t j = 0; j < (int64_t)c->deg * L * S; ++j)
+        if (c->M_stage[j] < 0) return ORC_ERR_RANGE;
+    }
     if (c->Rcut) {
       if (c->stage_cap) /* NEXT-1 and NEXT-2 are not combined: caps must all be the common cap */
         for (int i = 0; i < c->deg; ++i)
@@ -299,6 +304,19 @@ static void stage_strategies(const orc_tables* t, const orc_cfg* c, int a, int b
 /* Memory cap of stage i (0-based): Eq. (5) with the stage's own m_i when the
  * devices are heterogeneous, else the common cap. */
 static int stage_cap(const orc_tables* t, const orc_cfg* c, int i) { return c->stage_cap ? c->stage_cap[i] : t->cap; }
+/* Memory table of stage i (0-based): the schedule's own table when the
+ * memory of a layer depends on its stage (synchronous 1F1B: stage i holds
+ * min(c, deg - i) micro-batches in flight, the footnote of PAPER.md:122;
+ * reading A-32), else M. */
+static const int32_t* stage_M(const orc_tables* t, const orc_cfg* c, int i) {
+  return c->M_stage ? c->M_stage + (size_t)i * t->L * c->n_strat : c->M;
+}
+/* stage i's view of the config: the tables with M = its memory table */
+static orc_cfg stage_view(const orc_tables* t, const orc_cfg* c, int i) {
+  orc_cfg ci = *c;
+  ci.M = stage_M(t, c, i);
+  return ci;
+}
 
 static void solve_cfg(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
   int L = t->L, deg = c->deg;
@@ -308,13 +326,15 @@ static void solve_cfg(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
   /* P_i[a][b]: the stage optimum of [a,b] under stage i's cap -- the
    * interval table of the same tables with cap = cap_i, per stage index */
   int64_t* Pall = (int64_t*)malloc(sizeof(int64_t) * (size_t)deg * L * L);
+  const size_t mw = sizeof(int32_t) * (size_t)L * c->n_strat;
   for (int i = 0; i < deg; ++i) {
     int j = 0;
-    while (j < i && stage_cap(t, c, j) != stage_cap(t, c, i)) ++j;
+    while (j < i && (stage_cap(t, c, j) != stage_cap(t, c, i) || memcmp(stage_M(t, c, j), stage_M(t, c, i), mw))) ++j;
     if (j < i) { memcpy(Pall + (size_t)i * L * L, Pall + (size_t)j * L * L, sizeof(int64_t) * L * L); continue; }
     orc_tables ti = *t;
     ti.cap = stage_cap(t, c, i);
-    interval_table(&ti, c, Pall + (size_t)i * L * L);
+    orc_cfg ci = stage_view(t, c, i);
+    interval_table(&ti, &ci, Pall + (size_t)i * L * L);
   }
 #define PI(i, a, b) Pall[((size_t)((i) - 1) * L + (a)) * L + (b)] /* stage i = 1..deg */
   /* Set(i,a), i = 1..deg (index i-1), a = 0..L-1 */
@@ -381,12 +401,13 @@ static void solve_cfg(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
     }
     sol->end[deg - 1] = L - 1;
     sol->p[deg - 1] = PI(deg, a, L - 1);
-    /* strategies per stage, under the stage's own cap */
+    /* strategies per stage, under the stage's own cap and memory table */
     int start = 0;
     for (int i = 0; i < deg && sol->status == ORC_OK; ++i) {
       orc_tables ti = *t;
       ti.cap = stage_cap(t, c, i);
-      stage_strategies(&ti, c, start, sol->end[i], sol->p[i], sol->strat);
+      orc_cfg ci = stage_view(t, c, i);
+      stage_strategies(&ti, &ci, start, sol->end[i], sol->p[i], sol->strat);
       start = sol->end[i] + 1;
     }
   }
@@ -410,7 +431,7 @@ static int check_solution(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
       int k = sol->strat[u];
       if (k < 0 || k >= S) return ORC_ERR_INTERNAL;
       p += c->A[u * S + k];
-      mem += c->M[u * S + k];
+      mem += stage_M(t, c, i)[u * S + k];
       if (u < b) p += Rchain(c, u, k, sol->strat[u + 1]);
       if (c->Rskip && s >= 0 && start <= s && u >= s + 2) p += c->Rskip[((size_t)u * S + sol->strat[s]) * S + k];
     }
@@ -887,7 +908,8 @@ int orc_interval_table(const orc_tables* t, int cfg, int64_t* P) {
   int st = validate_tables(t);
   if (st != ORC_OK) return st;
   if (cfg < 0 || cfg >= t->n_cfg) return ORC_ERR_ARG;
-  interval_table(t, &t->cfg[cfg], P);
+  orc_cfg c0 = stage_view(t, &t->cfg[cfg], 0); /* (stage 1's memory table when stage-indexed) */
+  interval_table(t, &c0, P);
   for (int i = 0; i < t->L * t->L; ++i)
     if (P[i] >= INF) P[i] = INT64_MAX;
   return ORC_OK;
@@ -1045,6 +1067,7 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
     }
   }
   if (o->strategy_space != 0 && o->strategy_space != 1) return ORC_ERR_ARG;
+  if (o->schedule != 0 && o->schedule != 1) return ORC_ERR_ARG;
   /* the concatenated catalogue Cat of the per-edge resharding matrices:
    * S(g) of every divisor g of n, ascending */
   const int64_t ncat = cat_offset(n, n + 1, o->strategy_space);
@@ -1088,6 +1111,10 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
   }
   /* NEXT-1: a config carries Rcut when some chain edge has a cut matrix and it has cuts */
 #define CUTS(i) (any_cut && cand[2 * (i)] >= 2 && cand[2 * (i)] <= L)
+  /* words of config i's block (S = its strategy count) */
+#define BLKW(i, S)                                                                                              \
+  (4 + 2 * (int64_t)L * (S) + (int64_t)(L - 1) * (S) * (S) + (int64_t)L * (S) * (S) + (L - 1) + cand[2 * (i)] + \
+   1 + (CUTS(i) ? (int64_t)(L - 1) * (S) * (S) : 0) + 1 + (o->schedule ? (int64_t)cand[2 * (i)] * L * (S) : 0))
   /* pass 1: sizes and the int64 ns/byte values */
   int64_t words = 0;
   int Ss[4096];
@@ -1096,8 +1123,7 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
     Ss[i] = orc_catalogue(g, o->strategy_space, NULL, 0);
     if (Ss[i] > ORC_MAX_S) return ORC_ERR_RANGE;
     int S = Ss[i];
-    words += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + cand[2 * i] + 1 +
-             (CUTS(i) ? (int64_t)(L - 1) * S * S : 0);
+    words += BLKW(i, S);
   }
   *words_out = words;
   *n_cfg_out = n_cand;
@@ -1201,8 +1227,29 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
             if (v >= NS_LIMIT) st = ORC_ERR_RANGE;
             RC[((int64_t)e * S + k) * S + l] = (int64_t)v;
           }
-    off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + deg + 1 +
-           (CUTS(i) ? (int64_t)(L - 1) * S * S : 0);
+    /* synchronous 1F1B (reading A-32): stage sg keeps the activations of
+     * n = min(c, deg - sg) micro-batches in flight instead of GPipe's c
+     * (footnote of PAPER.md:122: only the memory constraint changes), so Eq. (1)
+     * + activations + context is evaluated per stage with that n */
+    int64_t* HM = RC + (CUTS(i) ? (int64_t)(L - 1) * S * S : 0);
+    HM[0] = o->schedule;
+    for (int sg = 0; o->schedule && sg < deg && st == ORC_OK; ++sg) {
+      const int64_t nf = c < deg - sg ? c : deg - sg;
+      for (int u = 0; u < L; ++u) {
+        const orc_layer* ly = &m->layers[u];
+        for (int k = 0; k < S; ++k) {
+          int64_t t = cat[3 * k], f = cat[3 * k + 1], d = cat[3 * k + 2], r = f * d;
+          int64_t* dst = &HM[1 + ((int64_t)sg * L + u) * S + k];
+          if (b % r) { *dst = -1; continue; } /* reading A-7 */
+          int64_t bl = b / r;
+          u128 mem = cdiv((u128)cdt * ly->param_bytes, (u128)(t * f)) + (u128)nf * bl * ly->act_bytes[ilog2((int)t)] +
+                     (u128)ly->ctx_bytes;
+          if (mem >= NS_LIMIT) { st = ORC_ERR_RANGE; break; }
+          *dst = (int64_t)mem;
+        }
+      }
+    }
+    off += BLKW(i, S);
   }
   /* time quantum (reading A-9): smallest power of two such that every entry
    * fits 2^22 and every config's sums fit 2^28 (or the caller's quantum). */
@@ -1236,8 +1283,7 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
         osum += x + xr; /* every o_j <= O + max Rcut (reading A-9 with NEXT-1) */
       }
       if (sum > SUM_MAX || osum > SUM_MAX) ok = 0;
-      off += 4 + 2 * (int64_t)L * S + (int64_t)(L - 1) * S * S + (int64_t)L * S * S + (L - 1) + cand[2 * i] + 1 +
-             (CUTS(i) ? (int64_t)(L - 1) * S * S : 0);
+      off += BLKW(i, S);
     }
     if (ok) break;
     if (o->quantum_ns) { st = ORC_ERR_RANGE; break; }
@@ -1265,11 +1311,20 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
       out[x0] = (int32_t)blk[x0]; /* has_rcut */
       int64_t nrc = CUTS(i) ? (int64_t)(L - 1) * S * S : 0;
       for (int64_t j = 0; j < nrc; ++j) out[x0 + 1 + j] = (int32_t)((blk[x0 + 1 + j] + qn - 1) / qn);
-      off += x0 + 1 + nrc;
+      int64_t x1 = x0 + 1 + nrc;
+      out[x1] = (int32_t)blk[x1]; /* has_mstage */
+      int64_t nms = o->schedule ? (int64_t)cand[2 * i] * nA : 0;
+      for (int64_t j = 0; j < nms; ++j) { /* memory buckets (reading A-8) */
+        int64_t byt = blk[x1 + 1 + j];
+        int64_t bk = byt < 0 ? (int64_t)cap + 1 : (byt + unit - 1) / unit;
+        out[x1 + 1 + j] = (int32_t)(bk > cap ? cap + 1 : bk);
+      }
+      off += x1 + 1 + nms;
     }
   }
   free(ns);
 #undef CUTS
+#undef BLKW
   return st;
 }
 

@@ -49,6 +49,11 @@ typedef struct {
                             Not combined with stage_cap.  Tie-break key (reading A-31):
                             (tpi, deg, c, stage_of, boundary vector, strategy_of) with the
                             boundary vector (k_{e_1}, k_{e_1+1}, k_{e_2}, k_{e_2+1}, ...)    */
+  const int32_t* M_stage; /* [deg][L][S] or NULL: the memory table of each pipeline stage
+                            (a schedule whose memory depends on the stage: synchronous 1F1B
+                            keeps min(c, deg - i) micro-batches of stage i in flight, footnote
+                            of PAPER.md:122; reading A-32).  When given, stage i uses
+                            M_stage[i] in Eq. 5 and M is ignored (may be NULL).  Not with Rcut. */
 } orc_cfg;
 
 typedef struct {
@@ -106,12 +111,16 @@ typedef struct {
   const int32_t* cand;       /* NULL = Algorithm 1; else n_cand (deg,c) pairs */
   int32_t n_cand;
   int32_t strategy_space;    /* 0 = (t,f,d) triples, 1 = SPEC's (dp,tp)+FSDP-flag pairs */
+  int32_t schedule;          /* 0 = GPipe, 1 = synchronous 1F1B (footnote of
+                                PAPER.md:122): stage i of deg keeps the activations of
+                                min(c, deg - i) micro-batches instead of c (reading A-32) */
 } orc_options;
 
 /* Builder': writes, per candidate config in order, the block
  *   [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1], stage_cap[deg],
- *    has_rcut, Rcut[L-1][S][S] if has_rcut]
- * (has_rcut: some chain edge carries cut_ns and 2 <= deg <= L)
+ *    has_rcut, Rcut[L-1][S][S] if has_rcut, has_mstage, M_stage[deg][L][S] if has_mstage]
+ * (has_rcut: some chain edge carries cut_ns and 2 <= deg <= L; has_mstage:
+ * schedule = 1, M_stage[i] the memory buckets of stage i under 1F1B)
  * into buf (int32).  *n_cfg, *skip_src, *quantum_ns, *words are outputs. */
 int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o,
               int32_t* buf, int64_t buf_len, int32_t* n_cfg, int32_t* skip_src,

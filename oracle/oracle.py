@@ -36,7 +36,8 @@ class _Cfg(C.Structure):
     _fields_ = [("deg", C.c_int32), ("c", C.c_int32), ("n_strat", C.c_int32),
                 ("A", C.POINTER(C.c_int32)), ("M", C.POINTER(C.c_int32)), ("R", C.POINTER(C.c_int32)),
                 ("Rskip", C.POINTER(C.c_int32)), ("O", C.POINTER(C.c_int32)),
-                ("stage_cap", C.POINTER(C.c_int32)), ("Rcut", C.POINTER(C.c_int32))]
+                ("stage_cap", C.POINTER(C.c_int32)), ("Rcut", C.POINTER(C.c_int32)),
+                ("M_stage", C.POINTER(C.c_int32))]
 
 
 class _Tables(C.Structure):
@@ -75,7 +76,8 @@ class _Model(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("B", C.c_int32), ("precision", C.c_int32), ("Q", C.c_int32), ("quantum_ns", C.c_int64),
-                ("cand", C.POINTER(C.c_int32)), ("n_cand", C.c_int32), ("strategy_space", C.c_int32)]
+                ("cand", C.POINTER(C.c_int32)), ("n_cand", C.c_int32), ("strategy_space", C.c_int32),
+                ("schedule", C.c_int32)]
 
 
 _lib = None
@@ -124,7 +126,7 @@ def _marshal_tables(t):
     for i, c in enumerate(t["cfgs"]):
         S = c["n_strat"]
         A = _i32(c["A"]).reshape(L, S)
-        M = _i32(c["M"]).reshape(L, S)
+        M = _i32(c["M"]).reshape(L, S) if c.get("M") is not None else None
         R = _i32(c["R"]).reshape(max(L - 1, 0), S, S) if L > 1 else np.zeros((1, S, S), np.int32)
         Rs = _i32(c["Rskip"]).reshape(L, S, S) if c.get("Rskip") is not None else None
         O = _i32(c["O"]).reshape(max(L - 1, 0)) if c.get("O") is not None else None
@@ -132,9 +134,10 @@ def _marshal_tables(t):
             O = np.zeros(1, np.int32)
         SC = _i32(c["stage_cap"]).reshape(c["deg"]) if c.get("stage_cap") is not None else None
         RC = _i32(c["Rcut"]).reshape(L - 1, S, S) if c.get("Rcut") is not None and L > 1 else None
-        keep += [A, M, R, Rs, O, SC, RC]
+        MS = _i32(c["M_stage"]).reshape(c["deg"], L, S) if c.get("M_stage") is not None else None
+        keep += [A, M, R, Rs, O, SC, RC, MS]
         cfgs[i] = _Cfg(c["deg"], c["c"], S, _ptr32(A), _ptr32(M), _ptr32(R), _ptr32(Rs), _ptr32(O), _ptr32(SC),
-                       _ptr32(RC))
+                       _ptr32(RC), _ptr32(MS))
     tb = _Tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs)
     keep.append(cfgs)
     return tb, keep
@@ -235,7 +238,8 @@ def _marshal_profile(p):
         cand = np.ascontiguousarray(np.array(o["cand"], dtype=np.int32).reshape(-1))
         keep.append(cand)
     opts = _Options(o["B"], o["precision"], o["Q"], o.get("quantum_ns", 0),
-                    _ptr32(cand), 0 if cand is None else len(cand) // 2, o.get("strategy_space", 0))
+                    _ptr32(cand), 0 if cand is None else len(cand) // 2, o.get("strategy_space", 0),
+                    o.get("schedule", 0))
     keep += [layers, edges]
     return model, cluster, opts, keep
 
@@ -272,8 +276,13 @@ def unpack_buffer(buf, L, cap, skip_src, n_cfg):
         RC = None
         if has_rcut:
             RC = buf[off:off + (L - 1) * S * S].reshape(L - 1, S, S); off += (L - 1) * S * S
+        has_ms = int(buf[off]); off += 1
+        MS = None
+        if has_ms:
+            MS = buf[off:off + deg * L * S].reshape(deg, L, S); off += deg * L * S
         cfgs.append({"deg": deg, "c": c, "n_strat": S, "g": g, "A": A, "M": M, "R": R,
-                     "Rskip": Rs if skip_src >= 0 else None, "O": O, "stage_cap": SC, "Rcut": RC})
+                     "Rskip": Rs if skip_src >= 0 else None, "O": O, "stage_cap": SC, "Rcut": RC,
+                     "M_stage": MS})
     return {"L": L, "cap": cap, "skip_src": skip_src, "cfgs": cfgs}
 
 
