@@ -118,6 +118,14 @@ typedef struct {
                                 (reading A-31).  Not combined with per-stage caps other than
                                 cap (_ARG); its configs need Q <= 2048 (Q <= 1024 for |S| > 12),
                                 else _RANGE                                                    */
+  const int32_t* M_stage;    /* [deg][L][n_strat] or NULL: the memory table of each pipeline stage,
+                                for a schedule whose memory depends on the stage -- synchronous
+                                1F1B keeps min(c, deg - i) micro-batches of stage i in flight
+                                instead of GPipe's c ("modify only the memory constraint",
+                                footnote of PAPER.md:122; reading A-32).  Stage i then uses
+                                M_stage[i] in Eq. 5 (entries >= 0, > its cap = forbidden) and M is
+                                ignored (may be NULL).  Not with Rcut (_ARG).  Each distinct
+                                (table, stage cap) pair is one interval table (<= deg per config) */
 } uniap_config;
 
 typedef struct {
@@ -214,6 +222,11 @@ typedef struct {
   int32_t strategy_space;             /* 0 = every (t,f,d) triple (reading A-6); 1 = SPEC's
                                          (dp, tp) pairs with an FSDP flag: the
                                          triples with f = 1 or d = 1                            */
+  int32_t schedule;                   /* 0 = GPipe (every stage keeps c micro-
+                                         batches of activations); 1 = synchronous 1F1B (footnote
+                                         of PAPER.md:122): stage i of deg keeps min(c, deg - i),
+                                         so the builder emits per-stage memory tables
+                                         (uniap_config.M_stage; reading A-32).  Time unchanged */
 } uniap_options;
 
 /* Algorithm 1 end to end: cost model on the GPU (K1), then the solve. */
@@ -223,7 +236,8 @@ uniap_status uniap_plan(uniap_handle* h, const uniap_model* m, const uniap_clust
 /* The builder's tables (for builder parity tests), per candidate config in
  * order, as int32 blocks
  *    [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1], stage_cap[deg],
- *     has_rcut, Rcut[L-1][S][S] if has_rcut]
+ *     has_rcut, Rcut[L-1][S][S] if has_rcut, has_mstage, M_stage[deg][L][S] if has_mstage]
+ * (has_mstage = options.schedule; M is GPipe's table either way)
  * Call with buf == NULL to get *words; then with buf_len >= *words. */
 uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
                                 const uniap_options* o, int32_t* buf, int64_t buf_len, int64_t* words,

@@ -1234,7 +1234,8 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
     int64_t* HM = RC + (CUTS(i) ? (int64_t)(L - 1) * S * S : 0);
     HM[0] = o->schedule;
     for (int sg = 0; o->schedule && sg < deg && st == ORC_OK; ++sg) {
-      const int64_t nf = c < deg - sg ? c : deg - sg;
+      /* (deg > L: no placement exists, reading A-22; its stage tables are GPipe's) */
+      const int64_t nf = deg > L ? c : (c < deg - sg ? c : deg - sg);
       for (int u = 0; u < L; ++u) {
         const orc_layer* ly = &m->layers[u];
         for (int k = 0; k < S; ++k) {

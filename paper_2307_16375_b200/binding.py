@@ -27,7 +27,8 @@ _P64 = C.POINTER(C.c_int64)
 
 class uniap_config(C.Structure):
     _fields_ = [("deg", C.c_int32), ("c", C.c_int32), ("n_strat", C.c_int32), ("A", _P32), ("M", _P32),
-                ("R", _P32), ("Rskip", _P32), ("O", _P32), ("stage_cap", _P32), ("Rcut", _P32)]
+                ("R", _P32), ("Rskip", _P32), ("O", _P32), ("stage_cap", _P32), ("Rcut", _P32),
+                ("M_stage", _P32)]
 
 
 class uniap_tables(C.Structure):
@@ -70,7 +71,7 @@ class uniap_model(C.Structure):
 
 class uniap_options(C.Structure):
     _fields_ = [("B", C.c_int32), ("precision", C.c_int32), ("Q", C.c_int32), ("quantum_ns", C.c_int64),
-                ("cand", _P32), ("n_cand", C.c_int32), ("strategy_space", C.c_int32)]
+                ("cand", _P32), ("n_cand", C.c_int32), ("strategy_space", C.c_int32), ("schedule", C.c_int32)]
 
 
 class uniap_record(C.Structure):
@@ -154,15 +155,16 @@ def _tables(t):
     for i, c in enumerate(t["cfgs"]):
         S = c["n_strat"]
         A = _i32(c["A"]).reshape(L, S)
-        M = _i32(c["M"]).reshape(L, S)
+        M = _i32(c["M"]).reshape(L, S) if c.get("M") is not None else None
         R = _i32(c["R"]).reshape(L - 1, S, S) if L > 1 else np.zeros((1, S, S), np.int32)
         Rs = _i32(c["Rskip"]).reshape(L, S, S) if c.get("Rskip") is not None else None
         O = _i32(c["O"]).reshape(L - 1) if c.get("O") is not None and L > 1 else None
         SC = _i32(c["stage_cap"]).reshape(c["deg"]) if c.get("stage_cap") is not None else None
         RC = _i32(c["Rcut"]).reshape(L - 1, S, S) if c.get("Rcut") is not None and L > 1 else None
-        keep += [A, M, R, Rs, O, SC, RC]
+        MS = _i32(c["M_stage"]).reshape(c["deg"], L, S) if c.get("M_stage") is not None else None
+        keep += [A, M, R, Rs, O, SC, RC, MS]
         cfgs[i] = uniap_config(c["deg"], c["c"], S, _p32(A), _p32(M), _p32(R), _p32(Rs), _p32(O), _p32(SC),
-                               _p32(RC))
+                               _p32(RC), _p32(MS))
     keep.append(cfgs)
     return uniap_tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs), keep
 
@@ -214,7 +216,7 @@ def _profile(p):
     if o.get("cand"):
         cand = np.ascontiguousarray(np.array(o["cand"], dtype=np.int32).reshape(-1))
     opts = uniap_options(o["B"], o["precision"], o["Q"], o.get("quantum_ns", 0), _p32(cand),
-                         0 if cand is None else len(cand) // 2, o.get("strategy_space", 0))
+                         0 if cand is None else len(cand) // 2, o.get("strategy_space", 0), o.get("schedule", 0))
     keep = [fwd, act, lay, ed, cand, mats]
     model = uniap_model(L, C.cast(lay.ctypes.data, C.POINTER(uniap_layer)), E,
                         C.cast(ed.ctypes.data, C.POINTER(uniap_edge)))
@@ -393,6 +395,12 @@ class Handle:
             if has_rcut:
                 blk["Rcut"] = buf[off:off + (L - 1) * S * S].reshape(L - 1, S, S)
                 off += (L - 1) * S * S
+            has_ms = int(buf[off])
+            off += 1
+            blk["M_stage"] = None
+            if has_ms:
+                blk["M_stage"] = buf[off:off + deg * L * S].reshape(deg, L, S)
+                off += deg * L * S
             cfgs.append({"deg": deg, "c": c, "n_strat": S, "g": g, **blk,
                          "Rskip": blk["Rskip"] if skip.value >= 0 else None})
         return {"L": L, "cap": cap, "skip_src": skip.value, "cfgs": cfgs}, qn.value, buf

@@ -61,29 +61,63 @@ bool env_flag(const char* name) {
 
 }  // namespace
 
-// Per-stage memory caps of one config (NEXT-2): the distinct caps in order
-// of first appearance over the stages, and each stage's level.
+// Interval-table levels of one config: the distinct (memory cap, memory
+// table) pairs over the stages in order of first appearance -- per-stage
+// caps (NEXT-2) and per-stage memory tables (1F1B, reading A-32) -- and each
+// stage's level.
 struct Levels {
   int nlev = 1;
-  int32_t lcap[MAXLEV] = {0, 0, 0, 0};
+  int32_t lcap[MAXLEV] = {};
+  int8_t lmt[MAXLEV] = {};
   std::vector<int8_t> lev_of;  // [deg]
 };
-// caps: [deg] per-stage caps (empty = every stage at cap).  false if more
-// than MAXLEV distinct values.
-static bool make_levels(int deg, int cap, const std::vector<int32_t>& caps, Levels& lv) {
+// caps: [deg] per-stage caps (empty = every stage at cap); mts: [deg] each
+// stage's memory table (empty = table 0).  false if more than
+// UNIAP_MAX_LEVELS distinct caps.
+static bool make_levels(int deg, int cap, const std::vector<int32_t>& caps, const std::vector<int>& mts, Levels& lv) {
   lv.nlev = 0;
   lv.lev_of.assign(std::max(deg, 1), 0);
+  int32_t dc[UNIAP_MAX_LEVELS];
+  int ndc = 0;
   for (int i = 0; i < std::max(deg, 1); ++i) {
     const int32_t c = caps.empty() ? cap : caps[i];
+    const int mt = i < (int)mts.size() ? mts[i] : 0;
+    int j = 0;
+    while (j < ndc && dc[j] != c) ++j;
+    if (j == ndc) {
+      if (ndc == UNIAP_MAX_LEVELS) return false;
+      dc[ndc++] = c;
+    }
     int l = 0;
-    while (l < lv.nlev && lv.lcap[l] != c) ++l;
+    while (l < lv.nlev && (lv.lcap[l] != c || lv.lmt[l] != mt)) ++l;
     if (l == lv.nlev) {
       if (lv.nlev == MAXLEV) return false;
-      lv.lcap[lv.nlev++] = c;
+      lv.lcap[lv.nlev] = c;
+      lv.lmt[lv.nlev++] = (int8_t)mt;
     }
     lv.lev_of[i] = (int8_t)l;
   }
   return true;
+}
+
+// The memory tables of a level-1 config: with M_stage, its distinct stage
+// tables (by content) in order of first appearance and each stage's table;
+// else the one table M (mts empty).
+static void stage_tables(const uniap_config& x, int L, std::vector<const int32_t*>& tabs, std::vector<int>& mts) {
+  tabs.clear();
+  mts.clear();
+  if (!x.M_stage) {
+    tabs.push_back(x.M);
+    return;
+  }
+  const size_t w = (size_t)L * x.n_strat;
+  for (int i = 0; i < std::min(x.deg, L); ++i) {  // (deg > L: infeasible, reading A-22)
+    const int32_t* m = x.M_stage + (size_t)i * w;
+    size_t j = 0;
+    while (j < tabs.size() && memcmp(tabs[j], m, w * sizeof(int32_t))) ++j;
+    if (j == tabs.size()) tabs.push_back(m);
+    mts.push_back((int)j);
+  }
 }
 
 // one K2 launch: instances of one kernel class
@@ -182,6 +216,8 @@ struct uniap_handle {
   // forward P sweep at its feasible prefix (Eq. 5).  Level 2: K1f does it on
   // the device from the builder's M (k1f_trim).
   std::vector<int32_t> minM;
+  std::vector<size_t> minMoff;  // per config: its block of minM, [memory table][layer]
+  int max_nmt = 1;              // level 2: the largest memory-table count of a config (K1a's grid)
   // per-stage memory caps (NEXT-2): per config its levels and stage caps
   std::vector<Levels> lev;
   std::vector<std::vector<int32_t>> scap;
@@ -207,8 +243,10 @@ static void update_signature(uniap_handle* h) {
     const K2Class& k = h->cls[i];
     for (int64_t x : {(int64_t)d.deg, (int64_t)d.c, (int64_t)d.S, (int64_t)d.NSP, (int64_t)d.skip, d.offA, d.offP,
                       (int64_t)k.NS, (int64_t)k.V, (int64_t)k.T, (int64_t)k.C, (int64_t)k.DB, (int64_t)k.TM,
-                      (int64_t)d.cut, d.offT})
+                      (int64_t)d.cut, d.offT, (int64_t)d.nlev, (int64_t)d.nmt})
       sg.push_back(x);
+    for (int l = 0; l < d.nlev; ++l) sg.push_back((int64_t)d.lcap[l] << 8 | (uint8_t)d.lmt[l]);
+    for (int st = 0; st < std::min(d.deg, MAXL); ++st) sg.push_back(d.lev_of[st]);
   }
   if (h->level2) {
     const int64_t* c = reinterpret_cast<const int64_t*>(&h->cl);
@@ -427,10 +465,15 @@ static void plan_fast(int L, int i, int deg, int S, int skip, const Levels& lv, 
 // keep[i]: the strategies of config i that can be feasible (ascending caller
 // indices); the tables, kernels and plan use only these (S = keep size).
 // caps[i]: the per-stage caps of config i ([deg], or empty = all at cap).
+// mts[i]: each stage's memory table ([deg], or empty = one table); mtn[i]:
+// per memory table its micro-batches in flight (level 2; 0 = c) -- its size
+// is the config's table count.
 static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vector<int>>& keep,
                                    const std::vector<int>& Sfull, const std::vector<int>& deg,
                                    const std::vector<int>& c, const std::vector<int>& g, const std::vector<int>& skipc,
-                                   const std::vector<std::vector<int32_t>>& caps) {
+                                   const std::vector<std::vector<int32_t>>& caps,
+                                   const std::vector<std::vector<int>>& mts,
+                                   const std::vector<std::vector<int8_t>>& mtn) {
   const int L = h->L;
   std::vector<int> S(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i) S[i] = (int)keep[i].size();
@@ -443,8 +486,8 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
   h->T_words = 0;
   int64_t off = 0, poff = 0;
   for (int i = 0; i < h->ncfg; ++i)
-    if (!make_levels(deg[i], h->cap, caps[i], h->lev[i]))
-      FAIL(h, UNIAP_ERR_RANGE, "config %d: more than %d distinct per-stage caps", i, MAXLEV);
+    if (!make_levels(deg[i], h->cap, caps[i], mts[i], h->lev[i]))
+      FAIL(h, UNIAP_ERR_RANGE, "config %d: more than %d distinct per-stage caps", i, UNIAP_MAX_LEVELS);
   for (int i = 0; i < h->ncfg; ++i) {
     // a config with only a few (long) chains spreads each over more SMs
     // (deg = 1: the whole chain, or its |S| skip-conditioned copies, is the
@@ -475,7 +518,8 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
       d.comp[keep[i][k]] = (int8_t)k;
     }
     d.offA = off; off += (int64_t)L * NSP;
-    d.offM = off; off += (int64_t)L * NSP;
+    const int nmt = std::max<int>(1, (int)mtn[i].size());
+    d.offM = off; off += (int64_t)nmt * L * NSP;  // the memory tables [nmt][L][NSP]
     d.offRt = off; off += (int64_t)(L - 1) * NSP * NSP;
     d.offRf = off; off += (int64_t)(L - 1) * NSP * NSP;
     d.offRs = off; off += (int64_t)L * NSP * NSP;
@@ -485,9 +529,12 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     d.offT = h->T_words; h->T_words += h->cut[i] ? (int64_t)L * L * (NSP + 1) * (NSP + 1) : 0;
     const Levels& lv = h->lev[i];
     d.nlev = lv.nlev;
-    for (int l = 0; l < MAXLEV; ++l) d.lcap[l] = l < lv.nlev ? lv.lcap[l] : h->cap;
+    for (int l = 0; l < MAXLEV; ++l) d.lcap[l] = (int16_t)(l < lv.nlev ? lv.lcap[l] : h->cap);
+    for (int l = 0; l < MAXLEV; ++l) d.lmt[l] = l < lv.nlev ? lv.lmt[l] : 0;
+    d.nmt = nmt;
+    for (int j = 0; j < MAXLEV; ++j) d.mtn[j] = j < (int)mtn[i].size() ? mtn[i][j] : 0;
     for (int st = 0; st < MAXL; ++st) d.lev_of[st] = st < (int)lv.lev_of.size() ? lv.lev_of[st] : 0;
-    d.offP = poff; poff += (int64_t)lv.nlev * L * L;  // one L*L interval table per cap level
+    d.offP = poff; poff += (int64_t)lv.nlev * L * L;  // one L*L interval table per level
   }
   h->arena_words = off;
   h->P_words = poff;
@@ -511,12 +558,14 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
   if (t->n_cfg < 1 || t->n_cfg > UNIAP_MAX_CFG) FAIL(h, UNIAP_ERR_ARG, "n_cfg=%d", t->n_cfg);
   h->L = L; h->cap = t->cap; h->Q = t->cap + 1; h->skip = t->skip_src; h->ncfg = t->n_cfg; h->level2 = false;
   std::vector<int> S(h->ncfg), deg(h->ncfg), c(h->ncfg), g(h->ncfg, 0), skc(h->ncfg);
-  std::vector<std::vector<int>> keep(h->ncfg);
+  std::vector<std::vector<int>> keep(h->ncfg), mts(h->ncfg);
+  std::vector<std::vector<const int32_t*>> tabs(h->ncfg);
+  std::vector<std::vector<int8_t>> mtn(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i) {
     const uniap_config& x = t->cfg[i];
     if (x.deg < 1 || x.c < 1 || x.n_strat < 1 || x.n_strat > UNIAP_MAX_STRAT)
       FAIL(h, UNIAP_ERR_ARG, "config %d: deg=%d c=%d n_strat=%d", i, x.deg, x.c, x.n_strat);
-    if (!x.A || !x.M || (L > 1 && !x.R)) FAIL(h, UNIAP_ERR_ARG, "config %d: null table", i);
+    if (!x.A || (!x.M && !x.M_stage) || (L > 1 && !x.R)) FAIL(h, UNIAP_ERR_ARG, "config %d: null table", i);
     for (int j = 0; j < i; ++j)
       if (t->cfg[j].deg == x.deg && t->cfg[j].c == x.c) FAIL(h, UNIAP_ERR_ARG, "duplicate (deg,c)=(%d,%d)", x.deg, x.c);
     const int s = x.n_strat;
@@ -524,7 +573,7 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
     for (int u = 0; u < L; ++u) {
       int64_t ma = 0, mr = 0, ms = 0;
       for (int k = 0; k < s; ++k) {
-        const int32_t a = x.A[u * s + k], m = x.M[u * s + k];
+        const int32_t a = x.A[u * s + k], m = x.M_stage ? 0 : x.M[u * s + k];
         if (a < 0 || a > UNIAP_MAX_ENTRY || m < 0) FAIL(h, UNIAP_ERR_RANGE, "config %d: A/M out of range at layer %d", i, u);
         ma = std::max<int64_t>(ma, a);
       }
@@ -548,6 +597,11 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
         osum += x.O[e];
       }
     if (sum > UNIAP_MAX_SUM || osum > UNIAP_MAX_SUM) FAIL(h, UNIAP_ERR_RANGE, "config %d: sum bound exceeds 2^28", i);
+    if (x.M_stage) {  // per-stage memory tables (1F1B, reading A-32)
+      if (x.Rcut) FAIL(h, UNIAP_ERR_ARG, "config %d: M_stage with Rcut is not supported", i);
+      for (int64_t j = 0; j < (int64_t)x.deg * L * s; ++j)
+        if (x.M_stage[j] < 0) FAIL(h, UNIAP_ERR_RANGE, "config %d: M_stage entry < 0", i);
+    }
     if (x.Rcut && L > 1) {  // NEXT-1: every o_j <= O[e] + max Rcut[e]; the sum of those bounded like O's
       for (int st = 0; x.stage_cap && st < x.deg; ++st)  // (per-stage caps other than cap: not combined)
         if (x.stage_cap[st] != t->cap) FAIL(h, UNIAP_ERR_ARG, "config %d: Rcut with per-stage caps is not supported", i);
@@ -565,19 +619,31 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
     }
     S[i] = s; deg[i] = x.deg; c[i] = x.c;
     skc[i] = (x.Rskip && t->skip_src >= 0) ? t->skip_src : -1;
-    // strategies with M > cap at every layer can never be part of a solution
+    // strategies with M > cap at every layer (of every stage table) can
+    // never be part of a solution
+    stage_tables(x, L, tabs[i], mts[i]);
     for (int k = 0; k < s; ++k) {
       bool ok = false;
-      for (int u = 0; u < L && !ok; ++u) ok = x.M[u * s + k] <= t->cap;
+      for (const int32_t* M : tabs[i])
+        for (int u = 0; u < L && !ok; ++u) ok = M[u * s + k] <= t->cap;
       if (ok || h->no_compact) keep[i].push_back(k);
     }
+    mtn[i].assign(tabs[i].size(), 0);
     if (keep[i].empty()) keep[i].push_back(0);  // all forbidden: the config is infeasible
   }
-  h->minM.assign((size_t)h->ncfg * L, t->cap + 1);  // (min over given integers: no cost model)
+  // per (config, memory table, layer) the smallest M over the config's
+  // strategies (min over given integers: no cost model)
+  h->minMoff.assign(h->ncfg, 0);
+  size_t nmin = 0;
+  for (int i = 0; i < h->ncfg; ++i) { h->minMoff[i] = nmin; nmin += tabs[i].size() * L; }
+  h->minM.assign(nmin, t->cap + 1);
   for (int i = 0; i < h->ncfg; ++i) {
     const uniap_config& x = t->cfg[i];
-    for (int u = 0; u < L; ++u)
-      for (int k : keep[i]) h->minM[(size_t)i * L + u] = std::min(h->minM[(size_t)i * L + u], x.M[u * x.n_strat + k]);
+    for (size_t j = 0; j < tabs[i].size(); ++j)
+      for (int u = 0; u < L; ++u) {
+        int32_t& mn = h->minM[h->minMoff[i] + j * L + u];
+        for (int k : keep[i]) mn = std::min(mn, tabs[i][j][u * x.n_strat + k]);
+      }
   }
   std::vector<std::vector<int32_t>> caps(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i)
@@ -591,7 +657,7 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
   h->any_cut = false;
   h->cut.assign(h->ncfg, 0);  // NEXT-1: a strategy-dependent cut cost matters only with cuts
   for (int i = 0; i < h->ncfg; ++i) h->cut[i] = t->cfg[i].Rcut && L > 1 && deg[i] >= 2 && deg[i] <= L;
-  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps);
+  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps, mts, mtn);
   if (st != UNIAP_OK) return st;
   // pack the host tables into the device layout (pads: A 0, M cap+1, R 0)
   std::vector<int32_t> a(h->arena_words, 0);
@@ -601,10 +667,11 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
     const int s = x.n_strat, N = d.NSP, sc = d.S;
     const std::vector<int>& kp = keep[i];
     for (int u = 0; u < L; ++u)
-      for (int k = 0; k < N; ++k) {
-        a[d.offA + u * N + k] = k < sc ? x.A[u * s + kp[k]] : 0;
-        a[d.offM + u * N + k] = k < sc ? std::min(x.M[u * s + kp[k]], h->cap + 1) : h->cap + 1;
-      }
+      for (int k = 0; k < N; ++k) a[d.offA + u * N + k] = k < sc ? x.A[u * s + kp[k]] : 0;
+    for (size_t j = 0; j < tabs[i].size(); ++j)
+      for (int u = 0; u < L; ++u)
+        for (int k = 0; k < N; ++k)
+          a[d.offM + ((int64_t)j * L + u) * N + k] = k < sc ? std::min(tabs[i][j][u * s + kp[k]], h->cap + 1) : h->cap + 1;
     for (int e = 0; e + 1 < L; ++e)
       for (int k = 0; k < sc; ++k)
         for (int l = 0; l < sc; ++l) {
@@ -654,7 +721,8 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
       cl->lat_ns < 0 || cl->ccoc_permille < 0 || cl->ccoc_permille > 1000)
     FAIL(h, UNIAP_ERR_ARG, "bad cluster record");
   if (o->B < 1 || o->B > 65536 || o->Q < 2 || o->Q > UNIAP_MAX_Q || (o->precision != 0 && o->precision != 1) ||
-      o->quantum_ns < 0 || o->quantum_ns > ((int64_t)1 << 61) || (o->strategy_space != 0 && o->strategy_space != 1))
+      o->quantum_ns < 0 || o->quantum_ns > ((int64_t)1 << 61) || (o->strategy_space != 0 && o->strategy_space != 1) ||
+      (o->schedule != 0 && o->schedule != 1))
     FAIL(h, UNIAP_ERR_ARG, "bad options");
   if (cl->mem_reserve_bytes < 0 || cl->mem_bytes <= cl->mem_reserve_bytes) FAIL(h, UNIAP_ERR_ARG, "memory <= reserve");
   if ((cl->mem_bytes - cl->mem_reserve_bytes) / (o->Q - 1) < 1) FAIL(h, UNIAP_ERR_ARG, "memory unit < 1 byte");
@@ -783,9 +851,32 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
       if (caps[i][st] != o->Q - 1) FAIL(h, UNIAP_ERR_ARG, "cut matrices with per-stage memory caps are not supported");
   }
   h->any_cut = any_cut;
-  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps);
+  // memory tables: GPipe keeps c micro-batches in flight on every stage
+  // (table 0); synchronous 1F1B keeps min(c, deg - i) on stage i (footnote of
+  // PAPER.md:122, reading A-32): one more table per distinct count below c
+  std::vector<std::vector<int>> mts(h->ncfg);
+  std::vector<std::vector<int8_t>> mtn(h->ncfg);
+  for (int i = 0; i < h->ncfg; ++i) {
+    mtn[i].assign(1, 0);
+    if (o->schedule != 1 || deg[i] > L) continue;  // (deg > L: infeasible, reading A-22: GPipe's table)
+    if (h->cut[i]) FAIL(h, UNIAP_ERR_ARG, "cut matrices with the 1F1B schedule are not supported");
+    for (int stg = 0; stg < deg[i]; ++stg) {
+      const int nf = std::min(c[i], deg[i] - stg);
+      int j = 0;
+      if (nf != c[i]) {
+        j = 1;
+        while (j < (int)mtn[i].size() && mtn[i][j] != nf) ++j;
+        if (j == (int)mtn[i].size()) mtn[i].push_back((int8_t)nf);
+      }
+      mts[i].push_back(j);
+    }
+  }
+  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps, mts, mtn);
   if (st != UNIAP_OK) return st;
+  h->max_nmt = 1;
+  for (int i = 0; i < h->ncfg; ++i) h->max_nmt = std::max(h->max_nmt, (int)mtn[i].size());
   h->minM.clear();  // the sweep trim runs on the device (k1f_trim)
+  h->minMoff.clear();
   h->cl = ClusterDev{cl->n_dev, cl->node_size, cl->ccoc_permille, o->B, o->precision, o->Q, NT, 0,
                      cl->mem_bytes, cl->mem_reserve_bytes, cl->bw_intra_Bps, cl->bw_inter_Bps, cl->p2p_Bps,
                      cl->lat_ns, o->quantum_ns};
@@ -924,6 +1015,7 @@ static void forward_instances(const uniap_handle* h, int i, bool all_intervals, 
   const size_t first = out.size();
   if (all_intervals) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, h->cap, out);
   else plan_fast(h->L, i, d.deg, d.S, d.skip, h->lev[i], h->cut[i], out);
+  for (size_t j = first; j < out.size(); ++j) out[j].mrel = (int32_t)(cfg_moff(d, out[j].lev, h->L) - d.offM);
   // Level 1: stop each forward P sweep where it becomes infeasible -- the
   // memory sum of Eq. 5 over the layers swept is at least the running sum of
   // the per-layer minima of the caller's M, so past the first layer where
@@ -938,7 +1030,7 @@ static void forward_instances(const uniap_handle* h, int i, bool all_intervals, 
     int64_t sum = 0;
     int n = 0;
     for (; n < x.n; ++n) {
-      sum += h->minM[(size_t)i * L + x.a + x.dir * n];  // (a lower bound also at a conditioned skip layer)
+      sum += h->minM[h->minMoff[i] + (size_t)d.lmt[x.lev] * L + x.a + x.dir * n];  // (a lower bound also at a conditioned skip layer)
       if (sum > x.ecap) break;
     }
     x.n = std::max(n, 1);
@@ -990,15 +1082,20 @@ extern "C" uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world,
     deg[i] = t->cfg[i].deg;
     std::vector<int32_t> caps;
     if (t->cfg[i].stage_cap) caps.assign(t->cfg[i].stage_cap, t->cfg[i].stage_cap + deg[i]);
-    if (!make_levels(deg[i], t->cap, caps, lev[i])) return UNIAP_ERR_RANGE;
+    std::vector<const int32_t*> tabs;
+    std::vector<int> mts;
+    if (!t->cfg[i].M && !t->cfg[i].M_stage) return UNIAP_ERR_ARG;
+    stage_tables(t->cfg[i], t->L, tabs, mts);
+    if (!make_levels(deg[i], t->cap, caps, mts, lev[i])) return UNIAP_ERR_RANGE;
     cut[i] = t->cfg[i].Rcut && deg[i] >= 2 && deg[i] <= t->L;
     // the strategy count the prepared tables hold (strategies feasible at some layer)
     const uniap_config& x = t->cfg[i];
-    if (!x.M || x.n_strat < 1) return UNIAP_ERR_ARG;
+    if (x.n_strat < 1) return UNIAP_ERR_ARG;
     S[i] = 0;
     for (int k = 0; k < x.n_strat; ++k) {
       bool ok = false;
-      for (int u = 0; u < t->L && !ok; ++u) ok = x.M[u * x.n_strat + k] <= t->cap;
+      for (const int32_t* M : tabs)
+        for (int u = 0; u < t->L && !ok; ++u) ok = M[u * x.n_strat + k] <= t->cap;
       S[i] += ok;
     }
     S[i] = std::max(S[i], 1);
@@ -1156,7 +1253,8 @@ static uniap_status launch_k2_groups(uniap_handle* h, std::vector<Inst>& all, De
 static BuildBufs build_bufs(uniap_handle* h) {
   return BuildBufs{h->fwd.p, h->act.p, h->ps.p, h->ctx.p, h->tpc.p, h->chain.p, h->skipb.p, h->edges.p,
                    h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->any_cut ? h->cut_mat.p : nullptr,
-                   h->dcat.p, nullptr, nullptr, nullptr, 0, nullptr, h->ns.p, h->qcfg.p, h->qmax.p, h->qglob.p};
+                   h->dcat.p, nullptr, nullptr, nullptr, 0, nullptr, h->ns.p, h->qcfg.p, h->qmax.p, h->qglob.p,
+                   h->max_nmt};
 }
 
 // ---------------------------------------------------------------------------
@@ -1584,7 +1682,7 @@ extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m
   int64_t need = 0;
   for (auto& d : h->cfg)
     need += 4 + 2 * (int64_t)L * d.S + (int64_t)(L - 1) * d.S * d.S + (int64_t)L * d.S * d.S + (L - 1) + d.deg + 1 +
-            (d.cut ? (int64_t)(L - 1) * d.S * d.S : 0);
+            (d.cut ? (int64_t)(L - 1) * d.S * d.S : 0) + 1 + (o->schedule ? (int64_t)d.deg * L * d.S : 0);
   if (words) *words = need;
   if (n_cfg) *n_cfg = h->ncfg;
   if (skip_src) *skip_src = h->skip;
@@ -1620,6 +1718,12 @@ extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m
     for (int e = 0; d.cut && e + 1 < L; ++e)
       for (int k = 0; k < S; ++k)
         for (int l = 0; l < S; ++l) buf[w++] = a[d.offRc + ((int64_t)e * N + k) * N + l];
+    buf[w++] = o->schedule;  // 1F1B: has_mstage, then each stage's memory table
+    for (int st = 0; o->schedule && st < d.deg; ++st) {
+      const int64_t mo = d.deg <= L ? cfg_moff(d, d.lev_of[st], L) : d.offM;  // (deg > L: GPipe's, A-32)
+      for (int u = 0; u < L; ++u)
+        for (int k = 0; k < S; ++k) buf[w++] = a[mo + u * N + k];
+    }
   }
   return UNIAP_OK;
 }

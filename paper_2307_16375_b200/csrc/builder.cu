@@ -6,7 +6,9 @@
 //   time: fp = (b/r) * fwd[t]; bp = 2 fp; TP all-reduces
 //     overlapped with computation through the CCOC; FSDP all-gathers; the
 //     per-iteration gradient sync divided by c (reading A-14)
-//   memory (Eq. 1): c_dtype*ps/(t*f) + c*(b/r)*act[t] + ctx
+//   memory (Eq. 1): c_dtype*ps/(t*f) + n*(b/r)*act[t] + ctx
+//     with n = c micro-batches in flight (GPipe), or per memory table the
+//     1F1B count min(c, deg - i) of its stages (CfgDev::mtn, reading A-32)
 //   resharding R / Rskip (reading A-15) and cut costs O (readings A-1, A-16)
 // in ns / bytes with 128-bit intermediates, then one global time quantum
 // (reading A-9) and memory buckets (reading A-8), written straight into the
@@ -110,21 +112,29 @@ __device__ __forceinline__ int64_t checked(u128 v, int64_t* flags) {
   return (int64_t)v;
 }
 
-// K1a: A (ns) and M (bytes, -1 = forbidden) for every (config, layer, strategy).
+// K1a: A (ns) and M (bytes, -1 = forbidden) for every (config, memory table,
+// layer, strategy); A once (table 0).
 __device__ void k1a_layers(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* __restrict__ cfgs, int L, int bx) {
-  const CfgDev cf = cfgs[blockIdx.y];
-  const int idx = bx * blockDim.x + threadIdx.x;
-  if (idx >= L * cf.NSP) return;
+  const CfgDev& cf = cfgs[blockIdx.y];
+  const int gi = bx * blockDim.x + threadIdx.x, nA = L * cf.NSP;
+  if (gi >= cf.nmt * nA) return;
+  const int mt = gi / nA, idx = gi - mt * nA;
   const int u = idx / cf.NSP, k = idx - u * cf.NSP;
   int64_t* A = bb.ns + cf.offA;
-  int64_t* M = bb.ns + cf.offM;
+  int64_t* M = bb.ns + cf.offM + (int64_t)mt * nA;
   const int64_t b = cl.B / cf.c;
-  if (k >= cf.S) { A[idx] = 0; M[idx] = -1; return; }
+  if (k >= cf.S) { if (mt == 0) A[idx] = 0; M[idx] = -1; return; }
   const int32_t* s = bb.cat[blockIdx.y].tfd + 3 * cf.orig[k];  // table strategy k = catalogue orig[k]
   const int64_t t = s[0], f = s[1], d = s[2], r = f * d;
-  if (b % r) { A[idx] = 0; M[idx] = -1; return; }  // reading A-7
+  if (b % r) { if (mt == 0) A[idx] = 0; M[idx] = -1; return; }  // reading A-7
   const int64_t bl = b / r;
   const int lt = lg2((int)t);
+  const int64_t cdt = cl.prec ? 8 : 4;  // c_dtype
+  const int64_t nfl = cf.mtn[mt] ? cf.mtn[mt] : cf.c;  // micro-batches of activations in flight
+  const u128 mem = cdiv128((u128)cdt * bb.ps[u], (u128)(t * f)) + (u128)nfl * bl * bb.act[u * cl.NT + lt] +
+                   (u128)bb.ctx[u];
+  M[idx] = checked(mem, bb.qglob + 1);
+  if (mt > 0) return;
   const Coll co{cl};
   const int64_t ps = bb.ps[u];
   const u128 fp = (u128)bl * bb.fwd[u * cl.NT + lt];
@@ -136,10 +146,7 @@ __device__ void k1a_layers(const ClusterDev& cl, const BuildBufs& bb, const CfgD
   const u128 fsdp = f > 1 ? 2 * co.allgather(ps_t, f, t) : 0;        // parameter gathers fwd + bwd
   const u128 sync = co.allreduce(ps_tf, d, t * f) + (f > 1 ? co.allgather(ps_t, f, t) : 0);
   const u128 a = ov + fsdp + cdiv128(sync, (u128)cf.c);
-  const int64_t cdt = cl.prec ? 8 : 4;                               // c_dtype
-  const u128 mem = cdiv128((u128)cdt * ps, (u128)(t * f)) + (u128)cf.c * bl * bb.act[u * cl.NT + lt] + (u128)bb.ctx[u];
   A[idx] = checked(a, bb.qglob + 1);
-  M[idx] = checked(mem, bb.qglob + 1);
   amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + u) * QMS, A[idx]);
 }
 
@@ -366,8 +373,13 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
   __shared__ unsigned long long wsum[2];
   const int cap = cl.Q - 1;
   const int64_t unit = (cl.mem_bytes - cl.mem_reserve) / cap;
-  const int64_t* M = bb.ns + cf.offM;
   const int t = threadIdx.x, lane = t & 31, nw = blockDim.x >> 5;
+  if (t < 2) wsum[t] = 0;
+  // per memory table (1F1B: one per distinct in-flight count), the sweeps
+  // whose level reads it
+  for (int mt = 0; mt < cf.nmt; ++mt) {
+  const int64_t* M = bb.ns + cf.offM + (int64_t)mt * L * cf.NSP;
+  __syncthreads();  // (minb / skb of the previous table consumed)
   if (t < L) {  // bucket(min bytes) = min bucket (ceil is monotone); forbidden (< 0) excluded
     int64_t mn = -1;
     for (int k = 0; k < cf.S; ++k) {
@@ -378,7 +390,6 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
   } else if (t >= 64 && t < 64 + cf.S && cf.skip >= 0) {
     skb[t - 64] = mem_bucket(M[cf.skip * cf.NSP + (t - 64)], unit, cap);
   }
-  if (t < 2) wsum[t] = 0;
   __syncthreads();
   const unsigned long long S = cf.S, Qw = cl.Q;
   const int i0 = bb.inst_off[cfg_id], i1 = bb.inst_off[cfg_id + 1];
@@ -386,6 +397,7 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
   for (int q = i0 + tb * nw + (t >> 5); q < i1; q += ntb * nw) {
     const int j = bb.inst_idx[q];
     const Inst in = bb.inst[j];
+    if (cf.lmt[in.lev] != mt) continue;  // (another memory table's pass)
     if (in.emit != 1 && in.emit != 2) {  // a G-keeping sweep runs in full
       if (lane == 0 && S > 1) {          // (|S| = 1: the closed form, no DP cells)
         atomicAdd(&wsum[0], (unsigned long long)in.n0 * S * Qw);
@@ -425,6 +437,7 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
       }
     }
   }
+  }  // memory tables
   __syncthreads();
   if (t < 2 && (wsum[t] || tb == 0)) atomicAdd(bb.work + 2 * cfg_id + t, wsum[t]);  // (zeroed by K1d)
 }
@@ -434,7 +447,7 @@ __device__ void k1f_trim(const ClusterDev& cl, const BuildBufs& bb, const CfgDev
 __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restrict__ cfgs, int L, int32_t* arena) {
   pdl_wait();  // K1d's quantum (PDL)
   TraceScope tr(TR_K1F);
-  const CfgDev cf = cfgs[blockIdx.y];
+  const CfgDev& cf = cfgs[blockIdx.y];  // (by reference: k1f_trim indexes its arrays)
   const int nqb = gridDim.x - bb.n_trim;  // quantising blocks; then the trim blocks
   if ((int)blockIdx.x >= nqb) {
     k1f_trim(cl, bb, cf, blockIdx.y, L, blockIdx.x - nqb, bb.n_trim);
@@ -446,18 +459,19 @@ __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restri
   const int64_t unit = (cl.mem_bytes - cl.mem_reserve) / cap;  // reading A-8
   const int nA = L * NSP, nR = (L - 1) * n2, nS = L * n2, nO = ((L - 1) + 3) & ~3;
   const int nRc = cf.cut ? (L - 1) * n2 : 0;  // NEXT-1 Rcut block
+  const int nMt = cf.nmt * nA;                  // the memory tables
   const bool pow2 = (q & (q - 1)) == 0;
   const int sh = __ffsll(q) - 1;
   auto qt = [&](int64_t x) { return (int32_t)(pow2 ? (x + q - 1) >> sh : (x + q - 1) / q); };
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nA + nR + nS + nO + nRc; idx += nqb * blockDim.x) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nA + nMt + nR + nS + nO + nRc; idx += nqb * blockDim.x) {
     int j = idx;
     if (j < nA) { arena[cf.offA + j] = qt(bb.ns[cf.offA + j]); continue; }
     j -= nA;
-    if (j < nA) {
+    if (j < nMt) {
       arena[cf.offM + j] = mem_bucket(bb.ns[cf.offM + j], unit, cap);
       continue;
     }
-    j -= nA;
+    j -= nMt;
     if (j < nR) {  // Rf = R, Rt = transpose within each edge
       const int e = j / n2, k = (j - e * n2) / NSP, l = j - e * n2 - k * NSP;
       const int32_t v = qt(bb.ns[cf.offRf + j]);
@@ -478,7 +492,7 @@ cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* c
                       int32_t* arena, cudaStream_t st) {
   // qmax / qglob are zeroed by uniap_prepare and left zeroed by K1d (qmax,
   // done counter); the range flags qglob[1] are sticky for the prepared input
-  const int nbA = (L * 32 + K1T - 1) / K1T;
+  const int nbA = (bb.max_nmt * L * 32 + K1T - 1) / K1T;  // (NSP <= 32) x the memory tables
   const int nbR = 2 * L - 1;  // one block per edge slot: L-1 chain edges, L skip destinations
   const int nbE = bb.cut_mat ? L - 1 : 0;  // NEXT-1 cut-cost blocks (per chain edge)
   k1_costs<<<dim3(nbA + nbR + nbE + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR, nbE);

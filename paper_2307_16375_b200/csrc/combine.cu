@@ -242,12 +242,16 @@ constexpr int K4T = 256;  // threads per K4 CTA
 constexpr int K4EW = MAXL + 1;  // words per config in `ends`
 // (+ 64 words of slack after H)
 size_t k4_smem(int L, int nlev) { return (size_t)(nlev * L * (L | 1) + (L + 1) * (L + 1) + 64) * sizeof(int32_t); }
+// dynamic shared memory K4 may take (its static arrays are ~3 KB); beyond it
+// the interval tables stay in global memory (k4_vals: tabs_smem = 0)
+constexpr size_t K4_SMEM_MAX = 200 * 1024;
 __device__ __forceinline__ void cp_async4(int32_t* dst, const int32_t* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+template <bool TABS_SMEM>
 __global__ void __launch_bounds__(K4T) k4_vals(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
                                                const int32_t* __restrict__ P, const int32_t* __restrict__ cfg_list,
                                                int li0, int L, int32_t* __restrict__ thetas,
@@ -307,14 +311,18 @@ __global__ void __launch_bounds__(K4T) k4_vals(const CfgDev* __restrict__ cfgs, 
     }
     return;
   }
-  const int PP = L | 1;
+  // the interval tables in shared memory (odd pitch), or -- when a launch's
+  // levels do not fit (1F1B: up to one level per stage) -- read in place
+  // from global memory (L2) with pitch L
+  // (two instantiations: the compiler sees a shared-memory pointer in the first)
+  const int PP = TABS_SMEM ? (L | 1) : L;
   const int nlev = cf.nlev;
-  int32_t* sP = k4dyn;                   // [nlev][L][PP]
-  int32_t* H = k4dyn + nlev * L * PP;    // [deg + 1][L + 1]
+  const int32_t* sP = TABS_SMEM ? k4dyn : P + cf.offP;  // [nlev][L][PP]
+  int32_t* H = k4dyn + (TABS_SMEM ? nlev * L * PP : 0);  // [deg + 1][L + 1]
   {  // asynchronous copies (LDGSTS): every load of the tables in flight at once
     const int32_t* Pc = P + cf.offP;
-    for (int r = w; r < nlev * L; r += K4T / 32)  // row r = level * L + a
-      for (int b = lane; b < L; b += 32) cp_async4(sP + r * PP + b, Pc + (int64_t)r * L + b);
+    for (int r = w; TABS_SMEM && r < nlev * L; r += K4T / 32)  // row r = level * L + a
+      for (int b = lane; b < L; b += 32) cp_async4(k4dyn + r * PP + b, Pc + (int64_t)r * L + b);
     for (int i = t; i < L - 1; i += K4T) cp_async4(sO + i, arena + cf.offO + i);
   }
   for (int i = t; i < MAXL; i += K4T) slev[i] = cf.lev_of[i];
@@ -415,8 +423,12 @@ cudaError_t launch_k4(const CfgDev* cfg, const int32_t* arena, const int32_t* P,
                       int n_local, int L, int nlev, int32_t* thetas, int64_t* vals, int32_t* ends, int64_t* cfg_opt,
                       long long* best_obj, cudaStream_t st) {
   if (n_local <= 0) return cudaSuccess;
-  k4_vals<<<n_local, K4T, k4_smem(L, nlev), st>>>(cfg, arena, P, cfg_list, li0, L, thetas, vals, ends, cfg_opt,
-                                                   best_obj);
+  if (k4_smem(L, nlev) <= K4_SMEM_MAX)
+    k4_vals<true><<<n_local, K4T, k4_smem(L, nlev), st>>>(cfg, arena, P, cfg_list, li0, L, thetas, vals, ends,
+                                                         cfg_opt, best_obj);
+  else
+    k4_vals<false><<<n_local, K4T, k4_smem(L, 0), st>>>(cfg, arena, P, cfg_list, li0, L, thetas, vals, ends,
+                                                          cfg_opt, best_obj);
   return cudaGetLastError();
 }
 
@@ -593,7 +605,8 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
           continue;
         }
         ra.bw->gofs[i * 33 + ks + 1] = goff;
-        ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1, len};
+        ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1, len, cf.lev_of[i], 0, -1,
+                               (int32_t)(cfg_moff(cf, cf.lev_of[i], L) - cf.offM)};  // (its stage's memory table)
         goff += (int64_t)len * cf.NSP * (ra.cap + 1);
       }
       a = b + 1;
@@ -637,7 +650,7 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
   const int nks = cond ? cf.S : 1;
   const int NSP = cf.NSP, Q = cap + 1, S = cf.S;
   const int32_t* A = arena + cf.offA;
-  const int32_t* M = arena + cf.offM;
+  const int32_t* M = arena + cfg_moff(cfgs[W.cfg], cfgs[W.cfg].lev_of[stage], L);  // the stage's memory table
   const int32_t* Rf = arena + cf.offRf;
   const int32_t* Rs = arena + cf.offRs;
   bool ok = false;
@@ -715,12 +728,16 @@ cudaError_t combine_trace(unsigned long long* p) { return cudaMemcpyToSymbol(g_t
 // Every kernel of the step prefers the maximum shared-memory carveout, as K2
 // needs it: no L1/shared reconfiguration between the kernels of the step.
 cudaError_t combine_init() {
-  for (const void* f : {(const void*)k_fill, (const void*)k4_vals, (const void*)k5a_winner, (const void*)k5c_walk}) {
+  for (const void* f : {(const void*)k_fill, (const void*)k4_vals<true>, (const void*)k4_vals<false>,
+                        (const void*)k5a_winner, (const void*)k5c_walk}) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
   }
-  return cudaFuncSetAttribute((const void*)k4_vals, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)k4_smem(MAXL, MAXLEV));
+  for (const void* f : {(const void*)k4_vals<true>, (const void*)k4_vals<false>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K4_SMEM_MAX);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace uniap

@@ -27,7 +27,10 @@ constexpr int32_t INF = UNIAP_INF;
 constexpr int MAXL = UNIAP_MAX_LAYERS;
 constexpr int TMAX = 2176;   // >= L(L+1)/2 + L - 1 theta candidates for L <= 64
 constexpr int SORTN = 4096;  // bitonic size (power of two >= TMAX)
-constexpr int MAXLEV = UNIAP_MAX_LEVELS;  // distinct per-stage caps of a config (NEXT-2)
+// Interval-table levels of a config: its distinct (memory cap, memory table)
+// pairs over the stages -- at most UNIAP_MAX_LEVELS distinct caps (NEXT-2),
+// and with stage-indexed memory tables (1F1B) up to one level per stage.
+constexpr int MAXLEV = UNIAP_MAX_LAYERS;
 
 struct CfgDev {
   int32_t deg, c, S, NSP, g, skip;        // skip: skip source of this config's tables (-1 none)
@@ -42,8 +45,14 @@ struct CfgDev {
   // Per-stage memory caps (NEXT-2): the config's distinct caps
   // lcap[0..nlev), stage i uses level lev_of[i]; the P block of the config
   // holds one L*L table per level (P_lev[a][b] = optimum of [a,b] under lcap).
-  int32_t lcap[MAXLEV];
+  int16_t lcap[MAXLEV];  // (caps <= UNIAP_MAX_Q - 1)
   int8_t lev_of[MAXL];
+  // Memory tables (1F1B, reading A-32): nmt tables [nmt][L][NSP] at offM;
+  // level l reads table lmt[l]; level 2: table j holds mtn[j] micro-batches
+  // of activations in flight (0 = the config's c, GPipe)
+  int32_t nmt, pad3_;
+  int8_t lmt[MAXLEV];
+  int8_t mtn[MAXLEV];
   // NEXT-1 (strategy-dependent cut cost, Eq. 4): cut = 1 when the config has
   // Rcut [L-1][NSP][NSP] at offRc; its stage tables are then
   // T[a][b][kf][kl] ((NSP+1)^2 per interval, index NSP = that end free) at
@@ -51,6 +60,11 @@ struct CfgDev {
   int32_t cut, pad2_;
   int64_t offRc, offT;
 };
+
+// Word offset of the memory table of level `lev` of a config.
+__host__ __device__ inline int64_t cfg_moff(const CfgDev& cf, int lev, int L) {
+  return cf.offM + (int64_t)cf.lmt[lev] * L * cf.NSP;
+}
 
 // One chain sweep of K2.
 struct Inst {
@@ -73,6 +87,7 @@ struct Inst {
   int32_t lev;   // the config's cap level this sweep emits (P block lev, column ecap)
   int32_t ecap;  // = lcap[lev]: the bucket whose state min_k D[k][ecap] is the stage optimum
   int32_t kf = -1;  // NEXT-1: the first layer swept restricted to strategy kf (-1: free)
+  int32_t mrel = 0;  // the sweep's memory table: word offset from CfgDev::offM (lmt[lev] * L * NSP, 1F1B)
 };
 
 struct K2Args {
@@ -283,6 +298,7 @@ struct BuildBufs {
   int64_t* qcfg;          // [ncfg] smallest passing quantum per config
   int64_t* qmax;          // [ncfg][MAXL][5] per layer: max A, max R into u, max Rskip into u, O[u], max Rcut[u]
   int64_t* qglob;         // [3]: quantum, error flags, completion counter of K1d
+  int32_t max_nmt = 1;    // the largest memory-table count of a config (K1a's grid)
 };
 cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* cfg, int ncfg, int L, int skip,
                       int32_t* arena, cudaStream_t st);

@@ -44,14 +44,23 @@ def stage_intervals(L, deg, i):
 
 
 def levels(t, cfg):
-    """The config's distinct stage caps in order of first appearance (the
-    library's cap levels) and each stage's level."""
-    caps = [t["cap"]] * cfg["deg"] if cfg.get("stage_cap") is None else [int(x) for x in cfg["stage_cap"]]
-    lcap = []
-    for c in caps:
-        if c not in lcap:
-            lcap.append(c)
-    return lcap, [lcap.index(c) for c in caps]
+    """The config's distinct (stage cap, stage memory table) pairs in order of
+    first appearance (the library's levels: per-stage caps, NEXT-2, and the
+    per-stage tables of 1F1B, reading A-32) as (cap, M) and each stage's
+    level."""
+    deg = cfg["deg"]
+    caps = [t["cap"]] * deg if cfg.get("stage_cap") is None else [int(x) for x in cfg["stage_cap"]]
+    MS = cfg.get("M_stage")
+    tabs = [np.asarray(cfg["M"]) if MS is None else np.asarray(MS[i]) for i in range(min(deg, t["L"]))]
+    tabs += [tabs[0] if tabs else None] * (deg - len(tabs))
+    lv, of = [], []
+    for c, m in zip(caps, tabs):
+        j = next((i for i, (c2, m2) in enumerate(lv) if c2 == c and np.array_equal(m2, m)), None)
+        if j is None:
+            lv.append((c, m))
+            j = len(lv) - 1
+        of.append(j)
+    return lv, of
 
 
 def check(h, orc, t, P, what):
@@ -60,15 +69,21 @@ def check(h, orc, t, P, what):
     L = t["L"]
     jobs, off = [], 0
     for i, cfg in enumerate(t["cfgs"]):
-        lcap, lev_of = levels(t, cfg)
-        for lv, cap in enumerate(lcap):
-            jobs.append((i, lv, cap, off))
+        lv_list, lev_of = levels(t, cfg)
+        for lv, (cap, m) in enumerate(lv_list):
+            jobs.append((i, lv, cap, off, m))
             off += L * L
     assert off == P.size, (what, off, P.size)
-    plain = dict(t, cfgs=[{k: v for k, v in c.items() if k != "stage_cap"} for c in t["cfgs"]])
+
+    def table(j):  # the level's interval table: the config with that cap and memory table
+        i, _, cap, _, m = j
+        cfgs = [{k: v for k, v in c.items() if k not in ("stage_cap", "M_stage")} for c in t["cfgs"]]
+        cfgs[i]["M"] = m
+        return orc.interval_table(dict(t, cap=cap, cfgs=cfgs), i)
+
     with cf.ThreadPoolExecutor() as ex:  # ctypes releases the GIL: one oracle call per table in parallel
-        tabs = list(ex.map(lambda j: orc.interval_table(dict(plain, cap=j[2]), j[0]), jobs))
-    for (i, lv, cap, o), want in zip(jobs, tabs):
+        tabs = list(ex.map(table, jobs))
+    for (i, lv, cap, o, _), want in zip(jobs, tabs):
         cfg = t["cfgs"][i]
         want = np.where(want == BIG, INF, want)
         _, lev_of = levels(t, cfg)
