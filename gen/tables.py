@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["toy_tables", "random_tables", "large_random_tables", "with_1f1b", "TOY_GRID"]
+__all__ = ["toy_tables", "random_tables", "large_random_tables", "with_1f1b", "with_skip_sources", "TOY_GRID"]
 
 TOY_GRID = [(1, 1), (1, 2), (2, 1), (2, 2)]
 
@@ -177,4 +177,26 @@ def with_1f1b(t, seed, act_max=None):
         M = np.where(bad, cap + 1, np.minimum(Mw + c * Ma, cap + 1))
         MS = np.stack([np.where(bad, cap + 1, np.minimum(Mw + min(c, deg - i) * Ma, cap + 1)) for i in range(deg)])
         out["cfgs"].append(dict(d, M=M.astype(np.int32), M_stage=MS.astype(np.int32)))
+    return out
+
+
+def with_skip_sources(t, seed, n_src, vmax=None):
+    """The same tables on a DAG with ``n_src`` skip sources (NEXT-4, reading
+    A-33): the chain edges plus edges from each source s_j to every later
+    layer v >= s_j + 2, costs ``Rskips[j][v][k_s][k_v]`` drawn like R's
+    (rows v < s_j + 2 zero).  Sources distinct and ascending in [0, L - 3]
+    (fewer when L is small).  Replaces any single skip source of ``t``."""
+    rng = np.random.default_rng(seed + 45_678_901)
+    L = t["L"]
+    cand = list(range(0, max(L - 2, 0)))
+    k = min(n_src, len(cand))
+    srcs = sorted(int(x) for x in rng.choice(cand, size=k, replace=False)) if k else []
+    out = dict(t, skip_src=-1, skip_srcs=srcs, cfgs=[])
+    for d in t["cfgs"]:
+        S = d["n_strat"]
+        hi = vmax if vmax is not None else int(max(2, np.max(d["R"]) + 1 if d["R"].size else 2))
+        Rss = np.zeros((len(srcs), L, S, S), dtype=np.int64)
+        for j, sj in enumerate(srcs):
+            Rss[j, sj + 2:] = rng.integers(0, hi + 1, size=(L - sj - 2, S, S))
+        out["cfgs"].append(dict(d, Rskip=None, Rskips=Rss.astype(np.int32) if srcs else None))
     return out

@@ -52,7 +52,13 @@ def solve_cfg(t, cfg, guard=2_000_000):
     Ms = ([np.asarray(cfg["M"], dtype=np.int64).reshape(L, S)] * deg if MS is None
           else list(np.asarray(MS, dtype=np.int64).reshape(deg, L, S)))
     R = np.asarray(cfg["R"], dtype=np.int64).reshape(max(L - 1, 0), S, S) if L > 1 else None
-    Rs = None if cfg.get("Rskip") is None or s < 0 else np.asarray(cfg["Rskip"], dtype=np.int64).reshape(L, S, S)
+    # skip edges: one source (skip_src, Rskip) or several (skip_srcs, Rskips; NEXT-4, reading A-33)
+    skips = []
+    if cfg.get("Rskip") is not None and s >= 0:
+        skips.append((s, np.asarray(cfg["Rskip"], dtype=np.int64).reshape(L, S, S)))
+    for j, sj in enumerate(t.get("skip_srcs") or []):
+        if cfg.get("Rskips") is not None:
+            skips.append((sj, np.asarray(cfg["Rskips"], dtype=np.int64).reshape(-1, L, S, S)[j]))
     O = np.zeros(max(L - 1, 0), dtype=np.int64) if cfg.get("O") is None else np.asarray(cfg["O"], dtype=np.int64)
     caps = [cap] * deg if cfg.get("stage_cap") is None else [int(x) for x in cfg["stage_cap"]]
     RC = None if cfg.get("Rcut") is None else np.asarray(cfg["Rcut"], dtype=np.int64).reshape(L - 1, S, S)
@@ -78,9 +84,10 @@ def solve_cfg(t, cfg, guard=2_000_000):
         for i in range(deg):
             a, b = starts[i], ends[i]
             p = Au[:, a:b + 1].sum(axis=1) + Ru[:, a:b].sum(axis=1)
-            if Rs is not None and a <= s:
-                for v in range(max(s + 2, a), b + 1):
-                    p = p + Rs[v, K[:, s], K[:, v]]
+            for sj, Rs in skips:  # every skip edge <s_j, v> with both ends in the stage (Eq. 3)
+                if a <= sj:
+                    for v in range(sj + 2, b + 1):
+                        p = p + Rs[v, K[:, sj], K[:, v]]
             mem = Mu[i][:, a:b + 1].sum(axis=1)
             feas &= mem <= caps[i]
             total += p

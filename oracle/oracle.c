@@ -37,6 +37,11 @@ static int64_t max64(int64_t x, int64_t y) { return x > y ? x : y; }
 static int validate_tables(const orc_tables* t) {
   if (!t || t->L < 1 || t->L > ORC_MAX_L || t->cap < 0 || t->n_cfg < 1 || !t->cfg) return ORC_ERR_ARG;
   if (t->skip_src < -1 || t->skip_src >= t->L) return ORC_ERR_ARG;
+  if (t->n_skip < 0 || t->n_skip > ORC_MAX_SKIP || (t->n_skip > 0 && (!t->skip_srcs || t->skip_src >= 0)))
+    return ORC_ERR_ARG;
+  for (int j = 0; j < t->n_skip; ++j) /* distinct, ascending (reading A-33) */
+    if (t->skip_srcs[j] < 0 || t->skip_srcs[j] >= t->L || (j > 0 && t->skip_srcs[j] <= t->skip_srcs[j - 1]))
+      return ORC_ERR_ARG;
   int L = t->L;
   for (int i = 0; i < t->n_cfg; ++i) {
     const orc_cfg* c = &t->cfg[i];
@@ -64,6 +69,16 @@ static int validate_tables(const orc_tables* t) {
           int32_t r = c->Rskip[(size_t)u * S * S + k];
           if (r < 0 || r > ENTRY_MAX) return ORC_ERR_RANGE;
           ms = max64(ms, r);
+        }
+      for (int j = 0; c->Rskips && j < t->n_skip; ++j) /* every source's edge into u */
+        if (u >= t->skip_srcs[j] + 2) {
+          int64_t mj = 0;
+          for (int k = 0; k < S * S; ++k) {
+            int32_t r = c->Rskips[((size_t)j * L + u) * S * S + k];
+            if (r < 0 || r > ENTRY_MAX) return ORC_ERR_RANGE;
+            mj = max64(mj, r);
+          }
+          ms += mj;
         }
       sum += ma + mr + ms;
     }
@@ -107,18 +122,66 @@ static int validate_tables(const orc_tables* t) {
 /* A'_uk: the execution cost A_uk plus, when the skip source s of the graph
  * lies in the same stage with strategy ks, the resharding term of the skip
  * edge <s,u> (Eq. 3's quadratic term; readings A-16, A-17). */
-static int64_t A_cond(const orc_tables* t, const orc_cfg* c, int u, int k, int ks) {
+/* Skip edges (one source: T5's cross-attention; several sources: NEXT-4,
+ * reading A-33).  A stage conditions on the strategy of every skip source it
+ * holds together with one of that source's edges; a "copy" fixes those
+ * strategies (kv[j] = -1: source j not conditioned in this copy). */
+typedef struct {
+  int n;                          /* skip sources of the graph with tables in this config */
+  int src[ORC_MAX_SKIP];
+  const int32_t* R[ORC_MAX_SKIP]; /* [L][S][S] per source: R[v][k_src][k_v] for v >= src + 2 */
+  int kv[ORC_MAX_SKIP];
+} cond_t;
+
+static void skip_sources(const orc_tables* t, const orc_cfg* c, cond_t* cd) {
+  cd->n = 0;
+  if (t->n_skip > 0) {
+    for (int j = 0; c->Rskips && j < t->n_skip; ++j) {
+      cd->src[cd->n] = t->skip_srcs[j];
+      cd->R[cd->n] = c->Rskips + (size_t)j * t->L * c->n_strat * c->n_strat;
+      cd->kv[cd->n++] = -1;
+    }
+  } else if (t->skip_src >= 0 && c->Rskip) {
+    cd->src[0] = t->skip_src;
+    cd->R[0] = c->Rskip;
+    cd->kv[0] = -1;
+    cd->n = 1;
+  }
+}
+/* number of copies of a stage [a, b]: |S| per source inside it with an edge inside it */
+static int n_copies(const cond_t* base, int a, int b, int S) {
+  int n = 1;
+  for (int j = 0; j < base->n; ++j)
+    if (a <= base->src[j] && base->src[j] + 2 <= b) n *= S;
+  return n;
+}
+/* copy ci of the stage [a, b] (mixed radix over its conditioned sources) */
+static cond_t copy_of(const cond_t* base, int a, int b, int S, int ci) {
+  cond_t cd = *base;
+  for (int j = 0; j < base->n; ++j) {
+    cd.kv[j] = -1;
+    if (a <= base->src[j] && base->src[j] + 2 <= b) {
+      cd.kv[j] = ci % S;
+      ci /= S;
+    }
+  }
+  return cd;
+}
+
+static int64_t A_cond(const orc_tables* t, const orc_cfg* c, int u, int k, const cond_t* ks) {
   int S = c->n_strat;
   int64_t a = c->A[u * S + k];
-  if (ks >= 0 && c->Rskip && u >= t->skip_src + 2)
-    a += c->Rskip[((size_t)u * S + ks) * S + k];
+  for (int j = 0; j < ks->n; ++j)
+    if (ks->kv[j] >= 0 && u >= ks->src[j] + 2) a += ks->R[j][((size_t)u * S + ks->kv[j]) * S + k];
+  (void)t;
   return a;
 }
 /* Strategy k of layer u is allowed: memory entry within the cap (Eq. 5 with
  * the forbidden sentinel), and layer s fixed to ks when conditioning. */
-static int allowed(const orc_tables* t, const orc_cfg* c, int u, int k, int ks) {
+static int allowed(const orc_tables* t, const orc_cfg* c, int u, int k, const cond_t* ks) {
   if (c->M[u * c->n_strat + k] > t->cap) return 0;
-  if (ks >= 0 && u == t->skip_src && k != ks) return 0;
+  for (int j = 0; j < ks->n; ++j)
+    if (ks->kv[j] >= 0 && u == ks->src[j] && k != ks->kv[j]) return 0;
   return 1;
 }
 static int32_t Rchain(const orc_cfg* c, int u, int k, int l) { /* edge u -> u+1 */
@@ -138,7 +201,7 @@ static int64_t Ocut(const orc_cfg* c, int e) { return c->O ? c->O[e] : 0; }
  * (INF otherwise), so D[u][k][q] is the minimum of Eq. (3)'s p over layers
  * a..u with layer u on strategy k and memory sum (Eq. 5) at most q.
  * Row b of the result is  min_k D[b][k][cap]. */
-static void interval_row(const orc_tables* t, const orc_cfg* c, int a, int ks, int64_t* row) {
+static void interval_row(const orc_tables* t, const orc_cfg* c, int a, const cond_t* ks, int64_t* row) {
   int L = t->L, S = c->n_strat, Q = t->cap + 1;
   int64_t* Dp = (int64_t*)malloc(sizeof(int64_t) * (size_t)S * Q);
   int64_t* Dc = (int64_t*)malloc(sizeof(int64_t) * (size_t)S * Q);
@@ -180,13 +243,17 @@ static void interval_row(const orc_tables* t, const orc_cfg* c, int a, int ks, i
  * minimum is taken over the conditioning ks of layer s (SURVEY.md Sec. 8c C-2
  * step 2). */
 static void interval_table(const orc_tables* t, const orc_cfg* c, int64_t* P) {
-  int L = t->L, S = c->n_strat, s = t->skip_src;
+  int L = t->L, S = c->n_strat;
+  cond_t base;
+  skip_sources(t, c, &base);
   int64_t* row = (int64_t*)malloc(sizeof(int64_t) * L);
   for (int i = 0; i < L * L; ++i) P[i] = INF;
   for (int a = 0; a < L; ++a) {
-    int cond = (s >= 0 && c->Rskip && a <= s && s + 2 < L);
-    for (int ks = cond ? 0 : -1; ks < (cond ? S : 0); ++ks) {
-      interval_row(t, c, a, ks, row);
+    /* the copies of the longest row: every source in [a, L-1] with an edge in it */
+    const int nc = n_copies(&base, a, L - 1, S);
+    for (int ci = 0; ci < nc; ++ci) {
+      const cond_t ks = copy_of(&base, a, L - 1, S, ci);
+      interval_row(t, c, a, &ks, row);
       for (int b = a; b < L; ++b) P[a * L + b] = min64(P[a * L + b], row[b]);
     }
   }
@@ -236,7 +303,7 @@ static int64_t tpi(int64_t sig, int64_t mx, int c) { return sig + (int64_t)(c - 
 /* Backward DP G[u][k][q] = min cost of layers u..b given layer u on k and
  * memory at most q for u..b; then walk forward taking the smallest k that
  * still reaches the stage optimum (reading A-11). Returns 1 if found. */
-static int stage_walk(const orc_tables* t, const orc_cfg* c, int a, int b, int ks, int64_t target,
+static int stage_walk(const orc_tables* t, const orc_cfg* c, int a, int b, const cond_t* ks, int64_t target,
                       int32_t* out) {
   int S = c->n_strat, Q = t->cap + 1, n = b - a + 1;
   int64_t* G = (int64_t*)malloc(sizeof(int64_t) * (size_t)n * S * Q);
@@ -279,16 +346,20 @@ static int stage_walk(const orc_tables* t, const orc_cfg* c, int a, int b, int k
 
 static void stage_strategies(const orc_tables* t, const orc_cfg* c, int a, int b, int64_t target,
                              int32_t* strat) {
-  int S = c->n_strat, s = t->skip_src;
-  int cond = (s >= 0 && c->Rskip && a <= s && s + 2 <= b);
-  if (!cond) {
-    stage_walk(t, c, a, b, -1, target, strat);
+  int S = c->n_strat;
+  cond_t base;
+  skip_sources(t, c, &base);
+  const int nc = n_copies(&base, a, b, S);
+  if (nc == 1) {
+    const cond_t ks = copy_of(&base, a, b, S, 0);
+    stage_walk(t, c, a, b, &ks, target, strat);
     return;
   }
   int32_t best[ORC_MAX_L], cur[ORC_MAX_L];
   int have = 0;
-  for (int ks = 0; ks < S; ++ks) {
-    if (!stage_walk(t, c, a, b, ks, target, cur)) continue;
+  for (int ci = 0; ci < nc; ++ci) {
+    const cond_t ks = copy_of(&base, a, b, S, ci);
+    if (!stage_walk(t, c, a, b, &ks, target, cur)) continue;
     int less = !have;
     for (int u = a; u <= b && !less; ++u) {
       if (cur[u] != best[u]) { less = cur[u] < best[u]; break; }
@@ -420,7 +491,9 @@ static void solve_cfg(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
 
 /* Literal re-evaluation of Eqs. (2), (3), (5) from (stage_of, strategy_of). */
 static int check_solution(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
-  int L = t->L, S = c->n_strat, s = t->skip_src, deg = c->deg;
+  int L = t->L, S = c->n_strat, deg = c->deg;
+  cond_t sk;
+  skip_sources(t, c, &sk);
   int start = 0;
   int64_t sum = 0, mx = 0;
   for (int i = 0; i < deg; ++i) {
@@ -433,7 +506,8 @@ static int check_solution(const orc_tables* t, const orc_cfg* c, cfg_sol* sol) {
       p += c->A[u * S + k];
       mem += stage_M(t, c, i)[u * S + k];
       if (u < b) p += Rchain(c, u, k, sol->strat[u + 1]);
-      if (c->Rskip && s >= 0 && start <= s && u >= s + 2) p += c->Rskip[((size_t)u * S + sol->strat[s]) * S + k];
+      for (int j = 0; j < sk.n; ++j) /* every skip edge <s_j, u> with both ends in the stage (Eq. 3) */
+        if (start <= sk.src[j] && u >= sk.src[j] + 2) p += sk.R[j][((size_t)u * S + sol->strat[sk.src[j]]) * S + k];
     }
     if (mem > stage_cap(t, c, i) || p != sol->p[i]) return ORC_ERR_INTERNAL;
     sol->mem[i] = (int32_t)mem;
@@ -469,7 +543,7 @@ static int32_t Rc(const orc_cfg* c, int e, int k, int l) {
 static int64_t ocut(const orc_cfg* c, int e, int kl, int kf) { return Ocut(c, e) + Rc(c, e, kl, kf); }
 
 /* Strategy k allowed at layer u with the start layer a restricted to kf. */
-static int allowed_f(const orc_tables* t, const orc_cfg* c, int u, int k, int ks, int a, int kf) {
+static int allowed_f(const orc_tables* t, const orc_cfg* c, int u, int k, const cond_t* ks, int a, int kf) {
   if (!allowed(t, c, u, k, ks)) return 0;
   if (kf >= 0 && u == a && k != kf) return 0;
   return 1;
@@ -477,7 +551,7 @@ static int allowed_f(const orc_tables* t, const orc_cfg* c, int u, int k, int ks
 
 /* The textbook forward DP of interval_row with the start layer on kf:
  * rowk[b][kl] = min cost of [a,b] with layer b on kl (INF if infeasible). */
-static void interval_row_k(const orc_tables* t, const orc_cfg* c, int a, int ks, int kf, int64_t* rowk) {
+static void interval_row_k(const orc_tables* t, const orc_cfg* c, int a, const cond_t* ks, int kf, int64_t* rowk) {
   int L = t->L, S = c->n_strat, Q = t->cap + 1;
   int64_t* Dp = (int64_t*)malloc(sizeof(int64_t) * (size_t)S * Q);
   int64_t* Dc = (int64_t*)malloc(sizeof(int64_t) * (size_t)S * Q);
@@ -513,15 +587,18 @@ static void interval_row_k(const orc_tables* t, const orc_cfg* c, int a, int ks,
 /* T[((a*L + b)*S + kf)*S + kl] for every a <= b (min over the skip
  * conditioning ks when the stage holds the skip source and one of its edges). */
 static void cut_tables(const orc_tables* t, const orc_cfg* c, int64_t* T) {
-  int L = t->L, S = c->n_strat, s = t->skip_src;
+  int L = t->L, S = c->n_strat;
+  cond_t base;
+  skip_sources(t, c, &base);
   size_t n = (size_t)L * L * S * S;
   for (size_t i = 0; i < n; ++i) T[i] = INF;
   int64_t* rowk = (int64_t*)malloc(sizeof(int64_t) * (size_t)L * S);
   for (int a = 0; a < L; ++a)
     for (int kf = 0; kf < S; ++kf) {
-      int cond = (s >= 0 && c->Rskip && a <= s && s + 2 < L);
-      for (int ks = cond ? 0 : -1; ks < (cond ? S : 0); ++ks) {
-        interval_row_k(t, c, a, ks, kf, rowk);
+      const int nc = n_copies(&base, a, L - 1, S);
+      for (int ci = 0; ci < nc; ++ci) {
+        const cond_t ks = copy_of(&base, a, L - 1, S, ci);
+        interval_row_k(t, c, a, &ks, kf, rowk);
         for (int b = a; b < L; ++b)
           for (int kl = 0; kl < S; ++kl) {
             int64_t* d = &T[(((size_t)a * L + b) * S + kf) * S + kl];
@@ -552,7 +629,7 @@ static int pset_hits(const pset* p, int64_t sig, int64_t mx, int c, int64_t opt)
 /* Backward DP of stage_walk with the first layer restricted to kf and the
  * last to kl (-1: free): the lexicographically smallest strategy vector of
  * [a,b] reaching `target` (reading A-11 within the stage). */
-static int stage_walk_fl(const orc_tables* t, const orc_cfg* c, int a, int b, int ks, int kf, int kl, int64_t target,
+static int stage_walk_fl(const orc_tables* t, const orc_cfg* c, int a, int b, const cond_t* ks, int kf, int kl, int64_t target,
                          int32_t* out) {
   int S = c->n_strat, Q = t->cap + 1, n = b - a + 1;
   int64_t* G = (int64_t*)malloc(sizeof(int64_t) * (size_t)n * S * Q);
@@ -596,12 +673,15 @@ static int stage_walk_fl(const orc_tables* t, const orc_cfg* c, int a, int b, in
 
 static int stage_strategies_fl(const orc_tables* t, const orc_cfg* c, int a, int b, int kf, int kl, int64_t target,
                                int32_t* strat) {
-  int S = c->n_strat, s = t->skip_src;
-  int cond = (s >= 0 && c->Rskip && a <= s && s + 2 <= b);
+  int S = c->n_strat;
+  cond_t base;
+  skip_sources(t, c, &base);
+  const int nc = n_copies(&base, a, b, S);
   int32_t best[ORC_MAX_L], cur[ORC_MAX_L];
   int have = 0;
-  for (int ks = cond ? 0 : -1; ks < (cond ? S : 0); ++ks) {
-    if (!stage_walk_fl(t, c, a, b, ks, kf, kl, target, cur)) continue;
+  for (int ci = 0; ci < nc; ++ci) {
+    const cond_t ks = copy_of(&base, a, b, S, ci);
+    if (!stage_walk_fl(t, c, a, b, &ks, kf, kl, target, cur)) continue;
     int less = !have;
     for (int u = a; u <= b && !less; ++u)
       if (cur[u] != best[u]) { less = cur[u] < best[u]; break; }

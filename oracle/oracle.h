@@ -28,6 +28,7 @@ extern "C" {
 
 #define ORC_MAX_L 64
 #define ORC_MAX_S 32
+#define ORC_MAX_SKIP 4 /* skip sources of a graph (NEXT-4, reading A-33) */
 
 enum { ORC_OK = 0, ORC_ERR_ARG = 1, ORC_ERR_INFEASIBLE = 2, ORC_ERR_RANGE = 3,
        ORC_ERR_INTERNAL = 99 };
@@ -54,11 +55,18 @@ typedef struct {
                             keeps min(c, deg - i) micro-batches of stage i in flight, footnote
                             of PAPER.md:122; reading A-32).  When given, stage i uses
                             M_stage[i] in Eq. 5 and M is ignored (may be NULL).  Not with Rcut. */
+  const int32_t* Rskips;  /* [n_skip][L][S][S] or NULL, with orc_tables.n_skip > 0 (NEXT-4,
+                            reading A-33): Rskips[j][v][k_s][k_v] for the skip edge
+                            skip_srcs[j] -> v, v >= skip_srcs[j] + 2 (other rows ignored) */
 } orc_cfg;
 
 typedef struct {
   int32_t L, cap, skip_src, n_cfg;
   const orc_cfg* cfg;
+  int32_t n_skip;            /* 0, or 1..ORC_MAX_SKIP skip sources (skip_src must be -1): a DAG
+                                whose layers are in topological order with the chain edges and
+                                further edges from these sources (NEXT-4, reading A-33)      */
+  const int32_t* skip_srcs;  /* [n_skip] ascending                                           */
 } orc_tables;
 
 typedef struct {

@@ -37,12 +37,12 @@ class _Cfg(C.Structure):
                 ("A", C.POINTER(C.c_int32)), ("M", C.POINTER(C.c_int32)), ("R", C.POINTER(C.c_int32)),
                 ("Rskip", C.POINTER(C.c_int32)), ("O", C.POINTER(C.c_int32)),
                 ("stage_cap", C.POINTER(C.c_int32)), ("Rcut", C.POINTER(C.c_int32)),
-                ("M_stage", C.POINTER(C.c_int32))]
+                ("M_stage", C.POINTER(C.c_int32)), ("Rskips", C.POINTER(C.c_int32))]
 
 
 class _Tables(C.Structure):
     _fields_ = [("L", C.c_int32), ("cap", C.c_int32), ("skip_src", C.c_int32), ("n_cfg", C.c_int32),
-                ("cfg", C.POINTER(_Cfg))]
+                ("cfg", C.POINTER(_Cfg)), ("n_skip", C.c_int32), ("skip_srcs", C.POINTER(C.c_int32))]
 
 
 class _Result(C.Structure):
@@ -135,10 +135,15 @@ def _marshal_tables(t):
         SC = _i32(c["stage_cap"]).reshape(c["deg"]) if c.get("stage_cap") is not None else None
         RC = _i32(c["Rcut"]).reshape(L - 1, S, S) if c.get("Rcut") is not None and L > 1 else None
         MS = _i32(c["M_stage"]).reshape(c["deg"], L, S) if c.get("M_stage") is not None else None
-        keep += [A, M, R, Rs, O, SC, RC, MS]
+        srcs = t.get("skip_srcs") or []
+        RSS = _i32(c["Rskips"]).reshape(len(srcs), L, S, S) if c.get("Rskips") is not None and srcs else None
+        keep += [A, M, R, Rs, O, SC, RC, MS, RSS]
         cfgs[i] = _Cfg(c["deg"], c["c"], S, _ptr32(A), _ptr32(M), _ptr32(R), _ptr32(Rs), _ptr32(O), _ptr32(SC),
-                       _ptr32(RC), _ptr32(MS))
-    tb = _Tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs)
+                       _ptr32(RC), _ptr32(MS), _ptr32(RSS))
+    srcs = _i32(t.get("skip_srcs") or [0])
+    keep.append(srcs)
+    tb = _Tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs, len(t.get("skip_srcs") or []),
+                 _ptr32(srcs))
     keep.append(cfgs)
     return tb, keep
 
