@@ -42,6 +42,9 @@ extern "C" {
 #define UNIAP_MAX_Q 8192            /* memory buckets (cap + 1) */
 #define UNIAP_MAX_CFG 4096
 #define UNIAP_MAX_LEVELS 4          /* distinct per-stage memory caps per config (NEXT-2)   */
+#define UNIAP_MAX_SKIP 4            /* skip sources of a DAG (NEXT-4, uniap_tables.skip_srcs) */
+#define UNIAP_MAX_COPIES 4096       /* per config: conditioning copies over every contiguous run of
+                                       its skip sources, sum of |S|^run length (NEXT-4)         */
 
 typedef enum {
   UNIAP_OK = 0,
@@ -126,6 +129,11 @@ typedef struct {
                                 M_stage[i] in Eq. 5 (entries >= 0, > its cap = forbidden) and M is
                                 ignored (may be NULL).  Not with Rcut (_ARG).  Each distinct
                                 (table, stage cap) pair is one interval table (<= deg per config) */
+  const int32_t* Rskips;     /* [n_skip][L][n_strat][n_strat] or NULL, with uniap_tables.n_skip > 0
+                                (NEXT-4): Rskips[j][v][k_s][k_v], the resharding cost of the skip
+                                edge skip_srcs[j] -> v for v >= skip_srcs[j] + 2 (other rows
+                                ignored), 0..2^22; NULL = this config has no skip edges.  Not with
+                                Rcut or M_stage (_ARG)                                          */
 } uniap_config;
 
 typedef struct {
@@ -135,6 +143,16 @@ typedef struct {
   int32_t n_cfg;             /* 1..4096 candidate configs, any order; ties broken by the (deg,c)
                                 VALUES; a duplicate (deg,c) is UNIAP_ERR_ARG                   */
   const uniap_config* cfg;
+  int32_t n_skip;            /* 0, or 1..UNIAP_MAX_SKIP skip sources (then skip_src must be -1):
+                                a DAG whose layers are given in topological order with every
+                                chain edge u -> u+1 plus edges from these sources to later layers
+                                (NEXT-4, general DAGs; reading A-33: with the
+                                chain edges Def. 1's contiguous sets are exactly the intervals of
+                                that order).  A stage pays every edge with both ends in it (Eq. 3)
+                                and conditions on the strategy of each source it holds together
+                                with an edge of it: sum over the contiguous runs of sources of
+                                |S|^run length at most UNIAP_MAX_COPIES per config (_RANGE)     */
+  const int32_t* skip_srcs;  /* [n_skip], strictly ascending layer indices                      */
 } uniap_tables;
 
 /* Solve level-1 tables: UNIAP_OK, UNIAP_ERR_INFEASIBLE (objective INT64_MAX,

@@ -28,12 +28,12 @@ _P64 = C.POINTER(C.c_int64)
 class uniap_config(C.Structure):
     _fields_ = [("deg", C.c_int32), ("c", C.c_int32), ("n_strat", C.c_int32), ("A", _P32), ("M", _P32),
                 ("R", _P32), ("Rskip", _P32), ("O", _P32), ("stage_cap", _P32), ("Rcut", _P32),
-                ("M_stage", _P32)]
+                ("M_stage", _P32), ("Rskips", _P32)]
 
 
 class uniap_tables(C.Structure):
     _fields_ = [("L", C.c_int32), ("cap", C.c_int32), ("skip_src", C.c_int32), ("n_cfg", C.c_int32),
-                ("cfg", C.POINTER(uniap_config))]
+                ("cfg", C.POINTER(uniap_config)), ("n_skip", C.c_int32), ("skip_srcs", _P32)]
 
 
 class uniap_result(C.Structure):
@@ -162,11 +162,16 @@ def _tables(t):
         SC = _i32(c["stage_cap"]).reshape(c["deg"]) if c.get("stage_cap") is not None else None
         RC = _i32(c["Rcut"]).reshape(L - 1, S, S) if c.get("Rcut") is not None and L > 1 else None
         MS = _i32(c["M_stage"]).reshape(c["deg"], L, S) if c.get("M_stage") is not None else None
-        keep += [A, M, R, Rs, O, SC, RC, MS]
+        srcs = t.get("skip_srcs") or []
+        RSS = _i32(c["Rskips"]).reshape(len(srcs), L, S, S) if c.get("Rskips") is not None and srcs else None
+        keep += [A, M, R, Rs, O, SC, RC, MS, RSS]
         cfgs[i] = uniap_config(c["deg"], c["c"], S, _p32(A), _p32(M), _p32(R), _p32(Rs), _p32(O), _p32(SC),
-                               _p32(RC), _p32(MS))
+                               _p32(RC), _p32(MS), _p32(RSS))
     keep.append(cfgs)
-    return uniap_tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs), keep
+    srcs = _i32(t.get("skip_srcs") or [0])
+    keep.append(srcs)
+    return uniap_tables(L, t["cap"], t.get("skip_src", -1), len(t["cfgs"]), cfgs, len(t.get("skip_srcs") or []),
+                        _p32(srcs)), keep
 
 
 _LAYER_DT = np.dtype([("fwd", np.uint64), ("param", np.int64), ("act", np.uint64), ("ctx", np.int64),

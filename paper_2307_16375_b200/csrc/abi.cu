@@ -246,6 +246,7 @@ static void update_signature(uniap_handle* h) {
                       (int64_t)d.cut, d.offT, (int64_t)d.nlev, (int64_t)d.nmt})
       sg.push_back(x);
     for (int l = 0; l < d.nlev; ++l) sg.push_back((int64_t)d.lcap[l] << 8 | (uint8_t)d.lmt[l]);
+    for (int j = 0; j < d.nsk; ++j) sg.push_back(d.sk[j]);
     for (int st = 0; st < std::min(d.deg, MAXL); ++st) sg.push_back(d.lev_of[st]);
   }
   if (h->level2) {
@@ -458,6 +459,7 @@ extern "C" void uniap_destroy(uniap_handle* h) {
 
 static void plan_instances(int L, int i, int deg, int S, int skip, bool all_intervals, int ecap, std::vector<Inst>& out);
 static void plan_fast(int L, int i, int deg, int S, int skip, const Levels& lv, bool cut, std::vector<Inst>& out);
+static void plan_multi(int L, int i, const CfgDev& d, const Levels& lv, bool all_intervals, std::vector<Inst>& out);
 
 // ---------------------------------------------------------------------------
 // Layout of the configs in the device arena.
@@ -473,7 +475,8 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
                                    const std::vector<int>& c, const std::vector<int>& g, const std::vector<int>& skipc,
                                    const std::vector<std::vector<int32_t>>& caps,
                                    const std::vector<std::vector<int>>& mts,
-                                   const std::vector<std::vector<int8_t>>& mtn) {
+                                   const std::vector<std::vector<int8_t>>& mtn,
+                                   const std::vector<std::vector<int>>* msrc = nullptr) {
   const int L = h->L;
   std::vector<int> S(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i) S[i] = (int)keep[i].size();
@@ -494,8 +497,16 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     // critical path of the step; measured: giving deg = 2's prefix + suffix
     // sweeps the same treatment starves the many-sweep classes of SMs)
     std::vector<Inst> v;
-    plan_fast(L, i, deg[i], S[i], skipc[i], h->lev[i], h->cut[i], v);
-    const bool single = !v.empty() && (deg[i] == 1 || v.size() <= 1);
+    const bool multi = msrc && (*msrc)[i].size() >= 2;  // NEXT-4: several skip sources
+    if (multi) {
+      CfgDev tmp{};
+      tmp.deg = deg[i]; tmp.S = S[i]; tmp.NSP = round4(S[i]); tmp.nsk = (int)(*msrc)[i].size();
+      for (int j = 0; j < tmp.nsk; ++j) tmp.sk[j] = (int16_t)(*msrc)[i][j];
+      plan_multi(L, i, tmp, h->lev[i], false, v);
+    } else {
+      plan_fast(L, i, deg[i], S[i], skipc[i], h->lev[i], h->cut[i], v);
+    }
+    const bool single = !v.empty() && ((deg[i] == 1 && !multi) || v.size() <= 1);
     const bool few = !v.empty() && v.size() <= 4;  // deg = 2 (prefix + suffix): keep clusters
     K2Class k;
     if (h->cut[i]) {  // NEXT-1: one-CTA per-strategy emission
@@ -535,6 +546,22 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     for (int j = 0; j < MAXLEV; ++j) d.mtn[j] = j < (int)mtn[i].size() ? mtn[i][j] : 0;
     for (int st = 0; st < MAXL; ++st) d.lev_of[st] = st < (int)lv.lev_of.size() ? lv.lev_of[st] : 0;
     d.offP = poff; poff += (int64_t)lv.nlev * L * L;  // one L*L interval table per level
+    // NEXT-4: the conditioning copies of every contiguous run of skip sources
+    d.nsk = multi ? (int)(*msrc)[i].size() : 0;
+    for (int j = 0; j < UNIAP_MAX_SKIP; ++j) d.sk[j] = (int16_t)(j < d.nsk ? (*msrc)[i][j] : -1);
+    for (int r = 0; r < UNIAP_MAX_SKIP * UNIAP_MAX_SKIP; ++r) d.cprel[r] = -1;
+    int64_t ncopies = 0;
+    for (int jlo = 0; jlo < d.nsk; ++jlo)
+      for (int jhi = jlo; jhi < d.nsk; ++jhi) {
+        int64_t ncp = 1;
+        for (int j = jlo; j <= jhi; ++j) ncp *= S[i];
+        ncopies += ncp;
+        if (ncopies > UNIAP_MAX_COPIES)
+          FAIL(h, UNIAP_ERR_RANGE, "config %d: more than %d skip-conditioning copies", i, UNIAP_MAX_COPIES);
+        d.cprel[jlo * UNIAP_MAX_SKIP + jhi] = (int32_t)(off - d.offA);
+        off += ncp * 2 * L * NSP;
+      }
+    if (off - d.offA > INT32_MAX) FAIL(h, UNIAP_ERR_RANGE, "config %d: tables too large", i);
   }
   h->arena_words = off;
   h->P_words = poff;
@@ -546,11 +573,38 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
 // ---------------------------------------------------------------------------
 static void reset_counters(uniap_handle* h) { h->h2d = h->d2h = 0; h->launches = h->k2_launches = 0; }
 
-extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables* t) {
+extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables* tin) {
   if (!h) return UNIAP_ERR_ARG;
   h->ready = false;
   reset_counters(h);
-  if (!t || !t->cfg) FAIL(h, UNIAP_ERR_ARG, "null tables");
+  if (!tin || !tin->cfg) FAIL(h, UNIAP_ERR_ARG, "null tables");
+  const uniap_tables* t = tin;
+  // NEXT-4: skip sources given as a list (one source: the single-source path)
+  uniap_tables t1;
+  std::vector<uniap_config> c1;
+  std::vector<int> srcs;
+  if (tin->n_skip != 0) {
+    if (tin->n_skip < 0 || tin->n_skip > UNIAP_MAX_SKIP || !tin->skip_srcs || tin->skip_src != -1 || tin->n_cfg < 1 ||
+        tin->n_cfg > UNIAP_MAX_CFG)
+      FAIL(h, UNIAP_ERR_ARG, "n_skip=%d (1..%d sources with skip_src = -1)", tin->n_skip, UNIAP_MAX_SKIP);
+    for (int j = 0; j < tin->n_skip; ++j) {
+      if (tin->skip_srcs[j] < 0 || tin->skip_srcs[j] >= tin->L || (j > 0 && tin->skip_srcs[j] <= tin->skip_srcs[j - 1]))
+        FAIL(h, UNIAP_ERR_ARG, "skip_srcs must be ascending layer indices");
+      srcs.push_back(tin->skip_srcs[j]);
+    }
+    t1 = *tin;
+    c1.assign(tin->cfg, tin->cfg + tin->n_cfg);
+    if (tin->n_skip == 1) {
+      t1.skip_src = srcs[0];
+      for (auto& x : c1) { x.Rskip = x.Rskips; x.Rskips = nullptr; }
+      srcs.clear();
+    } else {
+      for (auto& x : c1) x.Rskip = nullptr;
+    }
+    t1.n_skip = 0;
+    t1.cfg = c1.data();
+    t = &t1;
+  }
   const int L = t->L;
   if (L < 1 || L > UNIAP_MAX_LAYERS) FAIL(h, UNIAP_ERR_ARG, "L=%d out of 1..64", L);
   if (t->cap < 0 || t->cap + 1 > UNIAP_MAX_Q) FAIL(h, UNIAP_ERR_ARG, "cap=%d out of 0..%d", t->cap, UNIAP_MAX_Q - 1);
@@ -589,8 +643,20 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
           if (r < 0 || r > UNIAP_MAX_ENTRY) FAIL(h, UNIAP_ERR_RANGE, "config %d: Rskip out of range at %d", i, u);
           ms = std::max<int64_t>(ms, r);
         }
+      for (size_t j = 0; x.Rskips && j < srcs.size(); ++j)  // NEXT-4: every source's edge into u
+        if (u >= srcs[j] + 2) {
+          int64_t mj = 0;
+          for (int k = 0; k < s * s; ++k) {
+            const int32_t r = x.Rskips[((int64_t)j * L + u) * s * s + k];
+            if (r < 0 || r > UNIAP_MAX_ENTRY) FAIL(h, UNIAP_ERR_RANGE, "config %d: Rskips out of range at %d", i, u);
+            mj = std::max<int64_t>(mj, r);
+          }
+          ms += mj;
+        }
       sum += ma + mr + ms;
     }
+    if (x.Rskips && !srcs.empty() && (x.Rcut || x.M_stage))
+      FAIL(h, UNIAP_ERR_ARG, "config %d: several skip sources with Rcut or M_stage are not supported", i);
     if (x.O)
       for (int e = 0; e < L - 1; ++e) {
         if (x.O[e] < 0 || x.O[e] > UNIAP_MAX_ENTRY) FAIL(h, UNIAP_ERR_RANGE, "config %d: O out of range", i);
@@ -657,7 +723,10 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
   h->any_cut = false;
   h->cut.assign(h->ncfg, 0);  // NEXT-1: a strategy-dependent cut cost matters only with cuts
   for (int i = 0; i < h->ncfg; ++i) h->cut[i] = t->cfg[i].Rcut && L > 1 && deg[i] >= 2 && deg[i] <= L;
-  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps, mts, mtn);
+  std::vector<std::vector<int>> msrc(h->ncfg);  // NEXT-4: the sources of configs with skip edges
+  for (int i = 0; i < h->ncfg; ++i)
+    if (t->cfg[i].Rskips && srcs.size() >= 2) msrc[i] = srcs;
+  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps, mts, mtn, &msrc);
   if (st != UNIAP_OK) return st;
   // pack the host tables into the device layout (pads: A 0, M cap+1, R 0)
   std::vector<int32_t> a(h->arena_words, 0);
@@ -691,6 +760,34 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
         for (int k = 0; k < sc; ++k)
           for (int l = 0; l < sc; ++l)
             a[d.offRc + ((int64_t)e * N + k) * N + l] = x.Rcut[((int64_t)e * s + kp[k]) * s + kp[l]];
+    // NEXT-4: per run of skip sources and strategy vector kappa of the run,
+    // A' = A + the run's skip-edge terms into every later layer, M' = M with
+    // each run source held on its strategy (the others forbidden)
+    for (int jlo = 0; jlo < d.nsk; ++jlo)
+      for (int jhi = jlo; jhi < d.nsk; ++jhi) {
+        int ncp = 1;
+        for (int j = jlo; j <= jhi; ++j) ncp *= sc;
+        for (int kap = 0; kap < ncp; ++kap) {
+          int kv[UNIAP_MAX_SKIP];
+          for (int j = jlo, r = kap; j <= jhi; ++j, r /= sc) kv[j] = r % sc;
+          const int64_t o = d.offA + copy_rel(d, jlo, jhi - jlo + 1, kap, L);
+          for (int u = 0; u < L; ++u)
+            for (int k = 0; k < N; ++k) {
+              int64_t av = 0;
+              int32_t mv = h->cap + 1;
+              if (k < sc) {
+                av = x.A[u * s + kp[k]];
+                mv = std::min(x.M[u * s + kp[k]], h->cap + 1);
+                for (int j = jlo; j <= jhi; ++j) {
+                  if (u >= srcs[j] + 2) av += x.Rskips[(((int64_t)j * L + u) * s + kp[kv[j]]) * s + kp[k]];
+                  if (u == srcs[j] && k != kv[j]) mv = h->cap + 1;
+                }
+              }
+              a[o + (int64_t)u * N + k] = (int32_t)av;
+              a[o + (int64_t)(L + u) * N + k] = mv;
+            }
+        }
+      }
   }
   CK(h, cudaSetDevice(h->device));
   CK(h, h->arena.ensure(h->arena_words));
@@ -1010,12 +1107,71 @@ static void plan_fast(int L, int i, int deg, int S, int skip, const Levels& lv, 
   }
 }
 
+// NEXT-4 (several skip sources, reading A-33): the sweeps of plan_fast (or
+// of the canonical all-intervals plan), each conditioned on the run of skip
+// sources it holds with an edge (skip_run over its longest interval), one
+// copy per strategy vector of the run, reading the copy's own A' (skip-edge
+// terms folded in) and M' (each conditioned source on its strategy) through
+// Inst::arel / Inst::mrel, so K2 runs them as plain sweeps; several copies
+// combine by atomicMin.  Extra conditioning of a shorter interval is
+// harmless (the minimum over the copies).  The suffix sweep runs once per
+// segment of start layers with the same run.
+static void plan_multi(int L, int i, const CfgDev& d, const Levels& lv, bool all_intervals, std::vector<Inst>& out) {
+  const int deg = d.deg, S = d.S;
+  if (!all_intervals && deg > L) return;
+  auto put = [&](Inst x, int a, int b) {  // one Inst per copy of the run of [a, b]
+    int jlo;
+    const int n = skip_run(d, a, b, &jlo);
+    int ncp = 1;
+    for (int j = 0; j < n; ++j) ncp *= S;
+    for (int kp = 0; kp < ncp; ++kp) {
+      const int64_t ar = copy_rel(d, jlo, n, kp, L);
+      x.emit = ncp > 1 ? 2 : 1;
+      x.arel = (int32_t)ar;
+      x.mrel = n ? (int32_t)(d.offA + ar + (int64_t)L * d.NSP - d.offM) : 0;
+      out.push_back(x);
+    }
+  };
+  auto fwd = [&](int a, int bmax, int lev) {
+    if (bmax < a) return;
+    const int n = bmax - a + 1;
+    put(Inst{i, a, n, -1, +1, 1, 0, a, bmax, n, lev, lv.lcap[lev]}, a, bmax);
+  };
+  if (all_intervals) {
+    for (int a = 0; a < L; ++a) fwd(a, L - 1, 0);
+    return;
+  }
+  if (deg == 1) {
+    fwd(0, L - 1, lv.lev_of[0]);
+    return;
+  }
+  fwd(0, L - deg, lv.lev_of[0]);
+  for (int l = 0; l < lv.nlev && deg >= 3; ++l)
+    for (int a = 1; a <= L - 2; ++a) {
+      int im = -1;
+      for (int st = 1; st <= std::min(a, deg - 2); ++st)
+        if (lv.lev_of[st] == l) im = st;
+      if (im >= 0) fwd(a, L - deg + im, l);
+    }
+  const int amin = deg - 1, b = L - 1, ll = lv.lev_of[deg - 1];
+  for (int a = amin; a <= b;) {  // suffixes [a, L-1], per segment of equal runs
+    int j0, j1;
+    const int n0 = skip_run(d, a, b, &j0);
+    int a2 = a;
+    while (a2 + 1 <= b && skip_run(d, a2 + 1, b, &j1) == n0 && j1 == j0) ++a2;
+    put(Inst{i, b, b - a + 1, -1, -1, 1, 0, a, a2, b - a + 1, ll, lv.lcap[ll]}, a, b);
+    a = a2 + 1;
+  }
+}
+
 static void forward_instances(const uniap_handle* h, int i, bool all_intervals, std::vector<Inst>& out) {
   const CfgDev& d = h->cfg[i];
   const size_t first = out.size();
-  if (all_intervals) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, h->cap, out);
+  if (d.nsk >= 2) plan_multi(h->L, i, d, h->lev[i], all_intervals, out);  // NEXT-4
+  else if (all_intervals) plan_instances(h->L, i, d.deg, d.S, d.skip, all_intervals, h->cap, out);
   else plan_fast(h->L, i, d.deg, d.S, d.skip, h->lev[i], h->cut[i], out);
-  for (size_t j = first; j < out.size(); ++j) out[j].mrel = (int32_t)(cfg_moff(d, out[j].lev, h->L) - d.offM);
+  if (d.nsk < 2)  // (NEXT-4 copies carry their own M' offsets)
+    for (size_t j = first; j < out.size(); ++j) out[j].mrel = (int32_t)(cfg_moff(d, out[j].lev, h->L) - d.offM);
   // Level 1: stop each forward P sweep where it becomes infeasible -- the
   // memory sum of Eq. 5 over the layers swept is at least the running sum of
   // the per-layer minima of the caller's M, so past the first layer where
@@ -1043,13 +1199,14 @@ static void forward_instances(const uniap_handle* h, int i, bool all_intervals, 
 // keep the candidate order, the least-loaded (then lowest) rank takes the next.
 static void lpt_shapes(int L, int Q, const std::vector<int>& deg, const std::vector<int>& S,
                        const std::vector<int>& skip, const std::vector<Levels>& lev, const std::vector<char>& cut,
-                       int world, std::vector<int>& owner) {
+                       int world, std::vector<int>& owner, const std::vector<CfgDev>* multi = nullptr) {
   const int n = (int)deg.size();
   std::vector<int> order(n);
   std::vector<double> w(n);
   for (int i = 0; i < n; ++i) {
     std::vector<Inst> v;
-    plan_fast(L, i, deg[i], S[i], skip[i], lev[i], cut[i], v);  // the executed sweeps
+    if (multi && (*multi)[i].nsk >= 2) plan_multi(L, i, (*multi)[i], lev[i], false, v);  // NEXT-4
+    else plan_fast(L, i, deg[i], S[i], skip[i], lev[i], cut[i], v);  // the executed sweeps
     double x = 1.0;  // + the combine
     for (auto& e : v) x += (double)e.n * S[i] * S[i] * Q;
     order[i] = i;
@@ -1070,11 +1227,13 @@ static void lpt_shapes(int L, int Q, const std::vector<int>& deg, const std::vec
 static void lpt(const uniap_handle* h, int world, std::vector<int>& owner) {
   std::vector<int> deg(h->ncfg), S(h->ncfg), sk(h->ncfg);
   for (int i = 0; i < h->ncfg; ++i) { deg[i] = h->cfg[i].deg; S[i] = h->cfg[i].S; sk[i] = h->cfg[i].skip; }
-  lpt_shapes(h->L, h->Q, deg, S, sk, h->lev, h->cut, world, owner);
+  lpt_shapes(h->L, h->Q, deg, S, sk, h->lev, h->cut, world, owner, &h->cfg);
 }
 
 extern "C" uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world, int32_t* owner_out) {
   if (!t || !t->cfg || !owner_out || world < 1 || t->n_cfg < 1 || t->L < 1) return UNIAP_ERR_ARG;
+  if (t->n_skip < 0 || t->n_skip > UNIAP_MAX_SKIP || (t->n_skip > 0 && !t->skip_srcs)) return UNIAP_ERR_ARG;
+  std::vector<CfgDev> mc(t->n_cfg, CfgDev{});  // NEXT-4: the shapes plan_multi needs
   std::vector<int> deg(t->n_cfg), S(t->n_cfg), sk(t->n_cfg), owner;
   std::vector<Levels> lev(t->n_cfg);
   std::vector<char> cut(t->n_cfg);
@@ -1100,8 +1259,13 @@ extern "C" uniap_status uniap_shard_tables(const uniap_tables* t, int32_t world,
     }
     S[i] = std::max(S[i], 1);
     sk[i] = (x.Rskip && t->skip_src >= 0) ? t->skip_src : -1;
+    if (t->n_skip == 1 && x.Rskips) sk[i] = t->skip_srcs[0];
+    if (t->n_skip >= 2 && x.Rskips) {
+      mc[i].deg = deg[i]; mc[i].S = S[i]; mc[i].NSP = round4(S[i]); mc[i].nsk = t->n_skip;
+      for (int j = 0; j < t->n_skip; ++j) mc[i].sk[j] = (int16_t)t->skip_srcs[j];
+    }
   }
-  lpt_shapes(t->L, t->cap + 1, deg, S, sk, lev, cut, world, owner);
+  lpt_shapes(t->L, t->cap + 1, deg, S, sk, lev, cut, world, owner, &mc);
   for (int i = 0; i < t->n_cfg; ++i) owner_out[i] = owner[i];
   return UNIAP_OK;
 }
@@ -1322,7 +1486,12 @@ static uniap_status make_plan(uniap_handle* h, int rank, int world, const uniap_
   R.max_deg = 0;
   for (int i : R.local) {
     const CfgDev& d = h->cfg[i];
-    const int copies = d.skip >= 0 ? d.S : 1;
+    int copies = d.skip >= 0 ? d.S : 1;
+    if (d.nsk >= 2) {  // NEXT-4: the copies of the run of all sources (bounds any stage's)
+      copies = 1;
+      for (int j = 0; j < d.nsk && copies <= UNIAP_MAX_COPIES; ++j) copies *= d.S;
+      copies = std::min(copies, UNIAP_MAX_COPIES);
+    }
     const int bound = d.deg + copies - 1;  // stages + extra skip copies of one stage
     gmax = std::max<int64_t>(gmax, (int64_t)copies * h->L * d.NSP * h->Q);
     R.max_deg = std::max(R.max_deg, std::min(d.deg, h->L));

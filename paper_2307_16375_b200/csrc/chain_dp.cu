@@ -167,8 +167,8 @@ __global__ void k2_closed_s1(const K2Args args, int n_inst) {
   const Inst in = args.inst[ii];
   const CfgDev& cf = args.cfg[in.cfg];
   const int NSP = cf.NSP, L = args.L, skip = cf.skip;
-  const int32_t* A = args.arena + cf.offA;
-  const int32_t* M = args.arena + cfg_moff(cf, in.lev, L);
+  const int32_t* A = args.arena + cf.offA + in.arel;  // (NEXT-4: the copy's A', skip terms folded in)
+  const int32_t* M = args.arena + cf.offM + in.mrel;  // (its level's / copy's memory table)
   const int32_t* Rf = args.arena + cf.offRf;
   const int32_t* Rs = args.arena + cf.offRs;
   int32_t* Pc = args.P + cf.offP + (int64_t)in.lev * L * L;

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
   const unsigned long long t_start = (args.trace || args.tim) ? gtimer() : 0ull;
   const Inst in = args.inst[ii];
   const CfgDev cf = args.cfg[in.cfg];
-  const int32_t* __restrict__ gA = args.arena + cf.offA;
+  const int32_t* __restrict__ gA = args.arena + cf.offA + in.arel;  // (NEXT-4: a conditioning copy's A')
   const int32_t* __restrict__ gM = args.arena + cf.offM + in.mrel;  // the sweep's memory table (1F1B: its stage's)
   const int32_t* __restrict__ gR = args.arena + (in.dir > 0 ? cf.offRt : cf.offRf);
   const int32_t* __restrict__ gRs = args.arena + cf.offRs;

@@ -598,6 +598,21 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     int a = 0;
     for (int i = 0; i < deg && st_ok; ++i) {
       const int b = E[1 + i], len = b - a + 1;
+      if (cf.nsk >= 2) {  // NEXT-4: one sweep per copy of the stage's run of skip sources
+        int jlo;
+        const int nr = skip_run(cf, a, b, &jlo);
+        int ncp = 1;
+        for (int j = 0; j < nr; ++j) ncp *= cf.S;
+        ra.bw->gofs[i * 33] = goff;  // copy kappa at goff + kappa * len * NSP * Q (k5c_walk)
+        for (int kp = 0; kp < ncp; ++kp) {
+          const int64_t ar = copy_rel(cf, jlo, nr, kp, L);
+          ra.bw_inst[n++] = Inst{ci, b, len, -1, -1, 0, goff, 0, -1, len, cf.lev_of[i], 0, -1,
+                                 nr ? (int32_t)(cf.offA + ar + (int64_t)L * cf.NSP - cf.offM) : 0, (int32_t)ar};
+          goff += (int64_t)len * cf.NSP * (ra.cap + 1);
+        }
+        a = b + 1;
+        continue;
+      }
       const bool cond = cf.skip >= 0 && a <= cf.skip && cf.skip + 2 <= b;
       for (int ks = cond ? 0 : -1; ks < (cond ? cf.S : 0); ++ks) {
         if (kept >= 0) {
@@ -641,7 +656,7 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
   const int stage = blockIdx.x;
   const Winner& W = *win;  // by reference: fields are read on demand, no per-thread copy
   if (W.cfg < 0 || W.objective == INT64_MAX || W.status != 0 || stage >= W.deg || rec->status != 0) return;
-  const CfgDev cf = cfgs[W.cfg];
+  const CfgDev& cf = cfgs[W.cfg];  // (by reference: the NEXT-4 path indexes its arrays)
   int skip;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int a = stage == 0 ? 0 : W.end[stage - 1] + 1, b = W.end[stage];
@@ -649,6 +664,82 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
   const bool cond = skip >= 0 && a <= skip && skip + 2 <= b;
   const int nks = cond ? cf.S : 1;
   const int NSP = cf.NSP, Q = cap + 1, S = cf.S;
+  if (cf.nsk >= 2) {  // NEXT-4: the stage's conditioning copies, 32 at a time (one per warp)
+    __shared__ int32_t best[MAXL];
+    __shared__ int32_t best_mem, have;
+    int jlo;
+    const int nr = skip_run(cf, a, b, &jlo);
+    int ncp = 1;
+    for (int j = 0; j < nr; ++j) ncp *= S;
+    const int len = b - a + 1;
+    if (threadIdx.x == 0) have = 0;
+    for (int c0 = 0; c0 < ncp; c0 += 32) {
+      const int cp = c0 + w;
+      bool ok = false;
+      if (cp < ncp) {
+        const int64_t ar = copy_rel(cf, jlo, nr, cp, L);
+        const int32_t* Ac = arena + cf.offA + ar;  // A' (skip-edge terms folded in)
+        const int32_t* Mc = nr ? Ac + (int64_t)L * NSP : arena + cf.offM;  // M' (run sources held)
+        const int32_t* Rfc = arena + cf.offRf;
+        const int32_t* g = G + bw->gofs[stage * 33] + (int64_t)cp * len * NSP * Q;
+        int64_t rest = W.p[stage];
+        int q = cfgs[W.cfg].lcap[cfgs[W.cfg].lev_of[stage]], kprev = -1;
+        int32_t msum = 0;
+        ok = true;
+        for (int u = a; u <= b && ok; ++u) {
+          const int k = lane;
+          bool c = false;
+          int32_t edge = 0, ap = 0, mk = 0;
+          if (k < S) {
+            mk = Mc[u * NSP + k];
+            const int32_t gv = g[((int64_t)(u - a) * NSP + k) * Q + q];
+            edge = (u > a) ? Rfc[((int64_t)(u - 1) * NSP + kprev) * NSP + k] : 0;
+            ap = Ac[u * NSP + k];
+            c = gv < INF && (int64_t)edge + gv == rest;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, c);
+          if (!m) { ok = false; break; }
+          const int kk = __ffs(m) - 1;
+          rest -= (int64_t)__shfl_sync(0xffffffffu, edge, kk) + __shfl_sync(0xffffffffu, ap, kk);
+          const int32_t m2 = __shfl_sync(0xffffffffu, mk, kk);
+          q -= m2;
+          msum += m2;
+          kprev = kk;
+          if (lane == 0) vec[w][u] = kk;
+        }
+        if (lane == 0) mem[w] = msum;
+      }
+      if (lane == 0) okw[w] = ok;
+      __syncthreads();
+      if (threadIdx.x == 0)  // the lexicographically smallest vector over the copies so far
+        for (int j = 0; j < 32 && c0 + j < ncp; ++j) {
+          if (!okw[j]) continue;
+          bool better = !have;
+          for (int u = a; u <= b && !better; ++u)
+            if (vec[j][u] != best[u]) { better = vec[j][u] < best[u]; break; }
+          if (better) {
+            for (int u = a; u <= b; ++u) best[u] = vec[j][u];
+            best_mem = mem[j];
+            have = 1;
+          }
+        }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      if (!have) {
+        rec->status = UNIAP_ERR_INTERNAL;
+      } else {
+        for (int u = a; u <= b; ++u) {
+          rec->strategy_of[u] = cfgs[W.cfg].orig[best[u]];
+          rec->stage_of[u] = stage;
+        }
+        rec->stage_mem[stage] = best_mem;
+        rec->stage_cost[stage] = W.p[stage];
+        rec->cut_cost[stage] = W.o[stage];
+      }
+    }
+    return;
+  }
   const int32_t* A = arena + cf.offA;
   const int32_t* M = arena + cfg_moff(cfgs[W.cfg], cfgs[W.cfg].lev_of[stage], L);  // the stage's memory table
   const int32_t* Rf = arena + cf.offRf;

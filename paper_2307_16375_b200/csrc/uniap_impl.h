@@ -53,6 +53,14 @@ struct CfgDev {
   int32_t nmt, pad3_;
   int8_t lmt[MAXLEV];
   int8_t mtn[MAXLEV];
+  // NEXT-4 (several skip sources, level 1): the sources sk[0..nsk) ascending
+  // (nsk >= 2; one source uses `skip`), and per contiguous run of them
+  // (index jlo * UNIAP_MAX_SKIP + jhi) the word offset from offA of its
+  // conditioning copies: |S|^(jhi - jlo + 1) table pairs [A'][M'] of L*NSP
+  // words each, copy kappa = mixed radix over the run's strategies (-1: none)
+  int32_t nsk;
+  int16_t sk[UNIAP_MAX_SKIP];
+  int32_t cprel[UNIAP_MAX_SKIP * UNIAP_MAX_SKIP];
   // NEXT-1 (strategy-dependent cut cost, Eq. 4): cut = 1 when the config has
   // Rcut [L-1][NSP][NSP] at offRc; its stage tables are then
   // T[a][b][kf][kl] ((NSP+1)^2 per interval, index NSP = that end free) at
@@ -64,6 +72,25 @@ struct CfgDev {
 // Word offset of the memory table of level `lev` of a config.
 __host__ __device__ inline int64_t cfg_moff(const CfgDev& cf, int lev, int L) {
   return cf.offM + (int64_t)cf.lmt[lev] * L * cf.NSP;
+}
+
+// NEXT-4: the contiguous run of skip sources a stage [a, b] conditions on
+// (every source s with a <= s and s + 2 <= b: it holds s and an edge of s);
+// returns its length, *jlo its first source (sources ascending).
+__host__ __device__ inline int skip_run(const CfgDev& cf, int a, int b, int* jlo) {
+  int n = 0;
+  *jlo = -1;
+  for (int j = 0; j < cf.nsk; ++j)
+    if (a <= cf.sk[j] && cf.sk[j] + 2 <= b) {
+      if (*jlo < 0) *jlo = j;
+      ++n;
+    }
+  return n;
+}
+// Word offset from offA of copy kappa's [A'][M'] tables of the run
+// [jlo, jlo + n) (0: the plain tables, n = 0).
+__host__ __device__ inline int64_t copy_rel(const CfgDev& cf, int jlo, int n, int kappa, int L) {
+  return n == 0 ? 0 : cf.cprel[jlo * UNIAP_MAX_SKIP + jlo + n - 1] + (int64_t)kappa * 2 * L * cf.NSP;
 }
 
 // One chain sweep of K2.
@@ -88,6 +115,7 @@ struct Inst {
   int32_t ecap;  // = lcap[lev]: the bucket whose state min_k D[k][ecap] is the stage optimum
   int32_t kf = -1;  // NEXT-1: the first layer swept restricted to strategy kf (-1: free)
   int32_t mrel = 0;  // the sweep's memory table: word offset from CfgDev::offM (lmt[lev] * L * NSP, 1F1B)
+  int32_t arel = 0;  // the sweep's execution-cost table: word offset from CfgDev::offA (NEXT-4 copies)
 };
 
 struct K2Args {

@@ -1,0 +1,94 @@
+"""GPU parity on DAGs with several skip sources (NEXT-4, reading A-33):
+layers in topological order with every chain edge plus edges from up to four
+sources to later layers; a stage conditions on each source it holds with an
+edge.  The library runs every conditioning copy as a plain chain sweep over
+its own A' / M' tables (uniap_tables.skip_srcs, uniap_config.Rskips).
+Bit-exact against the oracle (itself pinned by brute force in
+test_oracle_dag.py): the whole result, the production plan's interval tables,
+tracebacks over more copies than a CTA has warps."""
+import numpy as np
+import pytest
+
+from gen import tables
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("objective", "cfg_index", "deg", "c", "cfg_objective")
+ASSIGN = ("stage_of", "strategy_of", "stage_cost", "cut_cost", "stage_mem")
+
+
+@pytest.fixture(scope="module")
+def h():
+    import paper_2307_16375_b200 as pkg
+    hd = pkg.Handle(0)
+    yield hd
+    hd.close()
+
+
+def _same(g, o, what=""):
+    for k in KEYS:
+        assert g[k] == o[k], (what, k, g[k], o[k])
+    if o["objective"] != (1 << 63) - 1:
+        for k in ASSIGN:
+            assert g[k] == o[k], (what, k, g[k], o[k])
+
+
+@pytest.mark.parametrize("chunk", range(3))
+def test_dag_tiny_brute_checked(h, orc, chunk):
+    for seed in range(chunk * 500, (chunk + 1) * 500):
+        t = tables.with_skip_sources(tables.random_tables(110_000 + seed, skip_p=0.0), seed, 2 + seed % 2)
+        _same(h.solve_tables(t), orc.solve_tables(t), seed)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_dag_large_tables_and_intervals(h, orc, seed):
+    """2-4 sources, |S| up to 6, ragged Q up to 4096 (cluster sweeps too),
+    per-stage caps on some: the solve and every interval table entry the
+    production plan emits."""
+    from test_gpu_plan_parity import check
+    rng = np.random.default_rng(700 + seed)
+    L = int(rng.integers(8, 22))
+    Q = int(rng.choice([64, 300, 1025, 2048, 4096]))
+    cands = [(1, 2), (2, 4), (3, 2), (4, 8), (5, 3)]
+    S = [int(rng.choice([2, 3, 4, 6])) for _ in cands]
+    t = tables.large_random_tables(800 + seed, L, S, Q - 1, cands, stage_caps=seed % 3 == 0,
+                                   dist="ties" if seed % 4 == 1 else "uniform")
+    t = tables.with_skip_sources(t, seed, 2 + seed % 3, vmax=1 << 19)
+    got = h.solve_tables(t)
+    check(h, orc, t, h.fetch_intervals(), ("dag", seed))
+    _same(got, orc.solve_tables(t, n_threads=0), seed)
+
+
+@pytest.mark.parametrize("S,n_src", [(6, 3), (5, 4), (32, 2)])
+def test_dag_deg1_traceback_over_many_copies(h, orc, S, n_src):
+    """deg = 1 winners holding every source: up to 6^3 = 216 / 5^4 = 625 /
+    32^2 = 1024 copies in the traceback (more than a CTA's 32 warps)."""
+    L = 12 if S < 32 else 6
+    t = tables.large_random_tables(S * 10 + n_src, L, [S, S], 255, [(1, 1), (1, 3)], mem_max=20)
+    t = tables.with_skip_sources(t, S, n_src, vmax=1 << 19)
+    assert len(t["skip_srcs"]) == n_src
+    _same(h.solve_tables(t), orc.solve_tables(t, n_threads=0), (S, n_src))
+
+
+def test_one_source_list_equals_single_source_tables(h, orc):
+    for seed in range(200):
+        t = tables.random_tables(120_000 + seed, skip_p=1.0)
+        if t["skip_src"] < 0:
+            continue
+        m = dict(t, skip_src=-1, skip_srcs=[t["skip_src"]],
+                 cfgs=[dict(c, Rskip=None, Rskips=None if c["Rskip"] is None else c["Rskip"][None]) for c in t["cfgs"]])
+        _same(h.solve_tables(m), h.solve_tables(t), seed)
+
+
+def test_dag_limits_rejected(h):
+    t = tables.with_skip_sources(tables.random_tables(9, L=7, S_max=3, skip_p=0.0), 9, 2)
+    bad = dict(t, skip_srcs=list(reversed(t["skip_srcs"])))
+    with pytest.raises(Exception):
+        h.solve_tables(bad)
+    with pytest.raises(Exception):
+        h.solve_tables(dict(t, skip_src=1))
+    # |S| = 32 with 3 sources: 32^3 copies exceed UNIAP_MAX_COPIES
+    big = tables.large_random_tables(3, 10, [32], 63, [(2, 2)], mem_max=4)
+    big = tables.with_skip_sources(big, 3, 3, vmax=100)
+    with pytest.raises(Exception):
+        h.solve_tables(big)
