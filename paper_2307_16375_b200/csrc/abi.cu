@@ -496,7 +496,8 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     // (deg = 1: the whole chain, or its |S| skip-conditioned copies, is the
     // critical path of the step; measured: giving deg = 2's prefix + suffix
     // sweeps the same treatment starves the many-sweep classes of SMs)
-    std::vector<Inst> v;
+    static thread_local std::vector<Inst> v;  // (only counted: no allocation per config)
+    v.clear();
     const bool multi = msrc && (*msrc)[i].size() >= 2;  // NEXT-4: several skip sources
     if (multi) {
       CfgDev tmp{};
@@ -529,7 +530,7 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
       d.comp[keep[i][k]] = (int8_t)k;
     }
     d.offA = off; off += (int64_t)L * NSP;
-    const int nmt = std::max<int>(1, (int)mtn[i].size());
+    const int nmt = std::max<int>(1, (int)mtn[i].size());  // (empty: one table, GPipe)
     d.offM = off; off += (int64_t)nmt * L * NSP;  // the memory tables [nmt][L][NSP]
     d.offRt = off; off += (int64_t)(L - 1) * NSP * NSP;
     d.offRf = off; off += (int64_t)(L - 1) * NSP * NSP;
@@ -539,17 +540,18 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     d.offRc = off; off += h->cut[i] ? (int64_t)(L - 1) * NSP * NSP : 0;
     d.offT = h->T_words; h->T_words += h->cut[i] ? (int64_t)L * L * (NSP + 1) * (NSP + 1) : 0;
     const Levels& lv = h->lev[i];
-    d.nlev = lv.nlev;
-    for (int l = 0; l < MAXLEV; ++l) d.lcap[l] = (int16_t)(l < lv.nlev ? lv.lcap[l] : h->cap);
-    for (int l = 0; l < MAXLEV; ++l) d.lmt[l] = l < lv.nlev ? lv.lmt[l] : 0;
+    d.nlev = lv.nlev;  // (d is zero-initialised: lmt / mtn of unused levels / tables stay 0)
+    for (int l = 0; l < lv.nlev; ++l) {
+      d.lcap[l] = (int16_t)lv.lcap[l];
+      d.lmt[l] = lv.lmt[l];
+    }
     d.nmt = nmt;
-    for (int j = 0; j < MAXLEV; ++j) d.mtn[j] = j < (int)mtn[i].size() ? mtn[i][j] : 0;
-    for (int st = 0; st < MAXL; ++st) d.lev_of[st] = st < (int)lv.lev_of.size() ? lv.lev_of[st] : 0;
+    for (size_t j = 0; j < mtn[i].size(); ++j) d.mtn[j] = mtn[i][j];
+    for (int st = 0; st < std::min<int>(MAXL, (int)lv.lev_of.size()); ++st) d.lev_of[st] = lv.lev_of[st];
     d.offP = poff; poff += (int64_t)lv.nlev * L * L;  // one L*L interval table per level
     // NEXT-4: the conditioning copies of every contiguous run of skip sources
     d.nsk = multi ? (int)(*msrc)[i].size() : 0;
-    for (int j = 0; j < UNIAP_MAX_SKIP; ++j) d.sk[j] = (int16_t)(j < d.nsk ? (*msrc)[i][j] : -1);
-    for (int r = 0; r < UNIAP_MAX_SKIP * UNIAP_MAX_SKIP; ++r) d.cprel[r] = -1;
+    for (int j = 0; j < d.nsk; ++j) d.sk[j] = (int16_t)(*msrc)[i][j];
     int64_t ncopies = 0;
     for (int jlo = 0; jlo < d.nsk; ++jlo)
       for (int jhi = jlo; jhi < d.nsk; ++jhi) {
@@ -953,9 +955,9 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   // PAPER.md:122, reading A-32): one more table per distinct count below c
   std::vector<std::vector<int>> mts(h->ncfg);
   std::vector<std::vector<int8_t>> mtn(h->ncfg);
-  for (int i = 0; i < h->ncfg; ++i) {
+  for (int i = 0; i < h->ncfg && o->schedule == 1; ++i) {
     mtn[i].assign(1, 0);
-    if (o->schedule != 1 || deg[i] > L) continue;  // (deg > L: infeasible, reading A-22: GPipe's table)
+    if (deg[i] > L) continue;  // (deg > L: infeasible, reading A-22: GPipe's table)
     if (h->cut[i]) FAIL(h, UNIAP_ERR_ARG, "cut matrices with the 1F1B schedule are not supported");
     for (int stg = 0; stg < deg[i]; ++stg) {
       const int nf = std::min(c[i], deg[i] - stg);
@@ -971,7 +973,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps, mts, mtn);
   if (st != UNIAP_OK) return st;
   h->max_nmt = 1;
-  for (int i = 0; i < h->ncfg; ++i) h->max_nmt = std::max(h->max_nmt, (int)mtn[i].size());
+  for (int i = 0; i < h->ncfg; ++i) h->max_nmt = std::max(h->max_nmt, std::max(1, (int)mtn[i].size()));
   h->minM.clear();  // the sweep trim runs on the device (k1f_trim)
   h->minMoff.clear();
   h->cl = ClusterDev{cl->n_dev, cl->node_size, cl->ccoc_permille, o->B, o->precision, o->Q, NT, 0,

@@ -644,6 +644,92 @@ cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P
 // One CTA per stage; warp w walks the conditioning ks = w (or none).
 // Also writes the record (objective, placement, costs, memory).
 // ---------------------------------------------------------------------------
+// NEXT-4 part of k5c_walk (a separate function, so the one-source walk's
+// code is unchanged): the stage's conditioning copies, 32 at a time (one per
+// warp), each walked on its own A' / M' tables; the lexicographically
+// smallest vector over the copies.
+__device__ __noinline__ void k5c_walk_copies(const CfgDev& cf, const CfgDev* __restrict__ cfgs,
+                                             const int32_t* __restrict__ arena, const int32_t* __restrict__ G,
+                                             const BwPlan* __restrict__ bw, const Winner& W, int L, int cap,
+                                             uniap_record* __restrict__ rec, int stage, int a, int b,
+                                             int32_t (*vec)[MAXL], int32_t* mem, int32_t* okw) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NSP = cf.NSP, Q = cap + 1, S = cf.S;
+  __shared__ int32_t best[MAXL];
+  __shared__ int32_t best_mem, have;
+  int jlo;
+  const int nr = skip_run(cf, a, b, &jlo);
+  int ncp = 1;
+  for (int j = 0; j < nr; ++j) ncp *= S;
+  const int len = b - a + 1;
+  if (threadIdx.x == 0) have = 0;
+  for (int c0 = 0; c0 < ncp; c0 += 32) {
+    const int cp = c0 + w;
+    bool ok = false;
+    if (cp < ncp) {
+      const int64_t ar = copy_rel(cf, jlo, nr, cp, L);
+      const int32_t* Ac = arena + cf.offA + ar;  // A' (skip-edge terms folded in)
+      const int32_t* Mc = nr ? Ac + (int64_t)L * NSP : arena + cf.offM;  // M' (run sources held)
+      const int32_t* Rfc = arena + cf.offRf;
+      const int32_t* g = G + bw->gofs[stage * 33] + (int64_t)cp * len * NSP * Q;
+      int64_t rest = W.p[stage];
+      int q = cfgs[W.cfg].lcap[cfgs[W.cfg].lev_of[stage]], kprev = -1;
+      int32_t msum = 0;
+      ok = true;
+      for (int u = a; u <= b && ok; ++u) {
+        const int k = lane;
+        bool c = false;
+        int32_t edge = 0, ap = 0, mk = 0;
+        if (k < S) {
+          mk = Mc[u * NSP + k];
+          const int32_t gv = g[((int64_t)(u - a) * NSP + k) * Q + q];
+          edge = (u > a) ? Rfc[((int64_t)(u - 1) * NSP + kprev) * NSP + k] : 0;
+          ap = Ac[u * NSP + k];
+          c = gv < INF && (int64_t)edge + gv == rest;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, c);
+        if (!m) { ok = false; break; }
+        const int kk = __ffs(m) - 1;
+        rest -= (int64_t)__shfl_sync(0xffffffffu, edge, kk) + __shfl_sync(0xffffffffu, ap, kk);
+        const int32_t m2 = __shfl_sync(0xffffffffu, mk, kk);
+        q -= m2;
+        msum += m2;
+        kprev = kk;
+        if (lane == 0) vec[w][u] = kk;
+      }
+      if (lane == 0) mem[w] = msum;
+    }
+    if (lane == 0) okw[w] = ok;
+    __syncthreads();
+    if (threadIdx.x == 0)  // the lexicographically smallest vector over the copies so far
+      for (int j = 0; j < 32 && c0 + j < ncp; ++j) {
+        if (!okw[j]) continue;
+        bool better = !have;
+        for (int u = a; u <= b && !better; ++u)
+          if (vec[j][u] != best[u]) { better = vec[j][u] < best[u]; break; }
+        if (better) {
+          for (int u = a; u <= b; ++u) best[u] = vec[j][u];
+          best_mem = mem[j];
+          have = 1;
+        }
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (!have) {
+      rec->status = UNIAP_ERR_INTERNAL;
+    } else {
+      for (int u = a; u <= b; ++u) {
+        rec->strategy_of[u] = cfgs[W.cfg].orig[best[u]];
+        rec->stage_of[u] = stage;
+      }
+      rec->stage_mem[stage] = best_mem;
+      rec->stage_cost[stage] = W.p[stage];
+      rec->cut_cost[stage] = W.o[stage];
+    }
+  }
+  }
+
 __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs, const int32_t* __restrict__ arena,
                                                  const int32_t* __restrict__ G, const BwPlan* __restrict__ bw,
                                                  const Winner* __restrict__ win, int L, int cap,
@@ -664,80 +750,8 @@ __global__ void __launch_bounds__(1024) k5c_walk(const CfgDev* __restrict__ cfgs
   const bool cond = skip >= 0 && a <= skip && skip + 2 <= b;
   const int nks = cond ? cf.S : 1;
   const int NSP = cf.NSP, Q = cap + 1, S = cf.S;
-  if (cf.nsk >= 2) {  // NEXT-4: the stage's conditioning copies, 32 at a time (one per warp)
-    __shared__ int32_t best[MAXL];
-    __shared__ int32_t best_mem, have;
-    int jlo;
-    const int nr = skip_run(cf, a, b, &jlo);
-    int ncp = 1;
-    for (int j = 0; j < nr; ++j) ncp *= S;
-    const int len = b - a + 1;
-    if (threadIdx.x == 0) have = 0;
-    for (int c0 = 0; c0 < ncp; c0 += 32) {
-      const int cp = c0 + w;
-      bool ok = false;
-      if (cp < ncp) {
-        const int64_t ar = copy_rel(cf, jlo, nr, cp, L);
-        const int32_t* Ac = arena + cf.offA + ar;  // A' (skip-edge terms folded in)
-        const int32_t* Mc = nr ? Ac + (int64_t)L * NSP : arena + cf.offM;  // M' (run sources held)
-        const int32_t* Rfc = arena + cf.offRf;
-        const int32_t* g = G + bw->gofs[stage * 33] + (int64_t)cp * len * NSP * Q;
-        int64_t rest = W.p[stage];
-        int q = cfgs[W.cfg].lcap[cfgs[W.cfg].lev_of[stage]], kprev = -1;
-        int32_t msum = 0;
-        ok = true;
-        for (int u = a; u <= b && ok; ++u) {
-          const int k = lane;
-          bool c = false;
-          int32_t edge = 0, ap = 0, mk = 0;
-          if (k < S) {
-            mk = Mc[u * NSP + k];
-            const int32_t gv = g[((int64_t)(u - a) * NSP + k) * Q + q];
-            edge = (u > a) ? Rfc[((int64_t)(u - 1) * NSP + kprev) * NSP + k] : 0;
-            ap = Ac[u * NSP + k];
-            c = gv < INF && (int64_t)edge + gv == rest;
-          }
-          const unsigned m = __ballot_sync(0xffffffffu, c);
-          if (!m) { ok = false; break; }
-          const int kk = __ffs(m) - 1;
-          rest -= (int64_t)__shfl_sync(0xffffffffu, edge, kk) + __shfl_sync(0xffffffffu, ap, kk);
-          const int32_t m2 = __shfl_sync(0xffffffffu, mk, kk);
-          q -= m2;
-          msum += m2;
-          kprev = kk;
-          if (lane == 0) vec[w][u] = kk;
-        }
-        if (lane == 0) mem[w] = msum;
-      }
-      if (lane == 0) okw[w] = ok;
-      __syncthreads();
-      if (threadIdx.x == 0)  // the lexicographically smallest vector over the copies so far
-        for (int j = 0; j < 32 && c0 + j < ncp; ++j) {
-          if (!okw[j]) continue;
-          bool better = !have;
-          for (int u = a; u <= b && !better; ++u)
-            if (vec[j][u] != best[u]) { better = vec[j][u] < best[u]; break; }
-          if (better) {
-            for (int u = a; u <= b; ++u) best[u] = vec[j][u];
-            best_mem = mem[j];
-            have = 1;
-          }
-        }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      if (!have) {
-        rec->status = UNIAP_ERR_INTERNAL;
-      } else {
-        for (int u = a; u <= b; ++u) {
-          rec->strategy_of[u] = cfgs[W.cfg].orig[best[u]];
-          rec->stage_of[u] = stage;
-        }
-        rec->stage_mem[stage] = best_mem;
-        rec->stage_cost[stage] = W.p[stage];
-        rec->cut_cost[stage] = W.o[stage];
-      }
-    }
+  if (cf.nsk >= 2) {  // NEXT-4: the conditioning copies (k5c_walk_copies)
+    k5c_walk_copies(cf, cfgs, arena, G, bw, W, L, cap, rec, stage, a, b, vec, mem, okw);
     return;
   }
   const int32_t* A = arena + cf.offA;
