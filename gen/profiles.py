@@ -223,7 +223,7 @@ def toy_profile():
             "cluster": cluster, "options": dict(B=2, precision=0, Q=8, quantum_ns=0, cand=None)}
 
 
-def random_profile(seed, L=None, n=None, B=None, Q=None, skip=None, mat_dim=None, space=0):
+def random_profile(seed, L=None, n=None, B=None, Q=None, skip=None, mat_dim=None, space=0, n_skip=0):
     """Random small profile for builder / end-to-end parity tests.
 
     ``mat_dim``: if given, about half of the edges carry a random resharding
@@ -251,6 +251,15 @@ def random_profile(seed, L=None, n=None, B=None, Q=None, skip=None, mat_dim=None
         for v in range(s + 2, L):
             if rng.random() < 0.7:
                 edges.append({"src": s, "dst": v, "tensor_bytes_per_sample": int(rng.integers(0, 1 << 24))})
+    if n_skip:  # NEXT-4: a DAG with several skip sources (separate stream: the rest is unchanged)
+        drng = np.random.default_rng(seed + 9_000_000)
+        edges = [e for e in edges if e["dst"] == e["src"] + 1]
+        cand = list(range(0, max(L - 2, 0)))
+        srcs = sorted(int(x) for x in drng.choice(cand, size=min(n_skip, len(cand)), replace=False)) if cand else []
+        for s in srcs:
+            for v in range(s + 2, L):
+                if drng.random() < 0.6:
+                    edges.append({"src": s, "dst": v, "tensor_bytes_per_sample": int(drng.integers(0, 1 << 22))})
     node = int(rng.choice([d for d in (1, 2, 4, 8) if n % d == 0] or [1]))
     cluster = dict(n_dev=n, node_size=node, mem_bytes=int(rng.integers(1 << 30, 1 << 36)),
                    mem_reserve_bytes=int(rng.integers(0, 1 << 29)),

@@ -1094,7 +1094,7 @@ static int64_t cat_offset(int n, int g, int space) {
 
 int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, int32_t* buf,
               int64_t buf_len, int32_t* n_cfg_out, int32_t* skip_out, int64_t* quantum_out,
-              int64_t* words_out) {
+              int64_t* words_out, int32_t* n_skip_out, int32_t* skip_srcs_out) {
   if (!m || !cl || !o || m->L < 1 || m->L > ORC_MAX_L || !m->layers) return ORC_ERR_ARG;
   if (cl->n_dev < 1 || cl->node_size < 1 || cl->bw_intra < 1 || cl->bw_inter < 1 || cl->p2p_bw < 1 ||
       cl->lat_ns < 0 || cl->ccoc_permille < 0 || cl->ccoc_permille > 1000)
@@ -1122,40 +1122,60 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
           ly->act_bytes[i] > LIM)
         return ORC_ERR_ARG;
   }
-  /* edges: chain edges u->u+1, plus skip edges from one source s to v >= s+2 */
-  int skip = -1;
+  /* edges: chain edges u->u+1, plus skip edges from up to ORC_MAX_SKIP
+   * sources s to v >= s+2 (one source: T5's cross-attention; several: NEXT-4,
+   * reading A-33), sources ascending */
+  int nsrc = 0, srcs[ORC_MAX_SKIP];
   int64_t chain_tb[ORC_MAX_L];
   int has_chain[ORC_MAX_L];
-  int64_t skip_tb[ORC_MAX_L];
-  int has_skip[ORC_MAX_L];
+  int64_t skip_tb[ORC_MAX_SKIP][ORC_MAX_L];
+  int has_skip[ORC_MAX_SKIP][ORC_MAX_L];
   memset(has_chain, 0, sizeof has_chain);
   memset(has_skip, 0, sizeof has_skip);
   for (int e = 0; e < m->n_edges; ++e) {
     const orc_edge* ed = &m->edges[e];
     if (ed->src < 0 || ed->dst >= L || ed->src >= ed->dst || ed->tensor_bytes < 0 || ed->tensor_bytes > LIM)
       return ORC_ERR_ARG;
+    if (ed->dst != ed->src + 1) {
+      int j = 0;
+      while (j < nsrc && srcs[j] != ed->src) ++j;
+      if (j == nsrc) {
+        if (nsrc == ORC_MAX_SKIP) return ORC_ERR_ARG;
+        srcs[nsrc++] = ed->src;
+      }
+    }
+  }
+  for (int a = 0; a < nsrc; ++a) /* ascending */
+    for (int b = a + 1; b < nsrc; ++b)
+      if (srcs[b] < srcs[a]) { int x = srcs[a]; srcs[a] = srcs[b]; srcs[b] = x; }
+  for (int e = 0; e < m->n_edges; ++e) {
+    const orc_edge* ed = &m->edges[e];
     if (ed->dst == ed->src + 1) {
       if (has_chain[ed->src]) return ORC_ERR_ARG;
       has_chain[ed->src] = 1;
       chain_tb[ed->src] = ed->tensor_bytes;
     } else {
-      if (skip >= 0 && skip != ed->src) return ORC_ERR_ARG; /* one skip source (NEXT-4 otherwise) */
-      skip = ed->src;
-      if (has_skip[ed->dst]) return ORC_ERR_ARG;
-      has_skip[ed->dst] = 1;
-      skip_tb[ed->dst] = ed->tensor_bytes;
+      int j = 0;
+      while (srcs[j] != ed->src) ++j;
+      if (has_skip[j][ed->dst]) return ORC_ERR_ARG;
+      has_skip[j][ed->dst] = 1;
+      skip_tb[j][ed->dst] = ed->tensor_bytes;
     }
   }
+  const int skip = nsrc == 1 ? srcs[0] : -1;
   if (o->strategy_space != 0 && o->strategy_space != 1) return ORC_ERR_ARG;
   if (o->schedule != 0 && o->schedule != 1) return ORC_ERR_ARG;
   /* the concatenated catalogue Cat of the per-edge resharding matrices:
    * S(g) of every divisor g of n, ascending */
   const int64_t ncat = cat_offset(n, n + 1, o->strategy_space);
   const int64_t* chain_mat[ORC_MAX_L];
-  const int64_t* skip_mat[ORC_MAX_L];
+  const int64_t* skip_mat[ORC_MAX_SKIP][ORC_MAX_L];
   const int64_t* cut_mat[ORC_MAX_L];
   int any_cut = 0;
-  for (int u = 0; u < L; ++u) chain_mat[u] = skip_mat[u] = cut_mat[u] = NULL;
+  for (int u = 0; u < L; ++u) {
+    chain_mat[u] = cut_mat[u] = NULL;
+    for (int j = 0; j < ORC_MAX_SKIP; ++j) skip_mat[j][u] = NULL;
+  }
   for (int e = 0; e < m->n_edges; ++e) {
     const orc_edge* ed = &m->edges[e];
     if (ed->cut_ns) {
@@ -1169,7 +1189,11 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
     for (int64_t j = 0; j < (int64_t)ncat * ncat; ++j)
       if (ed->reshard_ns[j] < 0 || ed->reshard_ns[j] > LIM) return ORC_ERR_ARG;
     if (ed->dst == ed->src + 1) chain_mat[ed->src] = ed->reshard_ns;
-    else skip_mat[ed->dst] = ed->reshard_ns;
+    else {
+      int j = 0;
+      while (srcs[j] != ed->src) ++j;
+      skip_mat[j][ed->dst] = ed->reshard_ns;
+    }
   }
   int32_t cand_buf[2 * 4096];
   int n_cand;
@@ -1194,7 +1218,8 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
   /* words of config i's block (S = its strategy count) */
 #define BLKW(i, S)                                                                                              \
   (4 + 2 * (int64_t)L * (S) + (int64_t)(L - 1) * (S) * (S) + (int64_t)L * (S) * (S) + (L - 1) + cand[2 * (i)] + \
-   1 + (CUTS(i) ? (int64_t)(L - 1) * (S) * (S) : 0) + 1 + (o->schedule ? (int64_t)cand[2 * (i)] * L * (S) : 0))
+   1 + (CUTS(i) ? (int64_t)(L - 1) * (S) * (S) : 0) + 1 + (o->schedule ? (int64_t)cand[2 * (i)] * L * (S) : 0) + \
+   (nsrc >= 2 ? (int64_t)nsrc * L * (S) * (S) : 0))
   /* pass 1: sizes and the int64 ns/byte values */
   int64_t words = 0;
   int Ss[4096];
@@ -1208,6 +1233,8 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
   *words_out = words;
   *n_cfg_out = n_cand;
   *skip_out = skip;
+  if (n_skip_out) *n_skip_out = nsrc >= 2 ? nsrc : 0;
+  for (int j = 0; skip_srcs_out && j < nsrc; ++j) skip_srcs_out[j] = srcs[j];
   if (!buf || buf_len < words) return ORC_OK; /* size query */
   /* int64 tables (ns / bytes), then quantised into buf */
   int64_t* ns = (int64_t*)calloc((size_t)words, sizeof(int64_t));
@@ -1264,15 +1291,19 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
           if (v >= NS_LIMIT) st = ORC_ERR_RANGE;
           R[((int64_t)u * S + k) * S + l] = (int64_t)v;
         }
-    for (int v = 0; v < L && st == ORC_OK; ++v)
-      for (int k = 0; k < S; ++k)
-        for (int l = 0; l < S; ++l) {
-          u128 x = !has_skip[v] ? 0
-                   : skip_mat[v] ? (u128)b * (u128)skip_mat[v][(co + k) * ncat + co + l]
-                                 : t_reshard(cl, &cat[3 * k], &cat[3 * l], (u128)b * skip_tb[v]);
-          if (x >= NS_LIMIT) st = ORC_ERR_RANGE;
-          Rs[((int64_t)v * S + k) * S + l] = (int64_t)x;
-        }
+    /* skip edges (same formula per source): the single source's table in
+     * Rs; several sources' tables at the block's tail (after M_stage), Rs 0 */
+    int64_t* RSS = nsrc >= 2 ? blk + BLKW(i, S) - (int64_t)nsrc * L * S * S : Rs;
+    for (int j = 0; j < (nsrc ? nsrc : 1) && st == ORC_OK; ++j)
+      for (int v = 0; v < L && st == ORC_OK; ++v)
+        for (int k = 0; k < S; ++k)
+          for (int l = 0; l < S; ++l) {
+            u128 x = (nsrc == 0 || !has_skip[j][v]) ? 0
+                     : skip_mat[j][v] ? (u128)b * (u128)skip_mat[j][v][(co + k) * ncat + co + l]
+                                      : t_reshard(cl, &cat[3 * k], &cat[3 * l], (u128)b * skip_tb[j][v]);
+            if (x >= NS_LIMIT) st = ORC_ERR_RANGE;
+            RSS[(((int64_t)j * L + v) * S + k) * S + l] = (int64_t)x;
+          }
     /* cut cost o_j: the P2P of every edge crossing the cut, forward and
      * backward (o_j = fo_j + bo_j; readings A-1, A-16) */
     for (int e = 0; e + 1 < L && st == ORC_OK; ++e) {
@@ -1352,7 +1383,17 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
           for (int k = 0; k < S * S; ++k) mr = max64(mr, (R[(int64_t)(u - 1) * S * S + k] + qn - 1) / qn);
         if (skip >= 0 && u >= skip + 2)
           for (int k = 0; k < S * S; ++k) ms = max64(ms, (Rs[(int64_t)u * S * S + k] + qn - 1) / qn);
-        if (ma > ENTRY_MAX || mr > ENTRY_MAX || ms > ENTRY_MAX) ok = 0;
+        if (nsrc >= 2) { /* every source's edge into u (the sum bound of reading A-9) */
+          const int64_t* RSS = ns + off + BLKW(i, S) - (int64_t)nsrc * L * S * S;
+          for (int j = 0; j < nsrc; ++j) {
+            int64_t mj = 0;
+            if (u >= srcs[j] + 2)
+              for (int k = 0; k < S * S; ++k) mj = max64(mj, (RSS[((int64_t)j * L + u) * S * S + k] + qn - 1) / qn);
+            if (mj > ENTRY_MAX) ok = 0;
+            ms += mj;
+          }
+        }
+        if (ma > ENTRY_MAX || mr > ENTRY_MAX || (nsrc < 2 && ms > ENTRY_MAX)) ok = 0;
         sum += ma + mr + ms;
       }
       const int64_t* RC = O + (L - 1) + cand[2 * i] + 1;
@@ -1400,7 +1441,9 @@ int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o, i
         int64_t bk = byt < 0 ? (int64_t)cap + 1 : (byt + unit - 1) / unit;
         out[x1 + 1 + j] = (int32_t)(bk > cap ? cap + 1 : bk);
       }
-      off += x1 + 1 + nms;
+      int64_t nrs = nsrc >= 2 ? (int64_t)nsrc * L * S * S : 0; /* several sources' skip tables */
+      for (int64_t j = 0; j < nrs; ++j) out[x1 + 1 + nms + j] = (int32_t)((blk[x1 + 1 + nms + j] + qn - 1) / qn);
+      off += x1 + 1 + nms + nrs;
     }
   }
   free(ns);

@@ -128,11 +128,14 @@ typedef struct {
  *   [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1], stage_cap[deg],
  *    has_rcut, Rcut[L-1][S][S] if has_rcut, has_mstage, M_stage[deg][L][S] if has_mstage]
  * (has_rcut: some chain edge carries cut_ns and 2 <= deg <= L; has_mstage:
- * schedule = 1, M_stage[i] the memory buckets of stage i under 1F1B)
+ * schedule = 1, M_stage[i] the memory buckets of stage i under 1F1B); with
+ * several skip sources (NEXT-4) *skip_src = -1, *n_skip = their count,
+ * skip_srcs[0..n_skip) ascending (ORC_MAX_SKIP entries), Rskip is 0 and the
+ * block ends with Rskips[n_skip][L][S][S]; else *n_skip = 0.
  * into buf (int32).  *n_cfg, *skip_src, *quantum_ns, *words are outputs. */
 int orc_build(const orc_model* m, const orc_cluster* cl, const orc_options* o,
               int32_t* buf, int64_t buf_len, int32_t* n_cfg, int32_t* skip_src,
-              int64_t* quantum_ns, int64_t* words);
+              int64_t* quantum_ns, int64_t* words, int32_t* n_skip, int32_t* skip_srcs);
 
 /* Strategy catalogue S(g) (reading A-6): writes (t,f,d) triples, returns count.
  * space 0: every (t,f,d) with t*f*d = g, t a power of two; space 1:

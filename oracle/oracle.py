@@ -92,7 +92,8 @@ def lib():
         _lib.orc_interval_table.argtypes = [C.POINTER(_Tables), C.c_int, C.POINTER(C.c_int64)]
         _lib.orc_build.argtypes = [C.POINTER(_Model), C.POINTER(_Cluster), C.POINTER(_Options),
                                    C.POINTER(C.c_int32), C.c_int64, C.POINTER(C.c_int32),
-                                   C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         _lib.orc_catalogue.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32]
         _lib.orc_candidates.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32]
         for f in ("orc_allreduce_ns", "orc_allgather_ns"):
@@ -252,21 +253,24 @@ def _marshal_profile(p):
 def build_tables(p):
     """Builder': profile -> (tables dict, quantum_ns, flat int32 buffer)."""
     model, cluster, opts, keep = _marshal_profile(p)
-    n_cfg, skip, qn, words = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
+    n_cfg, skip, qn, words, nsk = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64(), C.c_int32()
+    srcs = (C.c_int32 * 8)()
     st = lib().orc_build(C.byref(model), C.byref(cluster), C.byref(opts), None, 0, C.byref(n_cfg),
-                         C.byref(skip), C.byref(qn), C.byref(words))
+                         C.byref(skip), C.byref(qn), C.byref(words), C.byref(nsk), srcs)
     if st != ORC_OK:
         raise OracleError(st, "build(size)")
     buf = np.zeros(words.value, dtype=np.int32)
     st = lib().orc_build(C.byref(model), C.byref(cluster), C.byref(opts), _ptr32(buf), words.value,
-                         C.byref(n_cfg), C.byref(skip), C.byref(qn), C.byref(words))
+                         C.byref(n_cfg), C.byref(skip), C.byref(qn), C.byref(words), C.byref(nsk), srcs)
     if st != ORC_OK:
         raise OracleError(st, "build")
-    return unpack_buffer(buf, p["model"]["L"], p["options"]["Q"] - 1, skip.value, n_cfg.value), qn.value, buf
+    return unpack_buffer(buf, p["model"]["L"], p["options"]["Q"] - 1, skip.value, n_cfg.value,
+                         list(srcs[:nsk.value])), qn.value, buf
 
 
-def unpack_buffer(buf, L, cap, skip_src, n_cfg):
-    """Split the builder block layout into a tables dict."""
+def unpack_buffer(buf, L, cap, skip_src, n_cfg, skip_srcs=()):
+    """Split the builder block layout into a tables dict (``skip_srcs``:
+    several skip sources, their tables at each block's tail)."""
     cfgs, off = [], 0
     for _ in range(n_cfg):
         deg, c, S, g = (int(x) for x in buf[off:off + 4])
@@ -285,10 +289,17 @@ def unpack_buffer(buf, L, cap, skip_src, n_cfg):
         MS = None
         if has_ms:
             MS = buf[off:off + deg * L * S].reshape(deg, L, S); off += deg * L * S
+        RSS = None
+        if len(skip_srcs) >= 2:
+            n = len(skip_srcs)
+            RSS = buf[off:off + n * L * S * S].reshape(n, L, S, S); off += n * L * S * S
         cfgs.append({"deg": deg, "c": c, "n_strat": S, "g": g, "A": A, "M": M, "R": R,
                      "Rskip": Rs if skip_src >= 0 else None, "O": O, "stage_cap": SC, "Rcut": RC,
-                     "M_stage": MS})
-    return {"L": L, "cap": cap, "skip_src": skip_src, "cfgs": cfgs}
+                     "M_stage": MS, "Rskips": RSS})
+    t = {"L": L, "cap": cap, "skip_src": skip_src, "cfgs": cfgs}
+    if len(skip_srcs) >= 2:
+        t["skip_srcs"] = list(skip_srcs)
+    return t
 
 
 def plan(p, n_threads=1):

@@ -80,3 +80,45 @@ def test_bad_skip_sources_rejected(orc):
     both = dict(t, skip_src=1)
     with pytest.raises(orc.OracleError):
         orc.solve_tables(both)
+
+
+def test_builder_several_sources_match_single_source_builds(orc):
+    """Level 2 (builder'): with two skip sources, each source's table equals
+    the Rskip table of the same profile keeping only that source's edges
+    (the same formula per edge, PAPER.md:134 / reading A-15); the cut costs
+    count every edge crossing the cut (reading A-16), so they equal the
+    all-edges profile's."""
+    from gen import profiles
+    checked = 0
+    for seed in range(40):
+        p = profiles.random_profile(6000 + seed, L=6, Q=64, n_skip=2)
+        p = dict(p, options=dict(p["options"], quantum_ns=1 << 10))  # one quantum for every variant
+        t, _, _ = orc.build_tables(p)
+        if "skip_srcs" not in t:
+            continue
+        for j, s in enumerate(t["skip_srcs"]):
+            edges = [e for e in p["model"]["edges"] if e["dst"] == e["src"] + 1 or e["src"] == s]
+            pj = dict(p, model=dict(p["model"], edges=edges))
+            tj, _, _ = orc.build_tables(pj)
+            assert tj["skip_src"] == s
+            for c, cj in zip(t["cfgs"], tj["cfgs"]):
+                assert np.array_equal(c["Rskips"][j], cj["Rskip"]), (seed, j)
+                assert np.array_equal(c["A"], cj["A"]) and np.array_equal(c["M"], cj["M"])
+        checked += 1
+    assert checked >= 20
+
+
+def test_builder_several_sources_brute_force(orc):
+    from gen import profiles
+    n = 0
+    for seed in range(60):
+        p = profiles.random_profile(5000 + seed, L=5, Q=16, n_skip=2 + seed % 2)
+        t, _, _ = orc.build_tables(p)
+        if max(c["n_strat"] for c in t["cfgs"]) ** t["L"] * 16 > 2_000_000:
+            continue
+        want, got = brute.solve_tables(t), orc.solve_tables(t)
+        for k in KEYS:
+            if k in want:
+                assert got[k] == want[k], (seed, k)
+        n += "skip_srcs" in t
+    assert n >= 20

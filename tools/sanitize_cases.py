@@ -47,8 +47,20 @@ def main(cases):
         for c in t["cfgs"]:
             c["Rcut"] = rng.integers(0, 1 << 16, size=(8, c["n_strat"], c["n_strat"])).astype(np.int32)
         same(h.solve_tables(t), oracle.solve_tables(t, n_threads=0), "cut cost")
+    if "1f1b" in cases:  # NEXT-2 1F1B: per-stage memory tables (levels, K4 from global memory at 16 levels)
+        t = tables.with_1f1b(tables.large_random_tables(63, 20, [3, 4, 2], 255, [(4, 8), (16, 32), (2, 2)],
+                                                        mem_max=10), 63, act_max=3)
+        same(h.solve_tables(t), oracle.solve_tables(t, n_threads=0), "1f1b tables")
+        p = profiles.make_profile("bert")
+        p = dict(p, options=dict(p["options"], schedule=1))
+        want, _ = oracle.plan(p, n_threads=0)
+        same(h.plan(p), want, "bert 1f1b plan")
+    if "dag" in cases:  # NEXT-4: several skip sources (copy tables, per-copy traceback over > 32 copies)
+        t = tables.with_skip_sources(tables.large_random_tables(64, 12, [6, 4], 511, [(1, 1), (3, 2)], mem_max=60),
+                                     64, 3, vmax=1 << 18)
+        same(h.solve_tables(t), oracle.solve_tables(t, n_threads=0), "dag tables")
     h.close()
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["toy", "bert", "cluster", "skip", "levels", "cut"])
+    main(sys.argv[1:] or ["toy", "bert", "cluster", "skip", "levels", "cut", "1f1b", "dag"])
