@@ -189,7 +189,9 @@ typedef struct {
 
 typedef struct {
   int32_t src, dst;                   /* src < dst; dst == src+1 (chain) or a skip edge from
-                                         the single skip source to dst >= src+2               */
+                                         one of at most UNIAP_MAX_SKIP skip sources to dst >=
+                                         src+2 (several sources: NEXT-4, see uniap_tables.n_skip;
+                                         the builder emits per-source skip tables)             */
   int64_t tensor_bytes_per_sample;    /* activation bytes crossing the edge per sample (the
                                          cut cost o_j, Eq. 4 with a constant R', reading A-1)  */
   const int64_t* reshard_ns_per_sample; /* NULL, or the edge's resharding matrix R_uv
@@ -255,7 +257,9 @@ uniap_status uniap_plan(uniap_handle* h, const uniap_model* m, const uniap_clust
  * order, as int32 blocks
  *    [deg, c, S, g, A[L][S], M[L][S], R[L-1][S][S], Rskip[L][S][S], O[L-1], stage_cap[deg],
  *     has_rcut, Rcut[L-1][S][S] if has_rcut, has_mstage, M_stage[deg][L][S] if has_mstage]
- * (has_mstage = options.schedule; M is GPipe's table either way)
+ * (has_mstage = options.schedule; M is GPipe's table either way); with several
+ * skip sources (NEXT-4) *skip_src = -1, Rskip is 0 and the block ends with
+ * Rskips[n_src][L][S][S] (sources ascending, the model's skip-edge sources)
  * Call with buf == NULL to get *words; then with buf_len >= *words. */
 uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
                                 const uniap_options* o, int32_t* buf, int64_t buf_len, int64_t* words,

@@ -384,6 +384,7 @@ class Handle:
                                              buf.ctypes.data_as(_P32), words.value, C.byref(words),
                                              C.byref(ncfg), C.byref(skip), C.byref(qn)), "build")
         L, cap = p["model"]["L"], p["options"]["Q"] - 1
+        srcs = sorted({e["src"] for e in p["model"]["edges"] if e["dst"] != e["src"] + 1})
         cfgs, off = [], 0
         for _ in range(ncfg.value):
             deg, c, S, g = (int(x) for x in buf[off:off + 4])
@@ -406,9 +407,16 @@ class Handle:
             if has_ms:
                 blk["M_stage"] = buf[off:off + deg * L * S].reshape(deg, L, S)
                 off += deg * L * S
+            blk["Rskips"] = None
+            if len(srcs) >= 2:  # NEXT-4: each skip source's table at the block's tail
+                blk["Rskips"] = buf[off:off + len(srcs) * L * S * S].reshape(len(srcs), L, S, S)
+                off += len(srcs) * L * S * S
             cfgs.append({"deg": deg, "c": c, "n_strat": S, "g": g, **blk,
                          "Rskip": blk["Rskip"] if skip.value >= 0 else None})
-        return {"L": L, "cap": cap, "skip_src": skip.value, "cfgs": cfgs}, qn.value, buf
+        t = {"L": L, "cap": cap, "skip_src": skip.value, "cfgs": cfgs}
+        if len(srcs) >= 2:
+            t["skip_srcs"] = srcs
+        return t, qn.value, buf
 
     # ---- split pipeline ----
     def prepare(self, p):

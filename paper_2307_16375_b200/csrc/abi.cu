@@ -218,6 +218,7 @@ struct uniap_handle {
   std::vector<int32_t> minM;
   std::vector<size_t> minMoff;  // per config: its block of minM, [memory table][layer]
   int max_nmt = 1;              // level 2: the largest memory-table count of a config (K1a's grid)
+  int n_src = 0;                // level 2: skip sources of the model (NEXT-4: several)
   // per-stage memory caps (NEXT-2): per config its levels and stage caps
   std::vector<Levels> lev;
   std::vector<std::vector<int32_t>> scap;
@@ -236,7 +237,7 @@ struct uniap_handle {
 // nothing they depend on changed (shapes, classes, offsets, buffers, and the
 // kernel-parameter values of the builder); otherwise both are rebuilt.
 static void update_signature(uniap_handle* h) {
-  std::vector<int64_t> sg = {h->L, h->Q, h->ncfg, h->skip, h->level2, h->n_edges, h->arena_words};
+  std::vector<int64_t> sg = {h->L, h->Q, h->ncfg, h->skip, h->level2, h->n_edges, h->arena_words, h->n_src};
   for (int32_t m : h->minM) sg.push_back(m);  // level 1: the plan's sweep lengths depend on them
   for (int i = 0; i < h->ncfg; ++i) {
     const CfgDev& d = h->cfg[i];
@@ -534,7 +535,7 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
     d.offM = off; off += (int64_t)nmt * L * NSP;  // the memory tables [nmt][L][NSP]
     d.offRt = off; off += (int64_t)(L - 1) * NSP * NSP;
     d.offRf = off; off += (int64_t)(L - 1) * NSP * NSP;
-    d.offRs = off; off += (int64_t)L * NSP * NSP;
+    d.offRs = off; off += (int64_t)(multi ? (*msrc)[i].size() : 1) * L * NSP * NSP;  // (NEXT-4: per source)
     d.offO = off; off += std::max(4, round4(L - 1));
     d.cut = h->cut[i];
     d.offRc = off; off += h->cut[i] ? (int64_t)(L - 1) * NSP * NSP : 0;
@@ -613,6 +614,7 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
   if (t->skip_src < -1 || t->skip_src >= L) FAIL(h, UNIAP_ERR_ARG, "skip_src=%d", t->skip_src);
   if (t->n_cfg < 1 || t->n_cfg > UNIAP_MAX_CFG) FAIL(h, UNIAP_ERR_ARG, "n_cfg=%d", t->n_cfg);
   h->L = L; h->cap = t->cap; h->Q = t->cap + 1; h->skip = t->skip_src; h->ncfg = t->n_cfg; h->level2 = false;
+  h->n_src = 0;
   std::vector<int> S(h->ncfg), deg(h->ncfg), c(h->ncfg), g(h->ncfg, 0), skc(h->ncfg);
   std::vector<std::vector<int>> keep(h->ncfg), mts(h->ncfg);
   std::vector<std::vector<const int32_t*>> tabs(h->ncfg);
@@ -855,6 +857,18 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   const int64_t ncat = cat_off[n + 1];
   int skip = -1;
   std::vector<int64_t> ed, rmat, chain_mat(L, -1), skip_mat(L, -1), cut_mat(L, -1);
+  // skip sources (one: T5's path; several: NEXT-4, reading A-33), ascending;
+  // skipb / skip_mat hold one row of L per source
+  std::vector<int> srcs;
+  for (int i = 0; i < m->n_edges; ++i) {
+    const uniap_edge& e = m->edges[i];
+    if (e.dst != e.src + 1 && std::find(srcs.begin(), srcs.end(), e.src) == srcs.end()) srcs.push_back(e.src);
+  }
+  if ((int)srcs.size() > UNIAP_MAX_SKIP) FAIL(h, UNIAP_ERR_ARG, "more than %d skip sources", UNIAP_MAX_SKIP);
+  std::sort(srcs.begin(), srcs.end());
+  const int nsrc_rows = std::max<int>(1, (int)srcs.size());
+  skipb.assign((size_t)nsrc_rows * L, -1);
+  skip_mat.assign((size_t)nsrc_rows * L, -1);
   bool any_cut = false;
   for (int i = 0; i < m->n_edges; ++i) {
     const uniap_edge& e = m->edges[i];
@@ -864,10 +878,10 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
       if (chain[e.src] >= 0) FAIL(h, UNIAP_ERR_ARG, "duplicate edge %d->%d", e.src, e.dst);
       chain[e.src] = e.tensor_bytes_per_sample;
     } else {
-      if (skip >= 0 && skip != e.src) FAIL(h, UNIAP_ERR_ARG, "more than one skip source (general DAGs: NEXT-4)");
-      skip = e.src;
-      if (skipb[e.dst] >= 0) FAIL(h, UNIAP_ERR_ARG, "duplicate edge %d->%d", e.src, e.dst);
-      skipb[e.dst] = e.tensor_bytes_per_sample;
+      const int j = (int)(std::find(srcs.begin(), srcs.end(), e.src) - srcs.begin());
+      if (srcs.size() == 1) skip = e.src;
+      if (skipb[(size_t)j * L + e.dst] >= 0) FAIL(h, UNIAP_ERR_ARG, "duplicate edge %d->%d", e.src, e.dst);
+      skipb[(size_t)j * L + e.dst] = e.tensor_bytes_per_sample;
     }
     ed.push_back(e.src); ed.push_back(e.dst); ed.push_back(e.tensor_bytes_per_sample);
     if (e.cut_ns_per_sample) {  // NEXT-1: a cut after a chain edge only
@@ -883,7 +897,8 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
     }
     if (e.reshard_ns_per_sample) {
       if (ncat * ncat > ((int64_t)1 << 24)) FAIL(h, UNIAP_ERR_ARG, "resharding matrix too large (|Cat| = %lld)", (long long)ncat);
-      (e.dst == e.src + 1 ? chain_mat[e.src] : skip_mat[e.dst]) = (int64_t)rmat.size();
+      if (e.dst == e.src + 1) chain_mat[e.src] = (int64_t)rmat.size();
+      else skip_mat[(size_t)(std::find(srcs.begin(), srcs.end(), e.src) - srcs.begin()) * L + e.dst] = (int64_t)rmat.size();
       for (int64_t j = 0; j < ncat * ncat; ++j) {
         const int64_t v = e.reshard_ns_per_sample[j];
         if (v < 0 || v > LIM) FAIL(h, UNIAP_ERR_ARG, "edge %d: resharding matrix entry out of [0, 2^46]", i);
@@ -970,7 +985,11 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
       mts[i].push_back(j);
     }
   }
-  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps, mts, mtn);
+  std::vector<std::vector<int>> msrc(h->ncfg);  // NEXT-4: several skip sources (every config)
+  if (srcs.size() >= 2)
+    for (int i = 0; i < h->ncfg; ++i) msrc[i] = srcs;
+  h->n_src = (int)srcs.size();
+  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps, mts, mtn, &msrc);
   if (st != UNIAP_OK) return st;
   h->max_nmt = 1;
   for (int i = 0; i < h->ncfg; ++i) h->max_nmt = std::max(h->max_nmt, std::max(1, (int)mtn[i].size()));
@@ -992,9 +1011,9 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   {  // one pinned staging block -> one device blob, one DMA
     constexpr int NB = 15;  // ... qglob, zeroed by the same copy (no memset node), then the cut offsets
     const size_t sz[NB] = {fwd.size() * 8, act.size() * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8, (size_t)L * 8,
-                           (size_t)L * 8, std::max<size_t>(ed.size(), 3) * 8, h->ncfg * sizeof(CfgDev),
+                           skipb.size() * 8, std::max<size_t>(ed.size(), 3) * 8, h->ncfg * sizeof(CfgDev),
                            h->ncfg * sizeof(CatDev), std::max<size_t>(rmat.size(), 1) * 8, (size_t)L * 8,
-                           (size_t)L * 8, 3 * 8, (size_t)L * 8};
+                           skip_mat.size() * 8, 3 * 8, (size_t)L * 8};
     const size_t used[NB] = {sz[0], sz[1], sz[2], sz[3], sz[4], sz[5], sz[6], ed.size() * 8, sz[8], sz[9],
                              rmat.size() * 8, sz[11], sz[12], 0, sz[14]};
     const void* src[NB] = {fwd.data(), act.data(), ps.data(), ctx.data(), tpc.data(), chain.data(), skipb.data(),
@@ -1420,7 +1439,7 @@ static BuildBufs build_bufs(uniap_handle* h) {
   return BuildBufs{h->fwd.p, h->act.p, h->ps.p, h->ctx.p, h->tpc.p, h->chain.p, h->skipb.p, h->edges.p,
                    h->n_edges, h->rmat.p, h->chain_mat.p, h->skip_mat.p, h->any_cut ? h->cut_mat.p : nullptr,
                    h->dcat.p, nullptr, nullptr, nullptr, 0, nullptr, h->ns.p, h->qcfg.p, h->qmax.p, h->qglob.p,
-                   h->max_nmt};
+                   h->max_nmt, std::max(1, h->n_src)};
 }
 
 // ---------------------------------------------------------------------------
@@ -1622,7 +1641,7 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
     bb.work = h->work.p;
     CK(h, launch_k1(h->cl, bb, h->dcfg.p, h->ncfg, L, h->skip, h->arena.p, h->st));
     CK(h, cudaStreamWaitEvent(h->st, h->side_ev[0], 0));
-    h->launches += 3;
+    h->launches += 3 + (h->n_src >= 2);  // (K1g: NEXT-4 copies)
   } else {
     CK(h, cudaMemsetAsync(h->tim.p, 0, 2 * sizeof(unsigned long long), h->st));  // forward phase clock
     CK(h, launch_fill(h->P.p, h->P_words, INF, h->st));
@@ -1853,7 +1872,8 @@ extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m
   int64_t need = 0;
   for (auto& d : h->cfg)
     need += 4 + 2 * (int64_t)L * d.S + (int64_t)(L - 1) * d.S * d.S + (int64_t)L * d.S * d.S + (L - 1) + d.deg + 1 +
-            (d.cut ? (int64_t)(L - 1) * d.S * d.S : 0) + 1 + (o->schedule ? (int64_t)d.deg * L * d.S : 0);
+            (d.cut ? (int64_t)(L - 1) * d.S * d.S : 0) + 1 + (o->schedule ? (int64_t)d.deg * L * d.S : 0) +
+            (d.nsk >= 2 ? (int64_t)d.nsk * L * d.S * d.S : 0);
   if (words) *words = need;
   if (n_cfg) *n_cfg = h->ncfg;
   if (skip_src) *skip_src = h->skip;
@@ -1880,9 +1900,9 @@ extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m
     for (int e = 0; e + 1 < L; ++e)
       for (int k = 0; k < S; ++k)
         for (int l = 0; l < S; ++l) buf[w++] = a[d.offRf + ((int64_t)e * N + k) * N + l];
-    for (int v = 0; v < L; ++v)
+    for (int v = 0; v < L; ++v)  // (several sources: 0 here, their tables at the block's tail)
       for (int k = 0; k < S; ++k)
-        for (int l = 0; l < S; ++l) buf[w++] = a[d.offRs + ((int64_t)v * N + k) * N + l];
+        for (int l = 0; l < S; ++l) buf[w++] = d.nsk >= 2 ? 0 : a[d.offRs + ((int64_t)v * N + k) * N + l];
     for (int e = 0; e + 1 < L; ++e) buf[w++] = a[d.offO + e];
     for (int st = 0; st < d.deg; ++st) buf[w++] = h->scap[i].empty() ? h->cap : h->scap[i][st];
     buf[w++] = d.cut;  // NEXT-1: has_rcut, then Rcut
@@ -1895,6 +1915,10 @@ extern "C" uniap_status uniap_build_tables(uniap_handle* h, const uniap_model* m
       for (int u = 0; u < L; ++u)
         for (int k = 0; k < S; ++k) buf[w++] = a[mo + u * N + k];
     }
+    for (int j = 0; j < (d.nsk >= 2 ? d.nsk : 0); ++j)  // NEXT-4: each source's skip table
+      for (int v = 0; v < L; ++v)
+        for (int k = 0; k < S; ++k)
+          for (int l = 0; l < S; ++l) buf[w++] = a[d.offRs + (((int64_t)j * L + v) * N + k) * N + l];
   }
   return UNIAP_OK;
 }

@@ -171,9 +171,12 @@ __device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const Cfg
   const CfgDev& cf = cfgs[blockIdx.y];
   const int SF = cf.Sfull, NSP = cf.NSP, n2 = NSP * NSP;
   const bool isR = slot < L - 1;
-  const int e = isR ? slot : slot - (L - 1);  // R: edge e -> e+1; Rskip: destination v = e
-  int64_t* dst = bb.ns + (isR ? cf.offRf : cf.offRs) + (int64_t)e * n2;
-  const int64_t tb = isR ? bb.chain[e] : bb.skipb[e];
+  // R: edge e -> e+1; Rskip: destination v = e of skip source js (NEXT-4:
+  // one row of L slots per source, tables [source][v] from offRs)
+  const int js = isR ? 0 : (slot - (L - 1)) / L;
+  const int e = isR ? slot : slot - (L - 1) - js * L;
+  int64_t* dst = bb.ns + (isR ? cf.offRf : cf.offRs + (int64_t)js * L * n2) + (int64_t)e * n2;
+  const int64_t tb = isR ? bb.chain[e] : bb.skipb[(int64_t)js * L + e];
   const int32_t* tfd = bb.cat[blockIdx.y].tfd;
   if (tb < 0) {  // no such edge: all zero
     for (int j = threadIdx.x; j < n2; j += blockDim.x) dst[j] = 0;
@@ -183,7 +186,7 @@ __device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const Cfg
   const Coll co{cl};
   // the caller's matrix of this edge ("R_uv"; b * per-sample
   // value, the block of S(g)), else the built-in formula (reading A-15)
-  const int64_t mo = isR ? bb.chain_mat[e] : bb.skip_mat[e];
+  const int64_t mo = isR ? bb.chain_mat[e] : bb.skip_mat[(int64_t)js * L + e];
   const CatDev& cd = bb.cat[blockIdx.y];
   const int gmax = min(cf.g, K1G);
   if (mo < 0) {
@@ -208,9 +211,23 @@ __device__ void k1b_reshard(const ClusterDev& cl, const BuildBufs& bb, const Cfg
   }
   for (int j = threadIdx.x; j < n2; j += blockDim.x)  // pad rows / columns
     if (j / NSP >= cf.S || j % NSP >= cf.S) dst[j] = 0;
-  // per-layer maxima for the quantum: R of edge e goes into layer e+1
-  if (mx > 0 && (isR || (cf.skip >= 0 && e >= cf.skip + 2)))
-    amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + (isR ? e + 1 : e)) * QMS + (isR ? 1 : 2), mx);
+  // per-layer maxima for the quantum: R of edge e goes into layer e+1; the
+  // skip slot sums one maximum per source (every source's edge into v can be
+  // in a stage together: the sum bound of reading A-9)
+  const int sj = cf.nsk >= 2 ? cf.sk[js] : cf.skip;
+  if (mx > 0 && isR) amax(bb.qmax + ((int64_t)blockIdx.y * MAXL + e + 1) * QMS + 1, mx);
+  if (!isR && sj >= 0 && e >= sj + 2) {  // (uniform) the block's maximum, added once
+    __shared__ int64_t wmx[32];
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mx, o));
+    if ((threadIdx.x & 31) == 0) wmx[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = max(mx, wmx[w]);
+      if (mx > 0)
+        atomicAdd(reinterpret_cast<unsigned long long*>(bb.qmax + ((int64_t)blockIdx.y * MAXL + e) * QMS + 2),
+                  (unsigned long long)mx);
+    }
+  }
 }
 
 // K1c: cut costs: every edge crossing the cut after layer e, fwd + bwd P2P
@@ -457,7 +474,7 @@ __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restri
   const int64_t q = bb.qglob[0] > 0 ? bb.qglob[0] : 1;
   const int cap = cl.Q - 1;
   const int64_t unit = (cl.mem_bytes - cl.mem_reserve) / cap;  // reading A-8
-  const int nA = L * NSP, nR = (L - 1) * n2, nS = L * n2, nO = ((L - 1) + 3) & ~3;
+  const int nA = L * NSP, nR = (L - 1) * n2, nS = (cf.nsk >= 2 ? cf.nsk : 1) * L * n2, nO = ((L - 1) + 3) & ~3;
   const int nRc = cf.cut ? (L - 1) * n2 : 0;  // NEXT-1 Rcut block
   const int nMt = cf.nmt * nA;                  // the memory tables
   const bool pow2 = (q & (q - 1)) == 0;
@@ -488,18 +505,78 @@ __global__ void k1f_quantise(ClusterDev cl, BuildBufs bb, const CfgDev* __restri
   }
 }
 
+// K1g (NEXT-4, several skip sources): the conditioning copies of every
+// contiguous run of sources (CfgDev::cprel) from the quantised tables --
+// A' = A + the run's skip-edge terms into every later layer, M' = M with each
+// run source held on its strategy of the copy (the others forbidden); the
+// same rule as the level-1 packing (uniap_prepare_tables).
+__global__ void k1g_copies(const CfgDev* __restrict__ cfgs, int L, int cap, int32_t* arena) {
+  pdl_wait();  // K1f's quantised tables (PDL)
+  const CfgDev& cf = cfgs[blockIdx.y];
+  if (cf.nsk < 2) return;
+  const int S = cf.S, N = cf.NSP, n2 = N * N;
+  const int64_t pair = 2 * (int64_t)L * N;
+  int64_t total = 0;
+  for (int jlo = 0; jlo < cf.nsk; ++jlo)
+    for (int jhi = jlo; jhi < cf.nsk; ++jhi) {
+      int64_t ncp = 1;
+      for (int j = jlo; j <= jhi; ++j) ncp *= S;
+      total += ncp * pair;
+    }
+  const int32_t* A = arena + cf.offA;
+  const int32_t* M = arena + cf.offM;
+  const int32_t* Rs = arena + cf.offRs;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    // the run holding word idx (runs in layout order: jlo, then jhi)
+    int64_t rem = idx;
+    int jlo = 0, jhi = 0;
+    for (jlo = 0; jlo < cf.nsk; ++jlo) {
+      bool found = false;
+      for (jhi = jlo; jhi < cf.nsk; ++jhi) {
+        int64_t ncp = 1;
+        for (int j = jlo; j <= jhi; ++j) ncp *= S;
+        if (rem < ncp * pair) { found = true; break; }
+        rem -= ncp * pair;
+      }
+      if (found) break;
+    }
+    const int kap = (int)(rem / pair);
+    const int w = (int)(rem - (int64_t)kap * pair);
+    const bool isM = w >= L * N;
+    const int u = (w % (L * N)) / N, k = w % N;
+    int32_t v;
+    if (k >= S) {
+      v = isM ? cap + 1 : 0;
+    } else if (isM) {
+      v = M[u * N + k];
+      for (int j = jlo, r = kap; j <= jhi; ++j, r /= S)
+        if (u == cf.sk[j] && k != r % S) v = cap + 1;
+    } else {
+      v = A[u * N + k];
+      for (int j = jlo, r = kap; j <= jhi; ++j, r /= S)
+        if (u >= cf.sk[j] + 2) v += Rs[(((int64_t)j * L + u) * N + r % S) * N + k];
+    }
+    arena[cf.offA + cf.cprel[jlo * UNIAP_MAX_SKIP + jhi] + (int64_t)kap * pair + w] = v;
+  }
+  (void)n2;
+}
+
 cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* cfg, int ncfg, int L, int skip,
                       int32_t* arena, cudaStream_t st) {
   // qmax / qglob are zeroed by uniap_prepare and left zeroed by K1d (qmax,
   // done counter); the range flags qglob[1] are sticky for the prepared input
   const int nbA = (bb.max_nmt * L * 32 + K1T - 1) / K1T;  // (NSP <= 32) x the memory tables
-  const int nbR = 2 * L - 1;  // one block per edge slot: L-1 chain edges, L skip destinations
+  const int nbR = (L - 1) + bb.n_src * L;  // one block per edge slot: L-1 chain edges, L skip destinations per source
   const int nbE = bb.cut_mat ? L - 1 : 0;  // NEXT-1 cut-cost blocks (per chain edge)
   k1_costs<<<dim3(nbA + nbR + nbE + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR, nbE);
   cudaError_t e = pdl_launch(k1d_quantum, dim3(ncfg), dim3(64), 0, st, cl, bb, cfg, L, skip);
   if (e != cudaSuccess) return e;
   e = pdl_launch(k1f_quantise, dim3(16 + (bb.inst ? bb.n_trim : 0), ncfg), dim3(256), 0, st, cl, bb, cfg, L, arena);
   if (e != cudaSuccess) return e;
+  if (bb.n_src >= 2) {  // NEXT-4: the conditioning copies
+    e = pdl_launch(k1g_copies, dim3(32, ncfg), dim3(256), 0, st, cfg, L, cl.Q - 1, arena);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

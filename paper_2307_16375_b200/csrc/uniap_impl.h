@@ -327,6 +327,7 @@ struct BuildBufs {
   int64_t* qmax;          // [ncfg][MAXL][5] per layer: max A, max R into u, max Rskip into u, O[u], max Rcut[u]
   int64_t* qglob;         // [3]: quantum, error flags, completion counter of K1d
   int32_t max_nmt = 1;    // the largest memory-table count of a config (K1a's grid)
+  int32_t n_src = 1;      // rows of skipb / skip_mat (skip sources, at least 1; NEXT-4: several)
 };
 cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* cfg, int ncfg, int L, int skip,
                       int32_t* arena, cudaStream_t st);

@@ -92,3 +92,48 @@ def test_dag_limits_rejected(h):
     big = tables.with_skip_sources(big, 3, 3, vmax=100)
     with pytest.raises(Exception):
         h.solve_tables(big)
+
+
+def test_dag_profiles_builder_and_plan(h, orc):
+    """Level 2: random profiles with 2-4 skip sources -- K1's per-source skip
+    tables and K1g's conditioning copies: builder tables bit-equal to
+    builder', plan = the oracle's."""
+    from gen import profiles
+    n = 0
+    for seed in range(30):
+        rng = np.random.default_rng(seed)
+        p = profiles.random_profile(7000 + seed, L=int(rng.integers(5, 12)), Q=int(rng.choice([16, 64, 256])),
+                                    n_skip=2 + seed % 3)
+        try:
+            t, qn, buf = orc.build_tables(p)
+        except orc.OracleError:
+            with pytest.raises(Exception):
+                h.build_tables(p)
+            continue
+        ns = len(t.get("skip_srcs") or [])
+        copies = max(sum(c["n_strat"] ** (j1 - j0 + 1) for j0 in range(ns) for j1 in range(j0, ns))
+                     for c in t["cfgs"]) if ns >= 2 else 0
+        if copies > 4096:  # beyond UNIAP_MAX_COPIES: the library refuses (documented limit)
+            with pytest.raises(Exception, match="skip-conditioning copies"):
+                h.build_tables(p)
+            continue
+        gt, gq, gbuf = h.build_tables(p)
+        assert gq == qn and np.array_equal(gbuf, buf), seed
+        _same(h.plan(p), orc.solve_tables(t, n_threads=0), seed)
+        n += ns >= 2
+    assert n >= 12
+
+
+def test_t5_with_a_second_source_profile(h, orc):
+    """The T5-like profile plus edges from a second source (an extra encoder
+    tap 11 -> 13..23): two skip sources at full size."""
+    from gen import profiles
+    p = profiles.make_profile("t5")
+    edges = list(p["model"]["edges"]) + [{"src": 11, "dst": v, "tensor_bytes_per_sample": 512 * 1024 * 4}
+                                         for v in range(13, 24)]
+    p = dict(p, model=dict(p["model"], edges=edges))
+    t, qn, buf = orc.build_tables(p)
+    assert t.get("skip_srcs") == [11, 23]
+    gt, gq, gbuf = h.build_tables(p)
+    assert gq == qn and np.array_equal(gbuf, buf)
+    _same(h.plan(p), orc.solve_tables(t, n_threads=0), "t5 two sources")
