@@ -206,15 +206,20 @@ def main():
     RB = pkg.RECORD_BYTES
     rec = torch.zeros(RB, dtype=torch.uint8, device="cuda")
     all_recs = torch.zeros(ws * RB, dtype=torch.uint8, device="cuda")
+    hdrs = torch.zeros(ws * RB, dtype=torch.uint8, device="cuda")  # phase-1 records (uniap_run_phase)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     # ---------------- device-resident: profile uploaded once ----------------
     h.prepare(profile)
 
     def step():
-        h.run(rank, ws, rec.data_ptr())
-        if ws > 1:
+        if ws > 1:  # split run: only the owner of the global winner runs a traceback
+            h.run_phase(rank, ws, rec.data_ptr(), 1)
+            dist.all_gather_into_tensor(hdrs, rec)
+            h.run_phase(rank, ws, rec.data_ptr(), 2, hdrs.data_ptr())
             dist.all_gather_into_tensor(all_recs, rec)
+        else:
+            h.run(rank, ws, rec.data_ptr())
 
     for _ in range(args.warmup):
         step()
@@ -278,8 +283,7 @@ def main():
         t0 = time.perf_counter()
         if ws > 1:
             h.prepare(prof)                     # validation + H2D of the profile
-            h.run(rank, ws, rec.data_ptr())
-            dist.all_gather_into_tensor(all_recs, rec)
+            step()
             host = all_recs.cpu().numpy().tobytes()   # D2H of every rank's record
             st, res = pkg.pick(host, ws)
         else:

@@ -278,6 +278,18 @@ uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, const uniap_cl
                            const uniap_options* o);
 uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables* t);
 uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev);
+/* The same run in two halves, so that across ranks only the owner of the
+ * global winner runs a traceback (the stage strategies of Algorithm 1's
+ * output): phase 1 runs everything up to this rank's local
+ * winner and writes its record HEADER (objective, cfg_index, deg, c, status,
+ * counters) into rec_dev; the caller gathers the `world` records (e.g. one
+ * NCCL all_gather) into a device array recs_dev; phase 2 picks the global
+ * winner on the device by uniap_pick's key and, on the rank holding it only,
+ * runs the traceback into rec_dev; then one more gather and uniap_pick.  Both
+ * phases are enqueued on the handle's stream without host synchronisation;
+ * phase 2 must follow phase 1 of the same (rank, world, rec_dev). */
+uniap_status uniap_run_phase(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev, int32_t phase,
+                             const void* recs_dev);
 uniap_status uniap_fetch(uniap_handle* h, uniap_result* out);
 
 typedef struct {                      /* fixed-size record exchanged between ranks            */

@@ -87,7 +87,7 @@ RECORD_BYTES = C.sizeof(uniap_record)
 
 EXPORTS = ("uniap_create", "uniap_destroy", "uniap_last_error", "uniap_status_string", "uniap_version",
            "uniap_solve_tables", "uniap_interval_table", "uniap_plan", "uniap_build_tables", "uniap_prepare",
-           "uniap_prepare_tables", "uniap_run", "uniap_fetch", "uniap_shard_assign", "uniap_shard_tables",
+           "uniap_prepare_tables", "uniap_run", "uniap_run_phase", "uniap_fetch", "uniap_shard_assign", "uniap_shard_tables",
            "uniap_pick", "uniap_selftest", "uniap_fetch_intervals",
            "uniap_candidates", "uniap_catalogue")
 
@@ -119,6 +119,7 @@ def lib():
         L.uniap_prepare.argtypes = [H, C.POINTER(uniap_model), C.POINTER(uniap_cluster), C.POINTER(uniap_options)]
         L.uniap_prepare_tables.argtypes = [H, C.POINTER(uniap_tables)]
         L.uniap_run.argtypes = [H, C.c_int32, C.c_int32, C.c_void_p]
+        L.uniap_run_phase.argtypes = [H, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]
         L.uniap_fetch.argtypes = [H, C.POINTER(uniap_result)]
         L.uniap_fetch_intervals.argtypes = [H, _P32, C.c_int64, _P64]
         L.uniap_shard_assign.argtypes = [H, C.c_int32, _P32]
@@ -433,6 +434,13 @@ class Handle:
     def run(self, rank=0, world=1, rec_dev_ptr=None):
         self._check(lib().uniap_run(self._h, rank, world, C.c_void_p(rec_dev_ptr) if rec_dev_ptr else None), "run")
 
+    def run_phase(self, rank, world, rec_dev_ptr, phase, recs_dev_ptr=None):
+        """uniap_run_phase: 1 = up to this rank's local winner (record header),
+        2 = the traceback on the rank holding the global winner of the gathered
+        phase-1 records (device array of `world` records)."""
+        self._check(lib().uniap_run_phase(self._h, rank, world, C.c_void_p(rec_dev_ptr), phase,
+                                          C.c_void_p(recs_dev_ptr) if recs_dev_ptr else None), f"run_phase({phase})")
+
     def fetch(self):
         cfg_obj = (C.c_int64 * max(self.n_cfg, 1))()
         r = uniap_result()
@@ -444,29 +452,46 @@ class Handle:
 
     def plan_distributed(self, p, group=None):
         """Multi-GPU plan, one process per GPU: this rank runs
-        its LPT share of the candidate configs (uniap_run(rank, world)) on its
-        device, writing its best record into a device buffer; ONE all_gather of
-        the fixed-size records over the process group (NCCL over NVLink: the
-        device buffers directly; gloo: through host memory); uniap_pick on the
-        host.  Returns the picked result dict (every rank gets the same) plus
-        this rank's local per-config optima.  torch supplies only the memory
-        and the process group."""
+        its LPT share of the candidate configs on its device up to its local
+        winner (uniap_run_phase 1), writing the record header into a device
+        buffer; the headers are all_gathered over the process group (NCCL over
+        NVLink: the device buffers directly; gloo: through host memory); phase 2
+        runs the traceback only on the rank holding the global winner; a
+        second all_gather of the fixed-size records and uniap_pick on the host.
+        (world = 1: one uniap_run.)  Returns the picked result dict (every
+        rank gets the same) plus this rank's local per-config optima.  torch
+        supplies only the memory and the process group."""
         import torch
         import torch.distributed as dist
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         self.prepare(p)
         dev = torch.device("cuda", self.device)
-        rec = torch.zeros(RECORD_BYTES, dtype=torch.uint8, device=dev)
-        self.run(rank, world, rec.data_ptr())
-        local = self.fetch()  # synchronises the handle's stream: rec is complete
-        if dist.get_backend(group) == "nccl":
-            allr = torch.empty(world * RECORD_BYTES, dtype=torch.uint8, device=dev)
-            dist.all_gather_into_tensor(allr, rec, group=group)
-            host = allr.cpu().numpy().tobytes()
+        # persistent record buffers: the captured graphs keep their pointers
+        if getattr(self, "_dist_bufs", (None,))[0] != world:
+            self._dist_bufs = (world, torch.zeros(RECORD_BYTES, dtype=torch.uint8, device=dev),
+                               torch.zeros(world * RECORD_BYTES, dtype=torch.uint8, device=dev))
+        _, rec, allr = self._dist_bufs
+        nccl = dist.get_backend(group) == "nccl"
+
+        def gather():
+            if nccl:
+                dist.all_gather_into_tensor(allr, rec, group=group)
+                torch.cuda.current_stream(dev).synchronize()
+            else:
+                parts = [torch.empty(RECORD_BYTES, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(parts, rec.cpu(), group=group)
+                allr.copy_(torch.cat(parts))
+            return allr
+
+        if world == 1:
+            self.run(rank, world, rec.data_ptr())
         else:
-            parts = [torch.empty(RECORD_BYTES, dtype=torch.uint8) for _ in range(world)]
-            dist.all_gather(parts, rec.cpu(), group=group)
-            host = b"".join(x.numpy().tobytes() for x in parts)
+            self.run_phase(rank, world, rec.data_ptr(), 1)
+            self.fetch()  # synchronises the handle's stream: the header is complete
+            hdrs = gather()
+            self.run_phase(rank, world, rec.data_ptr(), 2, hdrs.data_ptr())
+        local = self.fetch()  # synchronises the handle's stream: rec is complete
+        host = gather().cpu().numpy().tobytes()
         st, out = pick(host, world)
         out["status"] = st
         out["cfg_objective_local"] = local.get("cfg_objective")

@@ -195,6 +195,8 @@ struct uniap_handle {
   DevBuf<unsigned long long> work;         // level 2: per config executed {cells, relax} (k1f_trim)
   DevBuf<int32_t> inst_csr;                // per config: its forward instances (offsets [ncfg+1], indices)
   cudaGraphExec_t graph_exec = nullptr;    // the captured pipeline of `plan`
+  cudaGraphExec_t graph_ph[2] = {nullptr, nullptr};  // its two halves (uniap_run_phase 1 / 2)
+  const void* ph2_recs = nullptr;          // the gathered records phase 2's graph reads
   uint32_t graph_launches = 0, graph_k2 = 0;
   bool capturing = false, timed = false;
   bool no_compact = false;  // uniap_build_tables: keep every strategy in the tables
@@ -233,6 +235,12 @@ struct uniap_handle {
   int64_t zstride = 0;
 };
 
+static void drop_graphs(uniap_handle* h) {
+  if (h->graph_exec) { cudaGraphExecDestroy(h->graph_exec); h->graph_exec = nullptr; }
+  for (auto& g : h->graph_ph)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+
 // A prepared problem keeps the launch plan and the captured graph when
 // nothing they depend on changed (shapes, classes, offsets, buffers, and the
 // kernel-parameter values of the builder); otherwise both are rebuilt.
@@ -264,10 +272,7 @@ static void update_signature(uniap_handle* h) {
   if (sg != h->sig) {
     h->sig.swap(sg);
     h->plan.valid = false;
-    if (h->graph_exec) {
-      cudaGraphExecDestroy(h->graph_exec);
-      h->graph_exec = nullptr;
-    }
+    drop_graphs(h);
   }
 }
 
@@ -429,7 +434,7 @@ extern "C" void uniap_destroy(uniap_handle* h) {
   for (auto* b : {&h->ns, &h->vals, &h->cfgopt, &h->qcfg, &h->gofs, &h->qmax, &h->gstore}) b->release();
   h->upb.release();
   h->dcfg1.release();
-  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+  drop_graphs(h);
   h->clsid.release();
   h->bwp.release();
   h->k4best.release();
@@ -1620,9 +1625,18 @@ static uniap_status enqueue_k4_range(uniap_handle* h, int li0, int cnt, cudaStre
 
 // The whole path for this rank, enqueued on h->st with no host
 // synchronisation (so it can be captured as one CUDA graph).
-static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
+// phase 0: the whole path; 1: up to the local winner (K5a: the record's
+// header), no traceback; 2: k_decide against the gathered phase-1 records
+// `recs` (the traceback runs only on the rank holding the global winner),
+// then the traceback and the publication.
+static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec, int phase = 0, const uniap_record* recs = nullptr) {
   const RunPlan& R = h->plan;
   const int L = h->L, nl = (int)R.local.size();
+  auto* fd = h->fb_dev;
+  if (phase == 2) {  // phase 2 starts from the gathered phase-1 records
+    CK(h, launch_decide(recs, R.world, R.rank, h->bwp.p, h->win.p, h->st));
+    h->launches++;
+  } else {
   if (h->trace.p) CK(h, cudaMemsetAsync(h->trace.p, 0, 8, h->st));
   if (h->level2) {
     // the P fill overlaps the builder (side stream, joined before K2)
@@ -1667,6 +1681,8 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->ends.p, h->cfgopt.p, h->win.p,
                    h->k4best.p, ra, h->st));
   h->launches += 1;
+  }  // (phase != 2)
+  if (phase != 1) {
   // traceback: backward sweeps sized on the device, then the strategy walk
   {
     uniap_status s = enqueue_k2(h, R.bgrp, h->binst.p, h->bwp.p->count, h->P.p);
@@ -1674,8 +1690,8 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
   }
   CK(h, launch_k5c_grid(R.max_deg, h->dcfg.p, h->arena.p, h->G.p, h->bwp.p, h->win.p, L, h->cap, rec, h->st));
   if (R.max_deg > 0) h->launches++;
+  }  // (phase != 1)
   // the results into the mapped host block (uniap_fetch: one sync, no copies)
-  auto* fd = h->fb_dev;
   CK(h, launch_publish(reinterpret_cast<int32_t*>(&fd->rec), rec, fd->qg, h->level2 ? h->qglob.p : nullptr, fd->tm,
                        h->tim.p, fd->cfgopt, h->cfgopt.p, h->ncfg, h->st));
   h->launches++;
@@ -1683,7 +1699,7 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec) {
 }
 
 
-extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev) {
+static uniap_status run_phase(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev, int phase, const void* recs) {
   if (!h) return UNIAP_ERR_ARG;
   if (!h->ready) FAIL(h, UNIAP_ERR_ARG, "nothing prepared");
   if (world < 1 || rank < 0 || rank >= world) FAIL(h, UNIAP_ERR_ARG, "rank %d / world %d", rank, world);
@@ -1699,10 +1715,16 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
     CK(h, cudaHostGetDevicePointer((void**)&h->fb_dev, h->fb, 0));
   }
   if (!h->plan.valid || h->plan.rank != rank || h->plan.world != world || h->plan.rec != rec) {
-    if (h->graph_exec) { cudaGraphExecDestroy(h->graph_exec); h->graph_exec = nullptr; }
+    drop_graphs(h);
     uniap_status s = make_plan(h, rank, world, rec);
     if (s != UNIAP_OK) return s;
   }
+  if (phase == 2 && h->ph2_recs != recs && h->graph_ph[1]) {  // its graph reads the gathered records
+    cudaGraphExecDestroy(h->graph_ph[1]);
+    h->graph_ph[1] = nullptr;
+  }
+  if (phase == 2) h->ph2_recs = recs;
+  cudaGraphExec_t& gx = phase == 0 ? h->graph_exec : h->graph_ph[phase - 1];
   if (getenv("UNIAP_TRACE") && !h->trace.p) {  // diagnostics: allocated before any capture
     CK(h, h->trace.ensure(4 + 4 * (size_t)TRACE_CAP));
     const unsigned long long hdr[2] = {0ull, (unsigned long long)TRACE_CAP};
@@ -1713,18 +1735,18 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
   const bool use_graph = !env_flag("UNIAP_NO_GRAPH");
   CK(h, cudaEventRecord(h->ev[0], h->st));
   if (use_graph) {
-    if (!h->graph_exec) {
+    if (!gx) {
       // capture the pipeline once; replay it on every later run of this plan
       const uint32_t l0 = h->launches, k0 = h->k2_launches;
       CK(h, cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
       h->capturing = true;
-      uniap_status s = enqueue_pipeline(h, rec);
+      uniap_status s = enqueue_pipeline(h, rec, phase, (const uniap_record*)recs);
       h->capturing = false;
       cudaGraph_t g = nullptr;
       cudaError_t e = cudaStreamEndCapture(h->st, &g);
       if (s != UNIAP_OK) { if (g) cudaGraphDestroy(g); return s; }
       CK(h, e);
-      e = cudaGraphInstantiate(&h->graph_exec, g, cudaGraphInstantiateFlagUseNodePriority);  // K2 launch priorities
+      e = cudaGraphInstantiate(&gx, g, cudaGraphInstantiateFlagUseNodePriority);  // K2 launch priorities
       cudaGraphDestroy(g);
       CK(h, e);
       h->graph_launches = h->launches - l0;
@@ -1732,17 +1754,32 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
       h->launches = l0;
       h->k2_launches = k0;
     }
-    CK(h, cudaGraphLaunch(h->graph_exec, h->st));
+    CK(h, cudaGraphLaunch(gx, h->st));
     h->launches += h->graph_launches;
     h->k2_launches += h->graph_k2;
   } else {
-    uniap_status s = enqueue_pipeline(h, rec);
+    uniap_status s = enqueue_pipeline(h, rec, phase, (const uniap_record*)recs);
     if (s != UNIAP_OK) return s;
   }
   CK(h, cudaEventRecord(h->ev[3], h->st));
   CK(h, cudaGetLastError());
   h->timed = true;
   return UNIAP_OK;
+}
+
+extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev) {
+  return run_phase(h, rank, world, rec_dev, 0, nullptr);
+}
+
+extern "C" uniap_status uniap_run_phase(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev, int32_t phase,
+                                        const void* recs_dev) {
+  if (!h) return UNIAP_ERR_ARG;
+  if (phase != 1 && phase != 2) FAIL(h, UNIAP_ERR_ARG, "phase %d (1 or 2)", phase);
+  if (!rec_dev) FAIL(h, UNIAP_ERR_ARG, "a split run needs the record device buffer");
+  if (phase == 2 && !recs_dev) FAIL(h, UNIAP_ERR_ARG, "phase 2 needs the gathered phase-1 records");
+  if (phase == 2 && (!h->plan.valid || h->plan.rank != rank || h->plan.world != world || h->plan.rec != rec_dev))
+    FAIL(h, UNIAP_ERR_ARG, "phase 2 without the phase 1 of the same (rank, world, record)");
+  return run_phase(h, rank, world, rec_dev, phase, recs_dev);
 }
 
 extern "C" uniap_status uniap_fetch(uniap_handle* h, uniap_result* out) {

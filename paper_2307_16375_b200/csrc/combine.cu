@@ -630,6 +630,32 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
   }
 }
 
+// Phase 2 of a split multi-GPU run (uniap_run_phase): the global winner
+// among the gathered phase-1 records, by uniap_pick's key (objective, deg, c);
+// a rank whose local winner is not it skips its traceback (no backward
+// sweeps, K5c idle), so only the winner's owner pays for one.
+__global__ void k_decide(const uniap_record* __restrict__ recs, int world, int rank, BwPlan* bw, Winner* win) {
+  if (threadIdx.x != 0) return;
+  int best = -1;
+  for (int r = 0; r < world; ++r) {
+    const uniap_record& x = recs[r];
+    if (x.status != 0 || x.objective == INT64_MAX) continue;
+    if (best < 0) { best = r; continue; }
+    const uniap_record& b = recs[best];
+    if (x.objective < b.objective || (x.objective == b.objective && (x.deg < b.deg || (x.deg == b.deg && x.c < b.c))))
+      best = r;
+  }
+  if (best != rank) {
+    for (int c = 0; c < MAXCLS; ++c) bw->count[c] = 0;
+    win->status = 97;  // (k5c_walk: nothing to walk)
+  }
+}
+
+cudaError_t launch_decide(const uniap_record* recs, int world, int rank, BwPlan* bw, Winner* win, cudaStream_t st) {
+  k_decide<<<1, 32, 0, st>>>(recs, world, rank, bw, win);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_k5a(const CfgDev* cfg, const int32_t* arena, const int32_t* P, const int32_t* cfg_list, int n_local,
                        int L, const int32_t* ends, const int64_t* cfg_opt, Winner* win, long long* best_obj,
                        const RecordArgs& ra, cudaStream_t st) {

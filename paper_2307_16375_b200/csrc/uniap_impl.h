@@ -270,6 +270,9 @@ struct RecordArgs {          // what K5a writes into the record besides the winn
 
 // combine.cu
 cudaError_t launch_fill(int32_t* p, int64_t n, int32_t v, cudaStream_t st);
+struct BwPlan;
+struct Winner;
+cudaError_t launch_decide(const uniap_record* recs, int world, int rank, BwPlan* bw, Winner* win, cudaStream_t st);
 cudaError_t launch_publish(int32_t* d_rec, const uniap_record* rec, int64_t* d_qg, const int64_t* qg,
                            unsigned long long* d_tm, const unsigned long long* tm, int64_t* d_cfg,
                            const int64_t* cfgopt, int ncfg, cudaStream_t st);
