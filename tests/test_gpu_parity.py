@@ -246,6 +246,37 @@ def test_world_size_invariance(h, orc, name):
             assert r[k] == ref[k], (world, k)
 
 
+@pytest.mark.parametrize("name", ["t5", "llama", "bert"])
+def test_split_run_world_sizes(h, orc, name):
+    """uniap_run_phase at world 2/4/8 (phase 1 on every rank, headers
+    gathered, phase 2: only the global winner's owner traces back), run one
+    rank after another on one GPU: the picked records == the ORACLE's plan;
+    every other rank's record carries no traceback (it loses the pick)."""
+    import torch
+    import paper_2307_16375_b200 as pkg
+    p = profiles.make_profile(name)
+    want, _ = orc.plan(p, n_threads=0)
+    RB = pkg.RECORD_BYTES
+    for world in (2, 4, 8):
+        h.prepare(p)
+        bufs = [torch.zeros(RB, dtype=torch.uint8, device="cuda") for _ in range(world)]
+        hdrs = torch.zeros(world * RB, dtype=torch.uint8, device="cuda")
+        for rank in range(world):
+            h.run_phase(rank, world, bufs[rank].data_ptr(), 1)
+            torch.cuda.synchronize()
+            hdrs[rank * RB:(rank + 1) * RB].copy_(bufs[rank])
+        recs = b""
+        for rank in range(world):
+            h.run_phase(rank, world, bufs[rank].data_ptr(), 1)
+            h.run_phase(rank, world, bufs[rank].data_ptr(), 2, hdrs.data_ptr())
+            torch.cuda.synchronize()
+            recs += bufs[rank].cpu().numpy().tobytes()
+        st, r = pkg.pick(recs, world)
+        for k in ("objective", "deg", "c", "cfg_index", "stage_of", "strategy_of", "stage_cost", "cut_cost",
+                  "stage_mem"):
+            assert r[k] == want[k], (world, k)
+
+
 def test_interval_table_between_solves_keeps_the_captured_plan(h, orc):
     """solve -> interval_table -> solve on the SAME tables: the second solve
     replays the captured graph of the first, so the all-intervals call must
