@@ -334,7 +334,8 @@ def main():
             "e2e": {"value": cells / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d_per_step,
                     "d2h_bytes_per_step": d2h_per_step, "seconds_per_step": e2e_s,
                     "path": "uniap_plan = uniap_prepare (validate + H2D of the ABI profile) + uniap_run + uniap_fetch "
-                            "(D2H + sync); N > 1: + NCCL all_gather of the records and uniap_pick",
+                            "(D2H + sync); N > 1: the split run (uniap_run_phase 1, NCCL all_gather of the headers, "
+                            "phase 2, all_gather of the records) and uniap_pick",
                     "python_marshal_us": statistics.median(marshal_us)},
             "gpu_launches": launches_per_step,
             "roofline": {"bound": "alu", "kernel": "k2_chain (VIADDMNMX min-plus)", "achieved": achieved,
