@@ -219,6 +219,8 @@ struct uniap_handle {
   // the device from the builder's M (k1f_trim).
   std::vector<int32_t> minM;
   std::vector<size_t> minMoff;  // per config: its block of minM, [memory table][layer]
+  std::vector<int64_t> layout_key;  // level 2: the inputs of the last layout (reused while equal)
+  bool layout_l2 = false;           // the current layout is a level-2 one built from layout_key
   int max_nmt = 1;              // level 2: the largest memory-table count of a config (K1a's grid)
   int n_src = 0;                // level 2: skip sources of the model (NEXT-4: several)
   // per-stage memory caps (NEXT-2): per config its levels and stage caps
@@ -620,6 +622,7 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
   if (t->n_cfg < 1 || t->n_cfg > UNIAP_MAX_CFG) FAIL(h, UNIAP_ERR_ARG, "n_cfg=%d", t->n_cfg);
   h->L = L; h->cap = t->cap; h->Q = t->cap + 1; h->skip = t->skip_src; h->ncfg = t->n_cfg; h->level2 = false;
   h->n_src = 0;
+  h->layout_l2 = false;  // (level-1 layouts are rebuilt every time: they depend on the tables' values)
   std::vector<int> S(h->ncfg), deg(h->ncfg), c(h->ncfg), g(h->ncfg, 0), skc(h->ncfg);
   std::vector<std::vector<int>> keep(h->ncfg), mts(h->ncfg);
   std::vector<std::vector<const int32_t*>> tabs(h->ncfg);
@@ -994,8 +997,29 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
   if (srcs.size() >= 2)
     for (int i = 0; i < h->ncfg; ++i) msrc[i] = srcs;
   h->n_src = (int)srcs.size();
-  uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps, mts, mtn, &msrc);
-  if (st != UNIAP_OK) return st;
+  // The layout (arena offsets, kernel classes, levels) depends on shapes
+  // only: a profile of the same shapes as the last level-2 prepare (new cost
+  // values, e.g. re-profiled layers) keeps it.  Key: every layout input.
+  std::vector<int64_t> key = {L, o->Q, o->strategy_space, o->schedule, h->no_compact, h->ncfg, (int64_t)srcs.size(),
+                              (int64_t)h->any_cut};
+  for (int x : srcs) key.push_back(x);
+  for (int i = 0; i < h->ncfg; ++i) {
+    for (int64_t x : {(int64_t)deg[i], (int64_t)c[i], (int64_t)g[i], (int64_t)S[i], (int64_t)skc[i],
+                      (int64_t)keep[i].size(), (int64_t)caps[i].size(), (int64_t)mts[i].size(), (int64_t)mtn[i].size(),
+                      (int64_t)h->cut[i]})
+      key.push_back(x);
+    for (int x : keep[i]) key.push_back(x);
+    for (int32_t x : caps[i]) key.push_back(x);
+    for (int x : mts[i]) key.push_back(x);
+    for (int8_t x : mtn[i]) key.push_back(x);
+  }
+  if (!(h->layout_l2 && key == h->layout_key)) {
+    h->layout_l2 = false;
+    uniap_status st = layout_configs(h, keep, S, deg, c, g, skc, caps, mts, mtn, &msrc);
+    if (st != UNIAP_OK) return st;
+    h->layout_key.swap(key);
+    h->layout_l2 = true;
+  }
   h->max_nmt = 1;
   for (int i = 0; i < h->ncfg; ++i) h->max_nmt = std::max(h->max_nmt, std::max(1, (int)mtn[i].size()));
   h->minM.clear();  // the sweep trim runs on the device (k1f_trim)
