@@ -1647,20 +1647,11 @@ static uniap_status enqueue_k4_range(uniap_handle* h, int li0, int cnt, cudaStre
   return UNIAP_OK;
 }
 
-// The whole path for this rank, enqueued on h->st with no host
-// synchronisation (so it can be captured as one CUDA graph).
-// phase 0: the whole path; 1: up to the local winner (K5a: the record's
-// header), no traceback; 2: k_decide against the gathered phase-1 records
-// `recs` (the traceback runs only on the rank holding the global winner),
-// then the traceback and the publication.
-static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec, int phase = 0, const uniap_record* recs = nullptr) {
+// Builder, forward chain-DP classes with their K4, and K5a (the local winner
+// and the record header), enqueued on h->st with no host synchronisation.
+static uniap_status enqueue_forward(uniap_handle* h, uniap_record* rec) {
   const RunPlan& R = h->plan;
   const int L = h->L, nl = (int)R.local.size();
-  auto* fd = h->fb_dev;
-  if (phase == 2) {  // phase 2 starts from the gathered phase-1 records
-    CK(h, launch_decide(recs, R.world, R.rank, h->bwp.p, h->win.p, h->st));
-    h->launches++;
-  } else {
   if (h->trace.p) CK(h, cudaMemsetAsync(h->trace.p, 0, 8, h->st));
   if (h->level2) {
     // the P fill overlaps the builder (side stream, joined before K2)
@@ -1705,21 +1696,47 @@ static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec, int pha
   CK(h, launch_k5a(h->dcfg.p, h->arena.p, h->P.p, h->cfglist.p, nl, L, h->ends.p, h->cfgopt.p, h->win.p,
                    h->k4best.p, ra, h->st));
   h->launches += 1;
-  }  // (phase != 2)
-  if (phase != 1) {
-  // traceback: backward sweeps sized on the device, then the strategy walk
+  return UNIAP_OK;
+}
+
+// The winner's traceback: backward sweeps sized on the device (K5a's plan),
+// then the strategy walk.
+static uniap_status enqueue_traceback(uniap_handle* h, uniap_record* rec) {
+  const RunPlan& R = h->plan;
+  const int L = h->L;
   {
     uniap_status s = enqueue_k2(h, R.bgrp, h->binst.p, h->bwp.p->count, h->P.p);
     if (s != UNIAP_OK) return s;
   }
   CK(h, launch_k5c_grid(R.max_deg, h->dcfg.p, h->arena.p, h->G.p, h->bwp.p, h->win.p, L, h->cap, rec, h->st));
   if (R.max_deg > 0) h->launches++;
-  }  // (phase != 1)
-  // the results into the mapped host block (uniap_fetch: one sync, no copies)
+  return UNIAP_OK;
+}
+
+// The results into the mapped host block (uniap_fetch: one sync, no copies).
+static uniap_status enqueue_publish(uniap_handle* h, uniap_record* rec) {
+  auto* fd = h->fb_dev;
   CK(h, launch_publish(reinterpret_cast<int32_t*>(&fd->rec), rec, fd->qg, h->level2 ? h->qglob.p : nullptr, fd->tm,
                        h->tim.p, fd->cfgopt, h->cfgopt.p, h->ncfg, h->st));
   h->launches++;
   return UNIAP_OK;
+}
+
+// The whole path for this rank (phase 0), or one half of the split run
+// (uniap_run_phase): 1 = up to the local winner, 2 = k_decide against the
+// gathered phase-1 records `recs` (the traceback runs only on the rank that
+// holds the global winner) and the traceback.  Captured as one CUDA graph.
+static uniap_status enqueue_pipeline(uniap_handle* h, uniap_record* rec, int phase = 0,
+                                     const uniap_record* recs = nullptr) {
+  uniap_status s = UNIAP_OK;
+  if (phase == 2) {
+    CK(h, launch_decide(recs, h->plan.world, h->plan.rank, h->bwp.p, h->win.p, h->st));
+    h->launches++;
+  } else if ((s = enqueue_forward(h, rec)) != UNIAP_OK) {
+    return s;
+  }
+  if (phase != 1 && (s = enqueue_traceback(h, rec)) != UNIAP_OK) return s;
+  return enqueue_publish(h, rec);
 }
 
 
