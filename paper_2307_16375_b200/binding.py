@@ -365,9 +365,7 @@ class Handle:
         """p: a profile dict or a Profile."""
         model, cluster, opts, keep, n = _structs(p)
         self.n_cfg = n
-        cfg_obj = (C.c_int64 * n)()
-        r = uniap_result()
-        r.cfg_objective = cfg_obj
+        r, cfg_obj = self._result_buffers(n)
         st = self._check(lib().uniap_plan(self._h, C.byref(model), C.byref(cluster), C.byref(opts), C.byref(r)),
                          "plan", (UNIAP_OK, UNIAP_ERR_INFEASIBLE))
         out = _result_dict(r, n, cfg_obj)
@@ -441,10 +439,17 @@ class Handle:
         self._check(lib().uniap_run_phase(self._h, rank, world, C.c_void_p(rec_dev_ptr), phase,
                                           C.c_void_p(recs_dev_ptr) if recs_dev_ptr else None), f"run_phase({phase})")
 
+    def _result_buffers(self, n):
+        """A result struct and its per-config array, kept per handle (reused)."""
+        if getattr(self, "_res", (None,))[0] != n:
+            cfg_obj = (C.c_int64 * max(n, 1))()
+            r = uniap_result()
+            r.cfg_objective = cfg_obj
+            self._res = (n, r, cfg_obj)
+        return self._res[1], self._res[2]
+
     def fetch(self):
-        cfg_obj = (C.c_int64 * max(self.n_cfg, 1))()
-        r = uniap_result()
-        r.cfg_objective = cfg_obj
+        r, cfg_obj = self._result_buffers(self.n_cfg)
         st = self._check(lib().uniap_fetch(self._h, C.byref(r)), "fetch", (UNIAP_OK, UNIAP_ERR_INFEASIBLE))
         out = _result_dict(r, self.n_cfg, cfg_obj)
         out["status"] = st
