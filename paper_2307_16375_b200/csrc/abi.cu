@@ -873,6 +873,8 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
     if (e.dst != e.src + 1 && std::find(srcs.begin(), srcs.end(), e.src) == srcs.end()) srcs.push_back(e.src);
   }
   if ((int)srcs.size() > UNIAP_MAX_SKIP) FAIL(h, UNIAP_ERR_ARG, "more than %d skip sources", UNIAP_MAX_SKIP);
+  if (srcs.size() >= 2 && o->schedule == 1)  // (the copies' M' derive from GPipe's table only)
+    FAIL(h, UNIAP_ERR_ARG, "several skip sources with the 1F1B schedule are not supported");
   std::sort(srcs.begin(), srcs.end());
   const int nsrc_rows = std::max<int>(1, (int)srcs.size());
   skipb.assign((size_t)nsrc_rows * L, -1);
@@ -966,6 +968,7 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
       }
   }
   // NEXT-1 at level 2: configs with cuts get Rcut from the edges' cut matrices
+  if (any_cut && srcs.size() >= 2) FAIL(h, UNIAP_ERR_ARG, "cut matrices with several skip sources are not supported");
   h->cut.assign(h->ncfg, 0);
   for (int i = 0; i < h->ncfg && any_cut; ++i) {
     h->cut[i] = deg[i] >= 2 && deg[i] <= L;

@@ -137,3 +137,24 @@ def test_t5_with_a_second_source_profile(h, orc):
     gt, gq, gbuf = h.build_tables(p)
     assert gq == qn and np.array_equal(gbuf, buf)
     _same(h.plan(p), orc.solve_tables(t, n_threads=0), "t5 two sources")
+
+
+def test_dag_profile_unsupported_combinations_rejected(h):
+    """Several skip sources with the 1F1B schedule or with cut matrices are
+    refused (UNIAP_ERR_ARG), not solved wrongly."""
+    from gen import profiles
+    p = None
+    for seed in range(40):
+        q = profiles.random_profile(7100 + seed, L=8, Q=64, n_skip=2)
+        if len({e["src"] for e in q["model"]["edges"] if e["dst"] != e["src"] + 1}) >= 2:
+            p = q
+            break
+    assert p is not None
+    with pytest.raises(Exception, match="1F1B"):
+        h.plan(dict(p, options=dict(p["options"], schedule=1)))
+    import paper_2307_16375_b200 as pkg
+    ncat = sum(len(pkg.catalogue(g)) for g in range(1, p["cluster"]["n_dev"] + 1) if p["cluster"]["n_dev"] % g == 0)
+    edges = [dict(e, cut_ns_per_sample=np.zeros((ncat, ncat), np.int64)) if e["dst"] == e["src"] + 1 else e
+             for e in p["model"]["edges"]]
+    with pytest.raises(Exception, match="cut matrices"):
+        h.plan(dict(p, model=dict(p["model"], edges=edges)))
