@@ -133,7 +133,7 @@ typedef struct {
                                 (NEXT-4): Rskips[j][v][k_s][k_v], the resharding cost of the skip
                                 edge skip_srcs[j] -> v for v >= skip_srcs[j] + 2 (other rows
                                 ignored), 0..2^22; NULL = this config has no skip edges.  Not with
-                                Rcut or M_stage (_ARG)                                          */
+                                Rcut (_ARG)                                                     */
 } uniap_config;
 
 typedef struct {

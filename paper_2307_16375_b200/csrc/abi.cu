@@ -569,7 +569,7 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
         if (ncopies > UNIAP_MAX_COPIES)
           FAIL(h, UNIAP_ERR_RANGE, "config %d: more than %d skip-conditioning copies", i, UNIAP_MAX_COPIES);
         d.cprel[jlo * UNIAP_MAX_SKIP + jhi] = (int32_t)(off - d.offA);
-        off += ncp * 2 * L * NSP;
+        off += ncp * (int64_t)(1 + nmt) * L * NSP;  // A' + one M' per memory table
       }
     if (off - d.offA > INT32_MAX) FAIL(h, UNIAP_ERR_RANGE, "config %d: tables too large", i);
   }
@@ -667,8 +667,8 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
         }
       sum += ma + mr + ms;
     }
-    if (x.Rskips && !srcs.empty() && (x.Rcut || x.M_stage))
-      FAIL(h, UNIAP_ERR_ARG, "config %d: several skip sources with Rcut or M_stage are not supported", i);
+    if (x.Rskips && !srcs.empty() && x.Rcut)
+      FAIL(h, UNIAP_ERR_ARG, "config %d: several skip sources with Rcut are not supported", i);
     if (x.O)
       for (int e = 0; e < L - 1; ++e) {
         if (x.O[e] < 0 || x.O[e] > UNIAP_MAX_ENTRY) FAIL(h, UNIAP_ERR_RANGE, "config %d: O out of range", i);
@@ -786,17 +786,18 @@ extern "C" uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables
           for (int u = 0; u < L; ++u)
             for (int k = 0; k < N; ++k) {
               int64_t av = 0;
-              int32_t mv = h->cap + 1;
+              bool held = false;  // a run source on another strategy than the copy's
               if (k < sc) {
                 av = x.A[u * s + kp[k]];
-                mv = std::min(x.M[u * s + kp[k]], h->cap + 1);
                 for (int j = jlo; j <= jhi; ++j) {
                   if (u >= srcs[j] + 2) av += x.Rskips[(((int64_t)j * L + u) * s + kp[kv[j]]) * s + kp[k]];
-                  if (u == srcs[j] && k != kv[j]) mv = h->cap + 1;
+                  if (u == srcs[j] && k != kv[j]) held = true;
                 }
               }
               a[o + (int64_t)u * N + k] = (int32_t)av;
-              a[o + (int64_t)(L + u) * N + k] = mv;
+              for (size_t mt = 0; mt < tabs[i].size(); ++mt)  // M' of every memory table
+                a[o + ((int64_t)(1 + mt) * L + u) * N + k] =
+                    (k < sc && !held) ? std::min(tabs[i][mt][u * s + kp[k]], h->cap + 1) : h->cap + 1;
             }
         }
       }
@@ -873,8 +874,6 @@ extern "C" uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, con
     if (e.dst != e.src + 1 && std::find(srcs.begin(), srcs.end(), e.src) == srcs.end()) srcs.push_back(e.src);
   }
   if ((int)srcs.size() > UNIAP_MAX_SKIP) FAIL(h, UNIAP_ERR_ARG, "more than %d skip sources", UNIAP_MAX_SKIP);
-  if (srcs.size() >= 2 && o->schedule == 1)  // (the copies' M' derive from GPipe's table only)
-    FAIL(h, UNIAP_ERR_ARG, "several skip sources with the 1F1B schedule are not supported");
   std::sort(srcs.begin(), srcs.end());
   const int nsrc_rows = std::max<int>(1, (int)srcs.size());
   skipb.assign((size_t)nsrc_rows * L, -1);
@@ -1181,7 +1180,7 @@ static void plan_multi(int L, int i, const CfgDev& d, const Levels& lv, bool all
       const int64_t ar = copy_rel(d, jlo, n, kp, L);
       x.emit = ncp > 1 ? 2 : 1;
       x.arel = (int32_t)ar;
-      x.mrel = n ? (int32_t)(d.offA + ar + (int64_t)L * d.NSP - d.offM) : 0;
+      x.mrel = (int32_t)copy_mrel(d, n, ar, x.lev, L);
       out.push_back(x);
     }
   };

@@ -515,7 +515,7 @@ __global__ void k1g_copies(const CfgDev* __restrict__ cfgs, int L, int cap, int3
   const CfgDev& cf = cfgs[blockIdx.y];
   if (cf.nsk < 2) return;
   const int S = cf.S, N = cf.NSP, n2 = N * N;
-  const int64_t pair = 2 * (int64_t)L * N;
+  const int64_t pair = copy_words(cf, L);  // A', then M' per memory table
   int64_t total = 0;
   for (int jlo = 0; jlo < cf.nsk; ++jlo)
     for (int jhi = jlo; jhi < cf.nsk; ++jhi) {
@@ -543,12 +543,13 @@ __global__ void k1g_copies(const CfgDev* __restrict__ cfgs, int L, int cap, int3
     const int kap = (int)(rem / pair);
     const int w = (int)(rem - (int64_t)kap * pair);
     const bool isM = w >= L * N;
+    const int mt = w / (L * N) - 1;  // (isM: the memory table of this M')
     const int u = (w % (L * N)) / N, k = w % N;
     int32_t v;
     if (k >= S) {
       v = isM ? cap + 1 : 0;
     } else if (isM) {
-      v = M[u * N + k];
+      v = M[((int64_t)mt * L + u) * N + k];
       for (int j = jlo, r = kap; j <= jhi; ++j, r /= S)
         if (u == cf.sk[j] && k != r % S) v = cap + 1;
     } else {

@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
         for (int kp = 0; kp < ncp; ++kp) {
           const int64_t ar = copy_rel(cf, jlo, nr, kp, L);
           ra.bw_inst[n++] = Inst{ci, b, len, -1, -1, 0, goff, 0, -1, len, cf.lev_of[i], 0, -1,
-                                 nr ? (int32_t)(cf.offA + ar + (int64_t)L * cf.NSP - cf.offM) : 0, (int32_t)ar};
+                                 (int32_t)copy_mrel(cf, nr, ar, cf.lev_of[i], L), (int32_t)ar};
           goff += (int64_t)len * cf.NSP * (ra.cap + 1);
         }
         a = b + 1;
@@ -695,7 +695,7 @@ __device__ __noinline__ void k5c_walk_copies(const CfgDev& cf, const CfgDev* __r
     if (cp < ncp) {
       const int64_t ar = copy_rel(cf, jlo, nr, cp, L);
       const int32_t* Ac = arena + cf.offA + ar;  // A' (skip-edge terms folded in)
-      const int32_t* Mc = nr ? Ac + (int64_t)L * NSP : arena + cf.offM;  // M' (run sources held)
+      const int32_t* Mc = arena + cf.offM + copy_mrel(cf, nr, ar, cf.lev_of[stage], L);  // M' (run sources held)
       const int32_t* Rfc = arena + cf.offRf;
       const int32_t* g = G + bw->gofs[stage * 33] + (int64_t)cp * len * NSP * Q;
       int64_t rest = W.p[stage];

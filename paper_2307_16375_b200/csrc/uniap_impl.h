@@ -87,10 +87,18 @@ __host__ __device__ inline int skip_run(const CfgDev& cf, int a, int b, int* jlo
     }
   return n;
 }
-// Word offset from offA of copy kappa's [A'][M'] tables of the run
-// [jlo, jlo + n) (0: the plain tables, n = 0).
+// Word offset from offA of copy kappa's tables of the run [jlo, jlo + n):
+// A', then one M' per memory table of the config (1F1B: per in-flight
+// count), L*NSP words each (0: the plain tables, n = 0).
+__host__ __device__ inline int64_t copy_words(const CfgDev& cf, int L) { return (int64_t)(1 + cf.nmt) * L * cf.NSP; }
 __host__ __device__ inline int64_t copy_rel(const CfgDev& cf, int jlo, int n, int kappa, int L) {
-  return n == 0 ? 0 : cf.cprel[jlo * UNIAP_MAX_SKIP + jlo + n - 1] + (int64_t)kappa * 2 * L * cf.NSP;
+  return n == 0 ? 0 : cf.cprel[jlo * UNIAP_MAX_SKIP + jlo + n - 1] + (int64_t)kappa * copy_words(cf, L);
+}
+// The memory table a sweep of level `lev` reads, relative to offM: the
+// copy's M' of the level's table (n > 0), else the level's table itself.
+__host__ __device__ inline int64_t copy_mrel(const CfgDev& cf, int n, int64_t arel, int lev, int L) {
+  const int64_t mt = cf.lmt[lev];
+  return n ? cf.offA + arel + (1 + mt) * L * cf.NSP - cf.offM : mt * L * cf.NSP;
 }
 
 // One chain sweep of K2.

@@ -140,8 +140,8 @@ def test_t5_with_a_second_source_profile(h, orc):
 
 
 def test_dag_profile_unsupported_combinations_rejected(h):
-    """Several skip sources with the 1F1B schedule or with cut matrices are
-    refused (UNIAP_ERR_ARG), not solved wrongly."""
+    """Several skip sources with cut matrices are refused (UNIAP_ERR_ARG),
+    not solved wrongly."""
     from gen import profiles
     p = None
     for seed in range(40):
@@ -150,11 +150,40 @@ def test_dag_profile_unsupported_combinations_rejected(h):
             p = q
             break
     assert p is not None
-    with pytest.raises(Exception, match="1F1B"):
-        h.plan(dict(p, options=dict(p["options"], schedule=1)))
     import paper_2307_16375_b200 as pkg
     ncat = sum(len(pkg.catalogue(g)) for g in range(1, p["cluster"]["n_dev"] + 1) if p["cluster"]["n_dev"] % g == 0)
     edges = [dict(e, cut_ns_per_sample=np.zeros((ncat, ncat), np.int64)) if e["dst"] == e["src"] + 1 else e
              for e in p["model"]["edges"]]
     with pytest.raises(Exception, match="cut matrices"):
         h.plan(dict(p, model=dict(p["model"], edges=edges)))
+
+
+def test_dag_with_1f1b_tables_and_profiles(h, orc):
+    """Several skip sources with 1F1B's per-stage memory tables: each copy
+    keeps one M' per memory table (level 1: brute-pinned tiny instances and
+    larger tables with the interval tables; level 2: schedule = 1 profiles)."""
+    from test_gpu_plan_parity import check
+    from gen import profiles
+    for seed in range(500):
+        t = tables.with_skip_sources(tables.with_1f1b(tables.random_tables(140_000 + seed, skip_p=0.0), seed), seed, 2)
+        _same(h.solve_tables(t), orc.solve_tables(t), seed)
+    for seed in range(4):
+        t = tables.large_random_tables(900 + seed, 14, [3, 4, 6], 1023, [(4, 8), (3, 2), (6, 12)], mem_max=60)
+        t = tables.with_skip_sources(tables.with_1f1b(t, seed, act_max=8), seed, 2 + seed % 2, vmax=1 << 18)
+        got = h.solve_tables(t)
+        check(h, orc, t, h.fetch_intervals(), ("dag 1f1b", seed))
+        _same(got, orc.solve_tables(t, n_threads=0), seed)
+    n = 0
+    for seed in range(20):
+        p = profiles.random_profile(7200 + seed, L=7, Q=64, n_skip=2)
+        p = dict(p, options=dict(p["options"], schedule=1))
+        t, qn, buf = orc.build_tables(p)
+        ns = len(t.get("skip_srcs") or [])
+        if ns < 2 or max(sum(c["n_strat"] ** (j1 - j0 + 1) for j0 in range(ns) for j1 in range(j0, ns))
+                         for c in t["cfgs"]) > 4096:
+            continue
+        gt, gq, gbuf = h.build_tables(p)
+        assert gq == qn and np.array_equal(gbuf, buf), seed
+        _same(h.plan(p), orc.solve_tables(t, n_threads=0), seed)
+        n += 1
+    assert n >= 8

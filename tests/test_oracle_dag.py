@@ -122,3 +122,14 @@ def test_builder_several_sources_brute_force(orc):
                 assert got[k] == want[k], (seed, k)
         n += "skip_srcs" in t
     assert n >= 20
+
+
+def test_brute_force_several_sources_with_1f1b(orc):
+    """Several skip sources together with 1F1B's per-stage memory tables."""
+    for seed in range(500):
+        t = tables.with_skip_sources(tables.with_1f1b(tables.random_tables(140_000 + seed, skip_p=0.0), seed), seed, 2)
+        want = brute.solve_tables(t)
+        got = orc.solve_tables(t)
+        for k in KEYS:
+            if k in want:
+                assert got[k] == want[k], (seed, k, got[k], want[k])
