@@ -278,6 +278,13 @@ uniap_status uniap_prepare(uniap_handle* h, const uniap_model* m, const uniap_cl
                            const uniap_options* o);
 uniap_status uniap_prepare_tables(uniap_handle* h, const uniap_tables* t);
 uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev);
+/* Algorithm 1 for this rank's share in one call:
+ * uniap_prepare(m, cl, o) + uniap_run(rank, world, rec_dev); rec_dev is the
+ * device buffer of one uniap_record, the send buffer of the exchange (one
+ * all_gather over ranks), after which uniap_pick gives every rank the plan.
+ * The stream-ordered result is in rec_dev when the handle's stream is. */
+uniap_status uniap_plan_shard(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl, const uniap_options* o,
+                              int32_t rank, int32_t world, void* rec_dev);
 /* The same run in two halves, so that across ranks only the owner of the
  * global winner runs a traceback (the stage strategies of Algorithm 1's
  * output): phase 1 runs everything up to this rank's local

@@ -87,7 +87,7 @@ RECORD_BYTES = C.sizeof(uniap_record)
 
 EXPORTS = ("uniap_create", "uniap_destroy", "uniap_last_error", "uniap_status_string", "uniap_version",
            "uniap_solve_tables", "uniap_interval_table", "uniap_plan", "uniap_build_tables", "uniap_prepare",
-           "uniap_prepare_tables", "uniap_run", "uniap_run_phase", "uniap_fetch", "uniap_shard_assign", "uniap_shard_tables",
+           "uniap_prepare_tables", "uniap_run", "uniap_run_phase", "uniap_plan_shard", "uniap_fetch", "uniap_shard_assign", "uniap_shard_tables",
            "uniap_pick", "uniap_selftest", "uniap_fetch_intervals",
            "uniap_candidates", "uniap_catalogue")
 
@@ -120,6 +120,8 @@ def lib():
         L.uniap_prepare_tables.argtypes = [H, C.POINTER(uniap_tables)]
         L.uniap_run.argtypes = [H, C.c_int32, C.c_int32, C.c_void_p]
         L.uniap_run_phase.argtypes = [H, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]
+        L.uniap_plan_shard.argtypes = [H, C.POINTER(uniap_model), C.POINTER(uniap_cluster), C.POINTER(uniap_options),
+                                       C.c_int32, C.c_int32, C.c_void_p]
         L.uniap_fetch.argtypes = [H, C.POINTER(uniap_result)]
         L.uniap_fetch_intervals.argtypes = [H, _P32, C.c_int64, _P64]
         L.uniap_shard_assign.argtypes = [H, C.c_int32, _P32]
@@ -431,6 +433,14 @@ class Handle:
 
     def run(self, rank=0, world=1, rec_dev_ptr=None):
         self._check(lib().uniap_run(self._h, rank, world, C.c_void_p(rec_dev_ptr) if rec_dev_ptr else None), "run")
+
+    def plan_shard(self, p, rank, world, rec_dev_ptr):
+        """uniap_plan_shard: this rank's LPT share of Algorithm 1 (prepare + run),
+        its best record into the device buffer at rec_dev_ptr."""
+        self._keep = _structs(p)
+        model, cluster, opts, _, self.n_cfg = self._keep
+        self._check(lib().uniap_plan_shard(self._h, C.byref(model), C.byref(cluster), C.byref(opts), rank, world,
+                                           C.c_void_p(rec_dev_ptr)), "plan_shard")
 
     def run_phase(self, rank, world, rec_dev_ptr, phase, recs_dev_ptr=None):
         """uniap_run_phase: 1 = up to this rank's local winner (record header),

@@ -1814,6 +1814,15 @@ extern "C" uniap_status uniap_run(uniap_handle* h, int32_t rank, int32_t world, 
   return run_phase(h, rank, world, rec_dev, 0, nullptr);
 }
 
+extern "C" uniap_status uniap_plan_shard(uniap_handle* h, const uniap_model* m, const uniap_cluster* cl,
+                                         const uniap_options* o, int32_t rank, int32_t world, void* rec_dev) {
+  if (!h) return UNIAP_ERR_ARG;
+  if (!rec_dev) FAIL(h, UNIAP_ERR_ARG, "uniap_plan_shard needs the record device buffer");
+  uniap_status s = uniap_prepare(h, m, cl, o);
+  if (s != UNIAP_OK) return s;
+  return uniap_run(h, rank, world, rec_dev);
+}
+
 extern "C" uniap_status uniap_run_phase(uniap_handle* h, int32_t rank, int32_t world, void* rec_dev, int32_t phase,
                                         const void* recs_dev) {
   if (!h) return UNIAP_ERR_ARG;

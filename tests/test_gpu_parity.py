@@ -277,6 +277,27 @@ def test_split_run_world_sizes(h, orc, name):
             assert r[k] == want[k], (world, k)
 
 
+def test_plan_shard_world_sizes(h, orc):
+    """uniap_plan_shard (prepare + this rank's share in one
+    call) for every rank of world 2 / 4, records picked on the host == the
+    oracle's plan (ViT)."""
+    import torch
+    import paper_2307_16375_b200 as pkg
+    p = profiles.make_profile("vit")
+    want, _ = orc.plan(p, n_threads=0)
+    for world in (2, 4):
+        recs = b""
+        for rank in range(world):
+            buf = torch.zeros(pkg.RECORD_BYTES, dtype=torch.uint8, device="cuda")
+            h.plan_shard(p, rank, world, buf.data_ptr())
+            h.fetch()
+            recs += buf.cpu().numpy().tobytes()
+        st, r = pkg.pick(recs, world)
+        for k in ("objective", "deg", "c", "cfg_index", "stage_of", "strategy_of", "stage_cost", "cut_cost",
+                  "stage_mem"):
+            assert r[k] == want[k], (world, k)
+
+
 def test_interval_table_between_solves_keeps_the_captured_plan(h, orc):
     """solve -> interval_table -> solve on the SAME tables: the second solve
     replays the captured graph of the first, so the all-intervals call must
