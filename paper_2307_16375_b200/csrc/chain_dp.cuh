@@ -313,13 +313,14 @@ __global__ void __launch_bounds__(T) k2_chain(const K2Args args) {
       }
       if constexpr (NS - NFULL > 0) rows(std::integral_constant<int, NS - NFULL>{}, NFULL);
     }
-    // stage the tables of the step after next, then one barrier per layer
-    if (step + 1 < in.n) store_stage(step + 1);
-    // Split-phase: arrive on the cluster barrier (release E), issue the next
-    // table fetch (after the release, so its fence does not wait for it),
-    // sync the CTA, shift from the local E while the other CTAs catch up,
-    // then wait (acquire) before the few reads from a lower CTA's range.
+    // Split-phase: arrive on the cluster barrier (release E; before staging
+    // the next tables, which only this CTA reads, so the release does not
+    // wait for those stores), stage the tables of the step after next, issue
+    // the next table fetch, sync the CTA, shift from the local E while the
+    // other CTAs catch up, then wait (acquire) before the few reads from a
+    // lower CTA's range.
     if constexpr (CL) cl_arrive();
+    if (step + 1 < in.n) store_stage(step + 1);
     if (step + 2 < in.n) fetch_stage(step + 2, u + 2 * in.dir);
     __syncthreads();
     // ---- shift by the layer's memory, add A' ----
