@@ -88,6 +88,12 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few, int single
   if (B == 32) { c.V = 1; c.T = 32; }
   if (B == 2048) { c.V = 4; c.T = 512; }
   if (B == 4096) { c.V = 8; c.T = 512; }
+  // A long chain spread over a cluster is latency-bound with one warp per
+  // SMSP (V = 2, T = B / 2): one bucket per thread doubles the warps that
+  // hide each other's latencies at the same DPX work per SM (measured, same
+  // session: the Llama deg = 1 chain 111 -> 92 us, T5's skip copies
+  // 108 -> 97 us; BERT / ViT / Swin steps -5 %).
+  if (single && C > 1 && (B == 256 || B == 512)) { c.V = 1; c.T = B; }
   *out = c;
   return true;
 }
