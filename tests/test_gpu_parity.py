@@ -338,3 +338,58 @@ def test_builder_reshard_matrices_and_strategy_space(h, orc, space):
         _same(h.plan(p), orc.solve_tables(t), seed)
         checked += 1
     assert checked > 10
+
+
+def _recost(p, seed):
+    """The same shapes (layers, edges, candidates, Q, schedule) with new cost
+    values: every time, byte count and the cluster's memory and bandwidths
+    drawn again -- what a re-profiled model looks like to uniap_prepare."""
+    rng = np.random.default_rng(seed)
+    q = {"name": p["name"] + "'", "options": dict(p["options"]), "cluster": dict(p["cluster"])}
+    layers = []
+    for ly in p["model"]["layers"]:
+        f = int(rng.integers(10_000, 5_000_000))
+        layers.append(dict(ly, fwd_ns_per_sample=[max(1, f // (i + 1) + int(rng.integers(0, 999)))
+                                                  for i in range(len(ly["fwd_ns_per_sample"]))],
+                           param_bytes=int(rng.integers(0, 1 << 31)),
+                           act_bytes_per_sample=sorted((int(rng.integers(0, 1 << 28))
+                                                        for _ in ly["act_bytes_per_sample"]), reverse=True),
+                           ctx_bytes=int(rng.integers(0, 1 << 24))))
+    edges = [dict(e, tensor_bytes_per_sample=int(rng.integers(0, 1 << 24))) for e in p["model"]["edges"]]
+    q["model"] = dict(p["model"], layers=layers, edges=edges)
+    q["cluster"].update(mem_bytes=int(rng.integers(1 << 30, 1 << 36)), bw_intra_Bps=int(rng.integers(1 << 30, 1 << 38)),
+                        p2p_Bps=int(rng.integers(1 << 27, 1 << 36)))
+    return q
+
+
+@pytest.mark.parametrize("kind", ["chain", "dag", "1f1b"])
+def test_layout_cache_sequences(h, orc, kind):
+    """uniap_prepare keeps the level-2 layout (arena offsets, classes, levels,
+    copies) and the captured graph when the shapes repeat: alternate
+    same-shape re-costed profiles with a different-shape one, every plan equal
+    to the oracle's (or failing with the oracle's status)."""
+    import paper_2307_16375_b200 as pkg
+    checked = 0
+    for seed in range(8):
+        rng = np.random.default_rng(seed)
+        L = int(rng.integers(5, 11))
+        p = profiles.random_profile(9100 + seed, L=L, Q=int(rng.choice([64, 256])), n_skip=2 if kind == "dag" else 0)
+        if kind == "1f1b":
+            p = dict(p, options=dict(p["options"], schedule=1))
+        other = profiles.random_profile(9200 + seed, L=L + 1, Q=p["options"]["Q"])
+        seq = [p, _recost(p, seed), p, other, _recost(p, seed + 50), _recost(p, seed)]
+        for i, x in enumerate(seq):
+            try:
+                want, _ = orc.plan(x)
+            except orc.OracleError as e:
+                with pytest.raises(pkg.UniapError) as ei:
+                    h.plan(x)
+                assert ei.value.status == e.status, (seed, i)
+                continue
+            got = h.plan(x)
+            for k in ("objective", "deg", "c", "quantum_ns", "cfg_objective"):
+                assert got[k] == want[k], (kind, seed, i, k)
+            if want["objective"] != (1 << 63) - 1:
+                assert got["stage_of"] == want["stage_of"] and got["strategy_of"] == want["strategy_of"], (seed, i)
+            checked += 1
+    assert checked >= 24
