@@ -522,7 +522,8 @@ static uniap_status layout_configs(uniap_handle* h, const std::vector<std::vecto
       if (!k2_pick_class_t(S[i], h->Q, &k))
         FAIL(h, UNIAP_ERR_RANGE, "config %d: a strategy-dependent cut cost needs Q <= %d at |S| = %d", i,
              S[i] > 12 ? 1024 : 2048, S[i]);
-    } else if (!k2_pick_class(S[i], h->Q, single, &k, few)) {
+    } else if (!k2_pick_class(S[i], h->Q, single, &k, few,
+                              (v.size() == 1 && h->Q <= 1024 && S[i] > 10) ? 128 : 256)) {  // (a lone chain)
       FAIL(h, UNIAP_ERR_ARG, "no kernel class for |S|=%d Q=%d", S[i], h->Q);
     }
     h->cls[i] = k;

@@ -54,9 +54,12 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few, int single
   if (single) {
     // a deg = 1 config (one long chain, or its skip copies): at least 256
     // buckets per CTA (4 warps), the bucket axis over a cluster of up to 16
-    // CTAs (measured on the bench workloads: C = 4 x 256 beats C = 8 x 128 at
-    // Q = 1024; at Q = 4096 the Llama chain takes 109 us at C = 16 x 256
-    // against 133 us at C = 8 x 512)
+    // CTAs (measured on the bench workloads with two buckets per thread: C =
+    // 4 x 256 beat C = 8 x 128 at Q = 1024; at Q = 4096 the Llama chain takes
+    // 109 us at C = 16 x 256 against 133 us at C = 8 x 512).  With one bucket
+    // per thread (below) the caller asks for 128 buckets for a lone chain
+    // with |S| > 10 at Q <= 1024: C = 8 x 128, Swin's chain 91 -> 83 us,
+    // ViT's 60 -> 56; BERT's |S| = 10 chain gains nothing
     const int bs = single_b;
     constexpr int cs = 16;
     B = std::min(B, bs);
@@ -93,7 +96,7 @@ bool k2_pick_class(int S, int Q, bool single, K2Class* out, bool few, int single
   // hide each other's latencies at the same DPX work per SM (measured, same
   // session: the Llama deg = 1 chain 111 -> 92 us, T5's skip copies
   // 108 -> 97 us; BERT / ViT / Swin steps -5 %).
-  if (single && C > 1 && (B == 256 || B == 512)) { c.V = 1; c.T = B; }
+  if (single && C > 1 && (B == 128 || B == 256 || B == 512)) { c.V = 1; c.T = B; }
   *out = c;
   return true;
 }

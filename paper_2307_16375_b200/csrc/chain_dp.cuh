@@ -470,6 +470,7 @@ k2_fn k2_get(int V, int T, bool CL, bool DB, bool TM) {
   UNIAP_SHAPE(2, 32)
   UNIAP_SHAPE(2, 64)
   UNIAP_SHAPE(2, 128)
+  UNIAP_SHAPE(1, 128)
   UNIAP_SHAPE(1, 256)
   UNIAP_SHAPE(1, 512)
   UNIAP_SHAPE(2, 256)
