@@ -573,6 +573,10 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     win->p[t] = P[cf.offP + (int64_t)cf.lev_of[t] * L * L + (int64_t)a * L + b];
     win->o[t] = (t + 1 < deg) ? arena[cf.offO + b] : 0;
   }
+  const int64_t kept = ra.gstore[ci];  // deg = 1: the forward phase's sweep kept its tables
+  const int cls = ra.cls_of_cfg[ci];
+  const bool st_ok = have && r->status == 0;  // (r->status: written before the barrier above)
+  __syncthreads();  // every thread has read r->status before thread 0 may overwrite it
   if (t == 0) {
     const int64_t OPT = s_opt[0];
     win->objective = OPT;
@@ -583,51 +587,83 @@ __global__ void __launch_bounds__(K5T) k5a_winner(const CfgDev* __restrict__ cfg
     win->NSP = cf.NSP;
     win->n_theta_star = 0;
     win->status = have ? 0 : 99;
-    const int64_t kept = ra.gstore[ci];  // deg = 1: the forward phase's sweep kept its tables
-    const int cls = ra.cls_of_cfg[ci];
-    const bool st_ok = have && r->status == 0;
     if (!have) r->status = UNIAP_ERR_INTERNAL;
     r->objective = OPT;
     r->cfg_index = ci;
     r->deg = deg;
     r->c = cf.c;
-    // the backward sweeps of the traceback: one per stage, one per skip
-    // conditioning ks when the stage contains the skip source and an edge of it
+  }
+  // the backward sweeps of the traceback: one per stage, one per skip
+  // conditioning ks when the stage contains the skip source and an edge of it
+  // (NEXT-4: one per copy of the stage's run of skip sources), in stage order
+  if (cf.nsk >= 2) {
+    if (t != 0) return;
     int n = 0;
     int64_t goff = 0;
     int a = 0;
     for (int i = 0; i < deg && st_ok; ++i) {
       const int b = E[1 + i], len = b - a + 1;
-      if (cf.nsk >= 2) {  // NEXT-4: one sweep per copy of the stage's run of skip sources
-        int jlo;
-        const int nr = skip_run(cf, a, b, &jlo);
-        int ncp = 1;
-        for (int j = 0; j < nr; ++j) ncp *= cf.S;
-        ra.bw->gofs[i * 33] = goff;  // copy kappa at goff + kappa * len * NSP * Q (k5c_walk)
-        for (int kp = 0; kp < ncp; ++kp) {
-          const int64_t ar = copy_rel(cf, jlo, nr, kp, L);
-          ra.bw_inst[n++] = Inst{ci, b, len, -1, -1, 0, goff, 0, -1, len, cf.lev_of[i], 0, -1,
-                                 (int32_t)copy_mrel(cf, nr, ar, cf.lev_of[i], L), (int32_t)ar};
-          goff += (int64_t)len * cf.NSP * (ra.cap + 1);
-        }
-        a = b + 1;
-        continue;
-      }
-      const bool cond = cf.skip >= 0 && a <= cf.skip && cf.skip + 2 <= b;
-      for (int ks = cond ? 0 : -1; ks < (cond ? cf.S : 0); ++ks) {
-        if (kept >= 0) {
-          ra.bw->gofs[i * 33 + ks + 1] = kept + (int64_t)(ks < 0 ? 0 : ks) * L * cf.NSP * (ra.cap + 1);
-          continue;
-        }
-        ra.bw->gofs[i * 33 + ks + 1] = goff;
-        ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1, len, cf.lev_of[i], 0, -1,
-                               (int32_t)(cfg_moff(cf, cf.lev_of[i], L) - cf.offM)};  // (its stage's memory table)
+      int jlo;
+      const int nr = skip_run(cf, a, b, &jlo);
+      int ncp = 1;
+      for (int j = 0; j < nr; ++j) ncp *= cf.S;
+      ra.bw->gofs[i * 33] = goff;  // copy kappa at goff + kappa * len * NSP * Q (k5c_walk)
+      for (int kp = 0; kp < ncp; ++kp) {
+        const int64_t ar = copy_rel(cf, jlo, nr, kp, L);
+        ra.bw_inst[n++] = Inst{ci, b, len, -1, -1, 0, goff, 0, -1, len, cf.lev_of[i], 0, -1,
+                               (int32_t)copy_mrel(cf, nr, ar, cf.lev_of[i], L), (int32_t)ar};
         goff += (int64_t)len * cf.NSP * (ra.cap + 1);
       }
       a = b + 1;
     }
     ra.bw->count[cls] = n;
+    return;
   }
+  // warp 0, lane l: stages 2l and 2l + 1 (deg <= 64); a scan of the sweep
+  // counts and G sizes gives each stage its first instance and G offset
+  if (w != 0) return;
+  const int64_t row = (int64_t)cf.NSP * (ra.cap + 1);
+  int cnt[2], a2[2], b2[2];
+  bool cond2[2];
+  int64_t sz[2];
+  for (int h = 0; h < 2; ++h) {
+    const int i = 2 * lane + h;
+    cnt[h] = 0;
+    sz[h] = 0;
+    if (i < deg && st_ok) {
+      b2[h] = E[1 + i];
+      a2[h] = i == 0 ? 0 : E[i] + 1;
+      cond2[h] = cf.skip >= 0 && a2[h] <= cf.skip && cf.skip + 2 <= b2[h];
+      cnt[h] = kept >= 0 ? 0 : (cond2[h] ? cf.S : 1);
+      sz[h] = (int64_t)cnt[h] * (b2[h] - a2[h] + 1) * row;
+    }
+  }
+  int n_in = cnt[0] + cnt[1];
+  int64_t g_in = sz[0] + sz[1];
+  for (int o = 1; o < 32; o <<= 1) {  // inclusive scan over the lanes
+    const int nn = __shfl_up_sync(0xffffffffu, n_in, o);
+    const int64_t gg = __shfl_up_sync(0xffffffffu, g_in, o);
+    if (lane >= o) { n_in += nn; g_in += gg; }
+  }
+  int n = n_in - cnt[0] - cnt[1];
+  int64_t goff = g_in - sz[0] - sz[1];
+  for (int h = 0; h < 2; ++h) {
+    const int i = 2 * lane + h;
+    if (i >= deg || !st_ok) break;
+    const int b = b2[h], len = b - a2[h] + 1;
+    const bool cond = cond2[h];
+    for (int ks = cond ? 0 : -1; ks < (cond ? cf.S : 0); ++ks) {
+      if (kept >= 0) {
+        ra.bw->gofs[i * 33 + ks + 1] = kept + (int64_t)(ks < 0 ? 0 : ks) * L * row;
+        continue;
+      }
+      ra.bw->gofs[i * 33 + ks + 1] = goff;
+      ra.bw_inst[n++] = Inst{ci, b, len, ks, -1, 0, goff, 0, -1, len, cf.lev_of[i], 0, -1,
+                             (int32_t)(cfg_moff(cf, cf.lev_of[i], L) - cf.offM)};  // (its stage's memory table)
+      goff += (int64_t)len * row;
+    }
+  }
+  if (lane == 31) ra.bw->count[cls] = st_ok ? n_in : 0;
 }
 
 // Phase 2 of a split multi-GPU run (uniap_run_phase): the global winner
