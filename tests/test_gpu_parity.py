@@ -393,3 +393,17 @@ def test_layout_cache_sequences(h, orc, kind):
                 assert got["stage_of"] == want["stage_of"] and got["strategy_of"] == want["strategy_of"], (seed, i)
             checked += 1
     assert checked >= 24
+
+
+@pytest.mark.parametrize("S,Q", [(11, 129), (16, 300), (24, 777), (32, 1024), (12, 1025)])
+def test_lone_chain_cluster_shapes(h, orc, S, Q):
+    """A lone deg = 1 chain (no skip source) with |S| > 10: at Q <= 1024 it
+    runs on a cluster of 128-bucket CTAs, one bucket per thread (2 .. 8 CTAs,
+    ragged tails); Q = 1025 keeps the 256-bucket shape.  The solve and every
+    interval-table entry against the oracle, with a deg = 2 config beside it."""
+    from test_gpu_plan_parity import check
+    t = tables.large_random_tables(60_000 + S * 7 + Q, 20, [S, max(2, S // 3)], Q - 1, [(1, 4), (2, 2)],
+                                   dist="ties" if S % 2 else "uniform")
+    got = h.solve_tables(t)
+    check(h, orc, t, h.fetch_intervals(), ("lone chain", S, Q))
+    _same(got, orc.solve_tables(t, n_threads=0), (S, Q))
