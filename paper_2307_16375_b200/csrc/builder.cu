@@ -309,36 +309,52 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
   }
   if (bb.work && t < 2) bb.work[2 * blockIdx.x + t] = 0;  // K1f's trim accumulates this run's work here
   __syncthreads();
-  if (t < 64) {
-    const bool expl = cl.quantum > 0;
-    okp[t] = 0;
-    if (!expl || t == 0) {
-      const int64_t q = expl ? cl.quantum : ((int64_t)1 << t);
-      if (expl || t <= 61) {
-        const int64_t EM = (int64_t)UNIAP_MAX_ENTRY, SM = (int64_t)UNIAP_MAX_SUM;
-        bool ok = true;
-        int64_t sum = 0, osum = 0;
-        // ceil(x / q): a shift for the power-of-two candidates
-        auto cq = [&](int64_t x) { return expl ? (x + q - 1) / q : (x + q - 1) >> t; };
-        for (int u = 0; u < L; ++u) {
-          const int64_t a = cq(mx[QMS * u]), r = cq(mx[QMS * u + 1]), s = cq(mx[QMS * u + 2]);
-          const int64_t o = u < L - 1 ? cq(mx[QMS * u + 3]) : 0, rc = u < L - 1 ? cq(mx[QMS * u + 4]) : 0;
-          ok = ok && a <= EM && r <= EM && s <= EM && o <= EM && rc <= EM;
-          sum += a + r + s;
-          osum += o + rc;  // every o_j <= O + max Rcut (NEXT-1)
-        }
-        ok = ok && sum <= SM && osum <= SM;
-        okp[t] = ok;
-      }
+  // candidate p = t % 64 (2^p, or the explicit quantum at p = 0), layers
+  // u = part, part + 4, ... (part = t / 64): partial sums and bounds, then
+  // combined per candidate and the smallest feasible one picked by ballot
+  __shared__ int64_t ps[4][64], pos[4][64];
+  __shared__ unsigned pmask[2];
+  const bool expl = cl.quantum > 0;
+  const int p = t & 63, part = t >> 6;
+  const bool live = expl ? p == 0 : p <= 61;
+  {
+    const int64_t q = expl ? cl.quantum : ((int64_t)1 << min(p, 61));
+    const int64_t EM = (int64_t)UNIAP_MAX_ENTRY;
+    bool ok = live;
+    int64_t sum = 0, osum = 0;
+    // ceil(x / q): a shift for the power-of-two candidates
+    auto cq = [&](int64_t x) { return expl ? (x + q - 1) / q : (x + q - 1) >> p; };
+    for (int u = part; live && u < L; u += 4) {
+      const int64_t a = cq(mx[QMS * u]), r = cq(mx[QMS * u + 1]), s = cq(mx[QMS * u + 2]);
+      const int64_t o = u < L - 1 ? cq(mx[QMS * u + 3]) : 0, rc = u < L - 1 ? cq(mx[QMS * u + 4]) : 0;
+      ok = ok && a <= EM && r <= EM && s <= EM && o <= EM && rc <= EM;
+      sum += a + r + s;
+      osum += o + rc;  // every o_j <= O + max Rcut (NEXT-1)
     }
+    ps[part][p] = ok ? sum : -1;
+    pos[part][p] = osum;
+  }
+  __syncthreads();
+  if (t < 64) {
+    const int64_t SM = (int64_t)UNIAP_MAX_SUM;
+    bool ok = live;
+    int64_t sum = 0, osum = 0;
+    for (int j = 0; j < 4; ++j) {
+      ok = ok && ps[j][t] >= 0;
+      sum += ps[j][t];
+      osum += pos[j][t];
+    }
+    ok = ok && sum <= SM && osum <= SM;
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if ((t & 31) == 0) pmask[t >> 5] = m;
   }
   __syncthreads();
   if (t == 0) {
+    // the smallest feasible candidate (every check is monotone in q)
+    const unsigned long long m = (unsigned long long)pmask[0] | (unsigned long long)pmask[1] << 32;
     int64_t q = -1;
-    if (cl.quantum > 0) q = okp[0] ? cl.quantum : -1;
-    else
-      for (int p = 0; p <= 61; ++p)
-        if (okp[p]) { q = (int64_t)1 << p; break; }
+    if (expl) q = (m & 1ull) ? cl.quantum : -1;
+    else if (m) q = (int64_t)1 << (__ffsll((long long)m) - 1);
     bb.qcfg[blockIdx.x] = q;
     __threadfence();
     unsigned int* done = reinterpret_cast<unsigned int*>(bb.qglob + 2);
@@ -347,21 +363,20 @@ __global__ void k1d_quantum(ClusterDev cl, BuildBufs bb, const CfgDev* __restric
   __syncthreads();
   // the last config block sets the global quantum = max over the configs
   // (every check is monotone in q), or flags "no quantum fits"
-  if (okp[0]) {
+  if (okp[0] && t < 32) {
     __threadfence();
-    __shared__ long long red[64];
     long long g = 1;
-    for (int i = t; i < (int)gridDim.x; i += blockDim.x) {
+    for (int i = t; i < (int)gridDim.x; i += 32) {
       const long long x = *reinterpret_cast<volatile long long*>(bb.qcfg + i);
       g = (x < 0 || g < 0) ? -1 : max(g, x);
     }
-    red[t] = g;
-    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long y = __shfl_xor_sync(0xffffffffu, g, o);
+      g = (y < 0 || g < 0) ? -1 : max(g, y);
+    }
     if (t == 0) {
-      long long r = 1;
-      for (int i = 0; i < (int)blockDim.x; ++i) r = (red[i] < 0 || r < 0) ? -1 : max(r, red[i]);
-      if (r < 0) atomicOr(reinterpret_cast<unsigned long long*>(bb.qglob + 1), 2ull);
-      bb.qglob[0] = r;
+      if (g < 0) atomicOr(reinterpret_cast<unsigned long long*>(bb.qglob + 1), 2ull);
+      bb.qglob[0] = g;
       *reinterpret_cast<unsigned int*>(bb.qglob + 2) = 0u;  // ready for the next run (graph replays)
     }
   }
@@ -570,7 +585,7 @@ cudaError_t launch_k1(const ClusterDev& cl, const BuildBufs& bb, const CfgDev* c
   const int nbR = (L - 1) + bb.n_src * L;  // one block per edge slot: L-1 chain edges, L skip destinations per source
   const int nbE = bb.cut_mat ? L - 1 : 0;  // NEXT-1 cut-cost blocks (per chain edge)
   k1_costs<<<dim3(nbA + nbR + nbE + 1, ncfg), K1T, 0, st>>>(cl, bb, cfg, L, nbA, nbR, nbE);
-  cudaError_t e = pdl_launch(k1d_quantum, dim3(ncfg), dim3(64), 0, st, cl, bb, cfg, L, skip);
+  cudaError_t e = pdl_launch(k1d_quantum, dim3(ncfg), dim3(256), 0, st, cl, bb, cfg, L, skip);
   if (e != cudaSuccess) return e;
   e = pdl_launch(k1f_quantise, dim3(16 + (bb.inst ? bb.n_trim : 0), ncfg), dim3(256), 0, st, cl, bb, cfg, L, arena);
   if (e != cudaSuccess) return e;
