@@ -59,8 +59,11 @@ def main(cases):
         t = tables.with_skip_sources(tables.large_random_tables(64, 12, [6, 4], 511, [(1, 1), (3, 2)], mem_max=60),
                                      64, 3, vmax=1 << 18)
         same(h.solve_tables(t), oracle.solve_tables(t, n_threads=0), "dag tables")
+    if "lone" in cases:  # a lone deg = 1 chain, |S| = 16 at Q = 1024: 8 x 128-bucket cluster, one bucket per thread
+        t = tables.large_random_tables(65, 10, [16, 5], 1023, [(1, 1), (2, 4)], mem_max=150)
+        same(h.solve_tables(t), oracle.solve_tables(t, n_threads=0), "lone chain")
     h.close()
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["toy", "bert", "cluster", "skip", "levels", "cut", "1f1b", "dag"])
+    main(sys.argv[1:] or ["toy", "bert", "cluster", "skip", "levels", "cut", "1f1b", "dag", "lone"])
